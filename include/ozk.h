@@ -1,0 +1,161 @@
+/*
+ * ozk.h -- C-ABI of the B200 Ozaki-scheme multiple-precision GEMM.
+ *
+ * This is the drop-in boundary for the reference mpmat library's hot path
+ * (paths relative to /root/reference/proj/include/mpmat/):
+ *
+ *   ozk_ozaki_gemm        replaces  template<int K> ozaki_gemm(a, b, d, backend,
+ *                                   drop_threshold)                  ozaki.hpp:180-183
+ *   ozk_split             replaces  template<int K> split_matrix(m, d, side)
+ *                                                                    ozaki.hpp:74-75
+ *   ozk_backend_gemm      replaces  reference_backend_gemm / the GemmBackend plugin
+ *                                                                    backend.hpp:12-20
+ *   ozk_split_shift_bits  replaces  split_shift_bits                 ozaki.hpp:43-48
+ *   ozk_exponent_ceil_log2 replaces exponent_ceil_log2               ozaki.hpp:36-40
+ *
+ * Conventions (identical to the reference, so the boundary is zero-copy):
+ *  - matrices are row-major; a K-word element is K consecutive doubles
+ *    (the memory image of DenseMatrix<MultiFloat<K>>, dense_matrix.hpp:12-45,
+ *    multifloat.hpp:218): element (i,j) word w at ((i*cols + j)*K + w);
+ *  - the split count is `int split_count` (>= 1), the component type is the
+ *    ozk_format (K = 2/3/4 words = DD/TD/QD);
+ *  - no exception crosses the ABI: every call returns an ozk_status and
+ *    ozk_last_error() (thread-local) describes the last failure.  The status
+ *    codes map 1:1 onto the reference's exception types (errors.hpp:7-25) and
+ *    are raised for the same conditions in the same order.
+ *
+ * All functions are reentrant (the reference calls its backend from an
+ * OpenMP parallel loop, ozaki.hpp:224-231); host-buffer entry points use a
+ * private CUDA stream per call.  `*_device` entry points take device
+ * pointers and a cudaStream_t (passed as void*, NULL = legacy default
+ * stream) and synchronise that stream before returning.
+ */
+#ifndef OZK_H
+#define OZK_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    OZK_OK = 0,
+    OZK_ESHAPE = 1, /* mpmat::shape_error  (errors.hpp:11-13) */
+    OZK_EPARAM = 2, /* mpmat::param_error  (errors.hpp:15-17) */
+    OZK_ECUDA = 3,  /* CUDA runtime / launch failure */
+    OZK_ENCCL = 4,  /* collective failure (multi-GPU entry points) */
+    OZK_ENOMEM = 5  /* device allocation failure */
+} ozk_status;
+
+/* words per element, = the reference's MultiFloat<K> template argument */
+typedef enum { OZK_DD = 2, OZK_TD = 3, OZK_QD = 4 } ozk_format;
+
+/* mpmat::SplitSide (ozaki.hpp:33) */
+typedef enum { OZK_SIDE_ROWS = 0, OZK_SIDE_COLS = 1 } ozk_side;
+
+/* superset of mpmat::OzakiProfile (ozaki.hpp:149-167).  product_seconds covers
+ * the fused slice-GEMM + accumulation kernel; accumulate_seconds is 0 when the
+ * accumulation is fused (always, today).  total = split + product + accumulate
+ * as in the reference; transfer_seconds (host entry points only) is the
+ * host<->device copy time, outside total. */
+typedef struct {
+    double split_seconds;
+    double product_seconds;
+    double accumulate_seconds;
+    double total_seconds;
+    double transfer_seconds;
+    int split_count;
+    int pairs;
+    int gpus;
+} ozk_profile;
+
+/* ---- the reference entry points ------------------------------------------ */
+
+/* C (m x n) = A (m x l) * B (l x n) in K-word precision via the Ozaki scheme
+ * (ozaki.hpp:180-249): host buffers.  Errors, in the reference's order:
+ * OZK_ESHAPE for a zero dimension (dense_matrix.hpp:23) or mismatched inner
+ * dimensions (ozaki.hpp:184), OZK_EPARAM for split_count < 1 (:185),
+ * drop_threshold < 0 (:186), a non-finite entry (:77-78) or an entry too
+ * large to shift (:109).  split_count is limited to 32 here. */
+ozk_status ozk_ozaki_gemm(ozk_format fmt, size_t m, size_t l, size_t n, const double* a,
+                          const double* b, int split_count, double drop_threshold, double* c,
+                          ozk_profile* prof);
+
+/* Same with device-resident a, b, c on `stream`. */
+ozk_status ozk_ozaki_gemm_device(ozk_format fmt, size_t m, size_t l, size_t n, const double* a,
+                                 const double* b, int split_count, double drop_threshold,
+                                 double* c, void* stream, ozk_profile* prof);
+
+/* split_matrix<K> (ozaki.hpp:74-147): host buffers.  pieces receives
+ * split_count row-major (rows x cols) binary64 slices, residual the K-word
+ * working matrix after the last extraction (SplitSet<K>, ozaki.hpp:59-67). */
+ozk_status ozk_split(ozk_format fmt, size_t rows, size_t cols, const double* mat, int split_count,
+                     ozk_side side, double* pieces, double* residual);
+
+/* GemmBackend (backend.hpp:12-13): C = A * B in binary64, row-major, host
+ * buffers.  Any summation order (the plugin contract, backend.hpp:8-11). */
+ozk_status ozk_backend_gemm(size_t m, size_t l, size_t n, const double* a, const double* b,
+                            double* c);
+ozk_status ozk_backend_gemm_device(size_t m, size_t l, size_t n, const double* a,
+                                   const double* b, double* c, void* stream);
+
+int ozk_split_shift_bits(size_t inner_dim);  /* ozaki.hpp:43-48 */
+int ozk_exponent_ceil_log2(double x);        /* ozaki.hpp:36-40 (x > 0, finite) */
+
+/* ---- slice-level entry points (sharded / multi-GPU orchestration) --------- *
+ * Slices are kept in the DMMA operand layout: split_count planes of `outer`
+ * rows of ozk_slice_ld(inner) doubles (k contiguous, zero padded).
+ *   side ROWS (left factor A, m x l):  slices[a][i][k] = piece_a(i, k)
+ *   side COLS (right factor B, l x n): slices[a][j][k] = piece_a(k, j)
+ * `ld` is the row stride (in elements) of the input K-word matrix, so a
+ * column block of B can be split in place.  piece_max (nullable) receives
+ * max|piece_a| per slice (for drop_threshold, ozaki.hpp:198-208), combined by
+ * max with whatever it held (zero-fill it first). */
+size_t ozk_slice_ld(size_t inner_dim);
+
+ozk_status ozk_split_slices_device(ozk_format fmt, size_t rows, size_t cols, size_t ld,
+                                   const double* mat, int split_count, ozk_side side,
+                                   double* slices, double* piece_max, void* stream);
+
+/* Pair list of ozaki.hpp:198-221 (alpha-major, triangular, drop pruning).
+ * pairs receives 2*npairs ints (alpha, beta); capacity split_count^2 ints. */
+ozk_status ozk_pair_list(int split_count, const double* amax, const double* bmax,
+                         double drop_threshold, int* pairs, int* npairs);
+
+/* Fused slice-pair GEMMs + K-word accumulation (ozaki.hpp:223-244) over
+ * precomputed slices.  a_slices: split_count x m x ozk_slice_ld(l).  The B
+ * slices may be stored in nblk column blocks of ncb columns each (the layout an
+ * all-gather of column-sharded B slices produces): column j = blk*ncb + jj is
+ * at b_slices + blk*b_blk_stride + beta*ncb*ld + jj*ld (ld = ozk_slice_ld(l)).
+ * Pass nblk = 1, ncb = n for a single block.  c is m x n K-word, row stride
+ * ldc elements; it is overwritten. */
+ozk_status ozk_slices_gemm_device(ozk_format fmt, size_t m, size_t l, size_t n,
+                                  const double* a_slices, const double* b_slices, size_t ncb,
+                                  size_t nblk, size_t b_blk_stride, int split_count,
+                                  const int* pairs, int npairs, double* c, size_t ldc,
+                                  void* stream);
+
+/* Parity hook: every slice product C_ab = A_alpha * B_beta of the pair list,
+ * binary64, into products[p] (m x n row-major). */
+ozk_status ozk_pair_products_device(size_t m, size_t l, size_t n, const double* a_slices,
+                                    const double* b_slices, int split_count, const int* pairs,
+                                    int npairs, double* products, void* stream);
+
+/* ---- utilities -------------------------------------------------------------- */
+
+/* Eq. (1)-distributed synthetic K-word matrix (rows*cols elements) in device
+ * memory; counter-based, so a pure function of (seed, shape).  Not the
+ * reference's sequential generator (gen.hpp:20-34) -- see csrc/gen.cu. */
+ozk_status ozk_gen_eq1_device(ozk_format fmt, size_t rows, size_t cols, uint64_t seed,
+                              double* out, void* stream);
+
+const char* ozk_last_error(void);
+int ozk_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* OZK_H */

@@ -1,0 +1,26 @@
+"""B200-native Ozaki-scheme multiple-precision GEMM (DD / TD / QD).
+
+The product is ``lib/libozk.so`` (CUDA kernels for sm_100a behind the C-ABI
+in ``include/ozk.h``).  ``mpmat`` mirrors the reference mpmat hot-path API on
+top of it; ``slices`` exposes the slice-level device entry points used for
+C block-row sharding across GPUs.
+"""
+from ._lib import LIB_PATH, lib  # noqa: F401  (raises if libozk.so is missing)
+from .mpmat import (  # noqa: F401
+    OzakiProfile,
+    SplitSet,
+    SplitSide,
+    error,
+    exponent_ceil_log2,
+    gpu_backend,
+    ozaki_gemm,
+    param_error,
+    shape_error,
+    split_matrix,
+    split_shift_bits,
+)
+
+__all__ = [
+    "OzakiProfile", "SplitSet", "SplitSide", "error", "exponent_ceil_log2", "gpu_backend",
+    "ozaki_gemm", "param_error", "shape_error", "split_matrix", "split_shift_bits", "lib",
+]

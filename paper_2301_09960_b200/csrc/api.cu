@@ -1,0 +1,577 @@
+// api.cu -- host runtime behind the C-ABI (include/ozk.h): argument checks in
+// the reference's order, device buffers from the stream-ordered pool, split
+// planning, pair lists, and the launches of K1 (split.cu) and K2+K3 (gemm.cu).
+//
+// Reference call stack being replaced: ozaki_gemm<K> (ozaki.hpp:180-249) ->
+// split_matrix (:74-147) x2 -> backend (backend.hpp:12-13) x P -> accumulate.
+#include <cuda_runtime.h>
+
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/ozk.h"
+#include "ozk_internal.cuh"
+
+using namespace ozk;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+ozk_status fail(ozk_status s, const std::string& msg) {
+    g_last_error = msg;
+    return s;
+}
+
+ozk_status cuda_fail(cudaError_t e, const char* where) {
+    (void)cudaGetLastError();  // clear sticky-free errors
+    if (e == cudaErrorMemoryAllocation) return fail(OZK_ENOMEM, std::string(where) + ": out of device memory");
+    return fail(OZK_ECUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define OZK_CUDA(call, where)                                  \
+    do {                                                       \
+        cudaError_t e_ = (call);                               \
+        if (e_ != cudaSuccess) return cuda_fail(e_, where);    \
+    } while (0)
+
+int num_sms_cached() {
+    static int sms = 0;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        // keep freed pool memory: repeated calls reuse it instead of re-mapping
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t thr = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+    });
+    return sms > 0 ? sms : 148;
+}
+
+// Stream-ordered device scratch, freed on scope exit.
+struct DevBuf {
+    void* p = nullptr;
+    cudaStream_t st = nullptr;
+    cudaError_t alloc(size_t bytes, cudaStream_t s) {
+        st = s;
+        return cudaMallocAsync(&p, bytes ? bytes : 16, s);
+    }
+    template <class T>
+    T* as() const {
+        return static_cast<T*>(p);
+    }
+    ~DevBuf() {
+        if (p) cudaFreeAsync(p, st);
+    }
+};
+
+// Private stream for host-buffer entry points (reentrancy).
+struct OwnStream {
+    cudaStream_t s = nullptr;
+    cudaError_t create() { return cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking); }
+    ~OwnStream() {
+        if (s) cudaStreamDestroy(s);
+    }
+};
+
+bool valid_fmt(int fmt) { return fmt == OZK_DD || fmt == OZK_TD || fmt == OZK_QD; }
+
+int shift_bits(size_t inner) {
+    int cl = 0;
+    while ((size_t(1) << cl) < inner) ++cl;
+    return (53 + cl + 1) / 2;
+}
+
+void triangular_pairs(int d, PairList& pl) {
+    pl.count = 0;
+    for (int a = 0; a < d; ++a)
+        for (int b = 0; a + b < d; ++b) {
+            pl.alpha[pl.count] = (unsigned char)a;
+            pl.beta[pl.count] = (unsigned char)b;
+            ++pl.count;
+        }
+}
+
+void pruned_pairs(int d, const double* amax, const double* bmax, double drop, PairList& pl) {
+    const double lead = amax[0] * bmax[0];
+    pl.count = 0;
+    for (int a = 0; a < d; ++a)
+        for (int b = 0; a + b < d; ++b) {
+            if (drop > 0.0 && amax[a] * bmax[b] < drop * lead) continue;
+            pl.alpha[pl.count] = (unsigned char)a;
+            pl.beta[pl.count] = (unsigned char)b;
+            ++pl.count;
+        }
+}
+
+ozk_status check_dev_err(int flag, const char* what) {
+    if (flag == kDevNonFinite) return fail(OZK_EPARAM, std::string(what) + ": non-finite entry");
+    if (flag == kDevTooLarge)
+        return fail(OZK_EPARAM, std::string(what) + ": entries too large to shift");
+    return OZK_OK;
+}
+
+// Split of a K-word matrix into slices in the operand layout (see ozk.h).
+// work must hold outer*inner*K doubles.  Returns a CUDA error code.
+cudaError_t split_to_slices(int K, size_t rows, size_t cols, size_t ld, const double* mat, int d,
+                            int side, double* slices, double* work, unsigned long long* pmax,
+                            int* err, cudaStream_t st) {
+    const size_t inner = side == OZK_SIDE_ROWS ? cols : rows;
+    const size_t outer = side == OZK_SIDE_ROWS ? rows : cols;
+    const size_t ldk = slice_ld(inner);
+    const int sigma = shift_bits(inner);
+    if (side == OZK_SIDE_ROWS)
+        return launch_split_rows(K, mat, ld, work, rows, cols, d, sigma, slices, ldk, outer * ldk,
+                                 pmax, err, st);
+    // columns: transpose to (cols x rows) so each column is a contiguous row
+    cudaError_t e = launch_transpose(K, mat, ld, work, rows, rows, cols, st);
+    if (e != cudaSuccess) return e;
+    return launch_split_rows(K, work, rows, work, cols, rows, d, sigma, slices, ldk, outer * ldk,
+                             pmax, err, st);
+}
+
+struct Timer {
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    bool on = false;
+    explicit Timer(bool enable) : on(enable) {
+        if (on)
+            for (auto& e : ev) cudaEventCreate(&e);
+    }
+    void mark(int i, cudaStream_t st) {
+        if (on) cudaEventRecord(ev[i], st);
+    }
+    double secs(int a, int b) const {
+        if (!on) return 0.0;
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, ev[a], ev[b]);
+        return ms * 1e-3;
+    }
+    ~Timer() {
+        if (on)
+            for (auto& e : ev) cudaEventDestroy(e);
+    }
+};
+
+ozk_status ozaki_device_impl(int K, size_t m, size_t l, size_t n, const double* a,
+                             const double* b, int d, double drop, double* c, cudaStream_t st,
+                             ozk_profile* prof) {
+    const int sms = num_sms_cached();
+    const size_t ldk = slice_ld(l);
+    DevBuf sa, sb, work, flags;
+    OZK_CUDA(sa.alloc(sizeof(double) * d * m * ldk, st), "ozaki_gemm: slices A");
+    OZK_CUDA(sb.alloc(sizeof(double) * d * n * ldk, st), "ozaki_gemm: slices B");
+    OZK_CUDA(work.alloc(sizeof(double) * (m > n ? m : n) * l * K, st), "ozaki_gemm: work");
+    // flags layout: [err int (8 B)][amax d][bmax d]
+    OZK_CUDA(flags.alloc(8 + 16 * (size_t)d, st), "ozaki_gemm: flags");
+    OZK_CUDA(cudaMemsetAsync(flags.p, 0, 8 + 16 * (size_t)d, st), "ozaki_gemm: memset");
+    int* err = flags.as<int>();
+    unsigned long long* amax = reinterpret_cast<unsigned long long*>(flags.as<char>() + 8);
+    unsigned long long* bmax = amax + d;
+    const bool want_max = drop > 0.0;
+
+    Timer tm(prof != nullptr);
+    tm.mark(0, st);
+    OZK_CUDA(split_to_slices(K, m, l, l, a, d, OZK_SIDE_ROWS, sa.as<double>(), work.as<double>(),
+                             want_max ? amax : nullptr, err, st),
+             "ozaki_gemm: split A");
+    OZK_CUDA(split_to_slices(K, l, n, n, b, d, OZK_SIDE_COLS, sb.as<double>(), work.as<double>(),
+                             want_max ? bmax : nullptr, err, st),
+             "ozaki_gemm: split B");
+    tm.mark(1, st);
+
+    PairList pl;
+    if (want_max) {
+        std::vector<double> host(1 + 2 * (size_t)d);
+        OZK_CUDA(cudaMemcpyAsync(host.data(), flags.p, 8 + 16 * (size_t)d, cudaMemcpyDeviceToHost,
+                                 st),
+                 "ozaki_gemm: maxima");
+        OZK_CUDA(cudaStreamSynchronize(st), "ozaki_gemm: split");
+        int flag;
+        std::memcpy(&flag, host.data(), sizeof(int));
+        if (ozk_status s = check_dev_err(flag, "split_matrix")) return s;
+        pruned_pairs(d, host.data() + 1, host.data() + 1 + d, drop, pl);
+    } else {
+        triangular_pairs(d, pl);
+    }
+
+    GemmProblem prob{};
+    prob.a = sa.as<double>();
+    prob.lda = ldk;
+    prob.a_slice_stride = m * ldk;
+    prob.a_slices = d;
+    prob.b = sb.as<double>();
+    prob.ldb = ldk;
+    prob.b_slice_stride = n * ldk;
+    prob.b_blk_stride = (size_t)d * n * ldk;
+    prob.b_slices = d;
+    prob.ncb = (int)n;
+    prob.nblk = 1;
+    prob.m = m;
+    prob.n = n;
+    prob.l = l;
+    prob.c = c;
+    prob.ldc = n;
+    if (pl.count == 0)  // every pair pruned (drop_threshold > 1): C = 0
+        OZK_CUDA(cudaMemsetAsync(c, 0, sizeof(double) * m * n * K, st), "ozaki_gemm: zero C");
+    else
+        OZK_CUDA(launch_pair_gemm(K, kAccumulate, prob, pl, st, sms), "ozaki_gemm: slice GEMM");
+    tm.mark(2, st);
+
+    int flag = 0;
+    OZK_CUDA(cudaMemcpyAsync(&flag, err, sizeof(int), cudaMemcpyDeviceToHost, st),
+             "ozaki_gemm: flag");
+    OZK_CUDA(cudaStreamSynchronize(st), "ozaki_gemm");
+    if (ozk_status s = check_dev_err(flag, "split_matrix")) return s;
+    if (prof) {
+        prof->split_seconds = tm.secs(0, 1);
+        prof->product_seconds = tm.secs(1, 2);
+        prof->accumulate_seconds = 0.0;
+        prof->total_seconds = prof->split_seconds + prof->product_seconds;
+        prof->split_count = d;
+        prof->pairs = pl.count;
+        prof->gpus = 1;
+    }
+    return OZK_OK;
+}
+
+ozk_status check_gemm_args(int fmt, size_t m, size_t l, size_t n, int d, double drop) {
+    if (!valid_fmt(fmt)) return fail(OZK_EPARAM, "ozaki_gemm: format must be DD, TD or QD");
+    if (m == 0 || l == 0 || n == 0) return fail(OZK_ESHAPE, "matrix dimensions must be positive");
+    if (d < 1) return fail(OZK_EPARAM, "ozaki_gemm: split count must be >= 1");
+    if (drop < 0.0) return fail(OZK_EPARAM, "ozaki_gemm: negative drop threshold");
+    if (d > kMaxSplits) return fail(OZK_EPARAM, "ozaki_gemm: split count above 32 is not supported");
+    if (m > 0x7fffffffull || n > 0x7fffffffull || l > 0x7fffffffull)
+        return fail(OZK_ESHAPE, "ozaki_gemm: dimension too large");
+    return OZK_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ozk_last_error(void) { return g_last_error.c_str(); }
+int ozk_version(void) { return 1; }
+
+int ozk_split_shift_bits(size_t inner) { return shift_bits(inner ? inner : 1); }
+
+int ozk_exponent_ceil_log2(double x) {
+    int e = std::ilogb(x);
+    return std::scalbn(1.0, e) == x ? e : e + 1;
+}
+
+size_t ozk_slice_ld(size_t inner) { return slice_ld(inner); }
+
+ozk_status ozk_ozaki_gemm_device(ozk_format fmt, size_t m, size_t l, size_t n, const double* a,
+                                 const double* b, int d, double drop, double* c, void* stream,
+                                 ozk_profile* prof) {
+    if (ozk_status s = check_gemm_args(fmt, m, l, n, d, drop)) return s;
+    return ozaki_device_impl((int)fmt, m, l, n, a, b, d, drop, c, (cudaStream_t)stream, prof);
+}
+
+ozk_status ozk_ozaki_gemm(ozk_format fmt, size_t m, size_t l, size_t n, const double* a,
+                          const double* b, int d, double drop, double* c, ozk_profile* prof) {
+    if (ozk_status s = check_gemm_args(fmt, m, l, n, d, drop)) return s;
+    const int K = (int)fmt;
+    auto t0 = std::chrono::steady_clock::now();
+    OwnStream os;
+    OZK_CUDA(os.create(), "ozaki_gemm: stream");
+    num_sms_cached();
+    DevBuf da, db, dc;
+    OZK_CUDA(da.alloc(sizeof(double) * m * l * K, os.s), "ozaki_gemm: A");
+    OZK_CUDA(db.alloc(sizeof(double) * l * n * K, os.s), "ozaki_gemm: B");
+    OZK_CUDA(dc.alloc(sizeof(double) * m * n * K, os.s), "ozaki_gemm: C");
+    OZK_CUDA(cudaMemcpyAsync(da.p, a, sizeof(double) * m * l * K, cudaMemcpyHostToDevice, os.s),
+             "ozaki_gemm: H2D A");
+    OZK_CUDA(cudaMemcpyAsync(db.p, b, sizeof(double) * l * n * K, cudaMemcpyHostToDevice, os.s),
+             "ozaki_gemm: H2D B");
+    ozk_profile local{};
+    ozk_status s = ozaki_device_impl(K, m, l, n, da.as<double>(), db.as<double>(), d, drop,
+                                     dc.as<double>(), os.s, &local);
+    if (s != OZK_OK) return s;
+    OZK_CUDA(cudaMemcpyAsync(c, dc.p, sizeof(double) * m * n * K, cudaMemcpyDeviceToHost, os.s),
+             "ozaki_gemm: D2H C");
+    OZK_CUDA(cudaStreamSynchronize(os.s), "ozaki_gemm");
+    if (prof) {
+        *prof = local;
+        const double wall =
+            std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        prof->transfer_seconds = wall > local.total_seconds ? wall - local.total_seconds : 0.0;
+    }
+    return OZK_OK;
+}
+
+ozk_status ozk_split(ozk_format fmt, size_t rows, size_t cols, const double* mat, int d,
+                     ozk_side side, double* pieces, double* residual) {
+    if (!valid_fmt(fmt)) return fail(OZK_EPARAM, "split_matrix: format must be DD, TD or QD");
+    if (rows == 0 || cols == 0) return fail(OZK_ESHAPE, "matrix dimensions must be positive");
+    if (d < 1) return fail(OZK_EPARAM, "split_matrix: split count must be >= 1");
+    if (d > kMaxSplits) return fail(OZK_EPARAM, "split_matrix: split count above 32 is not supported");
+    if (side != OZK_SIDE_ROWS && side != OZK_SIDE_COLS)
+        return fail(OZK_EPARAM, "split_matrix: bad side");
+    const int K = (int)fmt;
+    const size_t N = rows * cols;
+    const size_t inner = side == OZK_SIDE_ROWS ? cols : rows;
+    const size_t outer = side == OZK_SIDE_ROWS ? rows : cols;
+    const size_t ldk = slice_ld(inner);
+    OwnStream os;
+    OZK_CUDA(os.create(), "split_matrix: stream");
+    num_sms_cached();
+    DevBuf dm, work, sl, tmp, flags;
+    OZK_CUDA(dm.alloc(sizeof(double) * N * K, os.s), "split_matrix: input");
+    OZK_CUDA(work.alloc(sizeof(double) * N * K, os.s), "split_matrix: work");
+    OZK_CUDA(sl.alloc(sizeof(double) * d * outer * ldk, os.s), "split_matrix: slices");
+    OZK_CUDA(flags.alloc(8, os.s), "split_matrix: flags");
+    OZK_CUDA(cudaMemsetAsync(flags.p, 0, 8, os.s), "split_matrix: memset");
+    OZK_CUDA(cudaMemcpyAsync(dm.p, mat, sizeof(double) * N * K, cudaMemcpyHostToDevice, os.s),
+             "split_matrix: H2D");
+    OZK_CUDA(split_to_slices(K, rows, cols, cols, dm.as<double>(), d, side, sl.as<double>(),
+                             work.as<double>(), nullptr, flags.as<int>(), os.s),
+             "split_matrix");
+    int flag = 0;
+    OZK_CUDA(cudaMemcpyAsync(&flag, flags.p, sizeof(int), cudaMemcpyDeviceToHost, os.s),
+             "split_matrix: flag");
+    OZK_CUDA(cudaStreamSynchronize(os.s), "split_matrix");
+    if (ozk_status s = check_dev_err(flag, "split_matrix")) return s;
+    if (side == OZK_SIDE_ROWS) {
+        OZK_CUDA(cudaMemcpy2DAsync(pieces, cols * 8, sl.p, ldk * 8, cols * 8, rows * (size_t)d,
+                                   cudaMemcpyDeviceToHost, os.s),
+                 "split_matrix: D2H pieces");
+        OZK_CUDA(cudaMemcpyAsync(residual, work.p, sizeof(double) * N * K,
+                                 cudaMemcpyDeviceToHost, os.s),
+                 "split_matrix: D2H residual");
+    } else {
+        // slices are (cols x ldk) per piece, residual is (cols x rows) K-word:
+        // transpose both back to the reference layout
+        OZK_CUDA(tmp.alloc(sizeof(double) * (N * K > d * N ? N * K : d * N), os.s),
+                 "split_matrix: tmp");
+        for (int a = 0; a < d; ++a)
+            OZK_CUDA(launch_transpose(1, sl.as<double>() + (size_t)a * outer * ldk, ldk,
+                                      tmp.as<double>() + (size_t)a * N, cols, cols, rows, os.s),
+                     "split_matrix: transpose pieces");
+        OZK_CUDA(cudaMemcpyAsync(pieces, tmp.p, sizeof(double) * d * N, cudaMemcpyDeviceToHost,
+                                 os.s),
+                 "split_matrix: D2H pieces");
+        OZK_CUDA(launch_transpose(K, work.as<double>(), rows, tmp.as<double>(), cols, cols, rows,
+                                  os.s),
+                 "split_matrix: transpose residual");
+        OZK_CUDA(cudaMemcpyAsync(residual, tmp.p, sizeof(double) * N * K, cudaMemcpyDeviceToHost,
+                                 os.s),
+                 "split_matrix: D2H residual");
+    }
+    OZK_CUDA(cudaStreamSynchronize(os.s), "split_matrix");
+    return OZK_OK;
+}
+
+ozk_status ozk_split_slices_device(ozk_format fmt, size_t rows, size_t cols, size_t ld,
+                                   const double* mat, int d, ozk_side side, double* slices,
+                                   double* piece_max, void* stream) {
+    if (!valid_fmt(fmt)) return fail(OZK_EPARAM, "split_matrix: format must be DD, TD or QD");
+    if (rows == 0 || cols == 0) return fail(OZK_ESHAPE, "matrix dimensions must be positive");
+    if (d < 1) return fail(OZK_EPARAM, "split_matrix: split count must be >= 1");
+    if (d > kMaxSplits) return fail(OZK_EPARAM, "split_matrix: split count above 32 is not supported");
+    if (ld < cols) return fail(OZK_ESHAPE, "split_matrix: ld < cols");
+    const int K = (int)fmt;
+    cudaStream_t st = (cudaStream_t)stream;
+    num_sms_cached();
+    DevBuf work, flags;
+    OZK_CUDA(work.alloc(sizeof(double) * rows * cols * K, st), "split_matrix: work");
+    OZK_CUDA(flags.alloc(8, st), "split_matrix: flags");
+    OZK_CUDA(cudaMemsetAsync(flags.p, 0, 8, st), "split_matrix: memset");
+    OZK_CUDA(split_to_slices(K, rows, cols, ld, mat, d, side, slices, work.as<double>(),
+                             reinterpret_cast<unsigned long long*>(piece_max), flags.as<int>(), st),
+             "split_matrix");
+    int flag = 0;
+    OZK_CUDA(cudaMemcpyAsync(&flag, flags.p, sizeof(int), cudaMemcpyDeviceToHost, st),
+             "split_matrix: flag");
+    OZK_CUDA(cudaStreamSynchronize(st), "split_matrix");
+    return check_dev_err(flag, "split_matrix");
+}
+
+ozk_status ozk_pair_list(int d, const double* amax, const double* bmax, double drop, int* pairs,
+                         int* npairs) {
+    if (d < 1) return fail(OZK_EPARAM, "pair_list: split count must be >= 1");
+    if (d > kMaxSplits) return fail(OZK_EPARAM, "pair_list: split count above 32 is not supported");
+    if (drop < 0.0) return fail(OZK_EPARAM, "pair_list: negative drop threshold");
+    PairList pl;
+    if (drop > 0.0)
+        pruned_pairs(d, amax, bmax, drop, pl);
+    else
+        triangular_pairs(d, pl);
+    for (int p = 0; p < pl.count; ++p) {
+        pairs[2 * p] = pl.alpha[p];
+        pairs[2 * p + 1] = pl.beta[p];
+    }
+    *npairs = pl.count;
+    return OZK_OK;
+}
+
+static ozk_status fill_pairs(int d, const int* pairs, int npairs, PairList& pl) {
+    if (npairs < 0 || npairs > kMaxPairs) return fail(OZK_EPARAM, "pair list too long");
+    pl.count = npairs;
+    for (int p = 0; p < npairs; ++p) {
+        if (pairs[2 * p] < 0 || pairs[2 * p] >= d || pairs[2 * p + 1] < 0 ||
+            pairs[2 * p + 1] >= d)
+            return fail(OZK_EPARAM, "pair index out of range");
+        pl.alpha[p] = (unsigned char)pairs[2 * p];
+        pl.beta[p] = (unsigned char)pairs[2 * p + 1];
+    }
+    return OZK_OK;
+}
+
+ozk_status ozk_slices_gemm_device(ozk_format fmt, size_t m, size_t l, size_t n,
+                                  const double* a_slices, const double* b_slices, size_t ncb,
+                                  size_t nblk, size_t b_blk_stride, int d, const int* pairs,
+                                  int npairs, double* c, size_t ldc, void* stream) {
+    if (!valid_fmt(fmt)) return fail(OZK_EPARAM, "slices_gemm: format must be DD, TD or QD");
+    if (m == 0 || l == 0 || n == 0) return fail(OZK_ESHAPE, "matrix dimensions must be positive");
+    if (d < 1 || d > kMaxSplits) return fail(OZK_EPARAM, "slices_gemm: bad split count");
+    if (ncb == 0 || nblk == 0 || ncb * nblk < n) return fail(OZK_ESHAPE, "slices_gemm: bad column blocks");
+    if (ldc < n) return fail(OZK_ESHAPE, "slices_gemm: ldc < n");
+    PairList pl;
+    if (ozk_status s = fill_pairs(d, pairs, npairs, pl)) return s;
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t ldk = slice_ld(l);
+    GemmProblem prob{};
+    prob.a = a_slices;
+    prob.lda = ldk;
+    prob.a_slice_stride = m * ldk;
+    prob.a_slices = d;
+    prob.b = b_slices;
+    prob.ldb = ldk;
+    prob.b_slice_stride = ncb * ldk;
+    prob.b_blk_stride = nblk > 1 ? b_blk_stride : (size_t)d * ncb * ldk;
+    prob.b_slices = d;
+    prob.ncb = (int)ncb;
+    prob.nblk = (int)nblk;
+    prob.m = m;
+    prob.n = n;
+    prob.l = l;
+    prob.c = c;
+    prob.ldc = ldc;
+    if (pl.count == 0) {
+        // nothing survives pruning: C = 0
+        for (size_t i = 0; i < m; ++i)
+            OZK_CUDA(cudaMemsetAsync(c + i * ldc * (int)fmt, 0, sizeof(double) * n * (int)fmt, st),
+                     "slices_gemm: zero");
+    } else {
+        OZK_CUDA(launch_pair_gemm((int)fmt, kAccumulate, prob, pl, st, num_sms_cached()),
+                 "slices_gemm");
+    }
+    OZK_CUDA(cudaStreamSynchronize(st), "slices_gemm");
+    return OZK_OK;
+}
+
+ozk_status ozk_pair_products_device(size_t m, size_t l, size_t n, const double* a_slices,
+                                    const double* b_slices, int d, const int* pairs, int npairs,
+                                    double* products, void* stream) {
+    if (m == 0 || l == 0 || n == 0) return fail(OZK_ESHAPE, "matrix dimensions must be positive");
+    if (d < 1 || d > kMaxSplits) return fail(OZK_EPARAM, "pair_products: bad split count");
+    PairList pl;
+    if (ozk_status s = fill_pairs(d, pairs, npairs, pl)) return s;
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t ldk = slice_ld(l);
+    GemmProblem prob{};
+    prob.a = a_slices;
+    prob.lda = ldk;
+    prob.a_slice_stride = m * ldk;
+    prob.a_slices = d;
+    prob.b = b_slices;
+    prob.ldb = ldk;
+    prob.b_slice_stride = n * ldk;
+    prob.b_blk_stride = (size_t)d * n * ldk;
+    prob.b_slices = d;
+    prob.ncb = (int)n;
+    prob.nblk = 1;
+    prob.m = m;
+    prob.n = n;
+    prob.l = l;
+    prob.c = products;
+    prob.ldc = n;
+    prob.c_pair_stride = m * n;
+    OZK_CUDA(launch_pair_gemm(1, kStoreProducts, prob, pl, st, num_sms_cached()), "pair_products");
+    OZK_CUDA(cudaStreamSynchronize(st), "pair_products");
+    return OZK_OK;
+}
+
+ozk_status ozk_backend_gemm_device(size_t m, size_t l, size_t n, const double* a,
+                                   const double* b, double* c, void* stream) {
+    if (m == 0 || l == 0 || n == 0) return fail(OZK_ESHAPE, "matrix dimensions must be positive");
+    if (m > 0x7fffffffull || n > 0x7fffffffull || l > 0x7fffffffull)
+        return fail(OZK_ESHAPE, "backend_gemm: dimension too large");
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t ldk = slice_ld(l);
+    DevBuf ap, bt;
+    OZK_CUDA(ap.alloc(sizeof(double) * m * ldk, st), "backend_gemm: A");
+    OZK_CUDA(bt.alloc(sizeof(double) * n * ldk, st), "backend_gemm: B^T");
+    if (ldk != l) OZK_CUDA(cudaMemsetAsync(ap.p, 0, sizeof(double) * m * ldk, st), "backend_gemm");
+    OZK_CUDA(cudaMemsetAsync(bt.p, 0, sizeof(double) * n * ldk, st), "backend_gemm");
+    OZK_CUDA(cudaMemcpy2DAsync(ap.p, ldk * 8, a, l * 8, l * 8, m, cudaMemcpyDeviceToDevice, st),
+             "backend_gemm: pad A");
+    OZK_CUDA(launch_transpose(1, b, n, bt.as<double>(), ldk, l, n, st), "backend_gemm: B^T");
+    GemmProblem prob{};
+    prob.a = ap.as<double>();
+    prob.lda = ldk;
+    prob.a_slice_stride = m * ldk;
+    prob.a_slices = 1;
+    prob.b = bt.as<double>();
+    prob.ldb = ldk;
+    prob.b_slice_stride = n * ldk;
+    prob.b_blk_stride = n * ldk;
+    prob.b_slices = 1;
+    prob.ncb = (int)n;
+    prob.nblk = 1;
+    prob.m = m;
+    prob.n = n;
+    prob.l = l;
+    prob.c = c;
+    prob.ldc = n;
+    PairList pl;
+    triangular_pairs(1, pl);
+    OZK_CUDA(launch_pair_gemm(1, kStorePlain, prob, pl, st, num_sms_cached()), "backend_gemm");
+    OZK_CUDA(cudaStreamSynchronize(st), "backend_gemm");
+    return OZK_OK;
+}
+
+ozk_status ozk_backend_gemm(size_t m, size_t l, size_t n, const double* a, const double* b,
+                            double* c) {
+    if (m == 0 || l == 0 || n == 0) return fail(OZK_ESHAPE, "matrix dimensions must be positive");
+    OwnStream os;
+    OZK_CUDA(os.create(), "backend_gemm: stream");
+    num_sms_cached();
+    DevBuf da, db, dc;
+    OZK_CUDA(da.alloc(sizeof(double) * m * l, os.s), "backend_gemm: A");
+    OZK_CUDA(db.alloc(sizeof(double) * l * n, os.s), "backend_gemm: B");
+    OZK_CUDA(dc.alloc(sizeof(double) * m * n, os.s), "backend_gemm: C");
+    OZK_CUDA(cudaMemcpyAsync(da.p, a, sizeof(double) * m * l, cudaMemcpyHostToDevice, os.s),
+             "backend_gemm: H2D");
+    OZK_CUDA(cudaMemcpyAsync(db.p, b, sizeof(double) * l * n, cudaMemcpyHostToDevice, os.s),
+             "backend_gemm: H2D");
+    if (ozk_status s = ozk_backend_gemm_device(m, l, n, da.as<double>(), db.as<double>(),
+                                               dc.as<double>(), os.s))
+        return s;
+    OZK_CUDA(cudaMemcpyAsync(c, dc.p, sizeof(double) * m * n, cudaMemcpyDeviceToHost, os.s),
+             "backend_gemm: D2H");
+    OZK_CUDA(cudaStreamSynchronize(os.s), "backend_gemm");
+    return OZK_OK;
+}
+
+ozk_status ozk_gen_eq1_device(ozk_format fmt, size_t rows, size_t cols, uint64_t seed,
+                              double* out, void* stream) {
+    if (!valid_fmt(fmt)) return fail(OZK_EPARAM, "gen_eq1: format must be DD, TD or QD");
+    if (rows == 0 || cols == 0) return fail(OZK_ESHAPE, "matrix dimensions must be positive");
+    cudaStream_t st = (cudaStream_t)stream;
+    OZK_CUDA(launch_gen_eq1((int)fmt, out, rows * cols, seed, st), "gen_eq1");
+    OZK_CUDA(cudaStreamSynchronize(st), "gen_eq1");
+    return OZK_OK;
+}
+
+}  // extern "C"

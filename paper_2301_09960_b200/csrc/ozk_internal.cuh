@@ -1,0 +1,68 @@
+// ozk_internal.cuh -- launchers shared between the kernel TUs and the C-ABI TU.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include <stdint.h>
+
+namespace ozk {
+
+constexpr int kMaxSplits = 32;                                  // D <= 32
+constexpr int kMaxPairs = kMaxSplits * (kMaxSplits + 1) / 2;    // 528
+
+// Device-side error flags raised by the split kernel (read back by the host).
+enum DevErr : int { kDevOk = 0, kDevNonFinite = 1, kDevTooLarge = 2 };
+
+// Leading dimension (doubles) of a slice row: the inner dimension rounded up to
+// 16 bytes, as TMA requires 16-byte global strides.  Pad entries are zero.
+inline size_t slice_ld(size_t inner) { return (inner + 1) & ~size_t(1); }
+
+// K1: per-row Ozaki split of a K-word matrix (ozaki.hpp:74-147, side rows).
+//   in      : rows x cols K-word AoS, row stride in_ld elements (may alias work)
+//   work    : rows x cols K-word AoS scratch (row stride cols); holds the residual
+//   pieces  : d slices, slice a row r at pieces + a*slice_stride + r*ldk
+//   piece_max (optional): d values, max |piece_a| as ordered uint64 bits
+//   err     : device flag (DevErr)
+cudaError_t launch_split_rows(int K, const double* in, size_t in_ld, double* work, size_t rows,
+                              size_t cols, int d, int sigma, double* pieces, size_t ldk,
+                              size_t slice_stride, unsigned long long* piece_max, int* err,
+                              cudaStream_t st);
+
+// Transpose of a K-word matrix: out(j, i) = in(i, j).  in is rows x cols with
+// row stride in_ld elements; out is cols x rows with row stride out_ld elements.
+cudaError_t launch_transpose(int K, const double* in, size_t in_ld, double* out, size_t out_ld,
+                             size_t rows, size_t cols, cudaStream_t st);
+
+// Slice-pair GEMM with fused epilogue (K2 + K3).
+enum GemmMode : int { kStorePlain = 0, kAccumulate = 1, kStoreProducts = 2 };
+
+struct PairList {
+    int count;
+    unsigned char alpha[kMaxPairs];
+    unsigned char beta[kMaxPairs];
+};
+
+struct GemmProblem {
+    // A slices: [d][m][lda] doubles (k contiguous); B^T slices in column blocks:
+    // column j lives in block j / ncb at b + blk*b_blk_stride + beta*b_slice_stride
+    // + (j % ncb)*ldb.
+    const double* a;
+    size_t lda, a_slice_stride;
+    int a_slices;
+    const double* b;
+    size_t ldb, b_slice_stride, b_blk_stride;
+    int b_slices;
+    int ncb, nblk;
+    size_t m, n, l;
+    double* c;          // K-word AoS (kAccumulate) or doubles (other modes)
+    size_t ldc;         // elements per row of C
+    size_t c_pair_stride;  // kStoreProducts: doubles between consecutive pair products
+};
+
+cudaError_t launch_pair_gemm(int K, GemmMode mode, const GemmProblem& prob, const PairList& pairs,
+                             cudaStream_t st, int num_sms);
+
+// Device Eq. (1)-distributed K-word generator (synthetic bench inputs).
+cudaError_t launch_gen_eq1(int K, double* out, size_t count, uint64_t seed, cudaStream_t st);
+
+} // namespace ozk

@@ -1,0 +1,238 @@
+// split.cu -- K1: the Ozaki split (error-free extraction of FP64 slices) and
+// the K-word transpose that turns the B-side (per-column) split into a per-row
+// one with k-contiguous output slices.
+//
+// Reference: split_matrix<K> (proj/include/mpmat/ozaki.hpp:74-147) with
+// exponent_ceil_log2 (:36-40), shift_extract (:53-56), leading_image and the
+// per-row max (dense_matrix.hpp:72-96) and MultiFloat<K>::operator-=(double)
+// (multifloat.hpp:391 -> :290-300).
+//
+// Layout: one CTA owns one row (A side) / one column (B side, after the
+// transpose) and runs all D extraction passes on it, so the D dependent
+// row-max reductions are CTA-local (warp shuffles + one smem hop) and never
+// touch the grid.  The K-word residual is swept once per pass through the
+// `work` buffer; a row is at most l*K*8 bytes (256 KiB for QD at l=8192), so
+// the per-pass re-reads stay in L2 and HBM sees ~one read of the input plus
+// one write per slice.  Slices are written k-contiguous with a 16-byte padded
+// leading dimension, which is the operand layout the DMMA GEMM's TMA loads.
+#include "kword.cuh"
+#include "ozk_internal.cuh"
+
+namespace ozk {
+namespace {
+
+constexpr int kSplitThreads = 256;
+
+__device__ __forceinline__ int ceil_log2(double x) {
+    int e = ilogb(x);
+    return scalbn(1.0, e) == x ? e : e + 1;
+}
+
+// Block-wide max of a non-negative double; every thread gets the result.
+__device__ __forceinline__ double block_max(double v, double* red) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, off));
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    if (warp == 0) {
+        v = lane < (int)(blockDim.x >> 5) ? red[lane] : 0.0;
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, off));
+        if (lane == 0) red[32] = v;
+    }
+    __syncthreads();
+    v = red[32];
+    __syncthreads();
+    return v;
+}
+
+template <int K>
+__device__ __forceinline__ void load_kw(const double* p, double* c) {
+    if constexpr (K == 2) {
+        double2 v = *reinterpret_cast<const double2*>(p);
+        c[0] = v.x;
+        c[1] = v.y;
+    } else if constexpr (K == 4) {
+        double2 v0 = reinterpret_cast<const double2*>(p)[0];
+        double2 v1 = reinterpret_cast<const double2*>(p)[1];
+        c[0] = v0.x;
+        c[1] = v0.y;
+        c[2] = v1.x;
+        c[3] = v1.y;
+    } else {
+#pragma unroll
+        for (int k = 0; k < K; ++k) c[k] = p[k];
+    }
+}
+
+template <int K>
+__device__ __forceinline__ void store_kw(double* p, const double* c) {
+    if constexpr (K == 2) {
+        *reinterpret_cast<double2*>(p) = make_double2(c[0], c[1]);
+    } else if constexpr (K == 4) {
+        reinterpret_cast<double2*>(p)[0] = make_double2(c[0], c[1]);
+        reinterpret_cast<double2*>(p)[1] = make_double2(c[2], c[3]);
+    } else {
+#pragma unroll
+        for (int k = 0; k < K; ++k) p[k] = c[k];
+    }
+}
+
+template <int K>
+__global__ void __launch_bounds__(kSplitThreads)
+split_rows_kernel(const double* __restrict__ in, size_t in_ld, double* __restrict__ work,
+                  size_t cols, int d, int sigma, double* __restrict__ pieces, size_t ldk,
+                  size_t slice_stride, unsigned long long* __restrict__ piece_max,
+                  int* __restrict__ err) {
+    __shared__ double red[33];
+    const size_t r = blockIdx.x;
+    const double* src = in + r * in_ld * K;
+    double* w = work + r * cols * K;
+    double* prow = pieces + r * ldk;
+
+    // Sweep 0: leading image max, finiteness scan (ozaki.hpp:77-78), and the
+    // copy of the input row into the working residual.
+    double mx = 0.0;
+    int bad = 0;
+    for (size_t j = threadIdx.x; j < cols; j += kSplitThreads) {
+        double c[K];
+        load_kw<K>(src + j * K, c);
+        bad |= !dfinite(c[0]);
+        mx = fmax(mx, fabs(c[0]));
+        if (src != w) store_kw<K>(w + j * K, c);
+    }
+    if (__syncthreads_or(bad)) {
+        if (threadIdx.x == 0) atomicMax(err, (int)kDevNonFinite);
+        return;
+    }
+    mx = block_max(mx, red);
+
+    if (d == 1) {
+        // D = 1: the piece is the leading image, the residual keeps the tail
+        // (ozaki.hpp:90-96: every element, zero or not, gets residual -= lead).
+        double pmx = 0.0;
+        for (size_t j = threadIdx.x; j < cols; j += kSplitThreads) {
+            double c[K];
+            load_kw<K>(w + j * K, c);
+            const double lead = c[0];
+            prow[j] = lead;
+            kw_add<K>(c, -lead);
+            store_kw<K>(w + j * K, c);
+            pmx = fmax(pmx, fabs(lead));
+        }
+        for (size_t j = cols + threadIdx.x; j < ldk; j += kSplitThreads) prow[j] = 0.0;
+        if (piece_max) {
+            pmx = block_max(pmx, red);
+            if (threadIdx.x == 0)
+                atomicMax(piece_max, static_cast<unsigned long long>(__double_as_longlong(pmx)));
+        }
+        return;
+    }
+
+    for (int a = 0; a < d; ++a) {
+        double* pa = prow + (size_t)a * slice_stride;
+        double tau = 0.0;  // zero marks a skipped (all-zero) row, ozaki.hpp:105-107
+        if (mx != 0.0) {
+            const int e = ceil_log2(mx);
+            if (e + sigma > 1020) {  // ozaki.hpp:109 (mx is block-uniform)
+                if (threadIdx.x == 0) atomicMax(err, (int)kDevTooLarge);
+                return;
+            }
+            tau = scalbn(1.0, e + sigma);
+        }
+        double nmx = 0.0, pmx = 0.0;
+        for (size_t j = threadIdx.x; j < cols; j += kSplitThreads) {
+            if (tau == 0.0) {
+                pa[j] = 0.0;
+                continue;
+            }
+            double c[K];
+            load_kw<K>(w + j * K, c);
+            // shift_extract: (v + tau) - tau, strictly rounded (ozaki.hpp:53-56)
+            const double x = __dsub_rn(__dadd_rn(c[0], tau), tau);
+            pa[j] = x;
+            if (x != 0.0) {
+                kw_add<K>(c, -x);  // w -= x  ==  w + (-x)  (multifloat.hpp:302,391)
+                store_kw<K>(w + j * K, c);
+            }
+            nmx = fmax(nmx, fabs(c[0]));
+            pmx = fmax(pmx, fabs(x));
+        }
+        for (size_t j = cols + threadIdx.x; j < ldk; j += kSplitThreads) pa[j] = 0.0;
+        if (piece_max) {
+            pmx = block_max(pmx, red);
+            if (threadIdx.x == 0)
+                atomicMax(piece_max + a,
+                          static_cast<unsigned long long>(__double_as_longlong(pmx)));
+        }
+        mx = block_max(nmx, red);
+    }
+}
+
+template <int K>
+__global__ void transpose_kernel(const double* __restrict__ in, size_t in_ld,
+                                 double* __restrict__ out, size_t out_ld, size_t rows,
+                                 size_t cols) {
+    __shared__ double tile[32][32 * K + 1];
+    const size_t c0 = (size_t)blockIdx.x * 32, r0 = (size_t)blockIdx.y * 32;
+    for (int yy = threadIdx.y; yy < 32; yy += 8) {
+        const size_t i = r0 + yy;
+        if (i >= rows) break;
+        const double* src = in + (i * in_ld + c0) * K;
+        for (int q = threadIdx.x; q < 32 * K; q += 32)
+            if (c0 + q / K < cols) tile[yy][q] = src[q];
+    }
+    __syncthreads();
+    for (int xx = threadIdx.y; xx < 32; xx += 8) {
+        const size_t j = c0 + xx;
+        if (j >= cols) break;
+        double* dst = out + (j * out_ld + r0) * K;
+        for (int q = threadIdx.x; q < 32 * K; q += 32) {
+            const int yy = q / K, w = q - yy * K;
+            if (r0 + yy < rows) dst[q] = tile[yy][xx * K + w];
+        }
+    }
+}
+
+} // namespace
+
+cudaError_t launch_split_rows(int K, const double* in, size_t in_ld, double* work, size_t rows,
+                              size_t cols, int d, int sigma, double* pieces, size_t ldk,
+                              size_t slice_stride, unsigned long long* piece_max, int* err,
+                              cudaStream_t st) {
+    if (rows == 0) return cudaSuccess;
+    dim3 grid((unsigned)rows), block(kSplitThreads);
+    switch (K) {
+    case 2:
+        split_rows_kernel<2><<<grid, block, 0, st>>>(in, in_ld, work, cols, d, sigma, pieces, ldk,
+                                                     slice_stride, piece_max, err);
+        break;
+    case 3:
+        split_rows_kernel<3><<<grid, block, 0, st>>>(in, in_ld, work, cols, d, sigma, pieces, ldk,
+                                                     slice_stride, piece_max, err);
+        break;
+    case 4:
+        split_rows_kernel<4><<<grid, block, 0, st>>>(in, in_ld, work, cols, d, sigma, pieces, ldk,
+                                                     slice_stride, piece_max, err);
+        break;
+    default: return cudaErrorInvalidValue;
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_transpose(int K, const double* in, size_t in_ld, double* out, size_t out_ld,
+                             size_t rows, size_t cols, cudaStream_t st) {
+    if (rows == 0 || cols == 0) return cudaSuccess;
+    dim3 grid((unsigned)((cols + 31) / 32), (unsigned)((rows + 31) / 32)), block(32, 8);
+    switch (K) {
+    case 1: transpose_kernel<1><<<grid, block, 0, st>>>(in, in_ld, out, out_ld, rows, cols); break;
+    case 2: transpose_kernel<2><<<grid, block, 0, st>>>(in, in_ld, out, out_ld, rows, cols); break;
+    case 3: transpose_kernel<3><<<grid, block, 0, st>>>(in, in_ld, out, out_ld, rows, cols); break;
+    case 4: transpose_kernel<4><<<grid, block, 0, st>>>(in, in_ld, out, out_ld, rows, cols); break;
+    default: return cudaErrorInvalidValue;
+    }
+    return cudaGetLastError();
+}
+
+} // namespace ozk

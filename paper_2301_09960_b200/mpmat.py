@@ -1,0 +1,225 @@
+"""Python mirror of the reference mpmat hot-path API, running on the B200 library.
+
+Names, argument meaning and error behaviour follow the reference C++ library
+(paths relative to /root/reference/proj/include/mpmat/):
+
+=====================================  =====================================
+this module                            reference
+=====================================  =====================================
+``error``/``shape_error``/``param_error``  errors.hpp:7-17
+``SplitSide``                          ozaki.hpp:33
+``split_shift_bits``                   ozaki.hpp:43-48
+``exponent_ceil_log2``                 ozaki.hpp:36-40
+``SplitSet`` / ``split_matrix``        ozaki.hpp:59-67 / :74-147
+``OzakiProfile``                       ozaki.hpp:149-167
+``ozaki_gemm``                         ozaki.hpp:180-249 (returns ``(C, profile)``)
+``gpu_backend`` (a ``GemmBackend``)    backend.hpp:12-20
+=====================================  =====================================
+
+A K-word matrix ``DenseMatrix<MultiFloat<K>>`` is a float64 array of shape
+``(rows, cols, K)`` (its exact memory image).  numpy arrays and CPU torch
+tensors go through the host-buffer C entry points; CUDA torch tensors go
+through the device entry points on torch's current stream.
+"""
+from __future__ import annotations
+
+import ctypes
+import enum
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from ._lib import OZK_ECUDA, OZK_ENCCL, OZK_ENOMEM, OZK_EPARAM, OZK_ESHAPE, OzkProfile, lib
+
+try:  # torch is optional for the host path
+    import torch
+except ImportError:  # pragma: no cover
+    torch = None
+
+
+class error(RuntimeError):
+    """mpmat::error (errors.hpp:7-9)."""
+
+
+class shape_error(error):
+    """mpmat::shape_error (errors.hpp:11-13)."""
+
+
+class param_error(error):
+    """mpmat::param_error (errors.hpp:15-17)."""
+
+
+class cuda_error(error):
+    """Device failure (no reference counterpart: the reference is CPU-only)."""
+
+
+def _raise(status: int) -> None:
+    if status == 0:
+        return
+    msg = lib.ozk_last_error().decode(errors="replace")
+    if status == OZK_ESHAPE:
+        raise shape_error(msg)
+    if status == OZK_EPARAM:
+        raise param_error(msg)
+    if status == OZK_ENOMEM:
+        raise MemoryError(msg)
+    if status in (OZK_ECUDA, OZK_ENCCL):
+        raise cuda_error(msg)
+    raise error(msg)
+
+
+class SplitSide(enum.IntEnum):
+    rows = 0  # left factor A
+    cols = 1  # right factor B
+
+
+FORMATS = {2: "dd", 3: "td", 4: "qd"}
+
+
+def split_shift_bits(inner_dim: int) -> int:
+    return lib.ozk_split_shift_bits(inner_dim)
+
+
+def exponent_ceil_log2(x: float) -> int:
+    return lib.ozk_exponent_ceil_log2(float(x))
+
+
+@dataclass
+class OzakiProfile:
+    split_seconds: float = 0.0
+    product_seconds: float = 0.0
+    accumulate_seconds: float = 0.0
+    split_count: int = 0
+    pairs: int = 0
+    transfer_seconds: float = 0.0
+
+    def total_seconds(self) -> float:
+        return self.split_seconds + self.product_seconds + self.accumulate_seconds
+
+    def _frac(self, v: float) -> float:
+        t = self.total_seconds()
+        return v / t if t > 0 else 0.0
+
+    def split_fraction(self) -> float:
+        return self._frac(self.split_seconds)
+
+    def product_fraction(self) -> float:
+        return self._frac(self.product_seconds)
+
+    def accumulate_fraction(self) -> float:
+        return self._frac(self.accumulate_seconds)
+
+    @classmethod
+    def _of(cls, p: OzkProfile) -> "OzakiProfile":
+        return cls(p.split_seconds, p.product_seconds, p.accumulate_seconds, p.split_count,
+                   p.pairs, p.transfer_seconds)
+
+
+@dataclass
+class SplitSet:
+    pieces: list = field(default_factory=list)
+    residual: np.ndarray | None = None
+    side: SplitSide = SplitSide.rows
+    split_count: int = 0
+    short_bits: int = 53
+    inner_dim: int = 0
+
+
+def _is_cuda(x) -> bool:
+    return torch is not None and isinstance(x, torch.Tensor) and x.is_cuda
+
+
+def _kword_shape(x) -> tuple[int, int, int]:
+    if x.ndim != 3:
+        raise shape_error("K-word matrix must have shape (rows, cols, K)")
+    r, c, k = (int(s) for s in x.shape)
+    if k not in FORMATS:
+        raise param_error("K must be 2 (DD), 3 (TD) or 4 (QD)")
+    return r, c, k
+
+
+def _host(x) -> np.ndarray:
+    if torch is not None and isinstance(x, torch.Tensor):
+        x = x.detach().cpu().numpy()
+    a = np.ascontiguousarray(x, dtype=np.float64)
+    return a
+
+
+def _stream_handle() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def ozaki_gemm(a, b, d: int, backend=None, drop_threshold: float = 0.0):
+    """Long-precision product via the Ozaki split (ozaki.hpp:180-249).
+
+    ``backend`` must be ``None`` or :func:`gpu_backend` -- the slice products
+    always run on the fused DMMA kernel (any conforming backend gives the same
+    C, test_ozaki.cpp:227-233).  Returns ``(C, OzakiProfile)``.
+    """
+    if backend is not None and not getattr(backend, "_ozk_gpu", False):
+        raise param_error("ozaki_gemm: only the B200 DMMA backend is supported")
+    m, l, ka = _kword_shape(a)
+    l2, n, kb = _kword_shape(b)
+    if ka != kb:
+        raise param_error("ozaki_gemm: A and B must have the same K")
+    if l != l2:
+        raise shape_error("ozaki_gemm: inner dimensions differ")
+    prof = OzkProfile()
+    if _is_cuda(a) or _is_cuda(b):
+        if not (_is_cuda(a) and _is_cuda(b)):
+            raise param_error("ozaki_gemm: A and B must live on the same device")
+        ad, bd = a.contiguous(), b.contiguous()
+        if ad.dtype != torch.float64 or bd.dtype != torch.float64:
+            raise param_error("ozaki_gemm: float64 tensors required")
+        c = torch.empty((m, n, ka), dtype=torch.float64, device=a.device)
+        st = lib.ozk_ozaki_gemm_device(ka, m, l, n, ad.data_ptr(), bd.data_ptr(), int(d),
+                                       float(drop_threshold), c.data_ptr(), _stream_handle(),
+                                       ctypes.byref(prof))
+        _raise(st)
+        return c, OzakiProfile._of(prof)
+    ah, bh = _host(a), _host(b)
+    c = np.empty((m, n, ka), dtype=np.float64)
+    st = lib.ozk_ozaki_gemm(ka, m, l, n, ah.ctypes.data, bh.ctypes.data, int(d),
+                            float(drop_threshold), c.ctypes.data, ctypes.byref(prof))
+    _raise(st)
+    return c, OzakiProfile._of(prof)
+
+
+def split_matrix(m, d: int, side: SplitSide) -> SplitSet:
+    """split_matrix<K> (ozaki.hpp:74-147): pieces + K-word residual (host arrays)."""
+    rows, cols, k = _kword_shape(m)
+    mh = _host(m)
+    dd = max(int(d), 1)
+    pieces = np.zeros((dd, rows, cols), dtype=np.float64)
+    resid = np.empty_like(mh)
+    st = lib.ozk_split(k, rows, cols, mh.ctypes.data, int(d), int(side), pieces.ctypes.data,
+                       resid.ctypes.data)
+    _raise(st)
+    return SplitSet(pieces=[pieces[i] for i in range(dd)], residual=resid, side=SplitSide(side),
+                    split_count=int(d), inner_dim=cols if side == SplitSide.rows else rows)
+
+
+def gpu_backend():
+    """A GemmBackend (backend.hpp:12-13): ``c = backend(a, b)`` on binary64 matrices."""
+
+    def backend(a, b):
+        if _is_cuda(a) and _is_cuda(b):
+            ad, bd = a.contiguous(), b.contiguous()
+            m, l = ad.shape
+            l2, n = bd.shape
+            if l != l2:
+                raise shape_error("backend: inner dimensions differ")
+            c = torch.empty((m, n), dtype=torch.float64, device=a.device)
+            _raise(lib.ozk_backend_gemm_device(m, l, n, ad.data_ptr(), bd.data_ptr(),
+                                               c.data_ptr(), _stream_handle()))
+            return c
+        ah, bh = _host(a), _host(b)
+        if ah.ndim != 2 or bh.ndim != 2 or ah.shape[1] != bh.shape[0]:
+            raise shape_error("backend: inner dimensions differ")
+        c = np.empty((ah.shape[0], bh.shape[1]), dtype=np.float64)
+        _raise(lib.ozk_backend_gemm(ah.shape[0], ah.shape[1], bh.shape[1], ah.ctypes.data,
+                                    bh.ctypes.data, c.ctypes.data))
+        return c
+
+    backend._ozk_gpu = True
+    return backend
