@@ -1,0 +1,373 @@
+#!/usr/bin/env python3
+"""Benchmark of the B200 Ozaki-scheme multiple-precision GEMM (BASELINE.json metric).
+
+One "step" = one full Ozaki GEMM C = A*B at n = 8192 (split of A and B into
+FP64 slices, the P = D(D+1)/2 slice-pair DMMA GEMMs, and the fused K-word
+accumulation) on device-resident synthetic Eq. (1) inputs.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--format td] [--impl ours|reference]
+
+N > 1 runs under torchrun: C block-rows are sharded across ranks, each rank
+splits its A row block and its B column block, and the B slices are
+all-gathered over NCCL (paper_2301_09960_b200/sharded.py).  Rank 0 prints ONE
+JSON line.  ``--impl reference`` times the reference's own CPU implementation
+(oracle/_ref, the unmodified reference compiled in place; the C restatement
+when that is absent) on all host cores on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = ("effective DD/TD/QD GEMM GFLOP/s (2n^3/t), n=8192; slice DGEMM % of FP64 peak")
+WORKLOADS = {"dd": (2, 6), "td": (3, 9), "qd": (4, 12)}  # K, headline D
+NAMES = {"dd": "DD", "td": "TD", "qd": "QD"}
+KERNELS_PER_STEP = 4  # split A, transpose B, split B, fused slice GEMM
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=3)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    p.add_argument("--format", choices=sorted(WORKLOADS), default="td")
+    p.add_argument("--n", type=int, default=8192)
+    p.add_argument("--d", type=int, default=None)
+    p.add_argument("--variants", default="dd,qd",
+                   help="other formats timed (1 step each) and reported under 'variants'")
+    p.add_argument("--cpu-sample", type=int, default=1024,
+                   help="rows/cols of the CPU baseline sub-GEMM (inner dim stays n)")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-e2e", action="store_true")
+    return p.parse_args()
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")),
+            int(os.environ.get("LOCAL_RANK", "0")))
+
+
+# ---------------------------------------------------------------------------
+# clocks during the timed region (B200_PROFILING.md recipe)
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        rows = []
+        for line in open(self.path):
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                rows.append((float(parts[1]), float(parts[2]), float(parts[3]), parts[5:9]))
+            except ValueError:
+                continue
+        os.unlink(self.path)
+        if not rows:
+            return None
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i, v in enumerate(r[3]) if v == "Active"})
+        return {"sm_mhz": statistics.median(r[0] for r in rows), "sm_max_mhz": rows[0][1],
+                "power_w_max": max(r[2] for r in rows), "samples": len(rows),
+                "reasons": reasons}
+
+
+# ---------------------------------------------------------------------------
+# CPU arms (oracle/: the reference compiled in place, else the C restatement)
+# ---------------------------------------------------------------------------
+def cpu_sample_rate(K: int, d: int, n: int, r: int, reps: int = 1):
+    """Reference CPU Ozaki on an r x n . n x r sub-GEMM (same inner dimension,
+    so the same sigma, slice widths and D as the n x n workload)."""
+    import numpy as np
+
+    import oracle
+    cpu = oracle.best()
+    cores = os.cpu_count() or 1
+    if hasattr(cpu, "set_threads"):
+        cores = cpu.set_threads(cores)
+    else:
+        cores = 1  # the C restatement is single-threaded
+    a = cpu.gen_eq1(K, r, n, 1)
+    b = cpu.gen_eq1(K, n, r, 2)
+    best = None
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        c = cpu.ozaki_gemm(K, a, b, d)
+        dt = time.perf_counter() - t0
+        best = dt if best is None else min(best, dt)
+    del c, a, b, np
+    return 2.0 * r * r * n / best / 1e9, best, cores, cpu.kind
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    K, d0 = WORKLOADS[args.format]
+    d = args.d or d0
+    n, r = args.n, args.cpu_sample
+    for _ in range(args.warmup):
+        cpu_sample_rate(K, d, n, r)
+    rates, times = [], []
+    for _ in range(args.steps):
+        rate, dt, cores, kind = cpu_sample_rate(K, d, n, r)
+        rates.append(rate)
+        times.append(dt)
+    value = statistics.mean(rates)
+    sample = (f"{NAMES[args.format]} Ozaki sub-GEMM {r}x{n} . {n}x{r}, D={d} (inner dim n "
+              f"as in the workload), reference ozaki_gemm<K> + reference_backend()")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "GFLOP/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(1e3 * statistics.mean(times), 3), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": config_of(args, K, d, n),
+        "cpu_baseline": {"value": round(value, 4), "unit": "GFLOP/s", "cores": cores,
+                         "kind": kind, "sample": sample},
+        "e2e": {"value": round(value, 4), "unit": "GFLOP/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def config_of(args, K, d, n):
+    return {"workload": f"{NAMES[args.format]} Ozaki GEMM n={n} D={d} (BASELINE config 3)",
+            "format": args.format, "n": n, "split_count": d, "pairs": d * (d + 1) // 2,
+            "parallelism": f"C block-rows x{args.gpus}" if args.gpus > 1 else "single GPU",
+            "l2": "no flush: A, B and C are each > 126 MB L2 (K*8*n^2 bytes)"}
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+def run_ours(args):
+    import torch
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    from paper_2301_09960_b200 import lib
+    from paper_2301_09960_b200._lib import OzkProfile
+
+    K, d0 = WORKLOADS[args.format]
+    d = args.d or d0
+    n = args.n
+    P = d * (d + 1) // 2
+    stream = torch.cuda.current_stream()
+    sh = stream.cuda_stream
+
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl")
+        from paper_2301_09960_b200.sharded import ShardedOzaki
+        eng = ShardedOzaki(K, n, n, n, d, rank, world)
+
+    def check(st):
+        if st != 0:
+            raise RuntimeError(lib.ozk_last_error().decode())
+
+    # synthetic Eq. (1) inputs generated on device (outside the timed region)
+    A = torch.empty((n, n, K), dtype=torch.float64, device="cuda")
+    B = torch.empty((n, n, K), dtype=torch.float64, device="cuda")
+    check(lib.ozk_gen_eq1_device(K, n, n, 1, A.data_ptr(), sh))
+    check(lib.ozk_gen_eq1_device(K, n, n, 2, B.data_ptr(), sh))
+
+    peak = lib.ozk_probe_dmma_tflops(20000, sh)
+
+    if world == 1:
+        C = torch.empty((n, n, K), dtype=torch.float64, device="cuda")
+
+        def step(prof):
+            check(lib.ozk_ozaki_gemm_device(K, n, n, n, A.data_ptr(), B.data_ptr(), d, 0.0,
+                                            C.data_ptr(), sh, ctypes.byref(prof)))
+    else:
+        def step(prof):
+            eng.run(A, B, prof)
+
+    prof = OzkProfile()
+    for _ in range(args.warmup):
+        step(prof)
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    kern, split = [], []
+    e0.record(stream)
+    for _ in range(args.steps):
+        step(prof)
+        kern.append(prof.product_seconds)
+        split.append(prof.split_seconds)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    clk = clocks.stop()
+    t_step = e0.elapsed_time(e1) * 1e-3 / args.steps
+    if world > 1:
+        t = torch.tensor([t_step], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        t_step = float(t.item())
+    flops_eff = 2.0 * n ** 3
+    value = flops_eff / t_step / 1e9
+    t_kern = statistics.mean(kern)
+    rows_local = n if world == 1 else eng.rows_local
+    kern_flops = P * 2.0 * rows_local * n * n
+    achieved = kern_flops / t_kern / 1e12
+
+    e2e = None
+    if not args.no_e2e and world == 1:
+        e2e = run_e2e(args, lib, OzkProfile, A, B, K, d, n)
+
+    variants = []
+    if world == 1:
+        del C
+        for fmt in [v for v in args.variants.split(",") if v and v != args.format]:
+            variants.append(run_variant(lib, OzkProfile, fmt, n, peak, sh))
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        rate, dt, cores, kind = cpu_sample_rate(K, d, n, args.cpu_sample)
+        cpu = {"value": round(rate, 4), "unit": "GFLOP/s", "cores": cores, "kind": kind,
+               "sample": f"{NAMES[args.format]} Ozaki sub-GEMM {args.cpu_sample}x{n} . "
+                         f"{n}x{args.cpu_sample}, D={d}, one call ({dt:.2f} s)"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 3), "unit": "GFLOP/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * t_step, 3),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic: Eq. (1)-distributed K-word matrices generated on device "
+                    "(counter-based splitmix64, csrc/gen.cu)",
+            "config": config_of(args, K, d, n),
+            "slice_dgemm_frac_of_fp64_peak": round(achieved / peak, 4) if peak > 0 else None,
+            "phases_ms": {"split": round(1e3 * statistics.mean(split), 3),
+                          "slice_gemm_fused_accumulate": round(1e3 * t_kern, 3)},
+            "roofline": {"bound": "tensor", "kernel": "pair_gemm_kernel (DMMA + K-word epilogue)",
+                         "achieved": round(achieved, 3), "peak": round(peak, 3),
+                         "unit": "TFLOP/s", "frac": round(achieved / peak, 4) if peak > 0 else None,
+                         "traffic": None,
+                         "work_per_launch": f"P*2*m*n*l = {kern_flops:.4g} flop",
+                         "peak_source": "FP64 DMMA ceiling measured in this run "
+                                        "(ozk_probe_dmma_tflops: register-resident "
+                                        "mma.m8n8k4.f64 on all SMs); MEASURED_PEAKS.json has "
+                                        "no FP64 figure; nominal B200 FP64 tensor 40 TF"},
+            "gpu_launches": KERNELS_PER_STEP * args.steps,
+            "clocks": clk,
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+            "variants": variants,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+def run_e2e(args, lib, OzkProfile, A, B, K, d, n):
+    """Same metric through the host-buffer C-ABI entry point (ozk_ozaki_gemm):
+    H2D of A and B from pinned memory, the GEMM, D2H of C, every step."""
+    import torch
+    ha = A.cpu().pin_memory()
+    hb = B.cpu().pin_memory()
+    hc = torch.empty((n, n, K), dtype=torch.float64).pin_memory()
+    prof = OzkProfile()
+
+    def call():
+        st = lib.ozk_ozaki_gemm(K, n, n, n, ha.data_ptr(), hb.data_ptr(), d, 0.0, hc.data_ptr(),
+                                ctypes.byref(prof))
+        if st != 0:
+            raise RuntimeError(lib.ozk_last_error().decode())
+
+    call()
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        call()
+        times.append(time.perf_counter() - t0)
+    t = statistics.mean(times)
+    return {"value": round(2.0 * n ** 3 / t / 1e9, 3), "unit": "GFLOP/s",
+            "h2d_bytes_per_step": 2 * n * n * K * 8, "d2h_bytes_per_step": n * n * K * 8,
+            "ms_per_step": round(1e3 * t, 3), "api": "ozk_ozaki_gemm (host buffers, pinned)"}
+
+
+def run_variant(lib, OzkProfile, fmt, n, peak, sh):
+    import torch
+    K, d = WORKLOADS[fmt]
+    P = d * (d + 1) // 2
+    A = torch.empty((n, n, K), dtype=torch.float64, device="cuda")
+    B = torch.empty((n, n, K), dtype=torch.float64, device="cuda")
+    C = torch.empty((n, n, K), dtype=torch.float64, device="cuda")
+    lib.ozk_gen_eq1_device(K, n, n, 1, A.data_ptr(), sh)
+    lib.ozk_gen_eq1_device(K, n, n, 2, B.data_ptr(), sh)
+    prof = OzkProfile()
+
+    def call():
+        st = lib.ozk_ozaki_gemm_device(K, n, n, n, A.data_ptr(), B.data_ptr(), d, 0.0,
+                                       C.data_ptr(), sh, ctypes.byref(prof))
+        if st != 0:
+            raise RuntimeError(lib.ozk_last_error().decode())
+
+    call()
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    call()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    t = e0.elapsed_time(e1) * 1e-3
+    achieved = P * 2.0 * n ** 3 / prof.product_seconds / 1e12
+    return {"workload": f"{NAMES[fmt]} Ozaki GEMM n={n} D={d}", "value": round(2.0 * n ** 3 / t / 1e9, 3),
+            "unit": "GFLOP/s", "ms_per_step": round(1e3 * t, 3),
+            "split_ms": round(1e3 * prof.split_seconds, 3),
+            "slice_gemm_tflops": round(achieved, 3),
+            "slice_dgemm_frac_of_fp64_peak": round(achieved / peak, 4) if peak > 0 else None}
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -151,6 +151,11 @@ ozk_status ozk_pair_products_device(size_t m, size_t l, size_t n, const double* 
 ozk_status ozk_gen_eq1_device(ozk_format fmt, size_t rows, size_t cols, uint64_t seed,
                               double* out, void* stream);
 
+/* FP64 tensor-pipe (DMMA) ceiling of the current device in TFLOP/s, measured by a
+ * register-resident mma.sync.m8n8k4.f64 loop on every SM (the roofline
+ * denominator for the slice GEMMs).  Returns < 0 on failure. */
+double ozk_probe_dmma_tflops(int iters, void* stream);
+
 const char* ozk_last_error(void);
 int ozk_version(void);
 

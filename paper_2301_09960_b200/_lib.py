@@ -56,6 +56,7 @@ SIGNATURES = {
                                                 ctypes.c_int, _dp, ctypes.c_void_p]),
     "ozk_gen_eq1_device": (ctypes.c_int, [ctypes.c_int, _sz, _sz, ctypes.c_uint64, _dp,
                                           ctypes.c_void_p]),
+    "ozk_probe_dmma_tflops": (ctypes.c_double, [ctypes.c_int, ctypes.c_void_p]),
     "ozk_last_error": (ctypes.c_char_p, []),
     "ozk_version": (ctypes.c_int, []),
 }
