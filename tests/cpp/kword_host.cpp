@@ -1,0 +1,26 @@
+// Host build of the device K-word library (paper_2301_09960_b200/csrc/kword.cuh),
+// so its operation sequence can be checked bit-for-bit against the reference's
+// MultiFloat<K>::operator+(double) on the CPU (tests/test_kword_host.py).
+// Test infrastructure; compiled with -ffp-contract=off like the reference.
+#include <cstddef>
+
+#include "../../paper_2301_09960_b200/csrc/kword.cuh"
+
+template <int K>
+static void run(std::size_t n, const double* x, const double* y, double* out) {
+    for (std::size_t i = 0; i < n; ++i) {
+        double w[K];
+        for (int k = 0; k < K; ++k) w[k] = x[i * K + k];
+        ozk::kw_add<K>(w, y[i]);
+        for (int k = 0; k < K; ++k) out[i * K + k] = w[k];
+    }
+}
+
+extern "C" int kw_host_add(int K, std::size_t n, const double* x, const double* y, double* out) {
+    switch (K) {
+    case 2: run<2>(n, x, y, out); return 0;
+    case 3: run<3>(n, x, y, out); return 0;
+    case 4: run<4>(n, x, y, out); return 0;
+    default: return 2;
+    }
+}
