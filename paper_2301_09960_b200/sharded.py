@@ -1,0 +1,184 @@
+"""C block-row sharding of one Ozaki GEMM across the GPUs of a node.
+
+Rank r of W owns C rows [r0, r1) and B columns [c0, c1):
+
+1. split its A row block on its own GPU (per-row split: bit-identical to the
+   rows of the global split, ozaki.hpp:102-103);
+2. split its B column block (per-column split: bit-identical to the columns of
+   the global split);
+3. all-gather the B slices over NCCL (NVLink/NVSwitch) -- the path's one real
+   exchange step: D * l * ceil(n/W) * 8 bytes per rank;
+4. with drop_threshold > 0, all-reduce(max) the per-slice maxima so every rank
+   prunes the same pairs (ozaki.hpp:198-221);
+5. run every slice pair for its rows with the fused accumulation.  The
+   per-element accumulation order is unchanged, so C is bit-identical for any
+   number of GPUs.
+
+The gathered B slices stay in the layout the all-gather produces
+([W][D][ncb][ld]); the GEMM kernel addresses column j in block j // ncb
+directly (ozk_slices_gemm_device), so no re-layout copy is needed.
+
+Device work goes through an ``ops`` object; :class:`GpuOps` drives libozk.so.
+The CPU tests substitute an oracle-backed implementation of the same four
+operations to check the partitioning, padding, gather layout and pair logic
+with the gloo backend.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import torch
+import torch.distributed as dist
+
+
+def block_range(total: int, parts: int, idx: int) -> tuple[int, int]:
+    """Contiguous near-equal partition (first total % parts blocks get one more)."""
+    base, extra = divmod(total, parts)
+    lo = idx * base + min(idx, extra)
+    return lo, lo + base + (1 if idx < extra else 0)
+
+
+def triangular_pairs(d: int) -> list[tuple[int, int]]:
+    return [(a, b) for a in range(d) for b in range(d - a)]
+
+
+def pruned_pairs(d, amax, bmax, drop) -> list[tuple[int, int]]:
+    """ozaki.hpp:198-221."""
+    lead = amax[0] * bmax[0]
+    out = []
+    for a in range(d):
+        for b in range(d - a):
+            if drop > 0.0 and amax[a] * bmax[b] < drop * lead:
+                continue
+            out.append((a, b))
+    return out
+
+
+@dataclass
+class ShardPlan:
+    K: int
+    m: int
+    l: int
+    n: int
+    d: int
+    rank: int
+    world: int
+
+    def __post_init__(self):
+        self.r0, self.r1 = block_range(self.m, self.world, self.rank)
+        self.ncb = -(-self.n // self.world)          # columns per B block (padded)
+        self.c0 = min(self.rank * self.ncb, self.n)
+        self.c1 = min(self.c0 + self.ncb, self.n)
+        self.ld = (self.l + 1) & ~1                  # ozk_slice_ld
+
+    @property
+    def rows_local(self) -> int:
+        return self.r1 - self.r0
+
+
+class GpuOps:
+    """libozk.so device entry points on torch CUDA tensors (current stream)."""
+
+    def __init__(self):
+        from ._lib import lib
+        self.lib = lib
+        self.device = torch.device("cuda", torch.cuda.current_device())
+
+    def _check(self, st):
+        if st != 0:
+            raise RuntimeError(self.lib.ozk_last_error().decode())
+
+    def _stream(self):
+        return torch.cuda.current_stream().cuda_stream
+
+    def zeros(self, shape):
+        return torch.zeros(shape, dtype=torch.float64, device=self.device)
+
+    def split(self, K, mat, rows, cols, ld, d, side, out, pmax):
+        """mat: tensor view whose data_ptr is element (0,0); row stride ld elements."""
+        self._check(self.lib.ozk_split_slices_device(
+            K, rows, cols, ld, mat.data_ptr(), d, side, out.data_ptr(),
+            pmax.data_ptr() if pmax is not None else None, self._stream()))
+
+    def gemm(self, plan: ShardPlan, sa, sb_all, pairs, c):
+        flat = (ctypes.c_int * (2 * len(pairs)))(*[v for p in pairs for v in p])
+        self._check(self.lib.ozk_slices_gemm_device(
+            plan.K, plan.rows_local, plan.l, plan.n, sa.data_ptr(), sb_all.data_ptr(), plan.ncb,
+            plan.world, plan.d * plan.ncb * plan.ld, plan.d, flat, len(pairs), c.data_ptr(),
+            plan.n, self._stream()))
+
+
+class ShardedOzaki:
+    """One rank's part of a C block-row sharded Ozaki GEMM."""
+
+    def __init__(self, K, m, l, n, d, rank, world, ops=None, group=None, drop_threshold=0.0):
+        self.plan = ShardPlan(K, m, l, n, d, rank, world)
+        self.ops = ops if ops is not None else GpuOps()
+        self.group = group
+        self.drop = float(drop_threshold)
+        p = self.plan
+        self.sa = self.ops.zeros((d, max(p.rows_local, 1), p.ld))
+        self.sb = self.ops.zeros((d, p.ncb, p.ld))
+        self.sb_all = self.ops.zeros((world, d, p.ncb, p.ld))
+        self.c = self.ops.zeros((max(p.rows_local, 1), n, K))
+        self.pmax = self.ops.zeros((2, d)) if self.drop > 0.0 else None
+        self.timing = hasattr(self.ops, "device") and self.ops.device.type == "cuda"
+
+    @property
+    def rows_local(self) -> int:
+        return self.plan.rows_local
+
+    def _all_gather(self):
+        if dist.get_backend(self.group) == "nccl":
+            dist.all_gather_into_tensor(self.sb_all, self.sb, group=self.group)
+        else:
+            parts = list(self.sb_all.unbind(0))
+            dist.all_gather(parts, self.sb, group=self.group)
+
+    def run(self, A, B, prof=None):
+        """A: (m, l, K) or this rank's rows; B: (l, n, K) full (row stride n).
+        Returns this rank's C rows (rows_local, n, K)."""
+        p, ops = self.plan, self.ops
+        if self.timing:
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+            ev[0].record()
+        a_rows = A[p.r0:p.r1] if A.shape[0] == p.m else A
+        if self.pmax is not None:
+            self.pmax.zero_()
+        if p.rows_local:
+            ops.split(p.K, a_rows, p.rows_local, p.l, p.l, p.d, 0, self.sa,
+                      self.pmax[0] if self.pmax is not None else None)
+        if p.c1 > p.c0:
+            # column block [c0, c1) of the row-major (l x n) B, split in place
+            ops.split(p.K, B[:, p.c0:p.c1], p.l, p.c1 - p.c0, p.n, p.d, 1, self.sb,
+                      self.pmax[1] if self.pmax is not None else None)
+        if self.timing:
+            ev[1].record()
+        self._all_gather()
+        if self.pmax is not None:
+            dist.all_reduce(self.pmax, op=dist.ReduceOp.MAX, group=self.group)
+            mx = self.pmax.cpu().tolist()
+            pairs = pruned_pairs(p.d, mx[0], mx[1], self.drop)
+        else:
+            pairs = triangular_pairs(p.d)
+        if self.timing:
+            ev[2].record()
+        if p.rows_local:
+            if pairs:
+                ops.gemm(p, self.sa, self.sb_all, pairs, self.c)
+            else:
+                self.c.zero_()
+        if self.timing:
+            ev[3].record()
+            torch.cuda.current_stream().synchronize()
+            if prof is not None:
+                prof.split_seconds = ev[0].elapsed_time(ev[1]) * 1e-3
+                prof.transfer_seconds = ev[1].elapsed_time(ev[2]) * 1e-3
+                prof.product_seconds = ev[2].elapsed_time(ev[3]) * 1e-3
+                prof.accumulate_seconds = 0.0
+                prof.total_seconds = ev[0].elapsed_time(ev[3]) * 1e-3
+                prof.split_count = p.d
+                prof.pairs = len(pairs)
+                prof.gpus = p.world
+        return self.c[: p.rows_local]

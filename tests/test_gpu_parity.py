@@ -260,3 +260,36 @@ def test_config2_dd_n4096_slices_and_sampled_c(ozk, cpu, port, d):
     want, inexact = port.replay_elements(2, pa, pb, pairs, ii, jj)
     assert inexact == 0
     assert_bitwise(c[ii, jj], want, "sampled C")
+
+
+@pytest.mark.parametrize("K,m,l,n,d,world", [(2, 300, 257, 390, 6, 3), (3, 129, 140, 256, 9, 2),
+                                             (4, 64, 96, 130, 12, 4)])
+def test_sharded_layout_single_gpu(ozk, cpu, K, m, l, n, d, world):
+    """The sharded data path on one GPU: each emulated rank splits its B column
+    block in place (ld = n) into the all-gather layout [W][D][ncb][ld], splits
+    its A row block, and runs the block-addressed fused GEMM.  Its C rows must
+    equal the reference's rows bit for bit."""
+    import ctypes
+
+    import torch
+
+    from paper_2301_09960_b200.sharded import GpuOps, ShardPlan, triangular_pairs
+    a = cpu.gen_eq1(K, m, l, 41)
+    b = cpu.gen_eq1(K, l, n, 42)
+    want = cpu.ozaki_gemm(K, a, b, d)
+    A = torch.from_numpy(a).cuda()
+    B = torch.from_numpy(b).cuda()
+    ops = GpuOps()
+    plans = [ShardPlan(K, m, l, n, d, r, world) for r in range(world)]
+    p0 = plans[0]
+    sb_all = ops.zeros((world, d, p0.ncb, p0.ld))
+    for p in plans:
+        if p.c1 > p.c0:
+            ops.split(K, B[:, p.c0:p.c1], l, p.c1 - p.c0, n, d, 1, sb_all[p.rank], None)
+    pairs = triangular_pairs(d)
+    for p in plans:
+        sa = ops.zeros((d, p.rows_local, p.ld))
+        ops.split(K, A[p.r0:p.r1], p.rows_local, l, l, d, 0, sa, None)
+        c = ops.zeros((p.rows_local, n, K))
+        ops.gemm(p, sa, sb_all, pairs, c)
+        assert_bitwise(c.cpu().numpy(), want[p.r0:p.r1], f"rank {p.rank} rows")
