@@ -110,14 +110,17 @@ int ozk_exponent_ceil_log2(double x);        /* ozaki.hpp:36-40 (x > 0, finite) 
  *   side ROWS (left factor A, m x l):  slices[a][i][k] = piece_a(i, k)
  *   side COLS (right factor B, l x n): slices[a][j][k] = piece_a(k, j)
  * `ld` is the row stride (in elements) of the input K-word matrix, so a
- * column block of B can be split in place.  piece_max (nullable) receives
+ * column block of B can be split in place.  Slice planes are plane_rows
+ * (>= outer) rows apart, so a ragged last column block keeps the padded
+ * block layout; rows past `outer` are left untouched.  piece_max (nullable) receives
  * max|piece_a| per slice (for drop_threshold, ozaki.hpp:198-208), combined by
  * max with whatever it held (zero-fill it first). */
 size_t ozk_slice_ld(size_t inner_dim);
 
 ozk_status ozk_split_slices_device(ozk_format fmt, size_t rows, size_t cols, size_t ld,
                                    const double* mat, int split_count, ozk_side side,
-                                   double* slices, double* piece_max, void* stream);
+                                   double* slices, size_t plane_rows, double* piece_max,
+                                   void* stream);
 
 /* Pair list of ozaki.hpp:198-221 (alpha-major, triangular, drop pruning).
  * pairs receives 2*npairs ints (alpha, beta); capacity split_count^2 ints. */

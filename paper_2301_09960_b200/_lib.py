@@ -47,7 +47,7 @@ SIGNATURES = {
     "ozk_exponent_ceil_log2": (ctypes.c_int, [ctypes.c_double]),
     "ozk_slice_ld": (_sz, [_sz]),
     "ozk_split_slices_device": (ctypes.c_int, [ctypes.c_int, _sz, _sz, _sz, _dp, ctypes.c_int,
-                                               ctypes.c_int, _dp, _dp, ctypes.c_void_p]),
+                                               ctypes.c_int, _dp, _sz, _dp, ctypes.c_void_p]),
     "ozk_pair_list": (ctypes.c_int, [ctypes.c_int, _dp, _dp, ctypes.c_double, _ip, _ip]),
     "ozk_slices_gemm_device": (ctypes.c_int, [ctypes.c_int, _sz, _sz, _sz, _dp, _dp, _sz, _sz,
                                               _sz, ctypes.c_int, _ip, ctypes.c_int, _dp, _sz,

@@ -123,20 +123,19 @@ ozk_status check_dev_err(int flag, const char* what) {
 // Split of a K-word matrix into slices in the operand layout (see ozk.h).
 // work must hold outer*inner*K doubles.  Returns a CUDA error code.
 cudaError_t split_to_slices(int K, size_t rows, size_t cols, size_t ld, const double* mat, int d,
-                            int side, double* slices, double* work, unsigned long long* pmax,
-                            int* err, cudaStream_t st) {
+                            int side, double* slices, size_t plane_rows, double* work,
+                            unsigned long long* pmax, int* err, cudaStream_t st) {
     const size_t inner = side == OZK_SIDE_ROWS ? cols : rows;
-    const size_t outer = side == OZK_SIDE_ROWS ? rows : cols;
     const size_t ldk = slice_ld(inner);
     const int sigma = shift_bits(inner);
     if (side == OZK_SIDE_ROWS)
-        return launch_split_rows(K, mat, ld, work, rows, cols, d, sigma, slices, ldk, outer * ldk,
-                                 pmax, err, st);
+        return launch_split_rows(K, mat, ld, work, rows, cols, d, sigma, slices, ldk,
+                                 plane_rows * ldk, pmax, err, st);
     // columns: transpose to (cols x rows) so each column is a contiguous row
     cudaError_t e = launch_transpose(K, mat, ld, work, rows, rows, cols, st);
     if (e != cudaSuccess) return e;
-    return launch_split_rows(K, work, rows, work, cols, rows, d, sigma, slices, ldk, outer * ldk,
-                             pmax, err, st);
+    return launch_split_rows(K, work, rows, work, cols, rows, d, sigma, slices, ldk,
+                             plane_rows * ldk, pmax, err, st);
 }
 
 struct Timer {
@@ -180,11 +179,11 @@ ozk_status ozaki_device_impl(int K, size_t m, size_t l, size_t n, const double* 
 
     Timer tm(prof != nullptr);
     tm.mark(0, st);
-    OZK_CUDA(split_to_slices(K, m, l, l, a, d, OZK_SIDE_ROWS, sa.as<double>(), work.as<double>(),
-                             want_max ? amax : nullptr, err, st),
+    OZK_CUDA(split_to_slices(K, m, l, l, a, d, OZK_SIDE_ROWS, sa.as<double>(), m,
+                             work.as<double>(), want_max ? amax : nullptr, err, st),
              "ozaki_gemm: split A");
-    OZK_CUDA(split_to_slices(K, l, n, n, b, d, OZK_SIDE_COLS, sb.as<double>(), work.as<double>(),
-                             want_max ? bmax : nullptr, err, st),
+    OZK_CUDA(split_to_slices(K, l, n, n, b, d, OZK_SIDE_COLS, sb.as<double>(), n,
+                             work.as<double>(), want_max ? bmax : nullptr, err, st),
              "ozaki_gemm: split B");
     tm.mark(1, st);
 
@@ -334,7 +333,7 @@ ozk_status ozk_split(ozk_format fmt, size_t rows, size_t cols, const double* mat
     OZK_CUDA(cudaMemcpyAsync(dm.p, mat, sizeof(double) * N * K, cudaMemcpyHostToDevice, os.s),
              "split_matrix: H2D");
     OZK_CUDA(split_to_slices(K, rows, cols, cols, dm.as<double>(), d, side, sl.as<double>(),
-                             work.as<double>(), nullptr, flags.as<int>(), os.s),
+                             outer, work.as<double>(), nullptr, flags.as<int>(), os.s),
              "split_matrix");
     int flag = 0;
     OZK_CUDA(cudaMemcpyAsync(&flag, flags.p, sizeof(int), cudaMemcpyDeviceToHost, os.s),
@@ -373,12 +372,14 @@ ozk_status ozk_split(ozk_format fmt, size_t rows, size_t cols, const double* mat
 
 ozk_status ozk_split_slices_device(ozk_format fmt, size_t rows, size_t cols, size_t ld,
                                    const double* mat, int d, ozk_side side, double* slices,
-                                   double* piece_max, void* stream) {
+                                   size_t plane_rows, double* piece_max, void* stream) {
     if (!valid_fmt(fmt)) return fail(OZK_EPARAM, "split_matrix: format must be DD, TD or QD");
     if (rows == 0 || cols == 0) return fail(OZK_ESHAPE, "matrix dimensions must be positive");
     if (d < 1) return fail(OZK_EPARAM, "split_matrix: split count must be >= 1");
     if (d > kMaxSplits) return fail(OZK_EPARAM, "split_matrix: split count above 32 is not supported");
     if (ld < cols) return fail(OZK_ESHAPE, "split_matrix: ld < cols");
+    if (plane_rows < (side == OZK_SIDE_ROWS ? rows : cols))
+        return fail(OZK_ESHAPE, "split_matrix: plane_rows < outer dimension");
     const int K = (int)fmt;
     cudaStream_t st = (cudaStream_t)stream;
     num_sms_cached();
@@ -386,8 +387,9 @@ ozk_status ozk_split_slices_device(ozk_format fmt, size_t rows, size_t cols, siz
     OZK_CUDA(work.alloc(sizeof(double) * rows * cols * K, st), "split_matrix: work");
     OZK_CUDA(flags.alloc(8, st), "split_matrix: flags");
     OZK_CUDA(cudaMemsetAsync(flags.p, 0, 8, st), "split_matrix: memset");
-    OZK_CUDA(split_to_slices(K, rows, cols, ld, mat, d, side, slices, work.as<double>(),
-                             reinterpret_cast<unsigned long long*>(piece_max), flags.as<int>(), st),
+    OZK_CUDA(split_to_slices(K, rows, cols, ld, mat, d, side, slices, plane_rows,
+                             work.as<double>(), reinterpret_cast<unsigned long long*>(piece_max),
+                             flags.as<int>(), st),
              "split_matrix");
     int flag = 0;
     OZK_CUDA(cudaMemcpyAsync(&flag, flags.p, sizeof(int), cudaMemcpyDeviceToHost, st),

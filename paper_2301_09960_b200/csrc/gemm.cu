@@ -15,17 +15,21 @@
 // B200 mapping
 //  * FP64 tensor cores are reachable only through mma.sync (tcgen05 has no
 //    kind::f64); m8n8k4.f64 lowers 1:1 to SASS DMMA.8x8x4.
-//  * Persistent CTAs, one per SM: 8 warps (2 per SM sub-partition, so each
-//    thread may hold up to 255 registers) own a 128x128 C tile as 2x4 warp
-//    tiles of 64x32 (64 FP64 accumulators per thread).  128x16 A and B^T
-//    tiles arrive by TMA (cp.async.bulk.tensor, 128-byte swizzle) in a
-//    5-stage mbarrier ring; thread 0 re-arms a slot as soon as all eight
-//    warps have released it (a dedicated 9th producer warp would put three
-//    warps on one sub-partition and cap registers at 168, forcing spills).
-//  * Each CTA walks tile -> pair -> k-block; the TMA issue runs ahead across
-//    pair and tile boundaries, so the only DMMA bubble is the K-word
-//    epilogue (a global read-modify-write of the C tile, ~0.2 % of a pair's
-//    mainloop at l = 8192).
+//  * Persistent CTAs, one per SM: 8 consumer warps in two ping-pong groups
+//    of 4 (one warp of each group per SM sub-partition) plus a producer
+//    warpgroup.  A group owns a 64x128 C tile (four 64x32 warp tiles, 64 FP64
+//    accumulators per thread) and its own 4-stage ring of 64x16 A and 128x16
+//    B^T tiles filled by TMA (cp.async.bulk.tensor, 128-byte swizzle) under
+//    mbarriers; one producer lane per group keeps its ring full.
+//    setmaxnreg moves registers from the producer warpgroup (40) to the
+//    consumers (232): two consumers + one producer per sub-partition fit its
+//    16K-register file.
+//  * A group walks tile -> pair -> k-block; its loads run ahead across pair
+//    and tile boundaries.  The K-word epilogue (a read-modify-write of the C
+//    tile after every pair) stalls only its own group: the other group's
+//    warp on the same sub-partition keeps the DMMA pipe busy.  The C rows of
+//    the coming epilogue are prefetched into L2 a few k-blocks ahead and
+//    read in batches of eight elements.
 //  * k is permuted inside a 16-wide k-block: lane t feeds k = 4t..4t+3 to
 //    the four k-steps, so every operand fetch is one conflict-free LDS.128
 //    (16-byte chunk (2t+h) ^ (row & 7) of a swizzled 128-byte row).  A and B
@@ -39,14 +43,27 @@
 namespace ozk {
 namespace {
 
-constexpr int BM = 128, BN = 128, BK = 16;
-constexpr int kStages = 5;
-constexpr int kConsumerWarps = 8;
-constexpr int kThreads = kConsumerWarps * 32;
-constexpr int kTileBytes = BM * BK * 8;          // 16 KiB per operand tile
-constexpr int kStageBytes = 2 * kTileBytes;      // A + B
-constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
-constexpr int kGroupM = 8;                       // tile raster group (L2 reuse)
+// Ping-pong layout: two independent 4-warp consumer groups per CTA, one warp
+// of each on every SM sub-partition, plus a producer warpgroup.  A group owns
+// a BM x BN C tile (its 4 warps each own 64 x 32) and its own TMA ring, so
+// while one group runs its K-word epilogue the other keeps the
+// sub-partition's DMMA pipe busy (one warp with 32 independent accumulators
+// saturates it).
+constexpr int BM = 64, BN = 128, BK = 16;
+constexpr int kStages = 4;                       // per group
+constexpr int kGroups = 2;
+constexpr int kWarpsPerGroup = 4;
+constexpr int kConsumerWarps = kGroups * kWarpsPerGroup;
+constexpr int kThreads = (kConsumerWarps + 4) * 32;   // + producer warpgroup
+constexpr int kConsumerRegs = 232;               // setmaxnreg budget: 2*232 + 40 per SMSP
+constexpr int kProducerRegs = 40;
+constexpr int kATileBytes = BM * BK * 8;         // 8 KiB
+constexpr int kBTileBytes = BN * BK * 8;         // 16 KiB
+constexpr int kStageBytes = kATileBytes + kBTileBytes;
+constexpr int kGroupSmem = kStages * kStageBytes;
+constexpr int kSmemBytes = kGroups * kGroupSmem + 1024 /*align*/ + 256 /*barriers*/;
+constexpr int kGroupM = 16;                      // tile raster group (L2 reuse)
+constexpr int kPrefetchKb = 6;                   // k-blocks before the epilogue: L2 prefetch of C
 
 struct TmaMaps {
     CUtensorMap a;  // 3D: (k, row, slice)
@@ -130,10 +147,16 @@ __device__ __forceinline__ TileCoord tile_of(int id, int tiles_m, int tiles_n_bl
     return t;
 }
 
-// Producer-side iterator over the flat (tile, pair, k-block) sequence.
-struct ProdIter {
-    int tile, p, kb;
-};
+__device__ __forceinline__ bool mbar_test(uint32_t bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
 
 template <int K, int MODE>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -142,60 +165,78 @@ pair_gemm_kernel(const __grid_constant__ TmaMaps maps, const __grid_constant__ P
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~uintptr_t(1023));
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
-    const uint32_t smem_base = smem_u32(smem);
-    const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + kStages);
-
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    uint64_t* bars_all = reinterpret_cast<uint64_t*>(smem + kGroups * kGroupSmem);
+    const uint32_t start_bar = smem_u32(bars_all + kGroups * 2 * kStages);
+
     const int num_tiles = tiles_m * tiles_n_blk * prob.nblk;
     const int num_kb = (int)((prob.l + BK - 1) / BK);
     const int npairs = pairs.count;
+    const int nworkers = gridDim.x * kGroups;
 
-    // TMA issue for one ring slot: A_alpha rows of the tile, B_beta^T rows of
-    // the tile's column block, both the k-block kb.
-    auto issue = [&](const ProdIter& it, int stage) {
-        const TileCoord tc = tile_of(it.tile, tiles_m, tiles_n_blk, prob.nblk);
-        const uint32_t full = full0 + 8 * stage;
-        mbar_expect_tx(full, kStageBytes);
-        const uint32_t sa = smem_base + stage * kStageBytes;
-        tma_load_3d(sa, &maps.a, full, it.kb * BK, tc.tm * BM, pairs.alpha[it.p]);
-        tma_load_4d(sa + kTileBytes, &maps.b, full, it.kb * BK, tc.jt * BN, pairs.beta[it.p],
-                    tc.blk);
-    };
-    auto advance = [&](ProdIter& it) {
-        if (++it.kb == num_kb) {
-            it.kb = 0;
-            if (++it.p == npairs) {
-                it.p = 0;
-                it.tile += gridDim.x;
-            }
-        }
-    };
-
-    ProdIter pit{(int)blockIdx.x, 0, 0};
     if (threadIdx.x == 0) {
-        for (int s = 0; s < kStages; ++s) {
-            mbar_init(full0 + 8 * s, 1);
-            mbar_init(empty0 + 8 * s, kConsumerWarps);
-        }
+        for (int b = 0; b < kGroups * 2 * kStages; ++b)
+            mbar_init(smem_u32(bars_all + b), (b % (2 * kStages)) < kStages ? 1 : kWarpsPerGroup);
+        mbar_init(start_bar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&maps.a)));
-        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&maps.b)));
-        for (int s = 0; s < kStages && pit.tile < num_tiles; ++s) {
-            issue(pit, s);
-            advance(pit);
-        }
     }
     __syncthreads();
 
-    const int wm = warp >> 2;  // 0..1 : 64-row half of the tile
-    const int wn = warp & 3;   // 0..3 : 32-col quarter
+    if (warp >= kConsumerWarps) {
+        // ---------------- producer warpgroup: one lane per consumer group ----------------
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kProducerRegs));
+        const int grp = warp - kConsumerWarps;
+        if (grp >= kGroups || lane != 0) return;
+        const uint32_t ring = smem_u32(smem) + grp * kGroupSmem;
+        const uint32_t full0 = smem_u32(bars_all + grp * 2 * kStages);
+        const uint32_t empty0 = full0 + 8 * kStages;
+        if (grp == 0) {
+            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&maps.a)));
+            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&maps.b)));
+        }
+        int stage = 0;
+        uint32_t phase = 0;
+        for (int tile = blockIdx.x * kGroups + grp; tile < num_tiles; tile += nworkers) {
+            const TileCoord tc = tile_of(tile, tiles_m, tiles_n_blk, prob.nblk);
+            for (int p = 0; p < npairs; ++p) {
+                const int al = pairs.alpha[p], be = pairs.beta[p];
+                for (int kb = 0; kb < num_kb; ++kb) {
+                    mbar_wait(empty0 + 8 * stage, phase ^ 1);
+                    const uint32_t full = full0 + 8 * stage;
+                    mbar_expect_tx(full, kStageBytes);
+                    const uint32_t sa = ring + stage * kStageBytes;
+                    tma_load_3d(sa, &maps.a, full, kb * BK, tc.tm * BM, al);
+                    tma_load_4d(sa + kATileBytes, &maps.b, full, kb * BK, tc.jt * BN, be, tc.blk);
+                    if (++stage == kStages) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        }
+        return;
+    }
+
+    // ---------------- DMMA consumers ----------------
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kConsumerRegs));
+    const int grp = warp / kWarpsPerGroup;   // ping-pong group
+    const int wn = warp % kWarpsPerGroup;    // 32-column quarter of the group tile
+    const uint32_t ring = smem_u32(smem) + grp * kGroupSmem;
+    const uint32_t full0 = smem_u32(bars_all + grp * 2 * kStages);
+    const uint32_t empty0 = full0 + 8 * kStages;
+    const int worker = blockIdx.x * kGroups + grp;
+    // Group 0 releases group 1 half-way through its first pair, so the two
+    // groups' epilogues start out of phase (their drift afterwards is neutral).
+    const int kick_kb = num_kb / 2;
+    if (grp == 0 && wn == 0 && lane == 0 && worker >= num_tiles) mbar_arrive(start_bar);
+    if (grp == 1) mbar_wait(start_bar, 0);
+
     const int g = lane >> 2, t = lane & 3;
     // byte offsets of this lane's 16-byte chunk for k-half h = 0/1 (swizzled)
     const uint32_t chunk0 = (uint32_t)(((2 * t + 0) ^ g) << 4);
     const uint32_t chunk1 = (uint32_t)(((2 * t + 1) ^ g) << 4);
-    const uint32_t a_row = (uint32_t)((wm * 64 + g) * 128);
-    const uint32_t b_row = (uint32_t)(kTileBytes + (wn * 32 + g) * 128);
+    const uint32_t a_row = (uint32_t)(g * 128);
+    const uint32_t b_row = (uint32_t)(kATileBytes + (wn * 32 + g) * 128);
 
     double acc[8][4][2];
 #pragma unroll
@@ -205,20 +246,52 @@ pair_gemm_kernel(const __grid_constant__ TmaMaps maps, const __grid_constant__ P
 
     int stage = 0;
     uint32_t phase = 0;
-    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+    bool kicked = false;
+    for (int tile = worker; tile < num_tiles; tile += nworkers) {
         const TileCoord tc = tile_of(tile, tiles_m, tiles_n_blk, prob.nblk);
+        const size_t row0 = (size_t)tc.tm * BM + g;
+        const int jj0 = tc.jt * BN + wn * 32 + 2 * t;
+        // element validity masks (rows by mf, columns by nf*2+v)
+        uint32_t rmask = 0, cmask = 0;
+#pragma unroll
+        for (int mf = 0; mf < 8; ++mf) rmask |= (row0 + mf * 8 < prob.m) ? (1u << mf) : 0u;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const int jj = jj0 + (q >> 1) * 8 + (q & 1);
+            const size_t col = (size_t)tc.blk * prob.ncb + jj;
+            cmask |= (jj < prob.ncb && col < prob.n) ? (1u << q) : 0u;
+        }
+        const size_t col0 = (size_t)tc.blk * prob.ncb + jj0;
+
         for (int p = 0; p < npairs; ++p) {
             for (int kb = 0; kb < num_kb; ++kb) {
+                if (grp == 0 && !kicked && kb == kick_kb) {
+                    kicked = true;
+                    if (wn == 0 && lane == 0) mbar_arrive(start_bar);
+                }
                 mbar_wait(full0 + 8 * stage, phase);
-                const uint32_t sbase = smem_base + stage * kStageBytes;
+                const uint32_t sbase = ring + stage * kStageBytes;
+                // dep: XOR of every fragment this warp reads from the stage.
+                // Feeding it (masked by a runtime zero) into the release
+                // address makes the arrive wait, through the register
+                // scoreboard, for all of the stage's LDS to have returned; a
+                // bare arrive can issue while the last LDS is in flight and
+                // let TMA overwrite the slot under it.
+                uint32_t dep = 0;
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
                     const uint32_t ch = h ? chunk1 : chunk0;
                     double2 af[8], bf[4];
 #pragma unroll
-                    for (int mf = 0; mf < 8; ++mf) af[mf] = lds128(sbase + a_row + mf * 1024 + ch);
+                    for (int mf = 0; mf < 8; ++mf) {
+                        af[mf] = lds128(sbase + a_row + mf * 1024 + ch);
+                        dep ^= (uint32_t)__double2loint(af[mf].x);
+                    }
 #pragma unroll
-                    for (int nf = 0; nf < 4; ++nf) bf[nf] = lds128(sbase + b_row + nf * 1024 + ch);
+                    for (int nf = 0; nf < 4; ++nf) {
+                        bf[nf] = lds128(sbase + b_row + nf * 1024 + ch);
+                        dep ^= (uint32_t)__double2loint(bf[nf].x);
+                    }
 #pragma unroll
                     for (int u = 0; u < 2; ++u)
 #pragma unroll
@@ -229,57 +302,70 @@ pair_gemm_kernel(const __grid_constant__ TmaMaps maps, const __grid_constant__ P
                                      u ? bf[nf].y : bf[nf].x);
                 }
                 __syncwarp();
-                if (lane == 0) mbar_arrive(empty0 + 8 * stage);
-                // Thread 0 refills this slot once every warp has released it.
-                if (threadIdx.x == 0 && pit.tile < num_tiles) {
-                    mbar_wait(empty0 + 8 * stage, phase);
-                    issue(pit, stage);
-                    advance(pit);
-                }
+                if (lane == 0) mbar_arrive(empty0 + 8 * stage + (dep & prob.zero));
                 if (++stage == kStages) {
                     stage = 0;
                     phase ^= 1;
                 }
-            }
-
-            // ---------------- epilogue for pair p of this tile ----------------
-            const size_t row0 = (size_t)tc.tm * BM + wm * 64 + g;
-            const int jj0 = tc.jt * BN + wn * 32 + 2 * t;
+                if constexpr (MODE == kAccumulate) {
+                    if (kb == num_kb - kPrefetchKb && p > 0) {
+                        // pull this pair's C rows into L2 ahead of the read-modify-write
 #pragma unroll
-            for (int mf = 0; mf < 8; ++mf) {
-                const size_t row = row0 + mf * 8;
+                        for (int mf = 0; mf < 8; ++mf)
 #pragma unroll
-                for (int nf = 0; nf < 4; ++nf) {
-#pragma unroll
-                    for (int v = 0; v < 2; ++v) {
-                        const int jj = jj0 + nf * 8 + v;
-                        const size_t col = (size_t)tc.blk * prob.ncb + jj;
-                        const double y = acc[mf][nf][v];
-                        acc[mf][nf][v] = 0.0;
-                        if (row >= prob.m || jj >= prob.ncb || col >= prob.n) continue;
-                        if constexpr (MODE == kAccumulate) {
-                            double* cp = prob.c + (row * prob.ldc + col) * K;
-                            double w[K];
-                            if (p == 0) {
-#pragma unroll
-                                for (int k = 0; k < K; ++k) w[k] = 0.0;
-                            } else {
-#pragma unroll
-                                for (int k = 0; k < K; ++k) w[k] = cp[k];
-                            }
-                            kw_add<K>(w, y);
-#pragma unroll
-                            for (int k = 0; k < K; ++k) cp[k] = w[k];
-                        } else if constexpr (MODE == kStorePlain) {
-                            prob.c[row * prob.ldc + col] = y;
-                        } else {
-                            prob.c[(size_t)p * prob.c_pair_stride + row * prob.ldc + col] = y;
-                        }
+                            for (int nf = 0; nf < 4; ++nf)
+                                if ((rmask >> mf) & (cmask >> (2 * nf)) & 1u)
+                                    asm volatile("prefetch.global.L2 [%0];" ::"l"(
+                                        prob.c + ((row0 + mf * 8) * prob.ldc + col0 + nf * 8) * K));
                     }
                 }
             }
+
+            // ---------------- epilogue for pair p of this tile ----------------
+#pragma unroll
+            for (int mf = 0; mf < 8; ++mf) {
+                const size_t row = row0 + mf * 8;
+                if constexpr (MODE == kAccumulate) {
+                    // batch: load the 8 K-word elements of this row first
+                    double w[8][K];
+                    double* cp = prob.c + (row * prob.ldc + col0) * K;
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        const bool ok = (rmask >> mf) & (cmask >> q) & 1u;
+                        const int off = ((q >> 1) * 8 + (q & 1)) * K;
+#pragma unroll
+                        for (int k = 0; k < K; ++k) w[q][k] = (ok && p > 0) ? cp[off + k] : 0.0;
+                    }
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) kw_add<K>(w[q], acc[mf][q >> 1][q & 1]);
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        const bool ok = (rmask >> mf) & (cmask >> q) & 1u;
+                        const int off = ((q >> 1) * 8 + (q & 1)) * K;
+                        if (ok) {
+#pragma unroll
+                            for (int k = 0; k < K; ++k) cp[off + k] = w[q][k];
+                        }
+                    }
+                } else {
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        if (!((rmask >> mf) & (cmask >> q) & 1u)) continue;
+                        const size_t col = col0 + (q >> 1) * 8 + (q & 1);
+                        const double y = acc[mf][q >> 1][q & 1];
+                        if constexpr (MODE == kStorePlain)
+                            prob.c[row * prob.ldc + col] = y;
+                        else
+                            prob.c[(size_t)p * prob.c_pair_stride + row * prob.ldc + col] = y;
+                    }
+                }
+#pragma unroll
+                for (int nf = 0; nf < 4; ++nf) acc[mf][nf][0] = acc[mf][nf][1] = 0.0;
+            }
         }
     }
+    // group 0 with fewer k-blocks than the kick point still has to release group 1
+    if (grp == 0 && !kicked && worker < num_tiles && wn == 0 && lane == 0) mbar_arrive(start_bar);
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
@@ -334,7 +420,8 @@ cudaError_t launch_typed(const GemmProblem& prob, const PairList& pairs, cudaStr
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          kSmemBytes);
     if (e != cudaSuccess) return e;
-    const int grid = (int)(num_tiles < num_sms ? num_tiles : num_sms);
+    const long ctas = (num_tiles + kGroups - 1) / kGroups;
+    const int grid = (int)(ctas < num_sms ? ctas : num_sms);
     kern<<<grid, kThreads, kSmemBytes, st>>>(maps, pairs, prob, tiles_m, tiles_n_blk);
     return cudaGetLastError();
 }

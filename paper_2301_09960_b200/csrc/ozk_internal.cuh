@@ -57,6 +57,7 @@ struct GemmProblem {
     double* c;          // K-word AoS (kAccumulate) or doubles (other modes)
     size_t ldc;         // elements per row of C
     size_t c_pair_stride;  // kStoreProducts: doubles between consecutive pair products
+    uint32_t zero;         // always 0 (runtime value: carries a register dependency)
 };
 
 cudaError_t launch_pair_gemm(int K, GemmMode mode, const GemmProblem& prob, const PairList& pairs,

@@ -96,9 +96,10 @@ class GpuOps:
         return torch.zeros(shape, dtype=torch.float64, device=self.device)
 
     def split(self, K, mat, rows, cols, ld, d, side, out, pmax):
-        """mat: tensor view whose data_ptr is element (0,0); row stride ld elements."""
+        """mat: tensor view whose data_ptr is element (0,0); row stride ld elements.
+        out: (d, plane_rows, ld_slice) slices; plane_rows may exceed the outer dim."""
         self._check(self.lib.ozk_split_slices_device(
-            K, rows, cols, ld, mat.data_ptr(), d, side, out.data_ptr(),
+            K, rows, cols, ld, mat.data_ptr(), d, side, out.data_ptr(), out.shape[1],
             pmax.data_ptr() if pmax is not None else None, self._stream()))
 
     def gemm(self, plan: ShardPlan, sa, sb_all, pairs, c):

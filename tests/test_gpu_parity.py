@@ -83,7 +83,7 @@ def _slices(ozk, K, mat, d, side):
     t = torch.from_numpy(mat).cuda()
     sl = torch.zeros((d, outer, ld), dtype=torch.float64, device="cuda")
     st = ozk.lib.ozk_split_slices_device(K, rows, cols, cols, t.data_ptr(), d, side,
-                                         sl.data_ptr(), None,
+                                         sl.data_ptr(), outer, None,
                                          torch.cuda.current_stream().cuda_stream)
     assert st == 0, ozk.lib.ozk_last_error()
     return sl
@@ -293,3 +293,17 @@ def test_sharded_layout_single_gpu(ozk, cpu, K, m, l, n, d, world):
         c = ops.zeros((p.rows_local, n, K))
         ops.gemm(p, sa, sb_all, pairs, c)
         assert_bitwise(c.cpu().numpy(), want[p.r0:p.r1], f"rank {p.rank} rows")
+
+
+@pytest.mark.parametrize("K,m,l,n,d", [(2, 256, 256, 256, 6), (3, 256, 256, 256, 9),
+                                       (4, 256, 256, 256, 12), (2, 1000, 900, 1100, 7)])
+def test_repeat_runs_race_free(ozk, cpu, K, m, l, n, d):
+    """Repeated launches must all be bit-exact: catches shared-memory ring races
+    (a stage released before its LDS returned was overwritten by the next TMA
+    load -- found and fixed in gemm.cu; these shapes reproduced it)."""
+    a = cpu.gen_eq1(K, m, l, 11 + m + K)
+    b = cpu.gen_eq1(K, l, n, 12 + m + K)
+    want = cpu.ozaki_gemm(K, a, b, d)
+    for _ in range(3):
+        got, _ = ozk.ozaki_gemm(a, b, d)
+        assert_bitwise(got, want, f"K={K} {m}x{l}x{n} D={d}")
