@@ -544,3 +544,335 @@ void ozk_oracle_replay_elements(int K, size_t m, size_t l, size_t n, const doubl
     }
     if (inexact) *inexact = bad;
 }
+
+/* ======================================================================== *
+ * TS (triple-single): NOT in the reference (MultiFloat<K> is
+ * static_assert-ed to binary64 words, multifloat.hpp:216).  The paper uses a
+ * 3 x binary32 "triple-single" format.  Following SURVEY
+ * §8c, TS is defined here by restating the reference's GENERIC K >= 3
+ * algorithms with binary32 words and S = 24:
+ *   eft.hpp:25-39 (two_sum, fast_two_sum) in float;
+ *   multifloat.hpp:290-300 (K >= 3 branch: merge_components -> sum_ordered),
+ *   :121-150 (vec_sum, extract_components), :450-469 (strict_normalize),
+ *   :246-260 (renormalize) with K = 3 float words;
+ *   ozaki.hpp:36-147 with S = 24 (sigma = (24 + ceil(log2 l) + 1) / 2), a
+ *   float volatile shift, and the "too large to shift" guard at e + sigma > 124
+ *   (the binary64 guard 1020 keeps 3 binades below the 1023 maximum exponent;
+ *   binary32's maximum is 127).
+ * Parity for TS is therefore "unpinned by the reference": it is pinned against
+ * this restatement (GPU bit-exact) and against the exact big-int oracle
+ * (tests/test_ts.py: slices exact, C within the stated ulp bound).
+ * ======================================================================== */
+
+static inline uint32_t fbits_of(float x) {
+    uint32_t u;
+    memcpy(&u, &x, 4);
+    return u;
+}
+
+static inline void two_sum_f(float a, float b, float* s, float* e) {
+    float ss = a + b;
+    float bb = ss - a;
+    *e = (a - (ss - bb)) + (b - bb);
+    *s = ss;
+}
+
+static inline void fast_two_sum_f(float a, float b, float* s, float* e) {
+    float ss = a + b;
+    *e = b - (ss - a);
+    *s = ss;
+}
+
+static void vec_sum_f(float* t, int n) {
+    float s = t[n - 1];
+    for (int i = n - 2; i >= 0; --i) {
+        float hi, lo;
+        two_sum_f(t[i], s, &hi, &lo);
+        s = hi;
+        t[i + 1] = lo;
+    }
+    t[0] = s;
+}
+
+static void extract_components_f(const float* t, int n, float* out) {
+    for (int i = 0; i < 3; ++i) out[i] = 0.0f;
+    float acc = t[0];
+    int j = 0;
+    for (int i = 1; i < n; ++i) {
+        float hi, lo;
+        two_sum_f(acc, t[i], &hi, &lo);
+        if (lo == 0.0f) {
+            acc = hi;
+            continue;
+        }
+        out[j++] = hi;
+        acc = lo;
+        if (j == 3) return;
+    }
+    if (j < 3) out[j] = acc;
+}
+
+static void strict_normalize_f(float* c) {
+    for (int pass = 0; pass < 6; ++pass) {
+        int w = 0;
+        for (int i = 0; i < 3; ++i)
+            if (c[i] != 0.0f) c[w++] = c[i];
+        for (int i = w; i < 3; ++i) c[i] = 0.0f;
+        int changed = 0;
+        for (int i = w - 2; i >= 0; --i) {
+            float s, e;
+            fast_two_sum_f(c[i], c[i + 1], &s, &e);
+            if (s != c[i] || e != c[i + 1]) {
+                c[i] = s;
+                c[i + 1] = e;
+                changed = 1;
+            }
+        }
+        if (!changed) break;
+    }
+    for (int i = 0; i < 3; ++i)
+        if (c[i] == 0.0f) c[i] = 0.0f;
+}
+
+static void from_expansion_f(const float* t, int n, float* c) {
+    extract_components_f(t, n, c);
+    strict_normalize_f(c);
+    if (c[0] == 0.0f || !isfinite(c[0])) {
+        c[0] = c[0] + 0.0f;
+        c[1] = c[2] = 0.0f;
+    }
+}
+
+static void sum_ordered_f(const float* t, int n, float* c) {
+    float probe = 0.0f;
+    for (int i = 0; i < n; ++i) probe += t[i];
+    if (!isfinite(probe)) {
+        c[0] = probe;
+        c[1] = c[2] = 0.0f;
+        return;
+    }
+    float buf[16];
+    int m = 0;
+    for (int i = 0; i < n; ++i)
+        if (t[i] != 0.0f) buf[m++] = t[i];
+    if (m == 0) {
+        c[0] = c[1] = c[2] = 0.0f;
+        return;
+    }
+    vec_sum_f(buf, m);
+    from_expansion_f(buf, m, c);
+}
+
+static int before_f(float x, float y) {
+    float ax = fabsf(x), ay = fabsf(y);
+    if (ax != ay) return ax > ay;
+    return fbits_of(x) <= fbits_of(y);
+}
+
+/* TS + float: the K >= 3 branch of multifloat.hpp:290-300 with float words. */
+void ozk_oracle_ts_add_float(const float* x, float y, float* r) {
+    float m[4];
+    int i = 0, k = 0, placed = 0;
+    while (i < 3 && !placed) {
+        if (before_f(x[i], y))
+            m[k++] = x[i++];
+        else {
+            m[k++] = y;
+            placed = 1;
+        }
+    }
+    while (i < 3) m[k++] = x[i++];
+    if (!placed) m[k++] = y;
+    sum_ordered_f(m, 4, r);
+}
+
+static void renormalize_f(const float* terms, int nterms, float* c) {
+    float buf[16] = {0};
+    int n = 0;
+    float probe = 0.0f;
+    for (int i = 0; i < nterms; ++i) {
+        probe += terms[i];
+        if (terms[i] != 0.0f) buf[n++] = terms[i];
+    }
+    if (!isfinite(probe)) {
+        c[0] = probe;
+        c[1] = c[2] = 0.0f;
+        return;
+    }
+    if (n == 0) {
+        c[0] = c[1] = c[2] = 0.0f;
+        return;
+    }
+    vec_sum_f(buf, n);
+    if (n > 1) vec_sum_f(buf, n);
+    from_expansion_f(buf, n, c);
+}
+
+/* TS inputs: Eq. (1) TD values (gen_matrix_eq1<3>, gen.hpp:20-34) rounded to
+ * three binary32 words by successive leading-word extraction in binary64,
+ * then renormalised in TS (renormalize, multifloat.hpp:246-260). */
+void ozk_oracle_gen_eq1_ts(size_t m, size_t n, uint64_t seed, float* out) {
+    double* td = (double*)malloc(m * n * 3 * sizeof(double));
+    ozk_oracle_gen_eq1(3, m, n, seed, td);
+    for (size_t e = 0; e < m * n; ++e) {
+        const double* c = td + 3 * e;
+        float w[3];
+        double r0 = c[0];
+        w[0] = (float)r0;
+        double r1 = (r0 - (double)w[0]) + c[1];
+        w[1] = (float)r1;
+        double r2 = ((r1 - (double)w[1]) + c[2]);
+        w[2] = (float)r2;
+        renormalize_f(w, 3, out + 3 * e);
+    }
+    free(td);
+}
+
+int ozk_oracle_exponent_ceil_log2_f(float x) {
+    int e = ilogbf(x);
+    return scalbnf(1.0f, e) == x ? e : e + 1;
+}
+
+static float shift_extract_f(float v, float tau) {
+    volatile float shifted = v + tau;
+    return shifted - tau;
+}
+
+/* TS split: ozaki.hpp:74-147 with S = 24 (see block comment above). */
+int ozk_oracle_split_ts(size_t rows, size_t cols, const float* mat, int d, int side,
+                        float* pieces, float* residual) {
+    if (d < 1) return 2;
+    const size_t N = rows * cols;
+    for (size_t i = 0; i < N; ++i)
+        if (!isfinite(mat[i * 3])) return 2;
+    const size_t inner = side == 0 ? cols : rows;
+    const size_t outer = side == 0 ? rows : cols;
+    const int sigma = ozk_oracle_split_shift_bits(inner, 24);
+    memcpy(residual, mat, N * 3 * sizeof(float));
+    if (d == 1) {
+        for (size_t i = 0; i < N; ++i) {
+            float lead = residual[i * 3];
+            pieces[i] = lead;
+            float r[3];
+            ozk_oracle_ts_add_float(residual + i * 3, -lead, r);
+            memcpy(residual + i * 3, r, sizeof r);
+        }
+        return 0;
+    }
+    float* mu = (float*)malloc(outer * sizeof(float));
+    float* tau = (float*)malloc(outer * sizeof(float));
+    int status = 0;
+    for (int alpha = 0; alpha < d && status == 0; ++alpha) {
+        float* piece = pieces + (size_t)alpha * N;
+        for (size_t o = 0; o < outer; ++o) mu[o] = 0.0f;
+        for (size_t i = 0; i < rows; ++i)
+            for (size_t j = 0; j < cols; ++j) {
+                size_t o = side == 0 ? i : j;
+                mu[o] = fmaxf(mu[o], fabsf(residual[(i * cols + j) * 3]));
+            }
+        for (size_t o = 0; o < outer; ++o) {
+            tau[o] = 0.0f;
+            if (mu[o] == 0.0f) continue;
+            int e = ozk_oracle_exponent_ceil_log2_f(mu[o]);
+            if (e + sigma > 124) {
+                status = 2;
+                break;
+            }
+            tau[o] = scalbnf(1.0f, e + sigma);
+        }
+        if (status) break;
+        for (size_t i = 0; i < rows; ++i)
+            for (size_t j = 0; j < cols; ++j) {
+                size_t o = side == 0 ? i : j;
+                size_t e = i * cols + j;
+                if (tau[o] == 0.0f) {
+                    piece[e] = 0.0f;
+                    continue;
+                }
+                float x = shift_extract_f(residual[e * 3], tau[o]);
+                piece[e] = x;
+                if (x != 0.0f) {
+                    float r[3];
+                    ozk_oracle_ts_add_float(residual + e * 3, -x, r);
+                    memcpy(residual + e * 3, r, sizeof r);
+                }
+            }
+    }
+    free(mu);
+    free(tau);
+    return status;
+}
+
+/* binary32 slice product with an exactness witness (TwoProd via fmaf, TwoSum). */
+long ozk_oracle_exact_sgemm(size_t m, size_t l, size_t n, const float* A, const float* B,
+                            float* C) {
+    long inexact = 0;
+    for (size_t i = 0; i < m; ++i)
+        for (size_t j = 0; j < n; ++j) {
+            float s = 0.0f;
+            int bad = 0;
+            for (size_t k = 0; k < l; ++k) {
+                float a = A[i * l + k], b = B[k * n + j];
+                float p = a * b;
+                if (fmaf(a, b, -p) != 0.0f) bad = 1;
+                float hi, lo;
+                two_sum_f(s, p, &hi, &lo);
+                if (lo != 0.0f) bad = 1;
+                s = hi;
+            }
+            C[i * n + j] = s;
+            inexact += bad;
+        }
+    return inexact;
+}
+
+/* TS Ozaki GEMM: ozaki.hpp:180-249 over the TS split and binary32 products. */
+int ozk_oracle_ozaki_gemm_ts(size_t m, size_t l, size_t n, const float* A, const float* B, int d,
+                             double drop, float* C, int* npairs_out, long* inexact_out) {
+    if (d < 1 || drop < 0.0) return 2;
+    const size_t NA = m * l, NB = l * n, NC = m * n;
+    float* pa = (float*)malloc((size_t)d * NA * sizeof(float));
+    float* pb = (float*)malloc((size_t)d * NB * sizeof(float));
+    float* ra = (float*)malloc(NA * 3 * sizeof(float));
+    float* rb = (float*)malloc(NB * 3 * sizeof(float));
+    float* prod = (float*)malloc(NC * sizeof(float));
+    int* pairs = (int*)malloc(sizeof(int) * 2 * (size_t)d * (size_t)d);
+    double* amax = (double*)malloc(sizeof(double) * (size_t)d);
+    double* bmax = (double*)malloc(sizeof(double) * (size_t)d);
+    int st = 0;
+    if (!pa || !pb || !ra || !rb || !prod || !pairs || !amax || !bmax) st = 5;
+    if (!st) st = ozk_oracle_split_ts(m, l, A, d, 0, pa, ra);
+    if (!st) st = ozk_oracle_split_ts(l, n, B, d, 1, pb, rb);
+    if (!st) {
+        for (int i = 0; i < d; ++i) {
+            float ma = 0.0f, mb = 0.0f;
+            for (size_t e = 0; e < NA; ++e) ma = fmaxf(ma, fabsf(pa[(size_t)i * NA + e]));
+            for (size_t e = 0; e < NB; ++e) mb = fmaxf(mb, fabsf(pb[(size_t)i * NB + e]));
+            amax[i] = ma;
+            bmax[i] = mb;
+        }
+        int np = ozk_oracle_pair_list(d, amax, bmax, drop, pairs);
+        if (npairs_out) *npairs_out = np;
+        for (size_t e = 0; e < NC * 3; ++e) C[e] = 0.0f;
+        long inexact = 0;
+        for (int p = 0; p < np; ++p) {
+            inexact += ozk_oracle_exact_sgemm(m, l, n, pa + (size_t)pairs[2 * p] * NA,
+                                              pb + (size_t)pairs[2 * p + 1] * NB, prod);
+            for (size_t e = 0; e < NC; ++e) {
+                float r[3];
+                ozk_oracle_ts_add_float(C + e * 3, prod[e], r);
+                memcpy(C + e * 3, r, sizeof r);
+            }
+        }
+        if (inexact_out) *inexact_out = inexact;
+    }
+    free(pa);
+    free(pb);
+    free(ra);
+    free(rb);
+    free(prod);
+    free(pairs);
+    free(amax);
+    free(bmax);
+    return st;
+}

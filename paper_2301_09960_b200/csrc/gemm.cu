@@ -158,7 +158,10 @@ __device__ __forceinline__ bool mbar_test(uint32_t bar, uint32_t parity) {
     return ok != 0;
 }
 
-template <int K, int MODE>
+// W: word type of the K-word C in kAccumulate mode (double: DD/TD/QD, float:
+// TS -- an exact binary64 slice product of binary32 slices is exactly
+// representable in binary32, so the cast before the TS epilogue is exact).
+template <int K, int MODE, typename W>
 __global__ void __launch_bounds__(kThreads, 1)
 pair_gemm_kernel(const __grid_constant__ TmaMaps maps, const __grid_constant__ PairList pairs,
                  GemmProblem prob, int tiles_m, int tiles_n_blk) {
@@ -316,7 +319,8 @@ pair_gemm_kernel(const __grid_constant__ TmaMaps maps, const __grid_constant__ P
                             for (int nf = 0; nf < 4; ++nf)
                                 if ((rmask >> mf) & (cmask >> (2 * nf)) & 1u)
                                     asm volatile("prefetch.global.L2 [%0];" ::"l"(
-                                        prob.c + ((row0 + mf * 8) * prob.ldc + col0 + nf * 8) * K));
+                                        static_cast<W*>(prob.c) +
+                                        ((row0 + mf * 8) * prob.ldc + col0 + nf * 8) * K));
                     }
                 }
             }
@@ -327,17 +331,17 @@ pair_gemm_kernel(const __grid_constant__ TmaMaps maps, const __grid_constant__ P
                 const size_t row = row0 + mf * 8;
                 if constexpr (MODE == kAccumulate) {
                     // batch: load the 8 K-word elements of this row first
-                    double w[8][K];
-                    double* cp = prob.c + (row * prob.ldc + col0) * K;
+                    W w[8][K];
+                    W* cp = static_cast<W*>(prob.c) + (row * prob.ldc + col0) * K;
 #pragma unroll
                     for (int q = 0; q < 8; ++q) {
                         const bool ok = (rmask >> mf) & (cmask >> q) & 1u;
                         const int off = ((q >> 1) * 8 + (q & 1)) * K;
 #pragma unroll
-                        for (int k = 0; k < K; ++k) w[q][k] = (ok && p > 0) ? cp[off + k] : 0.0;
+                        for (int k = 0; k < K; ++k) w[q][k] = (ok && p > 0) ? cp[off + k] : W(0);
                     }
 #pragma unroll
-                    for (int q = 0; q < 8; ++q) kw_add<K>(w[q], acc[mf][q >> 1][q & 1]);
+                    for (int q = 0; q < 8; ++q) kw_add<K>(w[q], (W)acc[mf][q >> 1][q & 1]);
 #pragma unroll
                     for (int q = 0; q < 8; ++q) {
                         const bool ok = (rmask >> mf) & (cmask >> q) & 1u;
@@ -353,10 +357,11 @@ pair_gemm_kernel(const __grid_constant__ TmaMaps maps, const __grid_constant__ P
                         if (!((rmask >> mf) & (cmask >> q) & 1u)) continue;
                         const size_t col = col0 + (q >> 1) * 8 + (q & 1);
                         const double y = acc[mf][q >> 1][q & 1];
+                        double* cd = static_cast<double*>(prob.c);
                         if constexpr (MODE == kStorePlain)
-                            prob.c[row * prob.ldc + col] = y;
+                            cd[row * prob.ldc + col] = y;
                         else
-                            prob.c[(size_t)p * prob.c_pair_stride + row * prob.ldc + col] = y;
+                            cd[(size_t)p * prob.c_pair_stride + row * prob.ldc + col] = y;
                     }
                 }
 #pragma unroll
@@ -381,7 +386,7 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
     return fn;
 }
 
-template <int K, int MODE>
+template <int K, int MODE, typename W = double>
 cudaError_t launch_typed(const GemmProblem& prob, const PairList& pairs, cudaStream_t st,
                          int num_sms) {
     auto encode = get_encode();
@@ -416,7 +421,7 @@ cudaError_t launch_typed(const GemmProblem& prob, const PairList& pairs, cudaStr
     const int tiles_n_blk = (prob.ncb + BN - 1) / BN;
     const long num_tiles = (long)tiles_m * tiles_n_blk * prob.nblk;
     if (num_tiles == 0 || pairs.count == 0) return cudaSuccess;
-    auto kern = pair_gemm_kernel<K, MODE>;
+    auto kern = pair_gemm_kernel<K, MODE, W>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          kSmemBytes);
     if (e != cudaSuccess) return e;
@@ -429,8 +434,12 @@ cudaError_t launch_typed(const GemmProblem& prob, const PairList& pairs, cudaStr
 } // namespace
 
 cudaError_t launch_pair_gemm(int K, GemmMode mode, const GemmProblem& prob, const PairList& pairs,
-                             cudaStream_t st, int num_sms) {
+                             cudaStream_t st, int num_sms, int word_bytes) {
     if (mode == kStorePlain) return launch_typed<1, kStorePlain>(prob, pairs, st, num_sms);
+    if (mode == kAccumulate && word_bytes == 4) {
+        if (K != 3) return cudaErrorInvalidValue;
+        return launch_typed<3, kAccumulate, float>(prob, pairs, st, num_sms);
+    }
     if (mode == kStoreProducts) return launch_typed<1, kStoreProducts>(prob, pairs, st, num_sms);
     switch (K) {
     case 2: return launch_typed<2, kAccumulate>(prob, pairs, st, num_sms);

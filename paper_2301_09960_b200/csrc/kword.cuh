@@ -36,17 +36,40 @@
 #define OZK_HD inline
 #endif
 
-#if defined(__CUDA_ARCH__)
-#define OZK_DADD(a, b) __dadd_rn((a), (b))
-#define OZK_DSUB(a, b) __dsub_rn((a), (b))
-#else
-#define OZK_DADD(a, b) ((a) + (b))
-#define OZK_DSUB(a, b) ((a) - (b))
-#endif
-
 namespace ozk {
 
-OZK_HD uint64_t dbits(double x) {
+// ---- scalar primitives, overloaded for binary64 (DD/TD/QD) and binary32 (TS) ----
+
+OZK_HD double rn_add(double a, double b) {
+#if defined(__CUDA_ARCH__)
+    return __dadd_rn(a, b);
+#else
+    return a + b;
+#endif
+}
+OZK_HD double rn_sub(double a, double b) {
+#if defined(__CUDA_ARCH__)
+    return __dsub_rn(a, b);
+#else
+    return a - b;
+#endif
+}
+OZK_HD float rn_add(float a, float b) {
+#if defined(__CUDA_ARCH__)
+    return __fadd_rn(a, b);
+#else
+    return a + b;
+#endif
+}
+OZK_HD float rn_sub(float a, float b) {
+#if defined(__CUDA_ARCH__)
+    return __fsub_rn(a, b);
+#else
+    return a - b;
+#endif
+}
+
+OZK_HD uint64_t fbits(double x) {
 #if defined(__CUDA_ARCH__)
     return static_cast<uint64_t>(__double_as_longlong(x));
 #else
@@ -58,52 +81,79 @@ OZK_HD uint64_t dbits(double x) {
     return v.u;
 #endif
 }
+OZK_HD uint32_t fbits(float x) {
+#if defined(__CUDA_ARCH__)
+    return static_cast<uint32_t>(__float_as_uint(x));
+#else
+    union {
+        float f;
+        uint32_t u;
+    } v;
+    v.f = x;
+    return v.u;
+#endif
+}
+// kept for the split/gemm call sites
+OZK_HD uint64_t dbits(double x) { return fbits(x); }
 
-OZK_HD double dabs(double x) {
+OZK_HD double fabs_(double x) {
 #if defined(__CUDA_ARCH__)
     return fabs(x);
 #else
     return x < 0 ? -x : (x == 0 ? 0.0 : x);
 #endif
 }
-
-OZK_HD bool dfinite(double x) {
-    // exponent field not all ones
-    return (dbits(x) & 0x7ff0000000000000ull) != 0x7ff0000000000000ull;
+OZK_HD float fabs_(float x) {
+#if defined(__CUDA_ARCH__)
+    return fabsf(x);
+#else
+    return x < 0 ? -x : (x == 0 ? 0.0f : x);
+#endif
 }
+OZK_HD double dabs(double x) { return fabs_(x); }
+
+// exponent field not all ones
+OZK_HD bool is_finite(double x) {
+    return (fbits(x) & 0x7ff0000000000000ull) != 0x7ff0000000000000ull;
+}
+OZK_HD bool is_finite(float x) { return (fbits(x) & 0x7f800000u) != 0x7f800000u; }
+OZK_HD bool dfinite(double x) { return is_finite(x); }
 
 // eft.hpp:25-30
-OZK_HD void two_sum(double a, double b, double& s, double& e) {
-    double ss = OZK_DADD(a, b);
-    double bb = OZK_DSUB(ss, a);
-    e = OZK_DADD(OZK_DSUB(a, OZK_DSUB(ss, bb)), OZK_DSUB(b, bb));
+template <typename T>
+OZK_HD void two_sum(T a, T b, T& s, T& e) {
+    T ss = rn_add(a, b);
+    T bb = rn_sub(ss, a);
+    e = rn_add(rn_sub(a, rn_sub(ss, bb)), rn_sub(b, bb));
     s = ss;
 }
 
 // eft.hpp:35-39
-OZK_HD void fast_two_sum(double a, double b, double& s, double& e) {
-    double ss = OZK_DADD(a, b);
-    e = OZK_DSUB(b, OZK_DSUB(ss, a));
+template <typename T>
+OZK_HD void fast_two_sum(T a, T b, T& s, T& e) {
+    T ss = rn_add(a, b);
+    e = rn_sub(b, rn_sub(ss, a));
     s = ss;
 }
 
 // multifloat.hpp:509-512 (merge order predicate)
-OZK_HD bool merge_before(double x, double y) {
-    double ax = dabs(x), ay = dabs(y);
+template <typename T>
+OZK_HD bool merge_before(T x, T y) {
+    T ax = fabs_(x), ay = fabs_(y);
     if (ax != ay) return ax > ay;
-    return dbits(x) <= dbits(y);
+    return fbits(x) <= fbits(y);
 }
 
-template <int K>
-OZK_HD void non_finite(double head, double* c) {
+template <int K, typename T>
+OZK_HD void non_finite(T head, T* c) {
     c[0] = head;
 #pragma unroll
-    for (int i = 1; i < K; ++i) c[i] = 0.0;
+    for (int i = 1; i < K; ++i) c[i] = T(0);
 }
 
 // multifloat.hpp:450-469
-template <int K>
-OZK_HD void strict_normalize(double* c) {
+template <int K, typename T>
+OZK_HD void strict_normalize(T* c) {
 #pragma unroll
     for (int pass = 0; pass < 2 * K; ++pass) {
         // stable compaction of zeros to the tail (bubble, static indices)
@@ -111,19 +161,19 @@ OZK_HD void strict_normalize(double* c) {
         for (int r = 0; r < K - 1; ++r) {
 #pragma unroll
             for (int i = 0; i < K - 1; ++i) {
-                bool z = c[i] == 0.0;
-                double lo = c[i + 1];
-                c[i + 1] = z ? 0.0 : c[i + 1];
+                bool z = c[i] == T(0);
+                T lo = c[i + 1];
+                c[i + 1] = z ? T(0) : c[i + 1];
                 c[i] = z ? lo : c[i];
             }
         }
-        // trailing zeros written by the reference's compaction are +0.0
+        // trailing zeros written by the reference's compaction are +0
 #pragma unroll
-        for (int i = 0; i < K; ++i) c[i] = (c[i] == 0.0) ? 0.0 : c[i];
+        for (int i = 0; i < K; ++i) c[i] = (c[i] == T(0)) ? T(0) : c[i];
         bool changed = false;
 #pragma unroll
         for (int i = K - 2; i >= 0; --i) {
-            double s, e;
+            T s, e;
             fast_two_sum(c[i], c[i + 1], s, e);
             bool ch = (s != c[i]) || (e != c[i + 1]);
             c[i] = ch ? s : c[i];
@@ -133,22 +183,22 @@ OZK_HD void strict_normalize(double* c) {
         if (!changed) break;
     }
 #pragma unroll
-    for (int i = 0; i < K; ++i) c[i] = (c[i] == 0.0) ? 0.0 : c[i];
+    for (int i = 0; i < K; ++i) c[i] = (c[i] == T(0)) ? T(0) : c[i];
 }
 
 // multifloat.hpp:133-150 over N terms (zero terms are transparent)
-template <int K, int N>
-OZK_HD void extract_components(const double* t, double* out) {
+template <int K, int N, typename T>
+OZK_HD void extract_components(const T* t, T* out) {
 #pragma unroll
-    for (int q = 0; q < K; ++q) out[q] = 0.0;
-    double acc = t[0];
+    for (int q = 0; q < K; ++q) out[q] = T(0);
+    T acc = t[0];
     int j = 0;
 #pragma unroll
     for (int i = 1; i < N; ++i) {
         if (j < K) {
-            double hi, lo;
+            T hi, lo;
             two_sum(acc, t[i], hi, lo);
-            if (lo == 0.0) {
+            if (lo == T(0)) {
                 acc = hi;
             } else {
 #pragma unroll
@@ -162,51 +212,53 @@ OZK_HD void extract_components(const double* t, double* out) {
     for (int q = 0; q < K; ++q) out[q] = (j == q) ? acc : out[q];
 }
 
-// MultiFloat<K> + double (multifloat.hpp:290-300); x is updated in place.
-template <int K>
-OZK_HD void kw_add(double* x, double y) {
+// MultiFloat<K> + word (multifloat.hpp:290-300); x is updated in place.  T is
+// the word type: double for DD/TD/QD, float for TS (which uses the generic
+// K >= 3 branch with binary32 words, see oracle/ozk_oracle.c).
+template <int K, typename T = double>
+OZK_HD void kw_add(T* x, T y) {
     if constexpr (K == 2) {
-        double s, e;
+        T s, e;
         two_sum(x[0], y, s, e);
-        double v = OZK_DADD(x[1], e);
-        double fs, fe;
+        T v = rn_add(x[1], e);
+        T fs, fe;
         fast_two_sum(s, v, fs, fe);
         // from_pair (multifloat.hpp:471-479)
-        if (!dfinite(fs)) {
+        if (!is_finite(fs)) {
             x[0] = fs;
-            x[1] = 0.0;
+            x[1] = T(0);
             return;
         }
-        double ps, pe;
+        T ps, pe;
         fast_two_sum(fs, fe, ps, pe);
-        x[0] = ps == 0.0 ? 0.0 : ps;
-        x[1] = (pe == 0.0 || ps == 0.0) ? 0.0 : pe;
+        x[0] = ps == T(0) ? T(0) : ps;
+        x[1] = (pe == T(0) || ps == T(0)) ? T(0) : pe;
     } else {
         // merge_components(x, K, &y, 1): y goes before the first x[i] that
         // does not precede it
-        double m[K + 1];
+        T m[K + 1];
         bool placed = false;
 #pragma unroll
         for (int i = 0; i <= K; ++i) {
             bool take_x = !placed && i < K && merge_before(x[i < K ? i : 0], y);
-            double prev = x[i > 0 ? i - 1 : 0];
-            double cur = x[i < K ? i : K - 1];
+            T prev = x[i > 0 ? i - 1 : 0];
+            T cur = x[i < K ? i : K - 1];
             m[i] = placed ? prev : (take_x ? cur : y);
             placed = placed || !take_x;
         }
         // sum_ordered: finiteness probe over all terms
-        double probe = 0.0;
+        T probe = T(0);
 #pragma unroll
-        for (int i = 0; i <= K; ++i) probe = OZK_DADD(probe, m[i]);
-        if (!dfinite(probe)) {
+        for (int i = 0; i <= K; ++i) probe = rn_add(probe, m[i]);
+        if (!is_finite(probe)) {
             non_finite<K>(probe, x);
             return;
         }
         // vec_sum over all K+1 terms (zeros transparent, see header)
-        double s = m[K];
+        T s = m[K];
 #pragma unroll
         for (int i = K - 1; i >= 0; --i) {
-            double hi, lo;
+            T hi, lo;
             two_sum(m[i], s, hi, lo);
             s = hi;
             m[i + 1] = lo;
@@ -215,7 +267,7 @@ OZK_HD void kw_add(double* x, double y) {
         // from_expansion
         extract_components<K, K + 1>(m, x);
         strict_normalize<K>(x);
-        if (x[0] == 0.0 || !dfinite(x[0])) non_finite<K>(OZK_DADD(x[0], 0.0), x);
+        if (x[0] == T(0) || !is_finite(x[0])) non_finite<K>(rn_add(x[0], T(0)), x);
     }
 }
 

@@ -23,15 +23,16 @@ inline size_t slice_ld(size_t inner) { return (inner + 1) & ~size_t(1); }
 //   pieces  : d slices, slice a row r at pieces + a*slice_stride + r*ldk
 //   piece_max (optional): d values, max |piece_a| as ordered uint64 bits
 //   err     : device flag (DevErr)
-cudaError_t launch_split_rows(int K, const double* in, size_t in_ld, double* work, size_t rows,
-                              size_t cols, int d, int sigma, double* pieces, size_t ldk,
-                              size_t slice_stride, unsigned long long* piece_max, int* err,
-                              cudaStream_t st);
+// word_bytes = 8 for DD/TD/QD (binary64 words), 4 for TS (binary32 words, K = 3).
+cudaError_t launch_split_rows(int K, int word_bytes, const void* in, size_t in_ld, void* work,
+                              size_t rows, size_t cols, int d, int sigma, double* pieces,
+                              size_t ldk, size_t slice_stride, unsigned long long* piece_max,
+                              int* err, cudaStream_t st);
 
 // Transpose of a K-word matrix: out(j, i) = in(i, j).  in is rows x cols with
 // row stride in_ld elements; out is cols x rows with row stride out_ld elements.
-cudaError_t launch_transpose(int K, const double* in, size_t in_ld, double* out, size_t out_ld,
-                             size_t rows, size_t cols, cudaStream_t st);
+cudaError_t launch_transpose(int K, int word_bytes, const void* in, size_t in_ld, void* out,
+                             size_t out_ld, size_t rows, size_t cols, cudaStream_t st);
 
 // Slice-pair GEMM with fused epilogue (K2 + K3).
 enum GemmMode : int { kStorePlain = 0, kAccumulate = 1, kStoreProducts = 2 };
@@ -54,14 +55,14 @@ struct GemmProblem {
     int b_slices;
     int ncb, nblk;
     size_t m, n, l;
-    double* c;          // K-word AoS (kAccumulate) or doubles (other modes)
+    void* c;            // K-word AoS of word_bytes words (kAccumulate) or doubles
     size_t ldc;         // elements per row of C
     size_t c_pair_stride;  // kStoreProducts: doubles between consecutive pair products
     uint32_t zero;         // always 0 (runtime value: carries a register dependency)
 };
 
 cudaError_t launch_pair_gemm(int K, GemmMode mode, const GemmProblem& prob, const PairList& pairs,
-                             cudaStream_t st, int num_sms);
+                             cudaStream_t st, int num_sms, int word_bytes = 8);
 
 // Device Eq. (1)-distributed K-word generator (synthetic bench inputs).
 cudaError_t launch_gen_eq1(int K, double* out, size_t count, uint64_t seed, cudaStream_t st);

@@ -27,6 +27,18 @@ __device__ __forceinline__ int ceil_log2(double x) {
     int e = ilogb(x);
     return scalbn(1.0, e) == x ? e : e + 1;
 }
+__device__ __forceinline__ int ceil_log2(float x) {
+    int e = ilogbf(x);
+    return scalbnf(1.0f, e) == x ? e : e + 1;
+}
+__device__ __forceinline__ double pow2(double, int e) { return scalbn(1.0, e); }
+__device__ __forceinline__ float pow2(float, int e) { return scalbnf(1.0f, e); }
+
+// "entries too large to shift" guard: ozaki.hpp:109 keeps e + sigma <= 1020
+// (3 binades below binary64's 1023); TS keeps the same margin below 127.
+template <typename T> struct ShiftGuard;
+template <> struct ShiftGuard<double> { static constexpr int max_exp = 1020; };
+template <> struct ShiftGuard<float> { static constexpr int max_exp = 124; };
 
 // Block-wide max of a non-negative double; every thread gets the result.
 __device__ __forceinline__ double block_max(double v, double* red) {
@@ -47,13 +59,13 @@ __device__ __forceinline__ double block_max(double v, double* red) {
     return v;
 }
 
-template <int K>
-__device__ __forceinline__ void load_kw(const double* p, double* c) {
-    if constexpr (K == 2) {
+template <int K, typename T>
+__device__ __forceinline__ void load_kw(const T* p, T* c) {
+    if constexpr (K == 2 && sizeof(T) == 8) {
         double2 v = *reinterpret_cast<const double2*>(p);
         c[0] = v.x;
         c[1] = v.y;
-    } else if constexpr (K == 4) {
+    } else if constexpr (K == 4 && sizeof(T) == 8) {
         double2 v0 = reinterpret_cast<const double2*>(p)[0];
         double2 v1 = reinterpret_cast<const double2*>(p)[1];
         c[0] = v0.x;
@@ -66,11 +78,11 @@ __device__ __forceinline__ void load_kw(const double* p, double* c) {
     }
 }
 
-template <int K>
-__device__ __forceinline__ void store_kw(double* p, const double* c) {
-    if constexpr (K == 2) {
+template <int K, typename T>
+__device__ __forceinline__ void store_kw(T* p, const T* c) {
+    if constexpr (K == 2 && sizeof(T) == 8) {
         *reinterpret_cast<double2*>(p) = make_double2(c[0], c[1]);
-    } else if constexpr (K == 4) {
+    } else if constexpr (K == 4 && sizeof(T) == 8) {
         reinterpret_cast<double2*>(p)[0] = make_double2(c[0], c[1]);
         reinterpret_cast<double2*>(p)[1] = make_double2(c[2], c[3]);
     } else {
@@ -79,47 +91,50 @@ __device__ __forceinline__ void store_kw(double* p, const double* c) {
     }
 }
 
-template <int K>
+// T is the word type of the K-word input/residual (double: DD/TD/QD, float:
+// TS); slices are always written as binary64 (a TS slice is a binary32 value,
+// exactly representable), which is the DMMA GEMM's operand type.
+template <int K, typename T>
 __global__ void __launch_bounds__(kSplitThreads)
-split_rows_kernel(const double* __restrict__ in, size_t in_ld, double* __restrict__ work,
-                  size_t cols, int d, int sigma, double* __restrict__ pieces, size_t ldk,
+split_rows_kernel(const T* __restrict__ in, size_t in_ld, T* __restrict__ work, size_t cols,
+                  int d, int sigma, double* __restrict__ pieces, size_t ldk,
                   size_t slice_stride, unsigned long long* __restrict__ piece_max,
                   int* __restrict__ err) {
     __shared__ double red[33];
     const size_t r = blockIdx.x;
-    const double* src = in + r * in_ld * K;
-    double* w = work + r * cols * K;
+    const T* src = in + r * in_ld * K;
+    T* w = work + r * cols * K;
     double* prow = pieces + r * ldk;
 
     // Sweep 0: leading image max, finiteness scan (ozaki.hpp:77-78), and the
     // copy of the input row into the working residual.
-    double mx = 0.0;
+    T mx = T(0);
     int bad = 0;
     for (size_t j = threadIdx.x; j < cols; j += kSplitThreads) {
-        double c[K];
+        T c[K];
         load_kw<K>(src + j * K, c);
-        bad |= !dfinite(c[0]);
-        mx = fmax(mx, fabs(c[0]));
+        bad |= !is_finite(c[0]);
+        mx = fmax(mx, fabs_(c[0]));
         if (src != w) store_kw<K>(w + j * K, c);
     }
     if (__syncthreads_or(bad)) {
         if (threadIdx.x == 0) atomicMax(err, (int)kDevNonFinite);
         return;
     }
-    mx = block_max(mx, red);
+    mx = (T)block_max((double)mx, red);
 
     if (d == 1) {
         // D = 1: the piece is the leading image, the residual keeps the tail
         // (ozaki.hpp:90-96: every element, zero or not, gets residual -= lead).
         double pmx = 0.0;
         for (size_t j = threadIdx.x; j < cols; j += kSplitThreads) {
-            double c[K];
+            T c[K];
             load_kw<K>(w + j * K, c);
-            const double lead = c[0];
-            prow[j] = lead;
+            const T lead = c[0];
+            prow[j] = (double)lead;
             kw_add<K>(c, -lead);
             store_kw<K>(w + j * K, c);
-            pmx = fmax(pmx, fabs(lead));
+            pmx = fmax(pmx, (double)fabs_(lead));
         }
         for (size_t j = cols + threadIdx.x; j < ldk; j += kSplitThreads) prow[j] = 0.0;
         if (piece_max) {
@@ -132,32 +147,33 @@ split_rows_kernel(const double* __restrict__ in, size_t in_ld, double* __restric
 
     for (int a = 0; a < d; ++a) {
         double* pa = prow + (size_t)a * slice_stride;
-        double tau = 0.0;  // zero marks a skipped (all-zero) row, ozaki.hpp:105-107
-        if (mx != 0.0) {
+        T tau = T(0);  // zero marks a skipped (all-zero) row, ozaki.hpp:105-107
+        if (mx != T(0)) {
             const int e = ceil_log2(mx);
-            if (e + sigma > 1020) {  // ozaki.hpp:109 (mx is block-uniform)
+            if (e + sigma > ShiftGuard<T>::max_exp) {  // ozaki.hpp:109 (mx is block-uniform)
                 if (threadIdx.x == 0) atomicMax(err, (int)kDevTooLarge);
                 return;
             }
-            tau = scalbn(1.0, e + sigma);
+            tau = pow2(T(0), e + sigma);
         }
-        double nmx = 0.0, pmx = 0.0;
+        T nmx = T(0);
+        double pmx = 0.0;
         for (size_t j = threadIdx.x; j < cols; j += kSplitThreads) {
-            if (tau == 0.0) {
+            if (tau == T(0)) {
                 pa[j] = 0.0;
                 continue;
             }
-            double c[K];
+            T c[K];
             load_kw<K>(w + j * K, c);
             // shift_extract: (v + tau) - tau, strictly rounded (ozaki.hpp:53-56)
-            const double x = __dsub_rn(__dadd_rn(c[0], tau), tau);
-            pa[j] = x;
-            if (x != 0.0) {
+            const T x = rn_sub(rn_add(c[0], tau), tau);
+            pa[j] = (double)x;
+            if (x != T(0)) {
                 kw_add<K>(c, -x);  // w -= x  ==  w + (-x)  (multifloat.hpp:302,391)
                 store_kw<K>(w + j * K, c);
             }
-            nmx = fmax(nmx, fabs(c[0]));
-            pmx = fmax(pmx, fabs(x));
+            nmx = fmax(nmx, fabs_(c[0]));
+            pmx = fmax(pmx, (double)fabs_(x));
         }
         for (size_t j = cols + threadIdx.x; j < ldk; j += kSplitThreads) pa[j] = 0.0;
         if (piece_max) {
@@ -166,20 +182,19 @@ split_rows_kernel(const double* __restrict__ in, size_t in_ld, double* __restric
                 atomicMax(piece_max + a,
                           static_cast<unsigned long long>(__double_as_longlong(pmx)));
         }
-        mx = block_max(nmx, red);
+        mx = (T)block_max((double)nmx, red);
     }
 }
 
-template <int K>
-__global__ void transpose_kernel(const double* __restrict__ in, size_t in_ld,
-                                 double* __restrict__ out, size_t out_ld, size_t rows,
-                                 size_t cols) {
-    __shared__ double tile[32][32 * K + 1];
+template <int K, typename T>
+__global__ void transpose_kernel(const T* __restrict__ in, size_t in_ld, T* __restrict__ out,
+                                 size_t out_ld, size_t rows, size_t cols) {
+    __shared__ T tile[32][32 * K + 1];
     const size_t c0 = (size_t)blockIdx.x * 32, r0 = (size_t)blockIdx.y * 32;
     for (int yy = threadIdx.y; yy < 32; yy += 8) {
         const size_t i = r0 + yy;
         if (i >= rows) break;
-        const double* src = in + (i * in_ld + c0) * K;
+        const T* src = in + (i * in_ld + c0) * K;
         for (int q = threadIdx.x; q < 32 * K; q += 32)
             if (c0 + q / K < cols) tile[yy][q] = src[q];
     }
@@ -187,7 +202,7 @@ __global__ void transpose_kernel(const double* __restrict__ in, size_t in_ld,
     for (int xx = threadIdx.y; xx < 32; xx += 8) {
         const size_t j = c0 + xx;
         if (j >= cols) break;
-        double* dst = out + (j * out_ld + r0) * K;
+        T* dst = out + (j * out_ld + r0) * K;
         for (int q = threadIdx.x; q < 32 * K; q += 32) {
             const int yy = q / K, w = q - yy * K;
             if (r0 + yy < rows) dst[q] = tile[yy][xx * K + w];
@@ -197,41 +212,54 @@ __global__ void transpose_kernel(const double* __restrict__ in, size_t in_ld,
 
 } // namespace
 
-cudaError_t launch_split_rows(int K, const double* in, size_t in_ld, double* work, size_t rows,
-                              size_t cols, int d, int sigma, double* pieces, size_t ldk,
-                              size_t slice_stride, unsigned long long* piece_max, int* err,
-                              cudaStream_t st) {
+cudaError_t launch_split_rows(int K, int word_bytes, const void* in, size_t in_ld, void* work,
+                              size_t rows, size_t cols, int d, int sigma, double* pieces,
+                              size_t ldk, size_t slice_stride, unsigned long long* piece_max,
+                              int* err, cudaStream_t st) {
     if (rows == 0) return cudaSuccess;
     dim3 grid((unsigned)rows), block(kSplitThreads);
-    switch (K) {
-    case 2:
-        split_rows_kernel<2><<<grid, block, 0, st>>>(in, in_ld, work, cols, d, sigma, pieces, ldk,
-                                                     slice_stride, piece_max, err);
-        break;
-    case 3:
-        split_rows_kernel<3><<<grid, block, 0, st>>>(in, in_ld, work, cols, d, sigma, pieces, ldk,
-                                                     slice_stride, piece_max, err);
-        break;
-    case 4:
-        split_rows_kernel<4><<<grid, block, 0, st>>>(in, in_ld, work, cols, d, sigma, pieces, ldk,
-                                                     slice_stride, piece_max, err);
-        break;
-    default: return cudaErrorInvalidValue;
+#define OZK_SPLIT(KK, TT)                                                                         \
+    split_rows_kernel<KK, TT><<<grid, block, 0, st>>>(static_cast<const TT*>(in), in_ld,          \
+                                                      static_cast<TT*>(work), cols, d, sigma,     \
+                                                      pieces, ldk, slice_stride, piece_max, err)
+    if (word_bytes == 4) {
+        if (K != 3) return cudaErrorInvalidValue;
+        OZK_SPLIT(3, float);
+    } else {
+        switch (K) {
+        case 2: OZK_SPLIT(2, double); break;
+        case 3: OZK_SPLIT(3, double); break;
+        case 4: OZK_SPLIT(4, double); break;
+        default: return cudaErrorInvalidValue;
+        }
     }
+#undef OZK_SPLIT
     return cudaGetLastError();
 }
 
-cudaError_t launch_transpose(int K, const double* in, size_t in_ld, double* out, size_t out_ld,
-                             size_t rows, size_t cols, cudaStream_t st) {
+cudaError_t launch_transpose(int K, int word_bytes, const void* in, size_t in_ld, void* out,
+                             size_t out_ld, size_t rows, size_t cols, cudaStream_t st) {
     if (rows == 0 || cols == 0) return cudaSuccess;
     dim3 grid((unsigned)((cols + 31) / 32), (unsigned)((rows + 31) / 32)), block(32, 8);
-    switch (K) {
-    case 1: transpose_kernel<1><<<grid, block, 0, st>>>(in, in_ld, out, out_ld, rows, cols); break;
-    case 2: transpose_kernel<2><<<grid, block, 0, st>>>(in, in_ld, out, out_ld, rows, cols); break;
-    case 3: transpose_kernel<3><<<grid, block, 0, st>>>(in, in_ld, out, out_ld, rows, cols); break;
-    case 4: transpose_kernel<4><<<grid, block, 0, st>>>(in, in_ld, out, out_ld, rows, cols); break;
-    default: return cudaErrorInvalidValue;
+#define OZK_TR(KK, TT)                                                                       \
+    transpose_kernel<KK, TT><<<grid, block, 0, st>>>(static_cast<const TT*>(in), in_ld,       \
+                                                     static_cast<TT*>(out), out_ld, rows, cols)
+    if (word_bytes == 4) {
+        switch (K) {
+        case 1: OZK_TR(1, float); break;
+        case 3: OZK_TR(3, float); break;
+        default: return cudaErrorInvalidValue;
+        }
+    } else {
+        switch (K) {
+        case 1: OZK_TR(1, double); break;
+        case 2: OZK_TR(2, double); break;
+        case 3: OZK_TR(3, double); break;
+        case 4: OZK_TR(4, double); break;
+        default: return cudaErrorInvalidValue;
+        }
     }
+#undef OZK_TR
     return cudaGetLastError();
 }
 
