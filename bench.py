@@ -30,8 +30,15 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = ("effective DD/TD/QD GEMM GFLOP/s (2n^3/t), n=8192; slice DGEMM % of FP64 peak")
-WORKLOADS = {"dd": (2, 6), "td": (3, 9), "qd": (4, 12)}  # K, headline D
-NAMES = {"dd": "DD", "td": "TD", "qd": "QD"}
+# format -> (ozk_format code, words, headline D).  DD/TD/QD: SURVEY §8d saturating D at
+# l = 8192; TS (config 4): 5-bit slices at sigma_TS = 19, saturation near D = 15.
+WORKLOADS = {"dd": (2, 2, 6), "td": (3, 3, 9), "qd": (4, 4, 12), "ts": (0x103, 3, 15)}
+NAMES = {"dd": "DD", "td": "TD", "qd": "QD", "ts": "TS"}
+
+
+def fmt_info(fmt):
+    code, K, d = WORKLOADS[fmt]
+    return code, K, d, (4 if fmt == "ts" else 8)
 KERNELS_PER_STEP = 4  # split A, transpose B, split B, fused slice GEMM
 
 
@@ -44,7 +51,7 @@ def parse():
     p.add_argument("--format", choices=sorted(WORKLOADS), default="td")
     p.add_argument("--n", type=int, default=8192)
     p.add_argument("--d", type=int, default=None)
-    p.add_argument("--variants", default="dd,qd",
+    p.add_argument("--variants", default="dd,qd,ts",
                    help="other formats timed (1 step each) and reported under 'variants'")
     p.add_argument("--cpu-sample", type=int, default=1024,
                    help="rows/cols of the CPU baseline sub-GEMM (inner dim stays n)")
@@ -140,7 +147,11 @@ def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return 0
-    K, d0 = WORKLOADS[args.format]
+    code, K, d0, _ = fmt_info(args.format)
+    if args.format == "ts":
+        print(json.dumps({"impl": "reference", "unavailable":
+                          "TS is not implemented by the reference (SPEC.md:8)"}), flush=True)
+        return 0
     d = args.d or d0
     n, r = args.n, args.cpu_sample
     for _ in range(args.warmup):
@@ -186,11 +197,12 @@ def run_ours(args):
     from paper_2301_09960_b200 import lib
     from paper_2301_09960_b200._lib import OzkProfile
 
-    K, d0 = WORKLOADS[args.format]
+    code, K, d0, wb = fmt_info(args.format)
     d = args.d or d0
     n = args.n
     P = d * (d + 1) // 2
     stream = torch.cuda.current_stream()
+    wdt = torch.float32 if wb == 4 else torch.float64
     sh = stream.cuda_stream
 
     if world > 1:
@@ -204,18 +216,18 @@ def run_ours(args):
             raise RuntimeError(lib.ozk_last_error().decode())
 
     # synthetic Eq. (1) inputs generated on device (outside the timed region)
-    A = torch.empty((n, n, K), dtype=torch.float64, device="cuda")
-    B = torch.empty((n, n, K), dtype=torch.float64, device="cuda")
-    check(lib.ozk_gen_eq1_device(K, n, n, 1, A.data_ptr(), sh))
-    check(lib.ozk_gen_eq1_device(K, n, n, 2, B.data_ptr(), sh))
+    A = torch.empty((n, n, K), dtype=wdt, device="cuda")
+    B = torch.empty((n, n, K), dtype=wdt, device="cuda")
+    check(lib.ozk_gen_eq1_device(code, n, n, 1, A.data_ptr(), sh))
+    check(lib.ozk_gen_eq1_device(code, n, n, 2, B.data_ptr(), sh))
 
     peak = lib.ozk_probe_dmma_tflops(20000, sh)
 
     if world == 1:
-        C = torch.empty((n, n, K), dtype=torch.float64, device="cuda")
+        C = torch.empty((n, n, K), dtype=wdt, device="cuda")
 
         def step(prof):
-            check(lib.ozk_ozaki_gemm_device(K, n, n, n, A.data_ptr(), B.data_ptr(), d, 0.0,
+            check(lib.ozk_ozaki_gemm_device(code, n, n, n, A.data_ptr(), B.data_ptr(), d, 0.0,
                                             C.data_ptr(), sh, ctypes.byref(prof)))
     else:
         def step(prof):
@@ -255,7 +267,7 @@ def run_ours(args):
 
     e2e = None
     if not args.no_e2e and world == 1:
-        e2e = run_e2e(args, lib, OzkProfile, A, B, K, d, n)
+        e2e = run_e2e(args, lib, OzkProfile, A, B, code, K, wb, d, n)
 
     variants = []
     if world == 1:
@@ -264,7 +276,7 @@ def run_ours(args):
             variants.append(run_variant(lib, OzkProfile, fmt, n, peak, sh))
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and args.format != "ts":
         rate, dt, cores, kind = cpu_sample_rate(K, d, n, args.cpu_sample)
         cpu = {"value": round(rate, 4), "unit": "GFLOP/s", "cores": cores, "kind": kind,
                "sample": f"{NAMES[args.format]} Ozaki sub-GEMM {args.cpu_sample}x{n} . "
@@ -302,17 +314,17 @@ def run_ours(args):
     return 0
 
 
-def run_e2e(args, lib, OzkProfile, A, B, K, d, n):
+def run_e2e(args, lib, OzkProfile, A, B, code, K, wb, d, n):
     """Same metric through the host-buffer C-ABI entry point (ozk_ozaki_gemm):
     H2D of A and B from pinned memory, the GEMM, D2H of C, every step."""
     import torch
     ha = A.cpu().pin_memory()
     hb = B.cpu().pin_memory()
-    hc = torch.empty((n, n, K), dtype=torch.float64).pin_memory()
+    hc = torch.empty((n, n, K), dtype=A.dtype).pin_memory()
     prof = OzkProfile()
 
     def call():
-        st = lib.ozk_ozaki_gemm(K, n, n, n, ha.data_ptr(), hb.data_ptr(), d, 0.0, hc.data_ptr(),
+        st = lib.ozk_ozaki_gemm(code, n, n, n, ha.data_ptr(), hb.data_ptr(), d, 0.0, hc.data_ptr(),
                                 ctypes.byref(prof))
         if st != 0:
             raise RuntimeError(lib.ozk_last_error().decode())
@@ -325,23 +337,24 @@ def run_e2e(args, lib, OzkProfile, A, B, K, d, n):
         times.append(time.perf_counter() - t0)
     t = statistics.mean(times)
     return {"value": round(2.0 * n ** 3 / t / 1e9, 3), "unit": "GFLOP/s",
-            "h2d_bytes_per_step": 2 * n * n * K * 8, "d2h_bytes_per_step": n * n * K * 8,
+            "h2d_bytes_per_step": 2 * n * n * K * wb, "d2h_bytes_per_step": n * n * K * wb,
             "ms_per_step": round(1e3 * t, 3), "api": "ozk_ozaki_gemm (host buffers, pinned)"}
 
 
 def run_variant(lib, OzkProfile, fmt, n, peak, sh):
     import torch
-    K, d = WORKLOADS[fmt]
+    code, K, d, wb = fmt_info(fmt)
     P = d * (d + 1) // 2
-    A = torch.empty((n, n, K), dtype=torch.float64, device="cuda")
-    B = torch.empty((n, n, K), dtype=torch.float64, device="cuda")
-    C = torch.empty((n, n, K), dtype=torch.float64, device="cuda")
-    lib.ozk_gen_eq1_device(K, n, n, 1, A.data_ptr(), sh)
-    lib.ozk_gen_eq1_device(K, n, n, 2, B.data_ptr(), sh)
+    wdt = torch.float32 if wb == 4 else torch.float64
+    A = torch.empty((n, n, K), dtype=wdt, device="cuda")
+    B = torch.empty((n, n, K), dtype=wdt, device="cuda")
+    C = torch.empty((n, n, K), dtype=wdt, device="cuda")
+    lib.ozk_gen_eq1_device(code, n, n, 1, A.data_ptr(), sh)
+    lib.ozk_gen_eq1_device(code, n, n, 2, B.data_ptr(), sh)
     prof = OzkProfile()
 
     def call():
-        st = lib.ozk_ozaki_gemm_device(K, n, n, n, A.data_ptr(), B.data_ptr(), d, 0.0,
+        st = lib.ozk_ozaki_gemm_device(code, n, n, n, A.data_ptr(), B.data_ptr(), d, 0.0,
                                        C.data_ptr(), sh, ctypes.byref(prof))
         if st != 0:
             raise RuntimeError(lib.ozk_last_error().decode())

@@ -49,8 +49,12 @@ typedef enum {
     OZK_ENOMEM = 5  /* device allocation failure */
 } ozk_status;
 
-/* words per element, = the reference's MultiFloat<K> template argument */
-typedef enum { OZK_DD = 2, OZK_TD = 3, OZK_QD = 4 } ozk_format;
+/* Element format.  DD/TD/QD: K = 2/3/4 binary64 words, = the reference's
+ * MultiFloat<K> template argument.  TS (triple-single): 3 binary32 words per
+ * element -- not in the reference; defined by restating its
+ * generic K >= 3 algorithms with binary32 words and S = 24 (oracle/ozk_oracle.c).
+ * Matrix buffers are void*: K words of the format's word type per element. */
+typedef enum { OZK_DD = 2, OZK_TD = 3, OZK_QD = 4, OZK_TS = 0x103 } ozk_format;
 
 /* mpmat::SplitSide (ozaki.hpp:33) */
 typedef enum { OZK_SIDE_ROWS = 0, OZK_SIDE_COLS = 1 } ozk_side;
@@ -79,20 +83,21 @@ typedef struct {
  * dimensions (ozaki.hpp:184), OZK_EPARAM for split_count < 1 (:185),
  * drop_threshold < 0 (:186), a non-finite entry (:77-78) or an entry too
  * large to shift (:109).  split_count is limited to 32 here. */
-ozk_status ozk_ozaki_gemm(ozk_format fmt, size_t m, size_t l, size_t n, const double* a,
-                          const double* b, int split_count, double drop_threshold, double* c,
+ozk_status ozk_ozaki_gemm(ozk_format fmt, size_t m, size_t l, size_t n, const void* a,
+                          const void* b, int split_count, double drop_threshold, void* c,
                           ozk_profile* prof);
 
 /* Same with device-resident a, b, c on `stream`. */
-ozk_status ozk_ozaki_gemm_device(ozk_format fmt, size_t m, size_t l, size_t n, const double* a,
-                                 const double* b, int split_count, double drop_threshold,
-                                 double* c, void* stream, ozk_profile* prof);
+ozk_status ozk_ozaki_gemm_device(ozk_format fmt, size_t m, size_t l, size_t n, const void* a,
+                                 const void* b, int split_count, double drop_threshold, void* c,
+                                 void* stream, ozk_profile* prof);
 
 /* split_matrix<K> (ozaki.hpp:74-147): host buffers.  pieces receives
- * split_count row-major (rows x cols) binary64 slices, residual the K-word
- * working matrix after the last extraction (SplitSet<K>, ozaki.hpp:59-67). */
-ozk_status ozk_split(ozk_format fmt, size_t rows, size_t cols, const double* mat, int split_count,
-                     ozk_side side, double* pieces, double* residual);
+ * split_count row-major (rows x cols) slices (binary64; binary32 for TS),
+ * residual the K-word working matrix after the last extraction (SplitSet<K>,
+ * ozaki.hpp:59-67). */
+ozk_status ozk_split(ozk_format fmt, size_t rows, size_t cols, const void* mat, int split_count,
+                     ozk_side side, void* pieces, void* residual);
 
 /* GemmBackend (backend.hpp:12-13): C = A * B in binary64, row-major, host
  * buffers.  Any summation order (the plugin contract, backend.hpp:8-11). */
@@ -106,7 +111,8 @@ int ozk_exponent_ceil_log2(double x);        /* ozaki.hpp:36-40 (x > 0, finite) 
 
 /* ---- slice-level entry points (sharded / multi-GPU orchestration) --------- *
  * Slices are kept in the DMMA operand layout: split_count planes of `outer`
- * rows of ozk_slice_ld(inner) doubles (k contiguous, zero padded).
+ * rows of ozk_slice_ld(inner) doubles (k contiguous, zero padded; TS slices
+ * are binary32 values stored exactly as binary64).
  *   side ROWS (left factor A, m x l):  slices[a][i][k] = piece_a(i, k)
  *   side COLS (right factor B, l x n): slices[a][j][k] = piece_a(k, j)
  * `ld` is the row stride (in elements) of the input K-word matrix, so a
@@ -118,7 +124,7 @@ int ozk_exponent_ceil_log2(double x);        /* ozaki.hpp:36-40 (x > 0, finite) 
 size_t ozk_slice_ld(size_t inner_dim);
 
 ozk_status ozk_split_slices_device(ozk_format fmt, size_t rows, size_t cols, size_t ld,
-                                   const double* mat, int split_count, ozk_side side,
+                                   const void* mat, int split_count, ozk_side side,
                                    double* slices, size_t plane_rows, double* piece_max,
                                    void* stream);
 
@@ -137,7 +143,7 @@ ozk_status ozk_pair_list(int split_count, const double* amax, const double* bmax
 ozk_status ozk_slices_gemm_device(ozk_format fmt, size_t m, size_t l, size_t n,
                                   const double* a_slices, const double* b_slices, size_t ncb,
                                   size_t nblk, size_t b_blk_stride, int split_count,
-                                  const int* pairs, int npairs, double* c, size_t ldc,
+                                  const int* pairs, int npairs, void* c, size_t ldc,
                                   void* stream);
 
 /* Parity hook: every slice product C_ab = A_alpha * B_beta of the pair list,
@@ -152,7 +158,7 @@ ozk_status ozk_pair_products_device(size_t m, size_t l, size_t n, const double* 
  * memory; counter-based, so a pure function of (seed, shape).  Not the
  * reference's sequential generator (gen.hpp:20-34) -- see csrc/gen.cu. */
 ozk_status ozk_gen_eq1_device(ozk_format fmt, size_t rows, size_t cols, uint64_t seed,
-                              double* out, void* stream);
+                              void* out, void* stream);
 
 /* FP64 tensor-pipe (DMMA) ceiling of the current device in TFLOP/s, measured by a
  * register-resident mma.sync.m8n8k4.f64 loop on every SM (the roofline

@@ -100,6 +100,15 @@ class Port(CpuOzaki):
                                                    _dp, _lp]
         lib.ozk_oracle_xoshiro_u64.argtypes = [ctypes.c_uint64, _c_size,
                                                ctypes.POINTER(ctypes.c_uint64)]
+        _fp = ctypes.c_void_p
+        lib.ozk_oracle_gen_eq1_ts.argtypes = [_c_size, _c_size, ctypes.c_uint64, _fp]
+        lib.ozk_oracle_split_ts.argtypes = [_c_size, _c_size, _fp, ctypes.c_int, ctypes.c_int,
+                                            _fp, _fp]
+        lib.ozk_oracle_ozaki_gemm_ts.argtypes = [_c_size, _c_size, _c_size, _fp, _fp,
+                                                 ctypes.c_int, ctypes.c_double, _fp, _ip, _lp]
+        lib.ozk_oracle_ts_add_float.argtypes = [_fp, ctypes.c_float, _fp]
+        lib.ozk_oracle_exact_sgemm.argtypes = [_c_size, _c_size, _c_size, _fp, _fp, _fp]
+        lib.ozk_oracle_exact_sgemm.restype = ctypes.c_long
         self.lib = lib
 
     def gen_eq1(self, K, m, n, seed):
@@ -189,6 +198,59 @@ class Port(CpuOzaki):
 
     def split_shift_bits(self, inner, short_bits=53):
         return self.lib.ozk_oracle_split_shift_bits(inner, short_bits)
+
+    # ---- TS (triple-single, binary32 words; defined by this restatement) ----
+    def gen_eq1_ts(self, m, n, seed):
+        out = np.empty((m, n, 3), dtype=np.float32)
+        self.lib.ozk_oracle_gen_eq1_ts(m, n, seed, out.ctypes.data)
+        return out
+
+    def split_ts(self, mat, d, side):
+        mat = np.ascontiguousarray(mat, dtype=np.float32)
+        rows, cols = mat.shape[0], mat.shape[1]
+        pieces = np.zeros((max(d, 1), rows, cols), dtype=np.float32)
+        resid = np.empty_like(mat)
+        st = self.lib.ozk_oracle_split_ts(rows, cols, mat.ctypes.data, d, side,
+                                          pieces.ctypes.data, resid.ctypes.data)
+        if st:
+            raise OracleError(st, "split_ts")
+        return pieces, resid
+
+    def ozaki_gemm_ts(self, a, b, d, drop=0.0, want_inexact=False):
+        a = np.ascontiguousarray(a, dtype=np.float32)
+        b = np.ascontiguousarray(b, dtype=np.float32)
+        m, l, n = a.shape[0], a.shape[1], b.shape[1]
+        c = np.zeros((m, n, 3), dtype=np.float32)
+        np_ = ctypes.c_int(0)
+        inex = ctypes.c_long(0)
+        st = self.lib.ozk_oracle_ozaki_gemm_ts(m, l, n, a.ctypes.data, b.ctypes.data, d, drop,
+                                               c.ctypes.data, ctypes.byref(np_),
+                                               ctypes.byref(inex))
+        if st:
+            raise OracleError(st, "ozaki_gemm_ts")
+        if want_inexact:
+            return c, np_.value, inex.value
+        return c
+
+    def ts_add_float(self, x, y):
+        x = np.ascontiguousarray(x, dtype=np.float32).reshape(-1, 3)
+        y = np.ascontiguousarray(y, dtype=np.float32).reshape(-1)
+        out = np.empty_like(x)
+        r = np.empty(3, dtype=np.float32)
+        for i in range(x.shape[0]):
+            xi = np.ascontiguousarray(x[i])
+            self.lib.ozk_oracle_ts_add_float(xi.ctypes.data, ctypes.c_float(float(y[i])),
+                                             r.ctypes.data)
+            out[i] = r
+        return out
+
+    def exact_sgemm(self, a, b):
+        a = np.ascontiguousarray(a, dtype=np.float32)
+        b = np.ascontiguousarray(b, dtype=np.float32)
+        c = np.empty((a.shape[0], b.shape[1]), dtype=np.float32)
+        bad = self.lib.ozk_oracle_exact_sgemm(a.shape[0], a.shape[1], b.shape[1], a.ctypes.data,
+                                              b.ctypes.data, c.ctypes.data)
+        return c, bad
 
 
 class Ref(CpuOzaki):

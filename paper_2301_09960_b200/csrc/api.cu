@@ -83,12 +83,19 @@ struct OwnStream {
     }
 };
 
-bool valid_fmt(int fmt) { return fmt == OZK_DD || fmt == OZK_TD || fmt == OZK_QD; }
+bool valid_fmt(int fmt) {
+    return fmt == OZK_DD || fmt == OZK_TD || fmt == OZK_QD || fmt == OZK_TS;
+}
+// words per element and bytes per word of a format
+int words_of(int fmt) { return fmt == OZK_TS ? 3 : fmt; }
+int word_bytes_of(int fmt) { return fmt == OZK_TS ? 4 : 8; }
+size_t elem_bytes(int fmt) { return (size_t)words_of(fmt) * word_bytes_of(fmt); }
 
-int shift_bits(size_t inner) {
+// split_shift_bits (ozaki.hpp:43-48); short_bits = 53 for binary64 words, 24 for TS
+int shift_bits(size_t inner, int short_bits = 53) {
     int cl = 0;
     while ((size_t(1) << cl) < inner) ++cl;
-    return (53 + cl + 1) / 2;
+    return (short_bits + cl + 1) / 2;
 }
 
 void triangular_pairs(int d, PairList& pl) {
@@ -121,20 +128,21 @@ ozk_status check_dev_err(int flag, const char* what) {
 }
 
 // Split of a K-word matrix into slices in the operand layout (see ozk.h).
-// work must hold outer*inner*K doubles.  Returns a CUDA error code.
-cudaError_t split_to_slices(int K, size_t rows, size_t cols, size_t ld, const double* mat, int d,
-                            int side, double* slices, size_t plane_rows, double* work,
+// work must hold outer*inner elements.  Returns a CUDA error code.
+cudaError_t split_to_slices(int fmt, size_t rows, size_t cols, size_t ld, const void* mat, int d,
+                            int side, double* slices, size_t plane_rows, void* work,
                             unsigned long long* pmax, int* err, cudaStream_t st) {
+    const int K = words_of(fmt), wb = word_bytes_of(fmt);
     const size_t inner = side == OZK_SIDE_ROWS ? cols : rows;
     const size_t ldk = slice_ld(inner);
-    const int sigma = shift_bits(inner);
+    const int sigma = shift_bits(inner, wb == 4 ? 24 : 53);
     if (side == OZK_SIDE_ROWS)
-        return launch_split_rows(K, mat, ld, work, rows, cols, d, sigma, slices, ldk,
+        return launch_split_rows(K, wb, mat, ld, work, rows, cols, d, sigma, slices, ldk,
                                  plane_rows * ldk, pmax, err, st);
     // columns: transpose to (cols x rows) so each column is a contiguous row
-    cudaError_t e = launch_transpose(K, mat, ld, work, rows, rows, cols, st);
+    cudaError_t e = launch_transpose(K, wb, mat, ld, work, rows, rows, cols, st);
     if (e != cudaSuccess) return e;
-    return launch_split_rows(K, work, rows, work, cols, rows, d, sigma, slices, ldk,
+    return launch_split_rows(K, wb, work, rows, work, cols, rows, d, sigma, slices, ldk,
                              plane_rows * ldk, pmax, err, st);
 }
 
@@ -160,15 +168,15 @@ struct Timer {
     }
 };
 
-ozk_status ozaki_device_impl(int K, size_t m, size_t l, size_t n, const double* a,
-                             const double* b, int d, double drop, double* c, cudaStream_t st,
-                             ozk_profile* prof) {
+ozk_status ozaki_device_impl(int fmt, size_t m, size_t l, size_t n, const void* a, const void* b,
+                             int d, double drop, void* c, cudaStream_t st, ozk_profile* prof) {
+    const int K = words_of(fmt), wb = word_bytes_of(fmt);
     const int sms = num_sms_cached();
     const size_t ldk = slice_ld(l);
     DevBuf sa, sb, work, flags;
     OZK_CUDA(sa.alloc(sizeof(double) * d * m * ldk, st), "ozaki_gemm: slices A");
     OZK_CUDA(sb.alloc(sizeof(double) * d * n * ldk, st), "ozaki_gemm: slices B");
-    OZK_CUDA(work.alloc(sizeof(double) * (m > n ? m : n) * l * K, st), "ozaki_gemm: work");
+    OZK_CUDA(work.alloc(elem_bytes(fmt) * (m > n ? m : n) * l, st), "ozaki_gemm: work");
     // flags layout: [err int (8 B)][amax d][bmax d]
     OZK_CUDA(flags.alloc(8 + 16 * (size_t)d, st), "ozaki_gemm: flags");
     OZK_CUDA(cudaMemsetAsync(flags.p, 0, 8 + 16 * (size_t)d, st), "ozaki_gemm: memset");
@@ -179,11 +187,11 @@ ozk_status ozaki_device_impl(int K, size_t m, size_t l, size_t n, const double* 
 
     Timer tm(prof != nullptr);
     tm.mark(0, st);
-    OZK_CUDA(split_to_slices(K, m, l, l, a, d, OZK_SIDE_ROWS, sa.as<double>(), m,
-                             work.as<double>(), want_max ? amax : nullptr, err, st),
+    OZK_CUDA(split_to_slices(fmt, m, l, l, a, d, OZK_SIDE_ROWS, sa.as<double>(), m, work.p,
+                             want_max ? amax : nullptr, err, st),
              "ozaki_gemm: split A");
-    OZK_CUDA(split_to_slices(K, l, n, n, b, d, OZK_SIDE_COLS, sb.as<double>(), n,
-                             work.as<double>(), want_max ? bmax : nullptr, err, st),
+    OZK_CUDA(split_to_slices(fmt, l, n, n, b, d, OZK_SIDE_COLS, sb.as<double>(), n, work.p,
+                             want_max ? bmax : nullptr, err, st),
              "ozaki_gemm: split B");
     tm.mark(1, st);
 
@@ -220,9 +228,9 @@ ozk_status ozaki_device_impl(int K, size_t m, size_t l, size_t n, const double* 
     prob.c = c;
     prob.ldc = n;
     if (pl.count == 0)  // every pair pruned (drop_threshold > 1): C = 0
-        OZK_CUDA(cudaMemsetAsync(c, 0, sizeof(double) * m * n * K, st), "ozaki_gemm: zero C");
+        OZK_CUDA(cudaMemsetAsync(c, 0, elem_bytes(fmt) * m * n, st), "ozaki_gemm: zero C");
     else
-        OZK_CUDA(launch_pair_gemm(K, kAccumulate, prob, pl, st, sms), "ozaki_gemm: slice GEMM");
+        OZK_CUDA(launch_pair_gemm(K, kAccumulate, prob, pl, st, sms, wb), "ozaki_gemm: slice GEMM");
     tm.mark(2, st);
 
     int flag = 0;
@@ -243,7 +251,7 @@ ozk_status ozaki_device_impl(int K, size_t m, size_t l, size_t n, const double* 
 }
 
 ozk_status check_gemm_args(int fmt, size_t m, size_t l, size_t n, int d, double drop) {
-    if (!valid_fmt(fmt)) return fail(OZK_EPARAM, "ozaki_gemm: format must be DD, TD or QD");
+    if (!valid_fmt(fmt)) return fail(OZK_EPARAM, "ozaki_gemm: format must be DD, TD, QD or TS");
     if (m == 0 || l == 0 || n == 0) return fail(OZK_ESHAPE, "matrix dimensions must be positive");
     if (d < 1) return fail(OZK_EPARAM, "ozaki_gemm: split count must be >= 1");
     if (drop < 0.0) return fail(OZK_EPARAM, "ozaki_gemm: negative drop threshold");
@@ -269,35 +277,31 @@ int ozk_exponent_ceil_log2(double x) {
 
 size_t ozk_slice_ld(size_t inner) { return slice_ld(inner); }
 
-ozk_status ozk_ozaki_gemm_device(ozk_format fmt, size_t m, size_t l, size_t n, const double* a,
-                                 const double* b, int d, double drop, double* c, void* stream,
+ozk_status ozk_ozaki_gemm_device(ozk_format fmt, size_t m, size_t l, size_t n, const void* a,
+                                 const void* b, int d, double drop, void* c, void* stream,
                                  ozk_profile* prof) {
     if (ozk_status s = check_gemm_args(fmt, m, l, n, d, drop)) return s;
     return ozaki_device_impl((int)fmt, m, l, n, a, b, d, drop, c, (cudaStream_t)stream, prof);
 }
 
-ozk_status ozk_ozaki_gemm(ozk_format fmt, size_t m, size_t l, size_t n, const double* a,
-                          const double* b, int d, double drop, double* c, ozk_profile* prof) {
+ozk_status ozk_ozaki_gemm(ozk_format fmt, size_t m, size_t l, size_t n, const void* a,
+                          const void* b, int d, double drop, void* c, ozk_profile* prof) {
     if (ozk_status s = check_gemm_args(fmt, m, l, n, d, drop)) return s;
-    const int K = (int)fmt;
+    const size_t eb = elem_bytes(fmt);
     auto t0 = std::chrono::steady_clock::now();
     OwnStream os;
     OZK_CUDA(os.create(), "ozaki_gemm: stream");
     num_sms_cached();
     DevBuf da, db, dc;
-    OZK_CUDA(da.alloc(sizeof(double) * m * l * K, os.s), "ozaki_gemm: A");
-    OZK_CUDA(db.alloc(sizeof(double) * l * n * K, os.s), "ozaki_gemm: B");
-    OZK_CUDA(dc.alloc(sizeof(double) * m * n * K, os.s), "ozaki_gemm: C");
-    OZK_CUDA(cudaMemcpyAsync(da.p, a, sizeof(double) * m * l * K, cudaMemcpyHostToDevice, os.s),
-             "ozaki_gemm: H2D A");
-    OZK_CUDA(cudaMemcpyAsync(db.p, b, sizeof(double) * l * n * K, cudaMemcpyHostToDevice, os.s),
-             "ozaki_gemm: H2D B");
+    OZK_CUDA(da.alloc(eb * m * l, os.s), "ozaki_gemm: A");
+    OZK_CUDA(db.alloc(eb * l * n, os.s), "ozaki_gemm: B");
+    OZK_CUDA(dc.alloc(eb * m * n, os.s), "ozaki_gemm: C");
+    OZK_CUDA(cudaMemcpyAsync(da.p, a, eb * m * l, cudaMemcpyHostToDevice, os.s), "ozaki_gemm: H2D A");
+    OZK_CUDA(cudaMemcpyAsync(db.p, b, eb * l * n, cudaMemcpyHostToDevice, os.s), "ozaki_gemm: H2D B");
     ozk_profile local{};
-    ozk_status s = ozaki_device_impl(K, m, l, n, da.as<double>(), db.as<double>(), d, drop,
-                                     dc.as<double>(), os.s, &local);
+    ozk_status s = ozaki_device_impl((int)fmt, m, l, n, da.p, db.p, d, drop, dc.p, os.s, &local);
     if (s != OZK_OK) return s;
-    OZK_CUDA(cudaMemcpyAsync(c, dc.p, sizeof(double) * m * n * K, cudaMemcpyDeviceToHost, os.s),
-             "ozaki_gemm: D2H C");
+    OZK_CUDA(cudaMemcpyAsync(c, dc.p, eb * m * n, cudaMemcpyDeviceToHost, os.s), "ozaki_gemm: D2H C");
     OZK_CUDA(cudaStreamSynchronize(os.s), "ozaki_gemm");
     if (prof) {
         *prof = local;
@@ -308,15 +312,16 @@ ozk_status ozk_ozaki_gemm(ozk_format fmt, size_t m, size_t l, size_t n, const do
     return OZK_OK;
 }
 
-ozk_status ozk_split(ozk_format fmt, size_t rows, size_t cols, const double* mat, int d,
-                     ozk_side side, double* pieces, double* residual) {
-    if (!valid_fmt(fmt)) return fail(OZK_EPARAM, "split_matrix: format must be DD, TD or QD");
+ozk_status ozk_split(ozk_format fmt, size_t rows, size_t cols, const void* mat, int d,
+                     ozk_side side, void* pieces, void* residual) {
+    if (!valid_fmt(fmt)) return fail(OZK_EPARAM, "split_matrix: format must be DD, TD, QD or TS");
     if (rows == 0 || cols == 0) return fail(OZK_ESHAPE, "matrix dimensions must be positive");
     if (d < 1) return fail(OZK_EPARAM, "split_matrix: split count must be >= 1");
     if (d > kMaxSplits) return fail(OZK_EPARAM, "split_matrix: split count above 32 is not supported");
     if (side != OZK_SIDE_ROWS && side != OZK_SIDE_COLS)
         return fail(OZK_EPARAM, "split_matrix: bad side");
-    const int K = (int)fmt;
+    const int K = words_of(fmt), wb = word_bytes_of(fmt);
+    const size_t eb = elem_bytes(fmt);
     const size_t N = rows * cols;
     const size_t inner = side == OZK_SIDE_ROWS ? cols : rows;
     const size_t outer = side == OZK_SIDE_ROWS ? rows : cols;
@@ -324,72 +329,78 @@ ozk_status ozk_split(ozk_format fmt, size_t rows, size_t cols, const double* mat
     OwnStream os;
     OZK_CUDA(os.create(), "split_matrix: stream");
     num_sms_cached();
-    DevBuf dm, work, sl, tmp, flags;
-    OZK_CUDA(dm.alloc(sizeof(double) * N * K, os.s), "split_matrix: input");
-    OZK_CUDA(work.alloc(sizeof(double) * N * K, os.s), "split_matrix: work");
+    DevBuf dm, work, sl, tp, tr, flags;
+    OZK_CUDA(dm.alloc(eb * N, os.s), "split_matrix: input");
+    OZK_CUDA(work.alloc(eb * N, os.s), "split_matrix: work");
     OZK_CUDA(sl.alloc(sizeof(double) * d * outer * ldk, os.s), "split_matrix: slices");
+    OZK_CUDA(tp.alloc(sizeof(double) * d * N, os.s), "split_matrix: pieces");
     OZK_CUDA(flags.alloc(8, os.s), "split_matrix: flags");
     OZK_CUDA(cudaMemsetAsync(flags.p, 0, 8, os.s), "split_matrix: memset");
-    OZK_CUDA(cudaMemcpyAsync(dm.p, mat, sizeof(double) * N * K, cudaMemcpyHostToDevice, os.s),
-             "split_matrix: H2D");
-    OZK_CUDA(split_to_slices(K, rows, cols, cols, dm.as<double>(), d, side, sl.as<double>(),
-                             outer, work.as<double>(), nullptr, flags.as<int>(), os.s),
+    OZK_CUDA(cudaMemcpyAsync(dm.p, mat, eb * N, cudaMemcpyHostToDevice, os.s), "split_matrix: H2D");
+    OZK_CUDA(split_to_slices(fmt, rows, cols, cols, dm.p, d, side, sl.as<double>(), outer, work.p,
+                             nullptr, flags.as<int>(), os.s),
              "split_matrix");
     int flag = 0;
     OZK_CUDA(cudaMemcpyAsync(&flag, flags.p, sizeof(int), cudaMemcpyDeviceToHost, os.s),
              "split_matrix: flag");
     OZK_CUDA(cudaStreamSynchronize(os.s), "split_matrix");
     if (ozk_status s = check_dev_err(flag, "split_matrix")) return s;
+    // pieces back to the reference layout (rows x cols, row-major) in binary64
     if (side == OZK_SIDE_ROWS) {
-        OZK_CUDA(cudaMemcpy2DAsync(pieces, cols * 8, sl.p, ldk * 8, cols * 8, rows * (size_t)d,
-                                   cudaMemcpyDeviceToHost, os.s),
-                 "split_matrix: D2H pieces");
-        OZK_CUDA(cudaMemcpyAsync(residual, work.p, sizeof(double) * N * K,
-                                 cudaMemcpyDeviceToHost, os.s),
-                 "split_matrix: D2H residual");
+        OZK_CUDA(cudaMemcpy2DAsync(tp.p, cols * 8, sl.p, ldk * 8, cols * 8, rows * (size_t)d,
+                                   cudaMemcpyDeviceToDevice, os.s),
+                 "split_matrix: pack pieces");
     } else {
-        // slices are (cols x ldk) per piece, residual is (cols x rows) K-word:
-        // transpose both back to the reference layout
-        OZK_CUDA(tmp.alloc(sizeof(double) * (N * K > d * N ? N * K : d * N), os.s),
-                 "split_matrix: tmp");
         for (int a = 0; a < d; ++a)
-            OZK_CUDA(launch_transpose(1, sl.as<double>() + (size_t)a * outer * ldk, ldk,
-                                      tmp.as<double>() + (size_t)a * N, cols, cols, rows, os.s),
+            OZK_CUDA(launch_transpose(1, 8, sl.as<double>() + (size_t)a * outer * ldk, ldk,
+                                      tp.as<double>() + (size_t)a * N, cols, cols, rows, os.s),
                      "split_matrix: transpose pieces");
-        OZK_CUDA(cudaMemcpyAsync(pieces, tmp.p, sizeof(double) * d * N, cudaMemcpyDeviceToHost,
+    }
+    // residual back to the reference layout
+    const void* res_src = work.p;
+    if (side == OZK_SIDE_COLS) {
+        OZK_CUDA(tr.alloc(eb * N, os.s), "split_matrix: residual");
+        OZK_CUDA(launch_transpose(K, wb, work.p, rows, tr.p, cols, cols, rows, os.s),
+                 "split_matrix: transpose residual");
+        res_src = tr.p;
+    }
+    OZK_CUDA(cudaMemcpyAsync(residual, res_src, eb * N, cudaMemcpyDeviceToHost, os.s),
+             "split_matrix: D2H residual");
+    if (wb == 8) {
+        OZK_CUDA(cudaMemcpyAsync(pieces, tp.p, sizeof(double) * d * N, cudaMemcpyDeviceToHost, os.s),
+                 "split_matrix: D2H pieces");
+        OZK_CUDA(cudaStreamSynchronize(os.s), "split_matrix");
+    } else {
+        // TS pieces are binary32 values held exactly in binary64 slices
+        std::vector<double> host((size_t)d * N);
+        OZK_CUDA(cudaMemcpyAsync(host.data(), tp.p, sizeof(double) * d * N, cudaMemcpyDeviceToHost,
                                  os.s),
                  "split_matrix: D2H pieces");
-        OZK_CUDA(launch_transpose(K, work.as<double>(), rows, tmp.as<double>(), cols, cols, rows,
-                                  os.s),
-                 "split_matrix: transpose residual");
-        OZK_CUDA(cudaMemcpyAsync(residual, tmp.p, sizeof(double) * N * K, cudaMemcpyDeviceToHost,
-                                 os.s),
-                 "split_matrix: D2H residual");
+        OZK_CUDA(cudaStreamSynchronize(os.s), "split_matrix");
+        float* out = static_cast<float*>(pieces);
+        for (size_t i = 0; i < host.size(); ++i) out[i] = (float)host[i];
     }
-    OZK_CUDA(cudaStreamSynchronize(os.s), "split_matrix");
     return OZK_OK;
 }
 
 ozk_status ozk_split_slices_device(ozk_format fmt, size_t rows, size_t cols, size_t ld,
-                                   const double* mat, int d, ozk_side side, double* slices,
+                                   const void* mat, int d, ozk_side side, double* slices,
                                    size_t plane_rows, double* piece_max, void* stream) {
-    if (!valid_fmt(fmt)) return fail(OZK_EPARAM, "split_matrix: format must be DD, TD or QD");
+    if (!valid_fmt(fmt)) return fail(OZK_EPARAM, "split_matrix: format must be DD, TD, QD or TS");
     if (rows == 0 || cols == 0) return fail(OZK_ESHAPE, "matrix dimensions must be positive");
     if (d < 1) return fail(OZK_EPARAM, "split_matrix: split count must be >= 1");
     if (d > kMaxSplits) return fail(OZK_EPARAM, "split_matrix: split count above 32 is not supported");
     if (ld < cols) return fail(OZK_ESHAPE, "split_matrix: ld < cols");
     if (plane_rows < (side == OZK_SIDE_ROWS ? rows : cols))
         return fail(OZK_ESHAPE, "split_matrix: plane_rows < outer dimension");
-    const int K = (int)fmt;
     cudaStream_t st = (cudaStream_t)stream;
     num_sms_cached();
     DevBuf work, flags;
-    OZK_CUDA(work.alloc(sizeof(double) * rows * cols * K, st), "split_matrix: work");
+    OZK_CUDA(work.alloc(elem_bytes(fmt) * rows * cols, st), "split_matrix: work");
     OZK_CUDA(flags.alloc(8, st), "split_matrix: flags");
     OZK_CUDA(cudaMemsetAsync(flags.p, 0, 8, st), "split_matrix: memset");
-    OZK_CUDA(split_to_slices(K, rows, cols, ld, mat, d, side, slices, plane_rows,
-                             work.as<double>(), reinterpret_cast<unsigned long long*>(piece_max),
-                             flags.as<int>(), st),
+    OZK_CUDA(split_to_slices(fmt, rows, cols, ld, mat, d, side, slices, plane_rows, work.p,
+                             reinterpret_cast<unsigned long long*>(piece_max), flags.as<int>(), st),
              "split_matrix");
     int flag = 0;
     OZK_CUDA(cudaMemcpyAsync(&flag, flags.p, sizeof(int), cudaMemcpyDeviceToHost, st),
@@ -432,8 +443,8 @@ static ozk_status fill_pairs(int d, const int* pairs, int npairs, PairList& pl) 
 ozk_status ozk_slices_gemm_device(ozk_format fmt, size_t m, size_t l, size_t n,
                                   const double* a_slices, const double* b_slices, size_t ncb,
                                   size_t nblk, size_t b_blk_stride, int d, const int* pairs,
-                                  int npairs, double* c, size_t ldc, void* stream) {
-    if (!valid_fmt(fmt)) return fail(OZK_EPARAM, "slices_gemm: format must be DD, TD or QD");
+                                  int npairs, void* c, size_t ldc, void* stream) {
+    if (!valid_fmt(fmt)) return fail(OZK_EPARAM, "slices_gemm: format must be DD, TD, QD or TS");
     if (m == 0 || l == 0 || n == 0) return fail(OZK_ESHAPE, "matrix dimensions must be positive");
     if (d < 1 || d > kMaxSplits) return fail(OZK_EPARAM, "slices_gemm: bad split count");
     if (ncb == 0 || nblk == 0 || ncb * nblk < n) return fail(OZK_ESHAPE, "slices_gemm: bad column blocks");
@@ -461,11 +472,11 @@ ozk_status ozk_slices_gemm_device(ozk_format fmt, size_t m, size_t l, size_t n,
     prob.ldc = ldc;
     if (pl.count == 0) {
         // nothing survives pruning: C = 0
-        for (size_t i = 0; i < m; ++i)
-            OZK_CUDA(cudaMemsetAsync(c + i * ldc * (int)fmt, 0, sizeof(double) * n * (int)fmt, st),
-                     "slices_gemm: zero");
+        OZK_CUDA(cudaMemset2DAsync(c, ldc * elem_bytes(fmt), 0, n * elem_bytes(fmt), m, st),
+                 "slices_gemm: zero");
     } else {
-        OZK_CUDA(launch_pair_gemm((int)fmt, kAccumulate, prob, pl, st, num_sms_cached()),
+        OZK_CUDA(launch_pair_gemm(words_of(fmt), kAccumulate, prob, pl, st, num_sms_cached(),
+                                  word_bytes_of(fmt)),
                  "slices_gemm");
     }
     OZK_CUDA(cudaStreamSynchronize(st), "slices_gemm");
@@ -518,7 +529,7 @@ ozk_status ozk_backend_gemm_device(size_t m, size_t l, size_t n, const double* a
     OZK_CUDA(cudaMemsetAsync(bt.p, 0, sizeof(double) * n * ldk, st), "backend_gemm");
     OZK_CUDA(cudaMemcpy2DAsync(ap.p, ldk * 8, a, l * 8, l * 8, m, cudaMemcpyDeviceToDevice, st),
              "backend_gemm: pad A");
-    OZK_CUDA(launch_transpose(1, b, n, bt.as<double>(), ldk, l, n, st), "backend_gemm: B^T");
+    OZK_CUDA(launch_transpose(1, 8, b, n, bt.p, ldk, l, n, st), "backend_gemm: B^T");
     GemmProblem prob{};
     prob.a = ap.as<double>();
     prob.lda = ldk;
@@ -567,11 +578,12 @@ ozk_status ozk_backend_gemm(size_t m, size_t l, size_t n, const double* a, const
 }
 
 ozk_status ozk_gen_eq1_device(ozk_format fmt, size_t rows, size_t cols, uint64_t seed,
-                              double* out, void* stream) {
-    if (!valid_fmt(fmt)) return fail(OZK_EPARAM, "gen_eq1: format must be DD, TD or QD");
+                              void* out, void* stream) {
+    if (!valid_fmt(fmt)) return fail(OZK_EPARAM, "gen_eq1: format must be DD, TD, QD or TS");
     if (rows == 0 || cols == 0) return fail(OZK_ESHAPE, "matrix dimensions must be positive");
     cudaStream_t st = (cudaStream_t)stream;
-    OZK_CUDA(launch_gen_eq1((int)fmt, out, rows * cols, seed, st), "gen_eq1");
+    OZK_CUDA(launch_gen_eq1(words_of(fmt), word_bytes_of(fmt), out, rows * cols, seed, st),
+             "gen_eq1");
     OZK_CUDA(cudaStreamSynchronize(st), "gen_eq1");
     return OZK_OK;
 }

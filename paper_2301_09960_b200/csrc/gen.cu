@@ -11,6 +11,8 @@
 // memory speed.  The K-word value is renormalised with the same K-word
 // "+ double" used by the split (kword.cuh), so inputs are in renormalised form.
 // Parity tests use the reference generator itself (oracle/), never this one.
+// TS (K = 3 binary32 words) rounds the TD value to three floats, as the C
+// oracle's ozk_oracle_gen_eq1_ts does for the parity inputs.
 #include "kword.cuh"
 #include "ozk_internal.cuh"
 
@@ -28,8 +30,8 @@ __device__ __forceinline__ double uniform53(uint64_t& s) {
     return (double)(splitmix(s) >> 11) * 0x1p-53;
 }
 
-template <int K>
-__global__ void gen_eq1_kernel(double* __restrict__ out, size_t count, uint64_t seed) {
+template <int K, bool TS>
+__global__ void gen_eq1_kernel(void* __restrict__ out, size_t count, uint64_t seed) {
     for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < count;
          idx += (size_t)gridDim.x * blockDim.x) {
         uint64_t s = seed * 0xd1b54a32d192ed03ull ^ (idx * 0x9e3779b97f4a7c15ull);
@@ -54,23 +56,47 @@ __global__ void gen_eq1_kernel(double* __restrict__ out, size_t count, uint64_t 
             kw_add<K>(y, p);
             kw_add<K>(y, e);
         }
-        double* o = out + idx * K;
+        if constexpr (TS) {
+            // TS: round the TD value to three binary32 words by successive
+            // leading-word extraction, then renormalise in TS arithmetic
+            const float w0 = (float)y[0];
+            const double r1 = __dadd_rn(__dsub_rn(y[0], (double)w0), y[1]);
+            const float w1 = (float)r1;
+            const double r2 = __dadd_rn(__dsub_rn(r1, (double)w1), y[2]);
+            const float w2 = (float)r2;
+            float t[3] = {0.f, 0.f, 0.f};
+            kw_add<3, float>(t, w0);
+            kw_add<3, float>(t, w1);
+            kw_add<3, float>(t, w2);
+            float* o = static_cast<float*>(out) + idx * 3;
+            o[0] = t[0];
+            o[1] = t[1];
+            o[2] = t[2];
+        } else {
+            double* o = static_cast<double*>(out) + idx * K;
 #pragma unroll
-        for (int k = 0; k < K; ++k) o[k] = y[k];
+            for (int k = 0; k < K; ++k) o[k] = y[k];
+        }
     }
 }
 
 } // namespace
 
-cudaError_t launch_gen_eq1(int K, double* out, size_t count, uint64_t seed, cudaStream_t st) {
+cudaError_t launch_gen_eq1(int K, int word_bytes, void* out, size_t count, uint64_t seed,
+                           cudaStream_t st) {
     if (count == 0) return cudaSuccess;
     const int threads = 256;
     size_t blocks = (count + threads - 1) / threads;
     if (blocks > 148 * 64) blocks = 148 * 64;
+    if (word_bytes == 4) {
+        if (K != 3) return cudaErrorInvalidValue;
+        gen_eq1_kernel<3, true><<<(unsigned)blocks, threads, 0, st>>>(out, count, seed);
+        return cudaGetLastError();
+    }
     switch (K) {
-    case 2: gen_eq1_kernel<2><<<(unsigned)blocks, threads, 0, st>>>(out, count, seed); break;
-    case 3: gen_eq1_kernel<3><<<(unsigned)blocks, threads, 0, st>>>(out, count, seed); break;
-    case 4: gen_eq1_kernel<4><<<(unsigned)blocks, threads, 0, st>>>(out, count, seed); break;
+    case 2: gen_eq1_kernel<2, false><<<(unsigned)blocks, threads, 0, st>>>(out, count, seed); break;
+    case 3: gen_eq1_kernel<3, false><<<(unsigned)blocks, threads, 0, st>>>(out, count, seed); break;
+    case 4: gen_eq1_kernel<4, false><<<(unsigned)blocks, threads, 0, st>>>(out, count, seed); break;
     default: return cudaErrorInvalidValue;
     }
     return cudaGetLastError();

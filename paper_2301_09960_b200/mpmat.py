@@ -17,7 +17,9 @@ this module                            reference
 =====================================  =====================================
 
 A K-word matrix ``DenseMatrix<MultiFloat<K>>`` is a float64 array of shape
-``(rows, cols, K)`` (its exact memory image).  numpy arrays and CPU torch
+``(rows, cols, K)`` (its exact memory image); a triple-single (TS) matrix is a
+float32 array of shape ``(rows, cols, 3)`` (TS is not in the reference; see
+include/ozk.h).  numpy arrays and CPU torch
 tensors go through the host-buffer C entry points; CUDA torch tensors go
 through the device entry points on torch's current stream.
 """
@@ -74,6 +76,7 @@ class SplitSide(enum.IntEnum):
 
 
 FORMATS = {2: "dd", 3: "td", 4: "qd"}
+OZK_TS = 0x103  # include/ozk.h
 
 
 def split_shift_bits(inner_dim: int) -> int:
@@ -129,20 +132,38 @@ def _is_cuda(x) -> bool:
     return torch is not None and isinstance(x, torch.Tensor) and x.is_cuda
 
 
+def _is_f32(x) -> bool:
+    if torch is not None and isinstance(x, torch.Tensor):
+        return x.dtype == torch.float32
+    return np.asarray(x).dtype == np.float32
+
+
 def _kword_shape(x) -> tuple[int, int, int]:
     if x.ndim != 3:
         raise shape_error("K-word matrix must have shape (rows, cols, K)")
     r, c, k = (int(s) for s in x.shape)
+    if _is_f32(x):
+        if k != 3:
+            raise param_error("binary32 words: only TS (K = 3) is supported")
+        return r, c, OZK_TS
     if k not in FORMATS:
         raise param_error("K must be 2 (DD), 3 (TD) or 4 (QD)")
     return r, c, k
 
 
-def _host(x) -> np.ndarray:
+def _words(fmt: int) -> int:
+    return 3 if fmt == OZK_TS else fmt
+
+
+def _dtype(fmt: int):
+    return np.float32 if fmt == OZK_TS else np.float64
+
+
+def _host(x, fmt: int | None = None) -> np.ndarray:
     if torch is not None and isinstance(x, torch.Tensor):
         x = x.detach().cpu().numpy()
-    a = np.ascontiguousarray(x, dtype=np.float64)
-    return a
+    dt = _dtype(fmt) if fmt is not None else (np.float32 if _is_f32(x) else np.float64)
+    return np.ascontiguousarray(x, dtype=dt)
 
 
 def _stream_handle() -> int:
@@ -161,24 +182,23 @@ def ozaki_gemm(a, b, d: int, backend=None, drop_threshold: float = 0.0):
     m, l, ka = _kword_shape(a)
     l2, n, kb = _kword_shape(b)
     if ka != kb:
-        raise param_error("ozaki_gemm: A and B must have the same K")
+        raise param_error("ozaki_gemm: A and B must have the same format")
     if l != l2:
         raise shape_error("ozaki_gemm: inner dimensions differ")
     prof = OzkProfile()
+    K = _words(ka)
     if _is_cuda(a) or _is_cuda(b):
         if not (_is_cuda(a) and _is_cuda(b)):
             raise param_error("ozaki_gemm: A and B must live on the same device")
         ad, bd = a.contiguous(), b.contiguous()
-        if ad.dtype != torch.float64 or bd.dtype != torch.float64:
-            raise param_error("ozaki_gemm: float64 tensors required")
-        c = torch.empty((m, n, ka), dtype=torch.float64, device=a.device)
+        c = torch.empty((m, n, K), dtype=ad.dtype, device=a.device)
         st = lib.ozk_ozaki_gemm_device(ka, m, l, n, ad.data_ptr(), bd.data_ptr(), int(d),
                                        float(drop_threshold), c.data_ptr(), _stream_handle(),
                                        ctypes.byref(prof))
         _raise(st)
         return c, OzakiProfile._of(prof)
-    ah, bh = _host(a), _host(b)
-    c = np.empty((m, n, ka), dtype=np.float64)
+    ah, bh = _host(a, ka), _host(b, ka)
+    c = np.empty((m, n, K), dtype=_dtype(ka))
     st = lib.ozk_ozaki_gemm(ka, m, l, n, ah.ctypes.data, bh.ctypes.data, int(d),
                             float(drop_threshold), c.ctypes.data, ctypes.byref(prof))
     _raise(st)
@@ -188,15 +208,16 @@ def ozaki_gemm(a, b, d: int, backend=None, drop_threshold: float = 0.0):
 def split_matrix(m, d: int, side: SplitSide) -> SplitSet:
     """split_matrix<K> (ozaki.hpp:74-147): pieces + K-word residual (host arrays)."""
     rows, cols, k = _kword_shape(m)
-    mh = _host(m)
+    mh = _host(m, k)
     dd = max(int(d), 1)
-    pieces = np.zeros((dd, rows, cols), dtype=np.float64)
+    pieces = np.zeros((dd, rows, cols), dtype=_dtype(k))
     resid = np.empty_like(mh)
     st = lib.ozk_split(k, rows, cols, mh.ctypes.data, int(d), int(side), pieces.ctypes.data,
                        resid.ctypes.data)
     _raise(st)
     return SplitSet(pieces=[pieces[i] for i in range(dd)], residual=resid, side=SplitSide(side),
-                    split_count=int(d), inner_dim=cols if side == SplitSide.rows else rows)
+                    split_count=int(d), inner_dim=cols if side == SplitSide.rows else rows,
+                    short_bits=24 if k == OZK_TS else 53)
 
 
 def gpu_backend():

@@ -16,6 +16,14 @@ static void run(std::size_t n, const double* x, const double* y, double* out) {
     }
 }
 
+extern "C" void kw_host_add_ts(std::size_t n, const float* x, const float* y, float* out) {
+    for (std::size_t i = 0; i < n; ++i) {
+        float w[3] = {x[3 * i], x[3 * i + 1], x[3 * i + 2]};
+        ozk::kw_add<3, float>(w, y[i]);
+        for (int k = 0; k < 3; ++k) out[3 * i + k] = w[k];
+    }
+}
+
 extern "C" int kw_host_add(int K, std::size_t n, const double* x, const double* y, double* out) {
     switch (K) {
     case 2: run<2>(n, x, y, out); return 0;
