@@ -209,7 +209,7 @@ def run_ours(args):
         import torch.distributed as dist
         dist.init_process_group("nccl")
         from paper_2301_09960_b200.sharded import ShardedOzaki
-        eng = ShardedOzaki(K, n, n, n, d, rank, world)
+        eng = ShardedOzaki(code, n, n, n, d, rank, world)
 
     def check(st):
         if st != 0:
@@ -368,11 +368,29 @@ def run_variant(lib, OzkProfile, fmt, n, peak, sh):
     torch.cuda.synchronize()
     t = e0.elapsed_time(e1) * 1e-3
     achieved = P * 2.0 * n ** 3 / prof.product_seconds / 1e12
-    return {"workload": f"{NAMES[fmt]} Ozaki GEMM n={n} D={d}", "value": round(2.0 * n ** 3 / t / 1e9, 3),
-            "unit": "GFLOP/s", "ms_per_step": round(1e3 * t, 3),
-            "split_ms": round(1e3 * prof.split_seconds, 3),
-            "slice_gemm_tflops": round(achieved, 3),
-            "slice_dgemm_frac_of_fp64_peak": round(achieved / peak, 4) if peak > 0 else None}
+    out = {"workload": f"{NAMES[fmt]} Ozaki GEMM n={n} D={d}",
+           "value": round(2.0 * n ** 3 / t / 1e9, 3),
+           "unit": "GFLOP/s", "ms_per_step": round(1e3 * t, 3),
+           "split_ms": round(1e3 * prof.split_seconds, 3),
+           "slice_gemm_tflops": round(achieved, 3),
+           "slice_dgemm_frac_of_fp64_peak": round(achieved / peak, 4) if peak > 0 else None}
+    if fmt == "ts":
+        # config 4 comparator: the direct triple-single GEMM kernel on the same inputs
+        def direct():
+            st = lib.ozk_ts_direct_gemm_device(n, n, n, A.data_ptr(), B.data_ptr(), C.data_ptr(),
+                                               sh)
+            if st != 0:
+                raise RuntimeError(lib.ozk_last_error().decode())
+        direct()
+        e0.record(stream)
+        direct()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        td = e0.elapsed_time(e1) * 1e-3
+        out["direct_ts_gemm"] = {"value": round(2.0 * n ** 3 / td / 1e9, 3), "unit": "GFLOP/s",
+                                 "ms_per_step": round(1e3 * td, 3),
+                                 "kernel": "ts_direct_kernel (FP32 SIMT, csrc/ts_direct.cu)"}
+    return out
 
 
 def main():

@@ -152,6 +152,16 @@ ozk_status ozk_pair_products_device(size_t m, size_t l, size_t n, const double* 
                                     const double* b_slices, int split_count, const int* pairs,
                                     int npairs, double* products, void* stream);
 
+/* ---- direct triple-single GEMM (BASELINE config 4 comparator) ------------- *
+ * C = A * B with every term accumulated in triple-single arithmetic, k
+ * ascending (no reference counterpart; the operation sequence is defined in
+ * oracle/ozk_oracle.c: ozk_oracle_ts_fma).  a: m x l, b: l x n, c: m x n,
+ * 3 binary32 words per element, row-major. */
+ozk_status ozk_ts_direct_gemm(size_t m, size_t l, size_t n, const float* a, const float* b,
+                              float* c);
+ozk_status ozk_ts_direct_gemm_device(size_t m, size_t l, size_t n, const float* a,
+                                     const float* b, float* c, void* stream);
+
 /* ---- utilities -------------------------------------------------------------- */
 
 /* Eq. (1)-distributed synthetic K-word matrix (rows*cols elements) in device

@@ -109,6 +109,7 @@ class Port(CpuOzaki):
         lib.ozk_oracle_ts_add_float.argtypes = [_fp, ctypes.c_float, _fp]
         lib.ozk_oracle_exact_sgemm.argtypes = [_c_size, _c_size, _c_size, _fp, _fp, _fp]
         lib.ozk_oracle_exact_sgemm.restype = ctypes.c_long
+        lib.ozk_oracle_ts_direct_gemm.argtypes = [_c_size, _c_size, _c_size, _fp, _fp, _fp]
         self.lib = lib
 
     def gen_eq1(self, K, m, n, seed):
@@ -243,6 +244,14 @@ class Port(CpuOzaki):
                                              r.ctypes.data)
             out[i] = r
         return out
+
+    def ts_direct_gemm(self, a, b):
+        a = np.ascontiguousarray(a, dtype=np.float32)
+        b = np.ascontiguousarray(b, dtype=np.float32)
+        c = np.empty((a.shape[0], b.shape[1], 3), dtype=np.float32)
+        self.lib.ozk_oracle_ts_direct_gemm(a.shape[0], a.shape[1], b.shape[1], a.ctypes.data,
+                                           b.ctypes.data, c.ctypes.data)
+        return c
 
     def exact_sgemm(self, a, b):
         a = np.ascontiguousarray(a, dtype=np.float32)

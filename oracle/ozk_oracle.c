@@ -876,3 +876,50 @@ int ozk_oracle_ozaki_gemm_ts(size_t m, size_t l, size_t n, const float* A, const
     free(bmax);
     return st;
 }
+
+/* ---- direct TS GEMM (the config-4 comparator; no reference counterpart) ----
+ * C(i,j) = sum_k A(i,k) * B(k,j) in triple-single arithmetic, k ascending,
+ * one multiply-accumulate per term (the paper's GPU "direct" TS GEMM,
+ * PAPER.md:280-312, TwoProd/TwoSum in binary32).  This is its definition; the
+ * GPU kernel (csrc/ts_direct.cu) replays it bit for bit.
+ *   product, truncated below level 2 (|term| ~ u^2 |a0 b0|):
+ *     (p00,e00) = TwoProd(a0,b0); (p01,e01) = TwoProd(a0,b1); (p10,e10) = TwoProd(a1,b0)
+ *     t2 = ((a0*b2 + a1*b1) + a2*b0) + (e01 + e10)
+ *   accumulate into (s0,s1,s2):
+ *     (s0,r0) = TwoSum(s0,p00); (q,r1) = TwoSum(p01,p10); (q,r2) = TwoSum(q,e00)
+ *     (s1,r3) = TwoSum(s1,q);   (s1,r4) = TwoSum(s1,r0)
+ *     s2 = (((s2 + t2) + r1) + r2) + (r3 + r4)
+ *   renormalise: (s1,s2) = TwoSum(s1,s2); (s0,s1) = TwoSum(s0,s1); (s1,s2) = TwoSum(s1,s2)
+ */
+void ozk_oracle_ts_fma(float* s, const float* a, const float* b) {
+    float p00 = a[0] * b[0], e00 = fmaf(a[0], b[0], -p00);
+    float p01 = a[0] * b[1], e01 = fmaf(a[0], b[1], -p01);
+    float p10 = a[1] * b[0], e10 = fmaf(a[1], b[0], -p10);
+    float t2 = ((a[0] * b[2] + a[1] * b[1]) + a[2] * b[0]) + (e01 + e10);
+    float s0, r0, q, r1, r2, s1, r3, r4;
+    two_sum_f(s[0], p00, &s0, &r0);
+    two_sum_f(p01, p10, &q, &r1);
+    two_sum_f(q, e00, &q, &r2);
+    two_sum_f(s[1], q, &s1, &r3);
+    two_sum_f(s1, r0, &s1, &r4);
+    float s2 = (((s[2] + t2) + r1) + r2) + (r3 + r4);
+    two_sum_f(s1, s2, &s1, &s2);
+    two_sum_f(s0, s1, &s0, &s1);
+    two_sum_f(s1, s2, &s1, &s2);
+    s[0] = s0;
+    s[1] = s1;
+    s[2] = s2;
+}
+
+void ozk_oracle_ts_direct_gemm(size_t m, size_t l, size_t n, const float* A, const float* B,
+                               float* C) {
+    for (size_t i = 0; i < m; ++i)
+        for (size_t j = 0; j < n; ++j) {
+            float s[3] = {0.0f, 0.0f, 0.0f};
+            for (size_t k = 0; k < l; ++k)
+                ozk_oracle_ts_fma(s, A + (i * l + k) * 3, B + (k * n + j) * 3);
+            C[(i * n + j) * 3 + 0] = s[0];
+            C[(i * n + j) * 3 + 1] = s[1];
+            C[(i * n + j) * 3 + 2] = s[2];
+        }
+}

@@ -18,9 +18,11 @@ from .mpmat import (  # noqa: F401
     shape_error,
     split_matrix,
     split_shift_bits,
+    ts_direct_gemm,
 )
 
 __all__ = [
     "OzakiProfile", "SplitSet", "SplitSide", "error", "exponent_ceil_log2", "gpu_backend",
     "ozaki_gemm", "param_error", "shape_error", "split_matrix", "split_shift_bits", "lib",
+    "ts_direct_gemm",
 ]

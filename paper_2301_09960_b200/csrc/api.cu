@@ -577,6 +577,36 @@ ozk_status ozk_backend_gemm(size_t m, size_t l, size_t n, const double* a, const
     return OZK_OK;
 }
 
+ozk_status ozk_ts_direct_gemm_device(size_t m, size_t l, size_t n, const float* a, const float* b,
+                                     float* c, void* stream) {
+    if (m == 0 || l == 0 || n == 0) return fail(OZK_ESHAPE, "matrix dimensions must be positive");
+    if (m > 0x7fffffffull || n > 0x7fffffffull || l > 0x7fffffffull)
+        return fail(OZK_ESHAPE, "ts_direct_gemm: dimension too large");
+    cudaStream_t st = (cudaStream_t)stream;
+    OZK_CUDA(launch_ts_direct(a, b, c, m, l, n, st), "ts_direct_gemm");
+    OZK_CUDA(cudaStreamSynchronize(st), "ts_direct_gemm");
+    return OZK_OK;
+}
+
+ozk_status ozk_ts_direct_gemm(size_t m, size_t l, size_t n, const float* a, const float* b,
+                              float* c) {
+    if (m == 0 || l == 0 || n == 0) return fail(OZK_ESHAPE, "matrix dimensions must be positive");
+    OwnStream os;
+    OZK_CUDA(os.create(), "ts_direct_gemm: stream");
+    DevBuf da, db, dc;
+    OZK_CUDA(da.alloc(12 * m * l, os.s), "ts_direct_gemm: A");
+    OZK_CUDA(db.alloc(12 * l * n, os.s), "ts_direct_gemm: B");
+    OZK_CUDA(dc.alloc(12 * m * n, os.s), "ts_direct_gemm: C");
+    OZK_CUDA(cudaMemcpyAsync(da.p, a, 12 * m * l, cudaMemcpyHostToDevice, os.s), "ts_direct: H2D");
+    OZK_CUDA(cudaMemcpyAsync(db.p, b, 12 * l * n, cudaMemcpyHostToDevice, os.s), "ts_direct: H2D");
+    if (ozk_status s = ozk_ts_direct_gemm_device(m, l, n, da.as<float>(), db.as<float>(),
+                                                 dc.as<float>(), os.s))
+        return s;
+    OZK_CUDA(cudaMemcpyAsync(c, dc.p, 12 * m * n, cudaMemcpyDeviceToHost, os.s), "ts_direct: D2H");
+    OZK_CUDA(cudaStreamSynchronize(os.s), "ts_direct_gemm");
+    return OZK_OK;
+}
+
 ozk_status ozk_gen_eq1_device(ozk_format fmt, size_t rows, size_t cols, uint64_t seed,
                               void* out, void* stream) {
     if (!valid_fmt(fmt)) return fail(OZK_EPARAM, "gen_eq1: format must be DD, TD, QD or TS");

@@ -65,6 +65,11 @@ cudaError_t launch_pair_gemm(int K, GemmMode mode, const GemmProblem& prob, cons
                              cudaStream_t st, int num_sms, int word_bytes = 8);
 
 // Device Eq. (1)-distributed K-word generator (synthetic bench inputs).
+// Direct triple-single GEMM (csrc/ts_direct.cu): a (m x l), b (l x n), c (m x n),
+// 3 binary32 words per element.
+cudaError_t launch_ts_direct(const float* a, const float* b, float* c, size_t m, size_t l,
+                             size_t n, cudaStream_t st);
+
 // word_bytes = 4 selects TS (K = 3 binary32 words).
 cudaError_t launch_gen_eq1(int K, int word_bytes, void* out, size_t count, uint64_t seed,
                            cudaStream_t st);

@@ -244,3 +244,23 @@ def gpu_backend():
 
     backend._ozk_gpu = True
     return backend
+
+
+def ts_direct_gemm(a, b):
+    """Direct triple-single GEMM (config-4 comparator; csrc/ts_direct.cu)."""
+    m, l, fa = _kword_shape(a)
+    l2, n, fb = _kword_shape(b)
+    if fa != OZK_TS or fb != OZK_TS:
+        raise param_error("ts_direct_gemm: float32 (rows, cols, 3) TS matrices required")
+    if l != l2:
+        raise shape_error("ts_direct_gemm: inner dimensions differ")
+    if _is_cuda(a) and _is_cuda(b):
+        ad, bd = a.contiguous(), b.contiguous()
+        c = torch.empty((m, n, 3), dtype=torch.float32, device=a.device)
+        _raise(lib.ozk_ts_direct_gemm_device(m, l, n, ad.data_ptr(), bd.data_ptr(), c.data_ptr(),
+                                             _stream_handle()))
+        return c
+    ah, bh = _host(a, OZK_TS), _host(b, OZK_TS)
+    c = np.empty((m, n, 3), dtype=np.float32)
+    _raise(lib.ozk_ts_direct_gemm(m, l, n, ah.ctypes.data, bh.ctypes.data, c.ctypes.data))
+    return c

@@ -55,9 +55,12 @@ def pruned_pairs(d, amax, bmax, drop) -> list[tuple[int, int]]:
     return out
 
 
+OZK_TS = 0x103
+
+
 @dataclass
 class ShardPlan:
-    K: int
+    K: int          # ozk_format code: 2/3/4 (DD/TD/QD) or 0x103 (TS)
     m: int
     l: int
     n: int
@@ -76,6 +79,10 @@ class ShardPlan:
     def rows_local(self) -> int:
         return self.r1 - self.r0
 
+    @property
+    def words(self) -> int:
+        return 3 if self.K == OZK_TS else self.K
+
 
 class GpuOps:
     """libozk.so device entry points on torch CUDA tensors (current stream)."""
@@ -92,8 +99,8 @@ class GpuOps:
     def _stream(self):
         return torch.cuda.current_stream().cuda_stream
 
-    def zeros(self, shape):
-        return torch.zeros(shape, dtype=torch.float64, device=self.device)
+    def zeros(self, shape, dtype=torch.float64):
+        return torch.zeros(shape, dtype=dtype, device=self.device)
 
     def split(self, K, mat, rows, cols, ld, d, side, out, pmax):
         """mat: tensor view whose data_ptr is element (0,0); row stride ld elements.
@@ -122,7 +129,8 @@ class ShardedOzaki:
         self.sa = self.ops.zeros((d, max(p.rows_local, 1), p.ld))
         self.sb = self.ops.zeros((d, p.ncb, p.ld))
         self.sb_all = self.ops.zeros((world, d, p.ncb, p.ld))
-        self.c = self.ops.zeros((max(p.rows_local, 1), n, K))
+        self.c = self.ops.zeros((max(p.rows_local, 1), n, p.words),
+                                dtype=torch.float32 if K == OZK_TS else torch.float64)
         self.pmax = self.ops.zeros((2, d)) if self.drop > 0.0 else None
         self.timing = hasattr(self.ops, "device") and self.ops.device.type == "cuda"
 

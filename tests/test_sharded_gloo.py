@@ -23,8 +23,8 @@ class OracleOps:
         self.port = port
         self.device = torch.device("cpu")
 
-    def zeros(self, shape):
-        return torch.zeros(shape, dtype=torch.float64)
+    def zeros(self, shape, dtype=torch.float64):
+        return torch.zeros(shape, dtype=dtype)
 
     def split(self, K, mat, rows, cols, ld, d, side, out, pmax):
         arr = mat.contiguous().numpy().reshape(rows, cols, K)

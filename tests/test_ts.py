@@ -155,3 +155,26 @@ def test_ts_accuracy_bound_gpu(ozk, port):
     err = ex.componentwise_ulp_error(got.astype(np.float64), a.astype(np.float64),
                                      b.astype(np.float64), ref, -72)
     assert err <= 4.0
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("m,l,n", [(1, 1, 1), (5, 7, 4), (64, 64, 64), (65, 33, 130),
+                                   (200, 300, 100)])
+def test_ts_direct_gemm_bitexact(ozk, port, m, l, n):
+    """K5 direct TS GEMM replays ozk_oracle_ts_fma bit for bit."""
+    a = port.gen_eq1_ts(m, l, 30 + m)
+    b = port.gen_eq1_ts(l, n, 31 + m)
+    want = port.ts_direct_gemm(a, b)
+    got = ozk.ts_direct_gemm(a, b)
+    assert np.array_equal(fbits(got), fbits(want))
+
+
+@pytest.mark.gpu
+def test_ts_direct_accuracy(ozk, port):
+    a = port.gen_eq1_ts(32, 128, 5)
+    b = port.gen_eq1_ts(128, 24, 6)
+    ref = ex.exact_gemm(a.astype(np.float64), b.astype(np.float64))
+    got = ozk.ts_direct_gemm(a, b)
+    err = ex.componentwise_ulp_error(got.astype(np.float64), a.astype(np.float64),
+                                     b.astype(np.float64), ref, -72)
+    assert err <= 16.0  # grows ~linearly with l; 2.4 at l = 64 on the CPU restatement
