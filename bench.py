@@ -53,6 +53,8 @@ def parse():
     p.add_argument("--d", type=int, default=None)
     p.add_argument("--variants", default="dd,qd,ts",
                    help="other formats timed (1 step each) and reported under 'variants'")
+    p.add_argument("--spread", type=int, default=0,
+                   help="config 5: scale every element by 2^U[-s,s] (ill-conditioned inputs)")
     p.add_argument("--cpu-sample", type=int, default=1024,
                    help="rows/cols of the CPU baseline sub-GEMM (inner dim stays n)")
     p.add_argument("--no-cpu-baseline", action="store_true")
@@ -119,7 +121,7 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 # CPU arms (oracle/: the reference compiled in place, else the C restatement)
 # ---------------------------------------------------------------------------
-def cpu_sample_rate(K: int, d: int, n: int, r: int, reps: int = 1):
+def cpu_sample_rate(K: int, d: int, n: int, r: int, reps: int = 1, spread: int = 0):
     """Reference CPU Ozaki on an r x n . n x r sub-GEMM (same inner dimension,
     so the same sigma, slice widths and D as the n x n workload)."""
     import numpy as np
@@ -131,8 +133,13 @@ def cpu_sample_rate(K: int, d: int, n: int, r: int, reps: int = 1):
         cores = cpu.set_threads(cores)
     else:
         cores = 1  # the C restatement is single-threaded
-    a = cpu.gen_eq1(K, r, n, 1)
-    b = cpu.gen_eq1(K, n, r, 2)
+    if spread:
+        port = oracle.load_port()
+        a = port.gen_spread(K, r, n, 1, spread)
+        b = port.gen_spread(K, n, r, 2, spread)
+    else:
+        a = cpu.gen_eq1(K, r, n, 1)
+        b = cpu.gen_eq1(K, n, r, 2)
     best = None
     for _ in range(reps):
         t0 = time.perf_counter()
@@ -155,10 +162,10 @@ def run_reference(args):
     d = args.d or d0
     n, r = args.n, args.cpu_sample
     for _ in range(args.warmup):
-        cpu_sample_rate(K, d, n, r)
+        cpu_sample_rate(K, d, n, r, spread=args.spread)
     rates, times = [], []
     for _ in range(args.steps):
-        rate, dt, cores, kind = cpu_sample_rate(K, d, n, r)
+        rate, dt, cores, kind = cpu_sample_rate(K, d, n, r, spread=args.spread)
         rates.append(rate)
         times.append(dt)
     value = statistics.mean(rates)
@@ -180,7 +187,13 @@ def run_reference(args):
 
 
 def config_of(args, K, d, n):
-    return {"workload": f"{NAMES[args.format]} Ozaki GEMM n={n} D={d} (BASELINE config 3)",
+    wl = f"{NAMES[args.format]} Ozaki GEMM n={n} D={d} (BASELINE config 3)"
+    if args.spread:
+        wl = (f"ill-conditioned {NAMES[args.format]} Ozaki GEMM n={n} D={d}, exponent spread "
+              f"+-{args.spread} (BASELINE config 5)")
+    elif args.format == "ts":
+        wl = f"TS Ozaki GEMM n={n} D={d} (BASELINE config 4)"
+    return {"workload": wl, "spread": args.spread,
             "format": args.format, "n": n, "split_count": d, "pairs": d * (d + 1) // 2,
             "parallelism": f"C block-rows x{args.gpus}" if args.gpus > 1 else "single GPU",
             "l2": "no flush: A, B and C are each > 126 MB L2 (K*8*n^2 bytes)"}
@@ -218,8 +231,8 @@ def run_ours(args):
     # synthetic Eq. (1) inputs generated on device (outside the timed region)
     A = torch.empty((n, n, K), dtype=wdt, device="cuda")
     B = torch.empty((n, n, K), dtype=wdt, device="cuda")
-    check(lib.ozk_gen_eq1_device(code, n, n, 1, A.data_ptr(), sh))
-    check(lib.ozk_gen_eq1_device(code, n, n, 2, B.data_ptr(), sh))
+    check(lib.ozk_gen_spread_device(code, n, n, 1, args.spread, A.data_ptr(), sh))
+    check(lib.ozk_gen_spread_device(code, n, n, 2, args.spread, B.data_ptr(), sh))
 
     peak = lib.ozk_probe_dmma_tflops(20000, sh)
 
@@ -277,7 +290,7 @@ def run_ours(args):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline and args.format != "ts":
-        rate, dt, cores, kind = cpu_sample_rate(K, d, n, args.cpu_sample)
+        rate, dt, cores, kind = cpu_sample_rate(K, d, n, args.cpu_sample, spread=args.spread)
         cpu = {"value": round(rate, 4), "unit": "GFLOP/s", "cores": cores, "kind": kind,
                "sample": f"{NAMES[args.format]} Ozaki sub-GEMM {args.cpu_sample}x{n} . "
                          f"{n}x{args.cpu_sample}, D={d}, one call ({dt:.2f} s)"}

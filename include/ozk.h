@@ -170,6 +170,11 @@ ozk_status ozk_ts_direct_gemm_device(size_t m, size_t l, size_t n, const float* 
 ozk_status ozk_gen_eq1_device(ozk_format fmt, size_t rows, size_t cols, uint64_t seed,
                               void* out, void* stream);
 
+/* Ill-conditioned variant (BASELINE config 5): the same elements scaled by
+ * 2^e, e uniform on [-spread, spread] (0 <= spread <= 400). */
+ozk_status ozk_gen_spread_device(ozk_format fmt, size_t rows, size_t cols, uint64_t seed,
+                                 int spread, void* out, void* stream);
+
 /* FP64 tensor-pipe (DMMA) ceiling of the current device in TFLOP/s, measured by a
  * register-resident mma.sync.m8n8k4.f64 loop on every SM (the roofline
  * denominator for the slice GEMMs).  Returns < 0 on failure. */

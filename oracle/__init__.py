@@ -110,11 +110,19 @@ class Port(CpuOzaki):
         lib.ozk_oracle_exact_sgemm.argtypes = [_c_size, _c_size, _c_size, _fp, _fp, _fp]
         lib.ozk_oracle_exact_sgemm.restype = ctypes.c_long
         lib.ozk_oracle_ts_direct_gemm.argtypes = [_c_size, _c_size, _c_size, _fp, _fp, _fp]
+        lib.ozk_oracle_gen_spread.argtypes = [ctypes.c_int, _c_size, _c_size, ctypes.c_uint64,
+                                              ctypes.c_int, _dp]
         self.lib = lib
 
     def gen_eq1(self, K, m, n, seed):
         out = np.empty((m, n, K), dtype=np.float64)
         self.lib.ozk_oracle_gen_eq1(K, m, n, seed, _ptr(out))
+        return out
+
+    def gen_spread(self, K, m, n, seed, spread):
+        """Ill-conditioned inputs (config 5): Eq. (1) values scaled by 2^U[-s, s]."""
+        out = np.empty((m, n, K), dtype=np.float64)
+        self.lib.ozk_oracle_gen_spread(K, m, n, seed, spread, _ptr(out))
         return out
 
     def xoshiro(self, seed, count):

@@ -923,3 +923,26 @@ void ozk_oracle_ts_direct_gemm(size_t m, size_t l, size_t n, const float* A, con
             C[(i * n + j) * 3 + 2] = s[2];
         }
 }
+
+/* ---- ill-conditioned inputs (BASELINE config 5) -----------------------------
+ * Eq. (1) elements (gen.hpp:20-34, same per-element draws) each scaled by 2^e,
+ * e uniform on [-spread, spread] drawn from the same stream right after the
+ * element's Eq. (1) draws -- the exponent-spread idea of random_scaled
+ * (proj/tests/acceptance.cpp:53-58) applied to K-word values.  Scaling by a
+ * power of two is exact, so every element keeps its full K*53-bit significand
+ * while rows span up to 2*spread binades. */
+void ozk_oracle_gen_spread(int K, size_t m, size_t n, uint64_t seed, int spread, double* out) {
+    xoshiro rng;
+    xo_seed(&rng, seed);
+    double comp[OZK_MAXK], ru[OZK_MAXK], t[OZK_MAXK];
+    for (size_t idx = 0; idx < m * n; ++idx) {
+        for (int k = 0; k < K; ++k) comp[k] = scalbn(xo_uniform(&rng), -53 * k);
+        renormalize(K, comp, K, ru);
+        double scale = exp(xo_normal(&rng));
+        ozk_oracle_mf_add_double(K, ru, -0.5, t);
+        double* o = out + idx * (size_t)K;
+        mf_mul_double(K, t, scale, o);
+        int e = (int)(xo_next(&rng) % (uint64_t)(2 * spread + 1)) - spread;
+        for (int k = 0; k < K; ++k) o[k] = scalbn(o[k], e);
+    }
+}

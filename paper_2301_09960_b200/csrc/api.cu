@@ -607,15 +607,21 @@ ozk_status ozk_ts_direct_gemm(size_t m, size_t l, size_t n, const float* a, cons
     return OZK_OK;
 }
 
+ozk_status ozk_gen_spread_device(ozk_format fmt, size_t rows, size_t cols, uint64_t seed,
+                                 int spread, void* out, void* stream) {
+    if (!valid_fmt(fmt)) return fail(OZK_EPARAM, "gen: format must be DD, TD, QD or TS");
+    if (rows == 0 || cols == 0) return fail(OZK_ESHAPE, "matrix dimensions must be positive");
+    if (spread < 0 || spread > 400) return fail(OZK_EPARAM, "gen: spread must be in [0, 400]");
+    cudaStream_t st = (cudaStream_t)stream;
+    OZK_CUDA(launch_gen_eq1(words_of(fmt), word_bytes_of(fmt), out, rows * cols, seed, spread, st),
+             "gen");
+    OZK_CUDA(cudaStreamSynchronize(st), "gen");
+    return OZK_OK;
+}
+
 ozk_status ozk_gen_eq1_device(ozk_format fmt, size_t rows, size_t cols, uint64_t seed,
                               void* out, void* stream) {
-    if (!valid_fmt(fmt)) return fail(OZK_EPARAM, "gen_eq1: format must be DD, TD, QD or TS");
-    if (rows == 0 || cols == 0) return fail(OZK_ESHAPE, "matrix dimensions must be positive");
-    cudaStream_t st = (cudaStream_t)stream;
-    OZK_CUDA(launch_gen_eq1(words_of(fmt), word_bytes_of(fmt), out, rows * cols, seed, st),
-             "gen_eq1");
-    OZK_CUDA(cudaStreamSynchronize(st), "gen_eq1");
-    return OZK_OK;
+    return ozk_gen_spread_device(fmt, rows, cols, seed, 0, out, stream);
 }
 
 }  // extern "C"

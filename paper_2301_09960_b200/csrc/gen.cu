@@ -31,7 +31,7 @@ __device__ __forceinline__ double uniform53(uint64_t& s) {
 }
 
 template <int K, bool TS>
-__global__ void gen_eq1_kernel(void* __restrict__ out, size_t count, uint64_t seed) {
+__global__ void gen_eq1_kernel(void* __restrict__ out, size_t count, uint64_t seed, int spread) {
     for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < count;
          idx += (size_t)gridDim.x * blockDim.x) {
         uint64_t s = seed * 0xd1b54a32d192ed03ull ^ (idx * 0x9e3779b97f4a7c15ull);
@@ -55,6 +55,12 @@ __global__ void gen_eq1_kernel(void* __restrict__ out, size_t count, uint64_t se
             const double e = __fma_rn(x[k], scale, -p);
             kw_add<K>(y, p);
             kw_add<K>(y, e);
+        }
+        if (spread > 0) {
+            // ill-conditioned inputs (config 5): exact scaling by 2^U[-spread, spread]
+            const int ex = (int)(splitmix(s) % (uint64_t)(2 * spread + 1)) - spread;
+#pragma unroll
+            for (int k = 0; k < K; ++k) y[k] = scalbn(y[k], ex);
         }
         if constexpr (TS) {
             // TS: round the TD value to three binary32 words by successive
@@ -83,20 +89,20 @@ __global__ void gen_eq1_kernel(void* __restrict__ out, size_t count, uint64_t se
 } // namespace
 
 cudaError_t launch_gen_eq1(int K, int word_bytes, void* out, size_t count, uint64_t seed,
-                           cudaStream_t st) {
+                           int spread, cudaStream_t st) {
     if (count == 0) return cudaSuccess;
     const int threads = 256;
     size_t blocks = (count + threads - 1) / threads;
     if (blocks > 148 * 64) blocks = 148 * 64;
     if (word_bytes == 4) {
         if (K != 3) return cudaErrorInvalidValue;
-        gen_eq1_kernel<3, true><<<(unsigned)blocks, threads, 0, st>>>(out, count, seed);
+        gen_eq1_kernel<3, true><<<(unsigned)blocks, threads, 0, st>>>(out, count, seed, spread);
         return cudaGetLastError();
     }
     switch (K) {
-    case 2: gen_eq1_kernel<2, false><<<(unsigned)blocks, threads, 0, st>>>(out, count, seed); break;
-    case 3: gen_eq1_kernel<3, false><<<(unsigned)blocks, threads, 0, st>>>(out, count, seed); break;
-    case 4: gen_eq1_kernel<4, false><<<(unsigned)blocks, threads, 0, st>>>(out, count, seed); break;
+    case 2: gen_eq1_kernel<2, false><<<(unsigned)blocks, threads, 0, st>>>(out, count, seed, spread); break;
+    case 3: gen_eq1_kernel<3, false><<<(unsigned)blocks, threads, 0, st>>>(out, count, seed, spread); break;
+    case 4: gen_eq1_kernel<4, false><<<(unsigned)blocks, threads, 0, st>>>(out, count, seed, spread); break;
     default: return cudaErrorInvalidValue;
     }
     return cudaGetLastError();

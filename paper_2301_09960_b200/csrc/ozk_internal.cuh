@@ -71,7 +71,8 @@ cudaError_t launch_ts_direct(const float* a, const float* b, float* c, size_t m,
                              size_t n, cudaStream_t st);
 
 // word_bytes = 4 selects TS (K = 3 binary32 words).
+// spread > 0 scales every element by 2^U[-spread, spread] (config 5 inputs).
 cudaError_t launch_gen_eq1(int K, int word_bytes, void* out, size_t count, uint64_t seed,
-                           cudaStream_t st);
+                           int spread, cudaStream_t st);
 
 } // namespace ozk

@@ -307,3 +307,28 @@ def test_repeat_runs_race_free(ozk, cpu, K, m, l, n, d):
     for _ in range(3):
         got, _ = ozk.ozaki_gemm(a, b, d)
         assert_bitwise(got, want, f"K={K} {m}x{l}x{n} D={d}")
+
+
+@pytest.mark.parametrize("K,m,l,n,d,spread", [(2, 48, 96, 40, 10, 40), (4, 33, 70, 20, 16, 60),
+                                              (3, 64, 64, 64, 14, 100), (2, 130, 257, 129, 12, 250)])
+def test_ill_conditioned_bitexact(ozk, cpu, port, K, m, l, n, d, spread):
+    """BASELINE config 5 inputs (exponent spread up to 2*spread binades):
+    C bit-exact vs the reference, which handles them the same way."""
+    a = port.gen_spread(K, m, l, 60 + K, spread)
+    b = port.gen_spread(K, l, n, 61 + K, spread)
+    want = cpu.ozaki_gemm(K, a, b, d)
+    got, _ = ozk.ozaki_gemm(a, b, d)
+    assert_bitwise(got, want, f"spread={spread} K={K} D={d}")
+
+
+@pytest.mark.parametrize("K,dmax,ulp", [(2, 12, -106), (3, 16, -159), (4, 20, -212)])
+def test_accuracy_t2_bound(ozk, port, K, dmax, ulp):
+    """Tier T2: at saturation |C - C_exact| <= 4 u_L (|A||B|)_ij (SURVEY §8 parity
+    tiers; exact big-int oracle), including ill-conditioned (spread) inputs."""
+    import oracle.exact as ex
+    for spread in (0, 30):
+        a = port.gen_spread(K, 20, 64, 7, spread)
+        b = port.gen_spread(K, 64, 16, 8, spread)
+        ref = ex.exact_gemm(a, b)
+        got, _ = ozk.ozaki_gemm(a, b, dmax)
+        assert ex.componentwise_ulp_error(got, a, b, ref, ulp) <= 4.0
