@@ -326,8 +326,29 @@ pair_gemm_kernel(const __grid_constant__ TmaMaps maps, const __grid_constant__ P
             }
 
             // ---------------- epilogue for pair p of this tile ----------------
-#pragma unroll
+            // Two code shapes, chosen per format from B200 measurements
+            // (tools/exp_epilogue.py, profiles/r01_ncu_summary.md):
+            //  * fully unrolled over the 8 fragment rows: all C addresses are
+            //    compile-time offsets of one base, so the compiler batches the
+            //    loads of every row ahead of the K-word math (shortest epilogue
+            //    latency).  Best for DD: 95.0 % of the DMMA ceiling vs 90.3 %.
+            //  * runtime loop over the rows, the row's 8 accumulators picked out
+            //    with predicated selects: 5-8x less code; the unrolled K >= 3
+            //    epilogues (13.5K-18K SASS instructions) thrash the instruction
+            //    cache.  Best for TD (87.3 % vs 84.5-87.7 %), QD (85.0 % vs
+            //    80.1 %) and TS.
+            constexpr bool kLoopRows = K >= 3;
+#pragma unroll(kLoopRows ? 1 : 8)
             for (int mf = 0; mf < 8; ++mf) {
+                if (!((rmask >> mf) & 1u)) continue;
+                double y[8];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    double v = acc[0][q >> 1][q & 1];
+#pragma unroll
+                    for (int r = 1; r < 8; ++r) v = (mf == r) ? acc[r][q >> 1][q & 1] : v;
+                    y[q] = v;
+                }
                 const size_t row = row0 + mf * 8;
                 if constexpr (MODE == kAccumulate) {
                     // batch: load the 8 K-word elements of this row first
@@ -335,18 +356,22 @@ pair_gemm_kernel(const __grid_constant__ TmaMaps maps, const __grid_constant__ P
                     W* cp = static_cast<W*>(prob.c) + (row * prob.ldc + col0) * K;
 #pragma unroll
                     for (int q = 0; q < 8; ++q) {
-                        const bool ok = (rmask >> mf) & (cmask >> q) & 1u;
+                        const bool ok = (cmask >> q) & 1u;
                         const int off = ((q >> 1) * 8 + (q & 1)) * K;
 #pragma unroll
                         for (int k = 0; k < K; ++k) w[q][k] = (ok && p > 0) ? cp[off + k] : W(0);
                     }
+#ifdef OZK_EXPERIMENT_TRIVIAL_EPILOGUE
 #pragma unroll
-                    for (int q = 0; q < 8; ++q) kw_add<K>(w[q], (W)acc[mf][q >> 1][q & 1]);
+                    for (int q = 0; q < 8; ++q) w[q][0] = w[q][0] + (W)y[q];
+#else
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) kw_add<K>(w[q], (W)y[q]);
+#endif
 #pragma unroll
                     for (int q = 0; q < 8; ++q) {
-                        const bool ok = (rmask >> mf) & (cmask >> q) & 1u;
                         const int off = ((q >> 1) * 8 + (q & 1)) * K;
-                        if (ok) {
+                        if ((cmask >> q) & 1u) {
 #pragma unroll
                             for (int k = 0; k < K; ++k) cp[off + k] = w[q][k];
                         }
@@ -354,19 +379,20 @@ pair_gemm_kernel(const __grid_constant__ TmaMaps maps, const __grid_constant__ P
                 } else {
 #pragma unroll
                     for (int q = 0; q < 8; ++q) {
-                        if (!((rmask >> mf) & (cmask >> q) & 1u)) continue;
+                        if (!((cmask >> q) & 1u)) continue;
                         const size_t col = col0 + (q >> 1) * 8 + (q & 1);
-                        const double y = acc[mf][q >> 1][q & 1];
                         double* cd = static_cast<double*>(prob.c);
                         if constexpr (MODE == kStorePlain)
-                            cd[row * prob.ldc + col] = y;
+                            cd[row * prob.ldc + col] = y[q];
                         else
-                            cd[(size_t)p * prob.c_pair_stride + row * prob.ldc + col] = y;
+                            cd[(size_t)p * prob.c_pair_stride + row * prob.ldc + col] = y[q];
                     }
                 }
+            }
+#pragma unroll
+            for (int mf = 0; mf < 8; ++mf)
 #pragma unroll
                 for (int nf = 0; nf < 4; ++nf) acc[mf][nf][0] = acc[mf][nf][1] = 0.0;
-            }
         }
     }
     // group 0 with fewer k-blocks than the kick point still has to release group 1
