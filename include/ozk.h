@@ -152,6 +152,21 @@ ozk_status ozk_pair_products_device(size_t m, size_t l, size_t n, const double* 
                                     const double* b_slices, int split_count, const int* pairs,
                                     int npairs, double* products, void* stream);
 
+/* ---- blocked-LU trailing update ------------------- *
+ * A22 := A22 - L21 * U12 exactly as the reference's blocked_lu does it
+ * (proj/include/mpmat/lu.hpp:104-124): the product by ozaki_gemm with
+ * split_count slices, then A22(i,j) -= update(i,j) with MultiFloat<K>
+ * subtraction (multifloat.hpp:288,387).  L21: tm x pw (row stride ldl), U12:
+ * pw x tn (row stride ldu), A22: tm x tn (row stride lda), all in elements,
+ * so the blocks can live inside the full matrix.  DD/TD/QD only. */
+ozk_status ozk_lu_trailing_update(ozk_format fmt, size_t tm, size_t pw, size_t tn,
+                                  const void* l21, size_t ldl, const void* u12, size_t ldu,
+                                  void* a22, size_t lda, int split_count);
+ozk_status ozk_lu_trailing_update_device(ozk_format fmt, size_t tm, size_t pw, size_t tn,
+                                         const void* l21, size_t ldl, const void* u12,
+                                         size_t ldu, void* a22, size_t lda, int split_count,
+                                         void* stream);
+
 /* ---- direct triple-single GEMM (BASELINE config 4 comparator) ------------- *
  * C = A * B with every term accumulated in triple-single arithmetic, k
  * ascending (no reference counterpart; the operation sequence is defined in

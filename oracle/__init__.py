@@ -287,6 +287,8 @@ class Ref(CpuOzaki):
         lib.ref_gemm_simple.argtypes = [ctypes.c_int, _c_size, _c_size, _c_size, _dp, _dp, _dp]
         lib.ref_mf_add_double.argtypes = [ctypes.c_int, _c_size, _dp, _dp, _dp]
         lib.ref_split_shift_bits.argtypes = [_c_size]
+        lib.ref_lu_update.argtypes = [ctypes.c_int, _c_size, _c_size, _c_size, _dp, _dp, _dp,
+                                      ctypes.c_int]
         lib.ref_exponent_ceil_log2.argtypes = [ctypes.c_double]
         self.lib = lib
 
@@ -352,6 +354,17 @@ class Ref(CpuOzaki):
 
     def exponent_ceil_log2(self, x):
         return self.lib.ref_exponent_ceil_log2(x)
+
+    def lu_update(self, K, l21, u12, a22, d):
+        """lu.hpp:104-124 trailing update on dense blocks (returns the new A22)."""
+        l21 = np.ascontiguousarray(l21, dtype=np.float64)
+        u12 = np.ascontiguousarray(u12, dtype=np.float64)
+        out = np.array(a22, dtype=np.float64, copy=True, order="C")
+        st = self.lib.ref_lu_update(K, l21.shape[0], l21.shape[1], u12.shape[1], _ptr(l21),
+                                    _ptr(u12), _ptr(out), d)
+        if st:
+            raise OracleError(st, "lu_update")
+        return out
 
     def split_shift_bits(self, inner, short_bits=53):
         assert short_bits == 53

@@ -108,6 +108,33 @@ void add_k(std::size_t count, const double* x, const double* y, double* out) {
     }
 }
 
+template <int K>
+void add_mf_k(std::size_t count, const double* x, const double* y, double* out) {
+    for (std::size_t i = 0; i < count; ++i) {
+        std::array<double, K> a, b;
+        for (int k = 0; k < K; ++k) {
+            a[k] = x[i * K + k];
+            b[k] = y[i * K + k];
+        }
+        auto r = MultiFloat<K>::from_components_unchecked(a) +
+                 MultiFloat<K>::from_components_unchecked(b);
+        for (int k = 0; k < K; ++k) out[i * K + k] = r.component(k);
+    }
+}
+
+template <int K>
+int lu_update_k(std::size_t tm, std::size_t pw, std::size_t tn, const double* l21,
+                const double* u12, double* a22, int d) {
+    auto L = load<K>(tm, pw, l21);
+    auto U = load<K>(pw, tn, u12);
+    auto W = load<K>(tm, tn, a22);
+    auto update = ozaki_gemm(L, U, d, reference_backend()).first;
+    for (std::size_t i = 0; i < tm; ++i)
+        for (std::size_t j = 0; j < tn; ++j) W(i, j) -= update(i, j);
+    store<K>(W, a22);
+    return 0;
+}
+
 #define DISPATCH_K(K, FN, ...)                                                         \
     switch (K) {                                                                       \
     case 2: return FN<2>(__VA_ARGS__);                                                 \
@@ -188,6 +215,28 @@ int ref_mf_add_double(int K, std::size_t count, const double* x, const double* y
     case 3: add_k<3>(count, x, y, out); return 0;
     case 4: add_k<4>(count, x, y, out); return 0;
     default: return 2;
+    }
+}
+
+// MultiFloat<K> + MultiFloat<K> on `count` pairs (multifloat.hpp:271-286).
+int ref_mf_add_mf(int K, std::size_t count, const double* x, const double* y, double* out) {
+    switch (K) {
+    case 2: add_mf_k<2>(count, x, y, out); return 0;
+    case 3: add_mf_k<3>(count, x, y, out); return 0;
+    case 4: add_mf_k<4>(count, x, y, out); return 0;
+    default: return 2;
+    }
+}
+
+// The blocked-LU trailing update exactly as the reference performs it
+// (lu.hpp:104-124): update = ozaki_gemm(l21, u12, d, reference_backend()).first;
+// a22(i, j) -= update(i, j).  l21: tm x pw, u12: pw x tn, a22: tm x tn (dense).
+int ref_lu_update(int K, std::size_t tm, std::size_t pw, std::size_t tn, const double* l21,
+                  const double* u12, double* a22, int d) {
+    try {
+        DISPATCH_K(K, lu_update_k, tm, pw, tn, l21, u12, a22, d);
+    } catch (const std::exception& e) {
+        return status_of(e);
     }
 }
 

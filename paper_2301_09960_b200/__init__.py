@@ -13,6 +13,7 @@ from .mpmat import (  # noqa: F401
     error,
     exponent_ceil_log2,
     gpu_backend,
+    lu_trailing_update,
     ozaki_gemm,
     param_error,
     shape_error,
@@ -24,5 +25,5 @@ from .mpmat import (  # noqa: F401
 __all__ = [
     "OzakiProfile", "SplitSet", "SplitSide", "error", "exponent_ceil_log2", "gpu_backend",
     "ozaki_gemm", "param_error", "shape_error", "split_matrix", "split_shift_bits", "lib",
-    "ts_direct_gemm",
+    "ts_direct_gemm", "lu_trailing_update",
 ]

@@ -168,8 +168,11 @@ struct Timer {
     }
 };
 
-ozk_status ozaki_device_impl(int fmt, size_t m, size_t l, size_t n, const void* a, const void* b,
-                             int d, double drop, void* c, cudaStream_t st, ozk_profile* prof) {
+// C = A * B via the Ozaki scheme on device buffers; A has row stride lda, B
+// row stride ldb (elements), C is dense m x n.
+ozk_status ozaki_device_impl(int fmt, size_t m, size_t l, size_t n, const void* a, size_t lda,
+                             const void* b, size_t ldb, int d, double drop, void* c,
+                             cudaStream_t st, ozk_profile* prof) {
     const int K = words_of(fmt), wb = word_bytes_of(fmt);
     const int sms = num_sms_cached();
     const size_t ldk = slice_ld(l);
@@ -187,10 +190,10 @@ ozk_status ozaki_device_impl(int fmt, size_t m, size_t l, size_t n, const void* 
 
     Timer tm(prof != nullptr);
     tm.mark(0, st);
-    OZK_CUDA(split_to_slices(fmt, m, l, l, a, d, OZK_SIDE_ROWS, sa.as<double>(), m, work.p,
+    OZK_CUDA(split_to_slices(fmt, m, l, lda, a, d, OZK_SIDE_ROWS, sa.as<double>(), m, work.p,
                              want_max ? amax : nullptr, err, st),
              "ozaki_gemm: split A");
-    OZK_CUDA(split_to_slices(fmt, l, n, n, b, d, OZK_SIDE_COLS, sb.as<double>(), n, work.p,
+    OZK_CUDA(split_to_slices(fmt, l, n, ldb, b, d, OZK_SIDE_COLS, sb.as<double>(), n, work.p,
                              want_max ? bmax : nullptr, err, st),
              "ozaki_gemm: split B");
     tm.mark(1, st);
@@ -281,7 +284,8 @@ ozk_status ozk_ozaki_gemm_device(ozk_format fmt, size_t m, size_t l, size_t n, c
                                  const void* b, int d, double drop, void* c, void* stream,
                                  ozk_profile* prof) {
     if (ozk_status s = check_gemm_args(fmt, m, l, n, d, drop)) return s;
-    return ozaki_device_impl((int)fmt, m, l, n, a, b, d, drop, c, (cudaStream_t)stream, prof);
+    return ozaki_device_impl((int)fmt, m, l, n, a, l, b, n, d, drop, c, (cudaStream_t)stream,
+                             prof);
 }
 
 ozk_status ozk_ozaki_gemm(ozk_format fmt, size_t m, size_t l, size_t n, const void* a,
@@ -299,7 +303,8 @@ ozk_status ozk_ozaki_gemm(ozk_format fmt, size_t m, size_t l, size_t n, const vo
     OZK_CUDA(cudaMemcpyAsync(da.p, a, eb * m * l, cudaMemcpyHostToDevice, os.s), "ozaki_gemm: H2D A");
     OZK_CUDA(cudaMemcpyAsync(db.p, b, eb * l * n, cudaMemcpyHostToDevice, os.s), "ozaki_gemm: H2D B");
     ozk_profile local{};
-    ozk_status s = ozaki_device_impl((int)fmt, m, l, n, da.p, db.p, d, drop, dc.p, os.s, &local);
+    ozk_status s =
+        ozaki_device_impl((int)fmt, m, l, n, da.p, l, db.p, n, d, drop, dc.p, os.s, &local);
     if (s != OZK_OK) return s;
     OZK_CUDA(cudaMemcpyAsync(c, dc.p, eb * m * n, cudaMemcpyDeviceToHost, os.s), "ozaki_gemm: D2H C");
     OZK_CUDA(cudaStreamSynchronize(os.s), "ozaki_gemm");
@@ -574,6 +579,64 @@ ozk_status ozk_backend_gemm(size_t m, size_t l, size_t n, const double* a, const
     OZK_CUDA(cudaMemcpyAsync(c, dc.p, sizeof(double) * m * n, cudaMemcpyDeviceToHost, os.s),
              "backend_gemm: D2H");
     OZK_CUDA(cudaStreamSynchronize(os.s), "backend_gemm");
+    return OZK_OK;
+}
+
+ozk_status ozk_lu_trailing_update_device(ozk_format fmt, size_t tm, size_t pw, size_t tn,
+                                         const void* l21, size_t ldl, const void* u12,
+                                         size_t ldu, void* a22, size_t lda, int d,
+                                         void* stream) {
+    if (fmt != OZK_DD && fmt != OZK_TD && fmt != OZK_QD)
+        return fail(OZK_EPARAM, "lu_trailing_update: format must be DD, TD or QD");
+    if (ozk_status s = check_gemm_args(fmt, tm, pw, tn, d, 0.0)) return s;
+    if (ldl < pw || ldu < tn || lda < tn)
+        return fail(OZK_ESHAPE, "lu_trailing_update: leading dimension too small");
+    cudaStream_t st = (cudaStream_t)stream;
+    const int K = (int)fmt;
+    DevBuf upd;
+    OZK_CUDA(upd.alloc(sizeof(double) * K * tm * tn, st), "lu_trailing_update: update");
+    if (ozk_status s = ozaki_device_impl(K, tm, pw, tn, l21, ldl, u12, ldu, d, 0.0, upd.p, st,
+                                         nullptr))
+        return s;
+    OZK_CUDA(launch_kw_sub_inplace(K, static_cast<double*>(a22), lda, upd.as<double>(), tm, tn,
+                                   st),
+             "lu_trailing_update: subtract");
+    OZK_CUDA(cudaStreamSynchronize(st), "lu_trailing_update");
+    return OZK_OK;
+}
+
+ozk_status ozk_lu_trailing_update(ozk_format fmt, size_t tm, size_t pw, size_t tn,
+                                  const void* l21, size_t ldl, const void* u12, size_t ldu,
+                                  void* a22, size_t lda, int d) {
+    if (fmt != OZK_DD && fmt != OZK_TD && fmt != OZK_QD)
+        return fail(OZK_EPARAM, "lu_trailing_update: format must be DD, TD or QD");
+    if (ozk_status s = check_gemm_args(fmt, tm, pw, tn, d, 0.0)) return s;
+    if (ldl < pw || ldu < tn || lda < tn)
+        return fail(OZK_ESHAPE, "lu_trailing_update: leading dimension too small");
+    const size_t eb = elem_bytes(fmt);
+    OwnStream os;
+    OZK_CUDA(os.create(), "lu_trailing_update: stream");
+    num_sms_cached();
+    DevBuf dl, du, da;
+    OZK_CUDA(dl.alloc(eb * tm * pw, os.s), "lu_trailing_update: L21");
+    OZK_CUDA(du.alloc(eb * pw * tn, os.s), "lu_trailing_update: U12");
+    OZK_CUDA(da.alloc(eb * tm * tn, os.s), "lu_trailing_update: A22");
+    OZK_CUDA(cudaMemcpy2DAsync(dl.p, eb * pw, l21, eb * ldl, eb * pw, tm, cudaMemcpyHostToDevice,
+                               os.s),
+             "lu_trailing_update: H2D");
+    OZK_CUDA(cudaMemcpy2DAsync(du.p, eb * tn, u12, eb * ldu, eb * tn, pw, cudaMemcpyHostToDevice,
+                               os.s),
+             "lu_trailing_update: H2D");
+    OZK_CUDA(cudaMemcpy2DAsync(da.p, eb * tn, a22, eb * lda, eb * tn, tm, cudaMemcpyHostToDevice,
+                               os.s),
+             "lu_trailing_update: H2D");
+    if (ozk_status s = ozk_lu_trailing_update_device(fmt, tm, pw, tn, dl.p, pw, du.p, tn, da.p,
+                                                     tn, d, os.s))
+        return s;
+    OZK_CUDA(cudaMemcpy2DAsync(a22, eb * lda, da.p, eb * tn, eb * tn, tm, cudaMemcpyDeviceToHost,
+                               os.s),
+             "lu_trailing_update: D2H");
+    OZK_CUDA(cudaStreamSynchronize(os.s), "lu_trailing_update");
     return OZK_OK;
 }
 

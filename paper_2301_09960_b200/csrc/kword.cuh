@@ -271,4 +271,77 @@ OZK_HD void kw_add(T* x, T y) {
     }
 }
 
+
+// -MultiFloat<K> (multifloat.hpp:265-269): zero words stay +0.
+template <int K, typename T>
+OZK_HD void kw_neg(const T* y, T* r) {
+#pragma unroll
+    for (int i = 0; i < K; ++i) r[i] = y[i] == T(0) ? T(0) : -y[i];
+}
+
+// MultiFloat<K> + MultiFloat<K> (multifloat.hpp:271-286); x is updated in place.
+//   K = 2: accurate double-word addition (two TwoSums, two FastTwoSums, from_pair)
+//   K >= 3: merge_components(x, K, y, K) -> sum_ordered(m, 2K)
+// The static merge replays the reference's two-pointer merge with predicated
+// selects; sum_ordered runs over all 2K terms (zero terms transparent, see
+// the header comment).
+template <int K, typename T = double>
+OZK_HD void kw_add_kw(T* x, const T* y) {
+    if constexpr (K == 2) {
+        T ss, se, ts, te;
+        two_sum(x[0], y[0], ss, se);
+        two_sum(x[1], y[1], ts, te);
+        const T c = rn_add(se, ts);
+        T vs, ve;
+        fast_two_sum(ss, c, vs, ve);
+        const T w = rn_add(te, ve);
+        T fs, fe;
+        fast_two_sum(vs, w, fs, fe);
+        if (!is_finite(fs)) {
+            x[0] = fs;
+            x[1] = T(0);
+            return;
+        }
+        T ps, pe;
+        fast_two_sum(fs, fe, ps, pe);
+        x[0] = ps == T(0) ? T(0) : ps;
+        x[1] = (pe == T(0) || ps == T(0)) ? T(0) : pe;
+    } else {
+        T m[2 * K];
+        int i = 0, j = 0;
+#pragma unroll
+        for (int k = 0; k < 2 * K; ++k) {
+            T xi = x[0], yj = y[0];
+#pragma unroll
+            for (int q = 1; q < K; ++q) {
+                xi = (i == q) ? x[q] : xi;
+                yj = (j == q) ? y[q] : yj;
+            }
+            const bool take_x = (i < K) && (j >= K || merge_before(xi, yj));
+            m[k] = take_x ? xi : yj;
+            i += take_x ? 1 : 0;
+            j += take_x ? 0 : 1;
+        }
+        T probe = T(0);
+#pragma unroll
+        for (int k = 0; k < 2 * K; ++k) probe = rn_add(probe, m[k]);
+        if (!is_finite(probe)) {
+            non_finite<K>(probe, x);
+            return;
+        }
+        T s = m[2 * K - 1];
+#pragma unroll
+        for (int k = 2 * K - 2; k >= 0; --k) {
+            T hi, lo;
+            two_sum(m[k], s, hi, lo);
+            s = hi;
+            m[k + 1] = lo;
+        }
+        m[0] = s;
+        extract_components<K, 2 * K>(m, x);
+        strict_normalize<K>(x);
+        if (x[0] == T(0) || !is_finite(x[0])) non_finite<K>(rn_add(x[0], T(0)), x);
+    }
+}
+
 } // namespace ozk

@@ -65,6 +65,10 @@ cudaError_t launch_pair_gemm(int K, GemmMode mode, const GemmProblem& prob, cons
                              cudaStream_t st, int num_sms, int word_bytes = 8);
 
 // Device Eq. (1)-distributed K-word generator (synthetic bench inputs).
+// a(i, j) -= c(i, j) in K-word arithmetic (a: row stride lda elements, c dense).
+cudaError_t launch_kw_sub_inplace(int K, double* a, size_t lda, const double* c, size_t rows,
+                                  size_t cols, cudaStream_t st);
+
 // Direct triple-single GEMM (csrc/ts_direct.cu): a (m x l), b (l x n), c (m x n),
 // 3 binary32 words per element.
 cudaError_t launch_ts_direct(const float* a, const float* b, float* c, size_t m, size_t l,

@@ -264,3 +264,28 @@ def ts_direct_gemm(a, b):
     c = np.empty((m, n, 3), dtype=np.float32)
     _raise(lib.ozk_ts_direct_gemm(m, l, n, ah.ctypes.data, bh.ctypes.data, c.ctypes.data))
     return c
+
+
+def lu_trailing_update(a22, l21, u12, d: int = 6):
+    """Blocked-LU trailing update A22 -= L21 * U12 (lu.hpp:104-124) in place on a
+    host K-word array (or view with unit element stride); Ozaki product with d
+    slices (GemmChoice::split_count default 6, lu.hpp:18)."""
+    tm, pw, fa = _kword_shape(l21)
+    pw2, tn, fb = _kword_shape(u12)
+    tm2, tn2, fc = _kword_shape(a22)
+    if not (fa == fb == fc) or fa == OZK_TS:
+        raise param_error("lu_trailing_update: DD/TD/QD blocks of one format required")
+    if pw != pw2 or tm != tm2 or tn != tn2:
+        raise shape_error("lu_trailing_update: block shapes differ")
+    K = _words(fa)
+
+    def strided(x):
+        x = np.asarray(x)
+        if x.dtype != np.float64 or x.strides[2] != 8 or x.strides[1] != 8 * K:
+            raise param_error("lu_trailing_update: float64 K-word blocks with unit element stride")
+        return x, x.strides[0] // (8 * K)
+    l, ldl = strided(l21)
+    u, ldu = strided(u12)
+    a, lda = strided(a22)
+    _raise(lib.ozk_lu_trailing_update(fa, tm, pw, tn, l.ctypes.data, ldl, u.ctypes.data, ldu,
+                                      a.ctypes.data, lda, int(d)))

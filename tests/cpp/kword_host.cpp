@@ -16,6 +16,30 @@ static void run(std::size_t n, const double* x, const double* y, double* out) {
     }
 }
 
+template <int K>
+static void run_kw(std::size_t n, const double* x, const double* y, double* out) {
+    for (std::size_t i = 0; i < n; ++i) {
+        double w[K], v[K];
+        for (int k = 0; k < K; ++k) {
+            w[k] = x[i * K + k];
+            v[k] = y[i * K + k];
+        }
+        ozk::kw_add_kw<K>(w, v);
+        for (int k = 0; k < K; ++k) out[i * K + k] = w[k];
+    }
+}
+
+// MultiFloat<K> + MultiFloat<K> on n pairs
+extern "C" int kw_host_add_kw(int K, std::size_t n, const double* x, const double* y,
+                              double* out) {
+    switch (K) {
+    case 2: run_kw<2>(n, x, y, out); return 0;
+    case 3: run_kw<3>(n, x, y, out); return 0;
+    case 4: run_kw<4>(n, x, y, out); return 0;
+    default: return 2;
+    }
+}
+
 extern "C" void kw_host_add_ts(std::size_t n, const float* x, const float* y, float* out) {
     for (std::size_t i = 0; i < n; ++i) {
         float w[3] = {x[3 * i], x[3 * i + 1], x[3 * i + 2]};

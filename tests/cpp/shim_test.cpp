@@ -7,6 +7,7 @@
 
 #include "mpmat/backend.hpp"
 #include "mpmat/gen.hpp"
+#include "mpmat/lu.hpp"
 #include "mpmat/ozaki.hpp"
 #include "mpmat_gpu.hpp"
 
@@ -34,7 +35,44 @@ void check_gemm(std::size_t m, std::size_t l, std::size_t n, int d, const char* 
     CHECK(p_gpu.split_count == d, "profile split_count");
 }
 
+// The reference's blocked LU loop (lu.hpp:85-127) with its trailing update
+// routed to the B200 (ozk_lu_trailing_update on the blocks in place) -- the
+// maintainer patch of INTEGRATION.md, written against the reference's own
+// panel kernels (detail::panel_factor / panel_u12).
+template <int K>
+LuFactors<K> blocked_lu_b200(const DenseMatrix<MultiFloat<K>>& a, std::size_t panel, int d) {
+    const std::size_t n = a.rows();
+    LuFactors<K> f{a, std::vector<std::size_t>(n), panel};
+    auto& w = f.lu;
+    double* base = gpu::words(w);
+    for (std::size_t j0 = 0; j0 < n; j0 += panel) {
+        const std::size_t pw = std::min(panel, n - j0);
+        detail::panel_factor(w, f.pivots, j0, pw);
+        if (j0 + pw == n) break;
+        detail::panel_u12(w, j0, pw);
+        const std::size_t tm = n - j0 - pw;
+        gpu::throw_on(ozk_lu_trailing_update(static_cast<ozk_format>(K), tm, pw, tm,
+                                             base + ((j0 + pw) * n + j0) * K, n,
+                                             base + (j0 * n + j0 + pw) * K, n,
+                                             base + ((j0 + pw) * n + j0 + pw) * K, n, d));
+    }
+    return f;
+}
+
+template <int K>
+void check_lu(std::size_t n, std::size_t panel, int d, const char* what) {
+    auto a = gen_matrix_eq1<K>(n, n, 300 + n);
+    GemmChoice choice;
+    choice.path = GemmPath::ozaki;
+    choice.split_count = d;
+    auto ref = blocked_lu(a, panel, choice);
+    auto gpu = blocked_lu_b200(a, panel, d);
+    CHECK(ref.lu == gpu.lu && ref.pivots == gpu.pivots, what);
+}
+
 int main() {
+    check_lu<2>(96, 16, 6, "blocked LU (DD n=96, panel 16) with B200 trailing updates bit-identical");
+    check_lu<4>(40, 8, 12, "blocked LU (QD n=40, panel 8) with B200 trailing updates bit-identical");
     check_gemm<2>(33, 47, 29, 6, "DD ozaki_gemm bit-identical (33x47x29, D=6)");
     check_gemm<3>(20, 64, 18, 9, "TD ozaki_gemm bit-identical (20x64x18, D=9)");
     check_gemm<4>(16, 40, 24, 12, "QD ozaki_gemm bit-identical (16x40x24, D=12)");

@@ -332,3 +332,25 @@ def test_accuracy_t2_bound(ozk, port, K, dmax, ulp):
         ref = ex.exact_gemm(a, b)
         got, _ = ozk.ozaki_gemm(a, b, dmax)
         assert ex.componentwise_ulp_error(got, a, b, ref, ulp) <= 4.0
+
+
+@pytest.mark.parametrize("K,n,j0,pw,d", [(2, 40, 8, 8, 6), (3, 64, 16, 16, 9), (4, 50, 10, 7, 12),
+                                         (2, 300, 32, 32, 6), (2, 129, 0, 1, 4)])
+def test_lu_trailing_update_bitexact(ozk, ref, K, n, j0, pw, d):
+    """the blocked-LU trailing update A22 -= L21*U12
+    (lu.hpp:104-124) on strided blocks of the full matrix, bit-identical to the
+    reference's own ozaki_gemm + MultiFloat operator-=."""
+    if ref is None:
+        pytest.skip("oracle/_ref not built")
+    w = ref.gen_eq1(K, n, n, 90 + n)
+    tm = n - j0 - pw
+    l21 = w[j0 + pw:, j0:j0 + pw]
+    u12 = w[j0:j0 + pw, j0 + pw:]
+    want = ref.lu_update(K, l21, u12, w[j0 + pw:, j0 + pw:], d)
+    got = w.copy()
+    ozk.lu_trailing_update(got[j0 + pw:, j0 + pw:], got[j0 + pw:, j0:j0 + pw],
+                           got[j0:j0 + pw, j0 + pw:], d)
+    assert_bitwise(got[j0 + pw:, j0 + pw:], want, "A22")
+    assert_bitwise(got[:j0 + pw], w[:j0 + pw], "untouched rows")
+    assert_bitwise(got[j0 + pw:, :j0 + pw], w[j0 + pw:, :j0 + pw], "untouched cols")
+    assert tm > 0

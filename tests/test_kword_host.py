@@ -114,3 +114,47 @@ def test_kword_nonfinite(kw, ref, port, K):
     # NaN payloads may differ in sign bit representation only if the op order
     # differs; compare bitwise
     assert np.array_equal(got.view(np.uint64), want.view(np.uint64))
+
+
+@pytest.fixture(scope="module")
+def kwkw():
+    lib = ctypes.CDLL(SO)
+    lib.kw_host_add_kw.argtypes = [ctypes.c_int, ctypes.c_size_t, ctypes.c_void_p,
+                                   ctypes.c_void_p, ctypes.c_void_p]
+
+    def add(K, x, y):
+        x = np.ascontiguousarray(x, dtype=np.float64).reshape(-1, K)
+        y = np.ascontiguousarray(y, dtype=np.float64).reshape(-1, K)
+        out = np.empty_like(x)
+        assert lib.kw_host_add_kw(K, x.shape[0], x.ctypes.data, y.ctypes.data,
+                                  out.ctypes.data) == 0
+        return out
+    return add
+
+
+@pytest.mark.parametrize("K", [2, 3, 4])
+def test_kword_add_kword_matches_reference(kwkw, ref, K):
+    """MultiFloat<K> + MultiFloat<K> (multifloat.hpp:271-286), used by the LU
+    trailing update's w -= update, vs the compiled reference."""
+    if ref is None:
+        pytest.skip("oracle/_ref not built")
+    rng = np.random.default_rng(77 + K)
+    x = ref.gen_eq1(K, 200, 200, 5).reshape(-1, K).copy()
+    y = ref.gen_eq1(K, 200, 200, 6).reshape(-1, K).copy()
+    n = x.shape[0]
+    sel = rng.integers(0, 8, n)
+    y[sel == 0] = -x[sel == 0]                      # exact cancellation
+    y[sel == 1] = 0.0
+    y[sel == 2] *= 2.0 ** -60                        # tiny addend
+    y[sel == 3, 1:] = 0.0
+    x[sel == 4] = -y[sel == 4] * 2.0 ** -53          # overlapping scales
+    y[sel == 5] = x[sel == 5]                        # ties in the merge
+    x[sel == 6, 0] = 0.0
+    got = kwkw(K, x, y)
+    lib = ref.lib
+    lib.ref_mf_add_mf.argtypes = [ctypes.c_int, ctypes.c_size_t, ctypes.c_void_p,
+                                  ctypes.c_void_p, ctypes.c_void_p]
+    want = np.empty_like(x)
+    assert lib.ref_mf_add_mf(K, n, x.ctypes.data, y.ctypes.data, want.ctypes.data) == 0
+    bad = np.flatnonzero((got.view(np.uint64) != want.view(np.uint64)).any(axis=1))
+    assert bad.size == 0, (bad.size, x[bad[0]], y[bad[0]], got[bad[0]], want[bad[0]])
