@@ -12,11 +12,13 @@ from .mpmat import (  # noqa: F401
     SplitSide,
     error,
     exponent_ceil_log2,
+    get_engine,
     gpu_backend,
     lu_trailing_update,
     ozaki_gemm,
     param_error,
     shape_error,
+    set_engine,
     split_matrix,
     split_shift_bits,
     ts_direct_gemm,
@@ -25,5 +27,5 @@ from .mpmat import (  # noqa: F401
 __all__ = [
     "OzakiProfile", "SplitSet", "SplitSide", "error", "exponent_ceil_log2", "gpu_backend",
     "ozaki_gemm", "param_error", "shape_error", "split_matrix", "split_shift_bits", "lib",
-    "ts_direct_gemm", "lu_trailing_update",
+    "ts_direct_gemm", "lu_trailing_update", "set_engine", "get_engine",
 ]

@@ -29,6 +29,7 @@ class OzkProfile(ctypes.Structure):
         ("split_count", ctypes.c_int),
         ("pairs", ctypes.c_int),
         ("gpus", ctypes.c_int),
+        ("engine", ctypes.c_int),
     ]
 
 
@@ -66,6 +67,8 @@ SIGNATURES = {
     "ozk_ts_direct_gemm": (ctypes.c_int, [_sz, _sz, _sz, _dp, _dp, _dp]),
     "ozk_ts_direct_gemm_device": (ctypes.c_int, [_sz, _sz, _sz, _dp, _dp, _dp, ctypes.c_void_p]),
     "ozk_probe_dmma_tflops": (ctypes.c_double, [ctypes.c_int, ctypes.c_void_p]),
+    "ozk_set_engine": (ctypes.c_int, [ctypes.c_int]),
+    "ozk_get_engine": (ctypes.c_int, []),
     "ozk_last_error": (ctypes.c_char_p, []),
     "ozk_version": (ctypes.c_int, []),
 }

@@ -6,7 +6,9 @@
 // split_matrix (:74-147) x2 -> backend (backend.hpp:12-13) x P -> accumulate.
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <chrono>
+#include <cstdlib>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -22,6 +24,30 @@ using namespace ozk;
 namespace {
 
 thread_local std::string g_last_error;
+
+int word_bytes_of_fmt(int fmt) { return fmt == OZK_TS ? 4 : 8; }
+
+// Slice-product engine: OZK_ENGINE_AUTO picks the exact INT8-digit tcgen05
+// engine whenever it applies (binary64 words, D >= 2, 512 < l < 43690), else
+// the FP64 DMMA engine.  Initialised from $OZK_ENGINE (auto|dmma|int8).
+std::atomic<int> g_engine{-1};
+
+int engine_setting() {
+    int e = g_engine.load();
+    if (e < 0) {
+        e = OZK_ENGINE_AUTO;
+        if (const char* v = std::getenv("OZK_ENGINE")) {
+            if (!std::strcmp(v, "dmma")) e = OZK_ENGINE_DMMA;
+            if (!std::strcmp(v, "int8")) e = OZK_ENGINE_INT8;
+        }
+        g_engine.store(e);
+    }
+    return e;
+}
+
+bool int8_applicable(int fmt, size_t l, int d) {
+    return word_bytes_of_fmt(fmt) == 8 && d >= 2 && l > 512 && l < 43690;
+}
 
 ozk_status fail(ozk_status s, const std::string& msg) {
     g_last_error = msg;
@@ -131,19 +157,20 @@ ozk_status check_dev_err(int flag, const char* what) {
 // work must hold outer*inner elements.  Returns a CUDA error code.
 cudaError_t split_to_slices(int fmt, size_t rows, size_t cols, size_t ld, const void* mat, int d,
                             int side, double* slices, size_t plane_rows, void* work,
-                            unsigned long long* pmax, int* err, cudaStream_t st) {
+                            unsigned long long* pmax, int* err, cudaStream_t st,
+                            const DigitOut& dig = DigitOut{}) {
     const int K = words_of(fmt), wb = word_bytes_of(fmt);
     const size_t inner = side == OZK_SIDE_ROWS ? cols : rows;
     const size_t ldk = slice_ld(inner);
     const int sigma = shift_bits(inner, wb == 4 ? 24 : 53);
     if (side == OZK_SIDE_ROWS)
         return launch_split_rows(K, wb, mat, ld, work, rows, cols, d, sigma, slices, ldk,
-                                 plane_rows * ldk, pmax, err, st);
+                                 plane_rows * ldk, pmax, err, st, dig);
     // columns: transpose to (cols x rows) so each column is a contiguous row
     cudaError_t e = launch_transpose(K, wb, mat, ld, work, rows, rows, cols, st);
     if (e != cudaSuccess) return e;
     return launch_split_rows(K, wb, work, rows, work, cols, rows, d, sigma, slices, ldk,
-                             plane_rows * ldk, pmax, err, st);
+                             plane_rows * ldk, pmax, err, st, dig);
 }
 
 struct Timer {
@@ -176,9 +203,21 @@ ozk_status ozaki_device_impl(int fmt, size_t m, size_t l, size_t n, const void* 
     const int K = words_of(fmt), wb = word_bytes_of(fmt);
     const int sms = num_sms_cached();
     const size_t ldk = slice_ld(l);
-    DevBuf sa, sb, work, flags;
-    OZK_CUDA(sa.alloc(sizeof(double) * d * m * ldk, st), "ozaki_gemm: slices A");
-    OZK_CUDA(sb.alloc(sizeof(double) * d * n * ldk, st), "ozaki_gemm: slices B");
+    const int eng = engine_setting();
+    const bool use_i8 = eng != OZK_ENGINE_DMMA && int8_applicable(fmt, l, d);
+    if (eng == OZK_ENGINE_INT8 && !use_i8)
+        return fail(OZK_EPARAM, "ozaki_gemm: INT8 engine needs binary64 words, D >= 2, 512 < l < 43690");
+    const size_t ld8 = (l + 15) & ~size_t(15);
+    DevBuf sa, sb, work, flags, da8, db8, ga, gb;
+    if (use_i8) {
+        OZK_CUDA(da8.alloc((size_t)d * 3 * m * ld8, st), "ozaki_gemm: digits A");
+        OZK_CUDA(db8.alloc((size_t)d * 3 * n * ld8, st), "ozaki_gemm: digits B");
+        OZK_CUDA(ga.alloc(sizeof(int) * d * m, st), "ozaki_gemm: exponents A");
+        OZK_CUDA(gb.alloc(sizeof(int) * d * n, st), "ozaki_gemm: exponents B");
+    } else {
+        OZK_CUDA(sa.alloc(sizeof(double) * d * m * ldk, st), "ozaki_gemm: slices A");
+        OZK_CUDA(sb.alloc(sizeof(double) * d * n * ldk, st), "ozaki_gemm: slices B");
+    }
     OZK_CUDA(work.alloc(elem_bytes(fmt) * (m > n ? m : n) * l, st), "ozaki_gemm: work");
     // flags layout: [err int (8 B)][amax d][bmax d]
     OZK_CUDA(flags.alloc(8 + 16 * (size_t)d, st), "ozaki_gemm: flags");
@@ -187,14 +226,29 @@ ozk_status ozaki_device_impl(int fmt, size_t m, size_t l, size_t n, const void* 
     unsigned long long* amax = reinterpret_cast<unsigned long long*>(flags.as<char>() + 8);
     unsigned long long* bmax = amax + d;
     const bool want_max = drop > 0.0;
+    DigitOut digA, digB;
+    if (use_i8) {
+        digA.digits = da8.as<int8_t>();
+        digA.ld = ld8;
+        digA.digit_stride = m * ld8;
+        digA.slice_stride = 3 * m * ld8;
+        digA.exps = ga.as<int>();
+        digA.exp_stride = m;
+        digB.digits = db8.as<int8_t>();
+        digB.ld = ld8;
+        digB.digit_stride = n * ld8;
+        digB.slice_stride = 3 * n * ld8;
+        digB.exps = gb.as<int>();
+        digB.exp_stride = n;
+    }
 
     Timer tm(prof != nullptr);
     tm.mark(0, st);
     OZK_CUDA(split_to_slices(fmt, m, l, lda, a, d, OZK_SIDE_ROWS, sa.as<double>(), m, work.p,
-                             want_max ? amax : nullptr, err, st),
+                             want_max ? amax : nullptr, err, st, digA),
              "ozaki_gemm: split A");
     OZK_CUDA(split_to_slices(fmt, l, n, ldb, b, d, OZK_SIDE_COLS, sb.as<double>(), n, work.p,
-                             want_max ? bmax : nullptr, err, st),
+                             want_max ? bmax : nullptr, err, st, digB),
              "ozaki_gemm: split B");
     tm.mark(1, st);
 
@@ -230,10 +284,30 @@ ozk_status ozaki_device_impl(int fmt, size_t m, size_t l, size_t n, const void* 
     prob.l = l;
     prob.c = c;
     prob.ldc = n;
-    if (pl.count == 0)  // every pair pruned (drop_threshold > 1): C = 0
+    if (pl.count == 0) {  // every pair pruned (drop_threshold > 1): C = 0
         OZK_CUDA(cudaMemsetAsync(c, 0, elem_bytes(fmt) * m * n, st), "ozaki_gemm: zero C");
-    else
+    } else if (use_i8) {
+        I8Operands op{};
+        op.a = da8.as<int8_t>();
+        op.a_ld = ld8;
+        op.a_digit_stride = m * ld8;
+        op.a_slice_stride = 3 * m * ld8;
+        op.b = db8.as<int8_t>();
+        op.b_ld = ld8;
+        op.b_digit_stride = n * ld8;
+        op.b_slice_stride = 3 * n * ld8;
+        op.gA = ga.as<int>();
+        op.gB = gb.as<int>();
+        op.m = m;
+        op.n = n;
+        op.l = l;
+        op.d = d;
+        op.c = c;
+        op.ldc = n;
+        OZK_CUDA(launch_pair_gemm_i8(K, op, pl, st, sms), "ozaki_gemm: INT8 slice GEMM");
+    } else {
         OZK_CUDA(launch_pair_gemm(K, kAccumulate, prob, pl, st, sms, wb), "ozaki_gemm: slice GEMM");
+    }
     tm.mark(2, st);
 
     int flag = 0;
@@ -249,6 +323,7 @@ ozk_status ozaki_device_impl(int fmt, size_t m, size_t l, size_t n, const void* 
         prof->split_count = d;
         prof->pairs = pl.count;
         prof->gpus = 1;
+        prof->engine = use_i8 ? OZK_ENGINE_INT8 : OZK_ENGINE_DMMA;
     }
     return OZK_OK;
 }
@@ -269,6 +344,15 @@ ozk_status check_gemm_args(int fmt, size_t m, size_t l, size_t n, int d, double 
 extern "C" {
 
 const char* ozk_last_error(void) { return g_last_error.c_str(); }
+
+ozk_status ozk_set_engine(int engine) {
+    if (engine != OZK_ENGINE_AUTO && engine != OZK_ENGINE_DMMA && engine != OZK_ENGINE_INT8)
+        return fail(OZK_EPARAM, "set_engine: unknown engine");
+    g_engine.store(engine);
+    return OZK_OK;
+}
+
+int ozk_get_engine(void) { return engine_setting(); }
 int ozk_version(void) { return 1; }
 
 int ozk_split_shift_bits(size_t inner) { return shift_bits(inner ? inner : 1); }

@@ -23,11 +23,22 @@ inline size_t slice_ld(size_t inner) { return (inner + 1) & ~size_t(1); }
 //   pieces  : d slices, slice a row r at pieces + a*slice_stride + r*ldk
 //   piece_max (optional): d values, max |piece_a| as ordered uint64 bits
 //   err     : device flag (DevErr)
+// Optional INT8-digit output of the split (for the exact INT8 slice-product
+// engine): slice a, row r has grid exponent exps[a*exp_stride + r] = g and
+// digits[a*slice_stride + s*digit_stride + r*ld + k], s = 0..2, with
+// piece(r, k) = 2^g * (d0 + 256 d1 + 65536 d2).  digits == nullptr: off.
+struct DigitOut {
+    int8_t* digits = nullptr;
+    size_t ld = 0, digit_stride = 0, slice_stride = 0;
+    int* exps = nullptr;
+    size_t exp_stride = 0;
+};
+
 // word_bytes = 8 for DD/TD/QD (binary64 words), 4 for TS (binary32 words, K = 3).
 cudaError_t launch_split_rows(int K, int word_bytes, const void* in, size_t in_ld, void* work,
                               size_t rows, size_t cols, int d, int sigma, double* pieces,
                               size_t ldk, size_t slice_stride, unsigned long long* piece_max,
-                              int* err, cudaStream_t st);
+                              int* err, cudaStream_t st, const DigitOut& dig = DigitOut{});
 
 // Transpose of a K-word matrix: out(j, i) = in(i, j).  in is rows x cols with
 // row stride in_ld elements; out is cols x rows with row stride out_ld elements.
@@ -63,6 +74,23 @@ struct GemmProblem {
 
 cudaError_t launch_pair_gemm(int K, GemmMode mode, const GemmProblem& prob, const PairList& pairs,
                              cudaStream_t st, int num_sms, int word_bytes = 8);
+
+// Exact INT8-digit slice products on tcgen05 (gemm_i8.cu).  Digits as written
+// by the split's DigitOut: [d][3][rows][ld] int8, exponents [d][rows].
+struct I8Operands {
+    const int8_t* a;
+    size_t a_ld, a_digit_stride, a_slice_stride;
+    const int8_t* b;
+    size_t b_ld, b_digit_stride, b_slice_stride;
+    const int* gA;  // [d][m]
+    const int* gB;  // [d][n]
+    size_t m, n, l;
+    int d;
+    void* c;        // K-word AoS, row stride ldc elements
+    size_t ldc;
+};
+cudaError_t launch_pair_gemm_i8(int K, const I8Operands& op, const PairList& pairs,
+                                cudaStream_t st, int num_sms);
 
 // Device Eq. (1)-distributed K-word generator (synthetic bench inputs).
 // a(i, j) -= c(i, j) in K-word arithmetic (a: row stride lda elements, c dense).

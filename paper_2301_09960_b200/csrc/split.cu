@@ -99,12 +99,12 @@ __global__ void __launch_bounds__(kSplitThreads)
 split_rows_kernel(const T* __restrict__ in, size_t in_ld, T* __restrict__ work, size_t cols,
                   int d, int sigma, double* __restrict__ pieces, size_t ldk,
                   size_t slice_stride, unsigned long long* __restrict__ piece_max,
-                  int* __restrict__ err) {
+                  int* __restrict__ err, DigitOut dig) {
     __shared__ double red[33];
     const size_t r = blockIdx.x;
     const T* src = in + r * in_ld * K;
     T* w = work + r * cols * K;
-    double* prow = pieces + r * ldk;
+    double* prow = pieces ? pieces + r * ldk : nullptr;
 
     // Sweep 0: leading image max, finiteness scan (ozaki.hpp:77-78), and the
     // copy of the input row into the working residual.
@@ -146,7 +146,7 @@ split_rows_kernel(const T* __restrict__ in, size_t in_ld, T* __restrict__ work, 
     }
 
     for (int a = 0; a < d; ++a) {
-        double* pa = prow + (size_t)a * slice_stride;
+        double* pa = pieces ? prow + (size_t)a * slice_stride : nullptr;  // optional (INT8 engine)
         T tau = T(0);  // zero marks a skipped (all-zero) row, ozaki.hpp:105-107
         if (mx != T(0)) {
             const int e = ceil_log2(mx);
@@ -158,16 +158,33 @@ split_rows_kernel(const T* __restrict__ in, size_t in_ld, T* __restrict__ work, 
         }
         T nmx = T(0);
         double pmx = 0.0;
+        // INT8-digit output: the slice row is an integer multiple of
+        // 2^g, g = e + sigma - 54 (the half-grid of ozaki.hpp:15-29), with
+        // |x / 2^g| <= 2^(54 - sigma); written as 3 signed base-256 digits.
+        const int g = (tau == T(0)) ? 0 : (ceil_log2(mx) + sigma - 54);
+        int8_t* drow = dig.digits ? dig.digits + (size_t)a * dig.slice_stride + r * dig.ld : nullptr;
+        if (dig.digits && threadIdx.x == 0) dig.exps[(size_t)a * dig.exp_stride + r] = g;
         for (size_t j = threadIdx.x; j < cols; j += kSplitThreads) {
             if (tau == T(0)) {
-                pa[j] = 0.0;
+                if (pa) pa[j] = 0.0;
+                if (drow) drow[j] = drow[j + dig.digit_stride] = drow[j + 2 * dig.digit_stride] = 0;
                 continue;
             }
             T c[K];
             load_kw<K>(w + j * K, c);
             // shift_extract: (v + tau) - tau, strictly rounded (ozaki.hpp:53-56)
             const T x = rn_sub(rn_add(c[0], tau), tau);
-            pa[j] = (double)x;
+            if (pa) pa[j] = (double)x;
+            if (drow) {
+                const int mi = (int)scalbn((double)x, -g);  // exact integer, |mi| <= 2^22
+                const int d0 = (int)(int8_t)(mi & 0xff);
+                const int m1 = (mi - d0) >> 8;
+                const int d1 = (int)(int8_t)(m1 & 0xff);
+                const int d2 = (m1 - d1) >> 8;
+                drow[j] = (int8_t)d0;
+                drow[j + dig.digit_stride] = (int8_t)d1;
+                drow[j + 2 * dig.digit_stride] = (int8_t)d2;
+            }
             if (x != T(0)) {
                 kw_add<K>(c, -x);  // w -= x  ==  w + (-x)  (multifloat.hpp:302,391)
                 store_kw<K>(w + j * K, c);
@@ -175,7 +192,11 @@ split_rows_kernel(const T* __restrict__ in, size_t in_ld, T* __restrict__ work, 
             nmx = fmax(nmx, fabs_(c[0]));
             pmx = fmax(pmx, (double)fabs_(x));
         }
-        for (size_t j = cols + threadIdx.x; j < ldk; j += kSplitThreads) pa[j] = 0.0;
+        if (pa)
+            for (size_t j = cols + threadIdx.x; j < ldk; j += kSplitThreads) pa[j] = 0.0;
+        if (drow)
+            for (size_t j = cols + threadIdx.x; j < dig.ld; j += kSplitThreads)
+                drow[j] = drow[j + dig.digit_stride] = drow[j + 2 * dig.digit_stride] = 0;
         if (piece_max) {
             pmx = block_max(pmx, red);
             if (threadIdx.x == 0)
@@ -215,13 +236,14 @@ __global__ void transpose_kernel(const T* __restrict__ in, size_t in_ld, T* __re
 cudaError_t launch_split_rows(int K, int word_bytes, const void* in, size_t in_ld, void* work,
                               size_t rows, size_t cols, int d, int sigma, double* pieces,
                               size_t ldk, size_t slice_stride, unsigned long long* piece_max,
-                              int* err, cudaStream_t st) {
+                              int* err, cudaStream_t st, const DigitOut& dig) {
     if (rows == 0) return cudaSuccess;
     dim3 grid((unsigned)rows), block(kSplitThreads);
 #define OZK_SPLIT(KK, TT)                                                                         \
     split_rows_kernel<KK, TT><<<grid, block, 0, st>>>(static_cast<const TT*>(in), in_ld,          \
                                                       static_cast<TT*>(work), cols, d, sigma,     \
-                                                      pieces, ldk, slice_stride, piece_max, err)
+                                                      pieces, ldk, slice_stride, piece_max, err, \
+                                                      dig)
     if (word_bytes == 4) {
         if (K != 3) return cudaErrorInvalidValue;
         OZK_SPLIT(3, float);

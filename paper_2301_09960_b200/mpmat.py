@@ -77,6 +77,20 @@ class SplitSide(enum.IntEnum):
 
 FORMATS = {2: "dd", 3: "td", 4: "qd"}
 OZK_TS = 0x103  # include/ozk.h
+ENGINES = {0: "auto", 1: "dmma", 2: "int8"}
+
+
+def set_engine(name: str) -> None:
+    """Slice-product engine for subsequent calls: "auto", "dmma" or "int8"
+    (include/ozk.h ozk_engine; results are bit-identical across engines)."""
+    code = {v: k for k, v in ENGINES.items()}.get(name)
+    if code is None:
+        raise param_error(f"unknown engine {name!r}")
+    _raise(lib.ozk_set_engine(code))
+
+
+def get_engine() -> str:
+    return ENGINES[lib.ozk_get_engine()]
 
 
 def split_shift_bits(inner_dim: int) -> int:
@@ -95,6 +109,7 @@ class OzakiProfile:
     split_count: int = 0
     pairs: int = 0
     transfer_seconds: float = 0.0
+    engine: str = ""
 
     def total_seconds(self) -> float:
         return self.split_seconds + self.product_seconds + self.accumulate_seconds
@@ -115,7 +130,7 @@ class OzakiProfile:
     @classmethod
     def _of(cls, p: OzkProfile) -> "OzakiProfile":
         return cls(p.split_seconds, p.product_seconds, p.accumulate_seconds, p.split_count,
-                   p.pairs, p.transfer_seconds)
+                   p.pairs, p.transfer_seconds, ENGINES.get(p.engine, ""))
 
 
 @dataclass

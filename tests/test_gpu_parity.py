@@ -354,3 +354,61 @@ def test_lu_trailing_update_bitexact(ozk, ref, K, n, j0, pw, d):
     assert_bitwise(got[:j0 + pw], w[:j0 + pw], "untouched rows")
     assert_bitwise(got[j0 + pw:, :j0 + pw], w[j0 + pw:, :j0 + pw], "untouched cols")
     assert tm > 0
+
+
+@pytest.fixture
+def engine(ozk):
+    """Run a test under a chosen slice-product engine, restore auto afterwards."""
+    def use(name):
+        ozk.set_engine(name)
+    yield use
+    ozk.set_engine("auto")
+
+
+I8_CASES = [
+    # K, m, l, n, d  (l > 512: the exact INT8-digit engine applies)
+    (2, 130, 600, 70, 6), (3, 64, 1000, 64, 9), (4, 200, 777, 130, 12), (2, 256, 2048, 256, 7),
+    (2, 1, 513, 1, 2), (3, 300, 1024, 129, 10), (4, 129, 4096, 65, 12), (2, 64, 8192, 64, 6),
+]
+
+
+@pytest.mark.parametrize("K,m,l,n,d", I8_CASES)
+@pytest.mark.parametrize("eng", ["int8", "dmma"])
+def test_engines_bitexact(ozk, cpu, engine, eng, K, m, l, n, d):
+    """Both slice-product engines (FP64 DMMA, exact INT8 digits on tcgen05)
+    reproduce the reference C bit for bit."""
+    engine(eng)
+    a = cpu.gen_eq1(K, m, l, 5 + m + K)
+    b = cpu.gen_eq1(K, l, n, 6 + m + K)
+    want = cpu.ozaki_gemm(K, a, b, d)
+    got, prof = ozk.ozaki_gemm(a, b, d)
+    assert prof.engine == eng
+    assert_bitwise(got, want, f"{eng} K={K} {m}x{l}x{n} D={d}")
+
+
+@pytest.mark.parametrize("spread", [30, 200])
+def test_int8_engine_ill_conditioned_and_pruning(ozk, cpu, port, engine, spread):
+    engine("int8")
+    a = port.gen_spread(2, 70, 700, 3, spread)
+    b = port.gen_spread(2, 700, 50, 4, spread)
+    for d, drop in ((10, 0.0), (10, 2.0 ** -80), (14, 0.0)):
+        want = cpu.ozaki_gemm(2, a, b, d, drop)
+        got, _ = ozk.ozaki_gemm(a, b, d, drop_threshold=drop)
+        assert_bitwise(got, want, f"int8 spread={spread} D={d} drop={drop}")
+
+
+def test_int8_engine_repeat_runs(ozk, cpu, engine):
+    engine("int8")
+    a = cpu.gen_eq1(4, 300, 1200, 1)
+    b = cpu.gen_eq1(4, 1200, 300, 2)
+    want = cpu.ozaki_gemm(4, a, b, 12)
+    for _ in range(3):
+        got, _ = ozk.ozaki_gemm(a, b, 12)
+        assert_bitwise(got, want, "int8 repeat")
+
+
+def test_int8_engine_rejects_inapplicable(ozk, engine):
+    engine("int8")
+    a = np.zeros((4, 100, 2))
+    with pytest.raises(ozk.param_error):
+        ozk.ozaki_gemm(a, np.zeros((100, 4, 2)), 6)  # l <= 512
