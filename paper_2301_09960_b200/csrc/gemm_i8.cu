@@ -43,6 +43,11 @@ constexpr int kStages = 3;
 constexpr int kEpiGroups = 2;                 // epilogue warpgroups (column halves)
 constexpr int kThreads = (4 + 4 * kEpiGroups) * 32;
 constexpr int kEpiCols = 64 / kEpiGroups;     // columns per epilogue thread
+// K-word adds unrolled per epilogue step, per format (B200 A/B at n = 8192,
+// tools/variants_bench.py): DD 8 (104.6 ms; 2: 109.1), TD 2 (316 ms; 8: 349),
+// QD 2 (582 ms; 8: 664) -- the K >= 3 bodies are large enough that more
+// unrolling costs instruction-cache misses and registers instead of latency.
+template <int K> constexpr int kChunkFor = (K == 2) ? 8 : 2;
 constexpr int kATile = BM * BKB;              // 16 KiB per digit
 constexpr int kBTile = BN * BKB;              // 8 KiB per digit
 constexpr int kStageBytes = 3 * kATile + 3 * kBTile;
@@ -315,32 +320,33 @@ pair_gemm_i8_kernel(const __grid_constant__ MapsI8 maps, const __grid_constant__
                 double* cp = static_cast<double*>(prob.c) + (row * prob.ldc + col0) * K;
                 const int* gbp = prob.gB + (size_t)be * prob.gB_stride + col0;
 #pragma unroll 1
-                for (int c = 0; c < kEpiCols; c += 8) {
-                    // y[0..7] are this chunk's products; the array is shifted
-                    // down by 8 after each chunk so every index stays static
-                    double w[8][K];
+                constexpr int kChunk = kChunkFor<K>;
+                for (int c = 0; c < kEpiCols; c += kChunk) {
+                    // y[0..kChunk) are this chunk's products; the array is
+                    // shifted down after each chunk so every index stays static
+                    double w[kChunk][K];
 #pragma unroll
-                    for (int j = 0; j < 8; ++j) {
+                    for (int j = 0; j < kChunk; ++j) {
                         const bool ok = col0 + c + j < prob.n;
 #pragma unroll
                         for (int k = 0; k < K; ++k)
                             w[j][k] = (ok && p > 0) ? cp[(c + j) * K + k] : 0.0;
                     }
 #pragma unroll
-                    for (int j = 0; j < 8; ++j) {
+                    for (int j = 0; j < kChunk; ++j) {
                         const bool ok = col0 + c + j < prob.n;
                         const int gb = ok ? __ldg(gbp + c + j) : 0;
                         kw_add<K>(w[j], ldexp_fast(y[j], ga + gb));
                     }
 #pragma unroll
-                    for (int j = 0; j < 8; ++j) {
+                    for (int j = 0; j < kChunk; ++j) {
                         if (col0 + c + j < prob.n) {
 #pragma unroll
                             for (int k = 0; k < K; ++k) cp[(c + j) * K + k] = w[j][k];
                         }
                     }
 #pragma unroll
-                    for (int j = 0; j < kEpiCols - 8; ++j) y[j] = y[j + 8];
+                    for (int j = 0; j < kEpiCols - kChunk; ++j) y[j] = y[j + kChunk];
                 }
             }
         }

@@ -119,6 +119,39 @@ OZK_HD bool is_finite(double x) {
 OZK_HD bool is_finite(float x) { return (fbits(x) & 0x7f800000u) != 0x7f800000u; }
 OZK_HD bool dfinite(double x) { return is_finite(x); }
 
+// ---- comparisons -------------------------------------------------------------
+// kInt = false: the reference's floating-point comparisons.  kInt = true: the
+// same predicates on the bit patterns (integer ALU instead of DSETP, which on
+// B200 shares the slow XU pipe).  They agree for every finite operand whose
+// words stay below 2^1000 (2^120 for binary32), which kw_add checks before
+// taking that path: no NaN (where FP and bit comparisons differ), no overflow
+// to infinity inside the sweeps, and -0 never reaches a bitwise comparison
+// (the compaction writes +0; x - x rounds to +0).
+template <typename T> struct Bits;
+template <> struct Bits<double> {
+    using U = uint64_t;
+    static constexpr U kAbs = 0x7fffffffffffffffull;
+    static constexpr U kSafe = (uint64_t)(1023 + 1000) << 52;  // |x| < 2^1000
+};
+template <> struct Bits<float> {
+    using U = uint32_t;
+    static constexpr U kAbs = 0x7fffffffu;
+    static constexpr U kSafe = (uint32_t)(127 + 120) << 23;     // |x| < 2^120
+};
+
+template <bool kInt, typename T>
+OZK_HD bool is_zero(T x) {
+    if constexpr (kInt) return (fbits(x) & Bits<T>::kAbs) == 0;
+    else return x == T(0);
+}
+template <bool kInt, typename T>
+OZK_HD bool same(T a, T b) {  // a == b in the kInt domain described above
+    if constexpr (kInt) return fbits(a) == fbits(b);
+    else return a == b;
+}
+template <typename T>
+OZK_HD bool safe_word(T x) { return (fbits(x) & Bits<T>::kAbs) < Bits<T>::kSafe; }
+
 // eft.hpp:25-30
 template <typename T>
 OZK_HD void two_sum(T a, T b, T& s, T& e) {
@@ -137,10 +170,15 @@ OZK_HD void fast_two_sum(T a, T b, T& s, T& e) {
 }
 
 // multifloat.hpp:509-512 (merge order predicate)
-template <typename T>
+template <bool kInt = false, typename T>
 OZK_HD bool merge_before(T x, T y) {
-    T ax = fabs_(x), ay = fabs_(y);
-    if (ax != ay) return ax > ay;
+    if constexpr (kInt) {
+        const auto ax = fbits(x) & Bits<T>::kAbs, ay = fbits(y) & Bits<T>::kAbs;
+        if (ax != ay) return ax > ay;
+    } else {
+        T ax = fabs_(x), ay = fabs_(y);
+        if (ax != ay) return ax > ay;
+    }
     return fbits(x) <= fbits(y);
 }
 
@@ -152,7 +190,7 @@ OZK_HD void non_finite(T head, T* c) {
 }
 
 // multifloat.hpp:450-469
-template <int K, typename T>
+template <int K, bool kInt = false, typename T>
 OZK_HD void strict_normalize(T* c) {
 #pragma unroll
     for (int pass = 0; pass < 2 * K; ++pass) {
@@ -161,7 +199,7 @@ OZK_HD void strict_normalize(T* c) {
         for (int r = 0; r < K - 1; ++r) {
 #pragma unroll
             for (int i = 0; i < K - 1; ++i) {
-                bool z = c[i] == T(0);
+                bool z = is_zero<kInt>(c[i]);
                 T lo = c[i + 1];
                 c[i + 1] = z ? T(0) : c[i + 1];
                 c[i] = z ? lo : c[i];
@@ -169,13 +207,13 @@ OZK_HD void strict_normalize(T* c) {
         }
         // trailing zeros written by the reference's compaction are +0
 #pragma unroll
-        for (int i = 0; i < K; ++i) c[i] = (c[i] == T(0)) ? T(0) : c[i];
+        for (int i = 0; i < K; ++i) c[i] = is_zero<kInt>(c[i]) ? T(0) : c[i];
         bool changed = false;
 #pragma unroll
         for (int i = K - 2; i >= 0; --i) {
             T s, e;
             fast_two_sum(c[i], c[i + 1], s, e);
-            bool ch = (s != c[i]) || (e != c[i + 1]);
+            bool ch = !same<kInt>(s, c[i]) || !same<kInt>(e, c[i + 1]);
             c[i] = ch ? s : c[i];
             c[i + 1] = ch ? e : c[i + 1];
             changed = changed || ch;
@@ -183,11 +221,11 @@ OZK_HD void strict_normalize(T* c) {
         if (!changed) break;
     }
 #pragma unroll
-    for (int i = 0; i < K; ++i) c[i] = (c[i] == T(0)) ? T(0) : c[i];
+    for (int i = 0; i < K; ++i) c[i] = is_zero<kInt>(c[i]) ? T(0) : c[i];
 }
 
 // multifloat.hpp:133-150 over N terms (zero terms are transparent)
-template <int K, int N, typename T>
+template <int K, int N, bool kInt = false, typename T>
 OZK_HD void extract_components(const T* t, T* out) {
 #pragma unroll
     for (int q = 0; q < K; ++q) out[q] = T(0);
@@ -198,7 +236,7 @@ OZK_HD void extract_components(const T* t, T* out) {
         if (j < K) {
             T hi, lo;
             two_sum(acc, t[i], hi, lo);
-            if (lo == T(0)) {
+            if (is_zero<kInt>(lo)) {
                 acc = hi;
             } else {
 #pragma unroll
@@ -215,8 +253,8 @@ OZK_HD void extract_components(const T* t, T* out) {
 // MultiFloat<K> + word (multifloat.hpp:290-300); x is updated in place.  T is
 // the word type: double for DD/TD/QD, float for TS (which uses the generic
 // K >= 3 branch with binary32 words, see oracle/ozk_oracle.c).
-template <int K, typename T = double>
-OZK_HD void kw_add(T* x, T y) {
+template <int K, bool kInt, typename T>
+OZK_HD void kw_add_impl(T* x, T y) {
     if constexpr (K == 2) {
         T s, e;
         two_sum(x[0], y, s, e);
@@ -231,8 +269,8 @@ OZK_HD void kw_add(T* x, T y) {
         }
         T ps, pe;
         fast_two_sum(fs, fe, ps, pe);
-        x[0] = ps == T(0) ? T(0) : ps;
-        x[1] = (pe == T(0) || ps == T(0)) ? T(0) : pe;
+        x[0] = is_zero<kInt>(ps) ? T(0) : ps;
+        x[1] = (is_zero<kInt>(pe) || is_zero<kInt>(ps)) ? T(0) : pe;
     } else {
         // merge_components(x, K, &y, 1): y goes before the first x[i] that
         // does not precede it
@@ -240,7 +278,7 @@ OZK_HD void kw_add(T* x, T y) {
         bool placed = false;
 #pragma unroll
         for (int i = 0; i <= K; ++i) {
-            bool take_x = !placed && i < K && merge_before(x[i < K ? i : 0], y);
+            bool take_x = !placed && i < K && merge_before<kInt>(x[i < K ? i : 0], y);
             T prev = x[i > 0 ? i - 1 : 0];
             T cur = x[i < K ? i : K - 1];
             m[i] = placed ? prev : (take_x ? cur : y);
@@ -265,12 +303,43 @@ OZK_HD void kw_add(T* x, T y) {
         }
         m[0] = s;
         // from_expansion
-        extract_components<K, K + 1>(m, x);
-        strict_normalize<K>(x);
-        if (x[0] == T(0) || !is_finite(x[0])) non_finite<K>(rn_add(x[0], T(0)), x);
+        extract_components<K, K + 1, kInt>(m, x);
+        strict_normalize<K, kInt>(x);
+        if (is_zero<kInt>(x[0]) || !is_finite(x[0])) non_finite<K>(rn_add(x[0], T(0)), x);
     }
 }
 
+#if defined(__CUDA_ARCH__)
+template <int K, typename T>
+__device__ __noinline__ void kw_add_slow(T* x, T y) {
+    kw_add_impl<K, false>(x, y);
+}
+#endif
+
+// Integer-compare fast path: bit-exact (tests/test_kword_host.py) but measured
+// slower on B200 in both slice-GEMM epilogues (INT8 engine TD 384 vs 330 ms,
+// QD 736 vs 612 ms at n = 8192), so it is off by default.
+#ifndef OZK_KW_INTCMP
+#define OZK_KW_INTCMP 0
+#endif
+
+template <int K, typename T = double>
+OZK_HD void kw_add(T* x, T y) {
+#if defined(__CUDA_ARCH__) && OZK_KW_INTCMP
+    // integer comparisons whenever they are provably identical (see Bits<>);
+    // anything near the overflow threshold or non-finite takes the reference
+    // floating-point comparisons out of line
+    bool ok = safe_word(y);
+#pragma unroll
+    for (int i = 0; i < K; ++i) ok = ok && safe_word(x[i]);
+    if (ok)
+        kw_add_impl<K, true>(x, y);
+    else
+        kw_add_slow<K>(x, y);
+#else
+    kw_add_impl<K, false>(x, y);
+#endif
+}
 
 // -MultiFloat<K> (multifloat.hpp:265-269): zero words stay +0.
 template <int K, typename T>

@@ -158,3 +158,27 @@ def test_kword_add_kword_matches_reference(kwkw, ref, K):
     assert lib.ref_mf_add_mf(K, n, x.ctypes.data, y.ctypes.data, want.ctypes.data) == 0
     bad = np.flatnonzero((got.view(np.uint64) != want.view(np.uint64)).any(axis=1))
     assert bad.size == 0, (bad.size, x[bad[0]], y[bad[0]], got[bad[0]], want[bad[0]])
+
+
+@pytest.mark.parametrize("K", [2, 3, 4])
+def test_kword_add_integer_compare_variant(ref, port, K):
+    """The device's fast path (bit-pattern comparisons, kw_add_impl<K, true>)
+    equals the reference on every input it is used for: finite words below
+    2^1000 (kword.cuh Bits<>)."""
+    import __graft_entry__
+    if not os.path.exists(SO):
+        __graft_entry__._build_test_helpers()
+    lib = ctypes.CDLL(SO)
+    lib.kw_host_add_int.argtypes = [ctypes.c_int, ctypes.c_size_t, ctypes.c_void_p,
+                                    ctypes.c_void_p, ctypes.c_void_p]
+    cpu = _checker(ref, port)
+    rng = np.random.default_rng(4321 + K)
+    x, y = _cases(K, cpu, rng, 200_000)
+    safe = (np.abs(x) < 2.0 ** 1000).all(axis=1) & (np.abs(y) < 2.0 ** 1000)
+    safe &= np.isfinite(x).all(axis=1) & np.isfinite(y)
+    x, y = np.ascontiguousarray(x[safe]), np.ascontiguousarray(y[safe])
+    got = np.empty_like(x)
+    assert lib.kw_host_add_int(K, x.shape[0], x.ctypes.data, y.ctypes.data, got.ctypes.data) == 0
+    want = cpu.mf_add_double(K, x, y)
+    bad = np.flatnonzero((got.view(np.uint64) != want.view(np.uint64)).any(axis=1))
+    assert bad.size == 0, (bad.size, x[bad[0]], y[bad[0]], got[bad[0]], want[bad[0]])

@@ -1,0 +1,31 @@
+"""A/B timing of experimental libozk builds (INT8 engine), n=8192: python tools/variants_bench.py LIB..."""
+import ctypes
+import statistics
+import sys
+
+import torch
+
+sys.path.insert(0, ".")
+from paper_2301_09960_b200._lib import OzkProfile, load  # noqa: E402
+
+n = 8192
+sh = torch.cuda.current_stream().cuda_stream
+libs = [(p, load(p)) for p in sys.argv[1:]]
+for fmt, d in ((2, 6), (3, 9), (4, 12)):
+    A = torch.empty((n, n, fmt), dtype=torch.float64, device="cuda")
+    B = torch.empty_like(A)
+    C = torch.empty_like(A)
+    libs[0][1].ozk_gen_eq1_device(fmt, n, n, 1, A.data_ptr(), sh)
+    libs[0][1].ozk_gen_eq1_device(fmt, n, n, 2, B.data_ptr(), sh)
+    for path, lib in libs:
+        lib.ozk_set_engine(2)
+        prof = OzkProfile()
+        ts = []
+        for it in range(3):
+            assert lib.ozk_ozaki_gemm_device(fmt, n, n, n, A.data_ptr(), B.data_ptr(), d, 0.0,
+                                             C.data_ptr(), sh, ctypes.byref(prof)) == 0
+            if it:
+                ts.append(prof.product_seconds)
+        print(f"K={fmt} {path.split('/')[-1]}: slice GEMM {statistics.median(ts)*1e3:.1f} ms",
+              flush=True)
+    del A, B, C
