@@ -39,7 +39,7 @@ NAMES = {"dd": "DD", "td": "TD", "qd": "QD", "ts": "TS"}
 def fmt_info(fmt):
     code, K, d = WORKLOADS[fmt]
     return code, K, d, (4 if fmt == "ts" else 8)
-KERNELS_PER_STEP = 4  # split A, transpose B, split B, fused slice GEMM
+KERNELS_PER_STEP = 4  # split A, transpose B, split B, fused slice GEMM (either engine)
 
 
 def parse():
@@ -53,6 +53,9 @@ def parse():
     p.add_argument("--d", type=int, default=None)
     p.add_argument("--variants", default="dd,qd,ts",
                    help="other formats timed (1 step each) and reported under 'variants'")
+    p.add_argument("--engine", choices=["auto", "dmma", "int8"], default="auto",
+                   help="slice-product engine (bit-identical results; auto = INT8 where it "
+                        "applies)")
     p.add_argument("--spread", type=int, default=0,
                    help="config 5: scale every element by 2^U[-s,s] (ill-conditioned inputs)")
     p.add_argument("--cpu-sample", type=int, default=1024,
@@ -202,6 +205,51 @@ def config_of(args, K, d, n):
 # ---------------------------------------------------------------------------
 # our arm
 # ---------------------------------------------------------------------------
+ENGINE_CODES = {"auto": 0, "dmma": 1, "int8": 2}
+ENGINE_NAMES = {1: "dmma", 2: "int8"}
+
+
+def time_engine(lib, OzkProfile, code, n, d, A, B, C, sh, engine, warmup=1, steps=1):
+    """One format/engine on resident inputs: (seconds per step, kernel seconds, engine)."""
+    import torch
+    lib.ozk_set_engine(ENGINE_CODES[engine])
+    prof = OzkProfile()
+
+    def call():
+        st = lib.ozk_ozaki_gemm_device(code, n, n, n, A.data_ptr(), B.data_ptr(), d, 0.0,
+                                       C.data_ptr(), sh, ctypes.byref(prof))
+        if st != 0:
+            raise RuntimeError(lib.ozk_last_error().decode())
+
+    for _ in range(warmup):
+        call()
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    kern = []
+    e0.record(stream)
+    for _ in range(steps):
+        call()
+        kern.append(prof.product_seconds)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) * 1e-3 / steps, statistics.mean(kern), ENGINE_NAMES[prof.engine]
+
+
+def engine_summary(eng, n, d, t_step, t_kern, peak_fp64, peak_i8):
+    P = d * (d + 1) // 2
+    fp64_equiv = P * 2.0 * n ** 3 / t_kern / 1e12
+    out = {"engine": eng, "value": round(2.0 * n ** 3 / t_step / 1e9, 3), "unit": "GFLOP/s",
+           "ms_per_step": round(1e3 * t_step, 3), "slice_gemm_ms": round(1e3 * t_kern, 3),
+           "slice_gemm_fp64_equiv_tflops": round(fp64_equiv, 3)}
+    if eng == "dmma":
+        out["slice_dgemm_frac_of_fp64_peak"] = round(fp64_equiv / peak_fp64, 4)
+    else:
+        i8 = 9 * P * 2.0 * n ** 3 / t_kern / 1e12
+        out["int8_tensor_tops"] = round(i8, 1)
+        out["frac_of_int8_peak"] = round(i8 / peak_i8, 4)
+    return out
+
+
 def run_ours(args):
     import torch
 
@@ -217,6 +265,7 @@ def run_ours(args):
     stream = torch.cuda.current_stream()
     wdt = torch.float32 if wb == 4 else torch.float64
     sh = stream.cuda_stream
+    lib.ozk_set_engine(ENGINE_CODES[args.engine])
 
     if world > 1:
         import torch.distributed as dist
@@ -234,7 +283,8 @@ def run_ours(args):
     check(lib.ozk_gen_spread_device(code, n, n, 1, args.spread, A.data_ptr(), sh))
     check(lib.ozk_gen_spread_device(code, n, n, 2, args.spread, B.data_ptr(), sh))
 
-    peak = lib.ozk_probe_dmma_tflops(20000, sh)
+    peak_fp64 = lib.ozk_probe_dmma_tflops(20000, sh)
+    peak_i8 = lib.ozk_probe_i8_tops(4000, sh)
 
     if world == 1:
         C = torch.empty((n, n, K), dtype=wdt, device="cuda")
@@ -271,22 +321,51 @@ def run_ours(args):
         t = torch.tensor([t_step], device="cuda")
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         t_step = float(t.item())
-    flops_eff = 2.0 * n ** 3
-    value = flops_eff / t_step / 1e9
+    engine_used = ENGINE_NAMES.get(prof.engine, "dmma") if world == 1 else "dmma"
+    value = 2.0 * n ** 3 / t_step / 1e9
     t_kern = statistics.mean(kern)
     rows_local = n if world == 1 else eng.rows_local
-    kern_flops = P * 2.0 * rows_local * n * n
-    achieved = kern_flops / t_kern / 1e12
+    fp64_work = P * 2.0 * rows_local * n * n
+    if engine_used == "int8":
+        kern_work = 9 * fp64_work  # 9 int8 digit GEMMs per slice pair
+        roof = {"bound": "tensor", "kernel": "pair_gemm_i8_kernel (tcgen05.mma kind::i8 + K-word "
+                "epilogue)", "achieved": round(kern_work / t_kern / 1e12, 2),
+                "peak": round(peak_i8, 2), "unit": "TFLOP/s",
+                "frac": round(kern_work / t_kern / 1e12 / peak_i8, 4), "traffic": None,
+                "work_per_launch": f"9*P*2*m*n*l = {kern_work:.4g} int8 tensor ops "
+                                   "(counted like flops: 2 per multiply-add)",
+                "peak_source": "dense INT8 tcgen05 ceiling measured in this run "
+                               "(ozk_probe_i8_tops: M=128 N=256 kind::i8 MMAs from smem, one "
+                               "CTA per SM); nominal B200 dense INT8 4.5 POPS"}
+    else:
+        roof = {"bound": "tensor", "kernel": "pair_gemm_kernel (DMMA + K-word epilogue)",
+                "achieved": round(fp64_work / t_kern / 1e12, 3), "peak": round(peak_fp64, 3),
+                "unit": "TFLOP/s", "frac": round(fp64_work / t_kern / 1e12 / peak_fp64, 4),
+                "traffic": None, "work_per_launch": f"P*2*m*n*l = {fp64_work:.4g} flop",
+                "peak_source": "FP64 DMMA ceiling measured in this run (ozk_probe_dmma_tflops: "
+                               "register-resident mma.m8n8k4.f64 on all SMs); MEASURED_PEAKS.json "
+                               "has no FP64 figure; nominal B200 FP64 tensor 40 TF"}
 
     e2e = None
     if not args.no_e2e and world == 1:
         e2e = run_e2e(args, lib, OzkProfile, A, B, code, K, wb, d, n)
 
+    engines = {}
     variants = []
     if world == 1:
+        # both slice-product engines on the same resident inputs (results are
+        # bit-identical; the DMMA run carries the BASELINE metric's "slice DGEMM %
+        # of FP64 peak")
+        for e in ("dmma", "int8"):
+            if e == engine_used:
+                engines[e] = engine_summary(e, n, d, t_step, t_kern, peak_fp64, peak_i8)
+            elif wb == 8:
+                ts, tk, used = time_engine(lib, OzkProfile, code, n, d, A, B, C, sh, e)
+                engines[e] = engine_summary(used, n, d, ts, tk, peak_fp64, peak_i8)
+        lib.ozk_set_engine(ENGINE_CODES[args.engine])
         del C
         for fmt in [v for v in args.variants.split(",") if v and v != args.format]:
-            variants.append(run_variant(lib, OzkProfile, fmt, n, peak, sh))
+            variants.append(run_variant(lib, OzkProfile, fmt, n, peak_fp64, peak_i8, sh, args))
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline and args.format != "ts":
@@ -296,25 +375,19 @@ def run_ours(args):
                          f"{n}x{args.cpu_sample}, D={d}, one call ({dt:.2f} s)"}
 
     if rank == 0:
+        dm = engines.get("dmma", {})
         line = {
             "metric": METRIC, "value": round(value, 3), "unit": "GFLOP/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * t_step, 3),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic: Eq. (1)-distributed K-word matrices generated on device "
                     "(counter-based splitmix64, csrc/gen.cu)",
-            "config": config_of(args, K, d, n),
-            "slice_dgemm_frac_of_fp64_peak": round(achieved / peak, 4) if peak > 0 else None,
+            "config": dict(config_of(args, K, d, n), engine=engine_used),
+            "slice_dgemm_frac_of_fp64_peak": dm.get("slice_dgemm_frac_of_fp64_peak"),
             "phases_ms": {"split": round(1e3 * statistics.mean(split), 3),
                           "slice_gemm_fused_accumulate": round(1e3 * t_kern, 3)},
-            "roofline": {"bound": "tensor", "kernel": "pair_gemm_kernel (DMMA + K-word epilogue)",
-                         "achieved": round(achieved, 3), "peak": round(peak, 3),
-                         "unit": "TFLOP/s", "frac": round(achieved / peak, 4) if peak > 0 else None,
-                         "traffic": None,
-                         "work_per_launch": f"P*2*m*n*l = {kern_flops:.4g} flop",
-                         "peak_source": "FP64 DMMA ceiling measured in this run "
-                                        "(ozk_probe_dmma_tflops: register-resident "
-                                        "mma.m8n8k4.f64 on all SMs); MEASURED_PEAKS.json has "
-                                        "no FP64 figure; nominal B200 FP64 tensor 40 TF"},
+            "roofline": roof,
+            "engines": engines,
             "gpu_launches": KERNELS_PER_STEP * args.steps,
             "clocks": clk,
             "e2e": e2e,
@@ -322,6 +395,7 @@ def run_ours(args):
             "variants": variants,
         }
         print(json.dumps(line), flush=True)
+    lib.ozk_set_engine(0)
     if world > 1:
         torch.distributed.destroy_process_group()
     return 0
@@ -351,44 +425,32 @@ def run_e2e(args, lib, OzkProfile, A, B, code, K, wb, d, n):
     t = statistics.mean(times)
     return {"value": round(2.0 * n ** 3 / t / 1e9, 3), "unit": "GFLOP/s",
             "h2d_bytes_per_step": 2 * n * n * K * wb, "d2h_bytes_per_step": n * n * K * wb,
-            "ms_per_step": round(1e3 * t, 3), "api": "ozk_ozaki_gemm (host buffers, pinned)"}
+            "ms_per_step": round(1e3 * t, 3), "api": "ozk_ozaki_gemm (host buffers, pinned)",
+            "engine": ENGINE_NAMES.get(prof.engine, "?")}
 
 
-def run_variant(lib, OzkProfile, fmt, n, peak, sh):
+def run_variant(lib, OzkProfile, fmt, n, peak_fp64, peak_i8, sh, args):
     import torch
     code, K, d, wb = fmt_info(fmt)
-    P = d * (d + 1) // 2
     wdt = torch.float32 if wb == 4 else torch.float64
     A = torch.empty((n, n, K), dtype=wdt, device="cuda")
     B = torch.empty((n, n, K), dtype=wdt, device="cuda")
     C = torch.empty((n, n, K), dtype=wdt, device="cuda")
-    lib.ozk_gen_eq1_device(code, n, n, 1, A.data_ptr(), sh)
-    lib.ozk_gen_eq1_device(code, n, n, 2, B.data_ptr(), sh)
-    prof = OzkProfile()
-
-    def call():
-        st = lib.ozk_ozaki_gemm_device(code, n, n, n, A.data_ptr(), B.data_ptr(), d, 0.0,
-                                       C.data_ptr(), sh, ctypes.byref(prof))
-        if st != 0:
-            raise RuntimeError(lib.ozk_last_error().decode())
-
-    call()
-    stream = torch.cuda.current_stream()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    call()
-    e1.record(stream)
-    torch.cuda.synchronize()
-    t = e0.elapsed_time(e1) * 1e-3
-    achieved = P * 2.0 * n ** 3 / prof.product_seconds / 1e12
-    out = {"workload": f"{NAMES[fmt]} Ozaki GEMM n={n} D={d}",
-           "value": round(2.0 * n ** 3 / t / 1e9, 3),
-           "unit": "GFLOP/s", "ms_per_step": round(1e3 * t, 3),
-           "split_ms": round(1e3 * prof.split_seconds, 3),
-           "slice_gemm_tflops": round(achieved, 3),
-           "slice_dgemm_frac_of_fp64_peak": round(achieved / peak, 4) if peak > 0 else None}
+    lib.ozk_gen_spread_device(code, n, n, 1, args.spread, A.data_ptr(), sh)
+    lib.ozk_gen_spread_device(code, n, n, 2, args.spread, B.data_ptr(), sh)
+    out = {"workload": f"{NAMES[fmt]} Ozaki GEMM n={n} D={d}"}
+    engs = ("dmma", "int8") if wb == 8 else ("dmma",)
+    for e in engs:
+        ts, tk, used = time_engine(lib, OzkProfile, code, n, d, A, B, C, sh, e)
+        out[e] = engine_summary(used, n, d, ts, tk, peak_fp64, peak_i8)
+    lib.ozk_set_engine(ENGINE_CODES[args.engine])
+    best = min((out[e] for e in engs), key=lambda r: r["ms_per_step"])
+    out["value"], out["unit"], out["engine"] = best["value"], "GFLOP/s", best["engine"]
     if fmt == "ts":
         # config 4 comparator: the direct triple-single GEMM kernel on the same inputs
+        stream = torch.cuda.current_stream()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
         def direct():
             st = lib.ozk_ts_direct_gemm_device(n, n, n, A.data_ptr(), B.data_ptr(), C.data_ptr(),
                                                sh)

@@ -208,6 +208,11 @@ ozk_status ozk_gen_spread_device(ozk_format fmt, size_t rows, size_t cols, uint6
  * denominator for the slice GEMMs).  Returns < 0 on failure. */
 double ozk_probe_dmma_tflops(int iters, void* stream);
 
+/* Dense INT8 tensor ceiling (tcgen05.mma kind::i8, M=128 N=256, one CTA per SM,
+ * operands resident in shared memory) in TOPS -- the INT8 engine's roofline
+ * denominator.  Returns < 0 on failure. */
+double ozk_probe_i8_tops(int iters, void* stream);
+
 const char* ozk_last_error(void);
 int ozk_version(void);
 

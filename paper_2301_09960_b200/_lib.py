@@ -67,6 +67,7 @@ SIGNATURES = {
     "ozk_ts_direct_gemm": (ctypes.c_int, [_sz, _sz, _sz, _dp, _dp, _dp]),
     "ozk_ts_direct_gemm_device": (ctypes.c_int, [_sz, _sz, _sz, _dp, _dp, _dp, ctypes.c_void_p]),
     "ozk_probe_dmma_tflops": (ctypes.c_double, [ctypes.c_int, ctypes.c_void_p]),
+    "ozk_probe_i8_tops": (ctypes.c_double, [ctypes.c_int, ctypes.c_void_p]),
     "ozk_set_engine": (ctypes.c_int, [ctypes.c_int]),
     "ozk_get_engine": (ctypes.c_int, []),
     "ozk_last_error": (ctypes.c_char_p, []),
