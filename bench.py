@@ -235,7 +235,14 @@ def time_engine(lib, OzkProfile, code, n, d, A, B, C, sh, engine, warmup=1, step
     return e0.elapsed_time(e1) * 1e-3 / steps, statistics.mean(kern), ENGINE_NAMES[prof.engine]
 
 
-def engine_summary(eng, n, d, t_step, t_kern, peak_fp64, peak_i8):
+def int8_digits(fmt, l):
+    """Digits per slice integer on the INT8 engine (csrc/api.cu int8_digits)."""
+    if fmt != "ts":
+        return 3
+    return 1 if l > 4096 else 2
+
+
+def engine_summary(eng, n, d, t_step, t_kern, peak_fp64, peak_i8, nd=3):
     P = d * (d + 1) // 2
     fp64_equiv = P * 2.0 * n ** 3 / t_kern / 1e12
     out = {"engine": eng, "value": round(2.0 * n ** 3 / t_step / 1e9, 3), "unit": "GFLOP/s",
@@ -244,7 +251,8 @@ def engine_summary(eng, n, d, t_step, t_kern, peak_fp64, peak_i8):
     if eng == "dmma":
         out["slice_dgemm_frac_of_fp64_peak"] = round(fp64_equiv / peak_fp64, 4)
     else:
-        i8 = 9 * P * 2.0 * n ** 3 / t_kern / 1e12
+        i8 = nd * nd * P * 2.0 * n ** 3 / t_kern / 1e12  # nd^2 int8 digit GEMMs per pair
+        out["int8_digit_gemms_per_pair"] = nd * nd
         out["int8_tensor_tops"] = round(i8, 1)
         out["frac_of_int8_peak"] = round(i8 / peak_i8, 4)
     return out
@@ -326,13 +334,14 @@ def run_ours(args):
     t_kern = statistics.mean(kern)
     rows_local = n if world == 1 else eng.rows_local
     fp64_work = P * 2.0 * rows_local * n * n
+    nd = int8_digits(args.format, n)
     if engine_used == "int8":
-        kern_work = 9 * fp64_work  # 9 int8 digit GEMMs per slice pair
+        kern_work = nd * nd * fp64_work  # nd^2 int8 digit GEMMs per slice pair
         roof = {"bound": "tensor", "kernel": "pair_gemm_i8_kernel (tcgen05.mma kind::i8 + K-word "
                 "epilogue)", "achieved": round(kern_work / t_kern / 1e12, 2),
                 "peak": round(peak_i8, 2), "unit": "TFLOP/s",
                 "frac": round(kern_work / t_kern / 1e12 / peak_i8, 4), "traffic": None,
-                "work_per_launch": f"9*P*2*m*n*l = {kern_work:.4g} int8 tensor ops "
+                "work_per_launch": f"{nd*nd}*P*2*m*n*l = {kern_work:.4g} int8 tensor ops "
                                    "(counted like flops: 2 per multiply-add)",
                 "peak_source": "dense INT8 tcgen05 ceiling measured in this run "
                                "(ozk_probe_i8_tops: M=128 N=256 kind::i8 MMAs from smem, one "
@@ -358,10 +367,10 @@ def run_ours(args):
         # of FP64 peak")
         for e in ("dmma", "int8"):
             if e == engine_used:
-                engines[e] = engine_summary(e, n, d, t_step, t_kern, peak_fp64, peak_i8)
-            elif wb == 8:
+                engines[e] = engine_summary(e, n, d, t_step, t_kern, peak_fp64, peak_i8, nd)
+            else:
                 ts, tk, used = time_engine(lib, OzkProfile, code, n, d, A, B, C, sh, e)
-                engines[e] = engine_summary(used, n, d, ts, tk, peak_fp64, peak_i8)
+                engines[e] = engine_summary(used, n, d, ts, tk, peak_fp64, peak_i8, nd)
         lib.ozk_set_engine(ENGINE_CODES[args.engine])
         del C
         for fmt in [v for v in args.variants.split(",") if v and v != args.format]:
@@ -439,10 +448,10 @@ def run_variant(lib, OzkProfile, fmt, n, peak_fp64, peak_i8, sh, args):
     lib.ozk_gen_spread_device(code, n, n, 1, args.spread, A.data_ptr(), sh)
     lib.ozk_gen_spread_device(code, n, n, 2, args.spread, B.data_ptr(), sh)
     out = {"workload": f"{NAMES[fmt]} Ozaki GEMM n={n} D={d}"}
-    engs = ("dmma", "int8") if wb == 8 else ("dmma",)
+    engs = ("dmma", "int8")
     for e in engs:
         ts, tk, used = time_engine(lib, OzkProfile, code, n, d, A, B, C, sh, e)
-        out[e] = engine_summary(used, n, d, ts, tk, peak_fp64, peak_i8)
+        out[e] = engine_summary(used, n, d, ts, tk, peak_fp64, peak_i8, int8_digits(fmt, n))
     lib.ozk_set_engine(ENGINE_CODES[args.engine])
     best = min((out[e] for e in engs), key=lambda r: r["ms_per_step"])
     out["value"], out["unit"], out["engine"] = best["value"], "GFLOP/s", best["engine"]

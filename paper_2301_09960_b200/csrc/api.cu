@@ -45,9 +45,23 @@ int engine_setting() {
     return e;
 }
 
-bool int8_applicable(int fmt, size_t l, int d) {
-    return word_bytes_of_fmt(fmt) == 8 && d >= 2 && l > 512 && l < 43690;
+// Digits per slice integer for the INT8 engine, 0 = not applicable.  The
+// slice integer is bounded by 2^(S + 1 - sigma) (S = 53 / 24); signed
+// base-256 digits hold |M| <= 127 (1), 32639 (2), 8355711 (3).  Every digit
+// level (at most 3 digit products per output) stays below 2^31 for l < 43690.
+int int8_digits(int fmt, size_t l, int d) {
+    if (d < 2 || l >= 43690) return 0;
+    int cl = 0;
+    while ((size_t(1) << cl) < l) ++cl;
+    const int S = word_bytes_of_fmt(fmt) == 4 ? 24 : 53;
+    const int bits = S + 1 - (S + cl + 1) / 2;  // |M| <= 2^bits
+    if (bits <= 6) return 1;
+    if (bits <= 14) return 2;
+    if (bits <= 22) return word_bytes_of_fmt(fmt) == 8 ? 3 : 0;
+    return 0;  // binary64 slices at l <= 512 would need 4 digits: DMMA engine
 }
+
+bool int8_applicable(int fmt, size_t l, int d) { return int8_digits(fmt, l, d) > 0; }
 
 ozk_status fail(ozk_status s, const std::string& msg) {
     g_last_error = msg;
@@ -206,12 +220,14 @@ ozk_status ozaki_device_impl(int fmt, size_t m, size_t l, size_t n, const void* 
     const int eng = engine_setting();
     const bool use_i8 = eng != OZK_ENGINE_DMMA && int8_applicable(fmt, l, d);
     if (eng == OZK_ENGINE_INT8 && !use_i8)
-        return fail(OZK_EPARAM, "ozaki_gemm: INT8 engine needs binary64 words, D >= 2, 512 < l < 43690");
+        return fail(OZK_EPARAM, "ozaki_gemm: INT8 engine needs D >= 2 and 512 < l < 43690 "
+                                "(binary64 words) or l < 43690 (TS)");
+    const int nd = use_i8 ? int8_digits(fmt, l, d) : 0;
     const size_t ld8 = (l + 15) & ~size_t(15);
     DevBuf sa, sb, work, flags, da8, db8, ga, gb;
     if (use_i8) {
-        OZK_CUDA(da8.alloc((size_t)d * 3 * m * ld8, st), "ozaki_gemm: digits A");
-        OZK_CUDA(db8.alloc((size_t)d * 3 * n * ld8, st), "ozaki_gemm: digits B");
+        OZK_CUDA(da8.alloc((size_t)d * nd * m * ld8, st), "ozaki_gemm: digits A");
+        OZK_CUDA(db8.alloc((size_t)d * nd * n * ld8, st), "ozaki_gemm: digits B");
         OZK_CUDA(ga.alloc(sizeof(int) * d * m, st), "ozaki_gemm: exponents A");
         OZK_CUDA(gb.alloc(sizeof(int) * d * n, st), "ozaki_gemm: exponents B");
     } else {
@@ -228,16 +244,18 @@ ozk_status ozaki_device_impl(int fmt, size_t m, size_t l, size_t n, const void* 
     const bool want_max = drop > 0.0;
     DigitOut digA, digB;
     if (use_i8) {
+        digA.nd = nd;
         digA.digits = da8.as<int8_t>();
         digA.ld = ld8;
         digA.digit_stride = m * ld8;
-        digA.slice_stride = 3 * m * ld8;
+        digA.slice_stride = (size_t)nd * m * ld8;
         digA.exps = ga.as<int>();
         digA.exp_stride = m;
+        digB.nd = nd;
         digB.digits = db8.as<int8_t>();
         digB.ld = ld8;
         digB.digit_stride = n * ld8;
-        digB.slice_stride = 3 * n * ld8;
+        digB.slice_stride = (size_t)nd * n * ld8;
         digB.exps = gb.as<int>();
         digB.exp_stride = n;
     }
@@ -288,14 +306,15 @@ ozk_status ozaki_device_impl(int fmt, size_t m, size_t l, size_t n, const void* 
         OZK_CUDA(cudaMemsetAsync(c, 0, elem_bytes(fmt) * m * n, st), "ozaki_gemm: zero C");
     } else if (use_i8) {
         I8Operands op{};
+        op.nd = nd;
         op.a = da8.as<int8_t>();
         op.a_ld = ld8;
         op.a_digit_stride = m * ld8;
-        op.a_slice_stride = 3 * m * ld8;
+        op.a_slice_stride = (size_t)nd * m * ld8;
         op.b = db8.as<int8_t>();
         op.b_ld = ld8;
         op.b_digit_stride = n * ld8;
-        op.b_slice_stride = 3 * n * ld8;
+        op.b_slice_stride = (size_t)nd * n * ld8;
         op.gA = ga.as<int>();
         op.gB = gb.as<int>();
         op.m = m;
@@ -304,7 +323,7 @@ ozk_status ozaki_device_impl(int fmt, size_t m, size_t l, size_t n, const void* 
         op.d = d;
         op.c = c;
         op.ldc = n;
-        OZK_CUDA(launch_pair_gemm_i8(K, op, pl, st, sms), "ozaki_gemm: INT8 slice GEMM");
+        OZK_CUDA(launch_pair_gemm_i8(K, wb, op, pl, st, sms), "ozaki_gemm: INT8 slice GEMM");
     } else {
         OZK_CUDA(launch_pair_gemm(K, kAccumulate, prob, pl, st, sms, wb), "ozaki_gemm: slice GEMM");
     }

@@ -38,22 +38,36 @@
 namespace ozk {
 namespace {
 
-constexpr int BM = 128, BN = 64, BKB = 128;   // tile M, tile N, k bytes per stage
-constexpr int kStages = 3;
+constexpr int BM = 128, BKB = 128;            // tile M, k bytes per stage
 constexpr int kEpiGroups = 2;                 // epilogue warpgroups (column halves)
 constexpr int kThreads = (4 + 4 * kEpiGroups) * 32;
-constexpr int kEpiCols = 64 / kEpiGroups;     // columns per epilogue thread
-// K-word adds unrolled per epilogue step, per format (B200 A/B at n = 8192,
-// tools/variants_bench.py): DD 8 (104.6 ms; 2: 109.1), TD 2 (316 ms; 8: 349),
-// QD 2 (582 ms; 8: 664) -- the K >= 3 bodies are large enough that more
-// unrolling costs instruction-cache misses and registers instead of latency.
-template <int K> constexpr int kChunkFor = (K == 2) ? 8 : 2;
-constexpr int kATile = BM * BKB;              // 16 KiB per digit
-constexpr int kBTile = BN * BKB;              // 8 KiB per digit
-constexpr int kStageBytes = 3 * kATile + 3 * kBTile;
-constexpr int kSmemBytes = kStages * kStageBytes + 1024 + 256;
-constexpr int kTmemCols = 512;                // 5 levels x 64 columns used
 constexpr int kGroupM = 8;
+constexpr int kSmemBudget = 200 * 1024;       // operand ring
+
+// Compile-time shape of one engine instance.
+//   W   word type of C (double: DD/TD/QD, float: TS)
+//   ND  int8 digits per slice integer (3 for binary64 slices at l > 512; 1 for
+//       TS slices at l > 4096, where |M| <= 2^(25 - sigma) <= 64; 2 below)
+//   BN  tile width; 2*ND-1 level accumulators of BN TMEM columns each
+template <int K, typename W, int ND, int BN>
+struct I8Cfg {
+    static constexpr int kLevels = 2 * ND - 1;
+    static constexpr int kATile = BM * BKB;
+    static constexpr int kBTile = BN * BKB;
+    static constexpr int kStageBytes = ND * (kATile + kBTile);
+    static constexpr int kStages = kSmemBudget / kStageBytes < 8 ? kSmemBudget / kStageBytes : 8;
+    static constexpr int kSmemBytes = kStages * kStageBytes + 1024 + 256;
+    static constexpr int kTmemCols = kLevels * BN <= 32 ? 32 : kLevels * BN <= 64 ? 64
+                                   : kLevels * BN <= 128 ? 128 : kLevels * BN <= 256 ? 256 : 512;
+    static constexpr int kEpiCols = BN / kEpiGroups;  // columns per epilogue thread
+    // K-word adds unrolled per epilogue step (B200 A/B at n = 8192,
+    // tools/variants_bench.py): DD 8 (104.6 ms; 2: 109.1), TD 2 (316 ms; 8: 349),
+    // QD 2 (582 ms; 8: 664) -- the K >= 3 bodies are large enough that more
+    // unrolling costs instruction-cache misses and registers instead of latency.
+    static constexpr int kChunk = (K == 2 && sizeof(W) == 8) ? 8 : 2;
+    static_assert(kStages >= 2, "operand ring too small");
+    static_assert(kLevels * BN <= 512, "TMEM");
+};
 
 struct MapsI8 {
     CUtensorMap a;  // 4D: (k, row, digit, slice)
@@ -162,10 +176,14 @@ __device__ __forceinline__ TileCoord tile_of(int id, int tiles_m, int tiles_n) {
     return TileCoord{first_m + in_group % gm, in_group / gm};
 }
 
-template <int K>
+template <int K, typename W, int ND, int BN>
 __global__ void __launch_bounds__(kThreads, 1)
 pair_gemm_i8_kernel(const __grid_constant__ MapsI8 maps, const __grid_constant__ PairList pairs,
                     I8Problem prob, int tiles_m, int tiles_n) {
+    using Cfg = I8Cfg<K, W, ND, BN>;
+    constexpr int kStages = Cfg::kStages, kStageBytes = Cfg::kStageBytes;
+    constexpr int kATile = Cfg::kATile, kBTile = Cfg::kBTile, kEpiCols = Cfg::kEpiCols;
+    constexpr int kTmemCols = Cfg::kTmemCols, kLevels = Cfg::kLevels;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~uintptr_t(1023));
@@ -219,9 +237,9 @@ pair_gemm_i8_kernel(const __grid_constant__ MapsI8 maps, const __grid_constant__
                     mbar_expect_tx(full, kStageBytes);
                     const uint32_t sa = ring + stage * kStageBytes;
 #pragma unroll
-                    for (int dgt = 0; dgt < 3; ++dgt) {
+                    for (int dgt = 0; dgt < ND; ++dgt) {
                         tma_load_4d(sa + dgt * kATile, &maps.a, full, kb * BKB, tc.tm * BM, dgt, al);
-                        tma_load_4d(sa + 3 * kATile + dgt * kBTile, &maps.b, full, kb * BKB,
+                        tma_load_4d(sa + ND * kATile + dgt * kBTile, &maps.b, full, kb * BKB,
                                     tc.tn * BN, dgt, be);
                     }
                     if (++stage == kStages) {
@@ -250,19 +268,21 @@ pair_gemm_i8_kernel(const __grid_constant__ MapsI8 maps, const __grid_constant__
                     const uint32_t sa = ring + stage * kStageBytes;
 #pragma unroll
                     for (int kc = 0; kc < BKB / 32; ++kc) {
+                        // digit pairs level by level; the first MMA of each
+                        // level in a pair's first chunk overwrites the accumulator
 #pragma unroll
-                        for (int q = 0; q < 9; ++q) {
-                            // digit pairs ordered so each level's first MMA
-                            // (which overwrites) comes first within a chunk
-                            constexpr int ds[9] = {0, 0, 1, 0, 1, 2, 1, 2, 2};
-                            constexpr int dt[9] = {0, 1, 0, 2, 1, 0, 2, 1, 2};
-                            constexpr int first[9] = {1, 1, 0, 1, 0, 0, 1, 0, 1};
-                            const int lvl = ds[q] + dt[q];
-                            const uint64_t da = sw128_desc(sa + ds[q] * kATile + kc * 32);
-                            const uint64_t db =
-                                sw128_desc(sa + 3 * kATile + dt[q] * kBTile + kc * 32);
-                            const uint32_t acc = (kb | kc) ? 1u : (first[q] ? 0u : 1u);
-                            umma_i8(tmem + lvl * BN, da, db, idesc, acc);
+                        for (int lvl = 0; lvl < kLevels; ++lvl) {
+#pragma unroll
+                            for (int ds = 0; ds < ND; ++ds) {
+                                const int dt = lvl - ds;
+                                if (dt < 0 || dt >= ND) continue;
+                                const bool first = ds == (lvl - ND + 1 > 0 ? lvl - ND + 1 : 0);
+                                const uint64_t da = sw128_desc(sa + ds * kATile + kc * 32);
+                                const uint64_t db =
+                                    sw128_desc(sa + ND * kATile + dt * kBTile + kc * 32);
+                                const uint32_t acc = (kb | kc) ? 1u : (first ? 0u : 1u);
+                                umma_i8(tmem + lvl * BN, da, db, idesc, acc);
+                            }
                         }
                     }
                     umma_commit(empty0 + 8 * stage);  // frees the stage when the MMAs retire
@@ -299,16 +319,15 @@ pair_gemm_i8_kernel(const __grid_constant__ MapsI8 maps, const __grid_constant__
                 double y[kEpiCols];
 #pragma unroll
                 for (int c = 0; c < kEpiCols; c += 16) {
-                    int32_t lv[5][16];
+                    int32_t lv[kLevels][16];
 #pragma unroll
-                    for (int u = 0; u < 5; ++u) tmem_ld16(tlane + u * BN + c, lv[u]);
+                    for (int u = 0; u < kLevels; ++u) tmem_ld16(tlane + u * BN + c, lv[u]);
                     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
                     for (int j = 0; j < 16; ++j) {
-                        const long long s = (long long)lv[0][j] + ((long long)lv[1][j] << 8) +
-                                            ((long long)lv[2][j] << 16) +
-                                            ((long long)lv[3][j] << 24) +
-                                            ((long long)lv[4][j] << 32);
+                        long long s = lv[0][j];
+#pragma unroll
+                        for (int u = 1; u < kLevels; ++u) s += (long long)lv[u][j] << (8 * u);
                         y[c + j] = i64_to_f64_exact(s);  // exact: |s| < 2^53
                     }
                 }
@@ -317,26 +336,27 @@ pair_gemm_i8_kernel(const __grid_constant__ MapsI8 maps, const __grid_constant__
                 __syncwarp();
                 if (lane == 0) mbar_arrive(tmem_empty);
                 if (!row_ok) continue;
-                double* cp = static_cast<double*>(prob.c) + (row * prob.ldc + col0) * K;
+                W* cp = static_cast<W*>(prob.c) + (row * prob.ldc + col0) * K;
                 const int* gbp = prob.gB + (size_t)be * prob.gB_stride + col0;
 #pragma unroll 1
-                constexpr int kChunk = kChunkFor<K>;
+                constexpr int kChunk = Cfg::kChunk;
                 for (int c = 0; c < kEpiCols; c += kChunk) {
                     // y[0..kChunk) are this chunk's products; the array is
                     // shifted down after each chunk so every index stays static
-                    double w[kChunk][K];
+                    W w[kChunk][K];
 #pragma unroll
                     for (int j = 0; j < kChunk; ++j) {
                         const bool ok = col0 + c + j < prob.n;
 #pragma unroll
                         for (int k = 0; k < K; ++k)
-                            w[j][k] = (ok && p > 0) ? cp[(c + j) * K + k] : 0.0;
+                            w[j][k] = (ok && p > 0) ? cp[(c + j) * K + k] : W(0);
                     }
 #pragma unroll
                     for (int j = 0; j < kChunk; ++j) {
                         const bool ok = col0 + c + j < prob.n;
                         const int gb = ok ? __ldg(gbp + c + j) : 0;
-                        kw_add<K>(w[j], ldexp_fast(y[j], ga + gb));
+                        // exact scaled slice product (a TS product is exact in binary32)
+                        kw_add<K>(w[j], (W)ldexp_fast(y[j], ga + gb));
                     }
 #pragma unroll
                     for (int j = 0; j < kChunk; ++j) {
@@ -371,14 +391,15 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode_i8() {
     return fn;
 }
 
-template <int K>
+template <int K, typename W, int ND, int BN>
 cudaError_t launch_i8_typed(const I8Operands& op, const PairList& pairs, cudaStream_t st,
                             int num_sms) {
+    using Cfg = I8Cfg<K, W, ND, BN>;
     auto encode = get_encode_i8();
     if (!encode) return cudaErrorNotSupported;
     MapsI8 maps;
     {
-        cuuint64_t dims[4] = {op.l, op.m, 3, (cuuint64_t)op.d};
+        cuuint64_t dims[4] = {op.l, op.m, (cuuint64_t)ND, (cuuint64_t)op.d};
         cuuint64_t strides[3] = {op.a_ld, op.a_digit_stride, op.a_slice_stride};
         cuuint32_t box[4] = {BKB, BM, 1, 1};
         cuuint32_t es[4] = {1, 1, 1, 1};
@@ -389,7 +410,7 @@ cudaError_t launch_i8_typed(const I8Operands& op, const PairList& pairs, cudaStr
             return cudaErrorInvalidValue;
     }
     {
-        cuuint64_t dims[4] = {op.l, op.n, 3, (cuuint64_t)op.d};
+        cuuint64_t dims[4] = {op.l, op.n, (cuuint64_t)ND, (cuuint64_t)op.d};
         cuuint64_t strides[3] = {op.b_ld, op.b_digit_stride, op.b_slice_stride};
         cuuint32_t box[4] = {BKB, BN, 1, 1};
         cuuint32_t es[4] = {1, 1, 1, 1};
@@ -412,23 +433,30 @@ cudaError_t launch_i8_typed(const I8Operands& op, const PairList& pairs, cudaStr
     const int tiles_m = (int)((op.m + BM - 1) / BM), tiles_n = (int)((op.n + BN - 1) / BN);
     const int num_tiles = tiles_m * tiles_n;
     if (num_tiles == 0 || pairs.count == 0) return cudaSuccess;
-    auto kern = pair_gemm_i8_kernel<K>;
-    cudaError_t e =
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+    auto kern = pair_gemm_i8_kernel<K, W, ND, BN>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         Cfg::kSmemBytes);
     if (e != cudaSuccess) return e;
     const int grid = num_tiles < num_sms ? num_tiles : num_sms;
-    kern<<<grid, kThreads, kSmemBytes, st>>>(maps, pairs, prob, tiles_m, tiles_n);
+    kern<<<grid, kThreads, Cfg::kSmemBytes, st>>>(maps, pairs, prob, tiles_m, tiles_n);
     return cudaGetLastError();
 }
 
 } // namespace
 
-cudaError_t launch_pair_gemm_i8(int K, const I8Operands& op, const PairList& pairs,
-                                cudaStream_t st, int num_sms) {
+cudaError_t launch_pair_gemm_i8(int K, int word_bytes, const I8Operands& op,
+                                const PairList& pairs, cudaStream_t st, int num_sms) {
+    if (word_bytes == 4) {  // TS: binary32 words, 1 or 2 digits
+        if (K != 3) return cudaErrorInvalidValue;
+        if (op.nd == 1) return launch_i8_typed<3, float, 1, 128>(op, pairs, st, num_sms);
+        if (op.nd == 2) return launch_i8_typed<3, float, 2, 64>(op, pairs, st, num_sms);
+        return cudaErrorInvalidValue;
+    }
+    if (op.nd != 3) return cudaErrorInvalidValue;
     switch (K) {
-    case 2: return launch_i8_typed<2>(op, pairs, st, num_sms);
-    case 3: return launch_i8_typed<3>(op, pairs, st, num_sms);
-    case 4: return launch_i8_typed<4>(op, pairs, st, num_sms);
+    case 2: return launch_i8_typed<2, double, 3, 64>(op, pairs, st, num_sms);
+    case 3: return launch_i8_typed<3, double, 3, 64>(op, pairs, st, num_sms);
+    case 4: return launch_i8_typed<4, double, 3, 64>(op, pairs, st, num_sms);
     default: return cudaErrorInvalidValue;
     }
 }

@@ -25,9 +25,11 @@ inline size_t slice_ld(size_t inner) { return (inner + 1) & ~size_t(1); }
 //   err     : device flag (DevErr)
 // Optional INT8-digit output of the split (for the exact INT8 slice-product
 // engine): slice a, row r has grid exponent exps[a*exp_stride + r] = g and
-// digits[a*slice_stride + s*digit_stride + r*ld + k], s = 0..2, with
-// piece(r, k) = 2^g * (d0 + 256 d1 + 65536 d2).  digits == nullptr: off.
+// digits[a*slice_stride + s*digit_stride + r*ld + k], s = 0..nd-1, with
+// piece(r, k) = 2^g * sum_s 256^s d_s, g = e + sigma - (S + 1) (S = 53 for
+// binary64 words, 24 for TS).  digits == nullptr: off.
 struct DigitOut {
+    int nd = 3;     // digits written per element (1..3)
     int8_t* digits = nullptr;
     size_t ld = 0, digit_stride = 0, slice_stride = 0;
     int* exps = nullptr;
@@ -78,6 +80,7 @@ cudaError_t launch_pair_gemm(int K, GemmMode mode, const GemmProblem& prob, cons
 // Exact INT8-digit slice products on tcgen05 (gemm_i8.cu).  Digits as written
 // by the split's DigitOut: [d][3][rows][ld] int8, exponents [d][rows].
 struct I8Operands {
+    int nd;         // digits per slice integer (1..3)
     const int8_t* a;
     size_t a_ld, a_digit_stride, a_slice_stride;
     const int8_t* b;
@@ -89,8 +92,8 @@ struct I8Operands {
     void* c;        // K-word AoS, row stride ldc elements
     size_t ldc;
 };
-cudaError_t launch_pair_gemm_i8(int K, const I8Operands& op, const PairList& pairs,
-                                cudaStream_t st, int num_sms);
+cudaError_t launch_pair_gemm_i8(int K, int word_bytes, const I8Operands& op,
+                                const PairList& pairs, cudaStream_t st, int num_sms);
 
 // Device Eq. (1)-distributed K-word generator (synthetic bench inputs).
 // a(i, j) -= c(i, j) in K-word arithmetic (a: row stride lda elements, c dense).

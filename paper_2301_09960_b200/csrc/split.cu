@@ -37,8 +37,8 @@ __device__ __forceinline__ float pow2(float, int e) { return scalbnf(1.0f, e); }
 // "entries too large to shift" guard: ozaki.hpp:109 keeps e + sigma <= 1020
 // (3 binades below binary64's 1023); TS keeps the same margin below 127.
 template <typename T> struct ShiftGuard;
-template <> struct ShiftGuard<double> { static constexpr int max_exp = 1020; };
-template <> struct ShiftGuard<float> { static constexpr int max_exp = 124; };
+template <> struct ShiftGuard<double> { static constexpr int max_exp = 1020; static constexpr int S = 53; };
+template <> struct ShiftGuard<float> { static constexpr int max_exp = 124; static constexpr int S = 24; };
 
 // Block-wide max of a non-negative double; every thread gets the result.
 __device__ __forceinline__ double block_max(double v, double* red) {
@@ -158,16 +158,17 @@ split_rows_kernel(const T* __restrict__ in, size_t in_ld, T* __restrict__ work, 
         }
         T nmx = T(0);
         double pmx = 0.0;
-        // INT8-digit output: the slice row is an integer multiple of
-        // 2^g, g = e + sigma - 54 (the half-grid of ozaki.hpp:15-29), with
-        // |x / 2^g| <= 2^(54 - sigma); written as 3 signed base-256 digits.
-        const int g = (tau == T(0)) ? 0 : (ceil_log2(mx) + sigma - 54);
+        // INT8-digit output: the slice row is an integer multiple of 2^g,
+        // g = e + sigma - (S + 1) (the half-grid of ozaki.hpp:15-29), with
+        // |x / 2^g| <= 2^(S + 1 - sigma); written as nd signed base-256 digits.
+        const int g = (tau == T(0)) ? 0 : (ceil_log2(mx) + sigma - (ShiftGuard<T>::S + 1));
         int8_t* drow = dig.digits ? dig.digits + (size_t)a * dig.slice_stride + r * dig.ld : nullptr;
         if (dig.digits && threadIdx.x == 0) dig.exps[(size_t)a * dig.exp_stride + r] = g;
         for (size_t j = threadIdx.x; j < cols; j += kSplitThreads) {
             if (tau == T(0)) {
                 if (pa) pa[j] = 0.0;
-                if (drow) drow[j] = drow[j + dig.digit_stride] = drow[j + 2 * dig.digit_stride] = 0;
+                if (drow)
+                    for (int q = 0; q < dig.nd; ++q) drow[j + q * dig.digit_stride] = 0;
                 continue;
             }
             T c[K];
@@ -176,14 +177,14 @@ split_rows_kernel(const T* __restrict__ in, size_t in_ld, T* __restrict__ work, 
             const T x = rn_sub(rn_add(c[0], tau), tau);
             if (pa) pa[j] = (double)x;
             if (drow) {
-                const int mi = (int)scalbn((double)x, -g);  // exact integer, |mi| <= 2^22
-                const int d0 = (int)(int8_t)(mi & 0xff);
-                const int m1 = (mi - d0) >> 8;
-                const int d1 = (int)(int8_t)(m1 & 0xff);
-                const int d2 = (m1 - d1) >> 8;
-                drow[j] = (int8_t)d0;
-                drow[j + dig.digit_stride] = (int8_t)d1;
-                drow[j + 2 * dig.digit_stride] = (int8_t)d2;
+                // exact integer; |mi| fits nd digits by the planner's choice of nd
+                int mi = (int)scalbn((double)x, -g);
+                for (int q = 0; q < dig.nd - 1; ++q) {
+                    const int dq = (int)(int8_t)(mi & 0xff);
+                    drow[j + q * dig.digit_stride] = (int8_t)dq;
+                    mi = (mi - dq) >> 8;
+                }
+                drow[j + (dig.nd - 1) * dig.digit_stride] = (int8_t)mi;
             }
             if (x != T(0)) {
                 kw_add<K>(c, -x);  // w -= x  ==  w + (-x)  (multifloat.hpp:302,391)
@@ -196,7 +197,7 @@ split_rows_kernel(const T* __restrict__ in, size_t in_ld, T* __restrict__ work, 
             for (size_t j = cols + threadIdx.x; j < ldk; j += kSplitThreads) pa[j] = 0.0;
         if (drow)
             for (size_t j = cols + threadIdx.x; j < dig.ld; j += kSplitThreads)
-                drow[j] = drow[j + dig.digit_stride] = drow[j + 2 * dig.digit_stride] = 0;
+                for (int q = 0; q < dig.nd; ++q) drow[j + q * dig.digit_stride] = 0;
         if (piece_max) {
             pmx = block_max(pmx, red);
             if (threadIdx.x == 0)

@@ -178,3 +178,23 @@ def test_ts_direct_accuracy(ozk, port):
     err = ex.componentwise_ulp_error(got.astype(np.float64), a.astype(np.float64),
                                      b.astype(np.float64), ref, -72)
     assert err <= 16.0  # grows ~linearly with l; 2.4 at l = 64 on the CPU restatement
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("eng", ["int8", "dmma"])
+@pytest.mark.parametrize("m,l,n,d", [(64, 300, 70, 12), (130, 4097, 129, 15), (200, 5000, 64, 16),
+                                     (33, 700, 40, 8)])
+def test_ts_engines_bitexact(ozk, port, eng, m, l, n, d):
+    """TS on both slice-product engines: INT8 uses 2 digits (l <= 4096) or a
+    single digit (l > 4096: |M| <= 2^(25-sigma) <= 64)."""
+    a = port.gen_eq1_ts(m, l, 40 + m)
+    b = port.gen_eq1_ts(l, n, 41 + m)
+    want, _, inexact = port.ozaki_gemm_ts(a, b, d, want_inexact=True)
+    assert inexact == 0
+    ozk.set_engine(eng)
+    try:
+        got, prof = ozk.ozaki_gemm(a, b, d)
+    finally:
+        ozk.set_engine("auto")
+    assert prof.engine == eng
+    assert np.array_equal(fbits(got), fbits(want))
