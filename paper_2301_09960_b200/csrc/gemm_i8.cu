@@ -14,21 +14,29 @@
 // DMMA) computes.  The K-word accumulation that follows is the same
 // kw_add<K> sequence in the same pair order.
 //
-// B200 mapping (one persistent CTA per SM, 12 warps):
-//   warp 0      TMA producer: per 128-deep k-block, the 3 A-digit tiles (128x128
-//               int8) and 3 B-digit tiles (64x128 int8), 128-byte swizzle,
-//               3-stage mbarrier ring (72 KiB per stage).
-//   warp 1      TMEM allocator + single-thread MMA issuer: 9 digit pairs x 4
-//               k-chunks = 36 tcgen05.mma (M=128, N=64, K=32) per k-block into
-//               5 TMEM level accumulators (levels s+t = 0..4, 64 columns each);
-//               tcgen05.commit releases the smem stage and, after a pair's last
-//               k-block, hands TMEM to the epilogue.
-//   warps 4-11  two epilogue warpgroups, one per 32-column half of the tile (one
-//               TMEM lane = one C row per thread): tcgen05.ld the 5 levels,
-//               recombine in int64, scale by 2^(gA + gB), release TMEM (the MMAs
-//               of the next pair start), then the K-word read-modify-write of the
-//               thread's 32 contiguous C elements.  setmaxnreg moves registers
-//               from the producer/MMA warpgroup (40) to the epilogue (232).
+// B200 mapping (one persistent CTA per SM, 12 warps).  The tile is transposed
+// with respect to C: the MMA's M side (128 TMEM lanes) runs over 128 C COLUMNS
+// (B-slice digits) and its N side over TR C rows per A-slice digit, so every
+// epilogue thread owns one C column and a warp's C accesses are row-contiguous
+// (a K-word row segment of 32 columns) instead of 32 rows apart.
+//   warp 0      TMA producer: per 128-deep k-block, the ND B-digit tiles (128 x 128
+//               int8) and the ND A-digit tiles (TR x 128 int8, adjacent in shared
+//               memory), 128-byte swizzle, mbarrier ring.
+//   warp 1      TMEM allocator + single-thread MMA issuer.  The ND A-digit tiles
+//               form ONE N = ND*TR operand, so MMA(Bdigit t, [A_0;...;A_ND-1])
+//               with its accumulator based at level block t lands the product of
+//               digits (t, u) in block t + u = its level: ND MMAs per 32-deep
+//               k-chunk instead of ND^2, and each operand tile is read ND times
+//               instead of ND^2.  The first k-chunk of a pair issues the ND^2
+//               single-digit products instead, each level's first one
+//               overwriting (blocks t+u > t are not yet initialised then).
+//   warps 4-11  two epilogue warpgroups, one per TR/2-row half of the tile (one
+//               TMEM lane = one C column per thread): tcgen05.ld the 2ND-1
+//               levels, recombine in int64, scale by 2^(gA + gB), release TMEM
+//               (the MMAs of the next pair start), then the K-word
+//               read-modify-write of the thread's column segment, C loads
+//               issued kAhead steps ahead.  setmaxnreg moves registers from the
+//               producer/MMA warpgroup (40) to the epilogue (232).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -38,35 +46,50 @@
 namespace ozk {
 namespace {
 
-constexpr int BM = 128, BKB = 128;            // tile M, k bytes per stage
-constexpr int kEpiGroups = 2;                 // epilogue warpgroups (column halves)
-constexpr int kThreads = (4 + 4 * kEpiGroups) * 32;
+constexpr int TC = 128, BKB = 128;            // tile C columns (MMA M), k bytes per stage
 constexpr int kGroupM = 8;
-constexpr int kSmemBudget = 200 * 1024;       // operand ring
+#ifndef OZK_I8_EG
+#define OZK_I8_EG 4
+#endif
+constexpr int kSmemBudget = 221 * 1024;       // operand ring
 
 // Compile-time shape of one engine instance.
 //   W   word type of C (double: DD/TD/QD, float: TS)
 //   ND  int8 digits per slice integer (3 for binary64 slices at l > 512; 1 for
 //       TS slices at l > 4096, where |M| <= 2^(25 - sigma) <= 64; 2 below)
-//   BN  tile width; 2*ND-1 level accumulators of BN TMEM columns each
-template <int K, typename W, int ND, int BN>
+//   TR  tile C rows per digit (MMA N); 2*ND-1 level accumulators of TR TMEM
+//       columns each, stacked MMA width ND*TR <= 256, two accumulator buffers
+//   EG  epilogue warpgroups; each owns TR/EG rows of the tile
+template <int K, typename W, int ND, int TR, int EG>
 struct I8Cfg {
     static constexpr int kLevels = 2 * ND - 1;
-    static constexpr int kATile = BM * BKB;
-    static constexpr int kBTile = BN * BKB;
+    static constexpr int kBTile = TC * BKB;   // one B digit (C columns), MMA operand A
+    static constexpr int kATile = TR * BKB;   // one A digit (C rows), MMA operand B
     static constexpr int kStageBytes = ND * (kATile + kBTile);
     static constexpr int kStages = kSmemBudget / kStageBytes < 8 ? kSmemBudget / kStageBytes : 8;
     static constexpr int kSmemBytes = kStages * kStageBytes + 1024 + 256;
-    static constexpr int kTmemCols = kLevels * BN <= 32 ? 32 : kLevels * BN <= 64 ? 64
-                                   : kLevels * BN <= 128 ? 128 : kLevels * BN <= 256 ? 256 : 512;
-    static constexpr int kEpiCols = BN / kEpiGroups;  // columns per epilogue thread
-    // K-word adds unrolled per epilogue step (B200 A/B at n = 8192,
-    // tools/variants_bench.py): DD 8 (104.6 ms; 2: 109.1), TD 2 (316 ms; 8: 349),
-    // QD 2 (582 ms; 8: 664) -- the K >= 3 bodies are large enough that more
-    // unrolling costs instruction-cache misses and registers instead of latency.
-    static constexpr int kChunk = (K == 2 && sizeof(W) == 8) ? 8 : 2;
+    static constexpr int kBufCols = kLevels * TR;  // one accumulator buffer
+    static constexpr int kTmemCols = 2 * kBufCols <= 32 ? 32 : 2 * kBufCols <= 64 ? 64
+                                   : 2 * kBufCols <= 128 ? 128 : 2 * kBufCols <= 256 ? 256 : 512;
+    static constexpr int kThreads = (4 + 4 * EG) * 32;
+    static constexpr int kEpiRows = TR / EG;  // C rows per epilogue thread
+    // rows per K-word update step; two steps (ping-pong C buffers) per loop trip
+    static constexpr int kChunk = (K == 2 && sizeof(W) == 8 && EG == 2) ? 4 : 2;
+    // register split between the producer/MMA warpgroup and the epilogue:
+    // setmaxnreg.inc blocks until the registers released by the .dec are
+    // available, so the epilogue may grow only by what the first warpgroup
+    // gives back from the launch allocation (65536 / threads, rounded to 8)
+    static constexpr int kLaunchRegs = (65536 / ((4 + 4 * EG) * 32)) / 8 * 8;
+    static constexpr int kEpiRegs =
+        (kLaunchRegs + (kLaunchRegs - 40) / EG) / 8 * 8 > 232
+            ? 232 : (kLaunchRegs + (kLaunchRegs - 40) / EG) / 8 * 8;
     static_assert(kStages >= 2, "operand ring too small");
-    static_assert(kLevels * BN <= 512, "TMEM");
+    static_assert(2 * kBufCols <= 512, "TMEM: two accumulator buffers");
+    static_assert(ND * TR <= 256 && TR % 16 == 0, "stacked MMA width");
+    static_assert(kATile % 1024 == 0, "A-digit tiles must stack in 8-row swizzle groups");
+    static_assert(kEpiRows % (2 * kChunk) == 0, "epilogue rows per ping-pong trip");
+    static_assert(40 * 128 + kEpiRegs * 128 * EG <= kLaunchRegs * (4 + 4 * EG) * 32,
+                  "setmaxnreg pool");
 };
 
 struct MapsI8 {
@@ -133,14 +156,17 @@ __device__ __forceinline__ void umma_commit(uint32_t bar) {
         "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
         : "memory");
 }
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, int32_t* v) {
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
-        "%14,%15}, [%16];"
-        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
-          "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),
-          "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
-        : "r"(taddr));
+
+template <int N>
+__device__ __forceinline__ void tmem_ld(uint32_t taddr, int32_t (&v)[N]) {
+    static_assert(N == 2 || N == 4, "tmem_ld width");
+    if constexpr (N == 2) {
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0,%1}, [%2];"
+                     : "=r"(v[0]), "=r"(v[1]) : "r"(taddr));
+    } else {
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]) : "r"(taddr));
+    }
 }
 
 // Exact int64 -> binary64 for |s| < 2^53 on the FP64 pipe (I2F.F64.S64 runs on
@@ -165,6 +191,57 @@ __device__ __forceinline__ double ldexp_fast(double y, int e) {
     return scalbn(y, e);
 }
 
+// One K-word C element as few, wide memory operations.  kVec (16-byte aligned
+// C base, binary64 words): DD one 16-byte access, QD two; TD one 16-byte and
+// one 8-byte access whose order follows the parity q of the element's word
+// offset, so every lane issues the same instruction shape.  Otherwise (TS, or
+// a C base that is only 8-byte aligned) one access per word.
+template <int K, typename W>
+__device__ __forceinline__ void ld_kword(const W* p, int q, bool vec, W (&w)[K]) {
+    if constexpr (sizeof(W) == 8 && (K == 2 || K == 4)) {
+        if (vec) {
+#pragma unroll
+            for (int h = 0; h < K / 2; ++h) {
+                const double2 v = *reinterpret_cast<const double2*>(p + 2 * h);
+                w[2 * h] = v.x;
+                w[2 * h + 1] = v.y;
+            }
+            return;
+        }
+    } else if constexpr (sizeof(W) == 8 && K == 3) {
+        if (vec) {
+            const double2 v = *reinterpret_cast<const double2*>(p + q);
+            const double t = p[q ? 0 : 2];
+            w[0] = q ? t : v.x;
+            w[1] = q ? v.x : v.y;
+            w[2] = q ? v.y : t;
+            return;
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < K; ++k) w[k] = p[k];
+}
+template <int K, typename W>
+__device__ __forceinline__ void st_kword(W* p, int q, bool vec, const W (&w)[K]) {
+    if constexpr (sizeof(W) == 8 && (K == 2 || K == 4)) {
+        if (vec) {
+#pragma unroll
+            for (int h = 0; h < K / 2; ++h)
+                *reinterpret_cast<double2*>(p + 2 * h) = make_double2(w[2 * h], w[2 * h + 1]);
+            return;
+        }
+    } else if constexpr (sizeof(W) == 8 && K == 3) {
+        if (vec) {
+            *reinterpret_cast<double2*>(p + q) = q ? make_double2(w[1], w[2])
+                                                   : make_double2(w[0], w[1]);
+            p[q ? 0 : 2] = q ? w[0] : w[2];
+            return;
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < K; ++k) p[k] = w[k];
+}
+
 struct TileCoord {
     int tm, tn;
 };
@@ -176,22 +253,36 @@ __device__ __forceinline__ TileCoord tile_of(int id, int tiles_m, int tiles_n) {
     return TileCoord{first_m + in_group % gm, in_group / gm};
 }
 
-template <int K, typename W, int ND, int BN>
-__global__ void __launch_bounds__(kThreads, 1)
+// Diagnostic timeline (build with -DOZK_I8_TRACE, tools/i8_trace.py): SM clock
+// stamps of CTA 0's first kTracePairs (tile, pair) steps -- MMA issuer: wait for
+// TMEM, TMEM granted, last MMA issued; epilogue warp 4: wait start, levels
+// ready, TMEM released, K-word update done.
+#ifdef OZK_I8_TRACE
+constexpr int kTracePairs = 512;
+__device__ unsigned long long g_i8_trace[kTracePairs][8];
+__device__ __forceinline__ void trace_stamp(int step, int slot, bool on) {
+    if (on && blockIdx.x == 0 && step < kTracePairs) g_i8_trace[step][slot] = clock64();
+}
+#else
+__device__ __forceinline__ void trace_stamp(int, int, bool) {}
+#endif
+
+template <int K, typename W, int ND, int TR, int EG, bool kVec>
+__global__ void __launch_bounds__(I8Cfg<K, W, ND, TR, EG>::kThreads, 1)
 pair_gemm_i8_kernel(const __grid_constant__ MapsI8 maps, const __grid_constant__ PairList pairs,
                     I8Problem prob, int tiles_m, int tiles_n) {
-    using Cfg = I8Cfg<K, W, ND, BN>;
+    using Cfg = I8Cfg<K, W, ND, TR, EG>;
     constexpr int kStages = Cfg::kStages, kStageBytes = Cfg::kStageBytes;
-    constexpr int kATile = Cfg::kATile, kBTile = Cfg::kBTile, kEpiCols = Cfg::kEpiCols;
-    constexpr int kTmemCols = Cfg::kTmemCols, kLevels = Cfg::kLevels;
+    constexpr int kATile = Cfg::kATile, kBTile = Cfg::kBTile, kEpiRows = Cfg::kEpiRows;
+    constexpr int kTmemCols = Cfg::kTmemCols, kLevels = Cfg::kLevels, kBufCols = Cfg::kBufCols;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~uintptr_t(1023));
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
-    // bars: full[S], empty[S], tmem_full, tmem_empty ; then the TMEM base word
+    // bars: full[S], empty[S], tmem_full[2], tmem_empty[2] ; then the TMEM base word
     const uint32_t full0 = smem_u32(bars), empty0 = full0 + 8 * kStages;
-    const uint32_t tmem_full = empty0 + 8 * kStages, tmem_empty = tmem_full + 8;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 2);
+    const uint32_t tfull0 = empty0 + 8 * kStages, tempty0 = tfull0 + 16;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 4);
     const uint32_t ring = smem_u32(smem);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -204,8 +295,10 @@ pair_gemm_i8_kernel(const __grid_constant__ MapsI8 maps, const __grid_constant__
             mbar_init(full0 + 8 * s, 1);
             mbar_init(empty0 + 8 * s, 1);
         }
-        mbar_init(tmem_full, 1);
-        mbar_init(tmem_empty, 4 * kEpiGroups);  // one arrive per epilogue warp
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(tfull0 + 8 * b, 1);
+            mbar_init(tempty0 + 8 * b, 4 * EG);  // one arrive per epilogue warp
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 1) {
@@ -223,6 +316,8 @@ pair_gemm_i8_kernel(const __grid_constant__ MapsI8 maps, const __grid_constant__
       asm volatile("setmaxnreg.dec.sync.aligned.u32 40;");
       if (warp == 0 && lane == 0) {
         // ---------------- TMA producer ----------------
+        // stage layout: ND B-digit tiles (TC x BKB), then ND A-digit tiles
+        // (TR x BKB) back to back = the stacked MMA N operand
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&maps.a)));
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&maps.b)));
         int stage = 0;
@@ -238,9 +333,9 @@ pair_gemm_i8_kernel(const __grid_constant__ MapsI8 maps, const __grid_constant__
                     const uint32_t sa = ring + stage * kStageBytes;
 #pragma unroll
                     for (int dgt = 0; dgt < ND; ++dgt) {
-                        tma_load_4d(sa + dgt * kATile, &maps.a, full, kb * BKB, tc.tm * BM, dgt, al);
-                        tma_load_4d(sa + ND * kATile + dgt * kBTile, &maps.b, full, kb * BKB,
-                                    tc.tn * BN, dgt, be);
+                        tma_load_4d(sa + dgt * kBTile, &maps.b, full, kb * BKB, tc.tn * TC, dgt, be);
+                        tma_load_4d(sa + ND * kBTile + dgt * kATile, &maps.a, full, kb * BKB,
+                                    tc.tm * TR, dgt, al);
                     }
                     if (++stage == kStages) {
                         stage = 0;
@@ -251,39 +346,61 @@ pair_gemm_i8_kernel(const __grid_constant__ MapsI8 maps, const __grid_constant__
         }
       } else if (warp == 1 && lane == 0) {
         // ---------------- MMA issuer ----------------
-        // kind::i8 instruction descriptor: D s32, A/B signed 8-bit, K-major,
-        // N = 64, M = 128 (CuTe mma_sm100_desc.hpp InstrDescriptor)
-        constexpr uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) |
-                                   ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+        // kind::i8 instruction descriptors: D s32, A/B signed 8-bit, K-major,
+        // M = 128, N = TR (one digit) or ND*TR (stacked digits)
+        // (CuTe mma_sm100_desc.hpp InstrDescriptor)
+        constexpr uint32_t idesc1 = (2u << 4) | (1u << 7) | (1u << 10) |
+                                    ((uint32_t)(TR >> 3) << 17) | ((uint32_t)(TC >> 4) << 24);
+        constexpr uint32_t idescN = (2u << 4) | (1u << 7) | (1u << 10) |
+                                    ((uint32_t)((ND * TR) >> 3) << 17) | ((uint32_t)(TC >> 4) << 24);
         int stage = 0;
-        uint32_t phase = 0, tphase = 0;
+        uint32_t phase = 0;
+        int step = 0;
         for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-            for (int p = 0; p < npairs; ++p) {
-                mbar_wait(tmem_empty, tphase ^ 1);  // epilogue drained the levels
-                tphase ^= 1;
+            for (int p = 0; p < npairs; ++p, ++step) {
+                // accumulator buffer step % 2, free once the epilogue of step - 2 is done
+                const int buf = step & 1;
+                trace_stamp(step, 0, true);
+                mbar_wait(tempty0 + 8 * buf, ((step >> 1) & 1) ^ 1);
+                trace_stamp(step, 1, true);
                 asm volatile("tcgen05.fence::after_thread_sync;");
+                const uint32_t acc0 = tmem + buf * kBufCols;
+#ifdef OZK_I8_TRACE
+                unsigned long long full_wait = 0;
+#endif
                 for (int kb = 0; kb < num_kb; ++kb) {
+#ifdef OZK_I8_TRACE
+                    const unsigned long long w0 = clock64();
                     mbar_wait(full0 + 8 * stage, phase);
+                    full_wait += clock64() - w0;
+#else
+                    mbar_wait(full0 + 8 * stage, phase);
+#endif
                     asm volatile("tcgen05.fence::after_thread_sync;");
-                    const uint32_t sa = ring + stage * kStageBytes;
-#pragma unroll
-                    for (int kc = 0; kc < BKB / 32; ++kc) {
-                        // digit pairs level by level; the first MMA of each
-                        // level in a pair's first chunk overwrites the accumulator
+                    const uint32_t sb = ring + stage * kStageBytes;  // B digits (M side)
+                    const uint32_t sa = sb + ND * kBTile;            // A digits (N side)
+                    int kc = 0;
+                    if (kb == 0) {
+                        // first chunk: single-digit products level by level, the
+                        // first of each level overwriting its accumulator block
 #pragma unroll
                         for (int lvl = 0; lvl < kLevels; ++lvl) {
 #pragma unroll
-                            for (int ds = 0; ds < ND; ++ds) {
-                                const int dt = lvl - ds;
-                                if (dt < 0 || dt >= ND) continue;
-                                const bool first = ds == (lvl - ND + 1 > 0 ? lvl - ND + 1 : 0);
-                                const uint64_t da = sw128_desc(sa + ds * kATile + kc * 32);
-                                const uint64_t db =
-                                    sw128_desc(sa + ND * kATile + dt * kBTile + kc * 32);
-                                const uint32_t acc = (kb | kc) ? 1u : (first ? 0u : 1u);
-                                umma_i8(tmem + lvl * BN, da, db, idesc, acc);
+                            for (int t = 0; t < ND; ++t) {
+                                const int u = lvl - t;
+                                if (u < 0 || u >= ND) continue;
+                                const bool first = t == (lvl - ND + 1 > 0 ? lvl - ND + 1 : 0);
+                                umma_i8(acc0 + lvl * TR, sw128_desc(sb + t * kBTile),
+                                        sw128_desc(sa + u * kATile), idesc1, first ? 0u : 1u);
                             }
                         }
+                        kc = 1;
+                    }
+                    for (; kc < BKB / 32; ++kc) {
+#pragma unroll
+                        for (int t = 0; t < ND; ++t)
+                            umma_i8(acc0 + t * TR, sw128_desc(sb + t * kBTile + kc * 32),
+                                    sw128_desc(sa + kc * 32), idescN, 1u);
                     }
                     umma_commit(empty0 + 8 * stage);  // frees the stage when the MMAs retire
                     if (++stage == kStages) {
@@ -291,83 +408,118 @@ pair_gemm_i8_kernel(const __grid_constant__ MapsI8 maps, const __grid_constant__
                         phase ^= 1;
                     }
                 }
-                umma_commit(tmem_full);
+                umma_commit(tfull0 + 8 * buf);
+                trace_stamp(step, 2, true);
+#ifdef OZK_I8_TRACE
+                if (blockIdx.x == 0 && step < kTracePairs) g_i8_trace[step][7] = full_wait;
+#endif
             }
         }
       }
     } else {
-        asm volatile("setmaxnreg.inc.sync.aligned.u32 232;");
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(Cfg::kEpiRegs));
         // ---------------- epilogue warpgroups ----------------
-        // warpgroup eg owns columns [eg*32, eg*32+32) of every tile for every
-        // pair (so no two threads ever touch the same C element); warp % 4
-        // selects the 32 TMEM lanes (C rows) it may access.
+        // warpgroup eg owns rows [eg*kEpiRows, (eg+1)*kEpiRows) of every tile for
+        // every pair (no two threads ever touch the same C element); warp % 4
+        // selects the 32 TMEM lanes = C columns it may access, one per thread.
+        // The levels are read from TMEM chunk by chunk (no register copy of
+        // the tile), and the buffer is released after the last chunk: the
+        // MMAs of the next pair run meanwhile in the other buffer.
+        constexpr int kChunk = Cfg::kChunk;
         const int eg = (warp - 4) / 4;
         const int wq = warp % 4;
-        const uint32_t tlane = tmem + ((uint32_t)(wq * 32) << 16) + eg * kEpiCols;
-        uint32_t tphase = 0;
+        const uint32_t tlane = tmem + ((uint32_t)(wq * 32) << 16) + eg * kEpiRows;
+        int step = 0;
+        const bool tracer = warp == 4 && lane == 0;
         for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
             const TileCoord tc = tile_of(tile, tiles_m, tiles_n);
-            const size_t row = (size_t)tc.tm * BM + wq * 32 + lane;
-            const size_t col0 = (size_t)tc.tn * BN + eg * kEpiCols;
-            const bool row_ok = row < prob.m;
-            for (int p = 0; p < npairs; ++p) {
+            const size_t col = (size_t)tc.tn * TC + wq * 32 + lane;
+            const size_t row0 = (size_t)tc.tm * TR + eg * kEpiRows;
+            const bool col_ok = col < prob.n;
+            // out-of-range lanes and rows read a valid element and never store
+            const size_t col_c = col_ok ? col : prob.n - 1;
+            for (int p = 0; p < npairs; ++p, ++step) {
+                const int buf = step & 1;
                 const int al = pairs.alpha[p], be = pairs.beta[p];
-                const int ga = row_ok ? prob.gA[(size_t)al * prob.gA_stride + row] : 0;
-                mbar_wait(tmem_full, tphase);
-                tphase ^= 1;
+                const int gb = prob.gB[(size_t)be * prob.gB_stride + col_c];
+                const int* gap = prob.gA + (size_t)al * prob.gA_stride;
+                const bool first = p == 0;  // C starts from zero
+                trace_stamp(step, 3, tracer);
+                mbar_wait(tfull0 + 8 * buf, (step >> 1) & 1);
+                trace_stamp(step, 4, tracer);
                 asm volatile("tcgen05.fence::after_thread_sync;");
-                double y[kEpiCols];
+                const uint32_t tbuf = tlane + buf * kBufCols;
+                W* const cbase = static_cast<W*>(prob.c);
+                auto row_of = [&](int r) -> size_t {
+                    const size_t rr = row0 + r;
+                    return rr < prob.m ? rr : prob.m - 1;
+                };
+                auto load_chunk = [&](int r, W (&w)[kChunk][K]) {
 #pragma unroll
-                for (int c = 0; c < kEpiCols; c += 16) {
-                    int32_t lv[kLevels][16];
+                    for (int j = 0; j < kChunk; ++j) {
+                        const size_t e = row_of(r + j) * prob.ldc + col_c;
+#if defined(OZK_I8_EPI_MODE) && OZK_I8_EPI_MODE == 1
+                        if (true) {  // diagnostic: no C reads
+#else
+                        if (first) {
+#endif
 #pragma unroll
-                    for (int u = 0; u < kLevels; ++u) tmem_ld16(tlane + u * BN + c, lv[u]);
+                            for (int k = 0; k < K; ++k) w[j][k] = W(0);
+                        } else {
+                            ld_kword<K>(cbase + e * K, (int)(e & 1), kVec, w[j]);
+                        }
+                    }
+                };
+                auto update_chunk = [&](int r, W (&w)[kChunk][K]) {
+                    int32_t lv[kLevels][kChunk];
+#if defined(OZK_I8_EPI_MODE) && OZK_I8_EPI_MODE == 4
+#pragma unroll
+                    for (int u = 0; u < kLevels; ++u)  // diagnostic: no TMEM reads
+#pragma unroll
+                        for (int j = 0; j < kChunk; ++j) lv[u][j] = (int)(tbuf + u + j + r);
+#else
+#pragma unroll
+                    for (int u = 0; u < kLevels; ++u) tmem_ld<kChunk>(tbuf + u * TR + r, lv[u]);
                     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#endif
 #pragma unroll
-                    for (int j = 0; j < 16; ++j) {
+                    for (int j = 0; j < kChunk; ++j) {
                         long long s = lv[0][j];
 #pragma unroll
                         for (int u = 1; u < kLevels; ++u) s += (long long)lv[u][j] << (8 * u);
-                        y[c + j] = i64_to_f64_exact(s);  // exact: |s| < 2^53
-                    }
-                }
-                // levels are in registers: hand TMEM back to the MMA issuer
-                asm volatile("tcgen05.fence::before_thread_sync;");
-                __syncwarp();
-                if (lane == 0) mbar_arrive(tmem_empty);
-                if (!row_ok) continue;
-                W* cp = static_cast<W*>(prob.c) + (row * prob.ldc + col0) * K;
-                const int* gbp = prob.gB + (size_t)be * prob.gB_stride + col0;
-#pragma unroll 1
-                constexpr int kChunk = Cfg::kChunk;
-                for (int c = 0; c < kEpiCols; c += kChunk) {
-                    // y[0..kChunk) are this chunk's products; the array is
-                    // shifted down after each chunk so every index stays static
-                    W w[kChunk][K];
-#pragma unroll
-                    for (int j = 0; j < kChunk; ++j) {
-                        const bool ok = col0 + c + j < prob.n;
-#pragma unroll
-                        for (int k = 0; k < K; ++k)
-                            w[j][k] = (ok && p > 0) ? cp[(c + j) * K + k] : W(0);
-                    }
-#pragma unroll
-                    for (int j = 0; j < kChunk; ++j) {
-                        const bool ok = col0 + c + j < prob.n;
-                        const int gb = ok ? __ldg(gbp + c + j) : 0;
+                        const double y = i64_to_f64_exact(s);  // exact: |s| < 2^53
+                        const int ga = __ldg(gap + row_of(r + j));
                         // exact scaled slice product (a TS product is exact in binary32)
-                        kw_add<K>(w[j], (W)ldexp_fast(y[j], ga + gb));
+#if defined(OZK_I8_EPI_MODE) && OZK_I8_EPI_MODE == 2
+                        w[j][0] += (W)ldexp_fast(y, ga + gb);  // diagnostic: no K-word add
+#else
+                        kw_add<K>(w[j], (W)ldexp_fast(y, ga + gb));
+#endif
                     }
 #pragma unroll
                     for (int j = 0; j < kChunk; ++j) {
-                        if (col0 + c + j < prob.n) {
-#pragma unroll
-                            for (int k = 0; k < K; ++k) cp[(c + j) * K + k] = w[j][k];
+                        const size_t rr = row0 + r + j;
+                        if (col_ok && rr < prob.m) {
+                            const size_t e = rr * prob.ldc + col;
+                            st_kword<K>(cbase + e * K, (int)(e & 1), kVec, w[j]);
                         }
                     }
-#pragma unroll
-                    for (int j = 0; j < kEpiCols - kChunk; ++j) y[j] = y[j + kChunk];
+                };
+                W ca[kChunk][K], cb[kChunk][K];
+                load_chunk(0, ca);
+#pragma unroll 1
+                for (int r = 0; r < kEpiRows; r += 2 * kChunk) {
+                    load_chunk(r + kChunk, cb);  // in flight during the update of ca
+                    update_chunk(r, ca);
+                    if (r + 2 * kChunk < kEpiRows) load_chunk(r + 2 * kChunk, ca);
+                    update_chunk(r + kChunk, cb);
                 }
+                // all levels read: hand the buffer back to the MMA issuer
+                asm volatile("tcgen05.fence::before_thread_sync;");
+                __syncwarp();
+                if (lane == 0) mbar_arrive(tempty0 + 8 * buf);
+                trace_stamp(step, 5, tracer);
+                trace_stamp(step, 6, tracer);
             }
         }
     }
@@ -391,17 +543,17 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode_i8() {
     return fn;
 }
 
-template <int K, typename W, int ND, int BN>
+template <int K, typename W, int ND, int TR, int EG = 2>
 cudaError_t launch_i8_typed(const I8Operands& op, const PairList& pairs, cudaStream_t st,
                             int num_sms) {
-    using Cfg = I8Cfg<K, W, ND, BN>;
+    using Cfg = I8Cfg<K, W, ND, TR, EG>;
     auto encode = get_encode_i8();
     if (!encode) return cudaErrorNotSupported;
     MapsI8 maps;
     {
         cuuint64_t dims[4] = {op.l, op.m, (cuuint64_t)ND, (cuuint64_t)op.d};
         cuuint64_t strides[3] = {op.a_ld, op.a_digit_stride, op.a_slice_stride};
-        cuuint32_t box[4] = {BKB, BM, 1, 1};
+        cuuint32_t box[4] = {BKB, TR, 1, 1};
         cuuint32_t es[4] = {1, 1, 1, 1};
         if (encode(&maps.a, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<int8_t*>(op.a), dims,
                    strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -412,7 +564,7 @@ cudaError_t launch_i8_typed(const I8Operands& op, const PairList& pairs, cudaStr
     {
         cuuint64_t dims[4] = {op.l, op.n, (cuuint64_t)ND, (cuuint64_t)op.d};
         cuuint64_t strides[3] = {op.b_ld, op.b_digit_stride, op.b_slice_stride};
-        cuuint32_t box[4] = {BKB, BN, 1, 1};
+        cuuint32_t box[4] = {BKB, TC, 1, 1};
         cuuint32_t es[4] = {1, 1, 1, 1};
         if (encode(&maps.b, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<int8_t*>(op.b), dims,
                    strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -430,15 +582,18 @@ cudaError_t launch_i8_typed(const I8Operands& op, const PairList& pairs, cudaStr
     prob.gB_stride = op.n;
     prob.c = op.c;
     prob.ldc = op.ldc;
-    const int tiles_m = (int)((op.m + BM - 1) / BM), tiles_n = (int)((op.n + BN - 1) / BN);
+    const bool vec = sizeof(W) == 8 && (reinterpret_cast<uintptr_t>(op.c) & 15) == 0;
+    const int tiles_m = (int)((op.m + TR - 1) / TR), tiles_n = (int)((op.n + TC - 1) / TC);
     const int num_tiles = tiles_m * tiles_n;
     if (num_tiles == 0 || pairs.count == 0) return cudaSuccess;
-    auto kern = pair_gemm_i8_kernel<K, W, ND, BN>;
+    auto kern = pair_gemm_i8_kernel<K, W, ND, TR, EG, false>;
+    if constexpr (sizeof(W) == 8)
+        if (vec) kern = pair_gemm_i8_kernel<K, W, ND, TR, EG, true>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          Cfg::kSmemBytes);
     if (e != cudaSuccess) return e;
     const int grid = num_tiles < num_sms ? num_tiles : num_sms;
-    kern<<<grid, kThreads, Cfg::kSmemBytes, st>>>(maps, pairs, prob, tiles_m, tiles_n);
+    kern<<<grid, Cfg::kThreads, Cfg::kSmemBytes, st>>>(maps, pairs, prob, tiles_m, tiles_n);
     return cudaGetLastError();
 }
 
@@ -454,11 +609,19 @@ cudaError_t launch_pair_gemm_i8(int K, int word_bytes, const I8Operands& op,
     }
     if (op.nd != 3) return cudaErrorInvalidValue;
     switch (K) {
-    case 2: return launch_i8_typed<2, double, 3, 64>(op, pairs, st, num_sms);
-    case 3: return launch_i8_typed<3, double, 3, 64>(op, pairs, st, num_sms);
-    case 4: return launch_i8_typed<4, double, 3, 64>(op, pairs, st, num_sms);
+    case 2: return launch_i8_typed<2, double, 3, 48, OZK_I8_EG>(op, pairs, st, num_sms);
+    case 3: return launch_i8_typed<3, double, 3, 48, OZK_I8_EG>(op, pairs, st, num_sms);
+    case 4: return launch_i8_typed<4, double, 3, 48, OZK_I8_EG>(op, pairs, st, num_sms);
     default: return cudaErrorInvalidValue;
     }
 }
 
 } // namespace ozk
+
+#ifdef OZK_I8_TRACE
+// diagnostic builds only (tools/i8_trace.py): copy CTA 0's timeline to the host
+extern "C" int ozk_i8_trace_read(unsigned long long* out, int max_steps) {
+    const int n = max_steps < ozk::kTracePairs ? max_steps : ozk::kTracePairs;
+    return (int)cudaMemcpyFromSymbol(out, ozk::g_i8_trace, sizeof(unsigned long long) * 8 * n);
+}
+#endif

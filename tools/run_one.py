@@ -5,7 +5,11 @@ import sys
 import torch
 
 sys.path.insert(0, ".")
-from paper_2301_09960_b200._lib import OzkProfile, lib  # noqa: E402
+import os  # noqa: E402
+
+from paper_2301_09960_b200._lib import OzkProfile, load  # noqa: E402
+
+lib = load(os.environ["OZK_LIB"]) if os.environ.get("OZK_LIB") else load()
 
 fmt, n, d = int(sys.argv[1]), int(sys.argv[2]), int(sys.argv[3])
 eng = {"auto": 0, "dmma": 1, "int8": 2}[sys.argv[4]]

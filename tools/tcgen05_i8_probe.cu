@@ -111,11 +111,15 @@ __global__ void probe_kernel(const __grid_constant__ CUtensorMap ma, const __gri
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 64;" ::"r"(tmem));
 }
 
-int main() {
+int main(int argc, char** argv) {
+    // argv[1]: timed repetitions (default 20000); argv[2]: digit magnitude bound
+    // (default 128 = full-entropy int8; smaller values probe data-dependent power)
+    const int reps_arg = argc > 1 ? atoi(argv[1]) : 20000;
+    const int mag = argc > 2 ? atoi(argv[2]) : 128;
     std::vector<int8_t> A(M * KTOT), B(N * KTOT);
     srand(1);
-    for (auto& x : A) x = (int8_t)(rand() % 256 - 128);
-    for (auto& x : B) x = (int8_t)(rand() % 256 - 128);
+    for (auto& x : A) x = (int8_t)(rand() % (2 * mag) - mag);
+    for (auto& x : B) x = (int8_t)(rand() % (2 * mag) - mag);
     int8_t *dA, *dB;
     int* dC;
     CK(cudaMalloc(&dA, A.size()));
@@ -160,7 +164,7 @@ int main() {
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
-    const int reps = 20000;
+    const int reps = reps_arg;
     probe_kernel<<<sms, 128, smem>>>(ma, mb, dC, 10);
     cudaEventRecord(e0);
     probe_kernel<<<sms, 128, smem>>>(ma, mb, dC, reps);

@@ -17,6 +17,7 @@ for fmt, d in ((2, 6), (3, 9), (4, 12)):
     C = torch.empty_like(A)
     libs[0][1].ozk_gen_eq1_device(fmt, n, n, 1, A.data_ptr(), sh)
     libs[0][1].ozk_gen_eq1_device(fmt, n, n, 2, B.data_ptr(), sh)
+    ref = None
     for path, lib in libs:
         lib.ozk_set_engine(2)
         prof = OzkProfile()
@@ -26,6 +27,12 @@ for fmt, d in ((2, 6), (3, 9), (4, 12)):
                                              C.data_ptr(), sh, ctypes.byref(prof)) == 0
             if it:
                 ts.append(prof.product_seconds)
-        print(f"K={fmt} {path.split('/')[-1]}: slice GEMM {statistics.median(ts)*1e3:.1f} ms",
+        same = ""
+        if ref is None:
+            ref = C.clone()
+        else:
+            same = " (bit-identical)" if torch.equal(ref.view(torch.int64), C.view(torch.int64)) \
+                else " DIFFERS"
+        print(f"K={fmt} {path.split('/')[-1]}: slice GEMM {statistics.median(ts)*1e3:.1f} ms{same}",
               flush=True)
-    del A, B, C
+    del A, B, C, ref
