@@ -47,9 +47,18 @@ namespace ozk {
 namespace {
 
 constexpr int TC = 128, BKB = 128;            // tile C columns (MMA M), k bytes per stage
-constexpr int kGroupM = 8;
+#ifndef OZK_I8_GROUPM
+#define OZK_I8_GROUPM 8
+#endif
+constexpr int kGroupM = OZK_I8_GROUPM;  // tile rows per rasterization group
 #ifndef OZK_I8_EG
 #define OZK_I8_EG 4
+#endif
+#ifndef OZK_I8_CM
+#define OZK_I8_CM 2
+#endif
+#ifndef OZK_I8_CN
+#define OZK_I8_CN 1
 #endif
 constexpr int kSmemBudget = 221 * 1024;       // operand ring
 
@@ -150,6 +159,40 @@ __device__ __forceinline__ void umma_i8(uint32_t tmem_d, uint64_t da, uint64_t d
         "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
         " tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
         "l"(da), "l"(db), "r"(idesc), "r"(accumulate));
+}
+// Multicast variants for thread-block clusters: the tile lands at the same
+// shared-memory offset in every CTA of ctaMask and signals each one's barrier
+// at the same offset; the commit arrives on the barrier of every CTA in the mask.
+__device__ __forceinline__ void tma_load_4d_mc(uint32_t dst, const CUtensorMap* map, uint32_t bar,
+                                               int c0, int c1, int c2, int c3, uint16_t mask) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        ".multicast::cluster [%0], [%1, {%3, %4, %5, %6}], [%2], %7;" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1), "r"(c2), "r"(c3),
+        "h"(mask)
+        : "memory");
+}
+__device__ __forceinline__ void umma_commit_mc(uint32_t bar, uint16_t mask) {
+    asm volatile(
+        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+        " [%0], %1;" ::"r"(bar), "h"(mask)
+        : "memory");
+}
+__device__ __forceinline__ bool elect_one() {
+    uint32_t pred;
+    asm volatile(
+        "{\n .reg .pred p;\n elect.sync _|p, 0xffffffff;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(pred));
+    return pred != 0;
+}
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::
+                     : "memory");
 }
 __device__ __forceinline__ void umma_commit(uint32_t bar) {
     asm volatile(
@@ -267,10 +310,18 @@ __device__ __forceinline__ void trace_stamp(int step, int slot, bool on) {
 __device__ __forceinline__ void trace_stamp(int, int, bool) {}
 #endif
 
-template <int K, typename W, int ND, int TR, int EG, bool kVec>
+// CM x CN thread-block cluster: CTAs (cm, cn) own tile (gm*CM + cm, gn*CN + cn)
+// of tile group (gm, gn).  The CM CTAs of a cluster column share the B-digit
+// tile (same C columns): each loads TC/CM of its rows and multicasts them; the
+// CN CTAs of a cluster row share the A-digit tile the same way.  A stage of CTA
+// x is written by x's cluster row and column, so its empty barrier counts
+// CM + CN - 1 MMA completions, each CTA's commit arriving on all of them.
+template <int K, typename W, int ND, int TR, int EG, bool kVec, int CM, int CN>
 __global__ void __launch_bounds__(I8Cfg<K, W, ND, TR, EG>::kThreads, 1)
 pair_gemm_i8_kernel(const __grid_constant__ MapsI8 maps, const __grid_constant__ PairList pairs,
                     I8Problem prob, int tiles_m, int tiles_n) {
+    constexpr int kCluster = CM * CN;
+    static_assert((TC / CM) % 8 == 0 && (TR / CN) % 8 == 0, "multicast slices of 8-row atoms");
     using Cfg = I8Cfg<K, W, ND, TR, EG>;
     constexpr int kStages = Cfg::kStages, kStageBytes = Cfg::kStageBytes;
     constexpr int kATile = Cfg::kATile, kBTile = Cfg::kBTile, kEpiRows = Cfg::kEpiRows;
@@ -286,14 +337,29 @@ pair_gemm_i8_kernel(const __grid_constant__ MapsI8 maps, const __grid_constant__
     const uint32_t ring = smem_u32(smem);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int num_tiles = tiles_m * tiles_n;
     const int num_kb = (int)((prob.l + BKB - 1) / BKB);
     const int npairs = pairs.count;
+    // cluster coordinates and the persistent loop over tile groups
+    const int crank = kCluster > 1 ? (int)cluster_ctarank() : 0;
+    const int cm = crank % CM, cn = crank / CM;
+    const int groups_m = (tiles_m + CM - 1) / CM, groups_n = (tiles_n + CN - 1) / CN;
+    const int num_groups = groups_m * groups_n;
+    const int cluster_id = blockIdx.x / kCluster, num_clusters = gridDim.x / kCluster;
+    auto tile_of_group = [&](int g) {
+        const TileCoord gc = tile_of(g, groups_m, groups_n);
+        return TileCoord{gc.tm * CM + cm, gc.tn * CN + cn};
+    };
+    // CTAs sharing this CTA's B tile (same cn) and A tile (same cm)
+    uint16_t col_mask = 0, row_mask = 0;
+#pragma unroll
+    for (int i = 0; i < CM; ++i) col_mask |= (uint16_t)(1u << (i + cn * CM));
+#pragma unroll
+    for (int j = 0; j < CN; ++j) row_mask |= (uint16_t)(1u << (cm + j * CM));
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < kStages; ++s) {
             mbar_init(full0 + 8 * s, 1);
-            mbar_init(empty0 + 8 * s, 1);
+            mbar_init(empty0 + 8 * s, CM + CN - 1);
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(tfull0 + 8 * b, 1);
@@ -308,7 +374,10 @@ pair_gemm_i8_kernel(const __grid_constant__ MapsI8 maps, const __grid_constant__
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
-    __syncthreads();
+    if constexpr (kCluster > 1)
+        cluster_sync();  // peers' barriers initialised before any multicast
+    else
+        __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;");
     const uint32_t tmem = *tmem_slot;
 
@@ -322,20 +391,37 @@ pair_gemm_i8_kernel(const __grid_constant__ MapsI8 maps, const __grid_constant__
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&maps.b)));
         int stage = 0;
         uint32_t phase = 0;
-        for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-            const TileCoord tc = tile_of(tile, tiles_m, tiles_n);
+        for (int g = cluster_id; g < num_groups; g += num_clusters) {
+            const TileCoord tc = tile_of_group(g);
             for (int p = 0; p < npairs; ++p) {
                 const int al = pairs.alpha[p], be = pairs.beta[p];
                 for (int kb = 0; kb < num_kb; ++kb) {
                     mbar_wait(empty0 + 8 * stage, phase ^ 1);
                     const uint32_t full = full0 + 8 * stage;
+#if defined(OZK_I8_EPI_MODE) && OZK_I8_EPI_MODE == 5
+                    mbar_arrive(full);  // diagnostic: no operand traffic (stale tiles)
+                    if (++stage == kStages) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                    continue;
+#endif
                     mbar_expect_tx(full, kStageBytes);
                     const uint32_t sa = ring + stage * kStageBytes;
 #pragma unroll
                     for (int dgt = 0; dgt < ND; ++dgt) {
-                        tma_load_4d(sa + dgt * kBTile, &maps.b, full, kb * BKB, tc.tn * TC, dgt, be);
-                        tma_load_4d(sa + ND * kBTile + dgt * kATile, &maps.a, full, kb * BKB,
-                                    tc.tm * TR, dgt, al);
+                        // this CTA's slice of the shared tiles (whole tiles when unshared)
+                        const uint32_t db = sa + dgt * kBTile + cm * (TC / CM) * BKB;
+                        const uint32_t da = sa + ND * kBTile + dgt * kATile + cn * (TR / CN) * BKB;
+                        const int rb = tc.tn * TC + cm * (TC / CM), ra = tc.tm * TR + cn * (TR / CN);
+                        if constexpr (CM > 1)
+                            tma_load_4d_mc(db, &maps.b, full, kb * BKB, rb, dgt, be, col_mask);
+                        else
+                            tma_load_4d(db, &maps.b, full, kb * BKB, rb, dgt, be);
+                        if constexpr (CN > 1)
+                            tma_load_4d_mc(da, &maps.a, full, kb * BKB, ra, dgt, al, row_mask);
+                        else
+                            tma_load_4d(da, &maps.a, full, kb * BKB, ra, dgt, al);
                     }
                     if (++stage == kStages) {
                         stage = 0;
@@ -344,8 +430,11 @@ pair_gemm_i8_kernel(const __grid_constant__ MapsI8 maps, const __grid_constant__
                 }
             }
         }
-      } else if (warp == 1 && lane == 0) {
+      } else if (warp == 1) {
         // ---------------- MMA issuer ----------------
+        // The whole warp runs the loop so every descriptor is warp-uniform (kept
+        // in uniform registers) and one elected lane issues; descriptors of a
+        // stage are its base plus compile-time offsets.
         // kind::i8 instruction descriptors: D s32, A/B signed 8-bit, K-major,
         // M = 128, N = TR (one digit) or ND*TR (stacked digits)
         // (CuTe mma_sm100_desc.hpp InstrDescriptor)
@@ -356,13 +445,13 @@ pair_gemm_i8_kernel(const __grid_constant__ MapsI8 maps, const __grid_constant__
         int stage = 0;
         uint32_t phase = 0;
         int step = 0;
-        for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        for (int g = cluster_id; g < num_groups; g += num_clusters) {
             for (int p = 0; p < npairs; ++p, ++step) {
                 // accumulator buffer step % 2, free once the epilogue of step - 2 is done
                 const int buf = step & 1;
-                trace_stamp(step, 0, true);
+                trace_stamp(step, 0, lane == 0);
                 mbar_wait(tempty0 + 8 * buf, ((step >> 1) & 1) ^ 1);
-                trace_stamp(step, 1, true);
+                trace_stamp(step, 1, lane == 0);
                 asm volatile("tcgen05.fence::after_thread_sync;");
                 const uint32_t acc0 = tmem + buf * kBufCols;
 #ifdef OZK_I8_TRACE
@@ -378,40 +467,55 @@ pair_gemm_i8_kernel(const __grid_constant__ MapsI8 maps, const __grid_constant__
 #endif
                     asm volatile("tcgen05.fence::after_thread_sync;");
                     const uint32_t sb = ring + stage * kStageBytes;  // B digits (M side)
-                    const uint32_t sa = sb + ND * kBTile;            // A digits (N side)
-                    int kc = 0;
-                    if (kb == 0) {
-                        // first chunk: single-digit products level by level, the
-                        // first of each level overwriting its accumulator block
+                    const uint64_t db = sw128_desc(sb);              // B digit 0, k-chunk 0
+                    const uint64_t da = sw128_desc(sb + ND * kBTile);  // A digits (N side)
+                    if (elect_one()) {
 #pragma unroll
-                        for (int lvl = 0; lvl < kLevels; ++lvl) {
+                        for (int kc = 0; kc < BKB / 32; ++kc) {
+#if defined(OZK_I8_EPI_MODE) && OZK_I8_EPI_MODE == 6
+                            if (kc > 0) break;  // diagnostic: only the first chunk's MMAs
+#endif
+                            if (kc == 0 && kb == 0) {
+                                // first chunk: single-digit products level by level, the
+                                // first of each level overwriting its accumulator block
 #pragma unroll
-                            for (int t = 0; t < ND; ++t) {
-                                const int u = lvl - t;
-                                if (u < 0 || u >= ND) continue;
-                                const bool first = t == (lvl - ND + 1 > 0 ? lvl - ND + 1 : 0);
-                                umma_i8(acc0 + lvl * TR, sw128_desc(sb + t * kBTile),
-                                        sw128_desc(sa + u * kATile), idesc1, first ? 0u : 1u);
+                                for (int lvl = 0; lvl < kLevels; ++lvl) {
+#pragma unroll
+                                    for (int t = 0; t < ND; ++t) {
+                                        const int u = lvl - t;
+                                        if (u < 0 || u >= ND) continue;
+                                        const bool first =
+                                            t == (lvl - ND + 1 > 0 ? lvl - ND + 1 : 0);
+                                        umma_i8(acc0 + lvl * TR, db + (t * kBTile >> 4),
+                                                da + (u * kATile >> 4), idesc1, first ? 0u : 1u);
+                                    }
+                                }
+                            } else {
+#pragma unroll
+                                for (int t = 0; t < ND; ++t)
+                                    umma_i8(acc0 + t * TR, db + ((t * kBTile + kc * 32) >> 4),
+                                            da + (kc * 32 >> 4), idescN, 1u);
                             }
                         }
-                        kc = 1;
+                        // frees the stage (here and in every CTA that multicasts into
+                        // it) when the MMAs retire; commits track this lane's MMAs
+                        if constexpr (kCluster > 1)
+                            umma_commit_mc(empty0 + 8 * stage, (uint16_t)(col_mask | row_mask));
+                        else
+                            umma_commit(empty0 + 8 * stage);
                     }
-                    for (; kc < BKB / 32; ++kc) {
-#pragma unroll
-                        for (int t = 0; t < ND; ++t)
-                            umma_i8(acc0 + t * TR, sw128_desc(sb + t * kBTile + kc * 32),
-                                    sw128_desc(sa + kc * 32), idescN, 1u);
-                    }
-                    umma_commit(empty0 + 8 * stage);  // frees the stage when the MMAs retire
+                    __syncwarp();
                     if (++stage == kStages) {
                         stage = 0;
                         phase ^= 1;
                     }
                 }
-                umma_commit(tfull0 + 8 * buf);
-                trace_stamp(step, 2, true);
+                if (elect_one()) umma_commit(tfull0 + 8 * buf);
+                __syncwarp();
+                trace_stamp(step, 2, lane == 0);
 #ifdef OZK_I8_TRACE
-                if (blockIdx.x == 0 && step < kTracePairs) g_i8_trace[step][7] = full_wait;
+                if (lane == 0 && blockIdx.x == 0 && step < kTracePairs)
+                    g_i8_trace[step][7] = full_wait;
 #endif
             }
         }
@@ -431,8 +535,8 @@ pair_gemm_i8_kernel(const __grid_constant__ MapsI8 maps, const __grid_constant__
         const uint32_t tlane = tmem + ((uint32_t)(wq * 32) << 16) + eg * kEpiRows;
         int step = 0;
         const bool tracer = warp == 4 && lane == 0;
-        for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-            const TileCoord tc = tile_of(tile, tiles_m, tiles_n);
+        for (int g = cluster_id; g < num_groups; g += num_clusters) {
+            const TileCoord tc = tile_of_group(g);
             const size_t col = (size_t)tc.tn * TC + wq * 32 + lane;
             const size_t row0 = (size_t)tc.tm * TR + eg * kEpiRows;
             const bool col_ok = col < prob.n;
@@ -524,7 +628,11 @@ pair_gemm_i8_kernel(const __grid_constant__ MapsI8 maps, const __grid_constant__
         }
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
-    __syncthreads();
+    // no CTA leaves while a peer may still multicast into it or arrive on it
+    if constexpr (kCluster > 1)
+        cluster_sync();
+    else
+        __syncthreads();
     if (warp == 1)
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
                      "n"(kTmemCols));
@@ -543,7 +651,7 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode_i8() {
     return fn;
 }
 
-template <int K, typename W, int ND, int TR, int EG = 2>
+template <int K, typename W, int ND, int TR, int EG = 2, int CM = 1, int CN = 1>
 cudaError_t launch_i8_typed(const I8Operands& op, const PairList& pairs, cudaStream_t st,
                             int num_sms) {
     using Cfg = I8Cfg<K, W, ND, TR, EG>;
@@ -553,7 +661,7 @@ cudaError_t launch_i8_typed(const I8Operands& op, const PairList& pairs, cudaStr
     {
         cuuint64_t dims[4] = {op.l, op.m, (cuuint64_t)ND, (cuuint64_t)op.d};
         cuuint64_t strides[3] = {op.a_ld, op.a_digit_stride, op.a_slice_stride};
-        cuuint32_t box[4] = {BKB, TR, 1, 1};
+        cuuint32_t box[4] = {BKB, TR / CN, 1, 1};
         cuuint32_t es[4] = {1, 1, 1, 1};
         if (encode(&maps.a, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<int8_t*>(op.a), dims,
                    strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -564,7 +672,7 @@ cudaError_t launch_i8_typed(const I8Operands& op, const PairList& pairs, cudaStr
     {
         cuuint64_t dims[4] = {op.l, op.n, (cuuint64_t)ND, (cuuint64_t)op.d};
         cuuint64_t strides[3] = {op.b_ld, op.b_digit_stride, op.b_slice_stride};
-        cuuint32_t box[4] = {BKB, TC, 1, 1};
+        cuuint32_t box[4] = {BKB, TC / CM, 1, 1};
         cuuint32_t es[4] = {1, 1, 1, 1};
         if (encode(&maps.b, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<int8_t*>(op.b), dims,
                    strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -586,15 +694,38 @@ cudaError_t launch_i8_typed(const I8Operands& op, const PairList& pairs, cudaStr
     const int tiles_m = (int)((op.m + TR - 1) / TR), tiles_n = (int)((op.n + TC - 1) / TC);
     const int num_tiles = tiles_m * tiles_n;
     if (num_tiles == 0 || pairs.count == 0) return cudaSuccess;
-    auto kern = pair_gemm_i8_kernel<K, W, ND, TR, EG, false>;
+    auto kern = pair_gemm_i8_kernel<K, W, ND, TR, EG, false, CM, CN>;
     if constexpr (sizeof(W) == 8)
-        if (vec) kern = pair_gemm_i8_kernel<K, W, ND, TR, EG, true>;
+        if (vec) kern = pair_gemm_i8_kernel<K, W, ND, TR, EG, true, CM, CN>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          Cfg::kSmemBytes);
     if (e != cudaSuccess) return e;
-    const int grid = num_tiles < num_sms ? num_tiles : num_sms;
-    kern<<<grid, Cfg::kThreads, Cfg::kSmemBytes, st>>>(maps, pairs, prob, tiles_m, tiles_n);
-    return cudaGetLastError();
+    constexpr int kCluster = CM * CN;
+    const int groups = ((tiles_m + CM - 1) / CM) * ((tiles_n + CN - 1) / CN);
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = kCluster;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.blockDim = dim3(Cfg::kThreads);
+    cfg.dynamicSmemBytes = Cfg::kSmemBytes;
+    cfg.stream = st;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    // persistent clusters: as many as can be co-resident (GPC packing can
+    // leave SMs idle for clusters > 1), never more than there are tile groups
+    int clusters = num_sms / kCluster;
+    if constexpr (kCluster > 1) {
+        cfg.gridDim = dim3(clusters * kCluster);
+        int active = 0;
+        if (cudaOccupancyMaxActiveClusters(&active, kern, &cfg) == cudaSuccess && active > 0 &&
+            active < clusters)
+            clusters = active;
+    }
+    if (groups < clusters) clusters = groups;
+    cfg.gridDim = dim3(clusters * kCluster);
+    return cudaLaunchKernelEx(&cfg, kern, maps, pairs, prob, tiles_m, tiles_n);
 }
 
 } // namespace
@@ -609,9 +740,9 @@ cudaError_t launch_pair_gemm_i8(int K, int word_bytes, const I8Operands& op,
     }
     if (op.nd != 3) return cudaErrorInvalidValue;
     switch (K) {
-    case 2: return launch_i8_typed<2, double, 3, 48, OZK_I8_EG>(op, pairs, st, num_sms);
-    case 3: return launch_i8_typed<3, double, 3, 48, OZK_I8_EG>(op, pairs, st, num_sms);
-    case 4: return launch_i8_typed<4, double, 3, 48, OZK_I8_EG>(op, pairs, st, num_sms);
+    case 2: return launch_i8_typed<2, double, 3, 48, OZK_I8_EG, OZK_I8_CM, OZK_I8_CN>(op, pairs, st, num_sms);
+    case 3: return launch_i8_typed<3, double, 3, 48, OZK_I8_EG, OZK_I8_CM, OZK_I8_CN>(op, pairs, st, num_sms);
+    case 4: return launch_i8_typed<4, double, 3, 48, OZK_I8_EG, OZK_I8_CM, OZK_I8_CN>(op, pairs, st, num_sms);
     default: return cudaErrorInvalidValue;
     }
 }
