@@ -57,6 +57,9 @@ constexpr int kGroupM = OZK_I8_GROUPM;  // tile rows per rasterization group
 #ifndef OZK_I8_CM
 #define OZK_I8_CM 2
 #endif
+#ifndef OZK_I8_PACE
+#define OZK_I8_PACE 1
+#endif
 #ifndef OZK_I8_CN
 #define OZK_I8_CN 1
 #endif
@@ -113,6 +116,10 @@ struct I8Problem {
     size_t gA_stride, gB_stride;
     void* c;           // K-word AoS C, row stride ldc elements
     size_t ldc;
+    // wave pacing (see the producer): pace[s] counts the clusters that have
+    // started global step s = wave * npairs + pair; null disables pacing
+    unsigned int* pace;
+    int pace_slack;
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -391,10 +398,36 @@ pair_gemm_i8_kernel(const __grid_constant__ MapsI8 maps, const __grid_constant__
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&maps.b)));
         int stage = 0;
         uint32_t phase = 0;
-        for (int g = cluster_id; g < num_groups; g += num_clusters) {
+        int wave = 0;
+        bool pace = prob.pace != nullptr;
+        for (int g = cluster_id; g < num_groups; g += num_clusters, ++wave) {
             const TileCoord tc = tile_of_group(g);
             for (int p = 0; p < npairs; ++p) {
                 const int al = pairs.alpha[p], be = pairs.beta[p];
+                if (pace) {
+                    // Wave pacing: all clusters stream the same slice pair of
+                    // neighbouring tiles, but persistent clusters drift apart and
+                    // the live panels then span many slices and thrash L2 (1 TB of
+                    // DRAM reads for one TD n=8192 GEMM).  Start step s only after
+                    // every cluster has started step s - slack.  Pacing is only a
+                    // hint: a wait that exceeds ~5 ms (a cluster not co-resident,
+                    // e.g. the GPU shared with other work) turns it off.
+                    const int st = wave * npairs + p, wait = st - prob.pace_slack;
+                    if (wait >= 0) {
+                        const int w2 = wait / npairs;
+                        const int left = num_groups - w2 * num_clusters;
+                        const unsigned target = (unsigned)(left < num_clusters ? left : num_clusters);
+                        const volatile unsigned* slot = prob.pace + wait;
+                        for (int spin = 0; *slot < target; ++spin) {
+                            if (spin > 20000) {
+                                pace = false;
+                                break;
+                            }
+                            __nanosleep(256);
+                        }
+                    }
+                    if (crank == 0 && pace) atomicAdd(prob.pace + st, 1u);
+                }
                 for (int kb = 0; kb < num_kb; ++kb) {
                     mbar_wait(empty0 + 8 * stage, phase ^ 1);
                     const uint32_t full = full0 + 8 * stage;
@@ -690,6 +723,8 @@ cudaError_t launch_i8_typed(const I8Operands& op, const PairList& pairs, cudaStr
     prob.gB_stride = op.n;
     prob.c = op.c;
     prob.ldc = op.ldc;
+    prob.pace = nullptr;
+    prob.pace_slack = OZK_I8_PACE;
     const bool vec = sizeof(W) == 8 && (reinterpret_cast<uintptr_t>(op.c) & 15) == 0;
     const int tiles_m = (int)((op.m + TR - 1) / TR), tiles_n = (int)((op.n + TC - 1) / TC);
     const int num_tiles = tiles_m * tiles_n;
@@ -725,7 +760,20 @@ cudaError_t launch_i8_typed(const I8Operands& op, const PairList& pairs, cudaStr
     }
     if (groups < clusters) clusters = groups;
     cfg.gridDim = dim3(clusters * kCluster);
-    return cudaLaunchKernelEx(&cfg, kern, maps, pairs, prob, tiles_m, tiles_n);
+    // pacing counters: one per (wave, pair) step, stream-ordered scratch
+    const size_t steps = (size_t)((groups + clusters - 1) / clusters) * pairs.count;
+    if (OZK_I8_PACE > 0 && clusters > 1) {
+        e = cudaMallocAsync(reinterpret_cast<void**>(&prob.pace), steps * sizeof(unsigned), st);
+        if (e != cudaSuccess) return e;
+        e = cudaMemsetAsync(prob.pace, 0, steps * sizeof(unsigned), st);
+        if (e != cudaSuccess) return e;
+    }
+    e = cudaLaunchKernelEx(&cfg, kern, maps, pairs, prob, tiles_m, tiles_n);
+    if (prob.pace) {
+        const cudaError_t f = cudaFreeAsync(prob.pace, st);
+        if (e == cudaSuccess) e = f;
+    }
+    return e;
 }
 
 } // namespace
