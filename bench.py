@@ -329,7 +329,7 @@ def run_ours(args):
         t = torch.tensor([t_step], device="cuda")
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         t_step = float(t.item())
-    engine_used = ENGINE_NAMES.get(prof.engine, "dmma") if world == 1 else "dmma"
+    engine_used = ENGINE_NAMES.get(prof.engine, "dmma") if world == 1 else eng.engine
     value = 2.0 * n ** 3 / t_step / 1e9
     t_kern = statistics.mean(kern)
     rows_local = n if world == 1 else eng.rows_local

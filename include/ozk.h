@@ -159,6 +159,31 @@ ozk_status ozk_slices_gemm_device(ozk_format fmt, size_t m, size_t l, size_t n,
                                   const int* pairs, int npairs, void* c, size_t ldc,
                                   void* stream);
 
+/* ---- INT8-digit slice entry points (sharded orchestration, INT8 engine) ---- *
+ * The exact INT8 engine stores each slice as nd signed base-256 digit planes of
+ * the slice integers plus one grid exponent per row (A) / column (B):
+ *   piece_a(i, k) = 2^exps[a][i] * sum_t 256^t * digits[a][t][i][k]
+ * digits: split_count x nd x plane_rows x ld8 int8 (ld8 >= inner dimension, a
+ * multiple of 16, zero padded), exps: split_count x plane_rows ints.  nd is
+ * ozk_int8_digits(fmt, inner, split_count); 0 means the engine does not apply
+ * (binary64 slices at inner dimension <= 512, or inner >= 43690).  The products
+ * and the K-word accumulation are bit-identical to ozk_slices_gemm_device. */
+int ozk_int8_digits(ozk_format fmt, size_t inner_dim, int split_count);
+
+ozk_status ozk_split_digits_device(ozk_format fmt, size_t rows, size_t cols, size_t ld,
+                                   const void* mat, int split_count, ozk_side side,
+                                   int8_t* digits, size_t ld8, size_t plane_rows, int* exps,
+                                   double* piece_max, void* stream);
+
+/* Fused INT8 slice-pair GEMMs + K-word accumulation over digit planes: A digits
+ * for m rows (a_plane_rows >= m), B digits for n columns (b_plane_rows >= n),
+ * both with row length ld8; c is m x n K-word, row stride ldc, overwritten. */
+ozk_status ozk_digits_gemm_device(ozk_format fmt, size_t m, size_t l, size_t n,
+                                  const int8_t* a_digits, const int* a_exps, size_t a_plane_rows,
+                                  const int8_t* b_digits, const int* b_exps, size_t b_plane_rows,
+                                  size_t ld8, int split_count, const int* pairs, int npairs,
+                                  void* c, size_t ldc, void* stream);
+
 /* Parity hook: every slice product C_ab = A_alpha * B_beta of the pair list,
  * binary64, into products[p] (m x n row-major). */
 ozk_status ozk_pair_products_device(size_t m, size_t l, size_t n, const double* a_slices,

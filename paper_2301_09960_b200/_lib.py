@@ -53,6 +53,13 @@ SIGNATURES = {
     "ozk_slices_gemm_device": (ctypes.c_int, [ctypes.c_int, _sz, _sz, _sz, _dp, _dp, _sz, _sz,
                                               _sz, ctypes.c_int, _ip, ctypes.c_int, _dp, _sz,
                                               ctypes.c_void_p]),
+    "ozk_int8_digits": (ctypes.c_int, [ctypes.c_int, _sz, ctypes.c_int]),
+    "ozk_split_digits_device": (ctypes.c_int, [ctypes.c_int, _sz, _sz, _sz, _dp, ctypes.c_int,
+                                               ctypes.c_int, _dp, _sz, _sz, _dp, _dp,
+                                               ctypes.c_void_p]),
+    "ozk_digits_gemm_device": (ctypes.c_int, [ctypes.c_int, _sz, _sz, _sz, _dp, _dp, _sz, _dp,
+                                              _dp, _sz, _sz, ctypes.c_int, _ip, ctypes.c_int,
+                                              _dp, _sz, ctypes.c_void_p]),
     "ozk_pair_products_device": (ctypes.c_int, [_sz, _sz, _sz, _dp, _dp, ctypes.c_int, _ip,
                                                 ctypes.c_int, _dp, ctypes.c_void_p]),
     "ozk_gen_eq1_device": (ctypes.c_int, [ctypes.c_int, _sz, _sz, ctypes.c_uint64, _dp,

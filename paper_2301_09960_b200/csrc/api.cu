@@ -591,6 +591,100 @@ ozk_status ozk_slices_gemm_device(ozk_format fmt, size_t m, size_t l, size_t n,
     return OZK_OK;
 }
 
+int ozk_int8_digits(ozk_format fmt, size_t inner_dim, int d) {
+    if (!valid_fmt(fmt)) return 0;
+    return int8_digits(fmt, inner_dim, d);
+}
+
+ozk_status ozk_split_digits_device(ozk_format fmt, size_t rows, size_t cols, size_t ld,
+                                   const void* mat, int d, ozk_side side, int8_t* digits,
+                                   size_t ld8, size_t plane_rows, int* exps, double* piece_max,
+                                   void* stream) {
+    if (!valid_fmt(fmt)) return fail(OZK_EPARAM, "split_digits: format must be DD, TD, QD or TS");
+    if (rows == 0 || cols == 0) return fail(OZK_ESHAPE, "matrix dimensions must be positive");
+    if (d < 1) return fail(OZK_EPARAM, "split_matrix: split count must be >= 1");
+    if (d > kMaxSplits) return fail(OZK_EPARAM, "split_matrix: split count above 32 is not supported");
+    if (ld < cols) return fail(OZK_ESHAPE, "split_matrix: ld < cols");
+    const size_t inner = side == OZK_SIDE_ROWS ? cols : rows;
+    const size_t outer = side == OZK_SIDE_ROWS ? rows : cols;
+    const int nd = int8_digits(fmt, inner, d);
+    if (nd == 0) return fail(OZK_EPARAM, "split_digits: INT8 engine not applicable to this inner dimension");
+    if (ld8 < inner || ld8 % 16) return fail(OZK_ESHAPE, "split_digits: ld8 must be >= inner and a multiple of 16");
+    if (plane_rows < outer) return fail(OZK_ESHAPE, "split_digits: plane_rows < outer dimension");
+    if (!digits || !exps) return fail(OZK_EPARAM, "split_digits: null output");
+    cudaStream_t st = (cudaStream_t)stream;
+    num_sms_cached();
+    DigitOut dig;
+    dig.nd = nd;
+    dig.digits = digits;
+    dig.ld = ld8;
+    dig.digit_stride = plane_rows * ld8;
+    dig.slice_stride = (size_t)nd * plane_rows * ld8;
+    dig.exps = exps;
+    dig.exp_stride = plane_rows;
+    DevBuf work, flags;
+    OZK_CUDA(work.alloc(elem_bytes(fmt) * rows * cols, st), "split_digits: work");
+    OZK_CUDA(flags.alloc(8, st), "split_digits: flags");
+    OZK_CUDA(cudaMemsetAsync(flags.p, 0, 8, st), "split_digits: memset");
+    OZK_CUDA(split_to_slices(fmt, rows, cols, ld, mat, d, side, nullptr, plane_rows, work.p,
+                             reinterpret_cast<unsigned long long*>(piece_max), flags.as<int>(), st,
+                             dig),
+             "split_digits");
+    int flag = 0;
+    OZK_CUDA(cudaMemcpyAsync(&flag, flags.p, sizeof(int), cudaMemcpyDeviceToHost, st),
+             "split_digits: flag");
+    OZK_CUDA(cudaStreamSynchronize(st), "split_digits");
+    return check_dev_err(flag, "split_matrix");
+}
+
+ozk_status ozk_digits_gemm_device(ozk_format fmt, size_t m, size_t l, size_t n,
+                                  const int8_t* a_digits, const int* a_exps, size_t a_plane_rows,
+                                  const int8_t* b_digits, const int* b_exps, size_t b_plane_rows,
+                                  size_t ld8, int d, const int* pairs, int npairs, void* c,
+                                  size_t ldc, void* stream) {
+    if (!valid_fmt(fmt)) return fail(OZK_EPARAM, "digits_gemm: format must be DD, TD, QD or TS");
+    if (m == 0 || l == 0 || n == 0) return fail(OZK_ESHAPE, "matrix dimensions must be positive");
+    if (d < 1 || d > kMaxSplits) return fail(OZK_EPARAM, "digits_gemm: bad split count");
+    const int nd = int8_digits(fmt, l, d);
+    if (nd == 0) return fail(OZK_EPARAM, "digits_gemm: INT8 engine not applicable to this inner dimension");
+    if (ld8 < l || ld8 % 16) return fail(OZK_ESHAPE, "digits_gemm: ld8 must be >= l and a multiple of 16");
+    if (a_plane_rows < m || b_plane_rows < n) return fail(OZK_ESHAPE, "digits_gemm: plane_rows too small");
+    if (ldc < n) return fail(OZK_ESHAPE, "digits_gemm: ldc < n");
+    PairList pl;
+    if (ozk_status s = fill_pairs(d, pairs, npairs, pl)) return s;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (pl.count == 0) {
+        OZK_CUDA(cudaMemset2DAsync(c, ldc * elem_bytes(fmt), 0, n * elem_bytes(fmt), m, st),
+                 "digits_gemm: zero");
+    } else {
+        I8Operands op{};
+        op.nd = nd;
+        op.a = a_digits;
+        op.a_ld = ld8;
+        op.a_digit_stride = a_plane_rows * ld8;
+        op.a_slice_stride = (size_t)nd * a_plane_rows * ld8;
+        op.b = b_digits;
+        op.b_ld = ld8;
+        op.b_digit_stride = b_plane_rows * ld8;
+        op.b_slice_stride = (size_t)nd * b_plane_rows * ld8;
+        op.gA = a_exps;
+        op.gB = b_exps;
+        op.gA_stride = a_plane_rows;
+        op.gB_stride = b_plane_rows;
+        op.m = m;
+        op.n = n;
+        op.l = l;
+        op.d = d;
+        op.c = c;
+        op.ldc = ldc;
+        OZK_CUDA(launch_pair_gemm_i8(words_of(fmt), word_bytes_of(fmt), op, pl, st,
+                                     num_sms_cached()),
+                 "digits_gemm");
+    }
+    OZK_CUDA(cudaStreamSynchronize(st), "digits_gemm");
+    return OZK_OK;
+}
+
 ozk_status ozk_pair_products_device(size_t m, size_t l, size_t n, const double* a_slices,
                                     const double* b_slices, int d, const int* pairs, int npairs,
                                     double* products, void* stream) {

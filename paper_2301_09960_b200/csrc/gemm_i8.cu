@@ -719,8 +719,8 @@ cudaError_t launch_i8_typed(const I8Operands& op, const PairList& pairs, cudaStr
     prob.l = op.l;
     prob.gA = op.gA;
     prob.gB = op.gB;
-    prob.gA_stride = op.m;
-    prob.gB_stride = op.n;
+    prob.gA_stride = op.gA_stride ? op.gA_stride : op.m;
+    prob.gB_stride = op.gB_stride ? op.gB_stride : op.n;
     prob.c = op.c;
     prob.ldc = op.ldc;
     prob.pace = nullptr;

@@ -85,8 +85,9 @@ struct I8Operands {
     size_t a_ld, a_digit_stride, a_slice_stride;
     const int8_t* b;
     size_t b_ld, b_digit_stride, b_slice_stride;
-    const int* gA;  // [d][m]
-    const int* gB;  // [d][n]
+    const int* gA;  // [d][gA_stride]
+    const int* gB;  // [d][gB_stride]
+    size_t gA_stride = 0, gB_stride = 0;  // 0: m / n
     size_t m, n, l;
     int d;
     void* c;        // K-word AoS, row stride ldc elements

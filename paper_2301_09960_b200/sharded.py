@@ -14,6 +14,14 @@ Rank r of W owns C rows [r0, r1) and B columns [c0, c1):
    per-element accumulation order is unchanged, so C is bit-identical for any
    number of GPUs.
 
+Two slice representations, bit-identical results:
+* INT8 engine (default where it applies, ozk_int8_digits > 0): the splits write
+  nd int8 digit planes + one grid exponent per row/column
+  (ozk_split_digits_device), the all-gather moves D*nd*l*ceil(n/W) bytes per
+  rank (2.7x less than FP64 slices), the gathered planes are permuted once to
+  [D][nd][W*ncb][ld8] and ozk_digits_gemm_device runs the pairs on tcgen05;
+* DMMA engine: FP64 slices (ozk_split_slices_device / ozk_slices_gemm_device).
+
 The gathered B slices stay in the layout the all-gather produces
 ([W][D][ncb][ld]); the GEMM kernel addresses column j in block j // ncb
 directly (ozk_slices_gemm_device), so no re-layout copy is needed.
@@ -116,6 +124,32 @@ class GpuOps:
             plan.world, plan.d * plan.ncb * plan.ld, plan.d, flat, len(pairs), c.data_ptr(),
             plan.n, self._stream()))
 
+    # ---- INT8 engine ----
+    def int8_layout(self, K, l, d):
+        """(nd, ld8) of the digit planes, or None where the engine does not apply
+        (or the DMMA engine is forced with ozk_set_engine)."""
+        if self.lib.ozk_get_engine() == 1:
+            return None
+        nd = self.lib.ozk_int8_digits(K, l, d)
+        return (nd, (l + 15) & ~15) if nd > 0 else None
+
+    def digit_planes(self, d, nd, rows, ld8):
+        return (torch.zeros((d, nd, rows, ld8), dtype=torch.int8, device=self.device),
+                torch.zeros((d, rows), dtype=torch.int32, device=self.device))
+
+    def split_digits(self, K, mat, rows, cols, ld, d, side, digits, exps, pmax):
+        self._check(self.lib.ozk_split_digits_device(
+            K, rows, cols, ld, mat.data_ptr(), d, side, digits.data_ptr(), digits.shape[3],
+            digits.shape[2], exps.data_ptr(), pmax.data_ptr() if pmax is not None else None,
+            self._stream()))
+
+    def gemm_digits(self, plan: ShardPlan, a8, ga, b8, gb, pairs, c):
+        flat = (ctypes.c_int * (2 * len(pairs)))(*[v for p in pairs for v in p])
+        self._check(self.lib.ozk_digits_gemm_device(
+            plan.K, plan.rows_local, plan.l, plan.n, a8.data_ptr(), ga.data_ptr(), a8.shape[2],
+            b8.data_ptr(), gb.data_ptr(), b8.shape[2], a8.shape[3], plan.d, flat, len(pairs),
+            c.data_ptr(), plan.n, self._stream()))
+
 
 class ShardedOzaki:
     """One rank's part of a C block-row sharded Ozaki GEMM."""
@@ -126,9 +160,19 @@ class ShardedOzaki:
         self.group = group
         self.drop = float(drop_threshold)
         p = self.plan
-        self.sa = self.ops.zeros((d, max(p.rows_local, 1), p.ld))
-        self.sb = self.ops.zeros((d, p.ncb, p.ld))
-        self.sb_all = self.ops.zeros((world, d, p.ncb, p.ld))
+        layout = self.ops.int8_layout(K, l, d) if hasattr(self.ops, "int8_layout") else None
+        self.engine = "int8" if layout else "dmma"
+        if layout:
+            nd, ld8 = layout
+            self.a8, self.ga = self.ops.digit_planes(d, nd, max(p.rows_local, 1), ld8)
+            self.b8, self.gb = self.ops.digit_planes(d, nd, p.ncb, ld8)
+            self.b8_all, self.gb_all = self.ops.digit_planes(world * d, nd, p.ncb, ld8)
+            self.b8_all = self.b8_all.view(world, d, nd, p.ncb, ld8)
+            self.gb_all = self.gb_all.view(world, d, p.ncb)
+        else:
+            self.sa = self.ops.zeros((d, max(p.rows_local, 1), p.ld))
+            self.sb = self.ops.zeros((d, p.ncb, p.ld))
+            self.sb_all = self.ops.zeros((world, d, p.ncb, p.ld))
         self.c = self.ops.zeros((max(p.rows_local, 1), n, p.words),
                                 dtype=torch.float32 if K == OZK_TS else torch.float64)
         self.pmax = self.ops.zeros((2, d)) if self.drop > 0.0 else None
@@ -138,12 +182,27 @@ class ShardedOzaki:
     def rows_local(self) -> int:
         return self.plan.rows_local
 
-    def _all_gather(self):
+    def _gather(self, out, local):
         if dist.get_backend(self.group) == "nccl":
-            dist.all_gather_into_tensor(self.sb_all, self.sb, group=self.group)
+            dist.all_gather_into_tensor(out, local, group=self.group)
         else:
-            parts = list(self.sb_all.unbind(0))
-            dist.all_gather(parts, self.sb, group=self.group)
+            parts = list(out.unbind(0))
+            dist.all_gather(parts, local, group=self.group)
+
+    def _all_gather(self):
+        if self.engine == "int8":
+            # [W][D][nd][ncb][ld8] -> one plane set [D][nd][W*ncb][ld8]: column j
+            # of the gathered B is row j of every plane (the ceil partition puts
+            # rank r's columns at r*ncb), exponents likewise [D][W*ncb]
+            self._gather(self.b8_all, self.b8)
+            self._gather(self.gb_all, self.gb)
+            p = self.plan
+            w, d, nd, ncb, ld8 = self.b8_all.shape
+            self.b8_cat = self.b8_all.permute(1, 2, 0, 3, 4).reshape(d, nd, w * ncb, ld8)
+            self.gb_cat = self.gb_all.permute(1, 0, 2).reshape(d, w * ncb)
+            assert w * ncb >= p.n
+        else:
+            self._gather(self.sb_all, self.sb)
 
     def run(self, A, B, prof=None):
         """A: (m, l, K) or this rank's rows; B: (l, n, K) full (row stride n).
@@ -155,13 +214,21 @@ class ShardedOzaki:
         a_rows = A[p.r0:p.r1] if A.shape[0] == p.m else A
         if self.pmax is not None:
             self.pmax.zero_()
+        amax = self.pmax[0] if self.pmax is not None else None
+        bmax = self.pmax[1] if self.pmax is not None else None
         if p.rows_local:
-            ops.split(p.K, a_rows, p.rows_local, p.l, p.l, p.d, 0, self.sa,
-                      self.pmax[0] if self.pmax is not None else None)
+            if self.engine == "int8":
+                ops.split_digits(p.K, a_rows, p.rows_local, p.l, p.l, p.d, 0, self.a8, self.ga,
+                                 amax)
+            else:
+                ops.split(p.K, a_rows, p.rows_local, p.l, p.l, p.d, 0, self.sa, amax)
         if p.c1 > p.c0:
             # column block [c0, c1) of the row-major (l x n) B, split in place
-            ops.split(p.K, B[:, p.c0:p.c1], p.l, p.c1 - p.c0, p.n, p.d, 1, self.sb,
-                      self.pmax[1] if self.pmax is not None else None)
+            if self.engine == "int8":
+                ops.split_digits(p.K, B[:, p.c0:p.c1], p.l, p.c1 - p.c0, p.n, p.d, 1, self.b8,
+                                 self.gb, bmax)
+            else:
+                ops.split(p.K, B[:, p.c0:p.c1], p.l, p.c1 - p.c0, p.n, p.d, 1, self.sb, bmax)
         if self.timing:
             ev[1].record()
         self._all_gather()
@@ -174,10 +241,12 @@ class ShardedOzaki:
         if self.timing:
             ev[2].record()
         if p.rows_local:
-            if pairs:
-                ops.gemm(p, self.sa, self.sb_all, pairs, self.c)
-            else:
+            if not pairs:
                 self.c.zero_()
+            elif self.engine == "int8":
+                ops.gemm_digits(p, self.a8, self.ga, self.b8_cat, self.gb_cat, pairs, self.c)
+            else:
+                ops.gemm(p, self.sa, self.sb_all, pairs, self.c)
         if self.timing:
             ev[3].record()
             torch.cuda.current_stream().synchronize()
@@ -190,4 +259,5 @@ class ShardedOzaki:
                 prof.split_count = p.d
                 prof.pairs = len(pairs)
                 prof.gpus = p.world
+                prof.engine = 2 if self.engine == "int8" else 1
         return self.c[: p.rows_local]

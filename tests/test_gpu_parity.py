@@ -295,6 +295,62 @@ def test_sharded_layout_single_gpu(ozk, cpu, K, m, l, n, d, world):
         assert_bitwise(c.cpu().numpy(), want[p.r0:p.r1], f"rank {p.rank} rows")
 
 
+@pytest.mark.parametrize("K,m,l,n,d,world", [(2, 300, 600, 390, 6, 3), (3, 129, 1030, 256, 9, 2),
+                                             (4, 64, 700, 130, 12, 4), (2, 50, 4100, 70, 7, 8)])
+def test_sharded_digits_single_gpu(ozk, cpu, K, m, l, n, d, world):
+    """The sharded INT8-engine data path on one GPU: each emulated rank splits
+    its B column block in place into digit planes [D][nd][ncb][ld8] + exponents,
+    the gathered [W][D][nd][ncb] planes are permuted to [D][nd][W*ncb] exactly
+    as ShardedOzaki does after the all-gather, and every rank's digit-plane GEMM
+    gives the reference's C rows bit for bit."""
+    import torch
+
+    from paper_2301_09960_b200.sharded import GpuOps, ShardPlan, triangular_pairs
+    a = cpu.gen_eq1(K, m, l, 51)
+    b = cpu.gen_eq1(K, l, n, 52)
+    want = cpu.ozaki_gemm(K, a, b, d)
+    A = torch.from_numpy(a).cuda()
+    B = torch.from_numpy(b).cuda()
+    ops = GpuOps()
+    nd, ld8 = ops.int8_layout(K, l, d)
+    assert nd == 3
+    plans = [ShardPlan(K, m, l, n, d, r, world) for r in range(world)]
+    ncb = plans[0].ncb
+    b8_all, gb_all = ops.digit_planes(world * d, nd, ncb, ld8)
+    b8_all = b8_all.view(world, d, nd, ncb, ld8)
+    gb_all = gb_all.view(world, d, ncb)
+    for p in plans:
+        if p.c1 > p.c0:
+            ops.split_digits(K, B[:, p.c0:p.c1], l, p.c1 - p.c0, n, d, 1, b8_all[p.rank],
+                             gb_all[p.rank], None)
+    b8 = b8_all.permute(1, 2, 0, 3, 4).reshape(d, nd, world * ncb, ld8)
+    gb = gb_all.permute(1, 0, 2).reshape(d, world * ncb)
+    pairs = triangular_pairs(d)
+    for p in plans:
+        a8, ga = ops.digit_planes(d, nd, p.rows_local, ld8)
+        ops.split_digits(K, A[p.r0:p.r1], p.rows_local, l, l, d, 0, a8, ga, None)
+        c = ops.zeros((p.rows_local, n, K))
+        ops.gemm_digits(p, a8, ga, b8, gb, pairs, c)
+        assert_bitwise(c.cpu().numpy(), want[p.r0:p.r1], f"rank {p.rank} rows")
+
+
+def test_digit_entry_points_reject_inapplicable(ozk):
+    """ozk_int8_digits is 0 at l <= 512 (binary64), and the digit entry points
+    refuse such shapes instead of computing something else."""
+    import torch
+
+    from paper_2301_09960_b200._lib import lib
+    assert lib.ozk_int8_digits(2, 512, 6) == 0
+    assert lib.ozk_int8_digits(2, 513, 6) == 3
+    assert lib.ozk_int8_digits(0x103, 8192, 15) == 1
+    x = torch.zeros((8, 8, 2), dtype=torch.float64, device="cuda")
+    dg = torch.zeros((6, 3, 8, 16), dtype=torch.int8, device="cuda")
+    ex = torch.zeros((6, 8), dtype=torch.int32, device="cuda")
+    st = torch.cuda.current_stream().cuda_stream
+    assert lib.ozk_split_digits_device(2, 8, 8, 8, x.data_ptr(), 6, 0, dg.data_ptr(), 16, 8,
+                                       ex.data_ptr(), None, st) != 0
+
+
 @pytest.mark.parametrize("K,m,l,n,d", [(2, 256, 256, 256, 6), (3, 256, 256, 256, 9),
                                        (4, 256, 256, 256, 12), (2, 1000, 900, 1100, 7)])
 def test_repeat_runs_race_free(ozk, cpu, K, m, l, n, d):

@@ -48,7 +48,37 @@ class OracleOps:
         c[:mr] = torch.from_numpy(acc.reshape(mr, n, K))
 
 
-def _worker(rank, world, port_num, cases, q):
+class OracleDigitOps(OracleOps):
+    """The INT8-engine data path of ShardedOzaki (digit-plane buffers, exponent
+    gather, the [W][D][nd][ncb] -> [D][nd][W*ncb] permute, plane strides) with
+    the oracle's binary64 slices standing in for the digit planes (nd = 1,
+    float64 "digits") -- the layout logic is shape-generic; the digit encoding
+    itself is checked on the GPU (tests/test_gpu_parity.py)."""
+
+    def int8_layout(self, K, l, d):
+        return (1, l + (l & 1))
+
+    def digit_planes(self, d, nd, rows, ld8):
+        return torch.zeros((d, nd, rows, ld8), dtype=torch.float64), \
+            torch.zeros((d, rows), dtype=torch.int32)
+
+    def split_digits(self, K, mat, rows, cols, ld, d, side, digits, exps, pmax):
+        self.split(K, mat, rows, cols, ld, d, side, digits[:, 0], pmax)
+        exps.fill_(7)  # gathered alongside, checked in gemm_digits
+
+    def gemm_digits(self, plan, a8, ga, b8, gb, pairs, c):
+        assert b8.shape[2] == plan.world * plan.ncb and bool((gb[:, :plan.n] == 7).all())
+        assert a8.shape[2] >= plan.rows_local and bool((ga == 7).all())
+        K, l, n = plan.K, plan.l, plan.n
+        mr = plan.rows_local
+        acc = np.zeros((mr * n, K))
+        for (a, b) in pairs:
+            prod = a8[a, 0, :mr, :l].numpy() @ b8[b, 0, :n, :l].numpy().T
+            acc = self.port.mf_add_double(K, acc, prod.reshape(-1))
+        c[:mr] = torch.from_numpy(acc.reshape(mr, n, K))
+
+
+def _worker(rank, world, port_num, cases, q, digits=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port_num)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -60,8 +90,9 @@ def _worker(rank, world, port_num, cases, q):
             a = port.gen_eq1(K, m, l, 31 + m)
             b = port.gen_eq1(K, l, n, 32 + m)
             want = port.ozaki_gemm(K, a, b, d, drop)
-            eng = ShardedOzaki(K, m, l, n, d, rank, world, ops=OracleOps(port),
-                               drop_threshold=drop)
+            ops = OracleDigitOps(port) if digits else OracleOps(port)
+            eng = ShardedOzaki(K, m, l, n, d, rank, world, ops=ops, drop_threshold=drop)
+            assert eng.engine == ("int8" if digits else "dmma")
             got = eng.run(torch.from_numpy(a), torch.from_numpy(b)).numpy()
             r0, r1 = eng.plan.r0, eng.plan.r1
             ok = np.array_equal(got.view(np.uint64), want[r0:r1].view(np.uint64))
@@ -76,13 +107,14 @@ def _free_port():
         return s.getsockname()[1]
 
 
+@pytest.mark.parametrize("digits", [False, True], ids=["fp64-slices", "digit-planes"])
 @pytest.mark.parametrize("world", [2, 3])
-def test_sharded_matches_single_process(world):
+def test_sharded_matches_single_process(world, digits):
     cases = [(2, 10, 12, 9, 4, 0.0), (3, 7, 9, 11, 5, 0.0), (2, 13, 16, 14, 5, 2.0 ** -60),
              (4, 5, 6, 4, 6, 0.0)]
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    mp.spawn(_worker, args=(world, _free_port(), cases, q), nprocs=world, join=True)
+    mp.spawn(_worker, args=(world, _free_port(), cases, q, digits), nprocs=world, join=True)
     results = [q.get() for _ in range(world * len(cases))]
     bad = [r for r in results if not r[2]]
     assert not bad, bad
