@@ -57,6 +57,12 @@ constexpr int kGroupM = OZK_I8_GROUPM;  // tile rows per rasterization group
 #ifndef OZK_I8_CM
 #define OZK_I8_CM 2
 #endif
+#ifndef OZK_I8_TR
+#define OZK_I8_TR 64
+#endif
+#ifndef OZK_I8_NB
+#define OZK_I8_NB 1
+#endif
 #ifndef OZK_I8_PACE
 #define OZK_I8_PACE 1
 #endif
@@ -72,7 +78,11 @@ constexpr int kSmemBudget = 221 * 1024;       // operand ring
 //   TR  tile C rows per digit (MMA N); 2*ND-1 level accumulators of TR TMEM
 //       columns each, stacked MMA width ND*TR <= 256, two accumulator buffers
 //   EG  epilogue warpgroups; each owns TR/EG rows of the tile
-template <int K, typename W, int ND, int TR, int EG>
+//   NB  accumulator buffers in TMEM: 2 = the epilogue reads the levels in place
+//       while the next pair's MMAs fill the other buffer; 1 = the epilogue
+//       drains the levels to registers first and releases TMEM at once (taller
+//       tiles fit: 5 levels x TR <= 512)
+template <int K, typename W, int ND, int TR, int EG, int NB = 2>
 struct I8Cfg {
     static constexpr int kLevels = 2 * ND - 1;
     static constexpr int kBTile = TC * BKB;   // one B digit (C columns), MMA operand A
@@ -81,8 +91,8 @@ struct I8Cfg {
     static constexpr int kStages = kSmemBudget / kStageBytes < 8 ? kSmemBudget / kStageBytes : 8;
     static constexpr int kSmemBytes = kStages * kStageBytes + 1024 + 256;
     static constexpr int kBufCols = kLevels * TR;  // one accumulator buffer
-    static constexpr int kTmemCols = 2 * kBufCols <= 32 ? 32 : 2 * kBufCols <= 64 ? 64
-                                   : 2 * kBufCols <= 128 ? 128 : 2 * kBufCols <= 256 ? 256 : 512;
+    static constexpr int kTmemCols = NB * kBufCols <= 32 ? 32 : NB * kBufCols <= 64 ? 64
+                                   : NB * kBufCols <= 128 ? 128 : NB * kBufCols <= 256 ? 256 : 512;
     static constexpr int kThreads = (4 + 4 * EG) * 32;
     static constexpr int kEpiRows = TR / EG;  // C rows per epilogue thread
     // rows per K-word update step; two steps (ping-pong C buffers) per loop trip
@@ -96,7 +106,8 @@ struct I8Cfg {
         (kLaunchRegs + (kLaunchRegs - 40) / EG) / 8 * 8 > 232
             ? 232 : (kLaunchRegs + (kLaunchRegs - 40) / EG) / 8 * 8;
     static_assert(kStages >= 2, "operand ring too small");
-    static_assert(2 * kBufCols <= 512, "TMEM: two accumulator buffers");
+    static_assert(NB * kBufCols <= 512 && (NB == 1 || NB == 2), "TMEM accumulator buffers");
+    static_assert(NB == 2 || kEpiRows % 4 == 0, "drain width");
     static_assert(ND * TR <= 256 && TR % 16 == 0, "stacked MMA width");
     static_assert(kATile % 1024 == 0, "A-digit tiles must stack in 8-row swizzle groups");
     static_assert(kEpiRows % (2 * kChunk) == 0, "epilogue rows per ping-pong trip");
@@ -208,9 +219,22 @@ __device__ __forceinline__ void umma_commit(uint32_t bar) {
 }
 
 template <int N>
-__device__ __forceinline__ void tmem_ld(uint32_t taddr, int32_t (&v)[N]) {
-    static_assert(N == 2 || N == 4, "tmem_ld width");
-    if constexpr (N == 2) {
+__device__ __forceinline__ void tmem_ld(uint32_t taddr, int32_t* v) {
+    static_assert(N == 2 || N == 4 || N == 8 || N == 16, "tmem_ld width");
+    if constexpr (N == 16) {
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,"
+            "%13,%14,%15}, [%16];"
+            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+              "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),
+              "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+            : "r"(taddr));
+    } else if constexpr (N == 8) {
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                     : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]),
+                       "=r"(v[6]), "=r"(v[7])
+                     : "r"(taddr));
+    } else if constexpr (N == 2) {
         asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0,%1}, [%2];"
                      : "=r"(v[0]), "=r"(v[1]) : "r"(taddr));
     } else {
@@ -323,13 +347,13 @@ __device__ __forceinline__ void trace_stamp(int, int, bool) {}
 // CN CTAs of a cluster row share the A-digit tile the same way.  A stage of CTA
 // x is written by x's cluster row and column, so its empty barrier counts
 // CM + CN - 1 MMA completions, each CTA's commit arriving on all of them.
-template <int K, typename W, int ND, int TR, int EG, bool kVec, int CM, int CN>
-__global__ void __launch_bounds__(I8Cfg<K, W, ND, TR, EG>::kThreads, 1)
+template <int K, typename W, int ND, int TR, int EG, bool kVec, int CM, int CN, int NB>
+__global__ void __launch_bounds__(I8Cfg<K, W, ND, TR, EG, NB>::kThreads, 1)
 pair_gemm_i8_kernel(const __grid_constant__ MapsI8 maps, const __grid_constant__ PairList pairs,
                     I8Problem prob, int tiles_m, int tiles_n) {
     constexpr int kCluster = CM * CN;
     static_assert((TC / CM) % 8 == 0 && (TR / CN) % 8 == 0, "multicast slices of 8-row atoms");
-    using Cfg = I8Cfg<K, W, ND, TR, EG>;
+    using Cfg = I8Cfg<K, W, ND, TR, EG, NB>;
     constexpr int kStages = Cfg::kStages, kStageBytes = Cfg::kStageBytes;
     constexpr int kATile = Cfg::kATile, kBTile = Cfg::kBTile, kEpiRows = Cfg::kEpiRows;
     constexpr int kTmemCols = Cfg::kTmemCols, kLevels = Cfg::kLevels, kBufCols = Cfg::kBufCols;
@@ -481,9 +505,9 @@ pair_gemm_i8_kernel(const __grid_constant__ MapsI8 maps, const __grid_constant__
         for (int g = cluster_id; g < num_groups; g += num_clusters) {
             for (int p = 0; p < npairs; ++p, ++step) {
                 // accumulator buffer step % 2, free once the epilogue of step - 2 is done
-                const int buf = step & 1;
+                const int buf = NB == 2 ? step & 1 : 0;
                 trace_stamp(step, 0, lane == 0);
-                mbar_wait(tempty0 + 8 * buf, ((step >> 1) & 1) ^ 1);
+                mbar_wait(tempty0 + 8 * buf, ((step / NB) & 1) ^ 1);
                 trace_stamp(step, 1, lane == 0);
                 asm volatile("tcgen05.fence::after_thread_sync;");
                 const uint32_t acc0 = tmem + buf * kBufCols;
@@ -576,13 +600,13 @@ pair_gemm_i8_kernel(const __grid_constant__ MapsI8 maps, const __grid_constant__
             // out-of-range lanes and rows read a valid element and never store
             const size_t col_c = col_ok ? col : prob.n - 1;
             for (int p = 0; p < npairs; ++p, ++step) {
-                const int buf = step & 1;
+                const int buf = NB == 2 ? step & 1 : 0;
                 const int al = pairs.alpha[p], be = pairs.beta[p];
                 const int gb = prob.gB[(size_t)be * prob.gB_stride + col_c];
                 const int* gap = prob.gA + (size_t)al * prob.gA_stride;
                 const bool first = p == 0;  // C starts from zero
                 trace_stamp(step, 3, tracer);
-                mbar_wait(tfull0 + 8 * buf, (step >> 1) & 1);
+                mbar_wait(tfull0 + 8 * buf, (step / NB) & 1);
                 trace_stamp(step, 4, tracer);
                 asm volatile("tcgen05.fence::after_thread_sync;");
                 const uint32_t tbuf = tlane + buf * kBufCols;
@@ -607,24 +631,52 @@ pair_gemm_i8_kernel(const __grid_constant__ MapsI8 maps, const __grid_constant__
                         }
                     }
                 };
-                auto update_chunk = [&](int r, W (&w)[kChunk][K]) {
-                    int32_t lv[kLevels][kChunk];
-#if defined(OZK_I8_EPI_MODE) && OZK_I8_EPI_MODE == 4
+                // levels of rows [r, r + N) recombined to the exact binary64 products
+                auto read_levels = [&](int r, auto& y) {
+                    constexpr int N = sizeof(y) / sizeof(double);
+                    int32_t lv[kLevels][N];
 #pragma unroll
-                    for (int u = 0; u < kLevels; ++u)  // diagnostic: no TMEM reads
-#pragma unroll
-                        for (int j = 0; j < kChunk; ++j) lv[u][j] = (int)(tbuf + u + j + r);
-#else
-#pragma unroll
-                    for (int u = 0; u < kLevels; ++u) tmem_ld<kChunk>(tbuf + u * TR + r, lv[u]);
+                    for (int u = 0; u < kLevels; ++u) tmem_ld<N>(tbuf + u * TR + r, lv[u]);
                     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+                    for (int j = 0; j < N; ++j) {
+                        long long sum = lv[0][j];
+#pragma unroll
+                        for (int u = 1; u < kLevels; ++u) sum += (long long)lv[u][j] << (8 * u);
+                        y[j] = i64_to_f64_exact(sum);  // exact: |sum| < 2^53
+                    }
+                };
+                // NB == 1: drain every level of this thread's rows, then release TMEM
+                // so the next pair's MMAs start while the K-word updates run
+                double yall[NB == 1 ? kEpiRows : 1];
+                if constexpr (NB == 1) {
+#pragma unroll
+                    for (int r = 0; r < kEpiRows; r += (kEpiRows % 16 == 0 ? 16 : 4)) {
+                        double (&ys)[kEpiRows % 16 == 0 ? 16 : 4] =
+                            *reinterpret_cast<double (*)[kEpiRows % 16 == 0 ? 16 : 4]>(yall + r);
+                        read_levels(r, ys);
+                    }
+#if !(defined(OZK_I8_EPI_MODE) && OZK_I8_EPI_MODE == 3)
+                    asm volatile("tcgen05.fence::before_thread_sync;");
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(tempty0 + 8 * buf);
 #endif
+                }
+                auto update_chunk = [&](int r, W (&w)[kChunk][K]) {
+                    double yc[kChunk];
+                    if constexpr (NB == 1) {
+                        // this chunk's products are yall[0..kChunk); shift the rest
+                        // down so every register index stays static
+#pragma unroll
+                        for (int j = 0; j < kChunk; ++j) yc[j] = yall[j];
+#pragma unroll
+                        for (int j = 0; j < kEpiRows - kChunk; ++j) yall[j] = yall[j + kChunk];
+                    } else {
+                        read_levels(r, yc);
+                    }
 #pragma unroll
                     for (int j = 0; j < kChunk; ++j) {
-                        long long s = lv[0][j];
-#pragma unroll
-                        for (int u = 1; u < kLevels; ++u) s += (long long)lv[u][j] << (8 * u);
-                        const double y = i64_to_f64_exact(s);  // exact: |s| < 2^53
+                        const double y = yc[j];
                         const int ga = __ldg(gap + row_of(r + j));
                         // exact scaled slice product (a TS product is exact in binary32)
 #if defined(OZK_I8_EPI_MODE) && OZK_I8_EPI_MODE == 2
@@ -651,10 +703,16 @@ pair_gemm_i8_kernel(const __grid_constant__ MapsI8 maps, const __grid_constant__
                     if (r + 2 * kChunk < kEpiRows) load_chunk(r + 2 * kChunk, ca);
                     update_chunk(r + kChunk, cb);
                 }
-                // all levels read: hand the buffer back to the MMA issuer
-                asm volatile("tcgen05.fence::before_thread_sync;");
-                __syncwarp();
-                if (lane == 0) mbar_arrive(tempty0 + 8 * buf);
+#if defined(OZK_I8_EPI_MODE) && OZK_I8_EPI_MODE == 3
+                if (true) {  // diagnostic: the next pair's MMAs wait for the whole epilogue
+#else
+                if constexpr (NB == 2) {
+#endif
+                    // all levels read: hand the buffer back to the MMA issuer
+                    asm volatile("tcgen05.fence::before_thread_sync;");
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(tempty0 + 8 * buf);
+                }
                 trace_stamp(step, 5, tracer);
                 trace_stamp(step, 6, tracer);
             }
@@ -684,10 +742,10 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode_i8() {
     return fn;
 }
 
-template <int K, typename W, int ND, int TR, int EG = 2, int CM = 1, int CN = 1>
+template <int K, typename W, int ND, int TR, int EG = 2, int CM = 1, int CN = 1, int NB = 2>
 cudaError_t launch_i8_typed(const I8Operands& op, const PairList& pairs, cudaStream_t st,
                             int num_sms) {
-    using Cfg = I8Cfg<K, W, ND, TR, EG>;
+    using Cfg = I8Cfg<K, W, ND, TR, EG, NB>;
     auto encode = get_encode_i8();
     if (!encode) return cudaErrorNotSupported;
     MapsI8 maps;
@@ -729,9 +787,9 @@ cudaError_t launch_i8_typed(const I8Operands& op, const PairList& pairs, cudaStr
     const int tiles_m = (int)((op.m + TR - 1) / TR), tiles_n = (int)((op.n + TC - 1) / TC);
     const int num_tiles = tiles_m * tiles_n;
     if (num_tiles == 0 || pairs.count == 0) return cudaSuccess;
-    auto kern = pair_gemm_i8_kernel<K, W, ND, TR, EG, false, CM, CN>;
+    auto kern = pair_gemm_i8_kernel<K, W, ND, TR, EG, false, CM, CN, NB>;
     if constexpr (sizeof(W) == 8)
-        if (vec) kern = pair_gemm_i8_kernel<K, W, ND, TR, EG, true, CM, CN>;
+        if (vec) kern = pair_gemm_i8_kernel<K, W, ND, TR, EG, true, CM, CN, NB>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          Cfg::kSmemBytes);
     if (e != cudaSuccess) return e;
@@ -788,9 +846,9 @@ cudaError_t launch_pair_gemm_i8(int K, int word_bytes, const I8Operands& op,
     }
     if (op.nd != 3) return cudaErrorInvalidValue;
     switch (K) {
-    case 2: return launch_i8_typed<2, double, 3, 48, OZK_I8_EG, OZK_I8_CM, OZK_I8_CN>(op, pairs, st, num_sms);
-    case 3: return launch_i8_typed<3, double, 3, 48, OZK_I8_EG, OZK_I8_CM, OZK_I8_CN>(op, pairs, st, num_sms);
-    case 4: return launch_i8_typed<4, double, 3, 48, OZK_I8_EG, OZK_I8_CM, OZK_I8_CN>(op, pairs, st, num_sms);
+    case 2: return launch_i8_typed<2, double, 3, OZK_I8_TR, OZK_I8_EG, OZK_I8_CM, OZK_I8_CN, OZK_I8_NB>(op, pairs, st, num_sms);
+    case 3: return launch_i8_typed<3, double, 3, OZK_I8_TR, OZK_I8_EG, OZK_I8_CM, OZK_I8_CN, OZK_I8_NB>(op, pairs, st, num_sms);
+    case 4: return launch_i8_typed<4, double, 3, OZK_I8_TR, OZK_I8_EG, OZK_I8_CM, OZK_I8_CN, OZK_I8_NB>(op, pairs, st, num_sms);
     default: return cudaErrorInvalidValue;
     }
 }

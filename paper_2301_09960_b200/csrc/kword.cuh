@@ -139,14 +139,23 @@ template <> struct Bits<float> {
     static constexpr U kSafe = (uint32_t)(127 + 120) << 23;     // |x| < 2^120
 };
 
+// 32-bit halves: the high word carries sign + exponent (+ top significand)
+OZK_HD uint32_t hi_word(double x) { return (uint32_t)(fbits(x) >> 32); }
+OZK_HD uint32_t lo_word(double x) { return (uint32_t)fbits(x); }
+OZK_HD uint32_t hi_word(float x) { return fbits(x); }
+OZK_HD uint32_t lo_word(float) { return 0u; }
+
+// The kInt predicates work on the 32-bit halves: a 64-bit sign mask is
+// recognised by the compiler as |x| and issued as an FP64 DADD, which is
+// exactly the pipe (shared with the tensor cores on sm_100) these avoid.
 template <bool kInt, typename T>
 OZK_HD bool is_zero(T x) {
-    if constexpr (kInt) return (fbits(x) & Bits<T>::kAbs) == 0;
+    if constexpr (kInt) return ((hi_word(x) & 0x7fffffffu) | lo_word(x)) == 0u;
     else return x == T(0);
 }
 template <bool kInt, typename T>
 OZK_HD bool same(T a, T b) {  // a == b in the kInt domain described above
-    if constexpr (kInt) return fbits(a) == fbits(b);
+    if constexpr (kInt) return hi_word(a) == hi_word(b) && lo_word(a) == lo_word(b);
     else return a == b;
 }
 template <typename T>
@@ -173,8 +182,13 @@ OZK_HD void fast_two_sum(T a, T b, T& s, T& e) {
 template <bool kInt = false, typename T>
 OZK_HD bool merge_before(T x, T y) {
     if constexpr (kInt) {
-        const auto ax = fbits(x) & Bits<T>::kAbs, ay = fbits(y) & Bits<T>::kAbs;
-        if (ax != ay) return ax > ay;
+        // |x| vs |y| on the magnitude bits (monotone for non-NaN values),
+        // lexicographic over (high word without sign, low word)
+        const uint32_t hx = hi_word(x) & 0x7fffffffu, hy = hi_word(y) & 0x7fffffffu;
+        const uint32_t lx = lo_word(x), ly = lo_word(y);
+        if (hx != hy || lx != ly) return hx > hy || (hx == hy && lx > ly);
+        // equal magnitudes: raw-bit order puts +x before -x
+        return hi_word(x) <= hi_word(y);
     } else {
         T ax = fabs_(x), ay = fabs_(y);
         if (ax != ay) return ax > ay;
@@ -250,10 +264,59 @@ OZK_HD void extract_components(const T* t, T* out) {
     for (int q = 0; q < K; ++q) out[q] = (j == q) ? acc : out[q];
 }
 
+// extract_components<K, K+1> when t[1] is the exact rounding error of
+// t[0] = fl(a + b) (vec_sum's last two_sum): the first step two_sum(t[0], t[1])
+// then returns hi = t[0] (t[0] + t[1] = a + b exactly, and fl(a + b) = t[0]),
+// lo = t[1] (two_sum is error-free without overflow), so it reduces to a zero
+// test.  The one signed-zero exception, t[0] = -0 with t[1] = +0 (hi would be
+// +0), needs every term to be -0; callers exclude it (kw_add_fast's guard).
+template <int K, bool kInt, typename T>
+OZK_HD void extract_after_vec_sum(const T* t, T* out) {
+#pragma unroll
+    for (int q = 0; q < K; ++q) out[q] = T(0);
+    const bool emit = !is_zero<kInt>(t[1]);
+    out[0] = emit ? t[0] : T(0);
+    T acc = emit ? t[1] : t[0];
+    int j = emit ? 1 : 0;
+#pragma unroll
+    for (int i = 2; i <= K; ++i) {
+        // j <= i - 1 < K: the reference's `if (j < K)` always holds here
+        T hi, lo;
+        two_sum(acc, t[i], hi, lo);
+        if (is_zero<kInt>(lo)) {
+            acc = hi;
+        } else {
+#pragma unroll
+            for (int q = 0; q < K; ++q) out[q] = (j == q) ? hi : out[q];
+            ++j;
+            acc = lo;
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < K; ++q) out[q] = (j == q) ? acc : out[q];
+}
+
+// Guard of the K >= 3 fast path: every word finite with |w| < 2^1000 (2^120
+// for binary32) -- so sum_ordered's finiteness probe cannot fail and no sweep
+// can overflow -- and not all words zero.  Integer operations only.
+
+template <int K, typename T>
+OZK_HD bool kw_fast_ok(const T* x, T y) {
+    constexpr uint32_t kSafeHi = (uint32_t)(Bits<T>::kSafe >> (sizeof(T) == 8 ? 32 : 0));
+    uint32_t mx = hi_word(y) & 0x7fffffffu, any = mx | lo_word(y);
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+        const uint32_t a = hi_word(x[i]) & 0x7fffffffu;
+        mx = a > mx ? a : mx;
+        any |= a | lo_word(x[i]);
+    }
+    return mx < kSafeHi && any != 0;
+}
+
 // MultiFloat<K> + word (multifloat.hpp:290-300); x is updated in place.  T is
 // the word type: double for DD/TD/QD, float for TS (which uses the generic
 // K >= 3 branch with binary32 words, see oracle/ozk_oracle.c).
-template <int K, bool kInt, typename T>
+template <int K, bool kInt, typename T, bool kFast = false>
 OZK_HD void kw_add_impl(T* x, T y) {
     if constexpr (K == 2) {
         T s, e;
@@ -284,13 +347,16 @@ OZK_HD void kw_add_impl(T* x, T y) {
             m[i] = placed ? prev : (take_x ? cur : y);
             placed = placed || !take_x;
         }
-        // sum_ordered: finiteness probe over all terms
-        T probe = T(0);
+        // sum_ordered: finiteness probe over all terms (cannot fail under the
+        // kw_fast_ok guard: |probe| < (K + 1) * 2^1000)
+        if constexpr (!kFast) {
+            T probe = T(0);
 #pragma unroll
-        for (int i = 0; i <= K; ++i) probe = rn_add(probe, m[i]);
-        if (!is_finite(probe)) {
-            non_finite<K>(probe, x);
-            return;
+            for (int i = 0; i <= K; ++i) probe = rn_add(probe, m[i]);
+            if (!is_finite(probe)) {
+                non_finite<K>(probe, x);
+                return;
+            }
         }
         // vec_sum over all K+1 terms (zeros transparent, see header)
         T s = m[K];
@@ -303,7 +369,10 @@ OZK_HD void kw_add_impl(T* x, T y) {
         }
         m[0] = s;
         // from_expansion
-        extract_components<K, K + 1, kInt>(m, x);
+        if constexpr (kFast)
+            extract_after_vec_sum<K, kInt>(m, x);
+        else
+            extract_components<K, K + 1, kInt>(m, x);
         strict_normalize<K, kInt>(x);
         if (is_zero<kInt>(x[0]) || !is_finite(x[0])) non_finite<K>(rn_add(x[0], T(0)), x);
     }
@@ -312,6 +381,31 @@ OZK_HD void kw_add_impl(T* x, T y) {
 #if defined(__CUDA_ARCH__)
 template <int K, typename T>
 __device__ __noinline__ void kw_add_slow(T* x, T y) {
+    kw_add_impl<K, false>(x, y);
+}
+// the complete reference sequence, out of line on the device (rarely taken);
+// words passed by value so the caller's registers never go through memory
+template <int K, typename T>
+struct KWords {
+    T w[K];
+};
+template <int K, typename T>
+__device__ __noinline__ KWords<K, T> kw_add_full_v(KWords<K, T> v, T y) {
+    kw_add_impl<K, false>(v.w, y);
+    return v;
+}
+template <int K, typename T>
+__device__ __forceinline__ void kw_add_full(T* x, T y) {
+    KWords<K, T> v;
+#pragma unroll
+    for (int i = 0; i < K; ++i) v.w[i] = x[i];
+    v = kw_add_full_v<K, T>(v, y);
+#pragma unroll
+    for (int i = 0; i < K; ++i) x[i] = v.w[i];
+}
+#else
+template <int K, typename T>
+inline void kw_add_full(T* x, T y) {
     kw_add_impl<K, false>(x, y);
 }
 #endif
@@ -323,8 +417,23 @@ __device__ __noinline__ void kw_add_slow(T* x, T y) {
 #define OZK_KW_INTCMP 0
 #endif
 
+#ifndef OZK_KW_FAST
+#define OZK_KW_FAST 1
+#endif
+
 template <int K, typename T = double>
 OZK_HD void kw_add(T* x, T y) {
+#if OZK_KW_FAST
+    if constexpr (K >= 3) {
+        // the reference sequence minus two steps that are provably no-ops on
+        // guarded inputs (kw_fast_ok); anything else takes the full sequence
+        if (kw_fast_ok<K>(x, y))
+            kw_add_impl<K, true, T, true>(x, y);
+        else
+            kw_add_full<K>(x, y);
+        return;
+    }
+#endif
 #if defined(__CUDA_ARCH__) && OZK_KW_INTCMP
     // integer comparisons whenever they are provably identical (see Bits<>);
     // anything near the overflow threshold or non-finite takes the reference
