@@ -335,12 +335,22 @@ def run_ours(args):
     rows_local = n if world == 1 else eng.rows_local
     fp64_work = P * 2.0 * rows_local * n * n
     nd = int8_digits(args.format, n)
+    traffic = None
+    tfile = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles",
+                         "r01_i8_td8192_traffic.json")
+    if (engine_used == "int8" and world == 1 and args.format == "td" and n == 8192 and d == 9
+            and args.spread == 0 and os.path.exists(tfile)):
+        # dram__bytes_read.sum + dram__bytes_write.sum of this kernel on this
+        # workload from the committed ncu --set full capture (per launch)
+        tj = json.load(open(tfile))
+        traffic = {"bytes_per_launch": tj["dram_bytes_read"] + tj["dram_bytes_write"],
+                   "source": tj["source"]}
     if engine_used == "int8":
         kern_work = nd * nd * fp64_work  # nd^2 int8 digit GEMMs per slice pair
         roof = {"bound": "tensor", "kernel": "pair_gemm_i8_kernel (tcgen05.mma kind::i8 + K-word "
                 "epilogue)", "achieved": round(kern_work / t_kern / 1e12, 2),
                 "peak": round(peak_i8, 2), "unit": "TFLOP/s",
-                "frac": round(kern_work / t_kern / 1e12 / peak_i8, 4), "traffic": None,
+                "frac": round(kern_work / t_kern / 1e12 / peak_i8, 4), "traffic": traffic,
                 "work_per_launch": f"{nd*nd}*P*2*m*n*l = {kern_work:.4g} int8 tensor ops "
                                    "(counted like flops: 2 per multiply-add)",
                 "peak_source": "dense INT8 tcgen05 ceiling measured in this run "
