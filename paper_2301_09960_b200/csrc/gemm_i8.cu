@@ -63,6 +63,12 @@ constexpr int kGroupM = OZK_I8_GROUPM;  // tile rows per rasterization group
 #ifndef OZK_I8_NB
 #define OZK_I8_NB 1
 #endif
+#ifndef OZK_I8_TS_EG
+#define OZK_I8_TS_EG 4
+#endif
+#ifndef OZK_I8_TS_TR
+#define OZK_I8_TS_TR 128
+#endif
 #ifndef OZK_I8_PACE
 #define OZK_I8_PACE 1
 #endif
@@ -840,8 +846,10 @@ cudaError_t launch_pair_gemm_i8(int K, int word_bytes, const I8Operands& op,
                                 const PairList& pairs, cudaStream_t st, int num_sms) {
     if (word_bytes == 4) {  // TS: binary32 words, 1 or 2 digits
         if (K != 3) return cudaErrorInvalidValue;
-        if (op.nd == 1) return launch_i8_typed<3, float, 1, 128>(op, pairs, st, num_sms);
-        if (op.nd == 2) return launch_i8_typed<3, float, 2, 64>(op, pairs, st, num_sms);
+        if (op.nd == 1)
+            return launch_i8_typed<3, float, 1, OZK_I8_TS_TR, OZK_I8_TS_EG, OZK_I8_CM, OZK_I8_CN>(op, pairs, st, num_sms);
+        if (op.nd == 2)
+            return launch_i8_typed<3, float, 2, 64, OZK_I8_TS_EG, OZK_I8_CM, OZK_I8_CN>(op, pairs, st, num_sms);
         return cudaErrorInvalidValue;
     }
     if (op.nd != 3) return cudaErrorInvalidValue;

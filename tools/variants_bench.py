@@ -10,9 +10,16 @@ from paper_2301_09960_b200._lib import OzkProfile, load  # noqa: E402
 
 n = 8192
 sh = torch.cuda.current_stream().cuda_stream
-libs = [(p, load(p)) for p in sys.argv[1:]]
-for fmt, d in ((2, 6), (3, 9), (4, 12)):
-    A = torch.empty((n, n, fmt), dtype=torch.float64, device="cuda")
+args = sys.argv[1:]
+fmts = ((2, 6), (3, 9), (4, 12))
+if args and args[0].startswith("--fmts="):  # e.g. --fmts=3:9,259:15 (259 = TS)
+    fmts = tuple(tuple(int(x) for x in f.split(":")) for f in args[0][7:].split(","))
+    args = args[1:]
+libs = [(p, load(p)) for p in args]
+for fmt, d in fmts:
+    K = 3 if fmt == 0x103 else fmt
+    dt = torch.float32 if fmt == 0x103 else torch.float64
+    A = torch.empty((n, n, K), dtype=dt, device="cuda")
     B = torch.empty_like(A)
     C = torch.empty_like(A)
     libs[0][1].ozk_gen_eq1_device(fmt, n, n, 1, A.data_ptr(), sh)
@@ -31,7 +38,7 @@ for fmt, d in ((2, 6), (3, 9), (4, 12)):
         if ref is None:
             ref = C.clone()
         else:
-            same = " (bit-identical)" if torch.equal(ref.view(torch.int64), C.view(torch.int64)) \
+            same = " (bit-identical)" if torch.equal(ref.view(torch.int32), C.view(torch.int32)) \
                 else " DIFFERS"
         print(f"K={fmt} {path.split('/')[-1]}: slice GEMM {statistics.median(ts)*1e3:.1f} ms{same}",
               flush=True)
