@@ -62,6 +62,9 @@ def parse():
                    help="rows/cols of the CPU baseline sub-GEMM (inner dim stays n)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--csv", default=None,
+                   help="also append the headline run as a CSV v1 record (the reference's "
+                        "bench table format, bench.cpp:21-22,246-259; `threads` = GPUs)")
     return p.parse_args()
 
 
@@ -414,6 +417,17 @@ def run_ours(args):
             "variants": variants,
         }
         print(json.dumps(line), flush=True)
+        if args.csv:
+            from paper_2301_09960_b200.bench_csv import HEADER, BenchRecord, csv_line
+            rec = BenchRecord(algo="ozaki", precision=args.format, n=n, split_count=d,
+                              threads=world, seed=1, reps=args.steps,
+                              t_split=statistics.mean(split), t_product=t_kern, t_accum=0.0,
+                              t_total=t_step)
+            new_file = not os.path.exists(args.csv)
+            with open(args.csv, "a") as f:
+                if new_file:
+                    f.write(HEADER + "\n")
+                f.write(csv_line(rec) + "\n")
     lib.ozk_set_engine(0)
     if world > 1:
         torch.distributed.destroy_process_group()

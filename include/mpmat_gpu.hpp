@@ -29,6 +29,7 @@ inline void throw_on(ozk_status s) {
     std::string msg = ozk_last_error();
     if (s == OZK_ESHAPE) throw shape_error(msg);
     if (s == OZK_EPARAM) throw param_error(msg);
+    if (s == OZK_EIO) throw io_error(msg);
     throw error(msg);
 }
 

@@ -46,7 +46,8 @@ typedef enum {
     OZK_EPARAM = 2, /* mpmat::param_error  (errors.hpp:15-17) */
     OZK_ECUDA = 3,  /* CUDA runtime / launch failure */
     OZK_ENCCL = 4,  /* collective failure (multi-GPU entry points) */
-    OZK_ENOMEM = 5  /* device allocation failure */
+    OZK_ENOMEM = 5, /* device allocation failure */
+    OZK_EIO = 6     /* mpmat::io_error     (errors.hpp:23-25), MPMAT file I/O */
 } ozk_status;
 
 /* Element format.  DD/TD/QD: K = 2/3/4 binary64 words, = the reference's
@@ -183,6 +184,21 @@ ozk_status ozk_digits_gemm_device(ozk_format fmt, size_t m, size_t l, size_t n,
                                   const int8_t* b_digits, const int* b_exps, size_t b_plane_rows,
                                   size_t ld8, int split_count, const int* pairs, int npairs,
                                   void* c, size_t ldc, void* stream);
+
+/* ---- MPMAT v1 matrix files (proj/src/matrix_io.cpp) ---------- *
+ * Text: header "MPMAT v1 <tag> <m> <n>", then one matrix row per line, each
+ * element as its K words in C99 hex ("%a", space separated).  Tags d, dd, td,
+ * qd (fmt OZK_D = 1, OZK_DD, OZK_TD, OZK_QD) as in the reference, plus "ts"
+ * (OZK_TS, 3 binary32 words; this build's extension, each word written as the
+ * equal binary64 literal and read back exactly).  Round trips are bit-exact and
+ * the written bytes equal the reference writer's.  a: m x n elements of K words
+ * (float words for TS), row-major.  Errors: OZK_EIO with the reference's
+ * io_error messages (unopenable file, bad header, not MPMAT v1, tag mismatch,
+ * zero dimension, truncated row, malformed element). */
+#define OZK_D 1
+ozk_status ozk_mpmat_write(const char* path, int fmt, size_t m, size_t n, const void* a);
+ozk_status ozk_mpmat_read_header(const char* path, int* fmt, size_t* m, size_t* n);
+ozk_status ozk_mpmat_read(const char* path, int fmt, size_t m, size_t n, void* a);
 
 /* Parity hook: every slice product C_ab = A_alpha * B_beta of the pair list,
  * binary64, into products[p] (m x n row-major). */

@@ -290,7 +290,21 @@ class Ref(CpuOzaki):
         lib.ref_lu_update.argtypes = [ctypes.c_int, _c_size, _c_size, _c_size, _dp, _dp, _dp,
                                       ctypes.c_int]
         lib.ref_exponent_ceil_log2.argtypes = [ctypes.c_double]
+        lib.ref_mpmat_write.argtypes = [ctypes.c_char_p, ctypes.c_int, _c_size, _c_size, _dp]
+        lib.ref_mpmat_read.argtypes = [ctypes.c_char_p, ctypes.c_int, _c_size, _c_size, _dp]
         self.lib = lib
+
+    def mpmat_write(self, path, a):
+        """The reference's write_matrix_file (src/matrix_io.cpp); a is (m, n)
+        binary64 ("d") or (m, n, K).  Returns the status (4 = io_error)."""
+        a = np.ascontiguousarray(a, dtype=np.float64)
+        K = 1 if a.ndim == 2 else a.shape[2]
+        return self.lib.ref_mpmat_write(os.fsencode(path), K, a.shape[0], a.shape[1], _ptr(a))
+
+    def mpmat_read(self, path, K, m, n):
+        """The reference's read_matrix_file<E>: (status, array)."""
+        out = np.empty((m, n) if K == 1 else (m, n, K), dtype=np.float64)
+        return self.lib.ref_mpmat_read(os.fsencode(path), K, m, n, _ptr(out)), out
 
     def set_threads(self, t: int) -> int:
         return self.lib.ref_set_threads(t)

@@ -11,6 +11,7 @@
 #include "mpmat/dense_matrix.hpp"
 #include "mpmat/gemm.hpp"
 #include "mpmat/gen.hpp"
+#include "mpmat/matrix_io.hpp"
 #include "mpmat/ozaki.hpp"
 
 #include <array>
@@ -143,6 +144,15 @@ int lu_update_k(std::size_t tm, std::size_t pw, std::size_t tn, const double* l2
     default: return 2;                                                                 \
     }
 
+template <int K>
+int mpmat_read_k(const char* path, std::size_t m, std::size_t n, double* out) {
+    auto a = read_matrix_file<MultiFloat<K>>(path);
+    if (a.rows() != m || a.cols() != n) return 1;
+    for (std::size_t i = 0; i < m * n; ++i)
+        for (int k = 0; k < K; ++k) out[i * K + k] = a.data()[i].component(k);
+    return 0;
+}
+
 } // namespace
 
 extern "C" {
@@ -235,6 +245,48 @@ int ref_lu_update(int K, std::size_t tm, std::size_t pw, std::size_t tn, const d
                   const double* u12, double* a22, int d) {
     try {
         DISPATCH_K(K, lu_update_k, tm, pw, tn, l21, u12, a22, d);
+    } catch (const std::exception& e) {
+        return status_of(e);
+    }
+}
+
+// MPMAT v1 files through the reference's own reader/writer (src/matrix_io.cpp).
+// K = 1: DenseMatrix<double> (tag d).  Returns 0, or 4 for mpmat::io_error.
+int ref_mpmat_write(const char* path, int K, std::size_t m, std::size_t n, const double* a) {
+    try {
+        if (K == 1) {
+            write_matrix_file(path, load_d(m, n, a));
+            return 0;
+        }
+        switch (K) {
+        case 2: write_matrix_file(path, load<2>(m, n, a)); return 0;
+        case 3: write_matrix_file(path, load<3>(m, n, a)); return 0;
+        case 4: write_matrix_file(path, load<4>(m, n, a)); return 0;
+        default: return 2;
+        }
+    } catch (const io_error&) {
+        return 4;
+    } catch (const std::exception& e) {
+        return status_of(e);
+    }
+}
+
+int ref_mpmat_read(const char* path, int K, std::size_t m, std::size_t n, double* out) {
+    try {
+        if (K == 1) {
+            auto a = read_matrix_file<double>(path);
+            if (a.rows() != m || a.cols() != n) return 1;
+            std::memcpy(out, a.data(), m * n * sizeof(double));
+            return 0;
+        }
+        switch (K) {
+        case 2: return mpmat_read_k<2>(path, m, n, out);
+        case 3: return mpmat_read_k<3>(path, m, n, out);
+        case 4: return mpmat_read_k<4>(path, m, n, out);
+        default: return 2;
+        }
+    } catch (const io_error&) {
+        return 4;
     } catch (const std::exception& e) {
         return status_of(e);
     }

@@ -14,6 +14,8 @@ from .mpmat import (  # noqa: F401
     exponent_ceil_log2,
     get_engine,
     gpu_backend,
+    io_error,
+    read_matrix_file,
     lu_trailing_update,
     ozaki_gemm,
     param_error,
@@ -22,10 +24,12 @@ from .mpmat import (  # noqa: F401
     split_matrix,
     split_shift_bits,
     ts_direct_gemm,
+    write_matrix_file,
 )
 
 __all__ = [
     "OzakiProfile", "SplitSet", "SplitSide", "error", "exponent_ceil_log2", "gpu_backend",
     "ozaki_gemm", "param_error", "shape_error", "split_matrix", "split_shift_bits", "lib",
-    "ts_direct_gemm", "lu_trailing_update", "set_engine", "get_engine",
+    "ts_direct_gemm", "lu_trailing_update", "set_engine", "get_engine", "io_error",
+    "read_matrix_file", "write_matrix_file",
 ]

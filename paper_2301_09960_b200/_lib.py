@@ -12,7 +12,7 @@ import os
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "lib", "libozk.so")
 
-OZK_OK, OZK_ESHAPE, OZK_EPARAM, OZK_ECUDA, OZK_ENCCL, OZK_ENOMEM = range(6)
+OZK_OK, OZK_ESHAPE, OZK_EPARAM, OZK_ECUDA, OZK_ENCCL, OZK_ENOMEM, OZK_EIO = range(7)
 
 _sz = ctypes.c_size_t
 _dp = ctypes.c_void_p  # device or host double*, passed as raw addresses
@@ -60,6 +60,10 @@ SIGNATURES = {
     "ozk_digits_gemm_device": (ctypes.c_int, [ctypes.c_int, _sz, _sz, _sz, _dp, _dp, _sz, _dp,
                                               _dp, _sz, _sz, ctypes.c_int, _ip, ctypes.c_int,
                                               _dp, _sz, ctypes.c_void_p]),
+    "ozk_mpmat_write": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_int, _sz, _sz, _dp]),
+    "ozk_mpmat_read_header": (ctypes.c_int, [ctypes.c_char_p, _ip, ctypes.POINTER(_sz),
+                                             ctypes.POINTER(_sz)]),
+    "ozk_mpmat_read": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_int, _sz, _sz, _dp]),
     "ozk_pair_products_device": (ctypes.c_int, [_sz, _sz, _sz, _dp, _dp, ctypes.c_int, _ip,
                                                 ctypes.c_int, _dp, ctypes.c_void_p]),
     "ozk_gen_eq1_device": (ctypes.c_int, [ctypes.c_int, _sz, _sz, ctypes.c_uint64, _dp,

@@ -360,6 +360,11 @@ ozk_status check_gemm_args(int fmt, size_t m, size_t l, size_t n, int d, double 
 
 }  // namespace
 
+namespace ozk {
+// thread-local error text for the other host translation units (io.cu)
+void set_last_error(const std::string& msg) { g_last_error = msg; }
+}  // namespace ozk
+
 extern "C" {
 
 const char* ozk_last_error(void) { return g_last_error.c_str(); }

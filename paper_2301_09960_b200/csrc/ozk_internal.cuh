@@ -1,6 +1,8 @@
 // ozk_internal.cuh -- launchers shared between the kernel TUs and the C-ABI TU.
 #pragma once
 
+#include <string>
+
 #include <cuda_runtime.h>
 #include <stddef.h>
 #include <stdint.h>
@@ -110,5 +112,7 @@ cudaError_t launch_ts_direct(const float* a, const float* b, float* c, size_t m,
 // spread > 0 scales every element by 2^U[-spread, spread] (config 5 inputs).
 cudaError_t launch_gen_eq1(int K, int word_bytes, void* out, size_t count, uint64_t seed,
                            int spread, cudaStream_t st);
+
+void set_last_error(const std::string& msg);  // api.cu (ozk_last_error)
 
 } // namespace ozk

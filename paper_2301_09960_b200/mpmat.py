@@ -26,12 +26,14 @@ through the device entry points on torch's current stream.
 from __future__ import annotations
 
 import ctypes
+import os
 import enum
 from dataclasses import dataclass, field
 
 import numpy as np
 
-from ._lib import OZK_ECUDA, OZK_ENCCL, OZK_ENOMEM, OZK_EPARAM, OZK_ESHAPE, OzkProfile, lib
+from ._lib import (OZK_ECUDA, OZK_EIO, OZK_ENCCL, OZK_ENOMEM, OZK_EPARAM, OZK_ESHAPE, OzkProfile,
+                   lib)
 
 try:  # torch is optional for the host path
     import torch
@@ -51,6 +53,10 @@ class param_error(error):
     """mpmat::param_error (errors.hpp:15-17)."""
 
 
+class io_error(error):
+    """mpmat::io_error (errors.hpp:23-25): MPMAT file I/O."""
+
+
 class cuda_error(error):
     """Device failure (no reference counterpart: the reference is CPU-only)."""
 
@@ -65,6 +71,8 @@ def _raise(status: int) -> None:
         raise param_error(msg)
     if status == OZK_ENOMEM:
         raise MemoryError(msg)
+    if status == OZK_EIO:
+        raise io_error(msg)
     if status in (OZK_ECUDA, OZK_ENCCL):
         raise cuda_error(msg)
     raise error(msg)
@@ -304,3 +312,44 @@ def lu_trailing_update(a22, l21, u12, d: int = 6):
     a, lda = strided(a22)
     _raise(lib.ozk_lu_trailing_update(fa, tm, pw, tn, l.ctypes.data, ldl, u.ctypes.data, ldu,
                                       a.ctypes.data, lda, int(d)))
+
+
+# ---- MPMAT v1 matrix files (proj/src/matrix_io.cpp; csrc/io.cu) ------------
+
+OZK_D = 1  # plain binary64 matrix, tag "d"
+_TAGS = {OZK_D: "d", 2: "dd", 3: "td", 4: "qd", OZK_TS: "ts"}
+
+
+def write_matrix_file(path: str, a) -> None:
+    """write_matrix_file (matrix_io.hpp:43-46): a is (m, n) binary64 ("d"),
+    (m, n, K) binary64 K-word (dd/td/qd) or (m, n, 3) binary32 (ts)."""
+    x = a.detach().cpu().numpy() if torch is not None and isinstance(a, torch.Tensor) else a
+    x = np.asarray(x)
+    if x.ndim == 2:
+        fmt, m, n = OZK_D, int(x.shape[0]), int(x.shape[1])
+        x = np.ascontiguousarray(x, dtype=np.float64)
+    else:
+        m, n, fmt = _kword_shape(x)
+        x = _host(x, fmt)
+    _raise(lib.ozk_mpmat_write(os.fsencode(path), fmt, m, n, x.ctypes.data))
+
+
+def read_matrix_file(path: str, tag: str | None = None) -> np.ndarray:
+    """read_matrix_file<E> (matrix_io.hpp:51-52).  tag (d/dd/td/qd/ts) plays the
+    role of the element type E: a file with another tag raises io_error, as
+    in the reference.  Without it the file's own tag is used."""
+    fmt = ctypes.c_int(0)
+    m, n = ctypes.c_size_t(0), ctypes.c_size_t(0)
+    _raise(lib.ozk_mpmat_read_header(os.fsencode(path), ctypes.byref(fmt), ctypes.byref(m),
+                                     ctypes.byref(n)))
+    want = fmt.value
+    if tag is not None:
+        inv = {v: k for k, v in _TAGS.items()}
+        if tag not in inv:
+            raise param_error(f"unknown precision tag {tag!r}")
+        want = inv[tag]
+    k = 1 if want == OZK_D else _words(want)
+    shape = (m.value, n.value) if want == OZK_D else (m.value, n.value, k)
+    out = np.empty(shape, dtype=np.float32 if want == OZK_TS else np.float64)
+    _raise(lib.ozk_mpmat_read(os.fsencode(path), want, m.value, n.value, out.ctypes.data))
+    return out
