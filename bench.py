@@ -416,6 +416,8 @@ def run_ours(args):
             "cpu_baseline": cpu,
             "variants": variants,
         }
+        if world == 1 and args.format != "ts":
+            line["direct_kword_gemm"] = direct_rate(lib, code, K, sh)
         print(json.dumps(line), flush=True)
         if args.csv:
             from paper_2301_09960_b200.bench_csv import HEADER, BenchRecord, csv_line
@@ -462,6 +464,31 @@ def run_e2e(args, lib, OzkProfile, A, B, code, K, wb, d, n):
             "engine": ENGINE_NAMES.get(prof.engine, "?")}
 
 
+def direct_rate(lib, code, K, sh, nd=1024):
+    """Direct K-word GEMM comparator (gemm_simple<MultiFloat<K>> on the GPU,
+    csrc/direct.cu, bit-identical to the reference's): effective GFLOP/s at nd
+    (its cost is cubic; the rate carries to n = 8192, where one call would take
+    minutes for QD)."""
+    import torch
+    A = torch.empty((nd, nd, K), dtype=torch.float64, device="cuda")
+    B = torch.empty_like(A)
+    C = torch.empty_like(A)
+    lib.ozk_gen_eq1_device(code, nd, nd, 1, A.data_ptr(), sh)
+    lib.ozk_gen_eq1_device(code, nd, nd, 2, B.data_ptr(), sh)
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    if lib.ozk_direct_gemm_device(code, nd, nd, nd, A.data_ptr(), B.data_ptr(), C.data_ptr(),
+                                  sh) != 0:
+        raise RuntimeError(lib.ozk_last_error().decode())
+    e1.record(stream)
+    torch.cuda.synchronize()
+    t = e0.elapsed_time(e1) * 1e-3
+    return {"value": round(2.0 * nd ** 3 / t / 1e9, 3), "unit": "GFLOP/s", "n": nd,
+            "ms": round(1e3 * t, 3),
+            "kernel": "direct_gemm_kernel (gemm_simple<MultiFloat<K>>, csrc/direct.cu)"}
+
+
 def run_variant(lib, OzkProfile, fmt, n, peak_fp64, peak_i8, sh, args):
     import torch
     code, K, d, wb = fmt_info(fmt)
@@ -479,6 +506,8 @@ def run_variant(lib, OzkProfile, fmt, n, peak_fp64, peak_i8, sh, args):
     lib.ozk_set_engine(ENGINE_CODES[args.engine])
     best = min((out[e] for e in engs), key=lambda r: r["ms_per_step"])
     out["value"], out["unit"], out["engine"] = best["value"], "GFLOP/s", best["engine"]
+    if fmt != "ts":
+        out["direct_kword_gemm"] = direct_rate(lib, code, K, sh)
     if fmt == "ts":
         # config 4 comparator: the direct triple-single GEMM kernel on the same inputs
         stream = torch.cuda.current_stream()

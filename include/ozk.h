@@ -221,6 +221,17 @@ ozk_status ozk_lu_trailing_update_device(ozk_format fmt, size_t tm, size_t pw, s
                                          size_t ldu, void* a22, size_t lda, int split_count,
                                          void* stream);
 
+/* ---- direct K-word GEMM -------------------------------------- *
+ * The reference's gemm_simple<MultiFloat<K>> (gemm.hpp:16-33) bit for bit:
+ * per element c = 0; for k ascending: c = c + a(i,k) * b(k,j) with the
+ * reference's K-word multiply (multifloat.hpp:218-239) and add (:271-286).
+ * The comparator the Ozaki scheme is measured against (paper §5); DD/TD/QD,
+ * row-major AoS, a: m x l, b: l x n, c: m x n. */
+ozk_status ozk_direct_gemm(ozk_format fmt, size_t m, size_t l, size_t n, const void* a,
+                           const void* b, void* c);
+ozk_status ozk_direct_gemm_device(ozk_format fmt, size_t m, size_t l, size_t n, const void* a,
+                                  const void* b, void* c, void* stream);
+
 /* ---- direct triple-single GEMM (BASELINE config 4 comparator) ------------- *
  * C = A * B with every term accumulated in triple-single arithmetic, k
  * ascending (no reference counterpart; the operation sequence is defined in

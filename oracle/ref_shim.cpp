@@ -124,6 +124,20 @@ void add_mf_k(std::size_t count, const double* x, const double* y, double* out) 
 }
 
 template <int K>
+void mul_mf_k(std::size_t count, const double* x, const double* y, double* out) {
+    for (std::size_t i = 0; i < count; ++i) {
+        std::array<double, K> a, b;
+        for (int k = 0; k < K; ++k) {
+            a[k] = x[i * K + k];
+            b[k] = y[i * K + k];
+        }
+        auto r = MultiFloat<K>::from_components_unchecked(a) *
+                 MultiFloat<K>::from_components_unchecked(b);
+        for (int k = 0; k < K; ++k) out[i * K + k] = r.component(k);
+    }
+}
+
+template <int K>
 int lu_update_k(std::size_t tm, std::size_t pw, std::size_t tn, const double* l21,
                 const double* u12, double* a22, int d) {
     auto L = load<K>(tm, pw, l21);
@@ -234,6 +248,16 @@ int ref_mf_add_mf(int K, std::size_t count, const double* x, const double* y, do
     case 2: add_mf_k<2>(count, x, y, out); return 0;
     case 3: add_mf_k<3>(count, x, y, out); return 0;
     case 4: add_mf_k<4>(count, x, y, out); return 0;
+    default: return 2;
+    }
+}
+
+// MultiFloat<K> * MultiFloat<K> on `count` pairs (multifloat.hpp:218-239).
+int ref_mf_mul_mf(int K, std::size_t count, const double* x, const double* y, double* out) {
+    switch (K) {
+    case 2: mul_mf_k<2>(count, x, y, out); return 0;
+    case 3: mul_mf_k<3>(count, x, y, out); return 0;
+    case 4: mul_mf_k<4>(count, x, y, out); return 0;
     default: return 2;
     }
 }

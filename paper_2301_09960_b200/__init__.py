@@ -12,6 +12,7 @@ from .mpmat import (  # noqa: F401
     SplitSide,
     error,
     exponent_ceil_log2,
+    gemm_simple,
     get_engine,
     gpu_backend,
     io_error,
@@ -31,5 +32,5 @@ __all__ = [
     "OzakiProfile", "SplitSet", "SplitSide", "error", "exponent_ceil_log2", "gpu_backend",
     "ozaki_gemm", "param_error", "shape_error", "split_matrix", "split_shift_bits", "lib",
     "ts_direct_gemm", "lu_trailing_update", "set_engine", "get_engine", "io_error",
-    "read_matrix_file", "write_matrix_file",
+    "read_matrix_file", "write_matrix_file", "gemm_simple",
 ]

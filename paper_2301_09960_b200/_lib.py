@@ -75,6 +75,9 @@ SIGNATURES = {
     "ozk_lu_trailing_update_device": (ctypes.c_int, [ctypes.c_int, _sz, _sz, _sz, _dp, _sz, _dp,
                                                      _sz, _dp, _sz, ctypes.c_int,
                                                      ctypes.c_void_p]),
+    "ozk_direct_gemm": (ctypes.c_int, [ctypes.c_int, _sz, _sz, _sz, _dp, _dp, _dp]),
+    "ozk_direct_gemm_device": (ctypes.c_int, [ctypes.c_int, _sz, _sz, _sz, _dp, _dp, _dp,
+                                              ctypes.c_void_p]),
     "ozk_ts_direct_gemm": (ctypes.c_int, [_sz, _sz, _sz, _dp, _dp, _dp]),
     "ozk_ts_direct_gemm_device": (ctypes.c_int, [_sz, _sz, _sz, _dp, _dp, _dp, ctypes.c_void_p]),
     "ozk_probe_dmma_tflops": (ctypes.c_double, [ctypes.c_int, ctypes.c_void_p]),

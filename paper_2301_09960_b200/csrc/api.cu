@@ -872,6 +872,40 @@ ozk_status ozk_ts_direct_gemm(size_t m, size_t l, size_t n, const float* a, cons
     return OZK_OK;
 }
 
+ozk_status ozk_direct_gemm_device(ozk_format fmt, size_t m, size_t l, size_t n, const void* a,
+                                  const void* b, void* c, void* stream) {
+    if (fmt != OZK_DD && fmt != OZK_TD && fmt != OZK_QD)
+        return fail(OZK_EPARAM, "direct_gemm: format must be DD, TD or QD (TS: ozk_ts_direct_gemm)");
+    if (m == 0 || l == 0 || n == 0) return fail(OZK_ESHAPE, "matrix dimensions must be positive");
+    if (m > 0xffff0ull * 16 || n > 0xffff0ull * 16) return fail(OZK_ESHAPE, "direct_gemm: dimension too large");
+    cudaStream_t st = (cudaStream_t)stream;
+    OZK_CUDA(launch_direct_gemm(words_of(fmt), static_cast<const double*>(a),
+                                static_cast<const double*>(b), static_cast<double*>(c), m, l, n, st),
+             "direct_gemm");
+    OZK_CUDA(cudaStreamSynchronize(st), "direct_gemm");
+    return OZK_OK;
+}
+
+ozk_status ozk_direct_gemm(ozk_format fmt, size_t m, size_t l, size_t n, const void* a,
+                           const void* b, void* c) {
+    if (fmt != OZK_DD && fmt != OZK_TD && fmt != OZK_QD)
+        return fail(OZK_EPARAM, "direct_gemm: format must be DD, TD or QD (TS: ozk_ts_direct_gemm)");
+    if (m == 0 || l == 0 || n == 0) return fail(OZK_ESHAPE, "matrix dimensions must be positive");
+    const size_t eb = elem_bytes(fmt);
+    OwnStream os;
+    OZK_CUDA(os.create(), "direct_gemm: stream");
+    DevBuf da, db, dc;
+    OZK_CUDA(da.alloc(eb * m * l, os.s), "direct_gemm: A");
+    OZK_CUDA(db.alloc(eb * l * n, os.s), "direct_gemm: B");
+    OZK_CUDA(dc.alloc(eb * m * n, os.s), "direct_gemm: C");
+    OZK_CUDA(cudaMemcpyAsync(da.p, a, eb * m * l, cudaMemcpyHostToDevice, os.s), "direct: H2D");
+    OZK_CUDA(cudaMemcpyAsync(db.p, b, eb * l * n, cudaMemcpyHostToDevice, os.s), "direct: H2D");
+    if (ozk_status s = ozk_direct_gemm_device(fmt, m, l, n, da.p, db.p, dc.p, os.s)) return s;
+    OZK_CUDA(cudaMemcpyAsync(c, dc.p, eb * m * n, cudaMemcpyDeviceToHost, os.s), "direct: D2H");
+    OZK_CUDA(cudaStreamSynchronize(os.s), "direct_gemm");
+    return OZK_OK;
+}
+
 ozk_status ozk_gen_spread_device(ozk_format fmt, size_t rows, size_t cols, uint64_t seed,
                                  int spread, void* out, void* stream) {
     if (!valid_fmt(fmt)) return fail(OZK_EPARAM, "gen: format must be DD, TD, QD or TS");

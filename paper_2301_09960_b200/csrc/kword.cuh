@@ -29,6 +29,9 @@
 #pragma once
 
 #include <stdint.h>
+#if !defined(__CUDACC__)
+#include <cmath>
+#endif
 
 #if defined(__CUDACC__)
 #define OZK_HD __host__ __device__ __forceinline__
@@ -519,6 +522,130 @@ OZK_HD void kw_add_kw(T* x, const T* y) {
         extract_components<K, 2 * K>(m, x);
         strict_normalize<K>(x);
         if (x[0] == T(0) || !is_finite(x[0])) non_finite<K>(rn_add(x[0], T(0)), x);
+    }
+}
+
+// ---- MultiFloat<K> x MultiFloat<K> (multifloat.hpp:218-239), for the direct
+// K-word GEMM (gemm.hpp:16-33, csrc/direct.cu) -------------------------------
+
+// two_prod with a hardware FMA (eft.hpp:60-64; the reference is built with
+// -mfma, so MPMAT_HAVE_HW_FMA selects this variant, eft.hpp:75-85)
+template <typename T>
+OZK_HD void two_prod(T a, T b, T& p, T& e) {
+#if defined(__CUDA_ARCH__)
+    if constexpr (sizeof(T) == 8) {
+        p = __dmul_rn(a, b);
+        e = __fma_rn(a, b, -p);
+    } else {
+        p = __fmul_rn(a, b);
+        e = __fmaf_rn(a, b, -p);
+    }
+#else
+    p = a * b;
+    e = std::fma(a, b, -p);
+#endif
+}
+template <typename T>
+OZK_HD T rn_mul(T a, T b) {
+#if defined(__CUDA_ARCH__)
+    if constexpr (sizeof(T) == 8) return __dmul_rn(a, b);
+    else return __fmul_rn(a, b);
+#else
+    return a * b;
+#endif
+}
+
+// from_pair (multifloat.hpp:384-392) on (s, e)
+template <typename T>
+OZK_HD void from_pair(T s, T e, T* x) {
+    if (!is_finite(s)) {
+        x[0] = s;
+        x[1] = T(0);
+        return;
+    }
+    T ps, pe;
+    fast_two_sum(s, e, ps, pe);
+    x[0] = ps == T(0) ? T(0) : ps;
+    x[1] = (pe == T(0) || ps == T(0)) ? T(0) : pe;
+}
+
+// sum_ordered(t, N) (multifloat.hpp:405-416) -> x.  The zero compaction is
+// skipped: zero terms are transparent to vec_sum and extraction (header note).
+template <int K, int N, typename T>
+OZK_HD void sum_ordered_n(T* t, T* x) {
+    T probe = T(0);
+#pragma unroll
+    for (int i = 0; i < N; ++i) probe = rn_add(probe, t[i]);
+    if (!is_finite(probe)) {
+        non_finite<K>(probe, x);
+        return;
+    }
+    T s = t[N - 1];
+#pragma unroll
+    for (int i = N - 2; i >= 0; --i) {
+        T hi, lo;
+        two_sum(t[i], s, hi, lo);
+        s = hi;
+        t[i + 1] = lo;
+    }
+    t[0] = s;
+    extract_components<K, N>(t, x);
+    strict_normalize<K>(x);
+    if (x[0] == T(0) || !is_finite(x[0])) non_finite<K>(rn_add(x[0], T(0)), x);
+}
+
+// canonical_order (multifloat.hpp:68-81) as a fixed odd-even transposition
+// network: the order "|a| > |b|, ties by increasing bit pattern" is a strict
+// total order on distinct bit patterns, so every correct sort yields the
+// insertion sort's sequence (finite inputs; NaN terms end in a non-finite
+// result either way through the probe).
+template <typename T>
+OZK_HD bool after(T a, T b) {  // a must come after b
+    const T aa = fabs_(a), ab = fabs_(b);
+    if (aa != ab) return aa < ab;
+    return fbits(a) > fbits(b);
+}
+template <int N, typename T>
+OZK_HD void canonical_order_n(T* t) {
+#pragma unroll
+    for (int round = 0; round < N; ++round) {
+#pragma unroll
+        for (int i = round & 1; i + 1 < N; i += 2) {
+            const bool sw = after(t[i], t[i + 1]);
+            const T lo = t[i + 1];
+            t[i + 1] = sw ? t[i] : lo;
+            t[i] = sw ? lo : t[i];
+        }
+    }
+}
+
+template <int K, typename T = double>
+OZK_HD void kw_mul_kw(const T* x, const T* y, T* r) {
+    if constexpr (K == 2) {
+        T cp, ce;
+        two_prod(x[0], y[0], cp, ce);
+        T cs, cerr;
+        two_sum(rn_mul(x[0], y[1]), rn_mul(x[1], y[0]), cs, cerr);
+        const T tail = rn_add(ce, rn_add(cs, rn_add(rn_mul(x[1], y[1]), cerr)));
+        T fs, fe;
+        fast_two_sum(cp, tail, fs, fe);
+        from_pair(fs, fe, r);
+    } else {
+        constexpr int N = K * (K + 1) + K - 1;
+        T t[N];
+        int n = 0;
+#pragma unroll
+        for (int i = 0; i < K; ++i) {
+#pragma unroll
+            for (int j = 0; j + i < K; ++j) {
+                two_prod(x[i], y[j], t[n], t[n + 1]);
+                n += 2;
+            }
+        }
+#pragma unroll
+        for (int i = 1; i < K; ++i) t[n++] = rn_mul(x[i], y[K - i]);
+        canonical_order_n<N>(t);
+        sum_ordered_n<K, N>(t, r);
     }
 }
 

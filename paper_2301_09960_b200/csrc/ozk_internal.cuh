@@ -113,6 +113,10 @@ cudaError_t launch_ts_direct(const float* a, const float* b, float* c, size_t m,
 cudaError_t launch_gen_eq1(int K, int word_bytes, void* out, size_t count, uint64_t seed,
                            int spread, cudaStream_t st);
 
+// Direct K-word GEMM, gemm_simple<MultiFloat<K>> (csrc/direct.cu).
+cudaError_t launch_direct_gemm(int K, const double* a, const double* b, double* c, size_t m,
+                               size_t l, size_t n, cudaStream_t st);
+
 void set_last_error(const std::string& msg);  // api.cu (ozk_last_error)
 
 } // namespace ozk

@@ -289,6 +289,31 @@ def ts_direct_gemm(a, b):
     return c
 
 
+def gemm_simple(a, b):
+    """gemm_simple<MultiFloat<K>> (gemm.hpp:16-33) on the GPU, bit-identical:
+    fixed k-order K-word multiply-accumulate (csrc/direct.cu).  TS inputs go
+    to ts_direct_gemm."""
+    m, l, fa = _kword_shape(a)
+    l2, n, fb = _kword_shape(b)
+    if fa != fb:
+        raise param_error("gemm_simple: A and B must have the same format")
+    if fa == OZK_TS:
+        return ts_direct_gemm(a, b)
+    if l != l2:
+        raise shape_error("gemm_simple: inner dimensions differ")
+    K = _words(fa)
+    if _is_cuda(a) and _is_cuda(b):
+        ad, bd = a.contiguous(), b.contiguous()
+        c = torch.empty((m, n, K), dtype=torch.float64, device=a.device)
+        _raise(lib.ozk_direct_gemm_device(fa, m, l, n, ad.data_ptr(), bd.data_ptr(), c.data_ptr(),
+                                          _stream_handle()))
+        return c
+    ah, bh = _host(a, fa), _host(b, fa)
+    c = np.empty((m, n, K), dtype=np.float64)
+    _raise(lib.ozk_direct_gemm(fa, m, l, n, ah.ctypes.data, bh.ctypes.data, c.ctypes.data))
+    return c
+
+
 def lu_trailing_update(a22, l21, u12, d: int = 6):
     """Blocked-LU trailing update A22 -= L21 * U12 (lu.hpp:104-124) in place on a
     host K-word array (or view with unit element stride); Ozaki product with d

@@ -40,6 +40,30 @@ extern "C" int kw_host_add_kw(int K, std::size_t n, const double* x, const doubl
     }
 }
 
+template <int K>
+static void run_mul(std::size_t n, const double* x, const double* y, double* out) {
+    for (std::size_t i = 0; i < n; ++i) {
+        double w[K], v[K], r[K];
+        for (int k = 0; k < K; ++k) {
+            w[k] = x[i * K + k];
+            v[k] = y[i * K + k];
+        }
+        ozk::kw_mul_kw<K>(w, v, r);
+        for (int k = 0; k < K; ++k) out[i * K + k] = r[k];
+    }
+}
+
+// MultiFloat<K> * MultiFloat<K> on n pairs (the direct GEMM's multiply)
+extern "C" int kw_host_mul_kw(int K, std::size_t n, const double* x, const double* y,
+                              double* out) {
+    switch (K) {
+    case 2: run_mul<2>(n, x, y, out); return 0;
+    case 3: run_mul<3>(n, x, y, out); return 0;
+    case 4: run_mul<4>(n, x, y, out); return 0;
+    default: return 2;
+    }
+}
+
 extern "C" void kw_host_add_ts(std::size_t n, const float* x, const float* y, float* out) {
     for (std::size_t i = 0; i < n; ++i) {
         float w[3] = {x[3 * i], x[3 * i + 1], x[3 * i + 2]};

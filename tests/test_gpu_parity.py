@@ -468,3 +468,31 @@ def test_int8_engine_rejects_inapplicable(ozk, engine):
     a = np.zeros((4, 100, 2))
     with pytest.raises(ozk.param_error):
         ozk.ozaki_gemm(a, np.zeros((100, 4, 2)), 6)  # l <= 512
+
+
+@pytest.mark.parametrize("K,m,l,n", [(2, 33, 47, 29), (3, 20, 33, 18), (4, 16, 40, 24),
+                                     (2, 64, 64, 64), (3, 17, 1, 5), (4, 1, 70, 1)])
+def test_direct_gemm_bitexact(ozk, ref, K, m, l, n):
+    """Direct K-word GEMM = the reference's gemm_simple<MultiFloat<K>>
+    (gemm.hpp:16-33) bit for bit, host and device entry points."""
+    import torch
+    if ref is None:
+        pytest.skip("oracle/_ref not built")
+    a = ref.gen_eq1(K, m, l, 61 + K)
+    b = ref.gen_eq1(K, l, n, 62 + K)
+    want = ref.gemm_simple(K, a, b)
+    got = ozk.gemm_simple(a, b)
+    assert_bitwise(got, want, f"direct K={K} {m}x{l}x{n} (host API)")
+    gd = ozk.gemm_simple(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda())
+    assert_bitwise(gd.cpu().numpy(), want, f"direct K={K} {m}x{l}x{n} (device API)")
+
+
+def test_direct_gemm_spread_inputs(ozk, ref, port):
+    """Wide exponent range and exact cancellations inside the k loop."""
+    if ref is None:
+        pytest.skip("oracle/_ref not built")
+    a = port.gen_spread(3, 24, 30, 5, 200)
+    b = port.gen_spread(3, 30, 20, 6, 200)
+    b[3] = -b[3]
+    a[:, 4] = 0.0
+    assert_bitwise(ozk.gemm_simple(a, b), ref.gemm_simple(3, a, b), "direct TD spread")

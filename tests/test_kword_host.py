@@ -182,3 +182,40 @@ def test_kword_add_integer_compare_variant(ref, port, K):
     want = cpu.mf_add_double(K, x, y)
     bad = np.flatnonzero((got.view(np.uint64) != want.view(np.uint64)).any(axis=1))
     assert bad.size == 0, (bad.size, x[bad[0]], y[bad[0]], got[bad[0]], want[bad[0]])
+
+
+@pytest.mark.parametrize("K", [2, 3, 4])
+def test_kword_mul_kword_matches_reference(ref, K):
+    """MultiFloat<K> * MultiFloat<K> (multifloat.hpp:218-239: two_prod with FMA,
+    canonical_order, sum_ordered) -- the direct K-word GEMM's multiply -- vs the
+    compiled reference, incl. zeros, signs, ties and scale extremes."""
+    if ref is None:
+        pytest.skip("oracle/_ref not built")
+    import __graft_entry__
+    if not os.path.exists(SO):
+        __graft_entry__._build_test_helpers()
+    lib = ctypes.CDLL(SO)
+    lib.kw_host_mul_kw.argtypes = [ctypes.c_int, ctypes.c_size_t, ctypes.c_void_p,
+                                   ctypes.c_void_p, ctypes.c_void_p]
+    rng = np.random.default_rng(500 + K)
+    x = ref.gen_eq1(K, 300, 300, 9).reshape(-1, K).copy()
+    y = ref.gen_eq1(K, 300, 300, 10).reshape(-1, K).copy()
+    n = x.shape[0]
+    sel = rng.integers(0, 10, n)
+    x[sel == 0] = 0.0
+    y[sel == 1, 1:] = 0.0
+    y[sel == 2] = -x[sel == 2]
+    x[sel == 3] *= 2.0 ** -900
+    y[sel == 4] *= 2.0 ** 700
+    x[sel == 5] = -x[sel == 5]
+    x[sel == 6, K - 1] = 0.0
+    y[sel == 7] = x[sel == 7]
+    got = np.empty_like(x)
+    assert lib.kw_host_mul_kw(K, n, x.ctypes.data, y.ctypes.data, got.ctypes.data) == 0
+    rl = ref.lib
+    rl.ref_mf_mul_mf.argtypes = [ctypes.c_int, ctypes.c_size_t, ctypes.c_void_p,
+                                 ctypes.c_void_p, ctypes.c_void_p]
+    want = np.empty_like(x)
+    assert rl.ref_mf_mul_mf(K, n, x.ctypes.data, y.ctypes.data, want.ctypes.data) == 0
+    bad = np.flatnonzero((got.view(np.uint64) != want.view(np.uint64)).any(axis=1))
+    assert bad.size == 0, (bad.size, x[bad[0]], y[bad[0]], got[bad[0]], want[bad[0]])
