@@ -371,6 +371,8 @@ def run_ours(args):
     e2e = None
     if not args.no_e2e and world == 1:
         e2e = run_e2e(args, lib, OzkProfile, A, B, code, K, wb, d, n)
+    elif not args.no_e2e:
+        e2e = run_e2e_sharded(args, eng, A, B, K, wb, n)
 
     engines = {}
     variants = []
@@ -462,6 +464,51 @@ def run_e2e(args, lib, OzkProfile, A, B, code, K, wb, d, n):
             "h2d_bytes_per_step": 2 * n * n * K * wb, "d2h_bytes_per_step": n * n * K * wb,
             "ms_per_step": round(1e3 * t, 3), "api": "ozk_ozaki_gemm (host buffers, pinned)",
             "engine": ENGINE_NAMES.get(prof.engine, "?")}
+
+
+def run_e2e_sharded(args, eng, A, B, K, wb, n):
+    """N > 1: the same metric through the sharded public path
+    (ShardedOzaki.run): every step each rank copies its A row block and the B
+    column block it splits from pinned host memory, runs the split, the
+    all-gather and its pair GEMMs, and reads its C rows back; time = max over
+    ranks (device events bracketing the copies)."""
+    import torch
+    import torch.distributed as dist
+    p = eng.plan
+    ha = A[p.r0:p.r1].cpu().pin_memory()
+    hb = B[:, p.c0:p.c1].cpu().pin_memory() if p.c1 > p.c0 else None
+    da = torch.empty_like(A[p.r0:p.r1])
+    db = torch.zeros_like(B)  # only the rank's column block is read by its split
+    hc = torch.empty((max(p.rows_local, 1), n, K), dtype=A.dtype).pin_memory()
+    stream = torch.cuda.current_stream()
+
+    def step():
+        da.copy_(ha, non_blocking=True)
+        if hb is not None:
+            db[:, p.c0:p.c1].copy_(hb, non_blocking=True)
+        c = eng.run(da, db)
+        hc[: p.rows_local].copy_(c, non_blocking=True)
+
+    step()
+    torch.cuda.synchronize()
+    dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    t = torch.tensor([e0.elapsed_time(e1) * 1e-3 / args.steps], device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    t = float(t.item())
+    io = torch.tensor([(p.rows_local * n + n * (p.c1 - p.c0)) * K * wb,
+                       p.rows_local * n * K * wb], dtype=torch.float64, device="cuda")
+    dist.all_reduce(io)  # whole-job bytes per step (every rank's copies)
+    return {"value": round(2.0 * n ** 3 / t / 1e9, 3), "unit": "GFLOP/s",
+            "h2d_bytes_per_step": int(io[0].item()), "d2h_bytes_per_step": int(io[1].item()),
+            "ms_per_step": round(1e3 * t, 3),
+            "api": "ShardedOzaki.run (sharded.py) with host buffers, per rank; max over ranks",
+            "engine": eng.engine}
 
 
 def direct_rate(lib, code, K, sh, nd=1024):
