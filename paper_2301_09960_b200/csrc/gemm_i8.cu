@@ -196,6 +196,24 @@ __device__ __forceinline__ void tma_load_4d_mc(uint32_t dst, const CUtensorMap* 
         "h"(mask)
         : "memory");
 }
+__device__ __forceinline__ void tma_load_4d_h(uint32_t dst, const CUtensorMap* map, uint32_t bar,
+                                              int c0, int c1, int c2, int c3, uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%3, %4, %5, %6}], [%2], %7;" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "l"(pol)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_4d_mc_h(uint32_t dst, const CUtensorMap* map,
+                                                 uint32_t bar, int c0, int c1, int c2, int c3,
+                                                 uint16_t mask, uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        ".multicast::cluster.L2::cache_hint [%0], [%1, {%3, %4, %5, %6}], [%2], %7, %8;" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1), "r"(c2), "r"(c3),
+        "h"(mask), "l"(pol)
+        : "memory");
+}
 __device__ __forceinline__ void umma_commit_mc(uint32_t bar, uint16_t mask) {
     asm volatile(
         "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
@@ -271,18 +289,57 @@ __device__ __forceinline__ double ldexp_fast(double y, int e) {
     return scalbn(y, e);
 }
 
+// C accesses with an L2 eviction-priority hint (OZK_I8_CHINT >= 1: C loads and
+// stores evict_last; 2: also the operand TMA loads evict_first).  Off: with
+// wave pacing both measured within noise / worse (n=8192 DD/TD/QD: evict_last
+// 72.2/191.4/353.4 ms vs 73.8/187.3/359.7; +evict_first 79.9/201.5/363.2).
+#ifndef OZK_I8_CHINT
+#define OZK_I8_CHINT 0
+#endif
+__device__ __forceinline__ uint64_t l2_policy_evict_last() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ uint64_t l2_policy_evict_first() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ double2 ld2h(const double* p, uint64_t pol) {
+    double2 v;
+    asm volatile("ld.global.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
+                 : "=d"(v.x), "=d"(v.y) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ double ld1h(const double* p, uint64_t pol) {
+    double v;
+    asm volatile("ld.global.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ void st2h(double* p, double a, double b, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(p), "d"(a), "d"(b),
+                 "l"(pol) : "memory");
+}
+__device__ __forceinline__ void st1h(double* p, double a, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(a), "l"(pol)
+                 : "memory");
+}
+
 // One K-word C element as few, wide memory operations.  kVec (16-byte aligned
 // C base, binary64 words): DD one 16-byte access, QD two; TD one 16-byte and
 // one 8-byte access whose order follows the parity q of the element's word
 // offset, so every lane issues the same instruction shape.  Otherwise (TS, or
 // a C base that is only 8-byte aligned) one access per word.
 template <int K, typename W>
-__device__ __forceinline__ void ld_kword(const W* p, int q, bool vec, W (&w)[K]) {
+__device__ __forceinline__ void ld_kword(const W* p, int q, bool vec, W (&w)[K],
+                                         uint64_t pol = 0) {
     if constexpr (sizeof(W) == 8 && (K == 2 || K == 4)) {
         if (vec) {
 #pragma unroll
             for (int h = 0; h < K / 2; ++h) {
-                const double2 v = *reinterpret_cast<const double2*>(p + 2 * h);
+                const double2 v = OZK_I8_CHINT ? ld2h(p + 2 * h, pol)
+                                               : *reinterpret_cast<const double2*>(p + 2 * h);
                 w[2 * h] = v.x;
                 w[2 * h + 1] = v.y;
             }
@@ -290,8 +347,9 @@ __device__ __forceinline__ void ld_kword(const W* p, int q, bool vec, W (&w)[K])
         }
     } else if constexpr (sizeof(W) == 8 && K == 3) {
         if (vec) {
-            const double2 v = *reinterpret_cast<const double2*>(p + q);
-            const double t = p[q ? 0 : 2];
+            const double2 v = OZK_I8_CHINT ? ld2h(p + q, pol)
+                                           : *reinterpret_cast<const double2*>(p + q);
+            const double t = OZK_I8_CHINT ? ld1h(p + (q ? 0 : 2), pol) : p[q ? 0 : 2];
             w[0] = q ? t : v.x;
             w[1] = q ? v.x : v.y;
             w[2] = q ? v.y : t;
@@ -302,19 +360,30 @@ __device__ __forceinline__ void ld_kword(const W* p, int q, bool vec, W (&w)[K])
     for (int k = 0; k < K; ++k) w[k] = p[k];
 }
 template <int K, typename W>
-__device__ __forceinline__ void st_kword(W* p, int q, bool vec, const W (&w)[K]) {
+__device__ __forceinline__ void st_kword(W* p, int q, bool vec, const W (&w)[K],
+                                         uint64_t pol = 0) {
     if constexpr (sizeof(W) == 8 && (K == 2 || K == 4)) {
         if (vec) {
 #pragma unroll
-            for (int h = 0; h < K / 2; ++h)
-                *reinterpret_cast<double2*>(p + 2 * h) = make_double2(w[2 * h], w[2 * h + 1]);
+            for (int h = 0; h < K / 2; ++h) {
+                if (OZK_I8_CHINT)
+                    st2h(p + 2 * h, w[2 * h], w[2 * h + 1], pol);
+                else
+                    *reinterpret_cast<double2*>(p + 2 * h) = make_double2(w[2 * h], w[2 * h + 1]);
+            }
             return;
         }
     } else if constexpr (sizeof(W) == 8 && K == 3) {
         if (vec) {
-            *reinterpret_cast<double2*>(p + q) = q ? make_double2(w[1], w[2])
-                                                   : make_double2(w[0], w[1]);
-            p[q ? 0 : 2] = q ? w[0] : w[2];
+            const double2 v = q ? make_double2(w[1], w[2]) : make_double2(w[0], w[1]);
+            const double t = q ? w[0] : w[2];
+            if (OZK_I8_CHINT) {
+                st2h(p + q, v.x, v.y, pol);
+                st1h(p + (q ? 0 : 2), t, pol);
+            } else {
+                *reinterpret_cast<double2*>(p + q) = v;
+                p[q ? 0 : 2] = t;
+            }
             return;
         }
     }
@@ -430,6 +499,9 @@ pair_gemm_i8_kernel(const __grid_constant__ MapsI8 maps, const __grid_constant__
         uint32_t phase = 0;
         int wave = 0;
         bool pace = prob.pace != nullptr;
+#if OZK_I8_CHINT >= 2
+        const uint64_t opol = l2_policy_evict_first();
+#endif
         for (int g = cluster_id; g < num_groups; g += num_clusters, ++wave) {
             const TileCoord tc = tile_of_group(g);
             for (int p = 0; p < npairs; ++p) {
@@ -477,6 +549,16 @@ pair_gemm_i8_kernel(const __grid_constant__ MapsI8 maps, const __grid_constant__
                         const uint32_t db = sa + dgt * kBTile + cm * (TC / CM) * BKB;
                         const uint32_t da = sa + ND * kBTile + dgt * kATile + cn * (TR / CN) * BKB;
                         const int rb = tc.tn * TC + cm * (TC / CM), ra = tc.tm * TR + cn * (TR / CN);
+#if OZK_I8_CHINT >= 2
+                        if constexpr (CM > 1)
+                            tma_load_4d_mc_h(db, &maps.b, full, kb * BKB, rb, dgt, be, col_mask, opol);
+                        else
+                            tma_load_4d_h(db, &maps.b, full, kb * BKB, rb, dgt, be, opol);
+                        if constexpr (CN > 1)
+                            tma_load_4d_mc_h(da, &maps.a, full, kb * BKB, ra, dgt, al, row_mask, opol);
+                        else
+                            tma_load_4d_h(da, &maps.a, full, kb * BKB, ra, dgt, al, opol);
+#else
                         if constexpr (CM > 1)
                             tma_load_4d_mc(db, &maps.b, full, kb * BKB, rb, dgt, be, col_mask);
                         else
@@ -485,6 +567,7 @@ pair_gemm_i8_kernel(const __grid_constant__ MapsI8 maps, const __grid_constant__
                             tma_load_4d_mc(da, &maps.a, full, kb * BKB, ra, dgt, al, row_mask);
                         else
                             tma_load_4d(da, &maps.a, full, kb * BKB, ra, dgt, al);
+#endif
                     }
                     if (++stage == kStages) {
                         stage = 0;
@@ -598,6 +681,7 @@ pair_gemm_i8_kernel(const __grid_constant__ MapsI8 maps, const __grid_constant__
         const uint32_t tlane = tmem + ((uint32_t)(wq * 32) << 16) + eg * kEpiRows;
         int step = 0;
         const bool tracer = warp == 4 && lane == 0;
+        const uint64_t cpol = OZK_I8_CHINT ? l2_policy_evict_last() : 0;
         for (int g = cluster_id; g < num_groups; g += num_clusters) {
             const TileCoord tc = tile_of_group(g);
             const size_t col = (size_t)tc.tn * TC + wq * 32 + lane;
@@ -633,7 +717,7 @@ pair_gemm_i8_kernel(const __grid_constant__ MapsI8 maps, const __grid_constant__
 #pragma unroll
                             for (int k = 0; k < K; ++k) w[j][k] = W(0);
                         } else {
-                            ld_kword<K>(cbase + e * K, (int)(e & 1), kVec, w[j]);
+                            ld_kword<K>(cbase + e * K, (int)(e & 1), kVec, w[j], cpol);
                         }
                     }
                 };
@@ -696,7 +780,7 @@ pair_gemm_i8_kernel(const __grid_constant__ MapsI8 maps, const __grid_constant__
                         const size_t rr = row0 + r + j;
                         if (col_ok && rr < prob.m) {
                             const size_t e = rr * prob.ldc + col;
-                            st_kword<K>(cbase + e * K, (int)(e & 1), kVec, w[j]);
+                            st_kword<K>(cbase + e * K, (int)(e & 1), kVec, w[j], cpol);
                         }
                     }
                 };
