@@ -62,6 +62,9 @@ def parse():
                    help="rows/cols of the CPU baseline sub-GEMM (inner dim stays n)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-engine-compare", action="store_true",
+                   help="skip timing the other slice-product engine (for large n, where one "
+                        "DMMA step takes tens of seconds)")
     p.add_argument("--csv", default=None,
                    help="also append the headline run as a CSV v1 record (the reference's "
                         "bench table format, bench.cpp:21-22,246-259; `threads` = GPUs)")
@@ -383,7 +386,7 @@ def run_ours(args):
         for e in ("dmma", "int8"):
             if e == engine_used:
                 engines[e] = engine_summary(e, n, d, t_step, t_kern, peak_fp64, peak_i8, nd)
-            else:
+            elif not args.no_engine_compare:
                 ts, tk, used = time_engine(lib, OzkProfile, code, n, d, A, B, C, sh, e)
                 engines[e] = engine_summary(used, n, d, ts, tk, peak_fp64, peak_i8, nd)
         lib.ozk_set_engine(ENGINE_CODES[args.engine])
