@@ -245,7 +245,7 @@ def int8_digits(fmt, l):
     """Digits per slice integer on the INT8 engine (csrc/api.cu int8_digits)."""
     if fmt != "ts":
         return 3
-    return 1 if l > 4096 else 2
+    return 1 if l > 1024 else 2
 
 
 def engine_summary(eng, n, d, t_step, t_kern, peak_fp64, peak_i8, nd=3):

@@ -81,10 +81,11 @@ typedef struct {
  * exact either way):
  *   DMMA : FP64 tensor cores (mma.sync m8n8k4.f64), any shape;
  *   INT8 : each FP64 slice is an integer on its row/column power-of-two grid
- *          (|M| <= 2^(54-sigma)); for 512 < l < 43690 it is split into 3 signed
+ *          (|M| <= 2^(53-sigma)); for 128 < l < 43690 it is split into 3 signed
  *          int8 digits and the 9 digit GEMMs run on tcgen05.mma kind::i8 with
  *          exact int32 accumulation in TMEM (csrc/gemm_i8.cu);
- *   AUTO : INT8 where it applies (DD/TD/QD, D >= 2, 512 < l < 43690), else DMMA. */
+ *   AUTO : INT8 where it applies (DD/TD/QD, D >= 2, 128 < l < 43690; TS
+ *          l < 43690), else DMMA. */
 typedef enum { OZK_ENGINE_AUTO = 0, OZK_ENGINE_DMMA = 1, OZK_ENGINE_INT8 = 2 } ozk_engine;
 ozk_status ozk_set_engine(int engine); /* process-wide; default from $OZK_ENGINE */
 int ozk_get_engine(void);

@@ -28,7 +28,7 @@ thread_local std::string g_last_error;
 int word_bytes_of_fmt(int fmt) { return fmt == OZK_TS ? 4 : 8; }
 
 // Slice-product engine: OZK_ENGINE_AUTO picks the exact INT8-digit tcgen05
-// engine whenever it applies (binary64 words, D >= 2, 512 < l < 43690), else
+// engine whenever it applies (binary64 words, D >= 2, 128 < l < 43690), else
 // the FP64 DMMA engine.  Initialised from $OZK_ENGINE (auto|dmma|int8).
 std::atomic<int> g_engine{-1};
 
@@ -46,7 +46,8 @@ int engine_setting() {
 }
 
 // Digits per slice integer for the INT8 engine, 0 = not applicable.  The
-// slice integer is bounded by 2^(S + 1 - sigma) (S = 53 / 24); signed
+// slice integer on the split's grid 2^(e + sigma - S) is bounded by
+// 2^(S - sigma) (S = 53 / 24, split.cu); signed
 // base-256 digits hold |M| <= 127 (1), 32639 (2), 8355711 (3).  Every digit
 // level (at most 3 digit products per output) stays below 2^31 for l < 43690.
 int int8_digits(int fmt, size_t l, int d) {
@@ -54,11 +55,11 @@ int int8_digits(int fmt, size_t l, int d) {
     int cl = 0;
     while ((size_t(1) << cl) < l) ++cl;
     const int S = word_bytes_of_fmt(fmt) == 4 ? 24 : 53;
-    const int bits = S + 1 - (S + cl + 1) / 2;  // |M| <= 2^bits
+    const int bits = S - (S + cl + 1) / 2;  // |M| <= 2^bits
     if (bits <= 6) return 1;
     if (bits <= 14) return 2;
     if (bits <= 22) return word_bytes_of_fmt(fmt) == 8 ? 3 : 0;
-    return 0;  // binary64 slices at l <= 512 would need 4 digits: DMMA engine
+    return 0;  // binary64 slices at l <= 128 would need 4 digits: DMMA engine
 }
 
 bool int8_applicable(int fmt, size_t l, int d) { return int8_digits(fmt, l, d) > 0; }
@@ -220,7 +221,7 @@ ozk_status ozaki_device_impl(int fmt, size_t m, size_t l, size_t n, const void* 
     const int eng = engine_setting();
     const bool use_i8 = eng != OZK_ENGINE_DMMA && int8_applicable(fmt, l, d);
     if (eng == OZK_ENGINE_INT8 && !use_i8)
-        return fail(OZK_EPARAM, "ozaki_gemm: INT8 engine needs D >= 2 and 512 < l < 43690 "
+        return fail(OZK_EPARAM, "ozaki_gemm: INT8 engine needs D >= 2 and 128 < l < 43690 "
                                 "(binary64 words) or l < 43690 (TS)");
     const int nd = use_i8 ? int8_digits(fmt, l, d) : 0;
     const size_t ld8 = (l + 15) & ~size_t(15);

@@ -2,9 +2,9 @@
 // kind::i8), with the same fused K-word epilogue as the DMMA kernel.
 //
 // Why it is bit-identical to the reference.  Slice a of row i is an integer
-// multiple of 2^g(a,i), g = e + sigma - 54, with |piece / 2^g| <= 2^(54-sigma)
+// multiple of 2^g(a,i), g = e + sigma - 53, with |piece / 2^g| <= 2^(53-sigma)
 // (the split's grid, ozaki.hpp:15-29; test_ozaki.cpp:61-92).  For inner
-// dimension l > 512 (sigma >= 32) that integer M fits 3 signed base-256 digits
+// dimension l > 128 (sigma >= 31) that integer M fits 3 signed base-256 digits
 // d0 + 256 d1 + 65536 d2 (split.cu writes them next to the FP64 slice).  Then
 //   C_ab(i,j) = 2^(gA(i) + gB(j)) * sum_{s,t} 256^(s+t) * sum_k dA_s(i,k) dB_t(j,k)
 // where every int8 x int8 -> int32 digit GEMM is exact (|level| < 3 l 2^14 <
@@ -79,8 +79,8 @@ constexpr int kSmemBudget = 221 * 1024;       // operand ring
 
 // Compile-time shape of one engine instance.
 //   W   word type of C (double: DD/TD/QD, float: TS)
-//   ND  int8 digits per slice integer (3 for binary64 slices at l > 512; 1 for
-//       TS slices at l > 4096, where |M| <= 2^(25 - sigma) <= 64; 2 below)
+//   ND  int8 digits per slice integer (3 for binary64 slices at l > 128; 1 for
+//       TS slices at l > 1024, where |M| <= 2^(24 - sigma) <= 64; 2 below)
 //   TR  tile C rows per digit (MMA N); 2*ND-1 level accumulators of TR TMEM
 //       columns each, stacked MMA width ND*TR <= 256, two accumulator buffers
 //   EG  epilogue warpgroups; each owns TR/EG rows of the tile

@@ -159,9 +159,11 @@ split_rows_kernel(const T* __restrict__ in, size_t in_ld, T* __restrict__ work, 
         T nmx = T(0);
         double pmx = 0.0;
         // INT8-digit output: the slice row is an integer multiple of 2^g,
-        // g = e + sigma - (S + 1) (the half-grid of ozaki.hpp:15-29), with
-        // |x / 2^g| <= 2^(S + 1 - sigma); written as nd signed base-256 digits.
-        const int g = (tau == T(0)) ? 0 : (ceil_log2(mx) + sigma - (ShiftGuard<T>::S + 1));
+        // g = e + sigma - S: every piece is an integer multiple of this grid
+        // (ozaki.hpp:15-29: (v + tau) - tau lands on multiples of ulp of the
+        // binade below tau, 2^(e + sigma - S)) with |x| <= 2^e, so
+        // |x / 2^g| <= 2^(S - sigma); written as nd signed base-256 digits.
+        const int g = (tau == T(0)) ? 0 : (ceil_log2(mx) + sigma - ShiftGuard<T>::S);
         int8_t* drow = dig.digits ? dig.digits + (size_t)a * dig.slice_stride + r * dig.ld : nullptr;
         if (dig.digits && threadIdx.x == 0) dig.exps[(size_t)a * dig.exp_stride + r] = g;
         for (size_t j = threadIdx.x; j < cols; j += kSplitThreads) {

@@ -47,12 +47,12 @@ def test_int8_digit_counts():
     """ozk_int8_digits: digits per slice integer |M| <= 2^(S+1-sigma) in signed
     base 256 (csrc/api.cu int8_digits), 0 where the engine does not apply."""
     from paper_2301_09960_b200._lib import lib
-    for l, nd in [(1, 0), (512, 0), (513, 3), (4096, 3), (8192, 3), (16384, 3), (43689, 3),
+    for l, nd in [(1, 0), (128, 0), (129, 3), (512, 3), (4096, 3), (8192, 3), (16384, 3), (43689, 3),
                   (43690, 0)]:
         assert lib.ozk_int8_digits(2, l, 6) == nd, l
         assert lib.ozk_int8_digits(4, l, 12) == nd, l
-    # TS (S = 24): 2 digits up to l = 4096 (|M| <= 2^(25 - sigma)), 1 beyond
-    for l, nd in [(16, 2), (4096, 2), (4097, 1), (8192, 1), (43690, 0)]:
+    # TS (S = 24): 2 digits up to l = 1024 (|M| <= 2^(24 - sigma)), 1 beyond
+    for l, nd in [(16, 2), (1024, 2), (1025, 1), (4096, 1), (8192, 1), (43690, 0)]:
         assert lib.ozk_int8_digits(0x103, l, 15) == nd, l
     assert lib.ozk_int8_digits(2, 8192, 1) == 0  # D = 1 is the leading image: DMMA path
     assert lib.ozk_int8_digits(7, 8192, 6) == 0  # not a format

@@ -335,13 +335,13 @@ def test_sharded_digits_single_gpu(ozk, cpu, K, m, l, n, d, world):
 
 
 def test_digit_entry_points_reject_inapplicable(ozk):
-    """ozk_int8_digits is 0 at l <= 512 (binary64), and the digit entry points
+    """ozk_int8_digits is 0 at l <= 128 (binary64), and the digit entry points
     refuse such shapes instead of computing something else."""
     import torch
 
     from paper_2301_09960_b200._lib import lib
-    assert lib.ozk_int8_digits(2, 512, 6) == 0
-    assert lib.ozk_int8_digits(2, 513, 6) == 3
+    assert lib.ozk_int8_digits(2, 128, 6) == 0
+    assert lib.ozk_int8_digits(2, 129, 6) == 3
     assert lib.ozk_int8_digits(0x103, 8192, 15) == 1
     x = torch.zeros((8, 8, 2), dtype=torch.float64, device="cuda")
     dg = torch.zeros((6, 3, 8, 16), dtype=torch.int8, device="cuda")
@@ -422,8 +422,9 @@ def engine(ozk):
 
 
 I8_CASES = [
-    # K, m, l, n, d  (l > 512: the exact INT8-digit engine applies)
+    # K, m, l, n, d  (l > 128: the exact INT8-digit engine applies)
     (2, 130, 600, 70, 6), (3, 64, 1000, 64, 9), (4, 200, 777, 130, 12), (2, 256, 2048, 256, 7),
+    (2, 70, 129, 90, 6), (3, 33, 200, 47, 9), (4, 65, 256, 64, 12), (2, 40, 512, 40, 6),
     (2, 1, 513, 1, 2), (3, 300, 1024, 129, 10), (4, 129, 4096, 65, 12), (2, 64, 8192, 64, 6),
 ]
 
@@ -467,7 +468,7 @@ def test_int8_engine_rejects_inapplicable(ozk, engine):
     engine("int8")
     a = np.zeros((4, 100, 2))
     with pytest.raises(ozk.param_error):
-        ozk.ozaki_gemm(a, np.zeros((100, 4, 2)), 6)  # l <= 512
+        ozk.ozaki_gemm(a, np.zeros((100, 4, 2)), 6)  # l <= 128
 
 
 @pytest.mark.parametrize("K,m,l,n", [(2, 33, 47, 29), (3, 20, 33, 18), (4, 16, 40, 24),

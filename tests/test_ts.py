@@ -183,10 +183,10 @@ def test_ts_direct_accuracy(ozk, port):
 @pytest.mark.gpu
 @pytest.mark.parametrize("eng", ["int8", "dmma"])
 @pytest.mark.parametrize("m,l,n,d", [(64, 300, 70, 12), (130, 4097, 129, 15), (200, 5000, 64, 16),
-                                     (33, 700, 40, 8)])
+                                     (33, 700, 40, 8), (40, 1025, 50, 14), (31, 1024, 33, 13)])
 def test_ts_engines_bitexact(ozk, port, eng, m, l, n, d):
-    """TS on both slice-product engines: INT8 uses 2 digits (l <= 4096) or a
-    single digit (l > 4096: |M| <= 2^(25-sigma) <= 64)."""
+    """TS on both slice-product engines: INT8 uses 2 digits (l <= 1024) or a
+    single digit (l > 1024: |M| <= 2^(24-sigma) <= 64)."""
     a = port.gen_eq1_ts(m, l, 40 + m)
     b = port.gen_eq1_ts(l, n, 41 + m)
     want, _, inexact = port.ozaki_gemm_ts(a, b, d, want_inexact=True)
