@@ -424,14 +424,18 @@ inline void kw_add_full(T* x, T y) {
 #define OZK_KW_FAST 1
 #endif
 
-template <int K, typename T = double>
+// kIntCmp selects the comparison flavour of the fast path (same results):
+// integer ALU ops where the FP64 pipe is the contended one (the slice-GEMM
+// epilogue, which shares it with the tensor cores), FP64 compares where the
+// ALU pipe is (the split).
+template <int K, typename T = double, bool kIntCmp = true>
 OZK_HD void kw_add(T* x, T y) {
 #if OZK_KW_FAST
     if constexpr (K >= 3) {
         // the reference sequence minus two steps that are provably no-ops on
         // guarded inputs (kw_fast_ok); anything else takes the full sequence
         if (kw_fast_ok<K>(x, y))
-            kw_add_impl<K, true, T, true>(x, y);
+            kw_add_impl<K, kIntCmp, T, true>(x, y);
         else
             kw_add_full<K>(x, y);
         return;

@@ -165,6 +165,10 @@ split_rows_kernel(const T* __restrict__ in, size_t in_ld, T* __restrict__ work, 
         // |x / 2^g| <= 2^(S - sigma); written as nd signed base-256 digits.
         const int g = (tau == T(0)) ? 0 : (ceil_log2(mx) + sigma - ShiftGuard<T>::S);
         int8_t* drow = dig.digits ? dig.digits + (size_t)a * dig.slice_stride + r * dig.ld : nullptr;
+        // 2^-g as a bit-built binary64 when it is normal (x * 2^-g is then the
+        // exact integer, no XU-pipe scalbn); scalbn otherwise
+        const bool g_normal = -g >= -1022 && -g <= 1023;
+        const double inv_grid = g_normal ? __longlong_as_double((long long)(1023 - g) << 52) : 0.0;
         if (dig.digits && threadIdx.x == 0) dig.exps[(size_t)a * dig.exp_stride + r] = g;
         for (size_t j = threadIdx.x; j < cols; j += kSplitThreads) {
             if (tau == T(0)) {
@@ -180,7 +184,7 @@ split_rows_kernel(const T* __restrict__ in, size_t in_ld, T* __restrict__ work, 
             if (pa) pa[j] = (double)x;
             if (drow) {
                 // exact integer; |mi| fits nd digits by the planner's choice of nd
-                int mi = (int)scalbn((double)x, -g);
+                int mi = g_normal ? (int)((double)x * inv_grid) : (int)scalbn((double)x, -g);
                 for (int q = 0; q < dig.nd - 1; ++q) {
                     const int dq = (int)(int8_t)(mi & 0xff);
                     drow[j + q * dig.digit_stride] = (int8_t)dq;
@@ -189,7 +193,9 @@ split_rows_kernel(const T* __restrict__ in, size_t in_ld, T* __restrict__ work, 
                 drow[j + (dig.nd - 1) * dig.digit_stride] = (int8_t)mi;
             }
             if (x != T(0)) {
-                kw_add<K>(c, -x);  // w -= x  ==  w + (-x)  (multifloat.hpp:302,391)
+                // w -= x  ==  w + (-x)  (multifloat.hpp:302,391); FP64 compares:
+                // this kernel is ALU-bound, its FP64 pipe mostly idle
+                kw_add<K, T, false>(c, -x);
                 store_kw<K>(w + j * K, c);
             }
             nmx = fmax(nmx, fabs_(c[0]));

@@ -28,18 +28,20 @@ for fmt, d in fmts:
     for path, lib in libs:
         lib.ozk_set_engine(2)
         prof = OzkProfile()
-        ts = []
+        ts, tsp = [], []
         for it in range(3):
             assert lib.ozk_ozaki_gemm_device(fmt, n, n, n, A.data_ptr(), B.data_ptr(), d, 0.0,
                                              C.data_ptr(), sh, ctypes.byref(prof)) == 0
             if it:
                 ts.append(prof.product_seconds)
+                tsp.append(prof.split_seconds)
         same = ""
         if ref is None:
             ref = C.clone()
         else:
             same = " (bit-identical)" if torch.equal(ref.view(torch.int32), C.view(torch.int32)) \
                 else " DIFFERS"
-        print(f"K={fmt} {path.split('/')[-1]}: slice GEMM {statistics.median(ts)*1e3:.1f} ms{same}",
+        print(f"K={fmt} {path.split('/')[-1]}: slice GEMM {statistics.median(ts)*1e3:.1f} ms, "
+              f"split {statistics.median(tsp)*1e3:.1f} ms{same}",
               flush=True)
     del A, B, C, ref
