@@ -268,7 +268,11 @@ def run_ours(args):
     import torch
 
     rank, world, local = dist_env()
-    torch.cuda.set_device(local)
+    # OZK_BENCH_ONE_DEVICE=1 is a test hook: every rank on cuda:0 with gloo
+    # (NCCL refuses two ranks on one GPU), to exercise the N > 1 code path on a
+    # one-GPU box; timings from it are not scaling numbers
+    one_dev = os.environ.get("OZK_BENCH_ONE_DEVICE") == "1"
+    torch.cuda.set_device(0 if one_dev else local)
     from paper_2301_09960_b200 import lib
     from paper_2301_09960_b200._lib import OzkProfile
 
@@ -283,7 +287,7 @@ def run_ours(args):
 
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl")
+        dist.init_process_group("gloo" if one_dev else "nccl")
         from paper_2301_09960_b200.sharded import ShardedOzaki
         eng = ShardedOzaki(code, n, n, n, d, rank, world)
 
@@ -316,7 +320,7 @@ def run_ours(args):
     torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
-    clocks = ClockSampler(local)
+    clocks = ClockSampler(0 if one_dev else local)
     clocks.start()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     kern, split = [], []

@@ -1,0 +1,62 @@
+"""The sharded path with real device ops: W = 2, 3 ranks as separate processes
+on cuda:0 (gloo backend, which all-gathers CUDA tensors through the host;
+NCCL refuses two ranks on one device).  Each rank runs ShardedOzaki with
+GpuOps -- its splits into INT8 digit planes (or FP64 slices for l <= 128), the
+gathered-plane permute and its pair GEMMs on the B200 -- and its C rows must
+equal the reference's rows bit for bit.  The kernels of different ranks never
+wait on each other (the only exchange is the host-side collective), so sharing
+one GPU changes timing, not results.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+pytestmark = pytest.mark.gpu
+
+
+def _worker(rank, world, port, cases, q):
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        import oracle
+        from paper_2301_09960_b200.sharded import ShardedOzaki
+        cpu = oracle.best()
+        for (K, m, l, n, d, drop) in cases:
+            a = cpu.gen_eq1(K, m, l, 71 + m)
+            b = cpu.gen_eq1(K, l, n, 72 + m)
+            want = cpu.ozaki_gemm(K, a, b, d, drop)
+            eng = ShardedOzaki(K, m, l, n, d, rank, world, drop_threshold=drop)
+            got = eng.run(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda())
+            got = got.cpu().numpy()
+            r0, r1 = eng.plan.r0, eng.plan.r1
+            ok = np.array_equal(got.view(np.uint64), want[r0:r1].view(np.uint64))
+            q.put((rank, (K, m, l, n, d, drop), eng.engine, bool(ok)))
+    finally:
+        dist.destroy_process_group()
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_ranks_on_device(ozk, world):
+    cases = [(2, 100, 600, 90, 6, 0.0), (3, 64, 1030, 70, 9, 0.0), (4, 40, 300, 50, 12, 0.0),
+             (2, 70, 700, 64, 10, 2.0 ** -70), (2, 30, 100, 40, 6, 0.0)]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    mp.spawn(_worker, args=(world, _free_port(), cases, q), nprocs=world, join=True)
+    results = [q.get() for _ in range(world * len(cases))]
+    bad = [r for r in results if not r[3]]
+    assert not bad, bad
+    engines = {r[1][2]: r[2] for r in results}
+    assert engines[600] == "int8" and engines[100] == "dmma"  # keyed by l
