@@ -346,6 +346,7 @@ def run_ours(args):
     fp64_work = P * 2.0 * rows_local * n * n
     nd = int8_digits(args.format, n)
     traffic = None
+    traffic_src = None
     tfile = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles",
                          "r01_i8_td8192_traffic.json")
     if (engine_used == "int8" and world == 1 and args.format == "td" and n == 8192 and d == 9
@@ -353,14 +354,15 @@ def run_ours(args):
         # dram__bytes_read.sum + dram__bytes_write.sum of this kernel on this
         # workload from the committed ncu --set full capture (per launch)
         tj = json.load(open(tfile))
-        traffic = {"bytes_per_launch": tj["dram_bytes_read"] + tj["dram_bytes_write"],
-                   "source": tj["source"]}
+        traffic = tj["dram_bytes_read"] + tj["dram_bytes_write"]
+        traffic_src = tj["source"]
     if engine_used == "int8":
         kern_work = nd * nd * fp64_work  # nd^2 int8 digit GEMMs per slice pair
         roof = {"bound": "tensor", "kernel": "pair_gemm_i8_kernel (tcgen05.mma kind::i8 + K-word "
                 "epilogue)", "achieved": round(kern_work / t_kern / 1e12, 2),
                 "peak": round(peak_i8, 2), "unit": "TFLOP/s",
                 "frac": round(kern_work / t_kern / 1e12 / peak_i8, 4), "traffic": traffic,
+                "traffic_unit": "DRAM bytes per launch", "traffic_source": traffic_src,
                 "work_per_launch": f"{nd*nd}*P*2*m*n*l = {kern_work:.4g} int8 tensor ops "
                                    "(counted like flops: 2 per multiply-add)",
                 "peak_source": "dense INT8 tcgen05 ceiling measured in this run "
@@ -427,6 +429,24 @@ def run_ours(args):
         }
         if world == 1 and args.format != "ts":
             line["direct_kword_gemm"] = direct_rate(lib, code, K, sh)
+        # split (K1) against HBM: algorithmic bytes = read the K-word A and B
+        # once + write the slice representation (INT8 digit planes + one int32
+        # exponent per row/col and slice, or FP64 slices) -- SURVEY §8d
+        rows_a = rows_local
+        elems = rows_a * n + n * n if world == 1 else rows_a * n + n * (eng.plan.c1 - eng.plan.c0)
+        per_elem = K * wb + (d * nd if engine_used == "int8" else d * 8)
+        split_bytes = elems * per_elem + (rows_a + n) * d * 4
+        t_split = statistics.mean(split)
+        hbm_peak = None
+        pk = os.path.join(os.path.dirname(os.path.abspath(__file__)), "MEASURED_PEAKS.json")
+        if os.path.exists(pk):
+            hbm_peak = json.load(open(pk)).get("hbm_gbs")
+        gbs = split_bytes / t_split / 1e9 if t_split > 0 else None
+        line["split_hbm"] = {
+            "algorithmic_bytes": int(split_bytes), "ms": round(1e3 * t_split, 3),
+            "GB/s": round(gbs, 1) if gbs else None, "peak_GB/s": hbm_peak,
+            "frac": round(gbs / hbm_peak, 4) if gbs and hbm_peak else None,
+            "note": "ALU-bound (K-word residual updates), not HBM-bound: profiles/r01_ncu_summary.md"}
         print(json.dumps(line), flush=True)
         if args.csv:
             from paper_2301_09960_b200.bench_csv import HEADER, BenchRecord, csv_line
@@ -530,11 +550,15 @@ def direct_rate(lib, code, K, sh, nd=1024):
     lib.ozk_gen_eq1_device(code, nd, nd, 1, A.data_ptr(), sh)
     lib.ozk_gen_eq1_device(code, nd, nd, 2, B.data_ptr(), sh)
     stream = torch.cuda.current_stream()
+
+    def call():
+        if lib.ozk_direct_gemm_device(code, nd, nd, nd, A.data_ptr(), B.data_ptr(), C.data_ptr(),
+                                      sh) != 0:
+            raise RuntimeError(lib.ozk_last_error().decode())
+    call()  # warm-up
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
-    if lib.ozk_direct_gemm_device(code, nd, nd, nd, A.data_ptr(), B.data_ptr(), C.data_ptr(),
-                                  sh) != 0:
-        raise RuntimeError(lib.ozk_last_error().decode())
+    call()
     e1.record(stream)
     torch.cuda.synchronize()
     t = e0.elapsed_time(e1) * 1e-3
