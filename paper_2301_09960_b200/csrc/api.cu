@@ -14,6 +14,8 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <functional>
+#include <memory>
 #include <vector>
 
 #include "../../include/ozk.h"
@@ -210,11 +212,28 @@ struct Timer {
     }
 };
 
+// Host-buffer overlap hooks (ozk_ozaki_gemm): wait on b_ready before the B
+// split (its H2D copy runs on another stream during the A split), and run the
+// slice GEMM in `bands` row bands, calling on_band(r0, r1) after each is
+// enqueued so its D2H copy overlaps the next band (rows are independent, so
+// banding does not change a bit).
+struct HostOverlap {
+    cudaEvent_t b_ready = nullptr;
+    int bands = 1;
+    std::function<cudaError_t(size_t, size_t)> on_band;
+    // optional: A arrives band by band (a_ready[b] = rows of band b on the
+    // device); then B is split first and each band's A rows are split right
+    // before its GEMM (not with drop_threshold > 0: the pair list needs every
+    // slice maximum first)
+    const cudaEvent_t* a_ready = nullptr;
+};
+
 // C = A * B via the Ozaki scheme on device buffers; A has row stride lda, B
 // row stride ldb (elements), C is dense m x n.
 ozk_status ozaki_device_impl(int fmt, size_t m, size_t l, size_t n, const void* a, size_t lda,
                              const void* b, size_t ldb, int d, double drop, void* c,
-                             cudaStream_t st, ozk_profile* prof) {
+                             cudaStream_t st, ozk_profile* prof,
+                             const HostOverlap* ov = nullptr) {
     const int K = words_of(fmt), wb = word_bytes_of(fmt);
     const int sms = num_sms_cached();
     const size_t ldk = slice_ld(l);
@@ -263,9 +282,16 @@ ozk_status ozaki_device_impl(int fmt, size_t m, size_t l, size_t n, const void* 
 
     Timer tm(prof != nullptr);
     tm.mark(0, st);
-    OZK_CUDA(split_to_slices(fmt, m, l, lda, a, d, OZK_SIDE_ROWS, sa.as<double>(), m, work.p,
-                             want_max ? amax : nullptr, err, st, digA),
-             "ozaki_gemm: split A");
+    const bool banded_a = ov && ov->a_ready && !want_max && ov->bands > 1;
+    if (!banded_a) {
+        if (ov && ov->a_ready)
+            for (int q = 0; q < ov->bands; ++q)
+                OZK_CUDA(cudaStreamWaitEvent(st, ov->a_ready[q], 0), "ozaki_gemm: wait A");
+        OZK_CUDA(split_to_slices(fmt, m, l, lda, a, d, OZK_SIDE_ROWS, sa.as<double>(), m, work.p,
+                                 want_max ? amax : nullptr, err, st, digA),
+                 "ozaki_gemm: split A");
+    }
+    if (ov && ov->b_ready) OZK_CUDA(cudaStreamWaitEvent(st, ov->b_ready, 0), "ozaki_gemm: wait B");
     OZK_CUDA(split_to_slices(fmt, l, n, ldb, b, d, OZK_SIDE_COLS, sb.as<double>(), n, work.p,
                              want_max ? bmax : nullptr, err, st, digB),
              "ozaki_gemm: split B");
@@ -303,30 +329,64 @@ ozk_status ozaki_device_impl(int fmt, size_t m, size_t l, size_t n, const void* 
     prob.l = l;
     prob.c = c;
     prob.ldc = n;
-    if (pl.count == 0) {  // every pair pruned (drop_threshold > 1): C = 0
-        OZK_CUDA(cudaMemsetAsync(c, 0, elem_bytes(fmt) * m * n, st), "ozaki_gemm: zero C");
-    } else if (use_i8) {
-        I8Operands op{};
-        op.nd = nd;
-        op.a = da8.as<int8_t>();
-        op.a_ld = ld8;
-        op.a_digit_stride = m * ld8;
-        op.a_slice_stride = (size_t)nd * m * ld8;
-        op.b = db8.as<int8_t>();
-        op.b_ld = ld8;
-        op.b_digit_stride = n * ld8;
-        op.b_slice_stride = (size_t)nd * n * ld8;
-        op.gA = ga.as<int>();
-        op.gB = gb.as<int>();
-        op.m = m;
-        op.n = n;
-        op.l = l;
-        op.d = d;
-        op.c = c;
-        op.ldc = n;
-        OZK_CUDA(launch_pair_gemm_i8(K, wb, op, pl, st, sms), "ozaki_gemm: INT8 slice GEMM");
-    } else {
-        OZK_CUDA(launch_pair_gemm(K, kAccumulate, prob, pl, st, sms, wb), "ozaki_gemm: slice GEMM");
+    const int bands = (ov && ov->bands > 1 && (pl.count > 0 || banded_a)) ? ov->bands : 1;
+    const size_t band_rows = (m + bands - 1) / bands;
+    const size_t eb = elem_bytes(fmt);
+    std::vector<std::unique_ptr<Timer>> split_a_timers;  // per-band A splits (profile)
+    int band = 0;
+    for (size_t r0 = 0; r0 < m; r0 += band_rows, ++band) {
+        const size_t rows = m - r0 < band_rows ? m - r0 : band_rows;
+        char* cb = static_cast<char*>(c) + r0 * n * eb;
+        if (banded_a) {
+            // this band's A rows: per-row split, identical to the rows of the
+            // whole-matrix split (ozaki.hpp:102-103)
+            OZK_CUDA(cudaStreamWaitEvent(st, ov->a_ready[band], 0), "ozaki_gemm: wait A");
+            DigitOut dband = digA;
+            if (use_i8) {
+                dband.digits += r0 * ld8;
+                dband.exps += r0;
+            }
+            split_a_timers.push_back(std::make_unique<Timer>(prof != nullptr));
+            split_a_timers.back()->mark(0, st);
+            OZK_CUDA(split_to_slices(fmt, rows, l, lda,
+                                     static_cast<const char*>(a) + r0 * lda * eb, d,
+                                     OZK_SIDE_ROWS, use_i8 ? nullptr : sa.as<double>() + r0 * ldk,
+                                     m, work.p, nullptr, err, st, dband),
+                     "ozaki_gemm: split A band");
+            split_a_timers.back()->mark(1, st);
+        }
+        if (pl.count == 0) {  // every pair pruned (drop_threshold > 1): C = 0
+            OZK_CUDA(cudaMemsetAsync(cb, 0, eb * rows * n, st), "ozaki_gemm: zero C");
+        } else if (use_i8) {
+            I8Operands op{};
+            op.nd = nd;
+            op.a = da8.as<int8_t>() + r0 * ld8;
+            op.a_ld = ld8;
+            op.a_digit_stride = m * ld8;
+            op.a_slice_stride = (size_t)nd * m * ld8;
+            op.b = db8.as<int8_t>();
+            op.b_ld = ld8;
+            op.b_digit_stride = n * ld8;
+            op.b_slice_stride = (size_t)nd * n * ld8;
+            op.gA = ga.as<int>() + r0;
+            op.gB = gb.as<int>();
+            op.gA_stride = m;
+            op.gB_stride = n;
+            op.m = rows;
+            op.n = n;
+            op.l = l;
+            op.d = d;
+            op.c = cb;
+            op.ldc = n;
+            OZK_CUDA(launch_pair_gemm_i8(K, wb, op, pl, st, sms), "ozaki_gemm: INT8 slice GEMM");
+        } else {
+            GemmProblem pb = prob;
+            pb.a = prob.a + r0 * ldk;
+            pb.m = rows;
+            pb.c = cb;
+            OZK_CUDA(launch_pair_gemm(K, kAccumulate, pb, pl, st, sms, wb), "ozaki_gemm: slice GEMM");
+        }
+        if (ov && ov->on_band) OZK_CUDA(ov->on_band(r0, r0 + rows), "ozaki_gemm: band copy");
     }
     tm.mark(2, st);
 
@@ -336,8 +396,10 @@ ozk_status ozaki_device_impl(int fmt, size_t m, size_t l, size_t n, const void* 
     OZK_CUDA(cudaStreamSynchronize(st), "ozaki_gemm");
     if (ozk_status s = check_dev_err(flag, "split_matrix")) return s;
     if (prof) {
-        prof->split_seconds = tm.secs(0, 1);
-        prof->product_seconds = tm.secs(1, 2);
+        double split_a_banded = 0.0;
+        for (const auto& t : split_a_timers) split_a_banded += t->secs(0, 1);
+        prof->split_seconds = tm.secs(0, 1) + split_a_banded;
+        prof->product_seconds = tm.secs(1, 2) - split_a_banded;
         prof->accumulate_seconds = 0.0;
         prof->total_seconds = prof->split_seconds + prof->product_seconds;
         prof->split_count = d;
@@ -405,17 +467,75 @@ ozk_status ozk_ozaki_gemm(ozk_format fmt, size_t m, size_t l, size_t n, const vo
     OwnStream os;
     OZK_CUDA(os.create(), "ozaki_gemm: stream");
     num_sms_cached();
+    // Transfers overlap compute on a second stream: B's H2D runs during the A
+    // split, and C comes back band by band while later bands compute.
+    OwnStream xs, ys;  // H2D copies, D2H copies
+    OZK_CUDA(xs.create(), "ozaki_gemm: copy stream");
+    OZK_CUDA(ys.create(), "ozaki_gemm: copy stream");
     DevBuf da, db, dc;
     OZK_CUDA(da.alloc(eb * m * l, os.s), "ozaki_gemm: A");
     OZK_CUDA(db.alloc(eb * l * n, os.s), "ozaki_gemm: B");
     OZK_CUDA(dc.alloc(eb * m * n, os.s), "ozaki_gemm: C");
-    OZK_CUDA(cudaMemcpyAsync(da.p, a, eb * m * l, cudaMemcpyHostToDevice, os.s), "ozaki_gemm: H2D A");
-    OZK_CUDA(cudaMemcpyAsync(db.p, b, eb * l * n, cudaMemcpyHostToDevice, os.s), "ozaki_gemm: H2D B");
+    cudaEvent_t allocated = nullptr, b_ready = nullptr;
+    OZK_CUDA(cudaEventCreateWithFlags(&allocated, cudaEventDisableTiming), "ozaki_gemm: event");
+    OZK_CUDA(cudaEventCreateWithFlags(&b_ready, cudaEventDisableTiming), "ozaki_gemm: event");
+    const int bands = m >= 2048 ? 8 : 1;
+    std::vector<cudaEvent_t> band_done(bands, nullptr), a_ready(bands, nullptr);
+    struct EventGuard {
+        std::vector<cudaEvent_t*> evs;
+        ~EventGuard() {
+            for (auto* e : evs)
+                if (*e) cudaEventDestroy(*e);
+        }
+    } guard;
+    guard.evs = {&allocated, &b_ready};
+    for (auto* vec : {&band_done, &a_ready})
+        for (auto& e : *vec) {
+            OZK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "ozaki_gemm: event");
+            guard.evs.push_back(&e);
+        }
+    OZK_CUDA(cudaEventRecord(allocated, os.s), "ozaki_gemm: event");
+    OZK_CUDA(cudaStreamWaitEvent(xs.s, allocated, 0), "ozaki_gemm: wait");
+    OZK_CUDA(cudaStreamWaitEvent(ys.s, allocated, 0), "ozaki_gemm: wait");
+    // B first (its split gates every band), then A band by band
+    OZK_CUDA(cudaMemcpyAsync(db.p, b, eb * l * n, cudaMemcpyHostToDevice, xs.s), "ozaki_gemm: H2D B");
+    OZK_CUDA(cudaEventRecord(b_ready, xs.s), "ozaki_gemm: event");
+    const size_t band_rows = (m + bands - 1) / bands;
+    for (int q = 0; q < bands; ++q) {
+        const size_t r0 = q * band_rows, rows = r0 < m ? (m - r0 < band_rows ? m - r0 : band_rows) : 0;
+        if (rows)
+            OZK_CUDA(cudaMemcpyAsync(static_cast<char*>(da.p) + r0 * l * eb,
+                                     static_cast<const char*>(a) + r0 * l * eb, rows * l * eb,
+                                     cudaMemcpyHostToDevice, xs.s),
+                     "ozaki_gemm: H2D A");
+        OZK_CUDA(cudaEventRecord(a_ready[q], xs.s), "ozaki_gemm: event");
+    }
+    HostOverlap ov;
+    ov.b_ready = b_ready;
+    ov.bands = bands;
+    ov.a_ready = a_ready.data();
+    int band = 0;
+    ov.on_band = [&](size_t r0, size_t r1) -> cudaError_t {
+        cudaEvent_t ev = band_done[band < bands ? band : bands - 1];
+        ++band;
+        cudaError_t e = cudaEventRecord(ev, os.s);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(ys.s, ev, 0);
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(static_cast<char*>(c) + r0 * n * eb,
+                                static_cast<char*>(dc.p) + r0 * n * eb, (r1 - r0) * n * eb,
+                                cudaMemcpyDeviceToHost, ys.s);
+        return e;
+    };
     ozk_profile local{};
     ozk_status s =
-        ozaki_device_impl((int)fmt, m, l, n, da.p, l, db.p, n, d, drop, dc.p, os.s, &local);
-    if (s != OZK_OK) return s;
-    OZK_CUDA(cudaMemcpyAsync(c, dc.p, eb * m * n, cudaMemcpyDeviceToHost, os.s), "ozaki_gemm: D2H C");
+        ozaki_device_impl((int)fmt, m, l, n, da.p, l, db.p, n, d, drop, dc.p, os.s, &local, &ov);
+    if (s != OZK_OK) {
+        cudaStreamSynchronize(xs.s);
+        cudaStreamSynchronize(ys.s);
+        return s;
+    }
+    OZK_CUDA(cudaStreamSynchronize(xs.s), "ozaki_gemm: H2D");
+    OZK_CUDA(cudaStreamSynchronize(ys.s), "ozaki_gemm: D2H C");
     OZK_CUDA(cudaStreamSynchronize(os.s), "ozaki_gemm");
     if (prof) {
         *prof = local;
