@@ -497,3 +497,17 @@ def test_direct_gemm_spread_inputs(ozk, ref, port):
     b[3] = -b[3]
     a[:, 4] = 0.0
     assert_bitwise(ozk.gemm_simple(a, b), ref.gemm_simple(3, a, b), "direct TD spread")
+
+
+@pytest.mark.parametrize("K,m,l,n,d,drop", [(2, 2049, 600, 70, 6, 0.0), (3, 2048, 300, 64, 9, 2.0 ** -90),
+                                            (4, 2100, 130, 40, 12, 0.0), (2, 4097, 100, 33, 6, 0.0)])
+def test_host_api_banded_overlap(ozk, cpu, K, m, l, n, d, drop):
+    """ozk_ozaki_gemm with host buffers at m >= 2048 runs the banded, transfer-
+    overlapped schedule (B first, A + slice GEMM in 8 row bands, C copied back
+    per band; drop > 0 keeps the whole-matrix A split): bit-identical."""
+    a = cpu.gen_eq1(K, m, l, 90 + K)
+    b = cpu.gen_eq1(K, l, n, 91 + K)
+    want = cpu.ozaki_gemm(K, a, b, d, drop)
+    got, prof = ozk.ozaki_gemm(a, b, d, drop_threshold=drop)
+    assert_bitwise(got, want, f"banded host K={K} {m}x{l}x{n} D={d} drop={drop}")
+    assert prof.split_seconds > 0 and prof.product_seconds > 0
