@@ -124,12 +124,12 @@ OZK_HD bool dfinite(double x) { return is_finite(x); }
 
 // ---- comparisons -------------------------------------------------------------
 // kInt = false: the reference's floating-point comparisons.  kInt = true: the
-// same predicates on the bit patterns (integer ALU instead of DSETP, which on
-// B200 shares the slow XU pipe).  They agree for every finite operand whose
-// words stay below 2^1000 (2^120 for binary32), which kw_add checks before
-// taking that path: no NaN (where FP and bit comparisons differ), no overflow
-// to infinity inside the sweeps, and -0 never reaches a bitwise comparison
-// (the compaction writes +0; x - x rounds to +0).
+// same predicates on the bit patterns (integer ALU instead of DSETP on the FP64
+// pipe, which the tensor cores share on sm_100).  They agree for every finite
+// operand whose words stay below 2^1000 (2^120 for binary32), which kw_add's
+// guard (kw_fast_ok) checks before taking that path: no NaN (where FP and bit
+// comparisons differ), no overflow to infinity inside the sweeps, and -0 never
+// reaches a bitwise comparison (the compaction writes +0; x - x rounds to +0).
 template <typename T> struct Bits;
 template <> struct Bits<double> {
     using U = uint64_t;
@@ -161,8 +161,6 @@ OZK_HD bool same(T a, T b) {  // a == b in the kInt domain described above
     if constexpr (kInt) return hi_word(a) == hi_word(b) && lo_word(a) == lo_word(b);
     else return a == b;
 }
-template <typename T>
-OZK_HD bool safe_word(T x) { return (fbits(x) & Bits<T>::kAbs) < Bits<T>::kSafe; }
 
 // eft.hpp:25-30
 template <typename T>
@@ -382,10 +380,6 @@ OZK_HD void kw_add_impl(T* x, T y) {
 }
 
 #if defined(__CUDA_ARCH__)
-template <int K, typename T>
-__device__ __noinline__ void kw_add_slow(T* x, T y) {
-    kw_add_impl<K, false>(x, y);
-}
 // the complete reference sequence, out of line on the device (rarely taken);
 // words passed by value so the caller's registers never go through memory
 template <int K, typename T>
@@ -413,13 +407,7 @@ inline void kw_add_full(T* x, T y) {
 }
 #endif
 
-// Integer-compare fast path: bit-exact (tests/test_kword_host.py) but measured
-// slower on B200 in both slice-GEMM epilogues (INT8 engine TD 384 vs 330 ms,
-// QD 736 vs 612 ms at n = 8192), so it is off by default.
-#ifndef OZK_KW_INTCMP
-#define OZK_KW_INTCMP 0
-#endif
-
+// OZK_KW_FAST=0 restores the plain reference sequence everywhere (A/B builds).
 #ifndef OZK_KW_FAST
 #define OZK_KW_FAST 1
 #endif
@@ -441,20 +429,7 @@ OZK_HD void kw_add(T* x, T y) {
         return;
     }
 #endif
-#if defined(__CUDA_ARCH__) && OZK_KW_INTCMP
-    // integer comparisons whenever they are provably identical (see Bits<>);
-    // anything near the overflow threshold or non-finite takes the reference
-    // floating-point comparisons out of line
-    bool ok = safe_word(y);
-#pragma unroll
-    for (int i = 0; i < K; ++i) ok = ok && safe_word(x[i]);
-    if (ok)
-        kw_add_impl<K, true>(x, y);
-    else
-        kw_add_slow<K>(x, y);
-#else
     kw_add_impl<K, false>(x, y);
-#endif
 }
 
 // -MultiFloat<K> (multifloat.hpp:265-269): zero words stay +0.

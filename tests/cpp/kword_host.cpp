@@ -17,6 +17,26 @@ static void run(std::size_t n, const double* x, const double* y, double* out) {
 }
 
 template <int K>
+static void run_fp(std::size_t n, const double* x, const double* y, double* out) {
+    for (std::size_t i = 0; i < n; ++i) {
+        double w[K];
+        for (int k = 0; k < K; ++k) w[k] = x[i * K + k];
+        ozk::kw_add<K, double, false>(w, y[i]);  // the split's compare flavour
+        for (int k = 0; k < K; ++k) out[i * K + k] = w[k];
+    }
+}
+
+extern "C" int kw_host_add_fpcmp(int K, std::size_t n, const double* x, const double* y,
+                                 double* out) {
+    switch (K) {
+    case 2: run_fp<2>(n, x, y, out); return 0;
+    case 3: run_fp<3>(n, x, y, out); return 0;
+    case 4: run_fp<4>(n, x, y, out); return 0;
+    default: return 2;
+    }
+}
+
+template <int K>
 static void run_kw(std::size_t n, const double* x, const double* y, double* out) {
     for (std::size_t i = 0; i < n; ++i) {
         double w[K], v[K];

@@ -219,3 +219,23 @@ def test_kword_mul_kword_matches_reference(ref, K):
     assert rl.ref_mf_mul_mf(K, n, x.ctypes.data, y.ctypes.data, want.ctypes.data) == 0
     bad = np.flatnonzero((got.view(np.uint64) != want.view(np.uint64)).any(axis=1))
     assert bad.size == 0, (bad.size, x[bad[0]], y[bad[0]], got[bad[0]], want[bad[0]])
+
+
+@pytest.mark.parametrize("K", [3, 4])
+def test_kword_add_fp_compare_flavour(ref, port, K):
+    """kw_add<K, double, false> -- the fast path with FP64 comparisons, as the
+    split uses it -- equals the reference on the adversarial set."""
+    import __graft_entry__
+    if not os.path.exists(SO):
+        __graft_entry__._build_test_helpers()
+    lib = ctypes.CDLL(SO)
+    lib.kw_host_add_fpcmp.argtypes = [ctypes.c_int, ctypes.c_size_t, ctypes.c_void_p,
+                                      ctypes.c_void_p, ctypes.c_void_p]
+    cpu = _checker(ref, port)
+    rng = np.random.default_rng(8765 + K)
+    x, y = _cases(K, cpu, rng, 200_000)
+    got = np.empty_like(x)
+    assert lib.kw_host_add_fpcmp(K, x.shape[0], x.ctypes.data, y.ctypes.data, got.ctypes.data) == 0
+    want = cpu.mf_add_double(K, x, y)
+    bad = np.flatnonzero((got.view(np.uint64) != want.view(np.uint64)).any(axis=1))
+    assert bad.size == 0, (bad.size, x[bad[0]], y[bad[0]], got[bad[0]], want[bad[0]])
