@@ -161,6 +161,19 @@ ozk_status ozk_slices_gemm_device(ozk_format fmt, size_t m, size_t l, size_t n,
                                   const int* pairs, int npairs, void* c, size_t ldc,
                                   void* stream);
 
+/* ---- automatic split count (not in the reference) ------------- *
+ * A policy for (split_count, drop_threshold) from the format and the inner
+ * dimension alone: enough slices to capture the full K-word significand,
+ * D = ceil(S*K / (S - sigma)) + 2 (S = 53, or 24 for TS; capped at 32), and the
+ * reference's own pair pruning (ozaki.hpp:198-221) at
+ * drop = 2^-(S*K + ceil(log2 l) + 2): pairs whose products are normwise below
+ * the format's precision are skipped.  ozk_ozaki_gemm(..., D, drop, ...) with
+ * these values equals the reference's ozaki_gemm(a, b, D, backend, drop) bit
+ * for bit; for Eq. (1) inputs at l = 8192 it keeps the pairs of the measured
+ * accuracy saturation (DD 7, TD 9, QD 12). */
+int ozk_auto_split_count(ozk_format fmt, size_t inner_dim);
+double ozk_auto_drop_threshold(ozk_format fmt, size_t inner_dim);
+
 /* ---- INT8-digit slice entry points (sharded orchestration, INT8 engine) ---- *
  * The exact INT8 engine stores each slice as nd signed base-256 digit planes of
  * the slice integers plus one grid exponent per row (A) / column (B):

@@ -9,6 +9,7 @@ from ._lib import LIB_PATH, lib  # noqa: F401  (raises if libozk.so is missing)
 from .mpmat import (  # noqa: F401
     OzakiProfile,
     SplitSet,
+    auto_split_policy,
     SplitSide,
     error,
     exponent_ceil_log2,
@@ -19,6 +20,7 @@ from .mpmat import (  # noqa: F401
     read_matrix_file,
     lu_trailing_update,
     ozaki_gemm,
+    ozaki_gemm_auto,
     param_error,
     shape_error,
     set_engine,
@@ -32,5 +34,6 @@ __all__ = [
     "OzakiProfile", "SplitSet", "SplitSide", "error", "exponent_ceil_log2", "gpu_backend",
     "ozaki_gemm", "param_error", "shape_error", "split_matrix", "split_shift_bits", "lib",
     "ts_direct_gemm", "lu_trailing_update", "set_engine", "get_engine", "io_error",
-    "read_matrix_file", "write_matrix_file", "gemm_simple",
+    "read_matrix_file", "write_matrix_file", "gemm_simple", "auto_split_policy",
+    "ozaki_gemm_auto",
 ]

@@ -53,6 +53,8 @@ SIGNATURES = {
     "ozk_slices_gemm_device": (ctypes.c_int, [ctypes.c_int, _sz, _sz, _sz, _dp, _dp, _sz, _sz,
                                               _sz, ctypes.c_int, _ip, ctypes.c_int, _dp, _sz,
                                               ctypes.c_void_p]),
+    "ozk_auto_split_count": (ctypes.c_int, [ctypes.c_int, _sz]),
+    "ozk_auto_drop_threshold": (ctypes.c_double, [ctypes.c_int, _sz]),
     "ozk_int8_digits": (ctypes.c_int, [ctypes.c_int, _sz, ctypes.c_int]),
     "ozk_split_digits_device": (ctypes.c_int, [ctypes.c_int, _sz, _sz, _sz, _dp, ctypes.c_int,
                                                ctypes.c_int, _dp, _sz, _sz, _dp, _dp,

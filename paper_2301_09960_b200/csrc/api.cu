@@ -717,6 +717,25 @@ ozk_status ozk_slices_gemm_device(ozk_format fmt, size_t m, size_t l, size_t n,
     return OZK_OK;
 }
 
+int ozk_auto_split_count(ozk_format fmt, size_t inner_dim) {
+    if (!valid_fmt(fmt) || inner_dim == 0) return 0;
+    const int S = word_bytes_of(fmt) == 4 ? 24 : 53;
+    const int K = words_of(fmt);
+    const int sigma = shift_bits(inner_dim, S);
+    const int per = S - sigma;  // significand bits one slice captures
+    if (per <= 0) return kMaxSplits;
+    const int d = (S * K + per - 1) / per + 2;
+    return d < kMaxSplits ? d : kMaxSplits;
+}
+
+double ozk_auto_drop_threshold(ozk_format fmt, size_t inner_dim) {
+    if (!valid_fmt(fmt) || inner_dim == 0) return 0.0;
+    const int S = word_bytes_of(fmt) == 4 ? 24 : 53;
+    int cl = 0;
+    while ((size_t(1) << cl) < inner_dim) ++cl;
+    return std::ldexp(1.0, -(S * words_of(fmt) + cl + 2));
+}
+
 int ozk_int8_digits(ozk_format fmt, size_t inner_dim, int d) {
     if (!valid_fmt(fmt)) return 0;
     return int8_digits(fmt, inner_dim, d);

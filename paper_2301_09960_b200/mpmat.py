@@ -228,6 +228,25 @@ def ozaki_gemm(a, b, d: int, backend=None, drop_threshold: float = 0.0):
     return c, OzakiProfile._of(prof)
 
 
+def auto_split_policy(fmt: int, inner_dim: int) -> tuple[int, float]:
+    """(split_count, drop_threshold) of the automatic mode (include/ozk.h
+    ozk_auto_split_count / ozk_auto_drop_threshold; not in the reference)."""
+    return (int(lib.ozk_auto_split_count(fmt, inner_dim)),
+            float(lib.ozk_auto_drop_threshold(fmt, inner_dim)))
+
+
+def ozaki_gemm_auto(a, b):
+    """ozaki_gemm with the automatic split count: enough slices for the full
+    K-word significand and the reference's own pair pruning at the format's
+    precision, so only the pairs that can change C are computed.  Equals the
+    reference's ozaki_gemm(a, b, D, backend, drop) for the returned D, drop.
+    Returns (C, OzakiProfile, D, drop)."""
+    _, l, fmt = _kword_shape(a)
+    d, drop = auto_split_policy(fmt, l)
+    c, prof = ozaki_gemm(a, b, d, drop_threshold=drop)
+    return c, prof, d, drop
+
+
 def split_matrix(m, d: int, side: SplitSide) -> SplitSet:
     """split_matrix<K> (ozaki.hpp:74-147): pieces + K-word residual (host arrays)."""
     rows, cols, k = _kword_shape(m)

@@ -124,3 +124,15 @@ def test_product_path_has_no_cpu_fallback():
     from paper_2301_09960_b200 import _lib
     with pytest.raises(ImportError):
         _lib.load(os.path.join(ROOT, "does-not-exist.so"))
+
+
+def test_auto_split_policy():
+    """Automatic D: ceil(S*K / (S - sigma)) + 2 slices and pair
+    pruning at 2^-(S*K + ceil(log2 l) + 2)."""
+    import paper_2301_09960_b200 as ozk
+    assert ozk.auto_split_policy(2, 8192) == (8, 2.0 ** -121)
+    assert ozk.auto_split_policy(3, 8192) == (10, 2.0 ** -174)
+    assert ozk.auto_split_policy(4, 8192) == (13, 2.0 ** -227)
+    assert ozk.auto_split_policy(0x103, 8192) == (17, 2.0 ** -87)
+    assert ozk.auto_split_policy(2, 1) == (7, 2.0 ** -108)   # sigma = 27: 26 bits per slice
+    assert ozk.auto_split_policy(7, 8192) == (0, 0.0)

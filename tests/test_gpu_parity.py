@@ -511,3 +511,20 @@ def test_host_api_banded_overlap(ozk, cpu, K, m, l, n, d, drop):
     got, prof = ozk.ozaki_gemm(a, b, d, drop_threshold=drop)
     assert_bitwise(got, want, f"banded host K={K} {m}x{l}x{n} D={d} drop={drop}")
     assert prof.split_seconds > 0 and prof.product_seconds > 0
+
+
+
+@pytest.mark.parametrize("K,m,l,n", [(2, 64, 8192, 48), (3, 40, 8192, 40), (4, 32, 8192, 24),
+                                     (3, 50, 600, 70), (2, 33, 100, 20)])
+def test_auto_split_count_matches_reference(ozk, cpu, K, m, l, n):
+    """ozaki_gemm_auto = the reference's ozaki_gemm(a, b, D, backend, drop) for
+    the policy's D and drop; at l = 8192 the kept pairs are those of the
+    measured accuracy saturation (TD: alpha + beta <= 8 -> 45 pairs)."""
+    a = cpu.gen_eq1(K, m, l, 100 + K)
+    b = cpu.gen_eq1(K, l, n, 101 + K)
+    got, prof, d, drop = ozk.ozaki_gemm_auto(a, b)
+    want = cpu.ozaki_gemm(K, a, b, d, drop)
+    assert_bitwise(got, want, f"auto K={K} l={l} D={d}")
+    assert prof.pairs < d * (d + 1) // 2  # pruning removed the sub-precision pairs
+    if l == 8192 and K == 3:
+        assert prof.pairs == 45
