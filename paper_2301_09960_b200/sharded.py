@@ -7,7 +7,9 @@ Rank r of W owns C rows [r0, r1) and B columns [c0, c1):
 2. split its B column block (per-column split: bit-identical to the columns of
    the global split);
 3. all-gather the B slices over NCCL (NVLink/NVSwitch) -- the path's one real
-   exchange step: D * l * ceil(n/W) * 8 bytes per rank;
+   exchange step: D * l * ceil(n/W) * 8 bytes per rank (INT8 digits: D * nd *
+   l * ceil(n/W)); B is split first and the gather runs on a side stream while
+   the A rows are split;
 4. with drop_threshold > 0, all-reduce(max) the per-slice maxima so every rank
    prunes the same pairs (ozaki.hpp:198-221);
 5. run every slice pair for its rows with the fused accumulation.  The
@@ -177,6 +179,7 @@ class ShardedOzaki:
                                 dtype=torch.float32 if K == OZK_TS else torch.float64)
         self.pmax = self.ops.zeros((2, d)) if self.drop > 0.0 else None
         self.timing = hasattr(self.ops, "device") and self.ops.device.type == "cuda"
+        self._comm = None  # side stream of the B all-gather (NCCL)
 
     @property
     def rows_local(self) -> int:
@@ -216,12 +219,9 @@ class ShardedOzaki:
             self.pmax.zero_()
         amax = self.pmax[0] if self.pmax is not None else None
         bmax = self.pmax[1] if self.pmax is not None else None
-        if p.rows_local:
-            if self.engine == "int8":
-                ops.split_digits(p.K, a_rows, p.rows_local, p.l, p.l, p.d, 0, self.a8, self.ga,
-                                 amax)
-            else:
-                ops.split(p.K, a_rows, p.rows_local, p.l, p.l, p.d, 0, self.sa, amax)
+        # B first: its all-gather (the path's one exchange) then runs on a side
+        # stream while this rank splits its A rows (NCCL; gloo gathers on the
+        # host and cannot overlap)
         if p.c1 > p.c0:
             # column block [c0, c1) of the row-major (l x n) B, split in place
             if self.engine == "int8":
@@ -229,15 +229,32 @@ class ShardedOzaki:
                                  self.gb, bmax)
             else:
                 ops.split(p.K, B[:, p.c0:p.c1], p.l, p.c1 - p.c0, p.n, p.d, 1, self.sb, bmax)
+        comm = None
+        if self.timing and dist.get_backend(self.group) == "nccl":
+            if self._comm is None:
+                self._comm = torch.cuda.Stream()
+            comm = self._comm
+            comm.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(comm):
+                self._all_gather()
+        else:
+            self._all_gather()
+        if p.rows_local:
+            if self.engine == "int8":
+                ops.split_digits(p.K, a_rows, p.rows_local, p.l, p.l, p.d, 0, self.a8, self.ga,
+                                 amax)
+            else:
+                ops.split(p.K, a_rows, p.rows_local, p.l, p.l, p.d, 0, self.sa, amax)
         if self.timing:
             ev[1].record()
-        self._all_gather()
         if self.pmax is not None:
             dist.all_reduce(self.pmax, op=dist.ReduceOp.MAX, group=self.group)
             mx = self.pmax.cpu().tolist()
             pairs = pruned_pairs(p.d, mx[0], mx[1], self.drop)
         else:
             pairs = triangular_pairs(p.d)
+        if comm is not None:
+            torch.cuda.current_stream().wait_stream(comm)
         if self.timing:
             ev[2].record()
         if p.rows_local:
@@ -251,6 +268,8 @@ class ShardedOzaki:
             ev[3].record()
             torch.cuda.current_stream().synchronize()
             if prof is not None:
+                # split = both splits; transfer = the part of the all-gather
+                # (+ maxima all-reduce) not hidden behind the A split
                 prof.split_seconds = ev[0].elapsed_time(ev[1]) * 1e-3
                 prof.transfer_seconds = ev[1].elapsed_time(ev[2]) * 1e-3
                 prof.product_seconds = ev[2].elapsed_time(ev[3]) * 1e-3

@@ -60,3 +60,41 @@ def test_sharded_ranks_on_device(ozk, world):
     assert not bad, bad
     engines = {r[1][2]: r[2] for r in results}
     assert engines[600] == "int8" and engines[100] == "dmma"  # keyed by l
+
+
+def _nccl_single(rank, port, q):
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1)
+    try:
+        import oracle
+        from paper_2301_09960_b200.sharded import ShardedOzaki
+        from paper_2301_09960_b200._lib import OzkProfile
+        cpu = oracle.best()
+        for (K, m, l, n, d, drop) in [(3, 64, 1030, 70, 9, 0.0), (2, 80, 600, 64, 8, 2.0 ** -80)]:
+            a = cpu.gen_eq1(K, m, l, 81 + m)
+            b = cpu.gen_eq1(K, l, n, 82 + m)
+            want = cpu.ozaki_gemm(K, a, b, d, drop)
+            eng = ShardedOzaki(K, m, l, n, d, 0, 1, drop_threshold=drop)
+            prof = OzkProfile()
+            for _ in range(2):  # the second run reuses the side stream and buffers
+                got = eng.run(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda(), prof)
+            ok = np.array_equal(got.cpu().numpy().view(np.uint64), want.view(np.uint64))
+            q.put((K, eng.engine, eng._comm is not None, bool(ok), prof.engine))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_sharded_nccl_side_stream_gather(ozk):
+    """The NCCL branch of ShardedOzaki.run (B all-gather + plane permute on a
+    side stream overlapping the A split), on a one-rank NCCL group."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    mp.spawn(_nccl_single, args=(_free_port(), q), nprocs=1, join=True)
+    res = [q.get() for _ in range(2)]
+    assert all(r[3] for r in res), res
+    assert all(r[2] for r in res), res  # the side stream was used
+    assert all(r[1] == "int8" and r[4] == 2 for r in res), res
