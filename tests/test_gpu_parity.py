@@ -528,3 +528,28 @@ def test_auto_split_count_matches_reference(ozk, cpu, K, m, l, n):
     assert prof.pairs < d * (d + 1) // 2  # pruning removed the sub-precision pairs
     if l == 8192 and K == 3:
         assert prof.pairs == 45
+
+
+@pytest.mark.parametrize("K,m,l,n,d", [(2, 70, 600, 65, 6), (3, 33, 700, 40, 9), (4, 20, 300, 31, 12)])
+def test_int8_unaligned_c(ozk, cpu, engine, K, m, l, n, d):
+    """C at an 8-byte (not 16-byte) aligned address: the INT8 epilogue's
+    per-word access path (no 16-byte vector loads/stores), bit-identical."""
+    import ctypes
+
+    import torch
+    engine("int8")
+    a = cpu.gen_eq1(K, m, l, 120 + K)
+    b = cpu.gen_eq1(K, l, n, 121 + K)
+    want = cpu.ozaki_gemm(K, a, b, d)
+    A = torch.from_numpy(a).cuda()
+    B = torch.from_numpy(b).cuda()
+    buf = torch.full((m * n * K + 1,), 7.0, dtype=torch.float64, device="cuda")
+    C = buf[1:]  # base + 8 bytes
+    assert C.data_ptr() % 16 == 8
+    from paper_2301_09960_b200._lib import OzkProfile, lib
+    prof = OzkProfile()
+    st = lib.ozk_ozaki_gemm_device(K, m, l, n, A.data_ptr(), B.data_ptr(), d, 0.0, C.data_ptr(),
+                                   torch.cuda.current_stream().cuda_stream, ctypes.byref(prof))
+    assert st == 0 and prof.engine == 2
+    assert_bitwise(C.view(m, n, K).cpu().numpy(), want, f"unaligned C K={K}")
+    assert buf[0].item() == 7.0  # nothing written before C
