@@ -102,7 +102,11 @@ struct I8Cfg {
     static constexpr int kThreads = (4 + 4 * EG) * 32;
     static constexpr int kEpiRows = TR / EG;  // C rows per epilogue thread
     // rows per K-word update step; two steps (ping-pong C buffers) per loop trip
+#ifdef OZK_I8_CHUNK
+    static constexpr int kChunk = OZK_I8_CHUNK;
+#else
     static constexpr int kChunk = (K == 2 && sizeof(W) == 8 && EG == 2) ? 4 : 2;
+#endif
     // register split between the producer/MMA warpgroup and the epilogue:
     // setmaxnreg.inc blocks until the registers released by the .dec are
     // available, so the epilogue may grow only by what the first warpgroup
