@@ -553,3 +553,20 @@ def test_int8_unaligned_c(ozk, cpu, engine, K, m, l, n, d):
     assert st == 0 and prof.engine == 2
     assert_bitwise(C.view(m, n, K).cpu().numpy(), want, f"unaligned C K={K}")
     assert buf[0].item() == 7.0  # nothing written before C
+
+
+@pytest.mark.parametrize("K,d,ulp,bound", [(2, 7, -106, 1.0), (3, 9, -159, 1.0), (4, 12, -212, 1.0)])
+def test_accuracy_t2_large_inner_dim(ozk, port, engine, K, d, ulp, bound):
+    """T2 at the headline inner dimension l = 8192 on the INT8 engine, at the
+    split counts where SURVEY Appendix A measured saturation (DD 7, TD 9, QD 12):
+    |C - C_exact| <= bound * u_L * (|A||B|)_ij on sampled rows (exact big-int
+    oracle).  The measured saturated errors there were 0.22 / 0.128 / 0.055."""
+    import oracle.exact as ex
+    engine("int8")
+    a = port.gen_eq1(K, 6, 8192, 17 + K)
+    b = port.gen_eq1(K, 8192, 5, 27 + K)
+    ref = ex.exact_gemm(a, b)
+    got, prof = ozk.ozaki_gemm(a, b, d)
+    assert prof.engine == "int8"
+    err = ex.componentwise_ulp_error(got, a, b, ref, ulp)
+    assert err <= bound, err
