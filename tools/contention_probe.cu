@@ -17,6 +17,7 @@ __device__ __forceinline__ uint64_t desc(uint32_t a) {
            (1ull << 46) | (2ull << 61);
 }
 
+template <int MN>
 __global__ void __launch_bounds__(544, 1) probe(int mma_on, int mma_iters, int dadd_iters,
                                                 unsigned long long* out, double seed) {
     extern __shared__ __align__(1024) uint8_t sm_raw[];
@@ -39,7 +40,7 @@ __global__ void __launch_bounds__(544, 1) probe(int mma_on, int mma_iters, int d
     if (warp == 0) {
         if (mma_on && lane == 0) {
             const uint32_t a = smem_u32(sm), b = a + 16384;
-            const uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((192u >> 3) << 17) | ((128u >> 4) << 24);
+            const uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(MN >> 3) << 17) | ((128u >> 4) << 24);
             for (int i = 0; i < mma_iters; ++i)
                 asm volatile("{ .reg .pred p; setp.ne.b32 p, %4, 0; tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p; }"
                              ::"r"(tmem), "l"(desc(a + (i & 3) * 32)), "l"(desc(b + (i & 3) * 32)), "r"(idesc), "r"(i));
@@ -72,22 +73,39 @@ __global__ void __launch_bounds__(544, 1) probe(int mma_on, int mma_iters, int d
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
 }
 
+template <int MN>
+void run(int sms, unsigned long long* out, int smem, int dadd_iters, int warps, int on);
+
 int main() {
     int sms;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     unsigned long long* out;
     cudaMalloc(&out, sizeof(unsigned long long) * sms * 32);
-    const int smem = 16384 + 24576 + 2048;  // A 128x128 B, B 192x128 B (+ align)
-    cudaFuncSetAttribute(probe, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    const int smem = 16384 + 32768 + 2048;  // A 128x128 B, B up to 256x128 B (+ align)
     const int dadd_iters = 200000;
-    for (int warps : {4, 8, 16}) {
-        for (int on = 0; on < 2; ++on) {
+    run<192>(sms, out, smem, dadd_iters, 16, 0);
+    for (int on = 1; on < 2; ++on)
+        for (int mn : {64, 128, 192, 256}) {
+            if (mn == 64) run<64>(sms, out, smem, dadd_iters, 16, on);
+            if (mn == 128) run<128>(sms, out, smem, dadd_iters, 16, on);
+            if (mn == 192) run<192>(sms, out, smem, dadd_iters, 16, on);
+            if (mn == 256) run<256>(sms, out, smem, dadd_iters, 16, on);
+        }
+    return 0;
+}
+
+template <int MN>
+void run(int sms, unsigned long long* out, int smem, int dadd_iters, int warps, int on) {
+    cudaFuncSetAttribute(probe<MN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    {
+        {
             cudaEvent_t e0, e1;
             cudaEventCreate(&e0);
             cudaEventCreate(&e1);
-            probe<<<sms, 32 * (1 + warps), smem>>>(on, 1, 1000, out, 1.5);  // warm
+            probe<MN><<<sms, 32 * (1 + warps), smem>>>(on, 1, 1000, out, 1.5);  // warm
             cudaEventRecord(e0);
-            probe<<<sms, 32 * (1 + warps), smem>>>(on, 60000, dadd_iters, out, 1.5);
+            // MMA count scaled so the MMA stream outlasts the DADD loop
+            probe<MN><<<sms, 32 * (1 + warps), smem>>>(on, 60000 * 256 / MN, dadd_iters, out, 1.5);
             cudaEventRecord(e1);
             cudaError_t err = cudaEventSynchronize(e1);
             float ms = 0;
@@ -98,10 +116,9 @@ int main() {
             for (int w = 1; w <= warps; ++w) cyc += (double)h[w];
             cyc /= warps;
             const double per = cyc / dadd_iters;  // cycles per iteration (kChains DADDs per warp)
-            printf("dadd warps %2d mma %s: %.2f clk per chain step (%d chains/warp) -> %.3f DADD warp-ops/clk/SM; kernel %.2f ms %s\n",
-                   warps, on ? "ON " : "off", per, kChains, warps * kChains / per, ms,
+            printf("dadd warps %2d mma %s N=%3d: %.2f clk per chain step (%d chains/warp) -> %.3f DADD warp-ops/clk/SM; kernel %.2f ms %s\n",
+                   warps, on ? "ON " : "off", MN, per, kChains, warps * kChains / per, ms,
                    err == cudaSuccess ? "" : cudaGetErrorString(err));
         }
     }
-    return 0;
 }
