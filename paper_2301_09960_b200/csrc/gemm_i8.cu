@@ -63,6 +63,12 @@ constexpr int kGroupM = OZK_I8_GROUPM;  // tile rows per rasterization group
 #ifndef OZK_I8_NB
 #define OZK_I8_NB 1
 #endif
+#ifndef OZK_I8_EPI_UNROLL
+#define OZK_I8_EPI_UNROLL 1
+#endif
+// trips of the K-word ping-pong loop unrolled (2: DD/TD/QD/TS 76.0/191.1/370.5/102.7
+// ms vs 73.2/189.8/362.2/101.0 with 1 -- more code, no more overlap)
+constexpr int kEpiUnroll = OZK_I8_EPI_UNROLL;
 #ifndef OZK_I8_TS_EG
 #define OZK_I8_TS_EG 4
 #endif
@@ -790,7 +796,7 @@ pair_gemm_i8_kernel(const __grid_constant__ MapsI8 maps, const __grid_constant__
                 };
                 W ca[kChunk][K], cb[kChunk][K];
                 load_chunk(0, ca);
-#pragma unroll 1
+#pragma unroll kEpiUnroll
                 for (int r = 0; r < kEpiRows; r += 2 * kChunk) {
                     load_chunk(r + kChunk, cb);  // in flight during the update of ca
                     update_chunk(r, ca);
