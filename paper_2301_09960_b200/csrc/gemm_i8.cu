@@ -14,29 +14,41 @@
 // DMMA) computes.  The K-word accumulation that follows is the same
 // kw_add<K> sequence in the same pair order.
 //
-// B200 mapping (one persistent CTA per SM, 12 warps).  The tile is transposed
-// with respect to C: the MMA's M side (128 TMEM lanes) runs over 128 C COLUMNS
-// (B-slice digits) and its N side over TR C rows per A-slice digit, so every
-// epilogue thread owns one C column and a warp's C accesses are row-contiguous
-// (a K-word row segment of 32 columns) instead of 32 rows apart.
-//   warp 0      TMA producer: per 128-deep k-block, the ND B-digit tiles (128 x 128
-//               int8) and the ND A-digit tiles (TR x 128 int8, adjacent in shared
-//               memory), 128-byte swizzle, mbarrier ring.
-//   warp 1      TMEM allocator + single-thread MMA issuer.  The ND A-digit tiles
-//               form ONE N = ND*TR operand, so MMA(Bdigit t, [A_0;...;A_ND-1])
-//               with its accumulator based at level block t lands the product of
-//               digits (t, u) in block t + u = its level: ND MMAs per 32-deep
-//               k-chunk instead of ND^2, and each operand tile is read ND times
-//               instead of ND^2.  The first k-chunk of a pair issues the ND^2
-//               single-digit products instead, each level's first one
-//               overwriting (blocks t+u > t are not yet initialised then).
-//   warps 4-11  two epilogue warpgroups, one per TR/2-row half of the tile (one
-//               TMEM lane = one C column per thread): tcgen05.ld the 2ND-1
-//               levels, recombine in int64, scale by 2^(gA + gB), release TMEM
-//               (the MMAs of the next pair start), then the K-word
-//               read-modify-write of the thread's column segment, C loads
-//               issued kAhead steps ahead.  setmaxnreg moves registers from the
-//               producer/MMA warpgroup (40) to the epilogue (232).
+// B200 mapping: one persistent CTA per SM, 4 + 4*EG warps (EG = 4 epilogue
+// warpgroups by default), 2-CTA clusters.  The tile is transposed with respect
+// to C: the MMA's M side (128 TMEM lanes) runs over 128 C COLUMNS (B-slice
+// digits) and its N side over TR (64) C rows per A-slice digit, so every
+// epilogue thread owns one C column and a warp's C accesses are a contiguous
+// K-word row segment instead of 32 rows apart.
+//   warp 0      TMA producer: per 128-deep k-block, the ND B-digit tiles (128 x
+//               128 int8) and the ND A-digit tiles (TR x 128, adjacent in shared
+//               memory), 128-byte swizzle, 3-stage mbarrier ring.  The two CTAs
+//               of a cluster own vertically adjacent tiles and share the B-digit
+//               tile: each loads half and multicasts it (.multicast::cluster).
+//               Wave pacing: a cluster starts (wave, pair) step s only after
+//               every cluster has started s-1 (global arrival counters, bounded
+//               spin), so all clusters stream the same slices and L2 holds them.
+//   warp 1      TMEM allocator + MMA issuer (whole warp, elect.sync issue,
+//               warp-uniform descriptors).  The ND A-digit tiles form ONE
+//               N = ND*TR operand, so MMA(Bdigit t, [A_0;...;A_ND-1]) with its
+//               accumulator based at level block t lands digit product (t, u) in
+//               block t + u = its level: ND MMAs per 32-deep k-chunk instead of
+//               ND^2.  The first k-chunk of a pair issues the ND^2 single-digit
+//               products instead, each level's first one overwriting.  A stage's
+//               commit arrives on the empty barriers of every CTA that
+//               multicasts into it.
+//   warps 4..   EG epilogue warpgroups, TR/EG rows each (one TMEM lane = one C
+//               column per thread): NB = 1 (default for binary64) drains the
+//               2ND-1 levels to registers, recombines them exactly (int64 ->
+//               binary64, scale by 2^(gA + gB)) and releases TMEM at once; NB = 2
+//               (TS) reads them in place from a double-buffered accumulator.
+//               Then the K-word read-modify-write of the thread's column
+//               segment, ping-pong C prefetch, 16-byte accesses.  setmaxnreg
+//               moves registers from the producer/MMA warpgroup (40) to the
+//               epilogue.
+// Diagnostic builds: -DOZK_I8_TRACE (cycle stamps, tools/i8_trace.py) and
+// -DOZK_I8_EPI_MODE=1..6 (timing-only variants with parts of the work removed;
+// wrong results by design).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
