@@ -54,7 +54,8 @@ inline GemmBackend backend() {
     };
 }
 
-// ozaki_gemm<K>: the slice products always run on the fused DMMA kernel; the
+// ozaki_gemm<K>: the slice products run on the B200 (exact INT8 tcgen05 digit
+// GEMMs where they apply, FP64 DMMA otherwise, fused with the accumulation); the
 // backend argument is accepted for signature compatibility (any conforming
 // backend yields the same C, test_ozaki.cpp:227-233).
 template <int K>

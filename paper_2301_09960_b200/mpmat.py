@@ -197,11 +197,12 @@ def ozaki_gemm(a, b, d: int, backend=None, drop_threshold: float = 0.0):
     """Long-precision product via the Ozaki split (ozaki.hpp:180-249).
 
     ``backend`` must be ``None`` or :func:`gpu_backend` -- the slice products
-    always run on the fused DMMA kernel (any conforming backend gives the same
+    run on the B200 (exact INT8 tcgen05 digit GEMMs where they apply, else FP64
+    DMMA, fused with the accumulation; any conforming backend gives the same
     C, test_ozaki.cpp:227-233).  Returns ``(C, OzakiProfile)``.
     """
     if backend is not None and not getattr(backend, "_ozk_gpu", False):
-        raise param_error("ozaki_gemm: only the B200 DMMA backend is supported")
+        raise param_error("ozaki_gemm: only the B200 backend (gpu_backend()) is supported")
     m, l, ka = _kword_shape(a)
     l2, n, kb = _kword_shape(b)
     if ka != kb:
