@@ -570,3 +570,81 @@ def test_accuracy_t2_large_inner_dim(ozk, port, engine, K, d, ulp, bound):
     assert prof.engine == "int8"
     err = ex.componentwise_ulp_error(got, a, b, ref, ulp)
     assert err <= bound, err
+
+
+def test_identity_product_truncation_bounds(ozk, cpu):
+    """test_ozaki.cpp:260-268: A * I is pure split truncation -- max relative
+    error <= 2^-35 at D=2 and <= 2^-100 at D=6 (exact big-int oracle)."""
+    import oracle.exact as ex
+    m = cpu.gen_eq1(2, 10, 10, 96)
+    eye = np.zeros((10, 10, 2))
+    eye[np.arange(10), np.arange(10), 0] = 1.0
+    ref = ex.exact_gemm(m, eye)
+    c2, _ = ozk.ozaki_gemm(m, eye, 2)
+    assert ex.max_rel_error(c2, ref) <= 2.0 ** -35
+    c6, _ = ozk.ozaki_gemm(m, eye, 6)
+    assert ex.max_rel_error(c6, ref) <= 2.0 ** -100
+
+
+def test_accuracy_monotone_in_d(ozk, cpu):
+    """test_ozaki.cpp:305-320: error non-increasing in D (15 % slack) from D=2,
+    and <= 1e-30 at D=8 for DD n=48."""
+    import oracle.exact as ex
+    a = cpu.gen_eq1(2, 48, 48, 99)
+    b = cpu.gen_eq1(2, 48, 48, 100)
+    ref = ex.exact_gemm(a, b)
+    prev = 1e300
+    for d in range(2, 9):
+        c, _ = ozk.ozaki_gemm(a, b, d)
+        err = ex.max_rel_error(c, ref)
+        assert err <= prev * 1.15, (d, err, prev)
+        prev = min(prev, err)
+    assert err <= 1e-30
+
+
+def test_profile_accounts_for_phases(ozk, cpu):
+    """test_ozaki.cpp:322-332: non-negative phase times summing to the total,
+    split count and pair count reported."""
+    a = cpu.gen_eq1(2, 32, 600, 101)
+    b = cpu.gen_eq1(2, 600, 32, 102)
+    for d in (4, 6):
+        _, prof = ozk.ozaki_gemm(a, b, d)
+        assert prof.split_seconds >= 0 and prof.product_seconds >= 0
+        assert prof.accumulate_seconds >= 0 and prof.split_count == d
+        assert prof.pairs == d * (d + 1) // 2
+        assert prof.total_seconds() > 0
+        fr = prof.split_fraction() + prof.product_fraction() + prof.accumulate_fraction()
+        assert abs(fr - 1.0) <= 1e-12
+
+
+def test_acceptance_9_ozaki_faster_than_direct(ozk):
+    """acceptance.cpp:467-485 analogue on the B200: Ozaki DD D=6 at n=1024 is at
+    least 1.5x faster than the direct K-word GEMM (gemm_simple) on the same
+    device, both device-resident."""
+    import ctypes
+
+    import torch
+
+    from paper_2301_09960_b200._lib import OzkProfile, lib
+    n = 1024
+    st = torch.cuda.current_stream().cuda_stream
+    A = torch.empty((n, n, 2), dtype=torch.float64, device="cuda")
+    B = torch.empty_like(A)
+    C = torch.empty_like(A)
+    lib.ozk_gen_eq1_device(2, n, n, 1, A.data_ptr(), st)
+    lib.ozk_gen_eq1_device(2, n, n, 2, B.data_ptr(), st)
+    prof = OzkProfile()
+
+    def timed(fn):
+        fn()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        fn()
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1)
+    t_oz = timed(lambda: lib.ozk_ozaki_gemm_device(2, n, n, n, A.data_ptr(), B.data_ptr(), 6,
+                                                   0.0, C.data_ptr(), st, ctypes.byref(prof)))
+    t_dir = timed(lambda: lib.ozk_direct_gemm_device(2, n, n, n, A.data_ptr(), B.data_ptr(),
+                                                     C.data_ptr(), st))
+    assert t_dir >= 1.5 * t_oz, (t_oz, t_dir)
