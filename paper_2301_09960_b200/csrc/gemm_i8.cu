@@ -85,10 +85,10 @@ constexpr int kGroupM = OZK_I8_GROUPM;  // tile rows per rasterization group
 // ms vs 73.2/189.8/362.2/101.0 with 1 -- more code, no more overlap)
 constexpr int kEpiUnroll = OZK_I8_EPI_UNROLL;
 #ifndef OZK_I8_TS_EG
-#define OZK_I8_TS_EG 4
+#define OZK_I8_TS_EG 7
 #endif
 #ifndef OZK_I8_TS_TR
-#define OZK_I8_TS_TR 128
+#define OZK_I8_TS_TR 112
 #endif
 #ifndef OZK_I8_PACE
 #define OZK_I8_PACE 1
@@ -958,7 +958,7 @@ cudaError_t launch_pair_gemm_i8(int K, int word_bytes, const I8Operands& op,
         if (op.nd == 1)
             return launch_i8_typed<3, float, 1, OZK_I8_TS_TR, OZK_I8_TS_EG, OZK_I8_CM, OZK_I8_CN>(op, pairs, st, num_sms);
         if (op.nd == 2)
-            return launch_i8_typed<3, float, 2, 64, OZK_I8_TS_EG, OZK_I8_CM, OZK_I8_CN>(op, pairs, st, num_sms);
+            return launch_i8_typed<3, float, 2, 64, 4, OZK_I8_CM, OZK_I8_CN>(op, pairs, st, num_sms);
         return cudaErrorInvalidValue;
     }
     if (op.nd != 3) return cudaErrorInvalidValue;
