@@ -14,12 +14,12 @@
 // DMMA) computes.  The K-word accumulation that follows is the same
 // kw_add<K> sequence in the same pair order.
 //
-// B200 mapping: one persistent CTA per SM, 4 + 4*EG warps (EG = 4 epilogue
-// warpgroups by default), 2-CTA clusters.  The tile is transposed with respect
+// B200 mapping: one persistent CTA per SM, 4 + 4*EG warps (EG epilogue
+// warpgroups: DD 4, TD/QD 6, TS 7), 2-CTA clusters.  The tile is transposed with respect
 // to C: the MMA's M side (128 TMEM lanes) runs over 128 C COLUMNS (B-slice
-// digits) and its N side over TR (64) C rows per A-slice digit, so every
-// epilogue thread owns one C column and a warp's C accesses are a contiguous
-// K-word row segment instead of 32 rows apart.
+// digits) and its N side over TR (DD 64, TD/QD 48, TS 112) C rows per A-slice
+// digit, so every epilogue thread owns one C column and a warp's C accesses
+// are a contiguous K-word row segment instead of 32 rows apart.
 //   warp 0      TMA producer: per 128-deep k-block, the ND B-digit tiles (128 x
 //               128 int8) and the ND A-digit tiles (TR x 128, adjacent in shared
 //               memory), 128-byte swizzle, 3-stage mbarrier ring.  The two CTAs
@@ -38,10 +38,10 @@
 //               commit arrives on the empty barriers of every CTA that
 //               multicasts into it.
 //   warps 4..   EG epilogue warpgroups, TR/EG rows each (one TMEM lane = one C
-//               column per thread): NB = 1 (default for binary64) drains the
-//               2ND-1 levels to registers, recombines them exactly (int64 ->
-//               binary64, scale by 2^(gA + gB)) and releases TMEM at once; NB = 2
-//               (TS) reads them in place from a double-buffered accumulator.
+//               column per thread): NB = 1 (DD) drains the 2ND-1 levels to
+//               registers, recombines them exactly (int64 -> binary64, scale by
+//               2^(gA + gB)) and releases TMEM at once; NB = 2 (TD/QD/TS) reads
+//               them in place from a double-buffered accumulator.
 //               Then the K-word read-modify-write of the thread's column
 //               segment, ping-pong C prefetch, 16-byte accesses.  setmaxnreg
 //               moves registers from the producer/MMA warpgroup (40) to the
@@ -63,20 +63,31 @@ constexpr int TC = 128, BKB = 128;            // tile C columns (MMA M), k bytes
 #define OZK_I8_GROUPM 8
 #endif
 constexpr int kGroupM = OZK_I8_GROUPM;  // tile rows per rasterization group
+// binary64 TD/QD: 6 epilogue warpgroups over 48-row tiles, levels read in place
+// from 2 TMEM buffers (TD/QD slice GEMM 178-180 / 339 ms vs 188 / 361 with the
+// DD shape below; their epilogue is FP64-bound, more warps hide more latency)
 #ifndef OZK_I8_EG
-#define OZK_I8_EG 4
+#define OZK_I8_EG 6
 #endif
 #ifndef OZK_I8_CM
 #define OZK_I8_CM 2
 #endif
 #ifndef OZK_I8_TR
-#define OZK_I8_TR 64
-#endif
-#ifndef OZK_I8_TR_DD
-#define OZK_I8_TR_DD OZK_I8_TR  // DD alone (80 measured equal to 64: 72.5-73.6 vs 72.6-72.8 ms)
+#define OZK_I8_TR 48
 #endif
 #ifndef OZK_I8_NB
-#define OZK_I8_NB 1
+#define OZK_I8_NB 2
+#endif
+// DD: 4 warpgroups over 64-row tiles in drain mode (73.6 ms vs 78.1 with the
+// TD/QD shape: DD is operand-traffic bound, the larger tile wins; TR 80 = 64)
+#ifndef OZK_I8_DD_EG
+#define OZK_I8_DD_EG 4
+#endif
+#ifndef OZK_I8_DD_TR
+#define OZK_I8_DD_TR 64
+#endif
+#ifndef OZK_I8_DD_NB
+#define OZK_I8_DD_NB 1
 #endif
 #ifndef OZK_I8_EPI_UNROLL
 #define OZK_I8_EPI_UNROLL 1
@@ -963,7 +974,7 @@ cudaError_t launch_pair_gemm_i8(int K, int word_bytes, const I8Operands& op,
     }
     if (op.nd != 3) return cudaErrorInvalidValue;
     switch (K) {
-    case 2: return launch_i8_typed<2, double, 3, OZK_I8_TR_DD, OZK_I8_EG, OZK_I8_CM, OZK_I8_CN, OZK_I8_NB>(op, pairs, st, num_sms);
+    case 2: return launch_i8_typed<2, double, 3, OZK_I8_DD_TR, OZK_I8_DD_EG, OZK_I8_CM, OZK_I8_CN, OZK_I8_DD_NB>(op, pairs, st, num_sms);
     case 3: return launch_i8_typed<3, double, 3, OZK_I8_TR, OZK_I8_EG, OZK_I8_CM, OZK_I8_CN, OZK_I8_NB>(op, pairs, st, num_sms);
     case 4: return launch_i8_typed<4, double, 3, OZK_I8_TR, OZK_I8_EG, OZK_I8_CM, OZK_I8_CN, OZK_I8_NB>(op, pairs, st, num_sms);
     default: return cudaErrorInvalidValue;
