@@ -226,6 +226,15 @@ struct HostOverlap {
     // before its GEMM (not with drop_threshold > 0: the pair list needs every
     // slice maximum first)
     const cudaEvent_t* a_ready = nullptr;
+    // optional (INT8 engine, with a_ready): B arrives in b_blocks column blocks
+    // of b_block_cols columns (b_block_ready[j]); each block is split as it
+    // lands and the first A band is multiplied block by block, so the GEMM
+    // starts after one A band and one B block instead of all of B.  Columns
+    // are split independently (per-column maxima, ozaki.hpp:102-103) and C
+    // elements are independent, so this does not change a bit either.
+    int b_blocks = 1;
+    size_t b_block_cols = 0;
+    const cudaEvent_t* b_block_ready = nullptr;
 };
 
 // C = A * B via the Ozaki scheme on device buffers; A has row stride lda, B
@@ -283,6 +292,7 @@ ozk_status ozaki_device_impl(int fmt, size_t m, size_t l, size_t n, const void* 
     Timer tm(prof != nullptr);
     tm.mark(0, st);
     const bool banded_a = ov && ov->a_ready && !want_max && ov->bands > 1;
+    const bool blocked_b = banded_a && use_i8 && ov->b_block_ready && ov->b_blocks > 1;
     if (!banded_a) {
         if (ov && ov->a_ready)
             for (int q = 0; q < ov->bands; ++q)
@@ -291,10 +301,13 @@ ozk_status ozaki_device_impl(int fmt, size_t m, size_t l, size_t n, const void* 
                                  want_max ? amax : nullptr, err, st, digA),
                  "ozaki_gemm: split A");
     }
-    if (ov && ov->b_ready) OZK_CUDA(cudaStreamWaitEvent(st, ov->b_ready, 0), "ozaki_gemm: wait B");
-    OZK_CUDA(split_to_slices(fmt, l, n, ldb, b, d, OZK_SIDE_COLS, sb.as<double>(), n, work.p,
-                             want_max ? bmax : nullptr, err, st, digB),
-             "ozaki_gemm: split B");
+    if (!blocked_b) {
+        if (ov && ov->b_ready)
+            OZK_CUDA(cudaStreamWaitEvent(st, ov->b_ready, 0), "ozaki_gemm: wait B");
+        OZK_CUDA(split_to_slices(fmt, l, n, ldb, b, d, OZK_SIDE_COLS, sb.as<double>(), n, work.p,
+                                 want_max ? bmax : nullptr, err, st, digB),
+                 "ozaki_gemm: split B");
+    }
     tm.mark(1, st);
 
     PairList pl;
@@ -332,7 +345,7 @@ ozk_status ozaki_device_impl(int fmt, size_t m, size_t l, size_t n, const void* 
     const int bands = (ov && ov->bands > 1 && (pl.count > 0 || banded_a)) ? ov->bands : 1;
     const size_t band_rows = (m + bands - 1) / bands;
     const size_t eb = elem_bytes(fmt);
-    std::vector<std::unique_ptr<Timer>> split_a_timers;  // per-band A splits (profile)
+    std::vector<std::unique_ptr<Timer>> split_timers;  // per-band A / per-block B splits (profile)
     int band = 0;
     for (size_t r0 = 0; r0 < m; r0 += band_rows, ++band) {
         const size_t rows = m - r0 < band_rows ? m - r0 : band_rows;
@@ -346,39 +359,64 @@ ozk_status ozaki_device_impl(int fmt, size_t m, size_t l, size_t n, const void* 
                 dband.digits += r0 * ld8;
                 dband.exps += r0;
             }
-            split_a_timers.push_back(std::make_unique<Timer>(prof != nullptr));
-            split_a_timers.back()->mark(0, st);
+            split_timers.push_back(std::make_unique<Timer>(prof != nullptr));
+            split_timers.back()->mark(0, st);
             OZK_CUDA(split_to_slices(fmt, rows, l, lda,
                                      static_cast<const char*>(a) + r0 * lda * eb, d,
                                      OZK_SIDE_ROWS, use_i8 ? nullptr : sa.as<double>() + r0 * ldk,
                                      m, work.p, nullptr, err, st, dband),
                      "ozaki_gemm: split A band");
-            split_a_timers.back()->mark(1, st);
+            split_timers.back()->mark(1, st);
         }
         if (pl.count == 0) {  // every pair pruned (drop_threshold > 1): C = 0
             OZK_CUDA(cudaMemsetAsync(cb, 0, eb * rows * n, st), "ozaki_gemm: zero C");
         } else if (use_i8) {
-            I8Operands op{};
-            op.nd = nd;
-            op.a = da8.as<int8_t>() + r0 * ld8;
-            op.a_ld = ld8;
-            op.a_digit_stride = m * ld8;
-            op.a_slice_stride = (size_t)nd * m * ld8;
-            op.b = db8.as<int8_t>();
-            op.b_ld = ld8;
-            op.b_digit_stride = n * ld8;
-            op.b_slice_stride = (size_t)nd * n * ld8;
-            op.gA = ga.as<int>() + r0;
-            op.gB = gb.as<int>();
-            op.gA_stride = m;
-            op.gB_stride = n;
-            op.m = rows;
-            op.n = n;
-            op.l = l;
-            op.d = d;
-            op.c = cb;
-            op.ldc = n;
-            OZK_CUDA(launch_pair_gemm_i8(K, wb, op, pl, st, sms), "ozaki_gemm: INT8 slice GEMM");
+            // C rows [r0, r0+rows) x columns [c0, c0+w)
+            auto gemm_cols = [&](size_t c0, size_t w) -> cudaError_t {
+                I8Operands op{};
+                op.nd = nd;
+                op.a = da8.as<int8_t>() + r0 * ld8;
+                op.a_ld = ld8;
+                op.a_digit_stride = m * ld8;
+                op.a_slice_stride = (size_t)nd * m * ld8;
+                op.b = db8.as<int8_t>() + c0 * ld8;
+                op.b_ld = ld8;
+                op.b_digit_stride = n * ld8;
+                op.b_slice_stride = (size_t)nd * n * ld8;
+                op.gA = ga.as<int>() + r0;
+                op.gB = gb.as<int>() + c0;
+                op.gA_stride = m;
+                op.gB_stride = n;
+                op.m = rows;
+                op.n = w;
+                op.l = l;
+                op.d = d;
+                op.c = cb + c0 * eb;
+                op.ldc = n;
+                return launch_pair_gemm_i8(K, wb, op, pl, st, sms);
+            };
+            if (blocked_b && band == 0) {
+                // B column blocks: split each as it lands, then its GEMM block
+                for (int j = 0; j < ov->b_blocks; ++j) {
+                    const size_t c0 = (size_t)j * ov->b_block_cols;
+                    if (c0 >= n) break;
+                    const size_t w = n - c0 < ov->b_block_cols ? n - c0 : ov->b_block_cols;
+                    OZK_CUDA(cudaStreamWaitEvent(st, ov->b_block_ready[j], 0), "ozaki_gemm: wait B");
+                    DigitOut dblk = digB;
+                    dblk.digits += c0 * ld8;
+                    dblk.exps += c0;
+                    split_timers.push_back(std::make_unique<Timer>(prof != nullptr));
+                    split_timers.back()->mark(0, st);
+                    OZK_CUDA(split_to_slices(fmt, l, w, ldb, static_cast<const char*>(b) + c0 * eb,
+                                             d, OZK_SIDE_COLS, nullptr, n, work.p, nullptr, err,
+                                             st, dblk),
+                             "ozaki_gemm: split B block");
+                    split_timers.back()->mark(1, st);
+                    OZK_CUDA(gemm_cols(c0, w), "ozaki_gemm: INT8 slice GEMM");
+                }
+            } else {
+                OZK_CUDA(gemm_cols(0, n), "ozaki_gemm: INT8 slice GEMM");
+            }
         } else {
             GemmProblem pb = prob;
             pb.a = prob.a + r0 * ldk;
@@ -396,10 +434,10 @@ ozk_status ozaki_device_impl(int fmt, size_t m, size_t l, size_t n, const void* 
     OZK_CUDA(cudaStreamSynchronize(st), "ozaki_gemm");
     if (ozk_status s = check_dev_err(flag, "split_matrix")) return s;
     if (prof) {
-        double split_a_banded = 0.0;
-        for (const auto& t : split_a_timers) split_a_banded += t->secs(0, 1);
-        prof->split_seconds = tm.secs(0, 1) + split_a_banded;
-        prof->product_seconds = tm.secs(1, 2) - split_a_banded;
+        double split_banded = 0.0;
+        for (const auto& t : split_timers) split_banded += t->secs(0, 1);
+        prof->split_seconds = tm.secs(0, 1) + split_banded;
+        prof->product_seconds = tm.secs(1, 2) - split_banded;
         prof->accumulate_seconds = 0.0;
         prof->total_seconds = prof->split_seconds + prof->product_seconds;
         prof->split_count = d;
@@ -480,7 +518,16 @@ ozk_status ozk_ozaki_gemm(ozk_format fmt, size_t m, size_t l, size_t n, const vo
     OZK_CUDA(cudaEventCreateWithFlags(&allocated, cudaEventDisableTiming), "ozaki_gemm: event");
     OZK_CUDA(cudaEventCreateWithFlags(&b_ready, cudaEventDisableTiming), "ozaki_gemm: event");
     const int bands = m >= 2048 ? 8 : 1;
-    std::vector<cudaEvent_t> band_done(bands, nullptr), a_ready(bands, nullptr);
+    // B in column blocks of >= 2048 columns (whole 128-column tiles) when the
+    // first band can be multiplied block by block (INT8 engine, no pruning):
+    // 4 blocks at n = 8192 balance the per-block H2D time against the GEMM
+    // blocks' tile quantisation
+    const bool blockable = bands > 1 && drop == 0.0 && engine_setting() != OZK_ENGINE_DMMA &&
+                           int8_applicable((int)fmt, l, d) && n >= 4096;
+    const size_t b_block_cols = blockable ? (((n + 3) / 4 + 127) / 128) * 128 : n;
+    const int b_blocks = (int)((n + b_block_cols - 1) / b_block_cols);
+    std::vector<cudaEvent_t> band_done(bands, nullptr), a_ready(bands, nullptr),
+        b_block_ready(b_blocks, nullptr);
     struct EventGuard {
         std::vector<cudaEvent_t*> evs;
         ~EventGuard() {
@@ -489,7 +536,7 @@ ozk_status ozk_ozaki_gemm(ozk_format fmt, size_t m, size_t l, size_t n, const vo
         }
     } guard;
     guard.evs = {&allocated, &b_ready};
-    for (auto* vec : {&band_done, &a_ready})
+    for (auto* vec : {&band_done, &a_ready, &b_block_ready})
         for (auto& e : *vec) {
             OZK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "ozaki_gemm: event");
             guard.evs.push_back(&e);
@@ -497,23 +544,46 @@ ozk_status ozk_ozaki_gemm(ozk_format fmt, size_t m, size_t l, size_t n, const vo
     OZK_CUDA(cudaEventRecord(allocated, os.s), "ozaki_gemm: event");
     OZK_CUDA(cudaStreamWaitEvent(xs.s, allocated, 0), "ozaki_gemm: wait");
     OZK_CUDA(cudaStreamWaitEvent(ys.s, allocated, 0), "ozaki_gemm: wait");
-    // B first (its split gates every band), then A band by band
-    OZK_CUDA(cudaMemcpyAsync(db.p, b, eb * l * n, cudaMemcpyHostToDevice, xs.s), "ozaki_gemm: H2D B");
-    OZK_CUDA(cudaEventRecord(b_ready, xs.s), "ozaki_gemm: event");
+    // Copy order on the H2D stream.  Whole B: B (its split gates every band),
+    // then A band by band.  B in column blocks: A band 0, then the B blocks
+    // (strided copies of the row-major B), then the other A bands.
     const size_t band_rows = (m + bands - 1) / bands;
-    for (int q = 0; q < bands; ++q) {
+    auto copy_a_band = [&](int q) -> cudaError_t {
         const size_t r0 = q * band_rows, rows = r0 < m ? (m - r0 < band_rows ? m - r0 : band_rows) : 0;
+        cudaError_t e = cudaSuccess;
         if (rows)
-            OZK_CUDA(cudaMemcpyAsync(static_cast<char*>(da.p) + r0 * l * eb,
-                                     static_cast<const char*>(a) + r0 * l * eb, rows * l * eb,
-                                     cudaMemcpyHostToDevice, xs.s),
-                     "ozaki_gemm: H2D A");
-        OZK_CUDA(cudaEventRecord(a_ready[q], xs.s), "ozaki_gemm: event");
+            e = cudaMemcpyAsync(static_cast<char*>(da.p) + r0 * l * eb,
+                                static_cast<const char*>(a) + r0 * l * eb, rows * l * eb,
+                                cudaMemcpyHostToDevice, xs.s);
+        if (e == cudaSuccess) e = cudaEventRecord(a_ready[q], xs.s);
+        return e;
+    };
+    if (b_blocks > 1) {
+        OZK_CUDA(copy_a_band(0), "ozaki_gemm: H2D A");
+        for (int j = 0; j < b_blocks; ++j) {
+            const size_t c0 = (size_t)j * b_block_cols;
+            const size_t w = n - c0 < b_block_cols ? n - c0 : b_block_cols;
+            OZK_CUDA(cudaMemcpy2DAsync(static_cast<char*>(db.p) + c0 * eb, n * eb,
+                                       static_cast<const char*>(b) + c0 * eb, n * eb, w * eb, l,
+                                       cudaMemcpyHostToDevice, xs.s),
+                     "ozaki_gemm: H2D B block");
+            OZK_CUDA(cudaEventRecord(b_block_ready[j], xs.s), "ozaki_gemm: event");
+        }
+    } else {
+        OZK_CUDA(cudaMemcpyAsync(db.p, b, eb * l * n, cudaMemcpyHostToDevice, xs.s),
+                 "ozaki_gemm: H2D B");
     }
+    OZK_CUDA(cudaEventRecord(b_ready, xs.s), "ozaki_gemm: event");
+    for (int q = b_blocks > 1 ? 1 : 0; q < bands; ++q) OZK_CUDA(copy_a_band(q), "ozaki_gemm: H2D A");
     HostOverlap ov;
     ov.b_ready = b_ready;
     ov.bands = bands;
     ov.a_ready = a_ready.data();
+    if (b_blocks > 1) {
+        ov.b_blocks = b_blocks;
+        ov.b_block_cols = b_block_cols;
+        ov.b_block_ready = b_block_ready.data();
+    }
     int band = 0;
     ov.on_band = [&](size_t r0, size_t r1) -> cudaError_t {
         cudaEvent_t ev = band_done[band < bands ? band : bands - 1];

@@ -500,11 +500,16 @@ def test_direct_gemm_spread_inputs(ozk, ref, port):
 
 
 @pytest.mark.parametrize("K,m,l,n,d,drop", [(2, 2049, 600, 70, 6, 0.0), (3, 2048, 300, 64, 9, 2.0 ** -90),
-                                            (4, 2100, 130, 40, 12, 0.0), (2, 4097, 100, 33, 6, 0.0)])
+                                            (4, 2100, 130, 40, 12, 0.0), (2, 4097, 100, 33, 6, 0.0),
+                                            (3, 2048, 140, 4101, 3, 0.0), (2, 2050, 300, 4352, 4, 0.0),
+                                            (4, 2048, 129, 4096, 2, 0.0), (2, 2048, 200, 4100, 3, 2.0 ** -60)])
 def test_host_api_banded_overlap(ozk, cpu, K, m, l, n, d, drop):
     """ozk_ozaki_gemm with host buffers at m >= 2048 runs the banded, transfer-
     overlapped schedule (B first, A + slice GEMM in 8 row bands, C copied back
-    per band; drop > 0 keeps the whole-matrix A split): bit-identical."""
+    per band; drop > 0 keeps the whole-matrix A split); at n >= 4096 on the INT8
+    engine B also arrives in 4 column blocks, each split as it lands, and the
+    first band is multiplied block by block (ragged last block included):
+    bit-identical."""
     a = cpu.gen_eq1(K, m, l, 90 + K)
     b = cpu.gen_eq1(K, l, n, 91 + K)
     want = cpu.ozaki_gemm(K, a, b, d, drop)
