@@ -11,9 +11,9 @@
 // transpose) and runs all D extraction passes on it, so the D dependent
 // row-max reductions are CTA-local (warp shuffles + one smem hop) and never
 // touch the grid.  The K-word residual is swept once per pass through the
-// `work` buffer; a row is at most l*K*8 bytes (256 KiB for QD at l=8192), so
-// the per-pass re-reads stay in L2 and HBM sees ~one read of the input plus
-// one write per slice.  Slices are written k-contiguous with a 16-byte padded
+// `work` buffer; a row is at most l*K*8 bytes (256 KiB for QD at l=8192), and
+// 512-thread CTAs keep ~2 resident rows per SM, so the per-pass re-reads mostly
+// stay in L2.  Slices are written k-contiguous with a 16-byte padded
 // leading dimension, which is the operand layout the DMMA GEMM's TMA loads.
 #include "kword.cuh"
 #include "ozk_internal.cuh"
@@ -21,7 +21,11 @@
 namespace ozk {
 namespace {
 
-constexpr int kSplitThreads = 256;
+#ifndef OZK_SPLIT_THREADS
+#define OZK_SPLIT_THREADS 512  // 256: DD 7.0 / TD 18.8 ms; 512: 5.9 / 18.4 (residuals of the
+                                 // resident rows fit L2); 1024: 6.3 / 21.0
+#endif
+constexpr int kSplitThreads = OZK_SPLIT_THREADS;
 
 __device__ __forceinline__ int ceil_log2(double x) {
     int e = ilogb(x);
@@ -170,36 +174,41 @@ split_rows_kernel(const T* __restrict__ in, size_t in_ld, T* __restrict__ work, 
         const bool g_normal = -g >= -1022 && -g <= 1023;
         const double inv_grid = g_normal ? __longlong_as_double((long long)(1023 - g) << 52) : 0.0;
         if (dig.digits && threadIdx.x == 0) dig.exps[(size_t)a * dig.exp_stride + r] = g;
-        for (size_t j = threadIdx.x; j < cols; j += kSplitThreads) {
-            if (tau == T(0)) {
+        if (tau == T(0)) {  // block-uniform
+            for (size_t j = threadIdx.x; j < cols; j += kSplitThreads) {
                 if (pa) pa[j] = 0.0;
                 if (drow)
                     for (int q = 0; q < dig.nd; ++q) drow[j + q * dig.digit_stride] = 0;
-                continue;
             }
-            T c[K];
-            load_kw<K>(w + j * K, c);
-            // shift_extract: (v + tau) - tau, strictly rounded (ozaki.hpp:53-56)
-            const T x = rn_sub(rn_add(c[0], tau), tau);
-            if (pa) pa[j] = (double)x;
-            if (drow) {
-                // exact integer; |mi| fits nd digits by the planner's choice of nd
-                int mi = g_normal ? (int)((double)x * inv_grid) : (int)scalbn((double)x, -g);
-                for (int q = 0; q < dig.nd - 1; ++q) {
-                    const int dq = (int)(int8_t)(mi & 0xff);
-                    drow[j + q * dig.digit_stride] = (int8_t)dq;
-                    mi = (mi - dq) >> 8;
+        } else {
+            auto element = [&](size_t j) {
+                T c[K];
+                load_kw<K>(w + j * K, c);
+                // shift_extract: (v + tau) - tau, strictly rounded (ozaki.hpp:53-56)
+                const T x = rn_sub(rn_add(c[0], tau), tau);
+                if (pa) pa[j] = (double)x;
+                if (drow) {
+                    // exact integer; |mi| fits nd digits by the planner's choice of nd
+                    int mi = g_normal ? (int)((double)x * inv_grid) : (int)scalbn((double)x, -g);
+                    for (int q = 0; q < dig.nd - 1; ++q) {
+                        const int dq = (int)(int8_t)(mi & 0xff);
+                        drow[j + q * dig.digit_stride] = (int8_t)dq;
+                        mi = (mi - dq) >> 8;
+                    }
+                    drow[j + (dig.nd - 1) * dig.digit_stride] = (int8_t)mi;
                 }
-                drow[j + (dig.nd - 1) * dig.digit_stride] = (int8_t)mi;
-            }
-            if (x != T(0)) {
-                // w -= x  ==  w + (-x)  (multifloat.hpp:302,391); FP64 compares:
-                // this kernel is ALU-bound, its FP64 pipe mostly idle
-                kw_add<K, T, false>(c, -x);
-                store_kw<K>(w + j * K, c);
-            }
-            nmx = fmax(nmx, fabs_(c[0]));
-            pmx = fmax(pmx, (double)fabs_(x));
+                if (x != T(0)) {
+                    // w -= x  ==  w + (-x)  (multifloat.hpp:302,391); FP64 compares:
+                    // this kernel is ALU-bound, its FP64 pipe mostly idle
+                    kw_add<K, T, false>(c, -x);
+                    store_kw<K>(w + j * K, c);
+                }
+                nmx = fmax(nmx, fabs_(c[0]));
+                pmx = fmax(pmx, (double)fabs_(x));
+            };
+            // one element per trip: two interleaved per thread measured slower
+            // (TD 18.4 -> 22.1 ms, register pressure at 512 threads)
+            for (size_t j = threadIdx.x; j < cols; j += kSplitThreads) element(j);
         }
         if (pa)
             for (size_t j = cols + threadIdx.x; j < ldk; j += kSplitThreads) pa[j] = 0.0;
