@@ -16,7 +16,11 @@
 #include <string>
 #include <functional>
 #include <memory>
+#include <algorithm>
 #include <vector>
+#include <cstdint>
+#include <tuple>
+#include <map>
 
 #include "../../include/ozk.h"
 #include "ozk_internal.cuh"
@@ -212,6 +216,154 @@ struct Timer {
     }
 };
 
+// Row bands of the host-buffer schedule (ozk_ozaki_gemm), as row starts
+// [0, r_1, ..., m].  Each band is one slice-GEMM launch whose persistent
+// clusters take one cluster tile per wave, so a band of R cluster rows over T
+// cluster columns costs ceil(R*T / clusters) waves: bands whose tile counts sit
+// just below a multiple of the cluster count waste nothing, others up to a
+// wave each.  Band 0 (about m/8; the GEMM waits for it and for B) is sized for
+// the best wave fill of its B column blocks.  The rest is chosen by a DP from
+// the end: minimise GEMM waves x t_wave + the last band's C copy, with each
+// band's C copy no longer than the next band's GEMM (so copies stay hidden);
+// band sizes come from the sizes with >= 90 % wave fill (and 1..4 rows), and
+// each band's A rows must cross PCIe during the previous band's GEMM (band 1's
+// during band 0's last column block: A follows all of B on the copy stream).
+// t_wave: one cluster tile's work at the measured per-SM INT8 rate of the
+// format (bench_r01_f2: DD 19, TD 16.5, QD 15, TS 9.5 Tops/s per SM).
+struct BandKey {
+    size_t m, n, l, block_cols;
+    int fmt, d, rows, cols, clusters;
+    bool operator<(const BandKey& o) const {
+        return std::tie(m, n, l, block_cols, fmt, d, rows, cols, clusters) <
+               std::tie(o.m, o.n, o.l, o.block_cols, o.fmt, o.d, o.rows, o.cols, o.clusters);
+    }
+};
+
+std::vector<size_t> plan_bands_uncached(int fmt, size_t m, size_t n, size_t l, int d,
+                                        size_t block_cols, const I8Geometry& g) {
+    std::vector<size_t> starts{0};
+    const size_t rtot = g.group_rows > 0 ? (m + g.group_rows - 1) / g.group_rows : 0;
+    if (m < 2048 || g.clusters <= 0 || rtot < 8) {
+        starts.push_back(m);
+        return starts;
+    }
+    if (rtot > 512) {  // quantisation loss per band < 1 %: 8 equal bands
+        for (size_t q = 1; q <= 8; ++q) starts.push_back(m * q / 8);
+        return starts;
+    }
+    const size_t C = (size_t)g.clusters;
+    const size_t T = (n + g.group_cols - 1) / g.group_cols;
+    const size_t Tb = (block_cols + g.group_cols - 1) / g.group_cols;
+    auto waves = [&](size_t r, size_t t) { return (r * t + C - 1) / C; };
+    auto fill = [&](size_t r, size_t t) { return double(r * t) / double(waves(r, t) * C); };
+    // band 0: best fill of its column blocks within [rtot/12, rtot/6]
+    size_t r0 = 1;
+    {
+        const size_t lo = rtot / 12 > 0 ? rtot / 12 : 1, hi = rtot / 6 > lo ? rtot / 6 : lo;
+        double best = -1.0;
+        for (size_t r = lo; r <= hi; ++r)  // ties go to the larger band
+            if (fill(r, Tb) >= best - 1e-9) {
+                best = fill(r, Tb) > best ? fill(r, Tb) : best;
+                r0 = r;
+            }
+    }
+    const size_t rest = rtot - r0;
+    const int K = words_of(fmt), wb = word_bytes_of(fmt);
+    const int nd = int8_digits(fmt, l, d);
+    const double rate_sm = wb == 4 ? 9.5e12 : (K == 2 ? 19e12 : (K == 3 ? 16.5e12 : 15e12));
+    const double pairs = 0.5 * d * (d + 1);
+    const double t_wave = pairs * nd * nd * 2.0 * g.group_rows * g.group_cols * (double)l /
+                          (rate_sm * g.cluster_sms);
+    const double t_row_d2h = (double)g.group_rows * (double)n * elem_bytes(fmt) / 45e9;
+    const double t_row_h2d = (double)g.group_rows * (double)l * elem_bytes(fmt) / 45e9;
+    std::vector<size_t> cand;
+    for (size_t r = 1; r <= rest; ++r)
+        if (r <= 4 || fill(r, T) >= 0.9) cand.push_back(r);
+    const size_t nc = cand.size();
+    constexpr int kMaxBands = 7;  // after band 0
+    const double inf = 1e30;
+    auto idx = [&](int jj, size_t x, size_t c) { return ((size_t)jj * (rest + 1) + x) * nc + c; };
+    std::vector<double> best;
+    std::vector<size_t> from;
+    double bv = inf;
+    int bj = 0;
+    size_t bc = 0;
+    // the A-arrival constraints are dropped when nothing satisfies them (small
+    // GEMMs whose A bands take longer to copy than to multiply)
+    for (int pass = 0; pass < 2 && bj == 0; ++pass) {
+        const bool arrive = pass == 0;
+        // best[j][x][c]: cost of covering the last x cluster rows with j bands
+        // whose earliest band has size cand[c]
+        best.assign((size_t)(kMaxBands + 1) * (rest + 1) * nc, inf);
+        from.assign(best.size(), SIZE_MAX);
+        for (size_t c = 0; c < nc; ++c)
+            best[idx(1, cand[c], c)] = waves(cand[c], T) * t_wave + cand[c] * t_row_d2h;
+        for (int jj = 1; jj < kMaxBands; ++jj)
+            for (size_t x = 1; x <= rest; ++x)
+                for (size_t c = 0; c < nc && cand[c] <= x; ++c) {
+                    const double cur = best[idx(jj, x, c)];
+                    if (cur >= inf) continue;
+                    const double next_gemm = waves(cand[c], T) * t_wave;
+                    for (size_t p = 0; p < nc && x + cand[p] <= rest; ++p) {
+                        if (cand[p] * t_row_d2h > next_gemm) continue;  // its C copy must hide
+                        // the next band's A rows must land during this band's GEMM
+                        if (arrive && cand[c] * t_row_h2d > waves(cand[p], T) * t_wave) continue;
+                        const double v = cur + waves(cand[p], T) * t_wave;
+                        double& slot = best[idx(jj + 1, x + cand[p], p)];
+                        if (v < slot - 1e-12) {
+                            slot = v;
+                            from[idx(jj + 1, x + cand[p], p)] = c;
+                        }
+                    }
+                }
+        // band 1's A rows cross PCIe after all of B, during band 0's last block
+        const double band0_tail = waves(r0, Tb) * t_wave;
+        for (int jj = 1; jj <= kMaxBands; ++jj)
+            for (size_t c = 0; c < nc; ++c)
+                if ((!arrive || cand[c] * t_row_h2d <= band0_tail) &&
+                    best[idx(jj, rest, c)] < bv - 1e-12) {
+                    bv = best[idx(jj, rest, c)];
+                    bj = jj;
+                    bc = c;
+                }
+    }
+    if (bj == 0) {  // no feasible plan: 8 equal bands
+        for (size_t q = 1; q <= 8; ++q) starts.push_back(m * q / 8);
+        return starts;
+    }
+    std::vector<size_t> sizes{r0};
+    for (size_t x = rest, c = bc; bj > 0; --bj) {
+        sizes.push_back(cand[c]);
+        const size_t prev = from[idx(bj, x, c)];
+        x -= cand[c];
+        c = prev;
+    }
+    size_t acc = 0;
+    for (size_t q = 0; q < sizes.size(); ++q) {
+        acc += sizes[q] * (size_t)g.group_rows;
+        starts.push_back(acc < m ? acc : m);
+    }
+    starts.back() = m;
+    return starts;
+}
+
+std::vector<size_t> plan_bands(int fmt, size_t m, size_t n, size_t l, int d, size_t block_cols,
+                               const I8Geometry& g) {
+    static std::mutex mu;
+    static std::map<BandKey, std::vector<size_t>> cache;
+    const BandKey key{m, n, l, block_cols, fmt, d, g.group_rows, g.group_cols, g.clusters};
+    {
+        std::lock_guard<std::mutex> lock(mu);
+        auto it = cache.find(key);
+        if (it != cache.end()) return it->second;
+    }
+    std::vector<size_t> plan = plan_bands_uncached(fmt, m, n, l, d, block_cols, g);
+    std::lock_guard<std::mutex> lock(mu);
+    if (cache.size() > 256) cache.clear();
+    cache[key] = plan;
+    return plan;
+}
+
 // Host-buffer overlap hooks (ozk_ozaki_gemm): wait on b_ready before the B
 // split (its H2D copy runs on another stream during the A split), and run the
 // slice GEMM in `bands` row bands, calling on_band(r0, r1) after each is
@@ -220,6 +372,7 @@ struct Timer {
 struct HostOverlap {
     cudaEvent_t b_ready = nullptr;
     int bands = 1;
+    std::vector<size_t> band_start;  // bands + 1 row starts (plan_bands)
     std::function<cudaError_t(size_t, size_t)> on_band;
     // optional: A arrives band by band (a_ready[b] = rows of band b on the
     // device); then B is split first and each band's A rows are split right
@@ -343,12 +496,17 @@ ozk_status ozaki_device_impl(int fmt, size_t m, size_t l, size_t n, const void* 
     prob.c = c;
     prob.ldc = n;
     const int bands = (ov && ov->bands > 1 && (pl.count > 0 || banded_a)) ? ov->bands : 1;
-    const size_t band_rows = (m + bands - 1) / bands;
     const size_t eb = elem_bytes(fmt);
     std::vector<std::unique_ptr<Timer>> split_timers;  // per-band A / per-block B splits (profile)
     int band = 0;
-    for (size_t r0 = 0; r0 < m; r0 += band_rows, ++band) {
-        const size_t rows = m - r0 < band_rows ? m - r0 : band_rows;
+    for (; band < bands; ++band) {
+        size_t r0 = 0, r1 = m;
+        if (bands > 1) {
+            r0 = ov->band_start[band];
+            r1 = ov->band_start[band + 1];
+        }
+        const size_t rows = r1 - r0;
+        if (rows == 0) continue;
         char* cb = static_cast<char*>(c) + r0 * n * eb;
         if (banded_a) {
             // this band's A rows: per-row split, identical to the rows of the
@@ -517,14 +675,25 @@ ozk_status ozk_ozaki_gemm(ozk_format fmt, size_t m, size_t l, size_t n, const vo
     cudaEvent_t allocated = nullptr, b_ready = nullptr;
     OZK_CUDA(cudaEventCreateWithFlags(&allocated, cudaEventDisableTiming), "ozaki_gemm: event");
     OZK_CUDA(cudaEventCreateWithFlags(&b_ready, cudaEventDisableTiming), "ozaki_gemm: event");
-    const int bands = m >= 2048 ? 8 : 1;
-    // B in column blocks of >= 2048 columns (whole 128-column tiles) when the
-    // first band can be multiplied block by block (INT8 engine, no pruning):
-    // 4 blocks at n = 8192 balance the per-block H2D time against the GEMM
-    // blocks' tile quantisation
-    const bool blockable = bands > 1 && drop == 0.0 && engine_setting() != OZK_ENGINE_DMMA &&
-                           int8_applicable((int)fmt, l, d) && n >= 4096;
+    // B in 4 column blocks (whole 128-column tiles) when the first band can be
+    // multiplied block by block (INT8 engine, no pruning, n >= 4096): at
+    // n = 8192 a block's H2D time matches its GEMM block
+    const bool i8 = engine_setting() != OZK_ENGINE_DMMA && int8_applicable((int)fmt, l, d);
+    const bool blockable = m >= 2048 && drop == 0.0 && i8 && n >= 4096;
     const size_t b_block_cols = blockable ? (((n + 3) / 4 + 127) / 128) * 128 : n;
+    // row bands from the slice GEMM's tile geometry (DMMA engine: 8 equal bands)
+    const I8Geometry geo =
+        i8 ? pair_gemm_i8_geometry(words_of((int)fmt), word_bytes_of((int)fmt),
+                                   int8_digits((int)fmt, l, d), num_sms_cached())
+           : I8Geometry{};
+    std::vector<size_t> band_start;
+    if (i8) {
+        band_start = plan_bands((int)fmt, m, n, l, d, b_block_cols, geo);
+    } else {
+        const size_t nb = m >= 2048 ? 8 : 1;
+        for (size_t q = 0; q <= nb; ++q) band_start.push_back(m * q / nb);
+    }
+    const int bands = (int)band_start.size() - 1;
     const int b_blocks = (int)((n + b_block_cols - 1) / b_block_cols);
     std::vector<cudaEvent_t> band_done(bands, nullptr), a_ready(bands, nullptr),
         b_block_ready(b_blocks, nullptr);
@@ -547,9 +716,8 @@ ozk_status ozk_ozaki_gemm(ozk_format fmt, size_t m, size_t l, size_t n, const vo
     // Copy order on the H2D stream.  Whole B: B (its split gates every band),
     // then A band by band.  B in column blocks: A band 0, then the B blocks
     // (strided copies of the row-major B), then the other A bands.
-    const size_t band_rows = (m + bands - 1) / bands;
     auto copy_a_band = [&](int q) -> cudaError_t {
-        const size_t r0 = q * band_rows, rows = r0 < m ? (m - r0 < band_rows ? m - r0 : band_rows) : 0;
+        const size_t r0 = band_start[q], rows = band_start[q + 1] - r0;
         cudaError_t e = cudaSuccess;
         if (rows)
             e = cudaMemcpyAsync(static_cast<char*>(da.p) + r0 * l * eb,
@@ -578,6 +746,7 @@ ozk_status ozk_ozaki_gemm(ozk_format fmt, size_t m, size_t l, size_t n, const vo
     HostOverlap ov;
     ov.b_ready = b_ready;
     ov.bands = bands;
+    ov.band_start = band_start;
     ov.a_ready = a_ready.data();
     if (b_blocks > 1) {
         ov.b_blocks = b_blocks;

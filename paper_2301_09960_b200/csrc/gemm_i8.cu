@@ -868,6 +868,51 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode_i8() {
     return fn;
 }
 
+// Persistent clusters: as many as can be co-resident (GPC packing can leave
+// SMs idle for clusters > 1); the occupancy query is made once per instance.
+template <int K, typename W, int ND, int TR, int EG, int CM, int CN, int NB>
+int resident_clusters(int num_sms) {
+    using Cfg = I8Cfg<K, W, ND, TR, EG, NB>;
+    constexpr int kCluster = CM * CN;
+    static int cached = 0;  // per instance; the device's SM count does not change
+    if (cached > 0) return cached;
+    int clusters = num_sms / kCluster;
+    if constexpr (kCluster > 1) {
+        // the vectorised-C instance has the same resources as the scalar one
+        auto kern = pair_gemm_i8_kernel<K, W, ND, TR, EG, false, CM, CN, NB>;
+        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 Cfg::kSmemBytes) != cudaSuccess)
+            return 0;
+        cudaLaunchConfig_t cfg = {};
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = kCluster;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.blockDim = dim3(Cfg::kThreads);
+        cfg.dynamicSmemBytes = Cfg::kSmemBytes;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        cfg.gridDim = dim3(clusters * kCluster);
+        int active = 0;
+        if (cudaOccupancyMaxActiveClusters(&active, kern, &cfg) == cudaSuccess && active > 0 &&
+            active < clusters)
+            clusters = active;
+    }
+    cached = clusters;
+    return clusters;
+}
+
+template <int K, typename W, int ND, int TR, int EG, int CM, int CN, int NB>
+I8Geometry geometry_typed(int num_sms) {
+    I8Geometry g;
+    g.group_rows = CM * TR;
+    g.group_cols = CN * TC;
+    g.clusters = resident_clusters<K, W, ND, TR, EG, CM, CN, NB>(num_sms);
+    g.cluster_sms = CM * CN;
+    return g;
+}
+
 template <int K, typename W, int ND, int TR, int EG = 2, int CM = 1, int CN = 1, int NB = 2>
 cudaError_t launch_i8_typed(const I8Operands& op, const PairList& pairs, cudaStream_t st,
                             int num_sms) {
@@ -921,6 +966,8 @@ cudaError_t launch_i8_typed(const I8Operands& op, const PairList& pairs, cudaStr
     if (e != cudaSuccess) return e;
     constexpr int kCluster = CM * CN;
     const int groups = ((tiles_m + CM - 1) / CM) * ((tiles_n + CN - 1) / CN);
+    int clusters = resident_clusters<K, W, ND, TR, EG, CM, CN, NB>(num_sms);
+    if (clusters <= 0) return cudaErrorInvalidConfiguration;
     cudaLaunchConfig_t cfg = {};
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -932,16 +979,6 @@ cudaError_t launch_i8_typed(const I8Operands& op, const PairList& pairs, cudaStr
     cfg.stream = st;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    // persistent clusters: as many as can be co-resident (GPC packing can
-    // leave SMs idle for clusters > 1), never more than there are tile groups
-    int clusters = num_sms / kCluster;
-    if constexpr (kCluster > 1) {
-        cfg.gridDim = dim3(clusters * kCluster);
-        int active = 0;
-        if (cudaOccupancyMaxActiveClusters(&active, kern, &cfg) == cudaSuccess && active > 0 &&
-            active < clusters)
-            clusters = active;
-    }
     if (groups < clusters) clusters = groups;
     cfg.gridDim = dim3(clusters * kCluster);
     // pacing counters: one per (wave, pair) step, stream-ordered scratch
@@ -961,6 +998,23 @@ cudaError_t launch_i8_typed(const I8Operands& op, const PairList& pairs, cudaStr
 }
 
 } // namespace
+
+I8Geometry pair_gemm_i8_geometry(int K, int word_bytes, int nd, int num_sms) {
+    if (word_bytes == 4) {
+        if (K == 3 && nd == 1)
+            return geometry_typed<3, float, 1, OZK_I8_TS_TR, OZK_I8_TS_EG, OZK_I8_CM, OZK_I8_CN, 2>(num_sms);
+        if (K == 3 && nd == 2)
+            return geometry_typed<3, float, 2, 64, 4, OZK_I8_CM, OZK_I8_CN, 2>(num_sms);
+        return I8Geometry{};
+    }
+    if (nd != 3) return I8Geometry{};
+    switch (K) {
+    case 2: return geometry_typed<2, double, 3, OZK_I8_DD_TR, OZK_I8_DD_EG, OZK_I8_CM, OZK_I8_CN, OZK_I8_DD_NB>(num_sms);
+    case 3: return geometry_typed<3, double, 3, OZK_I8_TR, OZK_I8_EG, OZK_I8_CM, OZK_I8_CN, OZK_I8_NB>(num_sms);
+    case 4: return geometry_typed<4, double, 3, OZK_I8_TR, OZK_I8_EG, OZK_I8_CM, OZK_I8_CN, OZK_I8_NB>(num_sms);
+    default: return I8Geometry{};
+    }
+}
 
 cudaError_t launch_pair_gemm_i8(int K, int word_bytes, const I8Operands& op,
                                 const PairList& pairs, cudaStream_t st, int num_sms) {

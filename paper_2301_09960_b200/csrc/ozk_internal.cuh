@@ -95,6 +95,13 @@ struct I8Operands {
     void* c;        // K-word AoS, row stride ldc elements
     size_t ldc;
 };
+// Tile geometry of the INT8 slice GEMM for a format: C rows and columns per
+// cluster tile and the number of co-resident persistent clusters (one wave =
+// `clusters` cluster tiles).  Zeros if the engine does not apply.
+struct I8Geometry {
+    int group_rows = 0, group_cols = 0, clusters = 0, cluster_sms = 1;
+};
+I8Geometry pair_gemm_i8_geometry(int K, int word_bytes, int nd, int num_sms);
 cudaError_t launch_pair_gemm_i8(int K, int word_bytes, const I8Operands& op,
                                 const PairList& pairs, cudaStream_t st, int num_sms);
 
