@@ -52,6 +52,8 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <atomic>
+
 #include "kword.cuh"
 #include "ozk_internal.cuh"
 
@@ -874,8 +876,8 @@ template <int K, typename W, int ND, int TR, int EG, int CM, int CN, int NB>
 int resident_clusters(int num_sms) {
     using Cfg = I8Cfg<K, W, ND, TR, EG, NB>;
     constexpr int kCluster = CM * CN;
-    static int cached = 0;  // per instance; the device's SM count does not change
-    if (cached > 0) return cached;
+    static std::atomic<int> cached{0};  // per instance; one GPU model per process
+    if (const int c = cached.load(std::memory_order_relaxed); c > 0) return c;
     int clusters = num_sms / kCluster;
     if constexpr (kCluster > 1) {
         // the vectorised-C instance has the same resources as the scalar one
@@ -899,7 +901,7 @@ int resident_clusters(int num_sms) {
             active < clusters)
             clusters = active;
     }
-    cached = clusters;
+    cached.store(clusters, std::memory_order_relaxed);
     return clusters;
 }
 
