@@ -494,27 +494,22 @@ def run_e2e(args, lib, OzkProfile, A, B, code, K, wb, d, n):
 
 
 def run_e2e_sharded(args, eng, A, B, K, wb, n):
-    """N > 1: the same metric through the sharded public path
-    (ShardedOzaki.run): every step each rank copies its A row block and the B
-    column block it splits from pinned host memory, runs the split, the
-    all-gather and its pair GEMMs, and reads its C rows back; time = max over
+    """N > 1: the same metric through the sharded public path with host
+    buffers (ShardedOzaki.run_host): every step each rank brings its B column
+    block and its A rows from pinned host memory, splits, all-gathers the B
+    digit planes, runs its pair GEMMs and reads its C rows back, transfers
+    overlapped with compute (B first, A and C in row bands); time = max over
     ranks (device events bracketing the copies)."""
     import torch
     import torch.distributed as dist
     p = eng.plan
     ha = A[p.r0:p.r1].cpu().pin_memory()
-    hb = B[:, p.c0:p.c1].cpu().pin_memory() if p.c1 > p.c0 else None
-    da = torch.empty_like(A[p.r0:p.r1])
-    db = torch.zeros_like(B)  # only the rank's column block is read by its split
+    hb = B[:, p.c0:p.c1].contiguous().cpu().pin_memory() if p.c1 > p.c0 else None
     hc = torch.empty((max(p.rows_local, 1), n, K), dtype=A.dtype).pin_memory()
     stream = torch.cuda.current_stream()
 
     def step():
-        da.copy_(ha, non_blocking=True)
-        if hb is not None:
-            db[:, p.c0:p.c1].copy_(hb, non_blocking=True)
-        c = eng.run(da, db)
-        hc[: p.rows_local].copy_(c, non_blocking=True)
+        eng.run_host(ha, hb, hc)
 
     step()
     torch.cuda.synchronize()
@@ -534,7 +529,7 @@ def run_e2e_sharded(args, eng, A, B, K, wb, n):
     return {"value": round(2.0 * n ** 3 / t / 1e9, 3), "unit": "GFLOP/s",
             "h2d_bytes_per_step": int(io[0].item()), "d2h_bytes_per_step": int(io[1].item()),
             "ms_per_step": round(1e3 * t, 3),
-            "api": "ShardedOzaki.run (sharded.py) with host buffers, per rank; max over ranks",
+            "api": "ShardedOzaki.run_host (sharded.py), pinned host buffers, per rank; max over ranks",
             "engine": eng.engine}
 
 

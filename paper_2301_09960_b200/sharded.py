@@ -145,6 +145,22 @@ class GpuOps:
             digits.shape[2], exps.data_ptr(), pmax.data_ptr() if pmax is not None else None,
             self._stream()))
 
+    def split_digit_rows(self, K, mat, rows, cols, ld, d, side, digits, r0, exps):
+        """split_digits into rows [r0, r0 + rows) of full-height digit planes."""
+        ld8, plane_rows = digits.shape[3], digits.shape[2]
+        self._check(self.lib.ozk_split_digits_device(
+            K, rows, cols, ld, mat.data_ptr(), d, side, digits.data_ptr() + r0 * ld8, ld8,
+            plane_rows, exps.data_ptr() + 4 * r0, None, self._stream()))
+
+    def gemm_digit_rows(self, plan: ShardPlan, r0, rows, a8, ga, b8, gb, pairs, c):
+        """gemm_digits for C rows [r0, r0 + rows) of this rank (c: all its rows)."""
+        flat = (ctypes.c_int * (2 * len(pairs)))(*[v for p in pairs for v in p])
+        ld8, esz = a8.shape[3], c.element_size() * c.shape[2]
+        self._check(self.lib.ozk_digits_gemm_device(
+            plan.K, rows, plan.l, plan.n, a8.data_ptr() + r0 * ld8, ga.data_ptr() + 4 * r0,
+            a8.shape[2], b8.data_ptr(), gb.data_ptr(), b8.shape[2], ld8, plan.d, flat, len(pairs),
+            c.data_ptr() + r0 * plan.n * esz, plan.n, self._stream()))
+
     def gemm_digits(self, plan: ShardPlan, a8, ga, b8, gb, pairs, c):
         flat = (ctypes.c_int * (2 * len(pairs)))(*[v for p in pairs for v in p])
         self._check(self.lib.ozk_digits_gemm_device(
@@ -206,6 +222,78 @@ class ShardedOzaki:
             assert w * ncb >= p.n
         else:
             self._gather(self.sb_all, self.sb)
+
+    def run_host(self, hA, hB, hC, bands=4):
+        """The same C rows from pinned HOST buffers, transfers overlapped:
+        hA this rank's A rows (rows_local, l, K), hB its B column block
+        (l, c1 - c0, K) contiguous, hC receives its C rows (rows_local, n, K).
+        B's block crosses PCIe first on a copy stream and is split, its NCCL
+        all-gather runs on a side stream while A arrives in `bands` row bands,
+        each split right before its slice-GEMM band, and each band's C rows go
+        back on a second copy stream while later bands compute (rows are
+        independent: bit-identical to run()).  Other engines / pruning: the
+        copies around run()."""
+        p, ops = self.plan, self.ops
+        cur = torch.cuda.current_stream()
+        if self.engine != "int8" or self.pmax is not None or not p.rows_local:
+            da = hA.to(self.ops.device, non_blocking=True)
+            db = torch.zeros((p.l, p.n, p.words), dtype=hA.dtype, device=self.ops.device)
+            if p.c1 > p.c0:
+                db[:, p.c0:p.c1].copy_(hB, non_blocking=True)
+            c = self.run(da, db)
+            hC[: p.rows_local].copy_(c, non_blocking=True)
+            return
+        if getattr(self, "_host", None) is None:
+            dev = self.ops.device
+            self._host = dict(
+                xs=torch.cuda.Stream(dev), ys=torch.cuda.Stream(dev),
+                da=torch.empty((p.rows_local, p.l, p.words), dtype=hA.dtype, device=dev),
+                db=torch.empty((p.l, max(p.c1 - p.c0, 1), p.words), dtype=hA.dtype, device=dev))
+        h = self._host
+        xs, ys, da, db = h["xs"], h["ys"], h["da"], h["db"]
+        nb = max(1, min(bands, p.rows_local // 256))
+        bounds = [p.rows_local * q // nb for q in range(nb + 1)]
+        xs.wait_stream(cur)
+        ys.wait_stream(cur)
+        ev_b = torch.cuda.Event()
+        ev_a = [torch.cuda.Event() for _ in range(nb)]
+        with torch.cuda.stream(xs):
+            if p.c1 > p.c0:
+                db[:, : p.c1 - p.c0].copy_(hB, non_blocking=True)
+            ev_b.record(xs)
+            for q in range(nb):
+                da[bounds[q]:bounds[q + 1]].copy_(hA[bounds[q]:bounds[q + 1]], non_blocking=True)
+                ev_a[q].record(xs)
+        cur.wait_event(ev_b)
+        if p.c1 > p.c0:
+            ops.split_digit_rows(p.K, db, p.l, p.c1 - p.c0, p.c1 - p.c0, p.d, 1, self.b8, 0,
+                                 self.gb)
+        comm = None
+        if dist.get_backend(self.group) == "nccl":
+            if self._comm is None:
+                self._comm = torch.cuda.Stream()
+            comm = self._comm
+            comm.wait_stream(cur)
+            with torch.cuda.stream(comm):
+                self._all_gather()
+        else:
+            self._all_gather()
+        pairs = triangular_pairs(p.d)
+        for q in range(nb):
+            r0, r1 = bounds[q], bounds[q + 1]
+            cur.wait_event(ev_a[q])
+            ops.split_digit_rows(p.K, da[r0:r1], r1 - r0, p.l, p.l, p.d, 0, self.a8, r0, self.ga)
+            if q == 0 and comm is not None:
+                cur.wait_stream(comm)
+            ops.gemm_digit_rows(p, r0, r1 - r0, self.a8, self.ga, self.b8_cat, self.gb_cat,
+                                pairs, self.c)
+            done = torch.cuda.Event()
+            done.record(cur)
+            ys.wait_event(done)
+            with torch.cuda.stream(ys):
+                hC[r0:r1].copy_(self.c[r0:r1], non_blocking=True)
+        cur.wait_stream(ys)
+        cur.wait_stream(xs)
 
     def run(self, A, B, prof=None):
         """A: (m, l, K) or this rank's rows; B: (l, n, K) full (row stride n).

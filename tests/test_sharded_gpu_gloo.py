@@ -3,7 +3,8 @@ on cuda:0 (gloo backend, which all-gathers CUDA tensors through the host;
 NCCL refuses two ranks on one device).  Each rank runs ShardedOzaki with
 GpuOps -- its splits into INT8 digit planes (or FP64 slices for l <= 128), the
 gathered-plane permute and its pair GEMMs on the B200 -- and its C rows must
-equal the reference's rows bit for bit.  The kernels of different ranks never
+equal the reference's rows bit for bit, both from device tensors (run) and
+from pinned host buffers with overlapped, banded transfers (run_host).  The kernels of different ranks never
 wait on each other (the only exchange is the host-side collective), so sharing
 one GPU changes timing, not results.
 """
@@ -37,9 +38,25 @@ def _worker(rank, world, port, cases, q):
             got = got.cpu().numpy()
             r0, r1 = eng.plan.r0, eng.plan.r1
             ok = np.array_equal(got.view(np.uint64), want[r0:r1].view(np.uint64))
-            q.put((rank, (K, m, l, n, d, drop), eng.engine, bool(ok)))
+            # host-buffer path (overlapped copies, A/C in row bands)
+            ok_host = _host_rows_equal(eng, a, b, want)
+            q.put((rank, (K, m, l, n, d, drop), eng.engine, bool(ok and ok_host)))
     finally:
         dist.destroy_process_group()
+
+
+def _host_rows_equal(eng, a, b, want):
+    import torch
+    p = eng.plan
+    ha = torch.from_numpy(a[p.r0:p.r1].copy()).pin_memory()
+    hb = torch.from_numpy(b[:, p.c0:p.c1].copy()).pin_memory() if p.c1 > p.c0 else None
+    hc = torch.full((max(p.rows_local, 1), p.n, p.words), float("nan"),
+                    dtype=ha.dtype).pin_memory()
+    for _ in range(2):  # the second call reuses the streams and buffers
+        eng.run_host(ha, hb, hc, bands=3)
+        torch.cuda.synchronize()
+    got = hc[: p.rows_local].numpy()
+    return np.array_equal(got.view(np.uint64), want[p.r0:p.r1].view(np.uint64))
 
 
 def _free_port():
@@ -51,7 +68,8 @@ def _free_port():
 @pytest.mark.parametrize("world", [2, 3])
 def test_sharded_ranks_on_device(ozk, world):
     cases = [(2, 100, 600, 90, 6, 0.0), (3, 64, 1030, 70, 9, 0.0), (4, 40, 300, 50, 12, 0.0),
-             (2, 70, 700, 64, 10, 2.0 ** -70), (2, 30, 100, 40, 6, 0.0)]
+             (2, 70, 700, 64, 10, 2.0 ** -70), (2, 30, 100, 40, 6, 0.0),
+             (3, 1600, 300, 200, 4, 0.0)]  # >= 256 rows per rank: banded host path
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     mp.spawn(_worker, args=(world, _free_port(), cases, q), nprocs=world, join=True)
@@ -83,6 +101,7 @@ def _nccl_single(rank, port, q):
             for _ in range(2):  # the second run reuses the side stream and buffers
                 got = eng.run(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda(), prof)
             ok = np.array_equal(got.cpu().numpy().view(np.uint64), want.view(np.uint64))
+            ok = ok and _host_rows_equal(eng, a, b, want)
             q.put((K, eng.engine, eng._comm is not None, bool(ok), prof.engine))
     finally:
         dist.destroy_process_group()
