@@ -60,7 +60,15 @@
 namespace ozk {
 namespace {
 
-constexpr int TC = 128, BKB = 128;            // tile C columns (MMA M), k bytes per stage
+// k bytes per operand stage: 128 (128-byte swizzle) or 64 (64-byte swizzle:
+// half-depth stages, twice as many in the same shared memory).  64 measured
+// bit-identical but slower (TD slice GEMM 180 -> 217 ms, DD 74 -> 80, TS 94 ->
+// 130): twice the barrier/commit/TMA traffic per k outweighs the deeper ring.
+#ifndef OZK_I8_BKB
+#define OZK_I8_BKB 128
+#endif
+constexpr int TC = 128, BKB = OZK_I8_BKB;     // tile C columns (MMA M), k bytes per stage
+static_assert(BKB == 128 || BKB == 64, "operand stage depth");
 #ifndef OZK_I8_GROUPM
 #define OZK_I8_GROUPM 8
 #endif
@@ -153,7 +161,7 @@ struct I8Cfg {
     static_assert(NB * kBufCols <= 512 && (NB == 1 || NB == 2), "TMEM accumulator buffers");
     static_assert(NB == 2 || kEpiRows % 4 == 0, "drain width");
     static_assert(ND * TR <= 256 && TR % 16 == 0, "stacked MMA width");
-    static_assert(kATile % 1024 == 0, "A-digit tiles must stack in 8-row swizzle groups");
+    static_assert(kATile % (8 * BKB) == 0, "A-digit tiles must stack in 8-row swizzle groups");
     static_assert(kEpiRows % (2 * kChunk) == 0, "epilogue rows per ping-pong trip");
     static_assert(40 * 128 + kEpiRegs * 128 * EG <= kLaunchRegs * (4 + 4 * EG) * 32,
                   "setmaxnreg pool");
@@ -209,12 +217,16 @@ __device__ __forceinline__ void tma_load_4d(uint32_t dst, const CUtensorMap* map
         "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
         : "memory");
 }
-// UMMA shared-memory descriptor: K-major operand, 128-byte swizzle, 8-row groups
-// 1024 B apart (CuTe mma_sm100_desc.hpp SmemDescriptor, version 1 = Blackwell).
-__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+// UMMA shared-memory descriptor: K-major operand, BKB-byte swizzle (layout type
+// 2 = 128B, 4 = 64B), 8-row groups 8*BKB bytes apart (CuTe mma_sm100_desc.hpp
+// SmemDescriptor, version 1 = Blackwell).
+__device__ __forceinline__ uint64_t sw_desc(uint32_t saddr) {
+    constexpr uint64_t kLayout = BKB == 128 ? 2 : 4;
     return (uint64_t)((saddr >> 4) & 0x3fff) | ((uint64_t)1 << 16) |
-           ((uint64_t)(1024 >> 4) << 32) | ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+           ((uint64_t)((8 * BKB) >> 4) << 32) | ((uint64_t)1 << 46) | (kLayout << 61);
 }
+constexpr CUtensorMapSwizzle kTmaSwizzle =
+    BKB == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
 __device__ __forceinline__ void umma_i8(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc,
                                         uint32_t accumulate) {
     asm volatile(
@@ -651,8 +663,8 @@ pair_gemm_i8_kernel(const __grid_constant__ MapsI8 maps, const __grid_constant__
 #endif
                     asm volatile("tcgen05.fence::after_thread_sync;");
                     const uint32_t sb = ring + stage * kStageBytes;  // B digits (M side)
-                    const uint64_t db = sw128_desc(sb);              // B digit 0, k-chunk 0
-                    const uint64_t da = sw128_desc(sb + ND * kBTile);  // A digits (N side)
+                    const uint64_t db = sw_desc(sb);              // B digit 0, k-chunk 0
+                    const uint64_t da = sw_desc(sb + ND * kBTile);  // A digits (N side)
                     if (elect_one()) {
 #pragma unroll
                         for (int kc = 0; kc < BKB / 32; ++kc) {
@@ -928,7 +940,7 @@ cudaError_t launch_i8_typed(const I8Operands& op, const PairList& pairs, cudaStr
         cuuint32_t box[4] = {BKB, TR / CN, 1, 1};
         cuuint32_t es[4] = {1, 1, 1, 1};
         if (encode(&maps.a, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<int8_t*>(op.a), dims,
-                   strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, kTmaSwizzle,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) !=
             CUDA_SUCCESS)
             return cudaErrorInvalidValue;
@@ -939,7 +951,7 @@ cudaError_t launch_i8_typed(const I8Operands& op, const PairList& pairs, cudaStr
         cuuint32_t box[4] = {BKB, TC / CM, 1, 1};
         cuuint32_t es[4] = {1, 1, 1, 1};
         if (encode(&maps.b, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<int8_t*>(op.b), dims,
-                   strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, kTmaSwizzle,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) !=
             CUDA_SUCCESS)
             return cudaErrorInvalidValue;
