@@ -1,6 +1,7 @@
 """Split-count sweep at n = 8192: effective GFLOP/s of
 the INT8 engine for DD D=4..8, TD D=7..11, QD D=9..14 (median of 2 after a
-warm-up), one JSON object per line.  python tools/d_sweep.py [n]"""
+warm-up), one JSON object per line.  python tools/d_sweep.py [n] [K:lo-hi,...]
+(e.g. `4096 2:2-10` = BASELINE config 1, DD n=4096 with the split count swept)."""
 import ctypes
 import json
 import statistics
@@ -14,7 +15,12 @@ from paper_2301_09960_b200._lib import OzkProfile, lib  # noqa: E402
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 8192
 sh = torch.cuda.current_stream().cuda_stream
 lib.ozk_set_engine(2)
-for K, ds in ((2, range(4, 9)), (3, range(7, 12)), (4, range(9, 15))):
+plan = ((2, range(4, 9)), (3, range(7, 12)), (4, range(9, 15)))
+if len(sys.argv) > 2:
+    plan = tuple((int(f.split(":")[0]), range(int(f.split(":")[1].split("-")[0]),
+                                               int(f.split(":")[1].split("-")[1]) + 1))
+                 for f in sys.argv[2].split(","))
+for K, ds in plan:
     A = torch.empty((n, n, K), dtype=torch.float64, device="cuda")
     B = torch.empty_like(A)
     C = torch.empty_like(A)
