@@ -235,6 +235,18 @@ ozk_status ozk_lu_trailing_update_device(ozk_format fmt, size_t tm, size_t pw, s
                                          size_t ldu, void* a22, size_t lda, int split_count,
                                          void* stream);
 
+/* ---- host-buffer schedule (introspection) --------------------------------- *
+ * The row bands ozk_ozaki_gemm's overlapped host path uses for an m x n C on
+ * the INT8 engine, planned from the slice GEMM's tile geometry: group_rows /
+ * group_cols C rows / columns per cluster tile, `clusters` co-resident clusters
+ * of cluster_sms SMs each, B arriving in column blocks of block_cols.  Writes
+ * up to max_bands + 1 row starts (0, ..., m) to starts and returns the number
+ * of bands, or -1 (bad arguments / more than max_bands bands).  Pure host
+ * function; no GPU needed.  No reference counterpart (this build's schedule). */
+int ozk_plan_row_bands(ozk_format fmt, size_t m, size_t n, size_t l, int split_count,
+                       size_t block_cols, int group_rows, int group_cols, int clusters,
+                       int cluster_sms, size_t* starts, int max_bands);
+
 /* ---- direct K-word GEMM -------------------------------------- *
  * The reference's gemm_simple<MultiFloat<K>> (gemm.hpp:16-33) bit for bit:
  * per element c = 0; for k ascending: c = c + a(i,k) * b(k,j) with the

@@ -55,6 +55,9 @@ SIGNATURES = {
                                               ctypes.c_void_p]),
     "ozk_auto_split_count": (ctypes.c_int, [ctypes.c_int, _sz]),
     "ozk_auto_drop_threshold": (ctypes.c_double, [ctypes.c_int, _sz]),
+    "ozk_plan_row_bands": (ctypes.c_int, [ctypes.c_int, _sz, _sz, _sz, ctypes.c_int, _sz,
+                                          ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                          ctypes.c_int, ctypes.c_void_p, ctypes.c_int]),
     "ozk_int8_digits": (ctypes.c_int, [ctypes.c_int, _sz, ctypes.c_int]),
     "ozk_split_digits_device": (ctypes.c_int, [ctypes.c_int, _sz, _sz, _sz, _dp, ctypes.c_int,
                                                ctypes.c_int, _dp, _sz, _sz, _dp, _dp,

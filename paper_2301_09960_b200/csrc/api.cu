@@ -967,6 +967,25 @@ int ozk_auto_split_count(ozk_format fmt, size_t inner_dim) {
     return d < kMaxSplits ? d : kMaxSplits;
 }
 
+int ozk_plan_row_bands(ozk_format fmt, size_t m, size_t n, size_t l, int split_count,
+                       size_t block_cols, int group_rows, int group_cols, int clusters,
+                       int cluster_sms, size_t* starts, int max_bands) {
+    if (!valid_fmt(fmt) || !starts || max_bands < 1 || split_count < 1 || group_rows <= 0 ||
+        group_cols <= 0 || cluster_sms <= 0 || block_cols == 0)
+        return -1;
+    I8Geometry g;
+    g.group_rows = group_rows;
+    g.group_cols = group_cols;
+    g.clusters = clusters;
+    g.cluster_sms = cluster_sms;
+    const std::vector<size_t> plan =
+        plan_bands_uncached((int)fmt, m, n, l, split_count, block_cols, g);
+    const int bands = (int)plan.size() - 1;
+    if (bands > max_bands) return -1;
+    for (size_t q = 0; q < plan.size(); ++q) starts[q] = plan[q];
+    return bands;
+}
+
 double ozk_auto_drop_threshold(ozk_format fmt, size_t inner_dim) {
     if (!valid_fmt(fmt) || inner_dim == 0) return 0.0;
     const int S = word_bytes_of(fmt) == 4 ? 24 : 53;

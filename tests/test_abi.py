@@ -136,3 +136,52 @@ def test_auto_split_policy():
     assert ozk.auto_split_policy(0x103, 8192) == (17, 2.0 ** -87)
     assert ozk.auto_split_policy(2, 1) == (7, 2.0 ** -108)   # sigma = 27: 26 bits per slice
     assert ozk.auto_split_policy(7, 8192) == (0, 0.0)
+
+
+def _plan(fmt, m, n, l, d, block_cols, gr, gc, clusters, max_bands=8):
+    from paper_2301_09960_b200._lib import lib
+    starts = (ctypes.c_size_t * (max_bands + 1))()
+    nb = lib.ozk_plan_row_bands(fmt, m, n, l, d, block_cols, gr, gc, clusters, 2, starts,
+                                max_bands)
+    return nb, list(starts[: nb + 1]) if nb > 0 else []
+
+
+def _waves(rows, gr, n, gc, clusters):
+    r = -(-rows // gr)
+    return -(-(r * -(-n // gc)) // clusters)
+
+
+@pytest.mark.parametrize("fmt,gr", [(2, 128), (3, 96), (4, 96), (0x103, 224)])
+def test_row_band_plan_n8192(fmt, gr):
+    """ozk_ozaki_gemm's host schedule (csrc/api.cu plan_bands) at n = 8192 on the
+    B200 geometry (74 two-SM clusters, 128-column tiles): the bands cover every
+    row once, in whole cluster rows except the end, band 0 is a short first
+    wait (<= m/6), the last band is short (its C copy is the exposed tail), and
+    the total GEMM waves are within one wave of 8 equal bands' (fewer for TD)."""
+    m = n = l = 8192
+    d = {2: 6, 3: 9, 4: 12, 0x103: 15}[fmt]
+    nb, st = _plan(fmt, m, n, l, d, 2048, gr, 128, 74)
+    assert 2 <= nb <= 8, st
+    assert st[0] == 0 and st[-1] == m and all(a < b for a, b in zip(st, st[1:])), st
+    assert all(x % gr == 0 for x in st[1:-1]), st
+    assert st[1] <= m // 6 + gr, st
+    planned = sum(_waves(b - a, gr, n, 128, 74) for a, b in zip(st, st[1:]))
+    equal = sum(_waves(m * (q + 1) // 8 - m * q // 8, gr, n, 128, 74) for q in range(8))
+    assert planned <= equal + 1, (planned, equal, st)
+    if fmt == 3:
+        assert planned < equal, (planned, equal, st)
+    assert st[-1] - st[-2] <= m // 16, st
+    # within 3 waves of the monolithic GEMM's ceil(tiles / clusters)
+    assert planned <= _waves(m, gr, n, 128, 74) + 3, (planned, st)
+
+
+def test_row_band_plan_edges():
+    nb, st = _plan(3, 1000, 8192, 8192, 9, 2048, 96, 128, 74)
+    assert (nb, st) == (1, [0, 1000])  # m < 2048: one band
+    nb, st = _plan(3, 4097, 4101, 140, 3, 1152, 96, 128, 74)
+    assert nb >= 1 and st[-1] == 4097 and all(a < b for a, b in zip(st, st[1:]))
+    from paper_2301_09960_b200._lib import lib
+    starts = (ctypes.c_size_t * 9)()
+    assert lib.ozk_plan_row_bands(3, 8192, 8192, 8192, 9, 2048, 0, 128, 74, 2, starts, 8) == -1
+    assert lib.ozk_plan_row_bands(9, 8192, 8192, 8192, 9, 2048, 96, 128, 74, 2, starts, 8) == -1
+    assert lib.ozk_plan_row_bands(3, 8192, 8192, 8192, 9, 2048, 96, 128, 74, 2, starts, 1) == -1
