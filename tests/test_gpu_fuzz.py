@@ -1,0 +1,68 @@
+"""Seeded randomised parity sweep of the public GEMM path against the CPU
+oracle (the compiled reference where present): format DD/TD/QD/TS, ragged
+shapes on both sides of the INT8 engine's l > 128 boundary, split count,
+pruning threshold, Eq. (1) or exponent-spread inputs, zero rows/columns, host
+or device API, auto or forced-DMMA engine.  Every C must be bit-identical to
+the reference's (D >= 2; D = 1 products round, as in the reference).
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+TS = 0x103
+SEEDS = list(range(160))
+
+
+def _case(seed):
+    rng = np.random.default_rng(1000 + seed)
+    fmt = [2, 3, 4, TS][seed % 4]
+    m, n = (int(x) for x in rng.integers(1, 161, 2))
+    l = int(rng.integers(1, 129)) if rng.random() < 0.35 else int(rng.integers(129, 701))
+    dmax = {2: 8, 3: 11, 4: 14, TS: 16}[fmt]
+    d = int(rng.integers(2, dmax + 1))
+    drop = 0.0 if rng.random() < 0.6 else float(2.0 ** -int(rng.integers(10, 150)))
+    spread = int(rng.integers(8, 200)) if (fmt != TS and rng.random() < 0.3) else 0
+    zero_a = int(rng.integers(0, m)) if rng.random() < 0.25 else None
+    zero_b = int(rng.integers(0, n)) if rng.random() < 0.25 else None
+    device = bool(rng.random() < 0.5)
+    dmma = bool(rng.random() < 0.2)
+    return fmt, m, l, n, d, drop, spread, zero_a, zero_b, device, dmma
+
+
+def _inputs(cpu, port, fmt, m, l, n, spread, seed):
+    if fmt == TS:
+        return port.gen_eq1_ts(m, l, 2 * seed + 1), port.gen_eq1_ts(l, n, 2 * seed + 2)
+    if spread:
+        return (port.gen_spread(fmt, m, l, 2 * seed + 1, spread),
+                port.gen_spread(fmt, l, n, 2 * seed + 2, spread))
+    return cpu.gen_eq1(fmt, m, l, 2 * seed + 1), cpu.gen_eq1(fmt, l, n, 2 * seed + 2)
+
+
+@pytest.mark.parametrize("seed", SEEDS)
+def test_random_gemm_bitexact(ozk, cpu, port, seed):
+    import torch
+    fmt, m, l, n, d, drop, spread, zero_a, zero_b, device, dmma = _case(seed)
+    a, b = _inputs(cpu, port, fmt, m, l, n, spread, seed)
+    if zero_a is not None:
+        a[zero_a] = 0.0
+    if zero_b is not None:
+        b[:, zero_b] = 0.0
+    if fmt == TS:
+        want = port.ozaki_gemm_ts(a, b, d, drop)
+    else:
+        want = cpu.ozaki_gemm(fmt, a, b, d, drop)
+    ozk.set_engine("dmma" if dmma else "auto")
+    try:
+        if device:
+            got, _ = ozk.ozaki_gemm(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda(), d,
+                                    drop_threshold=drop)
+            got = got.cpu().numpy()
+        else:
+            got, _ = ozk.ozaki_gemm(a, b, d, drop_threshold=drop)
+    finally:
+        ozk.set_engine("auto")
+    u = np.uint32 if fmt == TS else np.uint64
+    bad = np.flatnonzero((got.view(u) != want.view(u)).reshape(m * n, -1).any(axis=1))
+    assert bad.size == 0, (f"case {_case(seed)}: {bad.size} of {m * n} elements differ, "
+                           f"first {divmod(int(bad[0]), n)}")
