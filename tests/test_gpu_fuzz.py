@@ -66,3 +66,21 @@ def test_random_gemm_bitexact(ozk, cpu, port, seed):
     bad = np.flatnonzero((got.view(u) != want.view(u)).reshape(m * n, -1).any(axis=1))
     assert bad.size == 0, (f"case {_case(seed)}: {bad.size} of {m * n} elements differ, "
                            f"first {divmod(int(bad[0]), n)}")
+
+
+@pytest.mark.parametrize("seed", list(range(16)))
+def test_random_gemm_bitexact_multi_tile(ozk, cpu, port, seed):
+    """Larger seeded cases (300-700 rows/columns: several tiles, waves and
+    paced clusters of the INT8 engine; D <= 6 keeps the CPU oracle fast)."""
+    rng = np.random.default_rng(5000 + seed)
+    fmt = [2, 3, 4, TS][seed % 4]
+    m, n = (int(x) for x in rng.integers(300, 701, 2))
+    l = int(rng.integers(129, 1025))
+    d = int(rng.integers(2, 7))
+    drop = 0.0 if seed % 3 else float(2.0 ** -int(rng.integers(30, 120)))
+    a, b = _inputs(cpu, port, fmt, m, l, n, 0 if seed % 5 else 60, seed + 777)
+    want = (port.ozaki_gemm_ts(a, b, d, drop) if fmt == TS else cpu.ozaki_gemm(fmt, a, b, d, drop))
+    got, _ = ozk.ozaki_gemm(a, b, d, drop_threshold=drop)
+    u = np.uint32 if fmt == TS else np.uint64
+    bad = np.flatnonzero((got.view(u) != want.view(u)).reshape(m * n, -1).any(axis=1))
+    assert bad.size == 0, (fmt, m, l, n, d, drop, bad.size)
