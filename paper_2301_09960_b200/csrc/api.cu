@@ -365,10 +365,10 @@ std::vector<size_t> plan_bands(int fmt, size_t m, size_t n, size_t l, int d, siz
 }
 
 // Host-buffer overlap hooks (ozk_ozaki_gemm): wait on b_ready before the B
-// split (its H2D copy runs on another stream during the A split), and run the
-// slice GEMM in `bands` row bands, calling on_band(r0, r1) after each is
-// enqueued so its D2H copy overlaps the next band (rows are independent, so
-// banding does not change a bit).
+// split (whole-B mode), and run the slice GEMM in `bands` row bands
+// [band_start[q], band_start[q+1]) (plan_bands), calling on_band(r0, r1) after
+// each is enqueued so its D2H copy overlaps the next band (rows are
+// independent, so banding does not change a bit).
 struct HostOverlap {
     cudaEvent_t b_ready = nullptr;
     int bands = 1;
@@ -663,8 +663,9 @@ ozk_status ozk_ozaki_gemm(ozk_format fmt, size_t m, size_t l, size_t n, const vo
     OwnStream os;
     OZK_CUDA(os.create(), "ozaki_gemm: stream");
     num_sms_cached();
-    // Transfers overlap compute on a second stream: B's H2D runs during the A
-    // split, and C comes back band by band while later bands compute.
+    // Transfers overlap compute on two copy streams: A arrives in row bands
+    // (plan_bands), B whole or in column blocks split as they land, and C goes
+    // back band by band while later bands compute (HostOverlap).
     OwnStream xs, ys;  // H2D copies, D2H copies
     OZK_CUDA(xs.create(), "ozaki_gemm: copy stream");
     OZK_CUDA(ys.create(), "ozaki_gemm: copy stream");
