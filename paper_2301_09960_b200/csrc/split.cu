@@ -22,8 +22,11 @@ namespace ozk {
 namespace {
 
 #ifndef OZK_SPLIT_THREADS
-#define OZK_SPLIT_THREADS 512  // 256: DD 7.0 / TD 18.8 ms; 512: 5.9 / 18.4 (residuals of the
-                                 // resident rows fit L2); 1024: 6.3 / 21.0
+// One 512-thread CTA per SM (~88 registers: ptxas keeps the K-word state and
+// the loop's ILP in registers): DD / TD / QD split 5.9 / 18.4 / 29.5 ms; 256,
+// 384, 768 threads and 2-4 CTAs per SM (forced register caps) all measured
+// slower (e.g. TD 19.1-26.8 ms), the residuals of the 148 resident rows fit L2
+#define OZK_SPLIT_THREADS 512
 #endif
 constexpr int kSplitThreads = OZK_SPLIT_THREADS;
 
@@ -99,7 +102,10 @@ __device__ __forceinline__ void store_kw(T* p, const T* c) {
 // TS); slices are always written as binary64 (a TS slice is a binary32 value,
 // exactly representable), which is the DMMA GEMM's operand type.
 template <int K, typename T>
-__global__ void __launch_bounds__(kSplitThreads)
+#ifndef OZK_SPLIT_MIN_BLOCKS
+#define OZK_SPLIT_MIN_BLOCKS 1  // CTAs per SM the register budget must allow
+#endif
+__global__ void __launch_bounds__(kSplitThreads, OZK_SPLIT_MIN_BLOCKS)
 split_rows_kernel(const T* __restrict__ in, size_t in_ld, T* __restrict__ work, size_t cols,
                   int d, int sigma, double* __restrict__ pieces, size_t ldk,
                   size_t slice_stride, unsigned long long* __restrict__ piece_max,
