@@ -22,10 +22,9 @@ namespace ozk {
 namespace {
 
 #ifndef OZK_SPLIT_THREADS
-// One 512-thread CTA per SM (~88 registers: ptxas keeps the K-word state and
-// the loop's ILP in registers): DD / TD / QD split 5.9 / 18.4 / 29.5 ms; 256,
-// 384, 768 threads and 2-4 CTAs per SM (forced register caps) all measured
-// slower (e.g. TD 19.1-26.8 ms), the residuals of the 148 resident rows fit L2
+// 512-thread CTAs, two per SM (50-64 registers; the ~300 resident rows'
+// residuals, 57 MB at TD l = 8192, fit L2): DD / TD / QD split 5.9 / 18.4 /
+// 29.5 ms; 256, 384, 768 and 1024 threads measured slower (TD 19.1-26.8 ms)
 #define OZK_SPLIT_THREADS 512
 #endif
 constexpr int kSplitThreads = OZK_SPLIT_THREADS;
@@ -102,10 +101,14 @@ __device__ __forceinline__ void store_kw(T* p, const T* c) {
 // TS); slices are always written as binary64 (a TS slice is a binary32 value,
 // exactly representable), which is the DMMA GEMM's operand type.
 template <int K, typename T>
-#ifndef OZK_SPLIT_MIN_BLOCKS
-#define OZK_SPLIT_MIN_BLOCKS 1  // CTAs per SM the register budget must allow
-#endif
+// No minimum-blocks hint by default: ptxas then keeps 50-64 registers (two
+// CTAs per SM).  An explicit hint of 1 lets it take ~88 and costs ~3 ms per TD
+// step; 2-4 (forced caps) measured slower too.
+#ifdef OZK_SPLIT_MIN_BLOCKS
 __global__ void __launch_bounds__(kSplitThreads, OZK_SPLIT_MIN_BLOCKS)
+#else
+__global__ void __launch_bounds__(kSplitThreads)
+#endif
 split_rows_kernel(const T* __restrict__ in, size_t in_ld, T* __restrict__ work, size_t cols,
                   int d, int sigma, double* __restrict__ pieces, size_t ldk,
                   size_t slice_stride, unsigned long long* __restrict__ piece_max,
