@@ -147,17 +147,6 @@ __device__ __forceinline__ TileCoord tile_of(int id, int tiles_m, int tiles_n_bl
     return t;
 }
 
-__device__ __forceinline__ bool mbar_test(uint32_t bar, uint32_t parity) {
-    uint32_t ok;
-    asm volatile(
-        "{\n .reg .pred p;\n mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n"
-        " selp.u32 %0, 1, 0, p;\n}\n"
-        : "=r"(ok)
-        : "r"(bar), "r"(parity)
-        : "memory");
-    return ok != 0;
-}
-
 // W: word type of the K-word C in kAccumulate mode (double: DD/TD/QD, float:
 // TS -- an exact binary64 slice product of binary32 slices is exactly
 // representable in binary32, so the cast before the TS epilogue is exact).

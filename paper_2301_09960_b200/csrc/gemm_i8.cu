@@ -246,7 +246,7 @@ __device__ __forceinline__ void tma_load_4d_mc(uint32_t dst, const CUtensorMap* 
         "h"(mask)
         : "memory");
 }
-__device__ __forceinline__ void tma_load_4d_h(uint32_t dst, const CUtensorMap* map, uint32_t bar,
+[[maybe_unused]] __device__ __forceinline__ void tma_load_4d_h(uint32_t dst, const CUtensorMap* map, uint32_t bar,
                                               int c0, int c1, int c2, int c3, uint64_t pol) {
     asm volatile(
         "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
@@ -254,7 +254,7 @@ __device__ __forceinline__ void tma_load_4d_h(uint32_t dst, const CUtensorMap* m
         "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "l"(pol)
         : "memory");
 }
-__device__ __forceinline__ void tma_load_4d_mc_h(uint32_t dst, const CUtensorMap* map,
+[[maybe_unused]] __device__ __forceinline__ void tma_load_4d_mc_h(uint32_t dst, const CUtensorMap* map,
                                                  uint32_t bar, int c0, int c1, int c2, int c3,
                                                  uint16_t mask, uint64_t pol) {
     asm volatile(
@@ -351,7 +351,7 @@ __device__ __forceinline__ uint64_t l2_policy_evict_last() {
     asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
     return pol;
 }
-__device__ __forceinline__ uint64_t l2_policy_evict_first() {
+[[maybe_unused]] __device__ __forceinline__ uint64_t l2_policy_evict_first() {
     uint64_t pol;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
     return pol;
