@@ -41,7 +41,8 @@
 //               column per thread): NB = 1 (DD) drains the 2ND-1 levels to
 //               registers, recombines them exactly (int64 -> binary64, scale by
 //               2^(gA + gB)) and releases TMEM at once; NB = 2 (TD/QD/TS) reads
-//               them in place from a double-buffered accumulator.
+//               them in place from double-buffered accumulators; TS keeps 4
+//               buffers and updates C once per two pairs.
 //               Then the K-word read-modify-write of the thread's column
 //               segment, ping-pong C prefetch, 16-byte accesses.  setmaxnreg
 //               moves registers from the producer/MMA warpgroup (40) to the
@@ -111,6 +112,13 @@ constexpr int kEpiUnroll = OZK_I8_EPI_UNROLL;
 #ifndef OZK_I8_TS_TR
 #define OZK_I8_TS_TR 112
 #endif
+// TS (one level per pair): TMEM accumulator buffers; 4 = two pairs share each
+// C read-modify-write while the MMAs fill the other two (TS slice GEMM 92.5 ->
+// 90.0 ms vs 2 buffers, bit-identical; binary64 formats need 240-320 columns
+// per buffer, so 4 do not fit)
+#ifndef OZK_I8_TS_NB
+#define OZK_I8_TS_NB 4
+#endif
 #ifndef OZK_I8_PACE
 #define OZK_I8_PACE 1
 #endif
@@ -158,7 +166,8 @@ struct I8Cfg {
         (kLaunchRegs + (kLaunchRegs - 40) / EG) / 8 * 8 > 232
             ? 232 : (kLaunchRegs + (kLaunchRegs - 40) / EG) / 8 * 8;
     static_assert(kStages >= 2, "operand ring too small");
-    static_assert(NB * kBufCols <= 512 && (NB == 1 || NB == 2), "TMEM accumulator buffers");
+    static_assert(NB * kBufCols <= 512 && (NB == 1 || NB == 2 || NB == 4),
+                  "TMEM accumulator buffers");
     static_assert(NB == 2 || kEpiRows % 4 == 0, "drain width");
     static_assert(ND * TR <= 256 && TR % 16 == 0, "stacked MMA width");
     static_assert(kATile % (8 * BKB) == 0, "A-digit tiles must stack in 8-row swizzle groups");
@@ -486,10 +495,10 @@ pair_gemm_i8_kernel(const __grid_constant__ MapsI8 maps, const __grid_constant__
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~uintptr_t(1023));
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
-    // bars: full[S], empty[S], tmem_full[2], tmem_empty[2] ; then the TMEM base word
+    // bars: full[S], empty[S], tmem_full[NB], tmem_empty[NB] ; then the TMEM base word
     const uint32_t full0 = smem_u32(bars), empty0 = full0 + 8 * kStages;
-    const uint32_t tfull0 = empty0 + 8 * kStages, tempty0 = tfull0 + 16;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 4);
+    const uint32_t tfull0 = empty0 + 8 * kStages, tempty0 = tfull0 + 8 * NB;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 2 * NB);
     const uint32_t ring = smem_u32(smem);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -517,7 +526,7 @@ pair_gemm_i8_kernel(const __grid_constant__ MapsI8 maps, const __grid_constant__
             mbar_init(full0 + 8 * s, 1);
             mbar_init(empty0 + 8 * s, CM + CN - 1);
         }
-        for (int b = 0; b < 2; ++b) {
+        for (int b = 0; b < NB; ++b) {
             mbar_init(tfull0 + 8 * b, 1);
             mbar_init(tempty0 + 8 * b, 4 * EG);  // one arrive per epilogue warp
         }
@@ -643,8 +652,8 @@ pair_gemm_i8_kernel(const __grid_constant__ MapsI8 maps, const __grid_constant__
         int step = 0;
         for (int g = cluster_id; g < num_groups; g += num_clusters) {
             for (int p = 0; p < npairs; ++p, ++step) {
-                // accumulator buffer step % 2, free once the epilogue of step - 2 is done
-                const int buf = NB == 2 ? step & 1 : 0;
+                // accumulator buffer step % NB, free once the epilogue of step - NB is done
+                const int buf = step % NB;
                 trace_stamp(step, 0, lane == 0);
                 mbar_wait(tempty0 + 8 * buf, ((step / NB) & 1) ^ 1);
                 trace_stamp(step, 1, lane == 0);
@@ -726,6 +735,7 @@ pair_gemm_i8_kernel(const __grid_constant__ MapsI8 maps, const __grid_constant__
         // the tile), and the buffer is released after the last chunk: the
         // MMAs of the next pair run meanwhile in the other buffer.
         constexpr int kChunk = Cfg::kChunk;
+        constexpr int PG = NB == 4 ? 2 : 1;  // slice pairs per C read-modify-write
         const int eg = (warp - 4) / 4;
         const int wq = warp % 4;
         const uint32_t tlane = tmem + ((uint32_t)(wq * 32) << 16) + eg * kEpiRows;
@@ -739,17 +749,27 @@ pair_gemm_i8_kernel(const __grid_constant__ MapsI8 maps, const __grid_constant__
             const bool col_ok = col < prob.n;
             // out-of-range lanes and rows read a valid element and never store
             const size_t col_c = col_ok ? col : prob.n - 1;
-            for (int p = 0; p < npairs; ++p, ++step) {
-                const int buf = NB == 2 ? step & 1 : 0;
-                const int al = pairs.alpha[p], be = pairs.beta[p];
-                const int gb = prob.gB[(size_t)be * prob.gB_stride + col_c];
-                const int* gap = prob.gA + (size_t)al * prob.gA_stride;
+            for (int p = 0; p < npairs;) {
+                // PG = 2 (4 TMEM buffers): consecutive pairs p, p + 1 share one C
+                // read-modify-write, their K-word adds in the reference order
+                const int np = (PG == 2 && p + 1 < npairs) ? 2 : 1;
+                int gbq[PG];
+                const int* gapq[PG];
+                uint32_t tbufq[PG];
+#pragma unroll
+                for (int q = 0; q < PG; ++q) {
+                    const int pq = q < np ? p + q : p;
+                    const int al = pairs.alpha[pq], be = pairs.beta[pq];
+                    gbq[q] = prob.gB[(size_t)be * prob.gB_stride + col_c];
+                    gapq[q] = prob.gA + (size_t)al * prob.gA_stride;
+                    tbufq[q] = tlane + ((step + q) % NB) * kBufCols;
+                }
                 const bool first = p == 0;  // C starts from zero
                 trace_stamp(step, 3, tracer);
-                mbar_wait(tfull0 + 8 * buf, (step / NB) & 1);
+                for (int q = 0; q < np; ++q)
+                    mbar_wait(tfull0 + 8 * ((step + q) % NB), ((step + q) / NB) & 1);
                 trace_stamp(step, 4, tracer);
                 asm volatile("tcgen05.fence::after_thread_sync;");
-                const uint32_t tbuf = tlane + buf * kBufCols;
                 W* const cbase = static_cast<W*>(prob.c);
                 auto row_of = [&](int r) -> size_t {
                     const size_t rr = row0 + r;
@@ -772,7 +792,7 @@ pair_gemm_i8_kernel(const __grid_constant__ MapsI8 maps, const __grid_constant__
                     }
                 };
                 // levels of rows [r, r + N) recombined to the exact binary64 products
-                auto read_levels = [&](int r, auto& y) {
+                auto read_levels = [&](int r, auto& y, uint32_t tbuf) {
                     constexpr int N = sizeof(y) / sizeof(double);
                     int32_t lv[kLevels][N];
 #pragma unroll
@@ -794,36 +814,41 @@ pair_gemm_i8_kernel(const __grid_constant__ MapsI8 maps, const __grid_constant__
                     for (int r = 0; r < kEpiRows; r += (kEpiRows % 16 == 0 ? 16 : 4)) {
                         double (&ys)[kEpiRows % 16 == 0 ? 16 : 4] =
                             *reinterpret_cast<double (*)[kEpiRows % 16 == 0 ? 16 : 4]>(yall + r);
-                        read_levels(r, ys);
+                        read_levels(r, ys, tbufq[0]);
                     }
 #if !(defined(OZK_I8_EPI_MODE) && OZK_I8_EPI_MODE == 3)
                     asm volatile("tcgen05.fence::before_thread_sync;");
                     __syncwarp();
-                    if (lane == 0) mbar_arrive(tempty0 + 8 * buf);
+                    if (lane == 0) mbar_arrive(tempty0 + 8 * (step % NB));
 #endif
                 }
                 auto update_chunk = [&](int r, W (&w)[kChunk][K]) {
-                    double yc[kChunk];
+                    double yc[PG][kChunk];
                     if constexpr (NB == 1) {
                         // this chunk's products are yall[0..kChunk); shift the rest
                         // down so every register index stays static
 #pragma unroll
-                        for (int j = 0; j < kChunk; ++j) yc[j] = yall[j];
+                        for (int j = 0; j < kChunk; ++j) yc[0][j] = yall[j];
 #pragma unroll
                         for (int j = 0; j < kEpiRows - kChunk; ++j) yall[j] = yall[j + kChunk];
                     } else {
-                        read_levels(r, yc);
+                        read_levels(r, yc[0], tbufq[0]);
+                        if (PG == 2 && np == 2) read_levels(r, yc[PG - 1], tbufq[PG - 1]);
                     }
 #pragma unroll
                     for (int j = 0; j < kChunk; ++j) {
-                        const double y = yc[j];
-                        const int ga = __ldg(gap + row_of(r + j));
-                        // exact scaled slice product (a TS product is exact in binary32)
+#pragma unroll
+                        for (int q = 0; q < PG; ++q) {
+                            if (q >= np) break;
+                            const double y = yc[q][j];
+                            const int ga = __ldg(gapq[q] + row_of(r + j));
+                            // exact scaled slice product (a TS product is exact in binary32)
 #if defined(OZK_I8_EPI_MODE) && OZK_I8_EPI_MODE == 2
-                        w[j][0] += (W)ldexp_fast(y, ga + gb);  // diagnostic: no K-word add
+                            w[j][0] += (W)ldexp_fast(y, ga + gbq[q]);  // diagnostic: no K-word add
 #else
-                        kw_add<K>(w[j], (W)ldexp_fast(y, ga + gb));
+                            kw_add<K>(w[j], (W)ldexp_fast(y, ga + gbq[q]));
 #endif
+                        }
                     }
 #pragma unroll
                     for (int j = 0; j < kChunk; ++j) {
@@ -846,15 +871,18 @@ pair_gemm_i8_kernel(const __grid_constant__ MapsI8 maps, const __grid_constant__
 #if defined(OZK_I8_EPI_MODE) && OZK_I8_EPI_MODE == 3
                 if (true) {  // diagnostic: the next pair's MMAs wait for the whole epilogue
 #else
-                if constexpr (NB == 2) {
+                if constexpr (NB >= 2) {
 #endif
-                    // all levels read: hand the buffer back to the MMA issuer
+                    // all levels read: hand the buffers back to the MMA issuer
                     asm volatile("tcgen05.fence::before_thread_sync;");
                     __syncwarp();
-                    if (lane == 0) mbar_arrive(tempty0 + 8 * buf);
+                    if (lane == 0)
+                        for (int q = 0; q < np; ++q) mbar_arrive(tempty0 + 8 * ((step + q) % NB));
                 }
                 trace_stamp(step, 5, tracer);
                 trace_stamp(step, 6, tracer);
+                p += np;
+                step += np;
             }
         }
     }
@@ -1016,7 +1044,7 @@ cudaError_t launch_i8_typed(const I8Operands& op, const PairList& pairs, cudaStr
 I8Geometry pair_gemm_i8_geometry(int K, int word_bytes, int nd, int num_sms) {
     if (word_bytes == 4) {
         if (K == 3 && nd == 1)
-            return geometry_typed<3, float, 1, OZK_I8_TS_TR, OZK_I8_TS_EG, OZK_I8_CM, OZK_I8_CN, 2>(num_sms);
+            return geometry_typed<3, float, 1, OZK_I8_TS_TR, OZK_I8_TS_EG, OZK_I8_CM, OZK_I8_CN, OZK_I8_TS_NB>(num_sms);
         if (K == 3 && nd == 2)
             return geometry_typed<3, float, 2, 64, 4, OZK_I8_CM, OZK_I8_CN, 2>(num_sms);
         return I8Geometry{};
@@ -1035,7 +1063,7 @@ cudaError_t launch_pair_gemm_i8(int K, int word_bytes, const I8Operands& op,
     if (word_bytes == 4) {  // TS: binary32 words, 1 or 2 digits
         if (K != 3) return cudaErrorInvalidValue;
         if (op.nd == 1)
-            return launch_i8_typed<3, float, 1, OZK_I8_TS_TR, OZK_I8_TS_EG, OZK_I8_CM, OZK_I8_CN>(op, pairs, st, num_sms);
+            return launch_i8_typed<3, float, 1, OZK_I8_TS_TR, OZK_I8_TS_EG, OZK_I8_CM, OZK_I8_CN, OZK_I8_TS_NB>(op, pairs, st, num_sms);
         if (op.nd == 2)
             return launch_i8_typed<3, float, 2, 64, 4, OZK_I8_CM, OZK_I8_CN>(op, pairs, st, num_sms);
         return cudaErrorInvalidValue;
