@@ -115,7 +115,8 @@ constexpr int kEpiUnroll = OZK_I8_EPI_UNROLL;
 // TS (one level per pair): TMEM accumulator buffers; 4 = two pairs share each
 // C read-modify-write while the MMAs fill the other two (TS slice GEMM 92.5 ->
 // 90.0 ms vs 2 buffers, bit-identical; binary64 formats need 240-320 columns
-// per buffer, so 4 do not fit)
+// per buffer, so 4 do not fit).  8 buffers (4 pairs per pass) need 64-row
+// tiles: 112 ms with 4 epilogue warpgroups, 129 with 2 -- worse.
 #ifndef OZK_I8_TS_NB
 #define OZK_I8_TS_NB 4
 #endif
@@ -145,7 +146,8 @@ struct I8Cfg {
     static constexpr int kATile = TR * BKB;   // one A digit (C rows), MMA operand B
     static constexpr int kStageBytes = ND * (kATile + kBTile);
     static constexpr int kStages = kSmemBudget / kStageBytes < 8 ? kSmemBudget / kStageBytes : 8;
-    static constexpr int kSmemBytes = kStages * kStageBytes + 1024 + 256;
+    // + 1024 alignment slack + barriers (2 per stage, 2 per TMEM buffer) and the TMEM word
+    static constexpr int kSmemBytes = kStages * kStageBytes + 1024 + 512;
     static constexpr int kBufCols = kLevels * TR;  // one accumulator buffer
     static constexpr int kTmemCols = NB * kBufCols <= 32 ? 32 : NB * kBufCols <= 64 ? 64
                                    : NB * kBufCols <= 128 ? 128 : NB * kBufCols <= 256 ? 256 : 512;
@@ -166,7 +168,8 @@ struct I8Cfg {
         (kLaunchRegs + (kLaunchRegs - 40) / EG) / 8 * 8 > 232
             ? 232 : (kLaunchRegs + (kLaunchRegs - 40) / EG) / 8 * 8;
     static_assert(kStages >= 2, "operand ring too small");
-    static_assert(NB * kBufCols <= 512 && (NB == 1 || NB == 2 || NB == 4),
+    static_assert((2 * kStages + 2 * NB) * 8 + 4 <= 512, "barrier area");
+    static_assert(NB * kBufCols <= 512 && (NB == 1 || NB == 2 || NB == 4 || NB == 8),
                   "TMEM accumulator buffers");
     static_assert(NB == 2 || kEpiRows % 4 == 0, "drain width");
     static_assert(ND * TR <= 256 && TR % 16 == 0, "stacked MMA width");
@@ -735,7 +738,7 @@ pair_gemm_i8_kernel(const __grid_constant__ MapsI8 maps, const __grid_constant__
         // the tile), and the buffer is released after the last chunk: the
         // MMAs of the next pair run meanwhile in the other buffer.
         constexpr int kChunk = Cfg::kChunk;
-        constexpr int PG = NB == 4 ? 2 : 1;  // slice pairs per C read-modify-write
+        constexpr int PG = NB >= 4 ? NB / 2 : 1;  // slice pairs per C read-modify-write
         const int eg = (warp - 4) / 4;
         const int wq = warp % 4;
         const uint32_t tlane = tmem + ((uint32_t)(wq * 32) << 16) + eg * kEpiRows;
@@ -750,9 +753,10 @@ pair_gemm_i8_kernel(const __grid_constant__ MapsI8 maps, const __grid_constant__
             // out-of-range lanes and rows read a valid element and never store
             const size_t col_c = col_ok ? col : prob.n - 1;
             for (int p = 0; p < npairs;) {
-                // PG = 2 (4 TMEM buffers): consecutive pairs p, p + 1 share one C
-                // read-modify-write, their K-word adds in the reference order
-                const int np = (PG == 2 && p + 1 < npairs) ? 2 : 1;
+                // PG = NB / 2 (>= 4 TMEM buffers): consecutive pairs p .. p+np-1
+                // share one C read-modify-write, their K-word adds in the
+                // reference order, while the MMAs fill the other NB / 2 buffers
+                const int np = npairs - p < PG ? npairs - p : PG;
                 int gbq[PG];
                 const int* gapq[PG];
                 uint32_t tbufq[PG];
@@ -832,8 +836,9 @@ pair_gemm_i8_kernel(const __grid_constant__ MapsI8 maps, const __grid_constant__
 #pragma unroll
                         for (int j = 0; j < kEpiRows - kChunk; ++j) yall[j] = yall[j + kChunk];
                     } else {
-                        read_levels(r, yc[0], tbufq[0]);
-                        if (PG == 2 && np == 2) read_levels(r, yc[PG - 1], tbufq[PG - 1]);
+#pragma unroll
+                        for (int q = 0; q < PG; ++q)
+                            if (q < np) read_levels(r, yc[q], tbufq[q]);
                     }
 #pragma unroll
                     for (int j = 0; j < kChunk; ++j) {
