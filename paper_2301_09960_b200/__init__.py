@@ -1,9 +1,10 @@
-"""B200-native Ozaki-scheme multiple-precision GEMM (DD / TD / QD).
+"""B200-native Ozaki-scheme multiple-precision GEMM (DD / TD / QD / TS).
 
 The product is ``lib/libozk.so`` (CUDA kernels for sm_100a behind the C-ABI
 in ``include/ozk.h``).  ``mpmat`` mirrors the reference mpmat hot-path API on
-top of it; ``slices`` exposes the slice-level device entry points used for
-C block-row sharding across GPUs.
+top of it; ``sharded`` is the C block-row sharded path across GPUs (one
+process per GPU, NCCL all-gather of the B digit planes); ``bench_csv`` reads
+and writes the reference's CSV v1 benchmark records.
 """
 from ._lib import LIB_PATH, lib  # noqa: F401  (raises if libozk.so is missing)
 from .mpmat import (  # noqa: F401
