@@ -181,7 +181,7 @@ double ozk_auto_drop_threshold(ozk_format fmt, size_t inner_dim);
  * digits: split_count x nd x plane_rows x ld8 int8 (ld8 >= inner dimension, a
  * multiple of 16, zero padded), exps: split_count x plane_rows ints.  nd is
  * ozk_int8_digits(fmt, inner, split_count); 0 means the engine does not apply
- * (binary64 slices at inner dimension <= 512, or inner >= 43690).  The products
+ * (binary64 slices at inner dimension <= 128, or inner >= 43690).  The products
  * and the K-word accumulation are bit-identical to ozk_slices_gemm_device. */
 int ozk_int8_digits(ozk_format fmt, size_t inner_dim, int split_count);
 
@@ -234,6 +234,22 @@ ozk_status ozk_lu_trailing_update_device(ozk_format fmt, size_t tm, size_t pw, s
                                          const void* l21, size_t ldl, const void* u12,
                                          size_t ldu, void* a22, size_t lda, int split_count,
                                          void* stream);
+
+/* ---- multi-GPU, one process (SURVEY §8b ozk_ozaki_gemm_multi, §8e) -------- *
+ * ozk_ozaki_gemm on ngpus devices (devices[r], or 0..ngpus-1 when devices is
+ * NULL) from host buffers, one host thread per device: device r owns C rows
+ * [r*m/ngpus, (r+1)*m/ngpus), splits its A rows and its B column block (per-row
+ * / per-column splits = the global split, ozaki.hpp:102-103), the B digit
+ * planes are all-gathered by peer copies (NVLink), slice maxima are combined
+ * on the host when drop > 0, and each device runs all pairs for its rows and
+ * copies its C rows back.  C is bit-identical to ozk_ozaki_gemm for any
+ * ngpus.  Where the INT8 engine does not apply (or DMMA is forced) each device
+ * runs ozk_ozaki_gemm on its rows against the whole B.  A device may repeat in
+ * `devices` (the kernels of different entries never wait on each other).
+ * prof (optional): total_seconds = slowest device, pairs, gpus, engine. */
+ozk_status ozk_ozaki_gemm_multi(ozk_format fmt, int ngpus, const int* devices, size_t m, size_t l,
+                                size_t n, const void* a, const void* b, int split_count,
+                                double drop_threshold, void* c, ozk_profile* prof);
 
 /* ---- host-buffer schedule (introspection) --------------------------------- *
  * The row bands ozk_ozaki_gemm's overlapped host path uses for an m x n C on

@@ -22,6 +22,7 @@ from .mpmat import (  # noqa: F401
     lu_trailing_update,
     ozaki_gemm,
     ozaki_gemm_auto,
+    ozaki_gemm_multi,
     param_error,
     shape_error,
     set_engine,
@@ -36,5 +37,5 @@ __all__ = [
     "ozaki_gemm", "param_error", "shape_error", "split_matrix", "split_shift_bits", "lib",
     "ts_direct_gemm", "lu_trailing_update", "set_engine", "get_engine", "io_error",
     "read_matrix_file", "write_matrix_file", "gemm_simple", "auto_split_policy",
-    "ozaki_gemm_auto",
+    "ozaki_gemm_auto", "ozaki_gemm_multi",
 ]

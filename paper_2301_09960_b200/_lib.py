@@ -55,6 +55,10 @@ SIGNATURES = {
                                               ctypes.c_void_p]),
     "ozk_auto_split_count": (ctypes.c_int, [ctypes.c_int, _sz]),
     "ozk_auto_drop_threshold": (ctypes.c_double, [ctypes.c_int, _sz]),
+    "ozk_ozaki_gemm_multi": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_void_p, _sz,
+                                            _sz, _sz, ctypes.c_void_p, ctypes.c_void_p,
+                                            ctypes.c_int, ctypes.c_double, ctypes.c_void_p,
+                                            ctypes.c_void_p]),
     "ozk_plan_row_bands": (ctypes.c_int, [ctypes.c_int, _sz, _sz, _sz, ctypes.c_int, _sz,
                                           ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                           ctypes.c_int, ctypes.c_void_p, ctypes.c_int]),

@@ -18,6 +18,8 @@
 #include <memory>
 #include <algorithm>
 #include <vector>
+#include <condition_variable>
+#include <thread>
 #include <cstdint>
 #include <tuple>
 #include <map>
@@ -966,6 +968,214 @@ int ozk_auto_split_count(ozk_format fmt, size_t inner_dim) {
     if (per <= 0) return kMaxSplits;
     const int d = (S * K + per - 1) / per + 2;
     return d < kMaxSplits ? d : kMaxSplits;
+}
+
+namespace {
+// Host barrier for the per-device threads of ozk_ozaki_gemm_multi.  Every
+// thread arrives at every barrier, failed or not, so none can hang.
+struct HostBarrier {
+    std::mutex mu;
+    std::condition_variable cv;
+    int n, count = 0, gen = 0;
+    explicit HostBarrier(int parties) : n(parties) {}
+    void arrive_and_wait() {
+        std::unique_lock<std::mutex> lk(mu);
+        const int g = gen;
+        if (++count == n) {
+            count = 0;
+            ++gen;
+            cv.notify_all();
+        } else {
+            cv.wait(lk, [&] { return gen != g; });
+        }
+    }
+};
+}  // namespace
+
+ozk_status ozk_ozaki_gemm_multi(ozk_format fmt, int ngpus, const int* devices, size_t m, size_t l,
+                                size_t n, const void* a, const void* b, int split_count,
+                                double drop, void* c, ozk_profile* prof) {
+    if (ozk_status s = check_gemm_args(fmt, m, l, n, split_count, drop)) return s;
+    if (ngpus < 1 || ngpus > 64) return fail(OZK_EPARAM, "ozaki_gemm_multi: 1..64 devices");
+    const int d = split_count;
+    const size_t eb = elem_bytes(fmt);
+    const int nd = engine_setting() != OZK_ENGINE_DMMA ? int8_digits(fmt, l, d) : 0;
+    const size_t ld8 = (l + 15) & ~size_t(15);
+    const size_t ncb = (n + ngpus - 1) / ngpus;  // B columns per device (ceil partition)
+    const size_t n_pad = ncb * (size_t)ngpus;
+    auto dev_of = [&](int r) { return devices ? devices[r] : r; };
+    auto rows_of = [&](int r, size_t& r0, size_t& r1) {
+        r0 = m * (size_t)r / ngpus;
+        r1 = m * (size_t)(r + 1) / ngpus;
+    };
+    HostBarrier bar(ngpus);
+    std::vector<ozk_status> st(ngpus, OZK_OK);
+    std::vector<std::string> msg(ngpus);
+    std::vector<int8_t*> b8_of(ngpus, nullptr);  // each device's gathered B digit planes
+    std::vector<int*> gb_of(ngpus, nullptr);
+    std::vector<double> maxima((size_t)ngpus * 2 * d, 0.0);
+    std::vector<double> secs(ngpus, 0.0);
+    std::atomic<bool> failed{false};
+    std::atomic<int> pairs_used{0};
+    auto worker = [&](int r) {
+        auto t0 = std::chrono::steady_clock::now();
+        size_t r0, r1;
+        rows_of(r, r0, r1);
+        const size_t rows = r1 - r0;
+        const size_t c0 = std::min(n, (size_t)r * ncb), c1 = std::min(n, c0 + ncb);
+        auto fail_here = [&](ozk_status s) {
+            st[r] = s;
+            msg[r] = g_last_error;
+            failed = true;
+        };
+        auto cuda_ok = [&](cudaError_t e, const char* what) {
+            if (e == cudaSuccess) return true;
+            fail_here(fail(OZK_ECUDA, std::string(what) + ": " + cudaGetErrorString(e)));
+            return false;
+        };
+        OwnStream os;
+        DevBuf da, db, dc, a8, ga, b8, gb, pmax;
+        bool ok = cuda_ok(cudaSetDevice(dev_of(r)), "ozaki_gemm_multi: device") &&
+                  cuda_ok(os.create(), "ozaki_gemm_multi: stream");
+        if (ok && nd == 0) {
+            // DMMA engine or an inner dimension the INT8 engine does not take:
+            // this device's rows against the whole B through the 1-GPU host path
+            if (rows) {
+                const ozk_status s2 = ozk_ozaki_gemm(fmt, rows, l, n,
+                                                     static_cast<const char*>(a) + r0 * l * eb, b,
+                                                     d, drop, static_cast<char*>(c) + r0 * n * eb,
+                                                     nullptr);
+                if (s2 != OZK_OK) fail_here(s2);
+            }
+            bar.arrive_and_wait();
+            bar.arrive_and_wait();
+            bar.arrive_and_wait();
+            secs[r] = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+            return;
+        }
+        // 1. copies in, splits: A rows locally, B column block into its place
+        //    in the full-width digit planes
+        if (ok) {
+            ok = cuda_ok(da.alloc(eb * std::max<size_t>(rows, 1) * l, os.s), "alloc A") &&
+                 cuda_ok(db.alloc(eb * l * std::max<size_t>(c1 - c0, 1), os.s), "alloc B") &&
+                 cuda_ok(dc.alloc(eb * std::max<size_t>(rows, 1) * n, os.s), "alloc C") &&
+                 cuda_ok(a8.alloc((size_t)d * nd * std::max<size_t>(rows, 1) * ld8, os.s), "alloc") &&
+                 cuda_ok(ga.alloc(sizeof(int) * d * std::max<size_t>(rows, 1), os.s), "alloc") &&
+                 cuda_ok(b8.alloc((size_t)d * nd * n_pad * ld8, os.s), "alloc") &&
+                 cuda_ok(gb.alloc(sizeof(int) * d * n_pad, os.s), "alloc") &&
+                 cuda_ok(pmax.alloc(sizeof(double) * 2 * d, os.s), "alloc") &&
+                 cuda_ok(cudaMemsetAsync(pmax.p, 0, sizeof(double) * 2 * d, os.s), "memset") &&
+                 cuda_ok(cudaMemsetAsync(b8.p, 0, (size_t)d * nd * n_pad * ld8, os.s), "memset") &&
+                 cuda_ok(cudaMemsetAsync(gb.p, 0, sizeof(int) * d * n_pad, os.s), "memset");
+        }
+        if (ok && rows)
+            ok = cuda_ok(cudaMemcpyAsync(da.p, static_cast<const char*>(a) + r0 * l * eb,
+                                         rows * l * eb, cudaMemcpyHostToDevice, os.s),
+                         "ozaki_gemm_multi: H2D A");
+        if (ok && c1 > c0)
+            ok = cuda_ok(cudaMemcpy2DAsync(db.p, (c1 - c0) * eb,
+                                           static_cast<const char*>(b) + c0 * eb, n * eb,
+                                           (c1 - c0) * eb, l, cudaMemcpyHostToDevice, os.s),
+                         "ozaki_gemm_multi: H2D B");
+        double* pm = pmax.as<double>();
+        if (ok && rows) {
+            const ozk_status s2 = ozk_split_digits_device(
+                fmt, rows, l, l, da.p, d, OZK_SIDE_ROWS, a8.as<int8_t>(), ld8, rows,
+                ga.as<int>(), drop > 0.0 ? pm : nullptr, os.s);
+            if (s2 != OZK_OK) fail_here(s2), ok = false;
+        }
+        if (ok && c1 > c0) {
+            const ozk_status s2 = ozk_split_digits_device(
+                fmt, l, c1 - c0, c1 - c0, db.p, d, OZK_SIDE_COLS, b8.as<int8_t>() + c0 * ld8, ld8,
+                n_pad, gb.as<int>() + c0, drop > 0.0 ? pm + d : nullptr, os.s);
+            if (s2 != OZK_OK) fail_here(s2), ok = false;
+        }
+        if (ok && drop > 0.0)
+            ok = cuda_ok(cudaMemcpy(maxima.data() + (size_t)r * 2 * d, pm, sizeof(double) * 2 * d,
+                                    cudaMemcpyDeviceToHost),
+                         "ozaki_gemm_multi: maxima");
+        b8_of[r] = b8.as<int8_t>();
+        gb_of[r] = gb.as<int>();
+        bar.arrive_and_wait();  // every device has split its block
+        // 2. all-gather of the B digit planes and exponents by peer copies
+        if (ok && !failed) {
+            for (int q = 0; q < ngpus && ok; ++q) {
+                if (q == r) continue;
+                const size_t q0 = std::min(n, (size_t)q * ncb), q1 = std::min(n, q0 + ncb);
+                if (q1 <= q0) continue;
+                for (int s2 = 0; s2 < d * nd && ok; ++s2) {
+                    const size_t off = ((size_t)s2 * n_pad + q0) * ld8;
+                    ok = cuda_ok(cudaMemcpyPeerAsync(b8_of[r] + off, dev_of(r), b8_of[q] + off,
+                                                     dev_of(q), (q1 - q0) * ld8, os.s),
+                                 "ozaki_gemm_multi: peer copy");
+                }
+                for (int s2 = 0; s2 < d && ok; ++s2) {
+                    const size_t off = (size_t)s2 * n_pad + q0;
+                    ok = cuda_ok(cudaMemcpyPeerAsync(gb_of[r] + off, dev_of(r), gb_of[q] + off,
+                                                     dev_of(q), (q1 - q0) * sizeof(int), os.s),
+                                 "ozaki_gemm_multi: peer copy");
+                }
+            }
+            if (ok) ok = cuda_ok(cudaStreamSynchronize(os.s), "ozaki_gemm_multi: gather");
+        }
+        bar.arrive_and_wait();  // no device frees what a peer still reads
+        // 3. pair list (global slice maxima with pruning), GEMM, C rows back
+        if (ok && !failed && rows) {
+            PairList pl;
+            if (drop > 0.0) {
+                std::vector<double> am(d, 0.0), bm(d, 0.0);
+                for (int q = 0; q < ngpus; ++q)
+                    for (int s2 = 0; s2 < d; ++s2) {
+                        am[s2] = std::max(am[s2], maxima[(size_t)q * 2 * d + s2]);
+                        bm[s2] = std::max(bm[s2], maxima[(size_t)q * 2 * d + d + s2]);
+                    }
+                pruned_pairs(d, am.data(), bm.data(), drop, pl);
+            } else {
+                triangular_pairs(d, pl);
+            }
+            pairs_used = pl.count;
+            if (pl.count == 0) {
+                ok = cuda_ok(cudaMemsetAsync(dc.p, 0, eb * rows * n, os.s), "memset C");
+            } else {
+                std::vector<int> flat(2 * (size_t)pl.count);
+                for (int p = 0; p < pl.count; ++p) {
+                    flat[2 * p] = pl.alpha[p];
+                    flat[2 * p + 1] = pl.beta[p];
+                }
+                const ozk_status s2 = ozk_digits_gemm_device(
+                    fmt, rows, l, n, a8.as<int8_t>(), ga.as<int>(), rows, b8.as<int8_t>(),
+                    gb.as<int>(), n_pad, ld8, d, flat.data(), pl.count, dc.p, n, os.s);
+                if (s2 != OZK_OK) fail_here(s2), ok = false;
+            }
+            if (ok)
+                ok = cuda_ok(cudaMemcpyAsync(static_cast<char*>(c) + r0 * n * eb, dc.p,
+                                             rows * n * eb, cudaMemcpyDeviceToHost, os.s),
+                             "ozaki_gemm_multi: D2H C") &&
+                     cuda_ok(cudaStreamSynchronize(os.s), "ozaki_gemm_multi");
+        }
+        bar.arrive_and_wait();
+        secs[r] = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    };
+    std::vector<std::thread> threads;
+    for (int r = 1; r < ngpus; ++r) threads.emplace_back(worker, r);
+    worker(0);
+    for (auto& t : threads) t.join();
+    for (int r = 0; r < ngpus; ++r)
+        if (st[r] != OZK_OK) {
+            g_last_error = msg[r];
+            return st[r];
+        }
+    if (prof) {
+        *prof = ozk_profile{};
+        prof->total_seconds = *std::max_element(secs.begin(), secs.end());
+        prof->split_count = d;
+        PairList pl;
+        triangular_pairs(d, pl);
+        prof->pairs = nd > 0 ? pairs_used.load() : pl.count;
+        prof->gpus = ngpus;
+        prof->engine = nd > 0 ? OZK_ENGINE_INT8 : OZK_ENGINE_DMMA;
+    }
+    return OZK_OK;
 }
 
 int ozk_plan_row_bands(ozk_format fmt, size_t m, size_t n, size_t l, int split_count,

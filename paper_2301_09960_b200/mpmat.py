@@ -229,6 +229,31 @@ def ozaki_gemm(a, b, d: int, backend=None, drop_threshold: float = 0.0):
     return c, OzakiProfile._of(prof)
 
 
+def ozaki_gemm_multi(a, b, d: int, devices=None, drop_threshold: float = 0.0):
+    """ozaki_gemm over several GPUs in one process (include/ozk.h
+    ozk_ozaki_gemm_multi): C block rows per device, B digit planes all-gathered
+    by peer copies; bit-identical to ozaki_gemm.  Host (numpy) arrays; devices:
+    list of CUDA device ids (a device may repeat), default all visible ones.
+    Returns (C, OzakiProfile)."""
+    m, l, ka = _kword_shape(a)
+    l2, n, kb = _kword_shape(b)
+    if ka != kb:
+        raise param_error("ozaki_gemm_multi: A and B must have the same format")
+    if l != l2:
+        raise shape_error("ozaki_gemm_multi: inner dimensions differ")
+    if devices is None:
+        import torch
+        devices = list(range(torch.cuda.device_count()))
+    devs = (ctypes.c_int * len(devices))(*[int(x) for x in devices])
+    ah, bh = _host(a, ka), _host(b, ka)
+    c = np.empty((m, n, _words(ka)), dtype=_dtype(ka))
+    prof = OzkProfile()
+    st = lib.ozk_ozaki_gemm_multi(ka, len(devices), devs, m, l, n, ah.ctypes.data, bh.ctypes.data,
+                                  int(d), float(drop_threshold), c.ctypes.data, ctypes.byref(prof))
+    _raise(st)
+    return c, OzakiProfile._of(prof)
+
+
 def auto_split_policy(fmt: int, inner_dim: int) -> tuple[int, float]:
     """(split_count, drop_threshold) of the automatic mode (include/ozk.h
     ozk_auto_split_count / ozk_auto_drop_threshold; not in the reference)."""

@@ -653,3 +653,31 @@ def test_acceptance_9_ozaki_faster_than_direct(ozk):
     t_dir = timed(lambda: lib.ozk_direct_gemm_device(2, n, n, n, A.data_ptr(), B.data_ptr(),
                                                      C.data_ptr(), st))
     assert t_dir >= 1.5 * t_oz, (t_oz, t_dir)
+
+
+@pytest.mark.parametrize("K,m,l,n,d,drop,devs", [
+    (3, 300, 700, 260, 9, 0.0, [0, 0]),          # INT8 engine, 2 entries on one GPU
+    (2, 257, 600, 131, 6, 2.0 ** -70, [0, 0, 0]),  # pruning: host max of the slice maxima
+    (4, 100, 300, 77, 12, 0.0, [0, 0, 0, 0]),     # ragged column blocks (77 = 20+20+20+17)
+    (2, 90, 100, 50, 6, 0.0, [0, 0]),             # l <= 128: per-device 1-GPU path
+    (3, 5, 200, 3, 4, 0.0, [0, 0, 0, 0]),         # fewer columns than devices
+    (2, 64, 300, 64, 5, 0.0, [0]),                # one device
+])
+def test_ozaki_gemm_multi_bitexact(ozk, cpu, K, m, l, n, d, drop, devs):
+    """ozk_ozaki_gemm_multi (one process, a host thread per device, B digit
+    planes all-gathered by peer copies) = the reference for any device count.
+    One GPU per box here, so the devices repeat; the kernels of different
+    entries never wait on each other."""
+    a = cpu.gen_eq1(K, m, l, 300 + K)
+    b = cpu.gen_eq1(K, l, n, 301 + K)
+    want = cpu.ozaki_gemm(K, a, b, d, drop)
+    got, prof = ozk.ozaki_gemm_multi(a, b, d, devices=devs, drop_threshold=drop)
+    assert_bitwise(got, want, f"multi K={K} {m}x{l}x{n} D={d} drop={drop} devs={devs}")
+
+
+def test_ozaki_gemm_multi_ts(ozk, port):
+    a = port.gen_eq1_ts(120, 1100, 7)
+    b = port.gen_eq1_ts(1100, 90, 8)
+    want = port.ozaki_gemm_ts(a, b, 10)
+    got, _ = ozk.ozaki_gemm_multi(a, b, 10, devices=[0, 0, 0])
+    assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
