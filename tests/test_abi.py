@@ -91,6 +91,13 @@ def test_argument_errors_without_gpu():
     assert lib.ozk_ozaki_gemm(7, 2, 2, 2, None, None, 2, 0.0, None, None) == 2
     assert lib.ozk_split(2, 2, 2, None, 0, 0, None, None) == 2
     assert b"split count" in lib.ozk_last_error()
+    # the one-process multi-GPU entry point checks the same arguments first
+    assert lib.ozk_ozaki_gemm_multi(2, 2, None, 0, 2, 2, None, None, 2, 0.0, None, None) == 1
+    assert lib.ozk_ozaki_gemm_multi(2, 2, None, 2, 2, 2, None, None, 0, 0.0, None, None) == 2
+    assert lib.ozk_ozaki_gemm_multi(2, 0, None, 2, 2, 2, None, None, 2, 0.0, None, None) == 2
+    assert b"devices" in lib.ozk_last_error()
+    with pytest.raises(ozk.shape_error):
+        ozk.ozaki_gemm_multi(a, np.zeros((3, 2, 2)), 2, devices=[0])
 
 
 def test_pair_list_matches_reference_order(port):
