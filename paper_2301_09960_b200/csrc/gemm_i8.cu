@@ -117,6 +117,12 @@ constexpr int kEpiUnroll = OZK_I8_EPI_UNROLL;
 // 90.0 ms vs 2 buffers, bit-identical; binary64 formats need 240-320 columns
 // per buffer, so 4 do not fit).  8 buffers (4 pairs per pass) need 64-row
 // tiles: 112 ms with 4 epilogue warpgroups, 129 with 2 -- worse.
+// TS epilogue K-word compares on the integer bits (1) or as FP32 compares (0):
+// same results; 1 measured faster (90.1 vs 91.7 ms) although the TS epilogue
+// is issue-bound and integer ops dominate its samples
+#ifndef OZK_I8_TS_INTCMP
+#define OZK_I8_TS_INTCMP 1
+#endif
 #ifndef OZK_I8_TS_NB
 #define OZK_I8_TS_NB 4
 #endif
@@ -739,6 +745,9 @@ pair_gemm_i8_kernel(const __grid_constant__ MapsI8 maps, const __grid_constant__
         // MMAs of the next pair run meanwhile in the other buffer.
         constexpr int kChunk = Cfg::kChunk;
         constexpr int PG = NB >= 4 ? NB / 2 : 1;  // slice pairs per C read-modify-write
+        // K-word compares on integer halves where FP64 is the contended pipe
+        // (binary64 words); binary32 (TS) words: see OZK_I8_TS_INTCMP
+        constexpr bool kEpiIntCmp = sizeof(W) == 8 ? true : (OZK_I8_TS_INTCMP != 0);
         const int eg = (warp - 4) / 4;
         const int wq = warp % 4;
         const uint32_t tlane = tmem + ((uint32_t)(wq * 32) << 16) + eg * kEpiRows;
@@ -851,7 +860,7 @@ pair_gemm_i8_kernel(const __grid_constant__ MapsI8 maps, const __grid_constant__
 #if defined(OZK_I8_EPI_MODE) && OZK_I8_EPI_MODE == 2
                             w[j][0] += (W)ldexp_fast(y, ga + gbq[q]);  // diagnostic: no K-word add
 #else
-                            kw_add<K>(w[j], (W)ldexp_fast(y, ga + gbq[q]));
+                            kw_add<K, W, kEpiIntCmp>(w[j], (W)ldexp_fast(y, ga + gbq[q]));
 #endif
                         }
                     }
