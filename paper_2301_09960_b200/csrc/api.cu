@@ -181,19 +181,19 @@ ozk_status check_dev_err(int flag, const char* what) {
 cudaError_t split_to_slices(int fmt, size_t rows, size_t cols, size_t ld, const void* mat, int d,
                             int side, double* slices, size_t plane_rows, void* work,
                             unsigned long long* pmax, int* err, cudaStream_t st,
-                            const DigitOut& dig = DigitOut{}) {
+                            const DigitOut& dig = DigitOut{}, bool keep_residual = false) {
     const int K = words_of(fmt), wb = word_bytes_of(fmt);
     const size_t inner = side == OZK_SIDE_ROWS ? cols : rows;
     const size_t ldk = slice_ld(inner);
     const int sigma = shift_bits(inner, wb == 4 ? 24 : 53);
     if (side == OZK_SIDE_ROWS)
         return launch_split_rows(K, wb, mat, ld, work, rows, cols, d, sigma, slices, ldk,
-                                 plane_rows * ldk, pmax, err, st, dig);
+                                 plane_rows * ldk, pmax, err, st, dig, keep_residual);
     // columns: transpose to (cols x rows) so each column is a contiguous row
     cudaError_t e = launch_transpose(K, wb, mat, ld, work, rows, rows, cols, st);
     if (e != cudaSuccess) return e;
     return launch_split_rows(K, wb, work, rows, work, cols, rows, d, sigma, slices, ldk,
-                             plane_rows * ldk, pmax, err, st, dig);
+                             plane_rows * ldk, pmax, err, st, dig, keep_residual);
 }
 
 struct Timer {
@@ -814,7 +814,7 @@ ozk_status ozk_split(ozk_format fmt, size_t rows, size_t cols, const void* mat, 
     OZK_CUDA(cudaMemsetAsync(flags.p, 0, 8, os.s), "split_matrix: memset");
     OZK_CUDA(cudaMemcpyAsync(dm.p, mat, eb * N, cudaMemcpyHostToDevice, os.s), "split_matrix: H2D");
     OZK_CUDA(split_to_slices(fmt, rows, cols, cols, dm.p, d, side, sl.as<double>(), outer, work.p,
-                             nullptr, flags.as<int>(), os.s),
+                             nullptr, flags.as<int>(), os.s, DigitOut{}, /*keep_residual=*/true),
              "split_matrix");
     int flag = 0;
     OZK_CUDA(cudaMemcpyAsync(&flag, flags.p, sizeof(int), cudaMemcpyDeviceToHost, os.s),

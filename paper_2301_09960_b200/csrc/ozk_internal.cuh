@@ -22,6 +22,8 @@ inline size_t slice_ld(size_t inner) { return (inner + 1) & ~size_t(1); }
 // K1: per-row Ozaki split of a K-word matrix (ozaki.hpp:74-147, side rows).
 //   in      : rows x cols K-word AoS, row stride in_ld elements (may alias work)
 //   work    : rows x cols K-word AoS scratch (row stride cols); holds the residual
+//             after the last pass only when keep_residual (else its last pass
+//             update is skipped: the GEMM path never reads it)
 //   pieces  : d slices, slice a row r at pieces + a*slice_stride + r*ldk
 //   piece_max (optional): d values, max |piece_a| as ordered uint64 bits
 //   err     : device flag (DevErr)
@@ -42,7 +44,8 @@ struct DigitOut {
 cudaError_t launch_split_rows(int K, int word_bytes, const void* in, size_t in_ld, void* work,
                               size_t rows, size_t cols, int d, int sigma, double* pieces,
                               size_t ldk, size_t slice_stride, unsigned long long* piece_max,
-                              int* err, cudaStream_t st, const DigitOut& dig = DigitOut{});
+                              int* err, cudaStream_t st, const DigitOut& dig = DigitOut{},
+                              bool keep_residual = true);
 
 // Transpose of a K-word matrix: out(j, i) = in(i, j).  in is rows x cols with
 // row stride in_ld elements; out is cols x rows with row stride out_ld elements.

@@ -112,15 +112,16 @@ __global__ void __launch_bounds__(kSplitThreads)
 split_rows_kernel(const T* __restrict__ in, size_t in_ld, T* __restrict__ work, size_t cols,
                   int d, int sigma, double* __restrict__ pieces, size_t ldk,
                   size_t slice_stride, unsigned long long* __restrict__ piece_max,
-                  int* __restrict__ err, DigitOut dig) {
+                  int* __restrict__ err, DigitOut dig, bool keep_residual) {
     __shared__ double red[33];
     const size_t r = blockIdx.x;
     const T* src = in + r * in_ld * K;
     T* w = work + r * cols * K;
     double* prow = pieces ? pieces + r * ldk : nullptr;
 
-    // Sweep 0: leading image max, finiteness scan (ozaki.hpp:77-78), and the
-    // copy of the input row into the working residual.
+    // Sweep 0: leading image max and finiteness scan (ozaki.hpp:77-78).  For
+    // D >= 2 the copy of the input row into the working residual is left to
+    // pass 0, which reads the input and stores every residual element.
     T mx = T(0);
     int bad = 0;
     for (size_t j = threadIdx.x; j < cols; j += kSplitThreads) {
@@ -128,7 +129,7 @@ split_rows_kernel(const T* __restrict__ in, size_t in_ld, T* __restrict__ work, 
         load_kw<K>(src + j * K, c);
         bad |= !is_finite(c[0]);
         mx = fmax(mx, fabs_(c[0]));
-        if (src != w) store_kw<K>(w + j * K, c);
+        if (d == 1 && src != w) store_kw<K>(w + j * K, c);
     }
     if (__syncthreads_or(bad)) {
         if (threadIdx.x == 0) atomicMax(err, (int)kDevNonFinite);
@@ -145,8 +146,10 @@ split_rows_kernel(const T* __restrict__ in, size_t in_ld, T* __restrict__ work, 
             load_kw<K>(w + j * K, c);
             const T lead = c[0];
             prow[j] = (double)lead;
-            kw_add<K>(c, -lead);
-            store_kw<K>(w + j * K, c);
+            if (keep_residual) {
+                kw_add<K>(c, -lead);
+                store_kw<K>(w + j * K, c);
+            }
             pmx = fmax(pmx, (double)fabs_(lead));
         }
         for (size_t j = cols + threadIdx.x; j < ldk; j += kSplitThreads) prow[j] = 0.0;
@@ -171,6 +174,13 @@ split_rows_kernel(const T* __restrict__ in, size_t in_ld, T* __restrict__ work, 
         }
         T nmx = T(0);
         double pmx = 0.0;
+        // the last pass updates the residual only when the caller reads it
+        // (ozk_split); the GEMM path drops it (ozaki.hpp:235 never reads it)
+        const bool update = keep_residual || a + 1 < d;
+        // pass 0 reads the input row; it must store every element when the
+        // residual row is a separate buffer (it was not copied in sweep 0)
+        const T* rd = a == 0 ? src : w;
+        const bool store_all = a == 0 && src != w;
         // INT8-digit output: the slice row is an integer multiple of 2^g,
         // g = e + sigma - S: every piece is an integer multiple of this grid
         // (ozaki.hpp:15-29: (v + tau) - tau lands on multiples of ulp of the
@@ -188,11 +198,16 @@ split_rows_kernel(const T* __restrict__ in, size_t in_ld, T* __restrict__ work, 
                 if (pa) pa[j] = 0.0;
                 if (drow)
                     for (int q = 0; q < dig.nd; ++q) drow[j + q * dig.digit_stride] = 0;
+                if (store_all) {  // skipped row: the residual is the input row
+                    T c[K];
+                    load_kw<K>(src + j * K, c);
+                    store_kw<K>(w + j * K, c);
+                }
             }
         } else {
             auto element = [&](size_t j) {
                 T c[K];
-                load_kw<K>(w + j * K, c);
+                load_kw<K>(rd + j * K, c);
                 // shift_extract: (v + tau) - tau, strictly rounded (ozaki.hpp:53-56)
                 const T x = rn_sub(rn_add(c[0], tau), tau);
                 if (pa) pa[j] = (double)x;
@@ -206,10 +221,12 @@ split_rows_kernel(const T* __restrict__ in, size_t in_ld, T* __restrict__ work, 
                     }
                     drow[j + (dig.nd - 1) * dig.digit_stride] = (int8_t)mi;
                 }
-                if (x != T(0)) {
+                if (update && x != T(0)) {
                     // w -= x  ==  w + (-x)  (multifloat.hpp:302,391); FP64 compares:
                     // this kernel is ALU-bound, its FP64 pipe mostly idle
                     kw_add<K, T, false>(c, -x);
+                    store_kw<K>(w + j * K, c);
+                } else if (store_all) {
                     store_kw<K>(w + j * K, c);
                 }
                 nmx = fmax(nmx, fabs_(c[0]));
@@ -230,7 +247,7 @@ split_rows_kernel(const T* __restrict__ in, size_t in_ld, T* __restrict__ work, 
                 atomicMax(piece_max + a,
                           static_cast<unsigned long long>(__double_as_longlong(pmx)));
         }
-        mx = (T)block_max((double)nmx, red);
+        if (update) mx = (T)block_max((double)nmx, red);
     }
 }
 
@@ -263,14 +280,15 @@ __global__ void transpose_kernel(const T* __restrict__ in, size_t in_ld, T* __re
 cudaError_t launch_split_rows(int K, int word_bytes, const void* in, size_t in_ld, void* work,
                               size_t rows, size_t cols, int d, int sigma, double* pieces,
                               size_t ldk, size_t slice_stride, unsigned long long* piece_max,
-                              int* err, cudaStream_t st, const DigitOut& dig) {
+                              int* err, cudaStream_t st, const DigitOut& dig,
+                              bool keep_residual) {
     if (rows == 0) return cudaSuccess;
     dim3 grid((unsigned)rows), block(kSplitThreads);
 #define OZK_SPLIT(KK, TT)                                                                         \
     split_rows_kernel<KK, TT><<<grid, block, 0, st>>>(static_cast<const TT*>(in), in_ld,          \
                                                       static_cast<TT*>(work), cols, d, sigma,     \
                                                       pieces, ldk, slice_stride, piece_max, err, \
-                                                      dig)
+                                                      dig, keep_residual)
     if (word_bytes == 4) {
         if (K != 3) return cudaErrorInvalidValue;
         OZK_SPLIT(3, float);
