@@ -124,12 +124,22 @@ split_rows_kernel(const T* __restrict__ in, size_t in_ld, T* __restrict__ work, 
     // pass 0, which reads the input and stores every residual element.
     T mx = T(0);
     int bad = 0;
-    for (size_t j = threadIdx.x; j < cols; j += kSplitThreads) {
-        T c[K];
-        load_kw<K>(src + j * K, c);
-        bad |= !is_finite(c[0]);
-        mx = fmax(mx, fabs_(c[0]));
-        if (d == 1 && src != w) store_kw<K>(w + j * K, c);
+    if (d == 1 && src != w) {
+        for (size_t j = threadIdx.x; j < cols; j += kSplitThreads) {
+            T c[K];
+            load_kw<K>(src + j * K, c);
+            bad |= !is_finite(c[0]);
+            mx = fmax(mx, fabs_(c[0]));
+            store_kw<K>(w + j * K, c);
+        }
+    } else {
+        // only the leading words: MultiFloat::is_finite and leading_image look
+        // at c[0] alone (multifloat.hpp:176, dense_matrix.hpp:91-96)
+        for (size_t j = threadIdx.x; j < cols; j += kSplitThreads) {
+            const T c0 = src[j * K];
+            bad |= !is_finite(c0);
+            mx = fmax(mx, fabs_(c0));
+        }
     }
     if (__syncthreads_or(bad)) {
         if (threadIdx.x == 0) atomicMax(err, (int)kDevNonFinite);
