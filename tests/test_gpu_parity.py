@@ -60,6 +60,25 @@ def test_split_zero_rows_and_cols(ozk, cpu):
         assert all((p == 0).all() for p in s.pieces)
 
 
+def test_split_skipped_rows_keep_their_residual(ozk, cpu):
+    # A row whose leading words are all zero is skipped on every pass
+    # (ozaki.hpp:105-107) and keeps its input as the residual, tail words
+    # included.  The row split reads the input in pass 0 instead of copying it
+    # in sweep 0, so the skipped branch writes the residual itself: dirty the
+    # device pool first so a missing write shows up as stale words.
+    big = cpu.gen_eq1(3, 40, 40, 73)
+    ozk.split_matrix(big, 4, ozk.SplitSide.rows)
+    m = cpu.gen_eq1(3, 7, 9, 74)
+    m[3, :, 0] = 0.0          # leading words zero, tails kept (not renormalised)
+    m[5, :, :] = 0.0
+    for d in (1, 2, 5):
+        for side in (0, 1):
+            want_p, want_r = cpu.split(3, m, d, side)
+            s = ozk.split_matrix(m, d, ozk.SplitSide(side))
+            assert_bitwise(np.stack(s.pieces), want_p, f"pieces d={d} side={side}")
+            assert_bitwise(s.residual, want_r, f"residual d={d} side={side}")
+
+
 def test_split_errors(ozk, cpu):
     m = cpu.gen_eq1(2, 2, 2, 72)
     with pytest.raises(ozk.param_error):
