@@ -20,8 +20,10 @@
 //     reaches extraction is therefore identical, in the same order.
 //   * strict_normalize runs its 2K passes unconditionally after the first
 //     unchanged pass; a pass with no change is idempotent (compaction finds no
-//     interior zero, the sweep finds only fixpoints).
-// Both claims are checked bit-for-bit against the compiled reference
+//     interior zero, the sweep finds only fixpoints).  On the K >= 3 fast path the
+//     first pass also skips its zero compaction: from_expansion's output has
+//     no interior zero (see kw_add_impl).
+// These claims are checked bit-for-bit against the compiled reference
 // (tests/test_kword_host.py on CPU, tests/test_gpu_parity.py on the GPU).
 //
 // Only additions/subtractions appear here, so FMA contraction cannot occur;
@@ -205,13 +207,20 @@ OZK_HD void non_finite(T head, T* c) {
 }
 
 // multifloat.hpp:450-469
-template <int K, bool kInt = false, typename T>
+// OZK_KW_TAILSKIP=0 keeps the first compaction on the fast path (A/B builds).
+#ifndef OZK_KW_TAILSKIP
+#define OZK_KW_TAILSKIP 1
+#endif
+
+// kTailZeros: the caller guarantees c has no zero before a nonzero word, so
+// the first pass's compaction is the identity and is skipped.
+template <int K, bool kInt = false, bool kTailZeros = false, typename T>
 OZK_HD void strict_normalize(T* c) {
 #pragma unroll
     for (int pass = 0; pass < 2 * K; ++pass) {
         // stable compaction of zeros to the tail (bubble, static indices)
 #pragma unroll
-        for (int r = 0; r < K - 1; ++r) {
+        for (int r = 0; r < ((kTailZeros && pass == 0) ? 0 : K - 1); ++r) {
 #pragma unroll
             for (int i = 0; i < K - 1; ++i) {
                 bool z = is_zero<kInt>(c[i]);
@@ -369,12 +378,18 @@ OZK_HD void kw_add_impl(T* x, T y) {
             m[i + 1] = lo;
         }
         m[0] = s;
-        // from_expansion
-        if constexpr (kFast)
+        // from_expansion.  Its output has zeros only at the tail: every word
+        // it emits before the last is a two_sum hi with lo != 0 (hi == 0
+        // would make the sum exact, lo == 0), and the fast path's leading
+        // t[0] is emitted only with t[1] != 0 (t[1] is t[0]'s rounding
+        // error), so strict_normalize's first compaction has nothing to move.
+        if constexpr (kFast) {
             extract_after_vec_sum<K, kInt>(m, x);
-        else
+            strict_normalize<K, kInt, OZK_KW_TAILSKIP != 0>(x);
+        } else {
             extract_components<K, K + 1, kInt>(m, x);
-        strict_normalize<K, kInt>(x);
+            strict_normalize<K, kInt>(x);
+        }
         if (is_zero<kInt>(x[0]) || !is_finite(x[0])) non_finite<K>(rn_add(x[0], T(0)), x);
     }
 }
