@@ -286,6 +286,21 @@ ozk_status ozk_ts_direct_gemm_device(size_t m, size_t l, size_t n, const float* 
 
 /* ---- utilities -------------------------------------------------------------- */
 
+/* The reference's input generator gen_matrix_eq1<K>(rows, cols, seed)
+ * (gen.hpp:20-34, Xoshiro256ss rng.hpp:21-54) into a HOST buffer, bit for bit:
+ * the same single xoshiro256** stream, entered by every worker thread at its
+ * first element by a GF(2) jump (csrc/gen_host.cpp), and the same libm calls.
+ * threads <= 0: all CPUs this process may run on.  TS: the TD value rounded
+ * to three binary32 words and renormalised (this build's TS definition). */
+ozk_status ozk_gen_eq1(ozk_format fmt, size_t rows, size_t cols, uint64_t seed, void* out,
+                       int threads);
+
+/* Ill-conditioned inputs (BASELINE config 5, acceptance.cpp:53-58 style): each
+ * gen_matrix_eq1 element scaled by 2^e, e uniform on [-spread, spread] from one
+ * further draw of the same stream (0 <= spread <= 400). */
+ozk_status ozk_gen_spread(ozk_format fmt, size_t rows, size_t cols, uint64_t seed, int spread,
+                          void* out, int threads);
+
 /* Eq. (1)-distributed synthetic K-word matrix (rows*cols elements) in device
  * memory; counter-based, so a pure function of (seed, shape).  Not the
  * reference's sequential generator (gen.hpp:20-34) -- see csrc/gen.cu. */

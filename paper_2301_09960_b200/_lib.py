@@ -75,6 +75,9 @@ SIGNATURES = {
     "ozk_mpmat_read": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_int, _sz, _sz, _dp]),
     "ozk_pair_products_device": (ctypes.c_int, [_sz, _sz, _sz, _dp, _dp, ctypes.c_int, _ip,
                                                 ctypes.c_int, _dp, ctypes.c_void_p]),
+    "ozk_gen_eq1": (ctypes.c_int, [ctypes.c_int, _sz, _sz, ctypes.c_uint64, _dp, ctypes.c_int]),
+    "ozk_gen_spread": (ctypes.c_int, [ctypes.c_int, _sz, _sz, ctypes.c_uint64, ctypes.c_int, _dp,
+                                      ctypes.c_int]),
     "ozk_gen_eq1_device": (ctypes.c_int, [ctypes.c_int, _sz, _sz, ctypes.c_uint64, _dp,
                                           ctypes.c_void_p]),
     "ozk_gen_spread_device": (ctypes.c_int, [ctypes.c_int, _sz, _sz, ctypes.c_uint64,

@@ -17,6 +17,7 @@ LIB_DIR = os.path.join(HERE, "lib")
 LIB = os.path.join(LIB_DIR, "libozk.so")
 SOURCES = ["api.cu", "split.cu", "gemm.cu", "gen.cu", "diag.cu", "ts_direct.cu", "lu.cu", "gemm_i8.cu",
            "io.cu", "direct.cu"]
+HOST_SOURCES = ["gen_host.cpp"]  # host-only C++ (g++, strict FP like the reference)
 HEADERS = ["kword.cuh", "ozk_internal.cuh"]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
@@ -29,7 +30,7 @@ def _stale() -> bool:
     if not os.path.exists(LIB):
         return True
     t = os.path.getmtime(LIB)
-    deps = [os.path.join(CSRC, f) for f in SOURCES + HEADERS]
+    deps = [os.path.join(CSRC, f) for f in SOURCES + HOST_SOURCES + HEADERS]
     deps.append(os.path.join(ROOT, "include", "ozk.h"))
     deps.append(os.path.abspath(__file__))
     return any(os.path.getmtime(d) > t for d in deps)
@@ -48,10 +49,19 @@ def build(force: bool = False, verbose: bool = False) -> str:
             print(" ".join(cmd), file=sys.stderr)
         procs.append((subprocess.Popen(cmd), cmd))
         objs.append(obj)
+    for src in HOST_SOURCES:
+        # -ffp-contract=off: no FMA contraction, as the reference's own build
+        # (proj/CMakeLists.txt:16-20); the generator must match it bit for bit
+        obj = os.path.join(LIB_DIR, src.replace(".cpp", ".o"))
+        cmd = ["g++", "-std=c++20", "-O2", "-ffp-contract=off", "-fPIC", "-Wall", "-Wno-unknown-pragmas", "-pthread",
+               f"-I{os.path.join(ROOT, 'include')}", "-c", os.path.join(CSRC, src), "-o", obj]
+        procs.append((subprocess.Popen(cmd), cmd))
+        objs.append(obj)
     for p, cmd in procs:
         if p.wait() != 0:
             raise RuntimeError("nvcc failed: " + " ".join(cmd))
-    link = [NVCC, *ARCH, "-shared", "-cudart", "static", "-ccbin", "g++", "-o", LIB, *objs]
+    link = [NVCC, *ARCH, "-shared", "-cudart", "static", "-ccbin", "g++", "-Xcompiler", "-pthread",
+            "-o", LIB, *objs]
     subprocess.run(link, check=True)
     return LIB
 
