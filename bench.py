@@ -30,6 +30,9 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = ("effective DD/TD/QD GEMM GFLOP/s (2n^3/t), n=8192; slice DGEMM % of FP64 peak")
+DATA = ("synthetic: the reference's own inputs gen_matrix_eq1<K>(n, n, 1) and (n, n, 2) "
+        "(gen.hpp:20-34, bench.cpp:111-112), generated bit-identically on the host by "
+        "ozk_gen_eq1; both arms see the same bytes")
 # format -> (ozk_format code, words, headline D).  DD/TD/QD: SURVEY §8d saturating D at
 # l = 8192; TS (config 4): 5-bit slices at sigma_TS = 19, saturation near D = 15.
 WORKLOADS = {"dd": (2, 2, 6), "td": (3, 3, 9), "qd": (4, 4, 12), "ts": (0x103, 3, 15)}
@@ -61,6 +64,9 @@ def parse():
     p.add_argument("--cpu-sample", type=int, default=1024,
                    help="rows/cols of the CPU baseline sub-GEMM (inner dim stays n)")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-cpu-direct", action="store_true",
+                   help="skip timing the reference's direct gemm_simple<K> on the host")
+    p.add_argument("--cpu-direct-n", type=int, default=256)
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-engine-compare", action="store_true",
                    help="skip timing the other slice-product engine (for large n, where one "
@@ -130,33 +136,94 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 # CPU arms (oracle/: the reference compiled in place, else the C restatement)
 # ---------------------------------------------------------------------------
-def cpu_sample_rate(K: int, d: int, n: int, r: int, reps: int = 1, spread: int = 0):
-    """Reference CPU Ozaki on an r x n . n x r sub-GEMM (same inner dimension,
-    so the same sigma, slice widths and D as the n x n workload)."""
-    import numpy as np
+def host_cpu_info():
+    """lscpu model, usable cores and OpenMP binding of the host running the CPU arm."""
+    info = {"cores_usable": len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity")
+            else os.cpu_count(), "OMP_PROC_BIND": os.environ.get("OMP_PROC_BIND"),
+            "OMP_PLACES": os.environ.get("OMP_PLACES")}
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            k, _, v = line.partition(":")
+            if k.strip() in ("Model name", "Socket(s)", "Core(s) per socket", "Thread(s) per core"):
+                info[k.strip()] = v.strip()
+    except (OSError, subprocess.SubprocessError):
+        pass
+    return info
 
-    import oracle
-    cpu = oracle.best()
-    cores = os.cpu_count() or 1
-    if hasattr(cpu, "set_threads"):
-        cores = cpu.set_threads(cores)
-    else:
-        cores = 1  # the C restatement is single-threaded
+
+def full_size_record(fmt):
+    """The one-off full-size reference run on this box type (tools/cpu_reference_full.py,
+    committed under profiles/), if present: validates the sampled estimate."""
+    path = os.path.join(ROOT, "profiles", "cpu_reference_full_r02.json")
+    if not os.path.exists(path):
+        return None
+    try:
+        res = json.load(open(path))
+    except (OSError, ValueError):
+        return None
+    for r in res.get("results", []):
+        if r.get("what") == "ozaki_full" and r.get("format") == fmt and "total_s" in r:
+            return {"n": r["n"], "d": r["d"], "total_s": round(r["total_s"], 2),
+                    "gflops": round(r["gflops"], 4), "split_s": round(r["split_s"], 2),
+                    "product_s": round(r["product_s"], 2),
+                    "accumulate_s": round(r["accumulate_s"], 2),
+                    "threads": res.get("threads"), "source": "profiles/cpu_reference_full_r02.json"}
+    return None
+
+
+def cpu_sample(cpu, K, d, n, r, a_rows, b_cols):
+    """Reference CPU Ozaki on the r x n . n x r sub-GEMM A[:r] . B[:, :r] of the
+    workload's own input bytes (same inner dimension, so the same sigma, slice
+    widths, D and pair list), timed as the reference's gemm_bench does
+    (bench.cpp:121-157: wall time of ozaki_gemm, phase times from its
+    OzakiProfile).  The full n x n time is estimated per phase: the split
+    scales with the split elements (2rn -> 2n^2: x n/r), the slice products and
+    the accumulation with the C elements (r^2 -> n^2: x (n/r)^2).
+    Returns (C_sub, sample wall s, estimated full-size s, profile)."""
+    import numpy as np
+    prof = np.zeros(4)
+    t0 = time.perf_counter()
+    c = cpu.ozaki_gemm(K, a_rows, b_cols, d, prof=prof) if cpu.kind == "reference" \
+        else cpu.ozaki_gemm(K, a_rows, b_cols, d)
+    wall = time.perf_counter() - t0
+    if cpu.kind != "reference":  # the C restatement has no phase timers: all as products
+        prof[:] = (0.0, wall, 0.0, wall)
+    s = n / r
+    est = prof[0] * s + (prof[1] + prof[2]) * s * s
+    return c, wall, est, prof
+
+
+def cpu_direct(cpu, K, n, nd, a, b):
+    """The reference's direct multi-component GEMM gemm_simple<MultiFloat<K>>
+    (gemm.hpp:15-31) on the leading nd x nd blocks of the same inputs, timed
+    on all host threads and extrapolated to n as n^3 (its cost is cubic)."""
+    import numpy as np
+    aa = np.ascontiguousarray(a[:nd, :nd])
+    bb = np.ascontiguousarray(b[:nd, :nd])
+    t0 = time.perf_counter()
+    cpu.gemm_simple(K, aa, bb)
+    dt = time.perf_counter() - t0
+    return {"n": nd, "seconds": round(dt, 4), "gflops": round(2.0 * nd ** 3 / dt / 1e9, 5),
+            "extrapolated_n": n, "extrapolated_seconds": round(dt * (n / nd) ** 3, 1),
+            "note": "reference gemm_simple<MultiFloat<K>> (gemm.hpp:15-31), all host threads, "
+                    "extrapolated as n^3"}
+
+
+def reference_inputs(cpu, K, n, r, spread):
+    """The sampled blocks A[:r] and B[:, :r] of gen_matrix_eq1<K>(n, n, 1) and
+    (n, n, 2) (bench.cpp:111-112 seeds), from the reference generator itself."""
+    import numpy as np
+    port = None
     if spread:
+        import oracle
         port = oracle.load_port()
-        a = port.gen_spread(K, r, n, 1, spread)
-        b = port.gen_spread(K, n, r, 2, spread)
+        a = port.gen_spread(K, r, n, 1, spread)  # first r rows of the stream
+        b = port.gen_spread(K, n, n, 2, spread)
     else:
-        a = cpu.gen_eq1(K, r, n, 1)
-        b = cpu.gen_eq1(K, n, r, 2)
-    best = None
-    for _ in range(reps):
-        t0 = time.perf_counter()
-        c = cpu.ozaki_gemm(K, a, b, d)
-        dt = time.perf_counter() - t0
-        best = dt if best is None else min(best, dt)
-    del c, a, b, np
-    return 2.0 * r * r * n / best / 1e9, best, cores, cpu.kind
+        a = cpu.gen_eq1(K, r, n, 1)  # the stream is row-major: rows 0..r-1 of (n, n)
+        b = cpu.gen_eq1(K, n, n, 2)
+    return a, np.ascontiguousarray(b[:, :r])
 
 
 def run_reference(args):
@@ -168,26 +235,37 @@ def run_reference(args):
         print(json.dumps({"impl": "reference", "unavailable":
                           "TS is not implemented by the reference (SPEC.md:8)"}), flush=True)
         return 0
+    import oracle
+    cpu = oracle.best()
+    cores = cpu.set_threads(len(os.sched_getaffinity(0))) if hasattr(cpu, "set_threads") else 1
     d = args.d or d0
-    n, r = args.n, args.cpu_sample
+    n, r = args.n, min(args.cpu_sample, args.n)
+    a, b = reference_inputs(cpu, K, n, r, args.spread)
     for _ in range(args.warmup):
-        cpu_sample_rate(K, d, n, r, spread=args.spread)
-    rates, times = [], []
+        cpu_sample(cpu, K, d, n, r, a, b)
+    walls, ests = [], []
     for _ in range(args.steps):
-        rate, dt, cores, kind = cpu_sample_rate(K, d, n, r, spread=args.spread)
-        rates.append(rate)
-        times.append(dt)
-    value = statistics.mean(rates)
-    sample = (f"{NAMES[args.format]} Ozaki sub-GEMM {r}x{n} . {n}x{r}, D={d} (inner dim n "
-              f"as in the workload), reference ozaki_gemm<K> + reference_backend()")
+        _, wall, est, _ = cpu_sample(cpu, K, d, n, r, a, b)
+        walls.append(wall)
+        ests.append(est)
+    t_full = min(ests)  # best of reps, as bench.cpp:144-152
+    value = 2.0 * n ** 3 / t_full / 1e9
+    sample = (f"{NAMES[args.format]} Ozaki sub-GEMM A[:{r}] . B[:, :{r}] of the n={n} inputs "
+              f"(gen_matrix_eq1 seeds 1, 2), D={d}, reference ozaki_gemm<K> + "
+              f"reference_backend(); full n x n time estimated per phase (split x n/r, "
+              f"products + accumulation x (n/r)^2), best of {args.steps}")
     line = {
         "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "GFLOP/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": round(1e3 * statistics.mean(times), 3), "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "ms_per_step": round(1e3 * statistics.mean(walls), 3), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": DATA,
         "config": config_of(args, K, d, n),
         "cpu_baseline": {"value": round(value, 4), "unit": "GFLOP/s", "cores": cores,
-                         "kind": kind, "sample": sample},
+                         "kind": cpu.kind, "sample": sample,
+                         "estimated_full_seconds": round(t_full, 2),
+                         "ms_per_step_is": "wall time of one sampled sub-GEMM",
+                         "host": host_cpu_info(),
+                         "full_size_measured": full_size_record(args.format)},
         "e2e": {"value": round(value, 4), "unit": "GFLOP/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -264,6 +342,54 @@ def engine_summary(eng, n, d, t_step, t_kern, peak_fp64, peak_i8, nd=3):
     return out
 
 
+def host_inputs(lib, code, K, wdt, n, spread, rows=None, pin=True):
+    """gen_matrix_eq1<K>(n, n, 1) and (n, n, 2) (or the config-5 spread variant)
+    from the library's host generator, into (pinned) CPU tensors."""
+    import torch
+    out = []
+    for seed in (1, 2):
+        h = torch.empty((n, n, K), dtype=wdt, pin_memory=pin)
+        st = (lib.ozk_gen_spread(code, n, n, seed, spread, h.data_ptr(), 0) if spread
+              else lib.ozk_gen_eq1(code, n, n, seed, h.data_ptr(), 0))
+        if st != 0:
+            raise RuntimeError(lib.ozk_last_error().decode())
+        out.append(h)
+    return out
+
+
+def cpu_leg(args, K, d, n, ha, hb, c_sub):
+    """cpu_baseline of our arm: the reference CPU path on the same input bytes
+    (A[:r] . B[:, :r] of this run's inputs, full-size time estimated per phase,
+    see cpu_sample), its direct gemm_simple, and a bit-exact check of this run's
+    GPU result C[:r, :r] against the reference's output on those bytes."""
+    import numpy as np
+
+    import oracle
+    cpu = oracle.best()
+    cores = cpu.set_threads(len(os.sched_getaffinity(0))) if hasattr(cpu, "set_threads") else 1
+    r = c_sub.shape[0]
+    a = np.ascontiguousarray(ha[:r].numpy())
+    b = np.ascontiguousarray(hb[:, :r].numpy())
+    c, wall, est, prof = cpu_sample(cpu, K, d, n, r, a, b)
+    exact = bool(np.array_equal(c.view(np.uint64), c_sub.view(np.uint64)))
+    if not exact:
+        raise AssertionError("GPU C[:r, :r] differs from the reference ozaki_gemm on the same "
+                             "inputs")
+    out = {"value": round(2.0 * n ** 3 / est / 1e9, 4), "unit": "GFLOP/s", "cores": cores,
+           "kind": cpu.kind,
+           "sample": f"{NAMES[args.format]} Ozaki sub-GEMM A[:{r}] . B[:, :{r}] of this run's "
+                     f"inputs, D={d}, one call ({wall:.2f} s: split {prof[0]:.2f} s, products "
+                     f"{prof[1]:.2f} s, accumulate {prof[2]:.2f} s); full n x n time estimated "
+                     f"per phase (split x n/r, products + accumulation x (n/r)^2) = {est:.1f} s",
+           "host": host_cpu_info(),
+           "full_size_measured": full_size_record(args.format),
+           "parity": {"checked": f"GPU C[:{r}, :{r}] (this run) vs reference ozaki_gemm on "
+                                 "the same bytes", "bit_exact": exact}}
+    if not args.no_cpu_direct:
+        out["direct"] = cpu_direct(cpu, K, n, args.cpu_direct_n, ha.numpy(), hb.numpy())
+    return out
+
+
 def run_ours(args):
     import torch
 
@@ -295,11 +421,11 @@ def run_ours(args):
         if st != 0:
             raise RuntimeError(lib.ozk_last_error().decode())
 
-    # synthetic Eq. (1) inputs generated on device (outside the timed region)
-    A = torch.empty((n, n, K), dtype=wdt, device="cuda")
-    B = torch.empty((n, n, K), dtype=wdt, device="cuda")
-    check(lib.ozk_gen_spread_device(code, n, n, 1, args.spread, A.data_ptr(), sh))
-    check(lib.ozk_gen_spread_device(code, n, n, 2, args.spread, B.data_ptr(), sh))
+    # the reference's inputs (gen_matrix_eq1 seeds 1, 2), generated bit-identically
+    # on the host into pinned buffers (outside the timed region), then resident
+    ha, hb = host_inputs(lib, code, K, wdt, n, args.spread)
+    A = ha.to("cuda", non_blocking=False)
+    B = hb.to("cuda", non_blocking=False)
 
     peak_fp64 = lib.ozk_probe_dmma_tflops(20000, sh)
     peak_i8 = lib.ozk_probe_i8_tops(4000, sh)
@@ -389,7 +515,7 @@ def run_ours(args):
 
     e2e = None
     if not args.no_e2e and world == 1:
-        e2e = run_e2e(args, lib, OzkProfile, A, B, code, K, wb, d, n)
+        e2e = run_e2e(args, lib, OzkProfile, ha, hb, code, K, wb, d, n)
     elif not args.no_e2e:
         e2e = run_e2e_sharded(args, eng, A, B, K, wb, n)
 
@@ -406,16 +532,15 @@ def run_ours(args):
                 ts, tk, used = time_engine(lib, OzkProfile, code, n, d, A, B, C, sh, e)
                 engines[e] = engine_summary(used, n, d, ts, tk, peak_fp64, peak_i8, nd)
         lib.ozk_set_engine(ENGINE_CODES[args.engine])
+        r = min(args.cpu_sample, n)
+        c_sub = C[:r, :r].cpu().numpy()  # for the bit-exact check against the CPU arm
         del C
         for fmt in [v for v in args.variants.split(",") if v and v != args.format]:
             variants.append(run_variant(lib, OzkProfile, fmt, n, peak_fp64, peak_i8, sh, args))
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline and args.format != "ts":
-        rate, dt, cores, kind = cpu_sample_rate(K, d, n, args.cpu_sample, spread=args.spread)
-        cpu = {"value": round(rate, 4), "unit": "GFLOP/s", "cores": cores, "kind": kind,
-               "sample": f"{NAMES[args.format]} Ozaki sub-GEMM {args.cpu_sample}x{n} . "
-                         f"{n}x{args.cpu_sample}, D={d}, one call ({dt:.2f} s)"}
+        cpu = cpu_leg(args, K, d, n, ha, hb, c_sub)
 
     if rank == 0:
         dm = engines.get("dmma", {})
@@ -423,9 +548,8 @@ def run_ours(args):
             "metric": METRIC, "value": round(value, 3), "unit": "GFLOP/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * t_step, 3),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic: Eq. (1)-distributed K-word matrices generated on device "
-                    "(counter-based splitmix64, csrc/gen.cu)",
-            "config": dict(config_of(args, K, d, n), engine=engine_used),
+            "data": DATA,
+            "config": config_of(args, K, d, n), "engine": engine_used,
             "slice_dgemm_frac_of_fp64_peak": dm.get("slice_dgemm_frac_of_fp64_peak"),
             "phases_ms": {"split": round(1e3 * statistics.mean(split), 3),
                           "slice_gemm_fused_accumulate": round(1e3 * t_kern, 3)},
@@ -475,13 +599,11 @@ def run_ours(args):
     return 0
 
 
-def run_e2e(args, lib, OzkProfile, A, B, code, K, wb, d, n):
+def run_e2e(args, lib, OzkProfile, ha, hb, code, K, wb, d, n):
     """Same metric through the host-buffer C-ABI entry point (ozk_ozaki_gemm):
     H2D of A and B from pinned memory, the GEMM, D2H of C, every step."""
     import torch
-    ha = A.cpu().pin_memory()
-    hb = B.cpu().pin_memory()
-    hc = torch.empty((n, n, K), dtype=A.dtype).pin_memory()
+    hc = torch.empty((n, n, K), dtype=ha.dtype).pin_memory()
     prof = OzkProfile()
 
     def call():
@@ -549,11 +671,9 @@ def direct_rate(lib, code, K, sh, nd=1024):
     (its cost is cubic; the rate carries to n = 8192, where one call would take
     minutes for QD)."""
     import torch
-    A = torch.empty((nd, nd, K), dtype=torch.float64, device="cuda")
-    B = torch.empty_like(A)
+    ha, hb = host_inputs(lib, code, K, torch.float64, nd, 0, pin=False)
+    A, B = ha.cuda(), hb.cuda()
     C = torch.empty_like(A)
-    lib.ozk_gen_eq1_device(code, nd, nd, 1, A.data_ptr(), sh)
-    lib.ozk_gen_eq1_device(code, nd, nd, 2, B.data_ptr(), sh)
     stream = torch.cuda.current_stream()
 
     def call():
@@ -576,11 +696,10 @@ def run_variant(lib, OzkProfile, fmt, n, peak_fp64, peak_i8, sh, args):
     import torch
     code, K, d, wb = fmt_info(fmt)
     wdt = torch.float32 if wb == 4 else torch.float64
-    A = torch.empty((n, n, K), dtype=wdt, device="cuda")
-    B = torch.empty((n, n, K), dtype=wdt, device="cuda")
+    ha, hb = host_inputs(lib, code, K, wdt, n, args.spread, pin=False)
+    A, B = ha.cuda(), hb.cuda()
+    del ha, hb
     C = torch.empty((n, n, K), dtype=wdt, device="cuda")
-    lib.ozk_gen_spread_device(code, n, n, 1, args.spread, A.data_ptr(), sh)
-    lib.ozk_gen_spread_device(code, n, n, 2, args.spread, B.data_ptr(), sh)
     out = {"workload": f"{NAMES[fmt]} Ozaki GEMM n={n} D={d}"}
     engs = ("dmma", "int8")
     for e in engs:
@@ -615,6 +734,9 @@ def run_variant(lib, OzkProfile, fmt, n, peak_fp64, peak_i8, sh, args):
 
 def main():
     args = parse()
+    # the CPU arms run the reference's OpenMP loops on all host threads, bound
+    # close (SURVEY §8d protocol); read by libgomp when oracle/_ref loads
+    os.environ.setdefault("OMP_PROC_BIND", "close")
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)

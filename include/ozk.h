@@ -220,6 +220,18 @@ ozk_status ozk_pair_products_device(size_t m, size_t l, size_t n, const double* 
                                     const double* b_slices, int split_count, const int* pairs,
                                     int npairs, double* products, void* stream);
 
+/* Parity hook of the INT8 engine: every slice product C_ab of the pair list,
+ * formed exactly as the INT8 slice GEMM forms it (nd^2 int8 digit GEMMs on
+ * tcgen05 with int32 accumulation, exact int64 recombination, scaling by
+ * 2^(gA + gB)), stored as binary64 into products[p] (m x n row-major) instead
+ * of being accumulated.  Operands as for ozk_digits_gemm_device. */
+ozk_status ozk_pair_products_digits_device(ozk_format fmt, size_t m, size_t l, size_t n,
+                                           const int8_t* a_digits, const int* a_exps,
+                                           size_t a_plane_rows, const int8_t* b_digits,
+                                           const int* b_exps, size_t b_plane_rows, size_t ld8,
+                                           int split_count, const int* pairs, int npairs,
+                                           double* products, void* stream);
+
 /* ---- blocked-LU trailing update ------------------- *
  * A22 := A22 - L21 * U12 exactly as the reference's blocked_lu does it
  * (proj/include/mpmat/lu.hpp:104-124): the product by ozaki_gemm with
@@ -321,6 +333,12 @@ double ozk_probe_dmma_tflops(int iters, void* stream);
  * operands resident in shared memory) in TOPS -- the INT8 engine's roofline
  * denominator.  Returns < 0 on failure. */
 double ozk_probe_i8_tops(int iters, void* stream);
+
+/* Scratch comes from the current device's stream-ordered pool, which keeps
+ * freed memory for the next call (release threshold: never).  This returns
+ * the pool's unused memory to the device, for callers that need it for other
+ * allocators.  Synchronises the device. */
+ozk_status ozk_trim_device_pool(void);
 
 const char* ozk_last_error(void);
 int ozk_version(void);

@@ -75,6 +75,9 @@ SIGNATURES = {
     "ozk_mpmat_read": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_int, _sz, _sz, _dp]),
     "ozk_pair_products_device": (ctypes.c_int, [_sz, _sz, _sz, _dp, _dp, ctypes.c_int, _ip,
                                                 ctypes.c_int, _dp, ctypes.c_void_p]),
+    "ozk_pair_products_digits_device": (ctypes.c_int, [ctypes.c_int, _sz, _sz, _sz, _dp, _dp, _sz,
+                                                       _dp, _dp, _sz, _sz, ctypes.c_int, _ip,
+                                                       ctypes.c_int, _dp, ctypes.c_void_p]),
     "ozk_gen_eq1": (ctypes.c_int, [ctypes.c_int, _sz, _sz, ctypes.c_uint64, _dp, ctypes.c_int]),
     "ozk_gen_spread": (ctypes.c_int, [ctypes.c_int, _sz, _sz, ctypes.c_uint64, ctypes.c_int, _dp,
                                       ctypes.c_int]),
@@ -96,6 +99,7 @@ SIGNATURES = {
     "ozk_probe_i8_tops": (ctypes.c_double, [ctypes.c_int, ctypes.c_void_p]),
     "ozk_set_engine": (ctypes.c_int, [ctypes.c_int]),
     "ozk_get_engine": (ctypes.c_int, []),
+    "ozk_trim_device_pool": (ctypes.c_int, []),
     "ozk_last_error": (ctypes.c_char_p, []),
     "ozk_version": (ctypes.c_int, []),
 }

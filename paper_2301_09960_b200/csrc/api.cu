@@ -638,6 +638,16 @@ ozk_status ozk_set_engine(int engine) {
 }
 
 int ozk_get_engine(void) { return engine_setting(); }
+
+ozk_status ozk_trim_device_pool(void) {
+    int dev = 0;
+    OZK_CUDA(cudaGetDevice(&dev), "trim_device_pool");
+    cudaMemPool_t pool;
+    OZK_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev), "trim_device_pool");
+    OZK_CUDA(cudaDeviceSynchronize(), "trim_device_pool");
+    OZK_CUDA(cudaMemPoolTrimTo(pool, 0), "trim_device_pool");
+    return OZK_OK;
+}
 int ozk_version(void) { return 1; }
 
 int ozk_split_shift_bits(size_t inner) { return shift_bits(inner ? inner : 1); }
@@ -1296,6 +1306,51 @@ ozk_status ozk_digits_gemm_device(ozk_format fmt, size_t m, size_t l, size_t n,
                  "digits_gemm");
     }
     OZK_CUDA(cudaStreamSynchronize(st), "digits_gemm");
+    return OZK_OK;
+}
+
+ozk_status ozk_pair_products_digits_device(ozk_format fmt, size_t m, size_t l, size_t n,
+                                           const int8_t* a_digits, const int* a_exps,
+                                           size_t a_plane_rows, const int8_t* b_digits,
+                                           const int* b_exps, size_t b_plane_rows, size_t ld8,
+                                           int d, const int* pairs, int npairs, double* products,
+                                           void* stream) {
+    if (!valid_fmt(fmt)) return fail(OZK_EPARAM, "pair_products: format must be DD, TD, QD or TS");
+    if (m == 0 || l == 0 || n == 0) return fail(OZK_ESHAPE, "matrix dimensions must be positive");
+    if (d < 1 || d > kMaxSplits) return fail(OZK_EPARAM, "pair_products: bad split count");
+    const int nd = int8_digits(fmt, l, d);
+    if (nd == 0) return fail(OZK_EPARAM, "pair_products: INT8 engine not applicable to this inner dimension");
+    if (ld8 < l || ld8 % 16) return fail(OZK_ESHAPE, "pair_products: ld8 must be >= l and a multiple of 16");
+    if (a_plane_rows < m || b_plane_rows < n) return fail(OZK_ESHAPE, "pair_products: plane_rows too small");
+    PairList pl;
+    if (ozk_status s = fill_pairs(d, pairs, npairs, pl)) return s;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (pl.count > 0) {
+        I8Operands op{};
+        op.nd = nd;
+        op.a = a_digits;
+        op.a_ld = ld8;
+        op.a_digit_stride = a_plane_rows * ld8;
+        op.a_slice_stride = (size_t)nd * a_plane_rows * ld8;
+        op.b = b_digits;
+        op.b_ld = ld8;
+        op.b_digit_stride = b_plane_rows * ld8;
+        op.b_slice_stride = (size_t)nd * b_plane_rows * ld8;
+        op.gA = a_exps;
+        op.gB = b_exps;
+        op.gA_stride = a_plane_rows;
+        op.gB_stride = b_plane_rows;
+        op.m = m;
+        op.n = n;
+        op.l = l;
+        op.d = d;
+        op.c = products;
+        op.ldc = n;
+        op.pair_stride = m * n;
+        OZK_CUDA(launch_pair_products_i8(word_bytes_of(fmt), op, pl, st, num_sms_cached()),
+                 "pair_products");
+    }
+    OZK_CUDA(cudaStreamSynchronize(st), "pair_products");
     return OZK_OK;
 }
 

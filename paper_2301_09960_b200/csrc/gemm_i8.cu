@@ -195,8 +195,11 @@ struct I8Problem {
     const int* gA;     // [d][m] grid exponents
     const int* gB;     // [d][n]
     size_t gA_stride, gB_stride;
-    void* c;           // K-word AoS C, row stride ldc elements
+    void* c;           // K-word AoS C, row stride ldc elements (PR: binary64 products)
     size_t ldc;
+    size_t pair_stride;  // PR: doubles between consecutive pair products
+    int c_init;          // 1: the first pair of the list starts C from zero; 0: C holds a
+                         //    running sum (a later chunk of a long pair list)
     // wave pacing (see the producer): pace[s] counts the clusters that have
     // started global step s = wave * npairs + pair; null disables pacing
     unsigned int* pace;
@@ -490,7 +493,11 @@ __device__ __forceinline__ void trace_stamp(int, int, bool) {}
 // CN CTAs of a cluster row share the A-digit tile the same way.  A stage of CTA
 // x is written by x's cluster row and column, so its empty barrier counts
 // CM + CN - 1 MMA completions, each CTA's commit arriving on all of them.
-template <int K, typename W, int ND, int TR, int EG, bool kVec, int CM, int CN, int NB>
+// PR (parity hook, ozk_pair_products_digits_device): instead of the K-word
+// accumulation, every exact slice product C_ab is stored as binary64 into its
+// own plane (products[p][row][col]).
+template <int K, typename W, int ND, int TR, int EG, bool kVec, int CM, int CN, int NB,
+          bool PR = false>
 __global__ void __launch_bounds__(I8Cfg<K, W, ND, TR, EG, NB>::kThreads, 1)
 pair_gemm_i8_kernel(const __grid_constant__ MapsI8 maps, const __grid_constant__ PairList pairs,
                     I8Problem prob, int tiles_m, int tiles_n) {
@@ -777,7 +784,7 @@ pair_gemm_i8_kernel(const __grid_constant__ MapsI8 maps, const __grid_constant__
                     gapq[q] = prob.gA + (size_t)al * prob.gA_stride;
                     tbufq[q] = tlane + ((step + q) % NB) * kBufCols;
                 }
-                const bool first = p == 0;  // C starts from zero
+                const bool first = p == 0 && prob.c_init;  // C starts from zero
                 trace_stamp(step, 3, tracer);
                 for (int q = 0; q < np; ++q)
                     mbar_wait(tfull0 + 8 * ((step + q) % NB), ((step + q) / NB) & 1);
@@ -790,7 +797,7 @@ pair_gemm_i8_kernel(const __grid_constant__ MapsI8 maps, const __grid_constant__
                 };
                 auto load_chunk = [&](int r, W (&w)[kChunk][K]) {
 #pragma unroll
-                    for (int j = 0; j < kChunk; ++j) {
+                    for (int j = 0; j < (PR ? 0 : kChunk); ++j) {
                         const size_t e = row_of(r + j) * prob.ldc + col_c;
 #if defined(OZK_I8_EPI_MODE) && OZK_I8_EPI_MODE == 1
                         if (true) {  // diagnostic: no C reads
@@ -856,6 +863,14 @@ pair_gemm_i8_kernel(const __grid_constant__ MapsI8 maps, const __grid_constant__
                             if (q >= np) break;
                             const double y = yc[q][j];
                             const int ga = __ldg(gapq[q] + row_of(r + j));
+                            if constexpr (PR) {
+                                const size_t rr = row0 + r + j;
+                                if (col_ok && rr < prob.m)
+                                    static_cast<double*>(prob.c)[(size_t)(p + q) * prob.pair_stride +
+                                                                 rr * prob.ldc + col] =
+                                        ldexp_fast(y, ga + gbq[q]);
+                                continue;
+                            }
                             // exact scaled slice product (a TS product is exact in binary32)
 #if defined(OZK_I8_EPI_MODE) && OZK_I8_EPI_MODE == 2
                             w[j][0] += (W)ldexp_fast(y, ga + gbq[q]);  // diagnostic: no K-word add
@@ -865,7 +880,7 @@ pair_gemm_i8_kernel(const __grid_constant__ MapsI8 maps, const __grid_constant__
                         }
                     }
 #pragma unroll
-                    for (int j = 0; j < kChunk; ++j) {
+                    for (int j = 0; j < (PR ? 0 : kChunk); ++j) {
                         const size_t rr = row0 + r + j;
                         if (col_ok && rr < prob.m) {
                             const size_t e = rr * prob.ldc + col;
@@ -969,7 +984,8 @@ I8Geometry geometry_typed(int num_sms) {
     return g;
 }
 
-template <int K, typename W, int ND, int TR, int EG = 2, int CM = 1, int CN = 1, int NB = 2>
+template <int K, typename W, int ND, int TR, int EG = 2, int CM = 1, int CN = 1, int NB = 2,
+          bool PR = false>
 cudaError_t launch_i8_typed(const I8Operands& op, const PairList& pairs, cudaStream_t st,
                             int num_sms) {
     using Cfg = I8Cfg<K, W, ND, TR, EG, NB>;
@@ -1008,14 +1024,16 @@ cudaError_t launch_i8_typed(const I8Operands& op, const PairList& pairs, cudaStr
     prob.gB_stride = op.gB_stride ? op.gB_stride : op.n;
     prob.c = op.c;
     prob.ldc = op.ldc;
+    prob.pair_stride = op.pair_stride;
+    prob.c_init = op.c_init ? 1 : 0;
     prob.pace = nullptr;
     prob.pace_slack = OZK_I8_PACE;
-    const bool vec = sizeof(W) == 8 && (reinterpret_cast<uintptr_t>(op.c) & 15) == 0;
+    const bool vec = !PR && sizeof(W) == 8 && (reinterpret_cast<uintptr_t>(op.c) & 15) == 0;
     const int tiles_m = (int)((op.m + TR - 1) / TR), tiles_n = (int)((op.n + TC - 1) / TC);
     const int num_tiles = tiles_m * tiles_n;
     if (num_tiles == 0 || pairs.count == 0) return cudaSuccess;
-    auto kern = pair_gemm_i8_kernel<K, W, ND, TR, EG, false, CM, CN, NB>;
-    if constexpr (sizeof(W) == 8)
+    auto kern = pair_gemm_i8_kernel<K, W, ND, TR, EG, false, CM, CN, NB, PR>;
+    if constexpr (sizeof(W) == 8 && !PR)
         if (vec) kern = pair_gemm_i8_kernel<K, W, ND, TR, EG, true, CM, CN, NB>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          Cfg::kSmemBytes);
@@ -1054,6 +1072,23 @@ cudaError_t launch_i8_typed(const I8Operands& op, const PairList& pairs, cudaStr
 }
 
 } // namespace
+
+cudaError_t launch_pair_products_i8(int word_bytes, const I8Operands& op, const PairList& pairs,
+                                    cudaStream_t st, int num_sms) {
+    // the binary64 engine shape (TD/QD); TS with its own digit counts
+    if (word_bytes == 4) {
+        if (op.nd == 1)
+            return launch_i8_typed<3, float, 1, OZK_I8_TS_TR, OZK_I8_TS_EG, OZK_I8_CM, OZK_I8_CN,
+                                   OZK_I8_TS_NB, true>(op, pairs, st, num_sms);
+        if (op.nd == 2)
+            return launch_i8_typed<3, float, 2, 64, 4, OZK_I8_CM, OZK_I8_CN, 2, true>(op, pairs, st,
+                                                                                      num_sms);
+        return cudaErrorInvalidValue;
+    }
+    if (op.nd != 3) return cudaErrorInvalidValue;
+    return launch_i8_typed<3, double, 3, OZK_I8_TR, OZK_I8_EG, OZK_I8_CM, OZK_I8_CN, OZK_I8_NB,
+                           true>(op, pairs, st, num_sms);
+}
 
 I8Geometry pair_gemm_i8_geometry(int K, int word_bytes, int nd, int num_sms) {
     if (word_bytes == 4) {

@@ -97,6 +97,8 @@ struct I8Operands {
     int d;
     void* c;        // K-word AoS, row stride ldc elements
     size_t ldc;
+    bool c_init = true;      // the first pair starts C from zero (false: accumulate onto C)
+    size_t pair_stride = 0;  // launch_pair_products_i8: doubles between pair planes
 };
 // Tile geometry of the INT8 slice GEMM for a format: C rows and columns per
 // cluster tile and the number of co-resident persistent clusters (one wave =
@@ -107,6 +109,10 @@ struct I8Geometry {
 I8Geometry pair_gemm_i8_geometry(int K, int word_bytes, int nd, int num_sms);
 cudaError_t launch_pair_gemm_i8(int K, int word_bytes, const I8Operands& op,
                                 const PairList& pairs, cudaStream_t st, int num_sms);
+// Parity hook: every exact slice product C_ab (binary64) into c + p*pair_stride
+// (row stride ldc) instead of the K-word accumulation.
+cudaError_t launch_pair_products_i8(int word_bytes, const I8Operands& op, const PairList& pairs,
+                                    cudaStream_t st, int num_sms);
 
 // Device Eq. (1)-distributed K-word generator (synthetic bench inputs).
 // a(i, j) -= c(i, j) in K-word arithmetic (a: row stride lda elements, c dense).
