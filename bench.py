@@ -28,6 +28,9 @@ import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+# the host CPUs this process may use, taken before torch's OpenMP runtime can
+# pin the main thread (the CPU legs restore it and use all of them)
+HOST_CPUS = sorted(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else None
 
 METRIC = ("effective DD/TD/QD GEMM GFLOP/s (2n^3/t), n=8192; slice DGEMM % of FP64 peak")
 DATA = ("synthetic: the reference's own inputs gen_matrix_eq1<K>(n, n, 1) and (n, n, 2) "
@@ -138,8 +141,7 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 def host_cpu_info():
     """lscpu model, usable cores and OpenMP binding of the host running the CPU arm."""
-    info = {"cores_usable": len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity")
-            else os.cpu_count(), "OMP_PROC_BIND": os.environ.get("OMP_PROC_BIND"),
+    info = {"cores_usable": len(HOST_CPUS) if HOST_CPUS else os.cpu_count(), "OMP_PROC_BIND": os.environ.get("OMP_PROC_BIND"),
             "OMP_PLACES": os.environ.get("OMP_PLACES")}
     try:
         out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
@@ -237,7 +239,7 @@ def run_reference(args):
         return 0
     import oracle
     cpu = oracle.best()
-    cores = cpu.set_threads(len(os.sched_getaffinity(0))) if hasattr(cpu, "set_threads") else 1
+    cores = cpu.set_threads(len(HOST_CPUS or [1])) if hasattr(cpu, "set_threads") else 1
     d = args.d or d0
     n, r = args.n, min(args.cpu_sample, args.n)
     a, b = reference_inputs(cpu, K, n, r, args.spread)
@@ -342,15 +344,24 @@ def engine_summary(eng, n, d, t_step, t_kern, peak_fp64, peak_i8, nd=3):
     return out
 
 
+def unpin():
+    """Give the main thread back every host CPU (torch's OpenMP runtime may have
+    pinned it); host worker threads inherit this mask."""
+    if HOST_CPUS:
+        os.sched_setaffinity(0, HOST_CPUS)
+    return len(HOST_CPUS) if HOST_CPUS else (os.cpu_count() or 1)
+
+
 def host_inputs(lib, code, K, wdt, n, spread, rows=None, pin=True):
     """gen_matrix_eq1<K>(n, n, 1) and (n, n, 2) (or the config-5 spread variant)
     from the library's host generator, into (pinned) CPU tensors."""
     import torch
+    threads = unpin()
     out = []
     for seed in (1, 2):
         h = torch.empty((n, n, K), dtype=wdt, pin_memory=pin)
-        st = (lib.ozk_gen_spread(code, n, n, seed, spread, h.data_ptr(), 0) if spread
-              else lib.ozk_gen_eq1(code, n, n, seed, h.data_ptr(), 0))
+        st = (lib.ozk_gen_spread(code, n, n, seed, spread, h.data_ptr(), threads) if spread
+              else lib.ozk_gen_eq1(code, n, n, seed, h.data_ptr(), threads))
         if st != 0:
             raise RuntimeError(lib.ozk_last_error().decode())
         out.append(h)
@@ -364,9 +375,11 @@ def cpu_leg(args, K, d, n, ha, hb, c_sub):
     GPU result C[:r, :r] against the reference's output on those bytes."""
     import numpy as np
 
+    unpin()  # undo any pinning by torch's OpenMP runtime
+    os.environ.setdefault("OMP_PROC_BIND", "close")  # read when oracle/_ref's libgomp loads
     import oracle
     cpu = oracle.best()
-    cores = cpu.set_threads(len(os.sched_getaffinity(0))) if hasattr(cpu, "set_threads") else 1
+    cores = cpu.set_threads(len(HOST_CPUS or [1])) if hasattr(cpu, "set_threads") else 1
     r = c_sub.shape[0]
     a = np.ascontiguousarray(ha[:r].numpy())
     b = np.ascontiguousarray(hb[:, :r].numpy())
@@ -734,9 +747,10 @@ def run_variant(lib, OzkProfile, fmt, n, peak_fp64, peak_i8, sh, args):
 
 def main():
     args = parse()
-    # the CPU arms run the reference's OpenMP loops on all host threads, bound
-    # close (SURVEY §8d protocol); read by libgomp when oracle/_ref loads
-    os.environ.setdefault("OMP_PROC_BIND", "close")
+    if args.impl == "reference":
+        # the reference's OpenMP loops on all host threads, bound close (SURVEY
+        # §8d protocol); read by libgomp when oracle/_ref loads
+        os.environ.setdefault("OMP_PROC_BIND", "close")
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)

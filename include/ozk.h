@@ -97,7 +97,9 @@ int ozk_get_engine(void);
  * OZK_ESHAPE for a zero dimension (dense_matrix.hpp:23) or mismatched inner
  * dimensions (ozaki.hpp:184), OZK_EPARAM for split_count < 1 (:185),
  * drop_threshold < 0 (:186), a non-finite entry (:77-78) or an entry too
- * large to shift (:109).  split_count is limited to 32 here. */
+ * large to shift (:109).  Any split_count >= 1 (slice indices are 16-bit:
+ * up to 65535; device memory, D slice planes per side, is the practical
+ * limit); pair lists longer than one launch run as consecutive launches. */
 ozk_status ozk_ozaki_gemm(ozk_format fmt, size_t m, size_t l, size_t n, const void* a,
                           const void* b, int split_count, double drop_threshold, void* c,
                           ozk_profile* prof);
@@ -164,7 +166,7 @@ ozk_status ozk_slices_gemm_device(ozk_format fmt, size_t m, size_t l, size_t n,
 /* ---- automatic split count (not in the reference) ------------- *
  * A policy for (split_count, drop_threshold) from the format and the inner
  * dimension alone: enough slices to capture the full K-word significand,
- * D = ceil(S*K / (S - sigma)) + 2 (S = 53, or 24 for TS; capped at 32), and the
+ * D = ceil(S*K / (S - sigma)) + 2 (S = 53, or 24 for TS), and the
  * reference's own pair pruning (ozaki.hpp:198-221) at
  * drop = 2^-(S*K + ceil(log2 l) + 2): pairs whose products are normwise below
  * the format's precision are skipped.  ozk_ozaki_gemm(..., D, drop, ...) with
@@ -213,6 +215,20 @@ ozk_status ozk_digits_gemm_device(ozk_format fmt, size_t m, size_t l, size_t n,
 ozk_status ozk_mpmat_write(const char* path, int fmt, size_t m, size_t n, const void* a);
 ozk_status ozk_mpmat_read_header(const char* path, int* fmt, size_t* m, size_t* n);
 ozk_status ozk_mpmat_read(const char* path, int fmt, size_t m, size_t n, void* a);
+
+/* The reference's accumulation phase on its own (ozaki.hpp:235-244): for each
+ * element, acc = 0; acc += products[p] for p = 0..nproducts-1 in order, with
+ * MultiFloat<K> + double; c receives the m x n K-word result (binary32 words
+ * for TS, each product rounded to binary32 first -- exact for TS slice
+ * products).  For callers that form the slice products with their own
+ * GemmBackend (mpmat::gpu::ozaki_gemm with a foreign backend).  Host version:
+ * products[p] are m x n row-major host arrays; device version: one contiguous
+ * nproducts x m x n device array. */
+ozk_status ozk_accumulate_products(ozk_format fmt, size_t m, size_t n,
+                                   const double* const* products, int nproducts, void* c);
+ozk_status ozk_accumulate_products_device(ozk_format fmt, size_t m, size_t n,
+                                          const double* products, int nproducts, void* c,
+                                          void* stream);
 
 /* Parity hook: every slice product C_ab = A_alpha * B_beta of the pair list,
  * binary64, into products[p] (m x n row-major). */

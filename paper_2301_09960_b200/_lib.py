@@ -99,6 +99,10 @@ SIGNATURES = {
     "ozk_probe_i8_tops": (ctypes.c_double, [ctypes.c_int, ctypes.c_void_p]),
     "ozk_set_engine": (ctypes.c_int, [ctypes.c_int]),
     "ozk_get_engine": (ctypes.c_int, []),
+    "ozk_accumulate_products": (ctypes.c_int, [ctypes.c_int, _sz, _sz, ctypes.c_void_p,
+                                               ctypes.c_int, _dp]),
+    "ozk_accumulate_products_device": (ctypes.c_int, [ctypes.c_int, _sz, _sz, _dp, ctypes.c_int,
+                                                      _dp, ctypes.c_void_p]),
     "ozk_trim_device_pool": (ctypes.c_int, []),
     "ozk_last_error": (ctypes.c_char_p, []),
     "ozk_version": (ctypes.c_int, []),

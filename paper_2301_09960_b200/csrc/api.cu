@@ -147,25 +147,20 @@ int shift_bits(size_t inner, int short_bits = 53) {
     return (short_bits + cl + 1) / 2;
 }
 
+// ozaki.hpp:209-221: alpha-major triangular set, optionally pruned
 void triangular_pairs(int d, PairList& pl) {
-    pl.count = 0;
+    pl.clear();
     for (int a = 0; a < d; ++a)
-        for (int b = 0; a + b < d; ++b) {
-            pl.alpha[pl.count] = (unsigned char)a;
-            pl.beta[pl.count] = (unsigned char)b;
-            ++pl.count;
-        }
+        for (int b = 0; a + b < d; ++b) pl.push(a, b);
 }
 
 void pruned_pairs(int d, const double* amax, const double* bmax, double drop, PairList& pl) {
     const double lead = amax[0] * bmax[0];
-    pl.count = 0;
+    pl.clear();
     for (int a = 0; a < d; ++a)
         for (int b = 0; a + b < d; ++b) {
             if (drop > 0.0 && amax[a] * bmax[b] < drop * lead) continue;
-            pl.alpha[pl.count] = (unsigned char)a;
-            pl.beta[pl.count] = (unsigned char)b;
-            ++pl.count;
+            pl.push(a, b);
         }
 }
 
@@ -613,7 +608,7 @@ ozk_status check_gemm_args(int fmt, size_t m, size_t l, size_t n, int d, double 
     if (m == 0 || l == 0 || n == 0) return fail(OZK_ESHAPE, "matrix dimensions must be positive");
     if (d < 1) return fail(OZK_EPARAM, "ozaki_gemm: split count must be >= 1");
     if (drop < 0.0) return fail(OZK_EPARAM, "ozaki_gemm: negative drop threshold");
-    if (d > kMaxSplits) return fail(OZK_EPARAM, "ozaki_gemm: split count above 32 is not supported");
+    if (d > kMaxSplits) return fail(OZK_EPARAM, "ozaki_gemm: split count above 65535 is not supported");
     if (m > 0x7fffffffull || n > 0x7fffffffull || l > 0x7fffffffull)
         return fail(OZK_ESHAPE, "ozaki_gemm: dimension too large");
     return OZK_OK;
@@ -803,7 +798,7 @@ ozk_status ozk_split(ozk_format fmt, size_t rows, size_t cols, const void* mat, 
     if (!valid_fmt(fmt)) return fail(OZK_EPARAM, "split_matrix: format must be DD, TD, QD or TS");
     if (rows == 0 || cols == 0) return fail(OZK_ESHAPE, "matrix dimensions must be positive");
     if (d < 1) return fail(OZK_EPARAM, "split_matrix: split count must be >= 1");
-    if (d > kMaxSplits) return fail(OZK_EPARAM, "split_matrix: split count above 32 is not supported");
+    if (d > kMaxSplits) return fail(OZK_EPARAM, "split_matrix: split count above 65535 is not supported");
     if (side != OZK_SIDE_ROWS && side != OZK_SIDE_COLS)
         return fail(OZK_EPARAM, "split_matrix: bad side");
     const int K = words_of(fmt), wb = word_bytes_of(fmt);
@@ -875,7 +870,7 @@ ozk_status ozk_split_slices_device(ozk_format fmt, size_t rows, size_t cols, siz
     if (!valid_fmt(fmt)) return fail(OZK_EPARAM, "split_matrix: format must be DD, TD, QD or TS");
     if (rows == 0 || cols == 0) return fail(OZK_ESHAPE, "matrix dimensions must be positive");
     if (d < 1) return fail(OZK_EPARAM, "split_matrix: split count must be >= 1");
-    if (d > kMaxSplits) return fail(OZK_EPARAM, "split_matrix: split count above 32 is not supported");
+    if (d > kMaxSplits) return fail(OZK_EPARAM, "split_matrix: split count above 65535 is not supported");
     if (ld < cols) return fail(OZK_ESHAPE, "split_matrix: ld < cols");
     if (plane_rows < (side == OZK_SIDE_ROWS ? rows : cols))
         return fail(OZK_ESHAPE, "split_matrix: plane_rows < outer dimension");
@@ -898,7 +893,7 @@ ozk_status ozk_split_slices_device(ozk_format fmt, size_t rows, size_t cols, siz
 ozk_status ozk_pair_list(int d, const double* amax, const double* bmax, double drop, int* pairs,
                          int* npairs) {
     if (d < 1) return fail(OZK_EPARAM, "pair_list: split count must be >= 1");
-    if (d > kMaxSplits) return fail(OZK_EPARAM, "pair_list: split count above 32 is not supported");
+    if (d > kMaxSplits) return fail(OZK_EPARAM, "pair_list: split count above 65535 is not supported");
     if (drop < 0.0) return fail(OZK_EPARAM, "pair_list: negative drop threshold");
     PairList pl;
     if (drop > 0.0)
@@ -914,14 +909,13 @@ ozk_status ozk_pair_list(int d, const double* amax, const double* bmax, double d
 }
 
 static ozk_status fill_pairs(int d, const int* pairs, int npairs, PairList& pl) {
-    if (npairs < 0 || npairs > kMaxPairs) return fail(OZK_EPARAM, "pair list too long");
-    pl.count = npairs;
+    if (npairs < 0 || (npairs > 0 && !pairs)) return fail(OZK_EPARAM, "bad pair list");
+    pl.clear();
     for (int p = 0; p < npairs; ++p) {
         if (pairs[2 * p] < 0 || pairs[2 * p] >= d || pairs[2 * p + 1] < 0 ||
             pairs[2 * p + 1] >= d)
             return fail(OZK_EPARAM, "pair index out of range");
-        pl.alpha[p] = (unsigned char)pairs[2 * p];
-        pl.beta[p] = (unsigned char)pairs[2 * p + 1];
+        pl.push(pairs[2 * p], pairs[2 * p + 1]);
     }
     return OZK_OK;
 }
@@ -1227,7 +1221,7 @@ ozk_status ozk_split_digits_device(ozk_format fmt, size_t rows, size_t cols, siz
     if (!valid_fmt(fmt)) return fail(OZK_EPARAM, "split_digits: format must be DD, TD, QD or TS");
     if (rows == 0 || cols == 0) return fail(OZK_ESHAPE, "matrix dimensions must be positive");
     if (d < 1) return fail(OZK_EPARAM, "split_matrix: split count must be >= 1");
-    if (d > kMaxSplits) return fail(OZK_EPARAM, "split_matrix: split count above 32 is not supported");
+    if (d > kMaxSplits) return fail(OZK_EPARAM, "split_matrix: split count above 65535 is not supported");
     if (ld < cols) return fail(OZK_ESHAPE, "split_matrix: ld < cols");
     const size_t inner = side == OZK_SIDE_ROWS ? cols : rows;
     const size_t outer = side == OZK_SIDE_ROWS ? rows : cols;
@@ -1445,6 +1439,58 @@ ozk_status ozk_backend_gemm(size_t m, size_t l, size_t n, const double* a, const
     OZK_CUDA(cudaMemcpyAsync(c, dc.p, sizeof(double) * m * n, cudaMemcpyDeviceToHost, os.s),
              "backend_gemm: D2H");
     OZK_CUDA(cudaStreamSynchronize(os.s), "backend_gemm");
+    return OZK_OK;
+}
+
+ozk_status ozk_accumulate_products_device(ozk_format fmt, size_t m, size_t n,
+                                          const double* products, int nproducts, void* c,
+                                          void* stream) {
+    if (!valid_fmt(fmt)) return fail(OZK_EPARAM, "accumulate: format must be DD, TD, QD or TS");
+    if (m == 0 || n == 0) return fail(OZK_ESHAPE, "matrix dimensions must be positive");
+    if (nproducts < 0) return fail(OZK_EPARAM, "accumulate: negative product count");
+    cudaStream_t st = (cudaStream_t)stream;
+    if (nproducts == 0) {
+        OZK_CUDA(cudaMemsetAsync(c, 0, elem_bytes(fmt) * m * n, st), "accumulate: zero");
+    } else {
+        OZK_CUDA(launch_accumulate_products(words_of(fmt), word_bytes_of(fmt), products, nproducts,
+                                            m * n, c, st),
+                 "accumulate");
+    }
+    OZK_CUDA(cudaStreamSynchronize(st), "accumulate");
+    return OZK_OK;
+}
+
+ozk_status ozk_accumulate_products(ozk_format fmt, size_t m, size_t n,
+                                   const double* const* products, int nproducts, void* c) {
+    if (!valid_fmt(fmt)) return fail(OZK_EPARAM, "accumulate: format must be DD, TD, QD or TS");
+    if (m == 0 || n == 0) return fail(OZK_ESHAPE, "matrix dimensions must be positive");
+    if (nproducts < 0 || (nproducts > 0 && !products))
+        return fail(OZK_EPARAM, "accumulate: bad product list");
+    const size_t eb = elem_bytes(fmt);
+    OwnStream os;
+    OZK_CUDA(os.create(), "accumulate: stream");
+    num_sms_cached();
+    // row blocks keep the device copy of the products under ~1 GiB
+    const size_t per_row = (size_t)(nproducts > 0 ? nproducts : 1) * n * sizeof(double);
+    size_t rb = ((size_t)1 << 30) / per_row;
+    rb = rb < 1 ? 1 : (rb > m ? m : rb);
+    DevBuf dp, dc;
+    OZK_CUDA(dp.alloc(per_row * rb, os.s), "accumulate: products");
+    OZK_CUDA(dc.alloc(eb * rb * n, os.s), "accumulate: C");
+    for (size_t r0 = 0; r0 < m; r0 += rb) {
+        const size_t rows = m - r0 < rb ? m - r0 : rb;
+        for (int p = 0; p < nproducts; ++p)
+            OZK_CUDA(cudaMemcpyAsync(dp.as<double>() + (size_t)p * rows * n, products[p] + r0 * n,
+                                     rows * n * sizeof(double), cudaMemcpyHostToDevice, os.s),
+                     "accumulate: H2D");
+        if (ozk_status s = ozk_accumulate_products_device(fmt, rows, n, dp.as<double>(), nproducts,
+                                                          dc.p, os.s))
+            return s;
+        OZK_CUDA(cudaMemcpyAsync(static_cast<char*>(c) + r0 * n * eb, dc.p, rows * n * eb,
+                                 cudaMemcpyDeviceToHost, os.s),
+                 "accumulate: D2H");
+    }
+    OZK_CUDA(cudaStreamSynchronize(os.s), "accumulate");
     return OZK_OK;
 }
 

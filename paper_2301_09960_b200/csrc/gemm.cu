@@ -152,7 +152,7 @@ __device__ __forceinline__ TileCoord tile_of(int id, int tiles_m, int tiles_n_bl
 // representable in binary32, so the cast before the TS epilogue is exact).
 template <int K, int MODE, typename W>
 __global__ void __launch_bounds__(kThreads, 1)
-pair_gemm_kernel(const __grid_constant__ TmaMaps maps, const __grid_constant__ PairList pairs,
+pair_gemm_kernel(const __grid_constant__ TmaMaps maps, const __grid_constant__ PairChunk pairs,
                  GemmProblem prob, int tiles_m, int tiles_n_blk) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -300,7 +300,7 @@ pair_gemm_kernel(const __grid_constant__ TmaMaps maps, const __grid_constant__ P
                     phase ^= 1;
                 }
                 if constexpr (MODE == kAccumulate) {
-                    if (kb == num_kb - kPrefetchKb && p > 0) {
+                    if (kb == num_kb - kPrefetchKb && (p > 0 || prob.c_continue)) {
                         // pull this pair's C rows into L2 ahead of the read-modify-write
 #pragma unroll
                         for (int mf = 0; mf < 8; ++mf)
@@ -348,7 +348,8 @@ pair_gemm_kernel(const __grid_constant__ TmaMaps maps, const __grid_constant__ P
                         const bool ok = (cmask >> q) & 1u;
                         const int off = ((q >> 1) * 8 + (q & 1)) * K;
 #pragma unroll
-                        for (int k = 0; k < K; ++k) w[q][k] = (ok && p > 0) ? cp[off + k] : W(0);
+                        for (int k = 0; k < K; ++k)
+                            w[q][k] = (ok && (p > 0 || prob.c_continue)) ? cp[off + k] : W(0);
                     }
 #ifdef OZK_EXPERIMENT_TRIVIAL_EPILOGUE
 #pragma unroll
@@ -402,7 +403,7 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
 }
 
 template <int K, int MODE, typename W = double>
-cudaError_t launch_typed(const GemmProblem& prob, const PairList& pairs, cudaStream_t st,
+cudaError_t launch_typed(const GemmProblem& prob, const PairChunk& pairs, cudaStream_t st,
                          int num_sms) {
     auto encode = get_encode();
     if (!encode) return cudaErrorNotSupported;
@@ -448,8 +449,9 @@ cudaError_t launch_typed(const GemmProblem& prob, const PairList& pairs, cudaStr
 
 } // namespace
 
-cudaError_t launch_pair_gemm(int K, GemmMode mode, const GemmProblem& prob, const PairList& pairs,
-                             cudaStream_t st, int num_sms, int word_bytes) {
+namespace {
+cudaError_t launch_chunk(int K, GemmMode mode, const GemmProblem& prob, const PairChunk& pairs,
+                         cudaStream_t st, int num_sms, int word_bytes) {
     if (mode == kStorePlain) return launch_typed<1, kStorePlain>(prob, pairs, st, num_sms);
     if (mode == kAccumulate && word_bytes == 4) {
         if (K != 3) return cudaErrorInvalidValue;
@@ -462,6 +464,23 @@ cudaError_t launch_pair_gemm(int K, GemmMode mode, const GemmProblem& prob, cons
     case 4: return launch_typed<4, kAccumulate>(prob, pairs, st, num_sms);
     default: return cudaErrorInvalidValue;
     }
+}
+}  // namespace
+
+// Pair lists longer than one launch's parameter block run as consecutive
+// launches: each later chunk continues the K-word sum already in C (same
+// per-element pair order), or writes its products further along.
+cudaError_t launch_pair_gemm(int K, GemmMode mode, const GemmProblem& prob, const PairList& pairs,
+                             cudaStream_t st, int num_sms, int word_bytes) {
+    for (int q0 = 0; q0 < pairs.count; q0 += kPairsPerLaunch) {
+        GemmProblem pb = prob;
+        if (mode == kAccumulate) pb.c_continue = prob.c_continue || q0 > 0;
+        if (mode == kStoreProducts) pb.c = static_cast<double*>(prob.c) + q0 * prob.c_pair_stride;
+        const cudaError_t e = launch_chunk(K, mode, pb, pair_chunk(pairs, q0), st, num_sms,
+                                           word_bytes);
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
 }
 
 } // namespace ozk

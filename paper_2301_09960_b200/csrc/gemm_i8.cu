@@ -499,7 +499,7 @@ __device__ __forceinline__ void trace_stamp(int, int, bool) {}
 template <int K, typename W, int ND, int TR, int EG, bool kVec, int CM, int CN, int NB,
           bool PR = false>
 __global__ void __launch_bounds__(I8Cfg<K, W, ND, TR, EG, NB>::kThreads, 1)
-pair_gemm_i8_kernel(const __grid_constant__ MapsI8 maps, const __grid_constant__ PairList pairs,
+pair_gemm_i8_kernel(const __grid_constant__ MapsI8 maps, const __grid_constant__ PairChunk pairs,
                     I8Problem prob, int tiles_m, int tiles_n) {
     constexpr int kCluster = CM * CN;
     static_assert((TC / CM) % 8 == 0 && (TR / CN) % 8 == 0, "multicast slices of 8-row atoms");
@@ -986,7 +986,7 @@ I8Geometry geometry_typed(int num_sms) {
 
 template <int K, typename W, int ND, int TR, int EG = 2, int CM = 1, int CN = 1, int NB = 2,
           bool PR = false>
-cudaError_t launch_i8_typed(const I8Operands& op, const PairList& pairs, cudaStream_t st,
+cudaError_t launch_i8_chunk(const I8Operands& op, const PairChunk& pairs, cudaStream_t st,
                             int num_sms) {
     using Cfg = I8Cfg<K, W, ND, TR, EG, NB>;
     auto encode = get_encode_i8();
@@ -1069,6 +1069,23 @@ cudaError_t launch_i8_typed(const I8Operands& op, const PairList& pairs, cudaStr
         if (e == cudaSuccess) e = f;
     }
     return e;
+}
+
+// Pair lists longer than one launch's parameter block: consecutive launches,
+// each later chunk continuing the K-word sum in C (PR: writing further along).
+template <int K, typename W, int ND, int TR, int EG = 2, int CM = 1, int CN = 1, int NB = 2,
+          bool PR = false>
+cudaError_t launch_i8_typed(const I8Operands& op, const PairList& pairs, cudaStream_t st,
+                            int num_sms) {
+    for (int q0 = 0; q0 < pairs.count; q0 += kPairsPerLaunch) {
+        I8Operands o = op;
+        o.c_init = op.c_init && q0 == 0;
+        if (PR) o.c = static_cast<double*>(op.c) + q0 * op.pair_stride;
+        const cudaError_t e = launch_i8_chunk<K, W, ND, TR, EG, CM, CN, NB, PR>(
+            o, pair_chunk(pairs, q0), st, num_sms);
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
 }
 
 } // namespace

@@ -2,6 +2,7 @@
 #pragma once
 
 #include <string>
+#include <vector>
 
 #include <cuda_runtime.h>
 #include <stddef.h>
@@ -9,8 +10,14 @@
 
 namespace ozk {
 
-constexpr int kMaxSplits = 32;                                  // D <= 32
-constexpr int kMaxPairs = kMaxSplits * (kMaxSplits + 1) / 2;    // 528
+// Split counts: slice indices are 16-bit in the kernels' pair lists; the
+// reference itself only requires d >= 1 (ozaki.hpp:185).  Memory (D slices per
+// side) is the practical limit long before this.
+constexpr int kMaxSplits = 65535;
+// Pairs per kernel launch (the pair list travels in the kernel parameter
+// block); longer lists run as consecutive launches that continue the K-word
+// accumulation in C, so the per-element pair order is unchanged.
+constexpr int kPairsPerLaunch = 528;
 
 // Device-side error flags raised by the split kernel (read back by the host).
 enum DevErr : int { kDevOk = 0, kDevNonFinite = 1, kDevTooLarge = 2 };
@@ -55,11 +62,37 @@ cudaError_t launch_transpose(int K, int word_bytes, const void* in, size_t in_ld
 // Slice-pair GEMM with fused epilogue (K2 + K3).
 enum GemmMode : int { kStorePlain = 0, kAccumulate = 1, kStoreProducts = 2 };
 
+// Host-side pair list (alpha-major, ozaki.hpp:210-221), any length.
 struct PairList {
-    int count;
-    unsigned char alpha[kMaxPairs];
-    unsigned char beta[kMaxPairs];
+    int count = 0;
+    std::vector<unsigned short> alpha, beta;
+    void clear() {
+        count = 0;
+        alpha.clear();
+        beta.clear();
+    }
+    void push(int a, int b) {
+        alpha.push_back((unsigned short)a);
+        beta.push_back((unsigned short)b);
+        ++count;
+    }
 };
+
+// One launch's slice of a PairList (kernel parameter).
+struct PairChunk {
+    int count;
+    unsigned short alpha[kPairsPerLaunch];
+    unsigned short beta[kPairsPerLaunch];
+};
+inline PairChunk pair_chunk(const PairList& pl, int first) {
+    PairChunk c;
+    c.count = pl.count - first < kPairsPerLaunch ? pl.count - first : kPairsPerLaunch;
+    for (int p = 0; p < c.count; ++p) {
+        c.alpha[p] = pl.alpha[first + p];
+        c.beta[p] = pl.beta[first + p];
+    }
+    return c;
+}
 
 struct GemmProblem {
     // A slices: [d][m][lda] doubles (k contiguous); B^T slices in column blocks:
@@ -77,6 +110,7 @@ struct GemmProblem {
     size_t ldc;         // elements per row of C
     size_t c_pair_stride;  // kStoreProducts: doubles between consecutive pair products
     uint32_t zero;         // always 0 (runtime value: carries a register dependency)
+    uint32_t c_continue;   // kAccumulate: 1 = C already holds a running sum (later pair chunk)
 };
 
 cudaError_t launch_pair_gemm(int K, GemmMode mode, const GemmProblem& prob, const PairList& pairs,
@@ -118,6 +152,11 @@ cudaError_t launch_pair_products_i8(int word_bytes, const I8Operands& op, const 
 // a(i, j) -= c(i, j) in K-word arithmetic (a: row stride lda elements, c dense).
 cudaError_t launch_kw_sub_inplace(int K, double* a, size_t lda, const double* c, size_t rows,
                                   size_t cols, cudaStream_t st);
+
+// Accumulation phase on its own (accumulate.cu, ozaki.hpp:235-244): c (count
+// K-word elements) = sum over p of prods[p * count + e], in p order.
+cudaError_t launch_accumulate_products(int K, int word_bytes, const double* prods, int np,
+                                       size_t count, void* c, cudaStream_t st);
 
 // Direct triple-single GEMM (csrc/ts_direct.cu): a (m x l), b (l x n), c (m x n),
 // 3 binary32 words per element.

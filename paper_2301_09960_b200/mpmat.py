@@ -196,13 +196,17 @@ def _stream_handle() -> int:
 def ozaki_gemm(a, b, d: int, backend=None, drop_threshold: float = 0.0):
     """Long-precision product via the Ozaki split (ozaki.hpp:180-249).
 
-    ``backend`` must be ``None`` or :func:`gpu_backend` -- the slice products
-    run on the B200 (exact INT8 tcgen05 digit GEMMs where they apply, else FP64
-    DMMA, fused with the accumulation; any conforming backend gives the same
-    C, test_ozaki.cpp:227-233).  Returns ``(C, OzakiProfile)``.
+    ``backend`` ``None`` or :func:`gpu_backend`: the slice products run on the
+    B200 (exact INT8 tcgen05 digit GEMMs where they apply, else FP64 DMMA,
+    fused with the accumulation; any conforming backend gives the same C,
+    test_ozaki.cpp:227-233).  Any other callable ``backend(a_slice, b_slice)``
+    is a caller's GemmBackend (backend.hpp:12-13) and is used as the reference
+    uses it: called once per pair of the (pruned) triangular set, alpha-major
+    (ozaki.hpp:223-231), with the split and the K-word accumulation
+    (ozaki.hpp:235-244) on the B200.  Returns ``(C, OzakiProfile)``.
     """
     if backend is not None and not getattr(backend, "_ozk_gpu", False):
-        raise param_error("ozaki_gemm: only the B200 backend (gpu_backend()) is supported")
+        return _ozaki_gemm_with_backend(a, b, int(d), backend, float(drop_threshold))
     m, l, ka = _kword_shape(a)
     l2, n, kb = _kword_shape(b)
     if ka != kb:
@@ -227,6 +231,46 @@ def ozaki_gemm(a, b, d: int, backend=None, drop_threshold: float = 0.0):
                             float(drop_threshold), c.ctypes.data, ctypes.byref(prof))
     _raise(st)
     return c, OzakiProfile._of(prof)
+
+
+def _ozaki_gemm_with_backend(a, b, d, backend, drop):
+    import time
+    m, l, ka = _kword_shape(a)
+    l2, n, kb = _kword_shape(b)
+    if ka != kb:
+        raise param_error("ozaki_gemm: A and B must have the same format")
+    if l != l2:
+        raise shape_error("ozaki_gemm: inner dimensions differ")
+    if d < 1:
+        raise param_error("ozaki_gemm: split count must be >= 1")
+    if drop < 0.0:
+        raise param_error("ozaki_gemm: negative drop threshold")
+    t0 = time.perf_counter()
+    sa = split_matrix(_host(a, ka), d, SplitSide.rows)
+    sb = split_matrix(_host(b, ka), d, SplitSide.cols)
+    t1 = time.perf_counter()
+    amax = np.array([np.max(np.abs(p)) if p.size else 0.0 for p in sa.pieces], dtype=np.float64)
+    bmax = np.array([np.max(np.abs(p)) if p.size else 0.0 for p in sb.pieces], dtype=np.float64)
+    pairs = (ctypes.c_int * (2 * d * d))()
+    np_ = ctypes.c_int(0)
+    _raise(lib.ozk_pair_list(d, amax.ctypes.data, bmax.ctypes.data, drop, pairs,
+                             ctypes.byref(np_)))
+    products = []
+    for p in range(np_.value):
+        c = np.ascontiguousarray(backend(sa.pieces[pairs[2 * p]].astype(np.float64),
+                                         sb.pieces[pairs[2 * p + 1]].astype(np.float64)),
+                                 dtype=np.float64)
+        if c.shape != (m, n):
+            raise shape_error("ozaki_gemm: backend returned a product of the wrong shape")
+        products.append(c)
+    t2 = time.perf_counter()
+    ptrs = (ctypes.c_void_p * max(len(products), 1))(*[c.ctypes.data for c in products])
+    out = np.empty((m, n, _words(ka)), dtype=_dtype(ka))
+    _raise(lib.ozk_accumulate_products(ka, m, n, ptrs, len(products), out.ctypes.data))
+    t3 = time.perf_counter()
+    prof = OzakiProfile(split_seconds=t1 - t0, product_seconds=t2 - t1,
+                        accumulate_seconds=t3 - t2, split_count=d, pairs=len(products))
+    return out, prof
 
 
 def ozaki_gemm_multi(a, b, d: int, devices=None, drop_threshold: float = 0.0):

@@ -145,9 +145,9 @@ def test_full_shape_parity(ozk, ref, port, fmt, n, d, spread, which):
         dig[side], ex[side] = dg, eg
     for side, idx, want, what in ((0, Rt, pa, "A"), (1, Ct, pb, "B")):
         dsel = dig[side][:, :, idx, :n].to(torch.int64)                  # d, nd, |idx|, n
-        val = sum(dsel[:, t] * (256 ** t) for t in range(nd))           # exact slice integers
-        g = ex[side][:, idx].to(torch.float64)                           # d, |idx|
-        rec = (val.to(torch.float64) * torch.pow(2.0, g)[:, :, None]).cpu().numpy()
+        val = sum(dsel[:, t] * (256 ** t) for t in range(nd)).cpu().numpy()  # slice integers
+        g = ex[side][:, idx].cpu().numpy()                               # d, |idx|
+        rec = np.ldexp(val.astype(np.float64), g[:, :, None])            # exact 2^g scaling
         w = want if side == 0 else np.swapaxes(want, 1, 2)              # d, |idx|, n
         assert_bitwise(rec.astype(np.float32) if ts else rec,
                        w.astype(np.float32) if ts else w.astype(np.float64),

@@ -700,3 +700,82 @@ def test_ozaki_gemm_multi_ts(ozk, port):
     want = port.ozaki_gemm_ts(a, b, 10)
     got, _ = ozk.ozaki_gemm_multi(a, b, 10, devices=[0, 0, 0])
     assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
+
+
+@pytest.mark.parametrize("engine", ["auto", "dmma"])
+@pytest.mark.parametrize("K,m,l,n,d", [(2, 6, 300, 5, 40), (3, 9, 64, 7, 36), (4, 5, 200, 4, 33)])
+def test_split_count_above_32(ozk, cpu, engine, K, m, l, n, d):
+    """The reference takes any D >= 1 (ozaki.hpp:185).  D(D+1)/2 > 528 pairs run as
+    consecutive launches continuing the K-word sum; the result is unchanged."""
+    a = cpu.gen_eq1(K, m, l, 600 + d)
+    b = cpu.gen_eq1(K, l, n, 601 + d)
+    want = cpu.ozaki_gemm(K, a, b, d)
+    ozk.set_engine(engine)
+    try:
+        got, prof = ozk.ozaki_gemm(a, b, d)
+    finally:
+        ozk.set_engine("auto")
+    assert prof.pairs == d * (d + 1) // 2
+    assert_bitwise(got, want, f"D={d} engine={engine}")
+    s = ozk.split_matrix(a, d, ozk.SplitSide.rows)
+    want_p, want_r = cpu.split(K, a, d, 0)
+    assert_bitwise(np.stack(s.pieces), want_p, "pieces D > 32")
+    assert_bitwise(s.residual, want_r, "residual D > 32")
+
+
+def test_caller_backend_called_per_pair(ozk, cpu):
+    """A caller's GemmBackend (test_ozaki.cpp:24-49 counting / shuffled
+    summation): called once per pair, reference order, C bit-identical."""
+    calls = []
+
+    def counting(x, y):
+        calls.append((x.shape, y.shape))
+        return cpu.backend_gemm(x, y)
+
+    def shuffled(x, y):
+        rng = np.random.default_rng(x.shape[0] * 131 + y.shape[1])
+        order = rng.permutation(x.shape[1])
+        c = np.zeros((x.shape[0], y.shape[1]))
+        for k in order:
+            c += np.outer(x[:, k], y[k, :])
+        return c
+
+    for K, d in ((2, 1), (2, 3), (3, 5), (4, 8)):
+        a = cpu.gen_eq1(K, 5, 4, 94 + K)
+        b = cpu.gen_eq1(K, 4, 7, 95 + K)
+        calls.clear()
+        got, prof = ozk.ozaki_gemm(a, b, d, backend=counting)
+        assert len(calls) == d * (d + 1) // 2
+        assert_bitwise(got, cpu.ozaki_gemm(K, a, b, d), f"counting backend K={K} D={d}")
+        got2, _ = ozk.ozaki_gemm(a, b, d, backend=shuffled)
+        assert_bitwise(got2, got, f"shuffled backend K={K} D={d}")
+    a = cpu.gen_eq1(4, 16, 24, 96)
+    b = cpu.gen_eq1(4, 24, 12, 97)
+    calls.clear()
+    got, prof = ozk.ozaki_gemm(a, b, 10, backend=counting, drop_threshold=1e-40)
+    assert 0 < len(calls) < 55 and prof.pairs == len(calls)
+    assert_bitwise(got, cpu.ozaki_gemm(4, a, b, 10, drop=1e-40), "pruned, caller backend")
+
+
+def test_accumulate_products_matches_reference(ozk, cpu, port):
+    """ozk_accumulate_products = the reference's accumulation phase
+    (ozaki.hpp:235-244) over exact slice products."""
+    import ctypes
+    for K, d in ((2, 6), (3, 9), (4, 12)):
+        a = cpu.gen_eq1(K, 17, 40, 700 + K)
+        b = cpu.gen_eq1(K, 40, 13, 701 + K)
+        pa, _ = cpu.split(K, a, d, 0)
+        pb, _ = cpu.split(K, b, d, 1)
+        prods = []
+        for x in range(d):
+            for y in range(d - x):
+                c, bad = port.exact_dgemm(pa[x], pb[y])
+                assert bad == 0
+                prods.append(c)
+        ptrs = (ctypes.c_void_p * len(prods))(*[p.ctypes.data for p in prods])
+        out = np.empty((17, 13, K))
+        assert ozk.lib.ozk_accumulate_products(K, 17, 13, ptrs, len(prods), out.ctypes.data) == 0
+        assert_bitwise(out, cpu.ozaki_gemm(K, a, b, d), f"accumulate K={K}")
+    zero = np.ones((3, 4, 2))
+    assert ozk.lib.ozk_accumulate_products(2, 3, 4, None, 0, zero.ctypes.data) == 0
+    assert (zero == 0).all()
