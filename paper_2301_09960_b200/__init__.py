@@ -15,6 +15,7 @@ from .mpmat import (  # noqa: F401
     error,
     exponent_ceil_log2,
     gemm_simple,
+    gen_matrix_eq1,
     get_engine,
     gpu_backend,
     io_error,
@@ -37,5 +38,5 @@ __all__ = [
     "ozaki_gemm", "param_error", "shape_error", "split_matrix", "split_shift_bits", "lib",
     "ts_direct_gemm", "lu_trailing_update", "set_engine", "get_engine", "io_error",
     "read_matrix_file", "write_matrix_file", "gemm_simple", "auto_split_policy",
-    "ozaki_gemm_auto", "ozaki_gemm_multi",
+    "ozaki_gemm_auto", "ozaki_gemm_multi", "gen_matrix_eq1",
 ]

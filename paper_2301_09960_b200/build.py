@@ -16,7 +16,8 @@ CSRC = os.path.join(HERE, "csrc")
 LIB_DIR = os.path.join(HERE, "lib")
 LIB = os.path.join(LIB_DIR, "libozk.so")
 SOURCES = ["api.cu", "split.cu", "gemm.cu", "gen.cu", "diag.cu", "ts_direct.cu", "lu.cu", "gemm_i8.cu",
-           "io.cu", "direct.cu", "accumulate.cu"]
+           "io.cu", "direct.cu", "accumulate.cu",
+           "staging.cu"]
 HOST_SOURCES = ["gen_host.cpp"]  # host-only C++ (g++, strict FP like the reference)
 HEADERS = ["kword.cuh", "ozk_internal.cuh"]
 

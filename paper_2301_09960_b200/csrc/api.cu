@@ -24,6 +24,8 @@
 #include <tuple>
 #include <map>
 
+#include <sched.h>
+
 #include "../../include/ozk.h"
 #include "ozk_internal.cuh"
 
@@ -385,14 +387,27 @@ struct HostOverlap {
     int b_blocks = 1;
     size_t b_block_cols = 0;
     const cudaEvent_t* b_block_ready = nullptr;
+    // optional: called before every wait on one of the events above (pageable
+    // buffers: blocks until the staging worker has recorded it)
+    std::function<cudaError_t(cudaEvent_t)> before_wait;
+    cudaError_t wait(cudaStream_t st, cudaEvent_t ev) const {
+        if (before_wait) {
+            const cudaError_t e = before_wait(ev);
+            if (e != cudaSuccess) return e;
+        }
+        return cudaStreamWaitEvent(st, ev, 0);
+    }
 };
 
 // C = A * B via the Ozaki scheme on device buffers; A has row stride lda, B
 // row stride ldb (elements), C is dense m x n.
+// forced (optional): the pair list to use instead of the one from this call's
+// own slice maxima (ozk_ozaki_gemm_multi: one list from the global maxima of
+// every device's rows).
 ozk_status ozaki_device_impl(int fmt, size_t m, size_t l, size_t n, const void* a, size_t lda,
                              const void* b, size_t ldb, int d, double drop, void* c,
                              cudaStream_t st, ozk_profile* prof,
-                             const HostOverlap* ov = nullptr) {
+                             const HostOverlap* ov = nullptr, const PairList* forced = nullptr) {
     const int K = words_of(fmt), wb = word_bytes_of(fmt);
     const int sms = num_sms_cached();
     const size_t ldk = slice_ld(l);
@@ -414,13 +429,16 @@ ozk_status ozaki_device_impl(int fmt, size_t m, size_t l, size_t n, const void* 
         OZK_CUDA(sb.alloc(sizeof(double) * d * n * ldk, st), "ozaki_gemm: slices B");
     }
     OZK_CUDA(work.alloc(elem_bytes(fmt) * (m > n ? m : n) * l, st), "ozaki_gemm: work");
-    // flags layout: [err int (8 B)][amax d][bmax d]
+    // flags layout: [A err int][B err int][amax d][bmax d]; separate A and B
+    // flags so an A error is reported first, as split_matrix(a) runs before
+    // split_matrix(b) (ozaki.hpp:194-195)
     OZK_CUDA(flags.alloc(8 + 16 * (size_t)d, st), "ozaki_gemm: flags");
     OZK_CUDA(cudaMemsetAsync(flags.p, 0, 8 + 16 * (size_t)d, st), "ozaki_gemm: memset");
     int* err = flags.as<int>();
+    int* errB = err + 1;
     unsigned long long* amax = reinterpret_cast<unsigned long long*>(flags.as<char>() + 8);
     unsigned long long* bmax = amax + d;
-    const bool want_max = drop > 0.0;
+    const bool want_max = drop > 0.0 && !forced;
     DigitOut digA, digB;
     if (use_i8) {
         digA.nd = nd;
@@ -446,30 +464,32 @@ ozk_status ozaki_device_impl(int fmt, size_t m, size_t l, size_t n, const void* 
     if (!banded_a) {
         if (ov && ov->a_ready)
             for (int q = 0; q < ov->bands; ++q)
-                OZK_CUDA(cudaStreamWaitEvent(st, ov->a_ready[q], 0), "ozaki_gemm: wait A");
+                OZK_CUDA(ov->wait(st, ov->a_ready[q]), "ozaki_gemm: wait A");
         OZK_CUDA(split_to_slices(fmt, m, l, lda, a, d, OZK_SIDE_ROWS, sa.as<double>(), m, work.p,
                                  want_max ? amax : nullptr, err, st, digA),
                  "ozaki_gemm: split A");
     }
     if (!blocked_b) {
-        if (ov && ov->b_ready)
-            OZK_CUDA(cudaStreamWaitEvent(st, ov->b_ready, 0), "ozaki_gemm: wait B");
+        if (ov && ov->b_ready) OZK_CUDA(ov->wait(st, ov->b_ready), "ozaki_gemm: wait B");
         OZK_CUDA(split_to_slices(fmt, l, n, ldb, b, d, OZK_SIDE_COLS, sb.as<double>(), n, work.p,
-                                 want_max ? bmax : nullptr, err, st, digB),
+                                 want_max ? bmax : nullptr, errB, st, digB),
                  "ozaki_gemm: split B");
     }
     tm.mark(1, st);
 
     PairList pl;
-    if (want_max) {
+    if (forced) {
+        pl = *forced;
+    } else if (want_max) {
         std::vector<double> host(1 + 2 * (size_t)d);
         OZK_CUDA(cudaMemcpyAsync(host.data(), flags.p, 8 + 16 * (size_t)d, cudaMemcpyDeviceToHost,
                                  st),
                  "ozaki_gemm: maxima");
         OZK_CUDA(cudaStreamSynchronize(st), "ozaki_gemm: split");
-        int flag;
-        std::memcpy(&flag, host.data(), sizeof(int));
-        if (ozk_status s = check_dev_err(flag, "split_matrix")) return s;
+        int flag[2];
+        std::memcpy(flag, host.data(), sizeof(flag));
+        if (ozk_status s = check_dev_err(flag[0], "split_matrix")) return s;
+        if (ozk_status s = check_dev_err(flag[1], "split_matrix")) return s;
         pruned_pairs(d, host.data() + 1, host.data() + 1 + d, drop, pl);
     } else {
         triangular_pairs(d, pl);
@@ -508,7 +528,7 @@ ozk_status ozaki_device_impl(int fmt, size_t m, size_t l, size_t n, const void* 
         if (banded_a) {
             // this band's A rows: per-row split, identical to the rows of the
             // whole-matrix split (ozaki.hpp:102-103)
-            OZK_CUDA(cudaStreamWaitEvent(st, ov->a_ready[band], 0), "ozaki_gemm: wait A");
+            OZK_CUDA(ov->wait(st, ov->a_ready[band]), "ozaki_gemm: wait A");
             DigitOut dband = digA;
             if (use_i8) {
                 dband.digits += r0 * ld8;
@@ -556,14 +576,14 @@ ozk_status ozaki_device_impl(int fmt, size_t m, size_t l, size_t n, const void* 
                     const size_t c0 = (size_t)j * ov->b_block_cols;
                     if (c0 >= n) break;
                     const size_t w = n - c0 < ov->b_block_cols ? n - c0 : ov->b_block_cols;
-                    OZK_CUDA(cudaStreamWaitEvent(st, ov->b_block_ready[j], 0), "ozaki_gemm: wait B");
+                    OZK_CUDA(ov->wait(st, ov->b_block_ready[j]), "ozaki_gemm: wait B");
                     DigitOut dblk = digB;
                     dblk.digits += c0 * ld8;
                     dblk.exps += c0;
                     split_timers.push_back(std::make_unique<Timer>(prof != nullptr));
                     split_timers.back()->mark(0, st);
                     OZK_CUDA(split_to_slices(fmt, l, w, ldb, static_cast<const char*>(b) + c0 * eb,
-                                             d, OZK_SIDE_COLS, nullptr, n, work.p, nullptr, err,
+                                             d, OZK_SIDE_COLS, nullptr, n, work.p, nullptr, errB,
                                              st, dblk),
                              "ozaki_gemm: split B block");
                     split_timers.back()->mark(1, st);
@@ -583,11 +603,12 @@ ozk_status ozaki_device_impl(int fmt, size_t m, size_t l, size_t n, const void* 
     }
     tm.mark(2, st);
 
-    int flag = 0;
-    OZK_CUDA(cudaMemcpyAsync(&flag, err, sizeof(int), cudaMemcpyDeviceToHost, st),
+    int flag[2] = {0, 0};
+    OZK_CUDA(cudaMemcpyAsync(flag, err, sizeof(flag), cudaMemcpyDeviceToHost, st),
              "ozaki_gemm: flag");
     OZK_CUDA(cudaStreamSynchronize(st), "ozaki_gemm");
-    if (ozk_status s = check_dev_err(flag, "split_matrix")) return s;
+    if (ozk_status s = check_dev_err(flag[0], "split_matrix")) return s;
+    if (ozk_status s = check_dev_err(flag[1], "split_matrix")) return s;
     if (prof) {
         double split_banded = 0.0;
         for (const auto& t : split_timers) split_banded += t->secs(0, 1);
@@ -677,12 +698,47 @@ ozk_status ozk_ozaki_gemm(ozk_format fmt, size_t m, size_t l, size_t n, const vo
     OZK_CUDA(xs.create(), "ozaki_gemm: copy stream");
     OZK_CUDA(ys.create(), "ozaki_gemm: copy stream");
     DevBuf da, db, dc;
+    // events are destroyed after the staging workers and copy streams drained
+    struct EventGuard {
+        std::vector<cudaEvent_t> evs;  // owned handles
+        ~EventGuard() {
+            for (cudaEvent_t e : evs) cudaEventDestroy(e);
+        }
+    } guard;
+    // Pageable caller buffers (DenseMatrix storage) move through pinned staging
+    // slots on worker threads (staging.cu), keeping the same band schedule.
+    const bool staging_on = [] {
+        const char* v = std::getenv("OZK_PAGEABLE_STAGING");
+        return !(v && !std::strcmp(v, "0"));
+    }();
+    const bool a_pg = staging_on && !host_is_pinned(a), b_pg = staging_on && !host_is_pinned(b),
+               c_pg = staging_on && !host_is_pinned(c);
+    std::unique_ptr<HostStaging> hs;
+    // on every exit: the staging workers drained and the copy streams idle
+    // before the device buffers go back to the pool
+    struct Drain {
+        std::unique_ptr<HostStaging>* hs;
+        cudaStream_t s[3];
+        ~Drain() {
+            if (*hs) (*hs)->finish();
+            for (cudaStream_t x : s) cudaStreamSynchronize(x);
+        }
+    } drain{&hs, {xs.s, ys.s, os.s}};
+    if (a_pg || b_pg || c_pg) {
+        int cpus = (int)std::thread::hardware_concurrency();
+        cpu_set_t set;
+        if (sched_getaffinity(0, sizeof(set), &set) == 0) cpus = CPU_COUNT(&set);
+        hs = std::make_unique<HostStaging>(xs.s, ys.s, std::max(1, std::min(8, cpus / 2)));
+    }
+    std::map<cudaEvent_t, int> staged_job;  // H2D event -> staging job number
     OZK_CUDA(da.alloc(eb * m * l, os.s), "ozaki_gemm: A");
     OZK_CUDA(db.alloc(eb * l * n, os.s), "ozaki_gemm: B");
     OZK_CUDA(dc.alloc(eb * m * n, os.s), "ozaki_gemm: C");
     cudaEvent_t allocated = nullptr, b_ready = nullptr;
     OZK_CUDA(cudaEventCreateWithFlags(&allocated, cudaEventDisableTiming), "ozaki_gemm: event");
+    guard.evs.push_back(allocated);
     OZK_CUDA(cudaEventCreateWithFlags(&b_ready, cudaEventDisableTiming), "ozaki_gemm: event");
+    guard.evs.push_back(b_ready);
     // B in 4 column blocks (whole 128-column tiles) when the first band can be
     // multiplied block by block (INT8 engine, no pruning, n >= 4096): at
     // n = 8192 a block's H2D time matches its GEMM block
@@ -705,51 +761,61 @@ ozk_status ozk_ozaki_gemm(ozk_format fmt, size_t m, size_t l, size_t n, const vo
     const int b_blocks = (int)((n + b_block_cols - 1) / b_block_cols);
     std::vector<cudaEvent_t> band_done(bands, nullptr), a_ready(bands, nullptr),
         b_block_ready(b_blocks, nullptr);
-    struct EventGuard {
-        std::vector<cudaEvent_t*> evs;
-        ~EventGuard() {
-            for (auto* e : evs)
-                if (*e) cudaEventDestroy(*e);
-        }
-    } guard;
-    guard.evs = {&allocated, &b_ready};
     for (auto* vec : {&band_done, &a_ready, &b_block_ready})
         for (auto& e : *vec) {
             OZK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "ozaki_gemm: event");
-            guard.evs.push_back(&e);
+            guard.evs.push_back(e);
         }
     OZK_CUDA(cudaEventRecord(allocated, os.s), "ozaki_gemm: event");
     OZK_CUDA(cudaStreamWaitEvent(xs.s, allocated, 0), "ozaki_gemm: wait");
     OZK_CUDA(cudaStreamWaitEvent(ys.s, allocated, 0), "ozaki_gemm: wait");
+    // one H2D copy of `rows` rows of `width` bytes (pitches dpitch / spitch),
+    // followed by `ev` on the H2D stream: staged when the source is pageable
+    auto h2d = [&](bool pageable, void* dst, size_t dpitch, const void* src, size_t spitch,
+                   size_t width, size_t rows, cudaEvent_t ev) -> cudaError_t {
+        if (pageable) {
+            StagedCopy sc;
+            sc.dev = dst;
+            sc.host = const_cast<void*>(src);
+            sc.width = width;
+            sc.height = rows;
+            sc.dev_pitch = dpitch;
+            sc.host_pitch = spitch;
+            sc.event = ev;
+            const int job = hs->push_h2d(sc);
+            if (ev) staged_job[ev] = job;
+            return cudaSuccess;
+        }
+        cudaError_t e = cudaSuccess;
+        if (width && rows)
+            e = rows == 1 ? cudaMemcpyAsync(dst, src, width, cudaMemcpyHostToDevice, xs.s)
+                          : cudaMemcpy2DAsync(dst, dpitch, src, spitch, width, rows,
+                                              cudaMemcpyHostToDevice, xs.s);
+        if (e == cudaSuccess && ev) e = cudaEventRecord(ev, xs.s);
+        return e;
+    };
     // Copy order on the H2D stream.  Whole B: B (its split gates every band),
     // then A band by band.  B in column blocks: A band 0, then the B blocks
     // (strided copies of the row-major B), then the other A bands.
     auto copy_a_band = [&](int q) -> cudaError_t {
         const size_t r0 = band_start[q], rows = band_start[q + 1] - r0;
-        cudaError_t e = cudaSuccess;
-        if (rows)
-            e = cudaMemcpyAsync(static_cast<char*>(da.p) + r0 * l * eb,
-                                static_cast<const char*>(a) + r0 * l * eb, rows * l * eb,
-                                cudaMemcpyHostToDevice, xs.s);
-        if (e == cudaSuccess) e = cudaEventRecord(a_ready[q], xs.s);
-        return e;
+        return h2d(a_pg, static_cast<char*>(da.p) + r0 * l * eb, 0,
+                   static_cast<const char*>(a) + r0 * l * eb, 0, rows * l * eb, 1, a_ready[q]);
     };
     if (b_blocks > 1) {
         OZK_CUDA(copy_a_band(0), "ozaki_gemm: H2D A");
         for (int j = 0; j < b_blocks; ++j) {
             const size_t c0 = (size_t)j * b_block_cols;
             const size_t w = n - c0 < b_block_cols ? n - c0 : b_block_cols;
-            OZK_CUDA(cudaMemcpy2DAsync(static_cast<char*>(db.p) + c0 * eb, n * eb,
-                                       static_cast<const char*>(b) + c0 * eb, n * eb, w * eb, l,
-                                       cudaMemcpyHostToDevice, xs.s),
+            OZK_CUDA(h2d(b_pg, static_cast<char*>(db.p) + c0 * eb, n * eb,
+                         static_cast<const char*>(b) + c0 * eb, n * eb, w * eb, l,
+                         b_block_ready[j]),
                      "ozaki_gemm: H2D B block");
-            OZK_CUDA(cudaEventRecord(b_block_ready[j], xs.s), "ozaki_gemm: event");
         }
+        OZK_CUDA(h2d(b_pg, nullptr, 0, nullptr, 0, 0, 0, b_ready), "ozaki_gemm: event");
     } else {
-        OZK_CUDA(cudaMemcpyAsync(db.p, b, eb * l * n, cudaMemcpyHostToDevice, xs.s),
-                 "ozaki_gemm: H2D B");
+        OZK_CUDA(h2d(b_pg, db.p, 0, b, 0, eb * l * n, 1, b_ready), "ozaki_gemm: H2D B");
     }
-    OZK_CUDA(cudaEventRecord(b_ready, xs.s), "ozaki_gemm: event");
     for (int q = b_blocks > 1 ? 1 : 0; q < bands; ++q) OZK_CUDA(copy_a_band(q), "ozaki_gemm: H2D A");
     HostOverlap ov;
     ov.b_ready = b_ready;
@@ -761,26 +827,38 @@ ozk_status ozk_ozaki_gemm(ozk_format fmt, size_t m, size_t l, size_t n, const vo
         ov.b_block_cols = b_block_cols;
         ov.b_block_ready = b_block_ready.data();
     }
+    if (hs)
+        ov.before_wait = [&](cudaEvent_t ev) -> cudaError_t {
+            auto it = staged_job.find(ev);
+            return it == staged_job.end() ? cudaSuccess : hs->wait_recorded(it->second);
+        };
     int band = 0;
     ov.on_band = [&](size_t r0, size_t r1) -> cudaError_t {
         cudaEvent_t ev = band_done[band < bands ? band : bands - 1];
         ++band;
         cudaError_t e = cudaEventRecord(ev, os.s);
-        if (e == cudaSuccess) e = cudaStreamWaitEvent(ys.s, ev, 0);
+        if (e != cudaSuccess) return e;
+        char* hc = static_cast<char*>(c) + r0 * n * eb;
+        char* dcp = static_cast<char*>(dc.p) + r0 * n * eb;
+        if (c_pg) {
+            StagedCopy sc;
+            sc.dev = dcp;
+            sc.host = hc;
+            sc.width = (r1 - r0) * n * eb;
+            sc.event = ev;
+            hs->push_d2h(sc);
+            return cudaSuccess;
+        }
+        e = cudaStreamWaitEvent(ys.s, ev, 0);
         if (e == cudaSuccess)
-            e = cudaMemcpyAsync(static_cast<char*>(c) + r0 * n * eb,
-                                static_cast<char*>(dc.p) + r0 * n * eb, (r1 - r0) * n * eb,
-                                cudaMemcpyDeviceToHost, ys.s);
+            e = cudaMemcpyAsync(hc, dcp, (r1 - r0) * n * eb, cudaMemcpyDeviceToHost, ys.s);
         return e;
     };
     ozk_profile local{};
     ozk_status s =
         ozaki_device_impl((int)fmt, m, l, n, da.p, l, db.p, n, d, drop, dc.p, os.s, &local, &ov);
-    if (s != OZK_OK) {
-        cudaStreamSynchronize(xs.s);
-        cudaStreamSynchronize(ys.s);
-        return s;
-    }
+    if (s != OZK_OK) return s;  // drain syncs the copy streams first
+    if (hs) OZK_CUDA(hs->finish(), "ozaki_gemm: staged copies");
     OZK_CUDA(cudaStreamSynchronize(xs.s), "ozaki_gemm: H2D");
     OZK_CUDA(cudaStreamSynchronize(ys.s), "ozaki_gemm: D2H C");
     OZK_CUDA(cudaStreamSynchronize(os.s), "ozaki_gemm");
@@ -1020,7 +1098,7 @@ ozk_status ozk_ozaki_gemm_multi(ozk_format fmt, int ngpus, const int* devices, s
     std::vector<double> maxima((size_t)ngpus * 2 * d, 0.0);
     std::vector<double> secs(ngpus, 0.0);
     std::atomic<bool> failed{false};
-    std::atomic<int> pairs_used{0};
+    std::atomic<int> pairs_used{-1};
     auto worker = [&](int r) {
         auto t0 = std::chrono::steady_clock::now();
         size_t r0, r1;
@@ -1043,15 +1121,80 @@ ozk_status ozk_ozaki_gemm_multi(ozk_format fmt, int ngpus, const int* devices, s
                   cuda_ok(os.create(), "ozaki_gemm_multi: stream");
         if (ok && nd == 0) {
             // DMMA engine or an inner dimension the INT8 engine does not take:
-            // this device's rows against the whole B through the 1-GPU host path
-            if (rows) {
-                const ozk_status s2 = ozk_ozaki_gemm(fmt, rows, l, n,
-                                                     static_cast<const char*>(a) + r0 * l * eb, b,
-                                                     d, drop, static_cast<char*>(c) + r0 * n * eb,
-                                                     nullptr);
-                if (s2 != OZK_OK) fail_here(s2);
+            // this device's rows against the whole B.  With pruning, the pair
+            // list comes from the GLOBAL slice maxima (every device's rows, as
+            // the reference's piece_max over all of A, ozaki.hpp:194-208), so
+            // every device keeps the same pairs as the 1-GPU call.
+            DevBuf work, mx;
+            ok = cuda_ok(da.alloc(eb * std::max<size_t>(rows, 1) * l, os.s), "alloc A") &&
+                 cuda_ok(db.alloc(eb * l * n, os.s), "alloc B") &&
+                 cuda_ok(dc.alloc(eb * std::max<size_t>(rows, 1) * n, os.s), "alloc C") &&
+                 cuda_ok(work.alloc(eb * l * std::max(std::max<size_t>(rows, 1), n), os.s),
+                         "alloc") &&
+                 cuda_ok(mx.alloc(8 + 16 * (size_t)d, os.s), "alloc") &&
+                 cuda_ok(cudaMemsetAsync(mx.p, 0, 8 + 16 * (size_t)d, os.s), "memset");
+            if (ok && rows)
+                ok = cuda_ok(cudaMemcpyAsync(da.p, static_cast<const char*>(a) + r0 * l * eb,
+                                             rows * l * eb, cudaMemcpyHostToDevice, os.s),
+                             "ozaki_gemm_multi: H2D A");
+            if (ok)
+                ok = cuda_ok(cudaMemcpyAsync(db.p, b, eb * l * n, cudaMemcpyHostToDevice, os.s),
+                             "ozaki_gemm_multi: H2D B");
+            if (ok && drop > 0.0) {
+                // maxima only: the split kernel without slice outputs
+                int* ferr = mx.as<int>();
+                auto* am = reinterpret_cast<unsigned long long*>(mx.as<char>() + 8);
+                if (rows)
+                    ok = cuda_ok(split_to_slices(fmt, rows, l, l, da.p, d, OZK_SIDE_ROWS, nullptr,
+                                                 rows, work.p, am, ferr, os.s),
+                                 "ozaki_gemm_multi: maxima A");
+                if (ok)
+                    ok = cuda_ok(split_to_slices(fmt, l, n, n, db.p, d, OZK_SIDE_COLS, nullptr, n,
+                                                 work.p, am + d, ferr + 1, os.s),
+                                 "ozaki_gemm_multi: maxima B");
+                std::vector<double> host(1 + 2 * (size_t)d);
+                if (ok)
+                    ok = cuda_ok(cudaMemcpyAsync(host.data(), mx.p, 8 + 16 * (size_t)d,
+                                                 cudaMemcpyDeviceToHost, os.s),
+                                 "ozaki_gemm_multi: maxima") &&
+                         cuda_ok(cudaStreamSynchronize(os.s), "ozaki_gemm_multi: maxima");
+                if (ok) {
+                    int flag[2];
+                    std::memcpy(flag, host.data(), sizeof(flag));
+                    for (int f : flag)
+                        if (ok && f) {
+                            const ozk_status s2 = check_dev_err(f, "split_matrix");
+                            fail_here(s2);
+                            ok = false;
+                        }
+                    std::memcpy(maxima.data() + (size_t)r * 2 * d, host.data() + 1,
+                                sizeof(double) * 2 * d);
+                }
             }
-            bar.arrive_and_wait();
+            bar.arrive_and_wait();  // every device's maxima are in
+            if (ok && !failed && rows) {
+                PairList pl;
+                if (drop > 0.0) {
+                    std::vector<double> am(d, 0.0), bm(d, 0.0);
+                    for (int q = 0; q < ngpus; ++q)
+                        for (int s2 = 0; s2 < d; ++s2) {
+                            am[s2] = std::max(am[s2], maxima[(size_t)q * 2 * d + s2]);
+                            bm[s2] = std::max(bm[s2], maxima[(size_t)q * 2 * d + d + s2]);
+                        }
+                    pruned_pairs(d, am.data(), bm.data(), drop, pl);
+                } else {
+                    triangular_pairs(d, pl);
+                }
+                pairs_used = pl.count;
+                const ozk_status s2 = ozaki_device_impl(fmt, rows, l, n, da.p, l, db.p, n, d, drop,
+                                                        dc.p, os.s, nullptr, nullptr, &pl);
+                if (s2 != OZK_OK) fail_here(s2), ok = false;
+                if (ok)
+                    ok = cuda_ok(cudaMemcpyAsync(static_cast<char*>(c) + r0 * n * eb, dc.p,
+                                                 rows * n * eb, cudaMemcpyDeviceToHost, os.s),
+                                 "ozaki_gemm_multi: D2H C") &&
+                         cuda_ok(cudaStreamSynchronize(os.s), "ozaki_gemm_multi");
+            }
             bar.arrive_and_wait();
             bar.arrive_and_wait();
             secs[r] = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
@@ -1160,10 +1303,14 @@ ozk_status ozk_ozaki_gemm_multi(ozk_format fmt, int ngpus, const int* devices, s
         bar.arrive_and_wait();
         secs[r] = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     };
+    // worker 0 runs on the caller's thread: its current device is restored after
+    int caller_dev = 0;
+    OZK_CUDA(cudaGetDevice(&caller_dev), "ozaki_gemm_multi: device");
     std::vector<std::thread> threads;
     for (int r = 1; r < ngpus; ++r) threads.emplace_back(worker, r);
     worker(0);
     for (auto& t : threads) t.join();
+    cudaSetDevice(caller_dev);
     for (int r = 0; r < ngpus; ++r)
         if (st[r] != OZK_OK) {
             g_last_error = msg[r];
@@ -1175,7 +1322,7 @@ ozk_status ozk_ozaki_gemm_multi(ozk_format fmt, int ngpus, const int* devices, s
         prof->split_count = d;
         PairList pl;
         triangular_pairs(d, pl);
-        prof->pairs = nd > 0 ? pairs_used.load() : pl.count;
+        prof->pairs = pairs_used.load() >= 0 ? pairs_used.load() : pl.count;
         prof->gpus = ngpus;
         prof->engine = nd > 0 ? OZK_ENGINE_INT8 : OZK_ENGINE_DMMA;
     }

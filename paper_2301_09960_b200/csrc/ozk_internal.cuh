@@ -19,8 +19,11 @@ constexpr int kMaxSplits = 65535;
 // accumulation in C, so the per-element pair order is unchanged.
 constexpr int kPairsPerLaunch = 528;
 
-// Device-side error flags raised by the split kernel (read back by the host).
-enum DevErr : int { kDevOk = 0, kDevNonFinite = 1, kDevTooLarge = 2 };
+// Device-side error flags raised by the split kernel (read back by the host),
+// combined with atomicMax: a non-finite entry anywhere outranks an entry too
+// large to shift, as the reference scans the whole matrix for finiteness before
+// any shift (ozaki.hpp:77-78 before :109).
+enum DevErr : int { kDevOk = 0, kDevTooLarge = 1, kDevNonFinite = 2 };
 
 // Leading dimension (doubles) of a slice row: the inner dimension rounded up to
 // 16 bytes, as TMA requires 16-byte global strides.  Pad entries are zero.
@@ -173,5 +176,38 @@ cudaError_t launch_direct_gemm(int K, const double* a, const double* b, double* 
                                size_t l, size_t n, cudaStream_t st);
 
 void set_last_error(const std::string& msg);  // api.cu (ozk_last_error)
+
+// ---- pageable host buffers (staging.cu) -------------------------------------
+bool host_is_pinned(const void* p);  // page-locked / registered host memory
+
+// One staged copy: `height` rows of `width` bytes, row pitches dev_pitch /
+// host_pitch.  H2D: `event` (optional) is recorded on the H2D stream after the
+// copy; D2H: the copy waits for `event` (already recorded) first.
+struct StagedCopy {
+    void* dev = nullptr;
+    void* host = nullptr;
+    size_t width = 0, height = 1, dev_pitch = 0, host_pitch = 0;
+    cudaEvent_t event = nullptr;
+};
+
+// Worker threads moving pageable buffers through pinned slot rings, in
+// submission order per direction.  push_h2d returns the job number;
+// wait_recorded(job) blocks until that job's event has been recorded (a
+// cudaStreamWaitEvent on an unrecorded event would not wait).  finish() drains
+// both queues (every D2H job is then in the caller's buffer).
+class HostStaging {
+public:
+    HostStaging(cudaStream_t h2d, cudaStream_t d2h, int threads);
+    ~HostStaging();
+    int push_h2d(const StagedCopy& c);
+    void push_d2h(const StagedCopy& c);
+    cudaError_t wait_recorded(int job);
+    cudaError_t finish();
+
+private:
+    struct Impl;
+    Impl* impl_;
+    int pushed_h2d_ = 0;
+};
 
 } // namespace ozk

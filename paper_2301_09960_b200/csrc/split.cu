@@ -155,14 +155,15 @@ split_rows_kernel(const T* __restrict__ in, size_t in_ld, T* __restrict__ work, 
             T c[K];
             load_kw<K>(w + j * K, c);
             const T lead = c[0];
-            prow[j] = (double)lead;
+            if (prow) prow[j] = (double)lead;
             if (keep_residual) {
                 kw_add<K>(c, -lead);
                 store_kw<K>(w + j * K, c);
             }
             pmx = fmax(pmx, (double)fabs_(lead));
         }
-        for (size_t j = cols + threadIdx.x; j < ldk; j += kSplitThreads) prow[j] = 0.0;
+        if (prow)
+            for (size_t j = cols + threadIdx.x; j < ldk; j += kSplitThreads) prow[j] = 0.0;
         if (piece_max) {
             pmx = block_max(pmx, red);
             if (threadIdx.x == 0)

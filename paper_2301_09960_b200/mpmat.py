@@ -193,6 +193,15 @@ def _stream_handle() -> int:
     return torch.cuda.current_stream().cuda_stream
 
 
+def _same_device(a, b, what: str):
+    """Device context for a CUDA call on a and b: the library allocates on the
+    current device and runs on its current stream, so make a's device current
+    (and refuse operands on different devices)."""
+    if a.device != b.device:
+        raise param_error(f"{what}: A and B must live on the same device")
+    return torch.cuda.device(a.device)
+
+
 def ozaki_gemm(a, b, d: int, backend=None, drop_threshold: float = 0.0):
     """Long-precision product via the Ozaki split (ozaki.hpp:180-249).
 
@@ -218,11 +227,12 @@ def ozaki_gemm(a, b, d: int, backend=None, drop_threshold: float = 0.0):
     if _is_cuda(a) or _is_cuda(b):
         if not (_is_cuda(a) and _is_cuda(b)):
             raise param_error("ozaki_gemm: A and B must live on the same device")
-        ad, bd = a.contiguous(), b.contiguous()
-        c = torch.empty((m, n, K), dtype=ad.dtype, device=a.device)
-        st = lib.ozk_ozaki_gemm_device(ka, m, l, n, ad.data_ptr(), bd.data_ptr(), int(d),
-                                       float(drop_threshold), c.data_ptr(), _stream_handle(),
-                                       ctypes.byref(prof))
+        with _same_device(a, b, "ozaki_gemm"):
+            ad, bd = a.contiguous(), b.contiguous()
+            c = torch.empty((m, n, K), dtype=ad.dtype, device=a.device)
+            st = lib.ozk_ozaki_gemm_device(ka, m, l, n, ad.data_ptr(), bd.data_ptr(), int(d),
+                                           float(drop_threshold), c.data_ptr(), _stream_handle(),
+                                           ctypes.byref(prof))
         _raise(st)
         return c, OzakiProfile._of(prof)
     ah, bh = _host(a, ka), _host(b, ka)
@@ -317,6 +327,19 @@ def ozaki_gemm_auto(a, b):
     return c, prof, d, drop
 
 
+def gen_matrix_eq1(fmt: int, m: int, n: int, seed: int, spread: int = 0) -> np.ndarray:
+    """gen_matrix_eq1<K>(m, n, seed) (gen.hpp:20-34): the reference's input
+    generator, bit for bit, on all host cores (csrc/gen_host.cpp).  fmt: K = 2,
+    3, 4 or OZK_TS; spread > 0 gives the config-5 exponent-spread variant."""
+    out = np.empty((m, n, _words(fmt)), dtype=_dtype(fmt))
+    if spread:
+        st = lib.ozk_gen_spread(fmt, m, n, seed, spread, out.ctypes.data, 0)
+    else:
+        st = lib.ozk_gen_eq1(fmt, m, n, seed, out.ctypes.data, 0)
+    _raise(st)
+    return out
+
+
 def split_matrix(m, d: int, side: SplitSide) -> SplitSet:
     """split_matrix<K> (ozaki.hpp:74-147): pieces + K-word residual (host arrays)."""
     rows, cols, k = _kword_shape(m)
@@ -342,9 +365,10 @@ def gpu_backend():
             l2, n = bd.shape
             if l != l2:
                 raise shape_error("backend: inner dimensions differ")
-            c = torch.empty((m, n), dtype=torch.float64, device=a.device)
-            _raise(lib.ozk_backend_gemm_device(m, l, n, ad.data_ptr(), bd.data_ptr(),
-                                               c.data_ptr(), _stream_handle()))
+            with _same_device(a, b, "backend"):
+                c = torch.empty((m, n), dtype=torch.float64, device=a.device)
+                _raise(lib.ozk_backend_gemm_device(m, l, n, ad.data_ptr(), bd.data_ptr(),
+                                                   c.data_ptr(), _stream_handle()))
             return c
         ah, bh = _host(a), _host(b)
         if ah.ndim != 2 or bh.ndim != 2 or ah.shape[1] != bh.shape[0]:
@@ -368,9 +392,10 @@ def ts_direct_gemm(a, b):
         raise shape_error("ts_direct_gemm: inner dimensions differ")
     if _is_cuda(a) and _is_cuda(b):
         ad, bd = a.contiguous(), b.contiguous()
-        c = torch.empty((m, n, 3), dtype=torch.float32, device=a.device)
-        _raise(lib.ozk_ts_direct_gemm_device(m, l, n, ad.data_ptr(), bd.data_ptr(), c.data_ptr(),
-                                             _stream_handle()))
+        with _same_device(a, b, "ts_direct_gemm"):
+            c = torch.empty((m, n, 3), dtype=torch.float32, device=a.device)
+            _raise(lib.ozk_ts_direct_gemm_device(m, l, n, ad.data_ptr(), bd.data_ptr(),
+                                                 c.data_ptr(), _stream_handle()))
         return c
     ah, bh = _host(a, OZK_TS), _host(b, OZK_TS)
     c = np.empty((m, n, 3), dtype=np.float32)
@@ -393,9 +418,10 @@ def gemm_simple(a, b):
     K = _words(fa)
     if _is_cuda(a) and _is_cuda(b):
         ad, bd = a.contiguous(), b.contiguous()
-        c = torch.empty((m, n, K), dtype=torch.float64, device=a.device)
-        _raise(lib.ozk_direct_gemm_device(fa, m, l, n, ad.data_ptr(), bd.data_ptr(), c.data_ptr(),
-                                          _stream_handle()))
+        with _same_device(a, b, "gemm_simple"):
+            c = torch.empty((m, n, K), dtype=torch.float64, device=a.device)
+            _raise(lib.ozk_direct_gemm_device(fa, m, l, n, ad.data_ptr(), bd.data_ptr(),
+                                              c.data_ptr(), _stream_handle()))
         return c
     ah, bh = _host(a, fa), _host(b, fa)
     c = np.empty((m, n, K), dtype=np.float64)

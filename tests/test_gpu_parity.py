@@ -779,3 +779,77 @@ def test_accumulate_products_matches_reference(ozk, cpu, port):
     zero = np.ones((3, 4, 2))
     assert ozk.lib.ozk_accumulate_products(2, 3, 4, None, 0, zero.ctypes.data) == 0
     assert (zero == 0).all()
+
+
+def test_host_api_pinned_and_pageable_agree(ozk, cpu, monkeypatch):
+    """ozk_ozaki_gemm's host path with every mix of pinned (page-locked) and
+    pageable caller buffers -- pageable ones are staged through pinned slots on
+    worker threads (csrc/staging.cu), strided B column blocks included -- and
+    with staging switched off (OZK_PAGEABLE_STAGING=0, the driver's own pageable
+    copies): bit-identical C."""
+    import ctypes
+
+    import torch
+    K, m, l, n, d = 3, 2304, 300, 4200, 4
+    a = cpu.gen_eq1(K, m, l, 31)
+    b = cpu.gen_eq1(K, l, n, 32)
+    pa, pb = torch.from_numpy(a).pin_memory(), torch.from_numpy(b).pin_memory()
+    pc = torch.empty((m, n, K), dtype=torch.float64).pin_memory()
+    ref_c = None
+    for a_pin in (True, False):
+        for b_pin in (True, False):
+            for c_pin in (True, False):
+                c = np.empty((m, n, K))
+                st = ozk.lib.ozk_ozaki_gemm(K, m, l, n, pa.data_ptr() if a_pin else a.ctypes.data,
+                                            pb.data_ptr() if b_pin else b.ctypes.data, d, 0.0,
+                                            pc.data_ptr() if c_pin else c.ctypes.data, None)
+                assert st == 0, ozk.lib.ozk_last_error()
+                got = pc.numpy().copy() if c_pin else c
+                if ref_c is None:
+                    ref_c = got
+                assert_bitwise(got, ref_c, f"pinned A={a_pin} B={b_pin} C={c_pin}")
+    monkeypatch.setenv("OZK_PAGEABLE_STAGING", "0")
+    c = np.empty((m, n, K))
+    assert ozk.lib.ozk_ozaki_gemm(K, m, l, n, a.ctypes.data, b.ctypes.data, d, 0.0,
+                                  c.ctypes.data, None) == 0
+    assert_bitwise(c, ref_c, "staging off")
+    rows = np.arange(0, m, 97)
+    want = cpu.ozaki_gemm(K, np.ascontiguousarray(a[rows]), b, d)
+    assert_bitwise(ref_c[rows], want, "sampled rows vs the reference")
+
+
+@pytest.mark.parametrize("K,l,devs", [(2, 100, [0, 0]), (3, 64, [0, 0, 0]), (2, 300, [0, 0])])
+def test_ozaki_gemm_multi_pruning_uses_global_maxima(ozk, cpu, K, l, devs):
+    """With drop_threshold > 0 every device prunes with the maxima of ALL rows
+    (ozaki.hpp:194-208), including the per-device fallback path (l <= 128 or
+    DMMA): device 0's rows are scaled down so its local maxima would keep a
+    different pair list."""
+    m, n, d = 96, 40, 8
+    a = cpu.gen_eq1(K, m, l, 400 + K)
+    b = cpu.gen_eq1(K, l, n, 401 + K)
+    a[: m // len(devs)] *= 2.0 ** -30
+    for drop in (2.0 ** -60, 2.0 ** -100):
+        want = cpu.ozaki_gemm(K, a, b, d, drop)
+        got, prof = ozk.ozaki_gemm_multi(a, b, d, devices=devs, drop_threshold=drop)
+        assert_bitwise(got, want, f"multi pruning K={K} l={l} drop={drop}")
+
+
+def test_error_precedence_matches_reference(ozk, cpu):
+    """Non-finite entries outrank entries too large to shift (the reference
+    scans for finiteness before any shift, ozaki.hpp:77-78 before :109), and
+    A's errors come before B's (split_matrix(a) runs first)."""
+    a = cpu.gen_eq1(2, 300, 300, 5)
+    b = cpu.gen_eq1(2, 300, 300, 6)
+    bad_nan = a.copy()
+    bad_nan[7, 3, 0] = np.nan
+    bad_nan[200, 9, :] = [2.0 ** 1010, 0.0]   # too large, in a later row
+    with pytest.raises(ozk.param_error, match="non-finite"):
+        ozk.ozaki_gemm(bad_nan, b, 4)
+    huge = a.copy()
+    huge[4, 4, :] = [2.0 ** 1010, 0.0]
+    nan_b = b.copy()
+    nan_b[1, 1, 0] = np.inf
+    with pytest.raises(ozk.param_error, match="too large"):
+        ozk.ozaki_gemm(huge, nan_b, 4)
+    with pytest.raises(ozk.param_error, match="non-finite"):
+        ozk.ozaki_gemm(a, nan_b, 4)
