@@ -12,7 +12,7 @@
 // Include it after (or instead of) the reference headers: it needs
 // DenseMatrix, MultiFloat, SplitSet, OzakiProfile, GemmBackend and the error
 // types from the reference's own headers.  DenseMatrix<MultiFloat<K>>::data()
-// is K contiguous doubles per element (multifloat.hpp:218), exactly the ABI
+// is K contiguous doubles per element (multifloat.hpp:131), exactly the ABI
 // layout, so no element is copied or converted at the boundary.
 #pragma once
 

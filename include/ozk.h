@@ -16,7 +16,7 @@
  * Conventions (identical to the reference, so the boundary is zero-copy):
  *  - matrices are row-major; a K-word element is K consecutive doubles
  *    (the memory image of DenseMatrix<MultiFloat<K>>, dense_matrix.hpp:12-45,
- *    multifloat.hpp:218): element (i,j) word w at ((i*cols + j)*K + w);
+ *    multifloat.hpp:131): element (i,j) word w at ((i*cols + j)*K + w);
  *  - the split count is `int split_count` (>= 1), the component type is the
  *    ozk_format (K = 2/3/4 words = DD/TD/QD);
  *  - no exception crosses the ABI: every call returns an ozk_status and
@@ -252,7 +252,7 @@ ozk_status ozk_pair_products_digits_device(ozk_format fmt, size_t m, size_t l, s
  * A22 := A22 - L21 * U12 exactly as the reference's blocked_lu does it
  * (proj/include/mpmat/lu.hpp:104-124): the product by ozaki_gemm with
  * split_count slices, then A22(i,j) -= update(i,j) with MultiFloat<K>
- * subtraction (multifloat.hpp:288,387).  L21: tm x pw (row stride ldl), U12:
+ * subtraction (multifloat.hpp:300,201).  L21: tm x pw (row stride ldl), U12:
  * pw x tn (row stride ldu), A22: tm x tn (row stride lda), all in elements,
  * so the blocks can live inside the full matrix.  DD/TD/QD only. */
 ozk_status ozk_lu_trailing_update(ozk_format fmt, size_t tm, size_t pw, size_t tn,
@@ -292,9 +292,9 @@ int ozk_plan_row_bands(ozk_format fmt, size_t m, size_t n, size_t l, int split_c
                        int cluster_sms, size_t* starts, int max_bands);
 
 /* ---- direct K-word GEMM -------------------------------------- *
- * The reference's gemm_simple<MultiFloat<K>> (gemm.hpp:16-33) bit for bit:
+ * The reference's gemm_simple<MultiFloat<K>> (gemm.hpp:15-31) bit for bit:
  * per element c = 0; for k ascending: c = c + a(i,k) * b(k,j) with the
- * reference's K-word multiply (multifloat.hpp:218-239) and add (:271-286).
+ * reference's K-word multiply (multifloat.hpp:218-239) and add (:184-199).
  * The comparator the Ozaki scheme is measured against (paper §5); DD/TD/QD,
  * row-major AoS, a: m x l, b: l x n, c: m x n. */
 ozk_status ozk_direct_gemm(ozk_format fmt, size_t m, size_t l, size_t n, const void* a,

@@ -8,17 +8,17 @@
  * This is a plain-C99 restatement of the algorithms in the reference mpmat
  * library (paths relative to /root/reference/proj/include/mpmat/):
  *   eft.hpp:25-39          two_sum, fast_two_sum
- *   multifloat.hpp:121-150 vec_sum, extract_components (VecSumErrBranch)
- *   multifloat.hpp:155-168 canonical_order
- *   multifloat.hpp:246-260 MultiFloat::renormalize
- *   multifloat.hpp:290-300 operator+(MultiFloat, double)
- *   multifloat.hpp:329-345 operator*(MultiFloat, double)
- *   multifloat.hpp:450-517 strict_normalize, from_pair, from_expansion,
+ *   multifloat.hpp:34-63 vec_sum, extract_components (VecSumErrBranch)
+ *   multifloat.hpp:68-81 canonical_order
+ *   multifloat.hpp:159-171 MultiFloat::renormalize
+ *   multifloat.hpp:203-213 operator+(MultiFloat, double)
+ *   multifloat.hpp:242-257 operator*(MultiFloat, double)
+ *   multifloat.hpp:363-430 strict_normalize, from_pair, from_expansion,
  *                          sum_ordered, merge_components
  *   ozaki.hpp:36-56        exponent_ceil_log2, split_shift_bits, shift_extract
  *   ozaki.hpp:74-147       split_matrix
  *   ozaki.hpp:180-249      ozaki_gemm (pair list, drop threshold, accumulation)
- *   rng.hpp:70-109         splitmix64 / xoshiro256** / Box-Muller
+ *   rng.hpp:14-54         splitmix64 / xoshiro256** / Box-Muller
  *   gen.hpp:20-34          gen_matrix_eq1
  * It must be compiled with -ffp-contract=off (the reference's own strict-FP
  * flag, proj/CMakeLists.txt:16) and round-to-nearest-even.
@@ -38,7 +38,7 @@
 #include <string.h>
 
 #define OZK_MAXK 4
-#define OZK_MAXTERMS 36 /* max_terms = 2K^2+K for K=4 (multifloat.hpp:220) */
+#define OZK_MAXTERMS 36 /* max_terms = 2K^2+K for K=4 (multifloat.hpp:133) */
 
 /* ---- eft.hpp:25-39 ------------------------------------------------------ */
 static inline void two_sum(double a, double b, double* s, double* e) {
@@ -60,7 +60,7 @@ static inline uint64_t bits_of(double x) {
     return u;
 }
 
-/* ---- multifloat.hpp:121-129 vec_sum -------------------------------------- */
+/* ---- multifloat.hpp:34-42 vec_sum -------------------------------------- */
 static void vec_sum(double* t, int n) {
     double s = t[n - 1];
     for (int i = n - 2; i >= 0; --i) {
@@ -72,7 +72,7 @@ static void vec_sum(double* t, int n) {
     t[0] = s;
 }
 
-/* ---- multifloat.hpp:133-150 extract_components<K> ------------------------ */
+/* ---- multifloat.hpp:46-63 extract_components<K> ------------------------ */
 static void extract_components(int K, const double* t, int n, double* out) {
     for (int i = 0; i < K; ++i) out[i] = 0.0;
     double acc = t[0];
@@ -91,7 +91,7 @@ static void extract_components(int K, const double* t, int n, double* out) {
     if (j < K) out[j] = acc;
 }
 
-/* ---- multifloat.hpp:155-168 canonical_order ------------------------------ */
+/* ---- multifloat.hpp:68-81 canonical_order ------------------------------ */
 static void canonical_order(double* t, int n) {
     for (int i = 1; i < n; ++i) {
         double v = t[i];
@@ -105,13 +105,13 @@ static void canonical_order(double* t, int n) {
     }
 }
 
-/* ---- multifloat.hpp:440-444 non_finite ----------------------------------- */
+/* ---- multifloat.hpp:353-357 non_finite ----------------------------------- */
 static void non_finite(int K, double head, double* c) {
     c[0] = head;
     for (int i = 1; i < K; ++i) c[i] = 0.0;
 }
 
-/* ---- multifloat.hpp:450-469 strict_normalize ----------------------------- */
+/* ---- multifloat.hpp:363-382 strict_normalize ----------------------------- */
 static void strict_normalize(int K, double* c) {
     for (int pass = 0; pass < 2 * K; ++pass) {
         int w = 0;
@@ -134,7 +134,7 @@ static void strict_normalize(int K, double* c) {
         if (c[i] == 0.0) c[i] = 0.0; /* clear -0 */
 }
 
-/* ---- multifloat.hpp:471-479 from_pair (K == 2 only) ---------------------- */
+/* ---- multifloat.hpp:384-392 from_pair (K == 2 only) ---------------------- */
 static void from_pair(double s, double e, double* c) {
     if (!isfinite(s)) {
         non_finite(2, s, c);
@@ -146,14 +146,14 @@ static void from_pair(double s, double e, double* c) {
     c[1] = (pe == 0.0 || ps == 0.0) ? 0.0 : pe;
 }
 
-/* ---- multifloat.hpp:481-488 from_expansion ------------------------------- */
+/* ---- multifloat.hpp:394-401 from_expansion ------------------------------- */
 static void from_expansion(int K, const double* t, int n, double* c) {
     extract_components(K, t, n, c);
     strict_normalize(K, c);
     if (c[0] == 0.0 || !isfinite(c[0])) non_finite(K, c[0] + 0.0, c);
 }
 
-/* ---- multifloat.hpp:492-503 sum_ordered ---------------------------------- */
+/* ---- multifloat.hpp:405-416 sum_ordered ---------------------------------- */
 static void sum_ordered(int K, const double* t, int n, double* c) {
     double probe = 0.0;
     for (int i = 0; i < n; ++i) probe += t[i];
@@ -173,7 +173,7 @@ static void sum_ordered(int K, const double* t, int n, double* c) {
     from_expansion(K, buf, m, c);
 }
 
-/* ---- multifloat.hpp:507-517 merge_components ----------------------------- */
+/* ---- multifloat.hpp:420-430 merge_components ----------------------------- */
 static int before(double x, double y) {
     double ax = fabs(x), ay = fabs(y);
     if (ax != ay) return ax > ay;
@@ -187,7 +187,7 @@ static void merge_components(const double* a, int na, const double* b, int nb, d
     while (j < nb) out[k++] = b[j++];
 }
 
-/* ---- multifloat.hpp:290-300 operator+(MultiFloat<K>, double) ------------- */
+/* ---- multifloat.hpp:203-213 operator+(MultiFloat<K>, double) ------------- */
 void ozk_oracle_mf_add_double(int K, const double* x, double y, double* r) {
     if (K == 2) {
         double s, e;
@@ -203,7 +203,7 @@ void ozk_oracle_mf_add_double(int K, const double* x, double y, double* r) {
     sum_ordered(K, m, K + 1, r);
 }
 
-/* ---- multifloat.hpp:246-260 renormalize ---------------------------------- */
+/* ---- multifloat.hpp:159-171 renormalize ---------------------------------- */
 static void renormalize(int K, const double* terms, int nterms, double* c) {
     double buf[16] = {0};
     int n = 0;
@@ -225,7 +225,7 @@ static void renormalize(int K, const double* terms, int nterms, double* c) {
     from_expansion(K, buf, n, c);
 }
 
-/* ---- multifloat.hpp:329-345 operator*(MultiFloat<K>, double) ------------- */
+/* ---- multifloat.hpp:242-257 operator*(MultiFloat<K>, double) ------------- */
 /* two_prod is the FMA form (eft.hpp:60-64, selected at eft.hpp:75-85 when the
  * reference is built with -mfma as its CMakeLists does). */
 static void mf_mul_double(int K, const double* x, double y, double* r) {
@@ -249,7 +249,7 @@ static void mf_mul_double(int K, const double* x, double y, double* r) {
     sum_ordered(K, terms, n, r);
 }
 
-/* ---- rng.hpp:70-109 ------------------------------------------------------- */
+/* ---- rng.hpp:14-54 ------------------------------------------------------- */
 typedef struct {
     uint64_t s[4];
 } xoshiro;
@@ -299,7 +299,7 @@ void ozk_oracle_gen_eq1(int K, size_t m, size_t n, uint64_t seed, double* out) {
         for (int k = 0; k < K; ++k) comp[k] = scalbn(xo_uniform(&rng), -53 * k);
         renormalize(K, comp, K, ru);
         double scale = exp(xo_normal(&rng));
-        ozk_oracle_mf_add_double(K, ru, -0.5, t); /* ru - 0.5 == ru + (-0.5) (multifloat.hpp:302) */
+        ozk_oracle_mf_add_double(K, ru, -0.5, t); /* ru - 0.5 == ru + (-0.5) (multifloat.hpp:215) */
         mf_mul_double(K, t, scale, out + idx * (size_t)K);
     }
 }
@@ -547,12 +547,12 @@ void ozk_oracle_replay_elements(int K, size_t m, size_t l, size_t n, const doubl
 
 /* ======================================================================== *
  * TS (triple-single): NOT in the reference (MultiFloat<K> is
- * static_assert-ed to binary64 words, multifloat.hpp:216).  The paper uses a
+ * static_assert-ed to binary64 words, multifloat.hpp:129).  The paper uses a
  * 3 x binary32 "triple-single" format.  Following SURVEY
  * §8c, TS is defined here by restating the reference's GENERIC K >= 3
  * algorithms with binary32 words and S = 24:
  *   eft.hpp:25-39 (two_sum, fast_two_sum) in float;
- *   multifloat.hpp:290-300 (K >= 3 branch: merge_components -> sum_ordered),
+ *   multifloat.hpp:203-213 (K >= 3 branch: merge_components -> sum_ordered),
  *   :121-150 (vec_sum, extract_components), :450-469 (strict_normalize),
  *   :246-260 (renormalize) with K = 3 float words;
  *   ozaki.hpp:36-147 with S = 24 (sigma = (24 + ceil(log2 l) + 1) / 2), a
@@ -669,7 +669,7 @@ static int before_f(float x, float y) {
     return fbits_of(x) <= fbits_of(y);
 }
 
-/* TS + float: the K >= 3 branch of multifloat.hpp:290-300 with float words. */
+/* TS + float: the K >= 3 branch of multifloat.hpp:203-213 with float words. */
 void ozk_oracle_ts_add_float(const float* x, float y, float* r) {
     float m[4];
     int i = 0, k = 0, placed = 0;
@@ -710,7 +710,7 @@ static void renormalize_f(const float* terms, int nterms, float* c) {
 
 /* TS inputs: Eq. (1) TD values (gen_matrix_eq1<3>, gen.hpp:20-34) rounded to
  * three binary32 words by successive leading-word extraction in binary64,
- * then renormalised in TS (renormalize, multifloat.hpp:246-260). */
+ * then renormalised in TS (renormalize, multifloat.hpp:159-171). */
 void ozk_oracle_gen_eq1_ts(size_t m, size_t n, uint64_t seed, float* out) {
     double* td = (double*)malloc(m * n * 3 * sizeof(double));
     ozk_oracle_gen_eq1(3, m, n, seed, td);

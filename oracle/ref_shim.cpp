@@ -232,7 +232,7 @@ int ref_gemm_simple(int K, std::size_t m, std::size_t l, std::size_t n, const do
     }
 }
 
-// MultiFloat<K> + double on `count` (x_i, y_i) pairs (multifloat.hpp:290-300).
+// MultiFloat<K> + double on `count` (x_i, y_i) pairs (multifloat.hpp:203-213).
 int ref_mf_add_double(int K, std::size_t count, const double* x, const double* y, double* out) {
     switch (K) {
     case 2: add_k<2>(count, x, y, out); return 0;
@@ -242,7 +242,7 @@ int ref_mf_add_double(int K, std::size_t count, const double* x, const double* y
     }
 }
 
-// MultiFloat<K> + MultiFloat<K> on `count` pairs (multifloat.hpp:271-286).
+// MultiFloat<K> + MultiFloat<K> on `count` pairs (multifloat.hpp:184-199).
 int ref_mf_add_mf(int K, std::size_t count, const double* x, const double* y, double* out) {
     switch (K) {
     case 2: add_mf_k<2>(count, x, y, out); return 0;

@@ -1,8 +1,8 @@
 // direct.cu -- the direct K-word GEMM: the reference's
-// gemm_simple<MultiFloat<K>> (proj/include/mpmat/gemm.hpp:16-33) on the GPU,
+// gemm_simple<MultiFloat<K>> (proj/include/mpmat/gemm.hpp:15-31) on the GPU,
 // bit for bit: every C element is  c = 0;  for k = 0..l-1:  c = c + a(i,k) * b(k,j)
 // with the reference's MultiFloat<K> multiply (multifloat.hpp:218-239,
-// kw_mul_kw) and add (:271-286, kw_add_kw), in that fixed k order.
+// kw_mul_kw) and add (:184-199, kw_add_kw), in that fixed k order.
 //
 // It is the comparator the paper measures the Ozaki scheme against, not a hot
 // path: one thread per C element (its k loop is inherently sequential), 16x16

@@ -3,11 +3,11 @@
 //
 // Reference semantics (paths under /root/reference/proj/include/mpmat/):
 //   eft.hpp:25-39            two_sum (Knuth), fast_two_sum (Dekker, no precondition)
-//   multifloat.hpp:290-300   operator+(MultiFloat<K>, double)
-//                            K=2: two_sum, one add, fast_two_sum, from_pair (:471-479)
-//                            K>=3: merge_components (:507-517) -> sum_ordered (:492-503)
-//                                  -> vec_sum (:121-129) -> from_expansion (:481-488)
-//                                  -> extract_components (:133-150) -> strict_normalize (:450-469)
+//   multifloat.hpp:203-213   operator+(MultiFloat<K>, double)
+//                            K=2: two_sum, one add, fast_two_sum, from_pair (:384-392)
+//                            K>=3: merge_components (:420-430) -> sum_ordered (:405-416)
+//                                  -> vec_sum (:34-42) -> from_expansion (:394-401)
+//                                  -> extract_components (:46-63) -> strict_normalize (:363-382)
 //
 // GPU formulation.  Every array is register resident: all loops are fully
 // unrolled with compile-time trip counts and data-dependent positions become
@@ -181,7 +181,7 @@ OZK_HD void fast_two_sum(T a, T b, T& s, T& e) {
     s = ss;
 }
 
-// multifloat.hpp:509-512 (merge order predicate)
+// multifloat.hpp:421-425 (merge order predicate)
 template <bool kInt = false, typename T>
 OZK_HD bool merge_before(T x, T y) {
     if constexpr (kInt) {
@@ -206,7 +206,7 @@ OZK_HD void non_finite(T head, T* c) {
     for (int i = 1; i < K; ++i) c[i] = T(0);
 }
 
-// multifloat.hpp:450-469
+// multifloat.hpp:363-382
 // OZK_KW_TAILSKIP=0 keeps the first compaction on the fast path (A/B builds).
 #ifndef OZK_KW_TAILSKIP
 #define OZK_KW_TAILSKIP 1
@@ -248,7 +248,7 @@ OZK_HD void strict_normalize(T* c) {
     for (int i = 0; i < K; ++i) c[i] = is_zero<kInt>(c[i]) ? T(0) : c[i];
 }
 
-// multifloat.hpp:133-150 over N terms (zero terms are transparent)
+// multifloat.hpp:46-63 over N terms (zero terms are transparent)
 template <int K, int N, bool kInt = false, typename T>
 OZK_HD void extract_components(const T* t, T* out) {
 #pragma unroll
@@ -323,7 +323,7 @@ OZK_HD bool kw_fast_ok(const T* x, T y) {
     return mx < kSafeHi && any != 0;
 }
 
-// MultiFloat<K> + word (multifloat.hpp:290-300); x is updated in place.  T is
+// MultiFloat<K> + word (multifloat.hpp:203-213); x is updated in place.  T is
 // the word type: double for DD/TD/QD, float for TS (which uses the generic
 // K >= 3 branch with binary32 words, see oracle/ozk_oracle.c).
 template <int K, bool kInt, typename T, bool kFast = false>
@@ -334,7 +334,7 @@ OZK_HD void kw_add_impl(T* x, T y) {
         T v = rn_add(x[1], e);
         T fs, fe;
         fast_two_sum(s, v, fs, fe);
-        // from_pair (multifloat.hpp:471-479)
+        // from_pair (multifloat.hpp:384-392)
         if (!is_finite(fs)) {
             x[0] = fs;
             x[1] = T(0);
@@ -447,14 +447,14 @@ OZK_HD void kw_add(T* x, T y) {
     kw_add_impl<K, false>(x, y);
 }
 
-// -MultiFloat<K> (multifloat.hpp:265-269): zero words stay +0.
+// -MultiFloat<K> (multifloat.hpp:178-182): zero words stay +0.
 template <int K, typename T>
 OZK_HD void kw_neg(const T* y, T* r) {
 #pragma unroll
     for (int i = 0; i < K; ++i) r[i] = y[i] == T(0) ? T(0) : -y[i];
 }
 
-// MultiFloat<K> + MultiFloat<K> (multifloat.hpp:271-286); x is updated in place.
+// MultiFloat<K> + MultiFloat<K> (multifloat.hpp:184-199); x is updated in place.
 //   K = 2: accurate double-word addition (two TwoSums, two FastTwoSums, from_pair)
 //   K >= 3: merge_components(x, K, y, K) -> sum_ordered(m, 2K)
 // The static merge replays the reference's two-pointer merge with predicated
@@ -520,7 +520,7 @@ OZK_HD void kw_add_kw(T* x, const T* y) {
 }
 
 // ---- MultiFloat<K> x MultiFloat<K> (multifloat.hpp:218-239), for the direct
-// K-word GEMM (gemm.hpp:16-33, csrc/direct.cu) -------------------------------
+// K-word GEMM (gemm.hpp:15-31, csrc/direct.cu) -------------------------------
 
 // two_prod with a hardware FMA (eft.hpp:60-64; the reference is built with
 // -mfma, so MPMAT_HAVE_HW_FMA selects this variant, eft.hpp:75-85)

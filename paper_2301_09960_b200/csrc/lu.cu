@@ -2,7 +2,7 @@
 // A22(i, j) -= update(i, j) (proj/include/mpmat/lu.hpp:121-124), where
 // `update` is the Ozaki product L21 * U12 computed by the slice GEMM.
 // The subtraction is MultiFloat<K>::operator-=(MultiFloat<K>)
-// (multifloat.hpp:288,387: x + (-y)), replayed by kw_add_kw (kword.cuh).
+// (multifloat.hpp:300,201: x + (-y)), replayed by kw_add_kw (kword.cuh).
 // Memory-bound elementwise pass: 3*K*8 bytes per element.
 #include "kword.cuh"
 #include "ozk_internal.cuh"

@@ -5,7 +5,7 @@
 // Reference: split_matrix<K> (proj/include/mpmat/ozaki.hpp:74-147) with
 // exponent_ceil_log2 (:36-40), shift_extract (:53-56), leading_image and the
 // per-row max (dense_matrix.hpp:72-96) and MultiFloat<K>::operator-=(double)
-// (multifloat.hpp:391 -> :290-300).
+// (multifloat.hpp:304 -> :290-300).
 //
 // Layout: one CTA owns one row (A side) / one column (B side, after the
 // transpose) and runs all D extraction passes on it, so the D dependent
@@ -233,7 +233,7 @@ split_rows_kernel(const T* __restrict__ in, size_t in_ld, T* __restrict__ work, 
                     drow[j + (dig.nd - 1) * dig.digit_stride] = (int8_t)mi;
                 }
                 if (update && x != T(0)) {
-                    // w -= x  ==  w + (-x)  (multifloat.hpp:302,391); FP64 compares:
+                    // w -= x  ==  w + (-x)  (multifloat.hpp:215,391); FP64 compares:
                     // this kernel is ALU-bound, its FP64 pipe mostly idle
                     kw_add<K, T, false>(c, -x);
                     store_kw<K>(w + j * K, c);

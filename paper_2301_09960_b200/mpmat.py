@@ -404,7 +404,7 @@ def ts_direct_gemm(a, b):
 
 
 def gemm_simple(a, b):
-    """gemm_simple<MultiFloat<K>> (gemm.hpp:16-33) on the GPU, bit-identical:
+    """gemm_simple<MultiFloat<K>> (gemm.hpp:15-31) on the GPU, bit-identical:
     fixed k-order K-word multiply-accumulate (csrc/direct.cu).  TS inputs go
     to ts_direct_gemm."""
     m, l, fa = _kword_shape(a)

@@ -494,7 +494,7 @@ def test_int8_engine_rejects_inapplicable(ozk, engine):
                                      (2, 64, 64, 64), (3, 17, 1, 5), (4, 1, 70, 1)])
 def test_direct_gemm_bitexact(ozk, ref, K, m, l, n):
     """Direct K-word GEMM = the reference's gemm_simple<MultiFloat<K>>
-    (gemm.hpp:16-33) bit for bit, host and device entry points."""
+    (gemm.hpp:15-31) bit for bit, host and device entry points."""
     import torch
     if ref is None:
         pytest.skip("oracle/_ref not built")
@@ -747,8 +747,9 @@ def test_caller_backend_called_per_pair(ozk, cpu):
         got, prof = ozk.ozaki_gemm(a, b, d, backend=counting)
         assert len(calls) == d * (d + 1) // 2
         assert_bitwise(got, cpu.ozaki_gemm(K, a, b, d), f"counting backend K={K} D={d}")
-        got2, _ = ozk.ozaki_gemm(a, b, d, backend=shuffled)
-        assert_bitwise(got2, got, f"shuffled backend K={K} D={d}")
+        if d > 1:  # D = 1 products are of unsplit leading images: not exact, order-dependent
+            got2, _ = ozk.ozaki_gemm(a, b, d, backend=shuffled)
+            assert_bitwise(got2, got, f"shuffled backend K={K} D={d}")
     a = cpu.gen_eq1(4, 16, 24, 96)
     b = cpu.gen_eq1(4, 24, 12, 97)
     calls.clear()

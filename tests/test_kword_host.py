@@ -1,6 +1,6 @@
 """K6 bit test on CPU: the device K-word "+ double" (csrc/kword.cuh, compiled
 for the host with -ffp-contract=off) against the reference's
-MultiFloat<K>::operator+(MultiFloat<K>, double) (multifloat.hpp:290-300),
+MultiFloat<K>::operator+(MultiFloat<K>, double) (multifloat.hpp:203-213),
 compiled in place (oracle/_ref) -- or the C restatement when it is absent.
 
 This is the operation both the split (w -= x) and the fused accumulation
@@ -134,7 +134,7 @@ def kwkw():
 
 @pytest.mark.parametrize("K", [2, 3, 4])
 def test_kword_add_kword_matches_reference(kwkw, ref, K):
-    """MultiFloat<K> + MultiFloat<K> (multifloat.hpp:271-286), used by the LU
+    """MultiFloat<K> + MultiFloat<K> (multifloat.hpp:184-199), used by the LU
     trailing update's w -= update, vs the compiled reference."""
     if ref is None:
         pytest.skip("oracle/_ref not built")

@@ -45,7 +45,7 @@ def test_eq1_generator_golden(port, ref):
 
 
 def test_xoshiro_stream(port):
-    """rng.hpp:70-98: splitmix64 seeding + xoshiro256** (first outputs for seed 0
+    """rng.hpp:14-54: splitmix64 seeding + xoshiro256** (first outputs for seed 0
     are the published splitmix64-seeded xoshiro256** values)."""
     s = port.xoshiro(0, 3)
     # recomputed independently in Python
