@@ -192,6 +192,23 @@ ozk_status ozk_split_digits_device(ozk_format fmt, size_t rows, size_t cols, siz
                                    int8_t* digits, size_t ld8, size_t plane_rows, int* exps,
                                    double* piece_max, void* stream);
 
+/* Asynchronous forms for pipelined callers (sharded.py): nothing is
+ * synchronised.  The split reports data errors (non-finite entry, too large to
+ * shift) through *dev_flag, a device int the caller zero-fills first and
+ * checks with ozk_check_split_flag (which synchronises `stream`); the return
+ * value covers argument and launch errors only.  Scratch is stream-ordered. */
+ozk_status ozk_split_digits_device_async(ozk_format fmt, size_t rows, size_t cols, size_t ld,
+                                         const void* mat, int split_count, ozk_side side,
+                                         int8_t* digits, size_t ld8, size_t plane_rows, int* exps,
+                                         double* piece_max, int* dev_flag, void* stream);
+ozk_status ozk_check_split_flag(const int* dev_flag, void* stream);
+ozk_status ozk_digits_gemm_device_async(ozk_format fmt, size_t m, size_t l, size_t n,
+                                        const int8_t* a_digits, const int* a_exps,
+                                        size_t a_plane_rows, const int8_t* b_digits,
+                                        const int* b_exps, size_t b_plane_rows, size_t ld8,
+                                        int split_count, const int* pairs, int npairs, void* c,
+                                        size_t ldc, void* stream);
+
 /* Fused INT8 slice-pair GEMMs + K-word accumulation over digit planes: A digits
  * for m rows (a_plane_rows >= m), B digits for n columns (b_plane_rows >= n),
  * both with row length ld8; c is m x n K-word, row stride ldc, overwritten. */

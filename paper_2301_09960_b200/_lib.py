@@ -66,6 +66,13 @@ SIGNATURES = {
     "ozk_split_digits_device": (ctypes.c_int, [ctypes.c_int, _sz, _sz, _sz, _dp, ctypes.c_int,
                                                ctypes.c_int, _dp, _sz, _sz, _dp, _dp,
                                                ctypes.c_void_p]),
+    "ozk_split_digits_device_async": (ctypes.c_int, [ctypes.c_int, _sz, _sz, _sz, _dp,
+                                                     ctypes.c_int, ctypes.c_int, _dp, _sz, _sz,
+                                                     _dp, _dp, _dp, ctypes.c_void_p]),
+    "ozk_check_split_flag": (ctypes.c_int, [_dp, ctypes.c_void_p]),
+    "ozk_digits_gemm_device_async": (ctypes.c_int, [ctypes.c_int, _sz, _sz, _sz, _dp, _dp, _sz,
+                                                    _dp, _dp, _sz, _sz, ctypes.c_int, _ip,
+                                                    ctypes.c_int, _dp, _sz, ctypes.c_void_p]),
     "ozk_digits_gemm_device": (ctypes.c_int, [ctypes.c_int, _sz, _sz, _sz, _dp, _dp, _sz, _dp,
                                               _dp, _sz, _sz, ctypes.c_int, _ip, ctypes.c_int,
                                               _dp, _sz, ctypes.c_void_p]),

@@ -725,10 +725,20 @@ ozk_status ozk_ozaki_gemm(ozk_format fmt, size_t m, size_t l, size_t n, const vo
         }
     } drain{&hs, {xs.s, ys.s, os.s}};
     if (a_pg || b_pg || c_pg) {
+        // host copy threads per direction: half the usable CPUs each (at most
+        // 8), or $OZK_STAGING_THREADS = "h2d[,d2h]"
         int cpus = (int)std::thread::hardware_concurrency();
         cpu_set_t set;
         if (sched_getaffinity(0, sizeof(set), &set) == 0) cpus = CPU_COUNT(&set);
-        hs = std::make_unique<HostStaging>(xs.s, ys.s, std::max(1, std::min(8, cpus / 2)));
+        int th = std::max(1, std::min(8, cpus / 2)), th2 = th;
+        if (const char* v = std::getenv("OZK_STAGING_THREADS")) {
+            const int x = std::atoi(v);
+            const char* comma = std::strchr(v, ',');
+            const int y = comma ? std::atoi(comma + 1) : x;
+            if (x > 0) th = x;
+            if (y > 0) th2 = y;
+        }
+        hs = std::make_unique<HostStaging>(xs.s, ys.s, th, th2);
     }
     std::map<cudaEvent_t, int> staged_job;  // H2D event -> staging job number
     OZK_CUDA(da.alloc(eb * m * l, os.s), "ozaki_gemm: A");
@@ -1306,6 +1316,31 @@ ozk_status ozk_ozaki_gemm_multi(ozk_format fmt, int ngpus, const int* devices, s
     // worker 0 runs on the caller's thread: its current device is restored after
     int caller_dev = 0;
     OZK_CUDA(cudaGetDevice(&caller_dev), "ozaki_gemm_multi: device");
+    // Direct peer access between every pair of distinct devices, so the
+    // digit-plane all-gather (cudaMemcpyPeerAsync) runs device to device over
+    // NVLink / NVSwitch instead of being staged through host memory.
+    {
+        std::vector<int> ids;
+        for (int r = 0; r < ngpus; ++r)
+            if (std::find(ids.begin(), ids.end(), dev_of(r)) == ids.end()) ids.push_back(dev_of(r));
+        for (int i : ids)
+            for (int j : ids) {
+                if (i == j) continue;
+                int can = 0;
+                if (cudaDeviceCanAccessPeer(&can, i, j) != cudaSuccess || !can) {
+                    (void)cudaGetLastError();
+                    continue;
+                }
+                OZK_CUDA(cudaSetDevice(i), "ozaki_gemm_multi: device");
+                const cudaError_t e = cudaDeviceEnablePeerAccess(j, 0);
+                if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) {
+                    cudaSetDevice(caller_dev);
+                    return cuda_fail(e, "ozaki_gemm_multi: peer access");
+                }
+                (void)cudaGetLastError();  // clear "already enabled"
+            }
+        OZK_CUDA(cudaSetDevice(caller_dev), "ozaki_gemm_multi: device");
+    }
     std::vector<std::thread> threads;
     for (int r = 1; r < ngpus; ++r) threads.emplace_back(worker, r);
     worker(0);
@@ -1361,10 +1396,10 @@ int ozk_int8_digits(ozk_format fmt, size_t inner_dim, int d) {
     return int8_digits(fmt, inner_dim, d);
 }
 
-ozk_status ozk_split_digits_device(ozk_format fmt, size_t rows, size_t cols, size_t ld,
-                                   const void* mat, int d, ozk_side side, int8_t* digits,
-                                   size_t ld8, size_t plane_rows, int* exps, double* piece_max,
-                                   void* stream) {
+ozk_status ozk_split_digits_device_async(ozk_format fmt, size_t rows, size_t cols, size_t ld,
+                                         const void* mat, int d, ozk_side side, int8_t* digits,
+                                         size_t ld8, size_t plane_rows, int* exps,
+                                         double* piece_max, int* dev_flag, void* stream) {
     if (!valid_fmt(fmt)) return fail(OZK_EPARAM, "split_digits: format must be DD, TD, QD or TS");
     if (rows == 0 || cols == 0) return fail(OZK_ESHAPE, "matrix dimensions must be positive");
     if (d < 1) return fail(OZK_EPARAM, "split_matrix: split count must be >= 1");
@@ -1376,7 +1411,7 @@ ozk_status ozk_split_digits_device(ozk_format fmt, size_t rows, size_t cols, siz
     if (nd == 0) return fail(OZK_EPARAM, "split_digits: INT8 engine not applicable to this inner dimension");
     if (ld8 < inner || ld8 % 16) return fail(OZK_ESHAPE, "split_digits: ld8 must be >= inner and a multiple of 16");
     if (plane_rows < outer) return fail(OZK_ESHAPE, "split_digits: plane_rows < outer dimension");
-    if (!digits || !exps) return fail(OZK_EPARAM, "split_digits: null output");
+    if (!digits || !exps || !dev_flag) return fail(OZK_EPARAM, "split_digits: null output");
     cudaStream_t st = (cudaStream_t)stream;
     num_sms_cached();
     DigitOut dig;
@@ -1387,26 +1422,44 @@ ozk_status ozk_split_digits_device(ozk_format fmt, size_t rows, size_t cols, siz
     dig.slice_stride = (size_t)nd * plane_rows * ld8;
     dig.exps = exps;
     dig.exp_stride = plane_rows;
-    DevBuf work, flags;
+    DevBuf work;  // stream-ordered: freed after the split on `stream`
     OZK_CUDA(work.alloc(elem_bytes(fmt) * rows * cols, st), "split_digits: work");
-    OZK_CUDA(flags.alloc(8, st), "split_digits: flags");
-    OZK_CUDA(cudaMemsetAsync(flags.p, 0, 8, st), "split_digits: memset");
     OZK_CUDA(split_to_slices(fmt, rows, cols, ld, mat, d, side, nullptr, plane_rows, work.p,
-                             reinterpret_cast<unsigned long long*>(piece_max), flags.as<int>(), st,
-                             dig),
+                             reinterpret_cast<unsigned long long*>(piece_max), dev_flag, st, dig),
              "split_digits");
+    return OZK_OK;
+}
+
+ozk_status ozk_check_split_flag(const int* dev_flag, void* stream) {
     int flag = 0;
-    OZK_CUDA(cudaMemcpyAsync(&flag, flags.p, sizeof(int), cudaMemcpyDeviceToHost, st),
-             "split_digits: flag");
-    OZK_CUDA(cudaStreamSynchronize(st), "split_digits");
+    cudaStream_t st = (cudaStream_t)stream;
+    OZK_CUDA(cudaMemcpyAsync(&flag, dev_flag, sizeof(int), cudaMemcpyDeviceToHost, st),
+             "split flag");
+    OZK_CUDA(cudaStreamSynchronize(st), "split flag");
     return check_dev_err(flag, "split_matrix");
 }
 
-ozk_status ozk_digits_gemm_device(ozk_format fmt, size_t m, size_t l, size_t n,
-                                  const int8_t* a_digits, const int* a_exps, size_t a_plane_rows,
-                                  const int8_t* b_digits, const int* b_exps, size_t b_plane_rows,
-                                  size_t ld8, int d, const int* pairs, int npairs, void* c,
-                                  size_t ldc, void* stream) {
+ozk_status ozk_split_digits_device(ozk_format fmt, size_t rows, size_t cols, size_t ld,
+                                   const void* mat, int d, ozk_side side, int8_t* digits,
+                                   size_t ld8, size_t plane_rows, int* exps, double* piece_max,
+                                   void* stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    DevBuf flags;
+    OZK_CUDA(flags.alloc(8, st), "split_digits: flags");
+    OZK_CUDA(cudaMemsetAsync(flags.p, 0, 8, st), "split_digits: memset");
+    if (ozk_status s = ozk_split_digits_device_async(fmt, rows, cols, ld, mat, d, side, digits,
+                                                     ld8, plane_rows, exps, piece_max,
+                                                     flags.as<int>(), stream))
+        return s;
+    return ozk_check_split_flag(flags.as<int>(), stream);
+}
+
+ozk_status ozk_digits_gemm_device_async(ozk_format fmt, size_t m, size_t l, size_t n,
+                                        const int8_t* a_digits, const int* a_exps,
+                                        size_t a_plane_rows, const int8_t* b_digits,
+                                        const int* b_exps, size_t b_plane_rows, size_t ld8, int d,
+                                        const int* pairs, int npairs, void* c, size_t ldc,
+                                        void* stream) {
     if (!valid_fmt(fmt)) return fail(OZK_EPARAM, "digits_gemm: format must be DD, TD, QD or TS");
     if (m == 0 || l == 0 || n == 0) return fail(OZK_ESHAPE, "matrix dimensions must be positive");
     if (d < 1 || d > kMaxSplits) return fail(OZK_EPARAM, "digits_gemm: bad split count");
@@ -1446,7 +1499,19 @@ ozk_status ozk_digits_gemm_device(ozk_format fmt, size_t m, size_t l, size_t n,
                                      num_sms_cached()),
                  "digits_gemm");
     }
-    OZK_CUDA(cudaStreamSynchronize(st), "digits_gemm");
+    return OZK_OK;
+}
+
+ozk_status ozk_digits_gemm_device(ozk_format fmt, size_t m, size_t l, size_t n,
+                                  const int8_t* a_digits, const int* a_exps, size_t a_plane_rows,
+                                  const int8_t* b_digits, const int* b_exps, size_t b_plane_rows,
+                                  size_t ld8, int d, const int* pairs, int npairs, void* c,
+                                  size_t ldc, void* stream) {
+    if (ozk_status s = ozk_digits_gemm_device_async(fmt, m, l, n, a_digits, a_exps, a_plane_rows,
+                                                    b_digits, b_exps, b_plane_rows, ld8, d, pairs,
+                                                    npairs, c, ldc, stream))
+        return s;
+    OZK_CUDA(cudaStreamSynchronize((cudaStream_t)stream), "digits_gemm");
     return OZK_OK;
 }
 

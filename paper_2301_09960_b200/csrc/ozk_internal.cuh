@@ -197,7 +197,7 @@ struct StagedCopy {
 // both queues (every D2H job is then in the caller's buffer).
 class HostStaging {
 public:
-    HostStaging(cudaStream_t h2d, cudaStream_t d2h, int threads);
+    HostStaging(cudaStream_t h2d, cudaStream_t d2h, int h2d_threads, int d2h_threads);
     ~HostStaging();
     int push_h2d(const StagedCopy& c);
     void push_d2h(const StagedCopy& c);

@@ -40,7 +40,7 @@ bool host_is_pinned(const void* p) {
 
 namespace {
 
-constexpr int kSlots = 4;                    // per direction
+constexpr int kSlots = 6;                    // per direction
 constexpr size_t kSlotBytes = size_t(32) << 20;
 
 // A set of pinned slots for both directions, reused across calls.
@@ -168,9 +168,9 @@ struct HostStaging::Impl {
     int slot_next[2] = {0, 0};
     bool slot_used[2][kSlots] = {};
 
-    Impl(cudaStream_t h2d, cudaStream_t d2h, int threads)
-        : h2d_stream(h2d), d2h_stream(d2h), slots(acquire_slots()), h2d_team(threads),
-          d2h_team(threads > 2 ? threads / 2 : 1) {
+    Impl(cudaStream_t h2d, cudaStream_t d2h, int h2d_threads, int d2h_threads)
+        : h2d_stream(h2d), d2h_stream(d2h), slots(acquire_slots()), h2d_team(h2d_threads),
+          d2h_team(d2h_threads) {
         if (!slots) err = cudaErrorMemoryAllocation;
         for (int d = 0; d < 2; ++d) worker[d] = std::thread([this, d] { run(d); });
     }
@@ -282,8 +282,8 @@ struct HostStaging::Impl {
     }
 };
 
-HostStaging::HostStaging(cudaStream_t h2d, cudaStream_t d2h, int threads)
-    : impl_(new Impl(h2d, d2h, threads)) {}
+HostStaging::HostStaging(cudaStream_t h2d, cudaStream_t d2h, int h2d_threads, int d2h_threads)
+    : impl_(new Impl(h2d, d2h, h2d_threads, d2h_threads)) {}
 
 HostStaging::~HostStaging() {
     finish();

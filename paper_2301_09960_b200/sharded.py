@@ -19,9 +19,13 @@ Rank r of W owns C rows [r0, r1) and B columns [c0, c1):
 Two slice representations, bit-identical results:
 * INT8 engine (default where it applies, ozk_int8_digits > 0): the splits write
   nd int8 digit planes + one grid exponent per row/column
-  (ozk_split_digits_device), the all-gather moves D*nd*l*ceil(n/W) bytes per
-  rank (2.7x less than FP64 slices), the gathered planes are permuted once to
-  [D][nd][W*ncb][ld8] and ozk_digits_gemm_device runs the pairs on tcgen05;
+  (ozk_split_digits_device_async), the all-gather moves D*nd*l*ceil(n/W)
+  bytes per rank (2.7x less than FP64 slices), one collective per digit plane
+  straight into the [D][nd][W*ncb][ld8] operand layout (each plane's rank
+  blocks are contiguous rows, so no re-layout copy), and
+  ozk_digits_gemm_device_async runs the pairs on tcgen05.  Nothing in the
+  device path synchronises the stream; the split's data-error flags are
+  checked once at the end of run();
 * DMMA engine: FP64 slices (ozk_split_slices_device / ozk_slices_gemm_device).
 
 The gathered B slices stay in the layout the all-gather produces
@@ -101,6 +105,18 @@ class GpuOps:
         from ._lib import lib
         self.lib = lib
         self.device = torch.device("cuda", torch.cuda.current_device())
+        # split data-error flags (A rows, B columns) of the asynchronous entries
+        self.flags = torch.zeros(2, dtype=torch.int32, device=self.device)
+
+    def reset_flags(self):
+        self.flags.zero_()
+
+    def check_flags(self):
+        """Non-finite / too-large entries found by the splits (A first, as
+        split_matrix(a) runs before split_matrix(b)); synchronises the stream."""
+        for i in (0, 1):
+            self._check(self.lib.ozk_check_split_flag(self.flags.data_ptr() + 4 * i,
+                                                      self._stream()))
 
     def _check(self, st):
         if st != 0:
@@ -140,30 +156,31 @@ class GpuOps:
                 torch.zeros((d, rows), dtype=torch.int32, device=self.device))
 
     def split_digits(self, K, mat, rows, cols, ld, d, side, digits, exps, pmax):
-        self._check(self.lib.ozk_split_digits_device(
+        self._check(self.lib.ozk_split_digits_device_async(
             K, rows, cols, ld, mat.data_ptr(), d, side, digits.data_ptr(), digits.shape[3],
             digits.shape[2], exps.data_ptr(), pmax.data_ptr() if pmax is not None else None,
-            self._stream()))
+            self.flags.data_ptr() + 4 * side, self._stream()))
 
     def split_digit_rows(self, K, mat, rows, cols, ld, d, side, digits, r0, exps):
         """split_digits into rows [r0, r0 + rows) of full-height digit planes."""
         ld8, plane_rows = digits.shape[3], digits.shape[2]
-        self._check(self.lib.ozk_split_digits_device(
+        self._check(self.lib.ozk_split_digits_device_async(
             K, rows, cols, ld, mat.data_ptr(), d, side, digits.data_ptr() + r0 * ld8, ld8,
-            plane_rows, exps.data_ptr() + 4 * r0, None, self._stream()))
+            plane_rows, exps.data_ptr() + 4 * r0, None, self.flags.data_ptr() + 4 * side,
+            self._stream()))
 
     def gemm_digit_rows(self, plan: ShardPlan, r0, rows, a8, ga, b8, gb, pairs, c):
         """gemm_digits for C rows [r0, r0 + rows) of this rank (c: all its rows)."""
         flat = (ctypes.c_int * (2 * len(pairs)))(*[v for p in pairs for v in p])
         ld8, esz = a8.shape[3], c.element_size() * c.shape[2]
-        self._check(self.lib.ozk_digits_gemm_device(
+        self._check(self.lib.ozk_digits_gemm_device_async(
             plan.K, rows, plan.l, plan.n, a8.data_ptr() + r0 * ld8, ga.data_ptr() + 4 * r0,
             a8.shape[2], b8.data_ptr(), gb.data_ptr(), b8.shape[2], ld8, plan.d, flat, len(pairs),
             c.data_ptr() + r0 * plan.n * esz, plan.n, self._stream()))
 
     def gemm_digits(self, plan: ShardPlan, a8, ga, b8, gb, pairs, c):
         flat = (ctypes.c_int * (2 * len(pairs)))(*[v for p in pairs for v in p])
-        self._check(self.lib.ozk_digits_gemm_device(
+        self._check(self.lib.ozk_digits_gemm_device_async(
             plan.K, plan.rows_local, plan.l, plan.n, a8.data_ptr(), ga.data_ptr(), a8.shape[2],
             b8.data_ptr(), gb.data_ptr(), b8.shape[2], a8.shape[3], plan.d, flat, len(pairs),
             c.data_ptr(), plan.n, self._stream()))
@@ -184,9 +201,9 @@ class ShardedOzaki:
             nd, ld8 = layout
             self.a8, self.ga = self.ops.digit_planes(d, nd, max(p.rows_local, 1), ld8)
             self.b8, self.gb = self.ops.digit_planes(d, nd, p.ncb, ld8)
-            self.b8_all, self.gb_all = self.ops.digit_planes(world * d, nd, p.ncb, ld8)
-            self.b8_all = self.b8_all.view(world, d, nd, p.ncb, ld8)
-            self.gb_all = self.gb_all.view(world, d, p.ncb)
+            # the GEMM operand layout [D][nd][W*ncb][ld8] / [D][W*ncb], filled
+            # by one all-gather per plane (rank r's block = rows r*ncb..)
+            self.b8_cat, self.gb_cat = self.ops.digit_planes(d, nd, world * p.ncb, ld8)
         else:
             self.sa = self.ops.zeros((d, max(p.rows_local, 1), p.ld))
             self.sb = self.ops.zeros((d, p.ncb, p.ld))
@@ -202,24 +219,35 @@ class ShardedOzaki:
         return self.plan.rows_local
 
     def _gather(self, out, local):
+        """out: world blocks of local's shape, back to back (dim 0 of out is
+        world * local.shape[0] rows, or world when out has one more dim)."""
         if dist.get_backend(self.group) == "nccl":
             dist.all_gather_into_tensor(out, local, group=self.group)
         else:
-            parts = list(out.unbind(0))
+            parts = list(out.reshape(self.plan.world, *local.shape).unbind(0))
             dist.all_gather(parts, local, group=self.group)
 
     def _all_gather(self):
         if self.engine == "int8":
-            # [W][D][nd][ncb][ld8] -> one plane set [D][nd][W*ncb][ld8]: column j
-            # of the gathered B is row j of every plane (the ceil partition puts
-            # rank r's columns at r*ncb), exponents likewise [D][W*ncb]
-            self._gather(self.b8_all, self.b8)
-            self._gather(self.gb_all, self.gb)
-            p = self.plan
-            w, d, nd, ncb, ld8 = self.b8_all.shape
-            self.b8_cat = self.b8_all.permute(1, 2, 0, 3, 4).reshape(d, nd, w * ncb, ld8)
-            self.gb_cat = self.gb_all.permute(1, 0, 2).reshape(d, w * ncb)
-            assert w * ncb >= p.n
+            # one collective per digit plane and per exponent row: column j of
+            # the gathered B is row j of every plane (the ceil partition puts
+            # rank r's columns at r*ncb), so the planes land in the GEMM's
+            # operand layout with no re-layout copy.  The D*nd + D calls are
+            # coalesced into one NCCL group where torch offers it.
+            d, nd = self.b8.shape[0], self.b8.shape[1]
+
+            def planes():
+                for s in range(d):
+                    for t in range(nd):
+                        self._gather(self.b8_cat[s, t], self.b8[s, t])
+                    self._gather(self.gb_cat[s], self.gb[s])
+
+            cm = getattr(dist, "_coalescing_manager", None)
+            if cm is not None and dist.get_backend(self.group) == "nccl":
+                with cm(group=self.group, device=self.b8.device):
+                    planes()
+            else:
+                planes()
         else:
             self._gather(self.sb_all, self.sb)
 
@@ -251,6 +279,7 @@ class ShardedOzaki:
                 db=torch.empty((p.l, max(p.c1 - p.c0, 1), p.words), dtype=hA.dtype, device=dev))
         h = self._host
         xs, ys, da, db = h["xs"], h["ys"], h["da"], h["db"]
+        ops.reset_flags()
         nb = max(1, min(bands, p.rows_local // 256))
         bounds = [p.rows_local * q // nb for q in range(nb + 1)]
         xs.wait_stream(cur)
@@ -294,6 +323,7 @@ class ShardedOzaki:
                 hC[r0:r1].copy_(self.c[r0:r1], non_blocking=True)
         cur.wait_stream(ys)
         cur.wait_stream(xs)
+        ops.check_flags()
 
     def run(self, A, B, prof=None):
         """A: (m, l, K) or this rank's rows; B: (l, n, K) full (row stride n).
@@ -303,6 +333,8 @@ class ShardedOzaki:
             ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
             ev[0].record()
         a_rows = A[p.r0:p.r1] if A.shape[0] == p.m else A
+        if hasattr(ops, "reset_flags"):
+            ops.reset_flags()
         if self.pmax is not None:
             self.pmax.zero_()
         amax = self.pmax[0] if self.pmax is not None else None
@@ -336,6 +368,8 @@ class ShardedOzaki:
         if self.timing:
             ev[1].record()
         if self.pmax is not None:
+            if hasattr(ops, "check_flags"):
+                ops.check_flags()  # the maxima are only meaningful for finite inputs
             dist.all_reduce(self.pmax, op=dist.ReduceOp.MAX, group=self.group)
             mx = self.pmax.cpu().tolist()
             pairs = pruned_pairs(p.d, mx[0], mx[1], self.drop)
@@ -352,6 +386,8 @@ class ShardedOzaki:
                 ops.gemm_digits(p, self.a8, self.ga, self.b8_cat, self.gb_cat, pairs, self.c)
             else:
                 ops.gemm(p, self.sa, self.sb_all, pairs, self.c)
+        if hasattr(ops, "check_flags"):
+            ops.check_flags()  # synchronises the stream
         if self.timing:
             ev[3].record()
             torch.cuda.current_stream().synchronize()

@@ -318,10 +318,11 @@ def test_sharded_layout_single_gpu(ozk, cpu, K, m, l, n, d, world):
                                              (4, 64, 700, 130, 12, 4), (2, 50, 4100, 70, 7, 8)])
 def test_sharded_digits_single_gpu(ozk, cpu, K, m, l, n, d, world):
     """The sharded INT8-engine data path on one GPU: each emulated rank splits
-    its B column block in place into digit planes [D][nd][ncb][ld8] + exponents,
-    the gathered [W][D][nd][ncb] planes are permuted to [D][nd][W*ncb] exactly
-    as ShardedOzaki does after the all-gather, and every rank's digit-plane GEMM
-    gives the reference's C rows bit for bit."""
+    its B column block in place into digit planes [D][nd][ncb][ld8] + exponents
+    (asynchronous entry points, data-error flags checked at the end), the
+    per-plane all-gathers place rank r's block at rows r*ncb of every
+    [D][nd][W*ncb][ld8] plane exactly as ShardedOzaki's do, and every rank's
+    digit-plane GEMM gives the reference's C rows bit for bit."""
     import torch
 
     from paper_2301_09960_b200.sharded import GpuOps, ShardPlan, triangular_pairs
@@ -331,25 +332,27 @@ def test_sharded_digits_single_gpu(ozk, cpu, K, m, l, n, d, world):
     A = torch.from_numpy(a).cuda()
     B = torch.from_numpy(b).cuda()
     ops = GpuOps()
+    ops.reset_flags()
     nd, ld8 = ops.int8_layout(K, l, d)
     assert nd == 3
     plans = [ShardPlan(K, m, l, n, d, r, world) for r in range(world)]
     ncb = plans[0].ncb
-    b8_all, gb_all = ops.digit_planes(world * d, nd, ncb, ld8)
-    b8_all = b8_all.view(world, d, nd, ncb, ld8)
-    gb_all = gb_all.view(world, d, ncb)
+    b8, gb = ops.digit_planes(d, nd, world * ncb, ld8)
     for p in plans:
         if p.c1 > p.c0:
-            ops.split_digits(K, B[:, p.c0:p.c1], l, p.c1 - p.c0, n, d, 1, b8_all[p.rank],
-                             gb_all[p.rank], None)
-    b8 = b8_all.permute(1, 2, 0, 3, 4).reshape(d, nd, world * ncb, ld8)
-    gb = gb_all.permute(1, 0, 2).reshape(d, world * ncb)
+            loc8, locg = ops.digit_planes(d, nd, ncb, ld8)
+            ops.split_digits(K, B[:, p.c0:p.c1], l, p.c1 - p.c0, n, d, 1, loc8, locg, None)
+            for s_ in range(d):  # what the per-plane all-gathers deliver
+                for t in range(nd):
+                    b8[s_, t, p.rank * ncb:(p.rank + 1) * ncb] = loc8[s_, t]
+                gb[s_, p.rank * ncb:(p.rank + 1) * ncb] = locg[s_]
     pairs = triangular_pairs(d)
     for p in plans:
         a8, ga = ops.digit_planes(d, nd, p.rows_local, ld8)
         ops.split_digits(K, A[p.r0:p.r1], p.rows_local, l, l, d, 0, a8, ga, None)
         c = ops.zeros((p.rows_local, n, K))
         ops.gemm_digits(p, a8, ga, b8, gb, pairs, c)
+        ops.check_flags()
         assert_bitwise(c.cpu().numpy(), want[p.r0:p.r1], f"rank {p.rank} rows")
 
 

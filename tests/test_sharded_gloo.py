@@ -49,8 +49,8 @@ class OracleOps:
 
 
 class OracleDigitOps(OracleOps):
-    """The INT8-engine data path of ShardedOzaki (digit-plane buffers, exponent
-    gather, the [W][D][nd][ncb] -> [D][nd][W*ncb] permute, plane strides) with
+    """The INT8-engine data path of ShardedOzaki (digit-plane buffers, the
+    per-plane gathers into the [D][nd][W*ncb] operand layout, plane strides) with
     the oracle's binary64 slices standing in for the digit planes (nd = 1,
     float64 "digits") -- the layout logic is shape-generic; the digit encoding
     itself is checked on the GPU (tests/test_gpu_parity.py)."""
@@ -108,7 +108,7 @@ def _free_port():
 
 
 @pytest.mark.parametrize("digits", [False, True], ids=["fp64-slices", "digit-planes"])
-@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("world", [2, 3, 8])
 def test_sharded_matches_single_process(world, digits):
     cases = [(2, 10, 12, 9, 4, 0.0), (3, 7, 9, 11, 5, 0.0), (2, 13, 16, 14, 5, 2.0 ** -60),
              (4, 5, 6, 4, 6, 0.0)]
