@@ -725,12 +725,15 @@ ozk_status ozk_ozaki_gemm(ozk_format fmt, size_t m, size_t l, size_t n, const vo
         }
     } drain{&hs, {xs.s, ys.s, os.s}};
     if (a_pg || b_pg || c_pg) {
-        // host copy threads per direction: half the usable CPUs each (at most
-        // 8), or $OZK_STAGING_THREADS = "h2d[,d2h]"
+        // host copy threads: H2D one per usable CPU (at most 16), D2H half as
+        // many (the copies are memory-bound, so the two teams may oversubscribe
+        // the cores; B200 host, 16 CPUs: 16 + 8 gave 219 ms for TD n=8192 vs
+        // 225 (8 + 8), 239 (8 + 4), 205 pinned, 540 unstaged --
+        // tools/staging_sweep.py), or $OZK_STAGING_THREADS = "h2d[,d2h]"
         int cpus = (int)std::thread::hardware_concurrency();
         cpu_set_t set;
         if (sched_getaffinity(0, sizeof(set), &set) == 0) cpus = CPU_COUNT(&set);
-        int th = std::max(1, std::min(8, cpus / 2)), th2 = th;
+        int th = std::max(1, std::min(16, cpus)), th2 = std::max(1, std::min(8, cpus / 2));
         if (const char* v = std::getenv("OZK_STAGING_THREADS")) {
             const int x = std::atoi(v);
             const char* comma = std::strchr(v, ',');
