@@ -498,26 +498,32 @@ def run_ours(args):
         traffic_src = tj["source"]
     if engine_used == "int8":
         kern_work = nd * nd * fp64_work  # nd^2 int8 digit GEMMs per slice pair
+        achieved = kern_work / t_kern / 1e12
+        # Denominator (B200_PROFILING.md): the driver-measured MEASURED_PEAKS.json
+        # figure, sustained variant for a kernel timed inside a long step.  It has
+        # bf16 only; B200 dense INT8 = 2 x dense bf16 (4.5 POPS vs 2.25 PF), so
+        # the INT8 ceiling is 2 x bf16_tflops_sustained ("of measured").  The
+        # in-run kind::i8 probe (no operand traffic, not power-capped: a burst
+        # figure near nominal) is reported beside it.
+        pk = os.path.join(os.path.dirname(os.path.abspath(__file__)), "MEASURED_PEAKS.json")
+        bf16_sus = json.load(open(pk)).get("bf16_tflops_sustained") if os.path.exists(pk) else None
+        peak = 2.0 * bf16_sus if bf16_sus else peak_i8
         roof = {"bound": "tensor", "kernel": "pair_gemm_i8_kernel (tcgen05.mma kind::i8 + K-word "
-                "epilogue)", "achieved": round(kern_work / t_kern / 1e12, 2),
-                "peak": round(peak_i8, 2), "unit": "TFLOP/s",
-                "frac": round(kern_work / t_kern / 1e12 / peak_i8, 4), "traffic": traffic,
+                "epilogue)", "achieved": round(achieved, 2),
+                "peak": round(peak, 2), "unit": "TFLOP/s", "frac": round(achieved / peak, 4),
+                "traffic": traffic,
                 "traffic_unit": "DRAM bytes per launch", "traffic_source": traffic_src,
                 "work_per_launch": f"{nd*nd}*P*2*m*n*l = {kern_work:.4g} int8 tensor ops "
                                    "(counted like flops: 2 per multiply-add)",
-                "peak_source": "dense INT8 tcgen05 ceiling measured in this run "
-                               "(ozk_probe_i8_tops: M=128 N=256 kind::i8 MMAs from smem, one "
-                               "CTA per SM); nominal B200 dense INT8 4.5 POPS"}
-        # driver-measured anchor: MEASURED_PEAKS.json has bf16 cuBLAS only; B200
-        # dense INT8 is 2x dense bf16, so 2x its sustained (power-capped) figure
-        pk = os.path.join(os.path.dirname(os.path.abspath(__file__)), "MEASURED_PEAKS.json")
-        if os.path.exists(pk):
-            bf16_sus = json.load(open(pk)).get("bf16_tflops_sustained")
-            if bf16_sus:
-                roof["frac_vs_2x_bf16_sustained"] = round(
-                    kern_work / t_kern / 1e12 / (2.0 * bf16_sus), 4)
-                roof["bf16_sustained_source"] = ("MEASURED_PEAKS.json bf16_tflops_sustained = "
-                                                 f"{bf16_sus} (torch.matmul, back to back 4 s)")
+                "peak_source": ("of measured: 2 x MEASURED_PEAKS.json bf16_tflops_sustained = "
+                                f"2 x {bf16_sus} (B200 dense INT8 = 2 x dense bf16; sustained: "
+                                "the kernel runs inside back-to-back steps at the 1 kW cap)")
+                if bf16_sus else "in-run kind::i8 probe (MEASURED_PEAKS.json absent)",
+                "in_run_i8_probe_tops": round(peak_i8, 2),
+                "frac_of_in_run_i8_probe": round(achieved / peak_i8, 4),
+                "in_run_i8_probe_source": "ozk_probe_i8_tops: M=128 N=256 kind::i8 MMAs from "
+                                          "resident smem, one CTA per SM, no operand traffic "
+                                          "(burst, not power-capped); nominal dense INT8 4.5 POPS"}
     else:
         roof = {"bound": "tensor", "kernel": "pair_gemm_kernel (DMMA + K-word epilogue)",
                 "achieved": round(fp64_work / t_kern / 1e12, 3), "peak": round(peak_fp64, 3),

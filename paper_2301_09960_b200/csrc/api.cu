@@ -109,12 +109,24 @@ int num_sms_cached() {
 }
 
 // Stream-ordered device scratch, freed on scope exit.
+// $OZK_POISON_SCRATCH=1 fills every scratch allocation with 0xFF bytes (NaN
+// words, -1 digits and exponents) before use: a kernel that reads scratch it
+// never wrote then corrupts the result, which the parity tests catch
+// (tests/test_gpu_parity.py::test_poisoned_scratch_bitexact; compute-sanitizer
+// is closed on this GPU pool, so this stands in for its initcheck).
+bool poison_scratch() {
+    const char* v = std::getenv("OZK_POISON_SCRATCH");
+    return v && v[0] == '1';
+}
+
 struct DevBuf {
     void* p = nullptr;
     cudaStream_t st = nullptr;
     cudaError_t alloc(size_t bytes, cudaStream_t s) {
         st = s;
-        return cudaMallocAsync(&p, bytes ? bytes : 16, s);
+        cudaError_t e = cudaMallocAsync(&p, bytes ? bytes : 16, s);
+        if (e == cudaSuccess && poison_scratch()) e = cudaMemsetAsync(p, 0xFF, bytes ? bytes : 16, s);
+        return e;
     }
     template <class T>
     T* as() const {

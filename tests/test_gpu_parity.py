@@ -857,3 +857,39 @@ def test_error_precedence_matches_reference(ozk, cpu):
         ozk.ozaki_gemm(huge, nan_b, 4)
     with pytest.raises(ozk.param_error, match="non-finite"):
         ozk.ozaki_gemm(a, nan_b, 4)
+
+
+@pytest.mark.parametrize("K,m,l,n,d", [(2, 300, 600, 390, 6), (3, 129, 1030, 256, 9),
+                                       (4, 97, 700, 130, 12), (3, 70, 96, 80, 6),
+                                       (2, 2049, 600, 4200, 4)])
+def test_poisoned_scratch_bitexact(ozk, cpu, monkeypatch, K, m, l, n, d):
+    """Every scratch allocation filled with 0xFF (NaN words, -1 digits and
+    exponents, OZK_POISON_SCRATCH=1) and the outputs pre-filled with NaN: a
+    kernel reading scratch or padding it never wrote, or leaving part of C
+    unwritten, changes the result.  Device and host (banded, staged) paths,
+    both engines.  (compute-sanitizer is closed on this GPU pool; this is the
+    stand-in for its initcheck.)"""
+    import torch
+    monkeypatch.setenv("OZK_POISON_SCRATCH", "1")
+    a = cpu.gen_eq1(K, m, l, 800 + m)
+    b = cpu.gen_eq1(K, l, n, 801 + m)
+    want = cpu.ozaki_gemm(K, a, b, d)
+    sh = torch.cuda.current_stream().cuda_stream
+    for engine in ("auto", "dmma"):
+        ozk.set_engine(engine)
+        try:
+            A, B = torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()
+            C = torch.full((m, n, K), float("nan"), dtype=torch.float64, device="cuda")
+            assert ozk.lib.ozk_ozaki_gemm_device(K, m, l, n, A.data_ptr(), B.data_ptr(), d, 0.0,
+                                                 C.data_ptr(), sh, None) == 0
+            assert_bitwise(C.cpu().numpy(), want, f"device path, poisoned, {engine}")
+            c = np.full((m, n, K), np.nan)
+            assert ozk.lib.ozk_ozaki_gemm(K, m, l, n, a.ctypes.data, b.ctypes.data, d, 0.0,
+                                          c.ctypes.data, None) == 0
+            assert_bitwise(c, want, f"host path, poisoned, {engine}")
+        finally:
+            ozk.set_engine("auto")
+    s = ozk.split_matrix(a, d, ozk.SplitSide.cols)
+    want_p, want_r = cpu.split(K, a, d, 1)
+    assert_bitwise(np.stack(s.pieces), want_p, "split pieces, poisoned")
+    assert_bitwise(s.residual, want_r, "split residual, poisoned")

@@ -23,10 +23,17 @@ def main():
                         obj], check=True)
         return obj
 
+    def compile_host(src):
+        obj = os.path.join(outdir, f"{name}.{src}.o")
+        subprocess.run(["g++", "-std=c++20", "-O2", "-ffp-contract=off", "-fPIC", "-pthread",
+                        "-Wno-unknown-pragmas", f"-I{os.path.join(ROOT, 'include')}", "-c",
+                        os.path.join(b.CSRC, src), "-o", obj], check=True)
+        return obj
+
     with ThreadPoolExecutor(8) as ex:
-        objs = list(ex.map(compile_one, b.SOURCES))
-    subprocess.run([b.NVCC, *b.ARCH, "-shared", "-cudart", "static", "-ccbin", "g++", "-o", out,
-                    *objs], check=True)
+        objs = list(ex.map(compile_one, b.SOURCES)) + list(ex.map(compile_host, b.HOST_SOURCES))
+    subprocess.run([b.NVCC, *b.ARCH, "-shared", "-cudart", "static", "-ccbin", "g++",
+                    "-Xcompiler", "-pthread", "-o", out, *objs], check=True)
     for o in objs:
         os.remove(o)
     print(out)

@@ -19,11 +19,12 @@ libs = [(p, load(p)) for p in args]
 for fmt, d in fmts:
     K = 3 if fmt == 0x103 else fmt
     dt = torch.float32 if fmt == 0x103 else torch.float64
-    A = torch.empty((n, n, K), dtype=dt, device="cuda")
+    A = torch.empty((n, n, K), dtype=dt)
     B = torch.empty_like(A)
+    libs[0][1].ozk_gen_eq1(fmt, n, n, 1, A.data_ptr(), 0)  # the reference's inputs
+    libs[0][1].ozk_gen_eq1(fmt, n, n, 2, B.data_ptr(), 0)
+    A, B = A.cuda(), B.cuda()
     C = torch.empty_like(A)
-    libs[0][1].ozk_gen_eq1_device(fmt, n, n, 1, A.data_ptr(), sh)
-    libs[0][1].ozk_gen_eq1_device(fmt, n, n, 2, B.data_ptr(), sh)
     ref = None
     for path, lib in libs:
         lib.ozk_set_engine(2)
