@@ -100,23 +100,28 @@ __device__ __forceinline__ void store_kw(T* p, const T* c) {
 // T is the word type of the K-word input/residual (double: DD/TD/QD, float:
 // TS); slices are always written as binary64 (a TS slice is a binary32 value,
 // exactly representable), which is the DMMA GEMM's operand type.
-template <int K, typename T>
-// No minimum-blocks hint by default: ptxas then keeps 50-64 registers (two
-// CTAs per SM).  An explicit hint of 1 lets it take ~88 and costs ~3 ms per TD
+//
+// NT threads per CTA (one row per CTA).  SM: the K-word residual row lives in
+// shared memory across the D passes (rows up to ~220 KB: TD/DD/TS at l = 8192,
+// not QD) -- one 1024-thread CTA per SM, and the per-pass residual sweeps
+// become shared-memory traffic instead of L2/DRAM round trips (the global
+// variant, two 512-thread CTAs per SM, wrote ~6 GB of evicted residual lines
+// to DRAM per TD n=8192 side).  Otherwise the residual row is `work`.
+// No minimum-blocks hint: ptxas then keeps <= 64 registers (two 512-thread
+// CTAs per SM); an explicit hint of 1 lets it take ~88 and costs ~3 ms per TD
 // step; 2-4 (forced caps) measured slower too.
-#ifdef OZK_SPLIT_MIN_BLOCKS
-__global__ void __launch_bounds__(kSplitThreads, OZK_SPLIT_MIN_BLOCKS)
-#else
-__global__ void __launch_bounds__(kSplitThreads)
-#endif
+template <int K, typename T, int NT, bool SM>
+__global__ void __launch_bounds__(NT)
 split_rows_kernel(const T* __restrict__ in, size_t in_ld, T* __restrict__ work, size_t cols,
                   int d, int sigma, double* __restrict__ pieces, size_t ldk,
                   size_t slice_stride, unsigned long long* __restrict__ piece_max,
                   int* __restrict__ err, DigitOut dig, bool keep_residual) {
     __shared__ double red[33];
+    extern __shared__ double srow_raw[];
     const size_t r = blockIdx.x;
     const T* src = in + r * in_ld * K;
-    T* w = work + r * cols * K;
+    T* gw = work + r * cols * K;                          // global residual row
+    T* w = SM ? reinterpret_cast<T*>(srow_raw) : gw;      // working residual row
     double* prow = pieces ? pieces + r * ldk : nullptr;
 
     // Sweep 0: leading image max and finiteness scan (ozaki.hpp:77-78).  For
@@ -125,7 +130,7 @@ split_rows_kernel(const T* __restrict__ in, size_t in_ld, T* __restrict__ work, 
     T mx = T(0);
     int bad = 0;
     if (d == 1 && src != w) {
-        for (size_t j = threadIdx.x; j < cols; j += kSplitThreads) {
+        for (size_t j = threadIdx.x; j < cols; j += NT) {
             T c[K];
             load_kw<K>(src + j * K, c);
             bad |= !is_finite(c[0]);
@@ -135,7 +140,7 @@ split_rows_kernel(const T* __restrict__ in, size_t in_ld, T* __restrict__ work, 
     } else {
         // only the leading words: MultiFloat::is_finite and leading_image look
         // at c[0] alone (multifloat.hpp:176, dense_matrix.hpp:91-96)
-        for (size_t j = threadIdx.x; j < cols; j += kSplitThreads) {
+        for (size_t j = threadIdx.x; j < cols; j += NT) {
             const T c0 = src[j * K];
             bad |= !is_finite(c0);
             mx = fmax(mx, fabs_(c0));
@@ -151,19 +156,19 @@ split_rows_kernel(const T* __restrict__ in, size_t in_ld, T* __restrict__ work, 
         // D = 1: the piece is the leading image, the residual keeps the tail
         // (ozaki.hpp:90-96: every element, zero or not, gets residual -= lead).
         double pmx = 0.0;
-        for (size_t j = threadIdx.x; j < cols; j += kSplitThreads) {
+        for (size_t j = threadIdx.x; j < cols; j += NT) {
             T c[K];
             load_kw<K>(w + j * K, c);
             const T lead = c[0];
             if (prow) prow[j] = (double)lead;
             if (keep_residual) {
                 kw_add<K>(c, -lead);
-                store_kw<K>(w + j * K, c);
+                store_kw<K>(gw + j * K, c);
             }
             pmx = fmax(pmx, (double)fabs_(lead));
         }
         if (prow)
-            for (size_t j = cols + threadIdx.x; j < ldk; j += kSplitThreads) prow[j] = 0.0;
+            for (size_t j = cols + threadIdx.x; j < ldk; j += NT) prow[j] = 0.0;
         if (piece_max) {
             pmx = block_max(pmx, red);
             if (threadIdx.x == 0)
@@ -190,7 +195,6 @@ split_rows_kernel(const T* __restrict__ in, size_t in_ld, T* __restrict__ work, 
         const bool update = keep_residual || a + 1 < d;
         // pass 0 reads the input row; it must store every element when the
         // residual row is a separate buffer (it was not copied in sweep 0)
-        const T* rd = a == 0 ? src : w;
         const bool store_all = a == 0 && src != w;
         // INT8-digit output: the slice row is an integer multiple of 2^g,
         // g = e + sigma - S: every piece is an integer multiple of this grid
@@ -205,7 +209,7 @@ split_rows_kernel(const T* __restrict__ in, size_t in_ld, T* __restrict__ work, 
         const double inv_grid = g_normal ? __longlong_as_double((long long)(1023 - g) << 52) : 0.0;
         if (dig.digits && threadIdx.x == 0) dig.exps[(size_t)a * dig.exp_stride + r] = g;
         if (tau == T(0)) {  // block-uniform
-            for (size_t j = threadIdx.x; j < cols; j += kSplitThreads) {
+            for (size_t j = threadIdx.x; j < cols; j += NT) {
                 if (pa) pa[j] = 0.0;
                 if (drow)
                     for (int q = 0; q < dig.nd; ++q) drow[j + q * dig.digit_stride] = 0;
@@ -216,7 +220,9 @@ split_rows_kernel(const T* __restrict__ in, size_t in_ld, T* __restrict__ work, 
                 }
             }
         } else {
-            auto element = [&](size_t j) {
+            // rd: the input row (pass 0) or the residual row; compile-time
+            // distinct so the shared-memory variant issues LDS/STS
+            auto element = [&](size_t j, const T* rd) {
                 T c[K];
                 load_kw<K>(rd + j * K, c);
                 // shift_extract: (v + tau) - tau, strictly rounded (ozaki.hpp:53-56)
@@ -233,7 +239,7 @@ split_rows_kernel(const T* __restrict__ in, size_t in_ld, T* __restrict__ work, 
                     drow[j + (dig.nd - 1) * dig.digit_stride] = (int8_t)mi;
                 }
                 if (update && x != T(0)) {
-                    // w -= x  ==  w + (-x)  (multifloat.hpp:215,391); FP64 compares:
+                    // w -= x  ==  w + (-x)  (multifloat.hpp:304,215); FP64 compares:
                     // this kernel is ALU-bound, its FP64 pipe mostly idle
                     kw_add<K, T, false>(c, -x);
                     store_kw<K>(w + j * K, c);
@@ -245,12 +251,15 @@ split_rows_kernel(const T* __restrict__ in, size_t in_ld, T* __restrict__ work, 
             };
             // one element per trip: two interleaved per thread measured slower
             // (TD 18.4 -> 22.1 ms, register pressure at 512 threads)
-            for (size_t j = threadIdx.x; j < cols; j += kSplitThreads) element(j);
+            if (a == 0)
+                for (size_t j = threadIdx.x; j < cols; j += NT) element(j, src);
+            else
+                for (size_t j = threadIdx.x; j < cols; j += NT) element(j, w);
         }
         if (pa)
-            for (size_t j = cols + threadIdx.x; j < ldk; j += kSplitThreads) pa[j] = 0.0;
+            for (size_t j = cols + threadIdx.x; j < ldk; j += NT) pa[j] = 0.0;
         if (drow)
-            for (size_t j = cols + threadIdx.x; j < dig.ld; j += kSplitThreads)
+            for (size_t j = cols + threadIdx.x; j < dig.ld; j += NT)
                 for (int q = 0; q < dig.nd; ++q) drow[j + q * dig.digit_stride] = 0;
         if (piece_max) {
             pmx = block_max(pmx, red);
@@ -259,6 +268,14 @@ split_rows_kernel(const T* __restrict__ in, size_t in_ld, T* __restrict__ work, 
                           static_cast<unsigned long long>(__double_as_longlong(pmx)));
         }
         if (update) mx = (T)block_max((double)nmx, red);
+    }
+    if (SM && keep_residual) {  // the caller reads the residual (ozk_split)
+        __syncthreads();
+        for (size_t j = threadIdx.x; j < cols; j += NT) {
+            T c[K];
+            load_kw<K>(w + j * K, c);
+            store_kw<K>(gw + j * K, c);
+        }
     }
 }
 
@@ -288,31 +305,58 @@ __global__ void transpose_kernel(const T* __restrict__ in, size_t in_ld, T* __re
 
 } // namespace
 
+// Shared-memory residual rows: up to this many bytes per row (227 KB per CTA
+// minus the reduction scratch), D >= 2; OZK_SPLIT_SMEM=0 forces the global
+// variant (A/B builds).
+#ifndef OZK_SPLIT_SMEM
+#define OZK_SPLIT_SMEM 1
+#endif
+constexpr size_t kSplitSmemMax = 220 * 1024;
+constexpr int kSplitSmemThreads = 1024;
+
+template <int K, typename T>
+cudaError_t launch_split_typed(const void* in, size_t in_ld, void* work, size_t rows, size_t cols,
+                               int d, int sigma, double* pieces, size_t ldk, size_t slice_stride,
+                               unsigned long long* piece_max, int* err, cudaStream_t st,
+                               const DigitOut& dig, bool keep_residual) {
+    const size_t row_bytes = cols * K * sizeof(T);
+    if (OZK_SPLIT_SMEM && d >= 2 && row_bytes <= kSplitSmemMax) {
+        auto kern = split_rows_kernel<K, T, kSplitSmemThreads, true>;
+        // per call: the attribute belongs to the current device
+        const cudaError_t e = cudaFuncSetAttribute(
+            kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSplitSmemMax);
+        if (e != cudaSuccess) return e;
+        kern<<<(unsigned)rows, kSplitSmemThreads, row_bytes, st>>>(
+            static_cast<const T*>(in), in_ld, static_cast<T*>(work), cols, d, sigma, pieces, ldk,
+            slice_stride, piece_max, err, dig, keep_residual);
+    } else {
+        split_rows_kernel<K, T, kSplitThreads, false><<<(unsigned)rows, kSplitThreads, 0, st>>>(
+            static_cast<const T*>(in), in_ld, static_cast<T*>(work), cols, d, sigma, pieces, ldk,
+            slice_stride, piece_max, err, dig, keep_residual);
+    }
+    return cudaGetLastError();
+}
+
 cudaError_t launch_split_rows(int K, int word_bytes, const void* in, size_t in_ld, void* work,
                               size_t rows, size_t cols, int d, int sigma, double* pieces,
                               size_t ldk, size_t slice_stride, unsigned long long* piece_max,
                               int* err, cudaStream_t st, const DigitOut& dig,
                               bool keep_residual) {
     if (rows == 0) return cudaSuccess;
-    dim3 grid((unsigned)rows), block(kSplitThreads);
-#define OZK_SPLIT(KK, TT)                                                                         \
-    split_rows_kernel<KK, TT><<<grid, block, 0, st>>>(static_cast<const TT*>(in), in_ld,          \
-                                                      static_cast<TT*>(work), cols, d, sigma,     \
-                                                      pieces, ldk, slice_stride, piece_max, err, \
-                                                      dig, keep_residual)
+#define OZK_SPLIT(KK, TT)                                                                      \
+    launch_split_typed<KK, TT>(in, in_ld, work, rows, cols, d, sigma, pieces, ldk, slice_stride, \
+                               piece_max, err, st, dig, keep_residual)
     if (word_bytes == 4) {
         if (K != 3) return cudaErrorInvalidValue;
-        OZK_SPLIT(3, float);
-    } else {
-        switch (K) {
-        case 2: OZK_SPLIT(2, double); break;
-        case 3: OZK_SPLIT(3, double); break;
-        case 4: OZK_SPLIT(4, double); break;
-        default: return cudaErrorInvalidValue;
-        }
+        return OZK_SPLIT(3, float);
+    }
+    switch (K) {
+    case 2: return OZK_SPLIT(2, double);
+    case 3: return OZK_SPLIT(3, double);
+    case 4: return OZK_SPLIT(4, double);
+    default: return cudaErrorInvalidValue;
     }
 #undef OZK_SPLIT
-    return cudaGetLastError();
 }
 
 cudaError_t launch_transpose(int K, int word_bytes, const void* in, size_t in_ld, void* out,
