@@ -212,21 +212,34 @@ OZK_HD void non_finite(T head, T* c) {
 #define OZK_KW_TAILSKIP 1
 #endif
 
+// OZK_KW_ZGUARD=0 runs the compaction unconditionally (A/B builds).
+#ifndef OZK_KW_ZGUARD
+#define OZK_KW_ZGUARD 1
+#endif
+
 // kTailZeros: the caller guarantees c has no zero before a nonzero word, so
 // the first pass's compaction is the identity and is skipped.
 template <int K, bool kInt = false, bool kTailZeros = false, typename T>
 OZK_HD void strict_normalize(T* c) {
 #pragma unroll
     for (int pass = 0; pass < 2 * K; ++pass) {
-        // stable compaction of zeros to the tail (bubble, static indices)
+        // stable compaction of zeros to the tail (bubble, static indices).  It
+        // is the identity unless a zero sits before the last word (a zero in
+        // the last word is already at the tail), so it runs only then: the
+        // common case costs K-1 zero tests instead of 2(K-1)^2 selects.
+        bool interior_zero = !OZK_KW_ZGUARD;
 #pragma unroll
-        for (int r = 0; r < ((kTailZeros && pass == 0) ? 0 : K - 1); ++r) {
+        for (int i = 0; i < K - 1; ++i) interior_zero = interior_zero || is_zero<kInt>(c[i]);
+        if (interior_zero) {
 #pragma unroll
-            for (int i = 0; i < K - 1; ++i) {
-                bool z = is_zero<kInt>(c[i]);
-                T lo = c[i + 1];
-                c[i + 1] = z ? T(0) : c[i + 1];
-                c[i] = z ? lo : c[i];
+            for (int r = 0; r < ((kTailZeros && pass == 0) ? 0 : K - 1); ++r) {
+#pragma unroll
+                for (int i = 0; i < K - 1; ++i) {
+                    bool z = is_zero<kInt>(c[i]);
+                    T lo = c[i + 1];
+                    c[i + 1] = z ? T(0) : c[i + 1];
+                    c[i] = z ? lo : c[i];
+                }
             }
         }
         // trailing zeros written by the reference's compaction are +0
@@ -326,7 +339,12 @@ OZK_HD bool kw_fast_ok(const T* x, T y) {
 // MultiFloat<K> + word (multifloat.hpp:203-213); x is updated in place.  T is
 // the word type: double for DD/TD/QD, float for TS (which uses the generic
 // K >= 3 branch with binary32 words, see oracle/ozk_oracle.c).
-template <int K, bool kInt, typename T, bool kFast = false>
+// kLead (K >= 3): the caller guarantees |y| > |x[1]| (or x[1] == 0, y != 0),
+// so merge_components places y right before or right after x[0] and only that
+// one comparison is made.  The split's w -= x satisfies it: x != 0 is w0
+// rounded to a grid of at least 2^(e+sigma-S) (e >= the binade of w0), while
+// |w1| <= 1/2 ulp(w0) <= 2^(e-S) (renormalised residual), sigma >= 1.
+template <int K, bool kInt, typename T, bool kFast = false, bool kLead = false>
 OZK_HD void kw_add_impl(T* x, T y) {
     if constexpr (K == 2) {
         T s, e;
@@ -348,14 +366,22 @@ OZK_HD void kw_add_impl(T* x, T y) {
         // merge_components(x, K, &y, 1): y goes before the first x[i] that
         // does not precede it
         T m[K + 1];
-        bool placed = false;
+        if constexpr (kLead) {
+            const bool x0_first = merge_before<kInt>(x[0], y);
+            m[0] = x0_first ? x[0] : y;
+            m[1] = x0_first ? y : x[0];
 #pragma unroll
-        for (int i = 0; i <= K; ++i) {
-            bool take_x = !placed && i < K && merge_before<kInt>(x[i < K ? i : 0], y);
-            T prev = x[i > 0 ? i - 1 : 0];
-            T cur = x[i < K ? i : K - 1];
-            m[i] = placed ? prev : (take_x ? cur : y);
-            placed = placed || !take_x;
+            for (int i = 2; i <= K; ++i) m[i] = x[i - 1];
+        } else {
+            bool placed = false;
+#pragma unroll
+            for (int i = 0; i <= K; ++i) {
+                bool take_x = !placed && i < K && merge_before<kInt>(x[i < K ? i : 0], y);
+                T prev = x[i > 0 ? i - 1 : 0];
+                T cur = x[i < K ? i : K - 1];
+                m[i] = placed ? prev : (take_x ? cur : y);
+                placed = placed || !take_x;
+            }
         }
         // sum_ordered: finiteness probe over all terms (cannot fail under the
         // kw_fast_ok guard: |probe| < (K + 1) * 2^1000)
@@ -431,14 +457,14 @@ inline void kw_add_full(T* x, T y) {
 // integer ALU ops where the FP64 pipe is the contended one (the slice-GEMM
 // epilogue, which shares it with the tensor cores), FP64 compares where the
 // ALU pipe is (the split).
-template <int K, typename T = double, bool kIntCmp = true>
+template <int K, typename T = double, bool kIntCmp = true, bool kLead = false>
 OZK_HD void kw_add(T* x, T y) {
 #if OZK_KW_FAST
     if constexpr (K >= 3) {
-        // the reference sequence minus two steps that are provably no-ops on
+        // the reference sequence minus steps that are provably no-ops on
         // guarded inputs (kw_fast_ok); anything else takes the full sequence
         if (kw_fast_ok<K>(x, y))
-            kw_add_impl<K, kIntCmp, T, true>(x, y);
+            kw_add_impl<K, kIntCmp, T, true, kLead>(x, y);
         else
             kw_add_full<K>(x, y);
         return;

@@ -28,6 +28,10 @@ namespace {
 #define OZK_SPLIT_THREADS 512
 #endif
 constexpr int kSplitThreads = OZK_SPLIT_THREADS;
+// the residual update's one-comparison merge (kword.cuh kLead); 0 = generic
+#ifndef OZK_SPLIT_LEAD
+#define OZK_SPLIT_LEAD 1
+#endif
 
 __device__ __forceinline__ int ceil_log2(double x) {
     int e = ilogb(x);
@@ -241,7 +245,7 @@ split_rows_kernel(const T* __restrict__ in, size_t in_ld, T* __restrict__ work, 
                 if (update && x != T(0)) {
                     // w -= x  ==  w + (-x)  (multifloat.hpp:304,215); FP64 compares:
                     // this kernel is ALU-bound, its FP64 pipe mostly idle
-                    kw_add<K, T, false>(c, -x);
+                    kw_add<K, T, false, OZK_SPLIT_LEAD != 0>(c, -x);  // kLead: see kword.cuh
                     store_kw<K>(w + j * K, c);
                 } else if (store_all) {
                     store_kw<K>(w + j * K, c);
@@ -309,7 +313,7 @@ __global__ void transpose_kernel(const T* __restrict__ in, size_t in_ld, T* __re
 // minus the reduction scratch), D >= 2; OZK_SPLIT_SMEM=0 forces the global
 // variant (A/B builds).
 #ifndef OZK_SPLIT_SMEM
-#define OZK_SPLIT_SMEM 1
+#define OZK_SPLIT_SMEM 0
 #endif
 constexpr size_t kSplitSmemMax = 220 * 1024;
 constexpr int kSplitSmemThreads = 1024;

@@ -239,3 +239,89 @@ def test_kword_add_fp_compare_flavour(ref, port, K):
     want = cpu.mf_add_double(K, x, y)
     bad = np.flatnonzero((got.view(np.uint64) != want.view(np.uint64)).any(axis=1))
     assert bad.size == 0, (bad.size, x[bad[0]], y[bad[0]], got[bad[0]], want[bad[0]])
+
+
+def _split_chain_cases(K, cpu, rng, rows):
+    """(w, -x) pairs exactly as the split produces them: w a renormalised
+    residual, x = fl(fl(w0 + tau) - tau) with tau = 2^(e + sigma), e at or above
+    the binade of w0 (the row maximum may be larger), for realistic sigma (the
+    split's 24..34 at l = 2..16384 and TS's 13..19) and extreme ones (1, 2),
+    followed through several passes so later residuals (tails, zeros, exact
+    cancellations) are covered too."""
+    ws, ys = [], []
+    w = cpu.gen_eq1(K, rows, 8, int(rng.integers(1, 1 << 30))).reshape(-1, K).copy()
+    w[rng.random(w.shape[0]) < 0.05, 1:] = 0.0
+    w *= np.exp2(rng.integers(-40, 40, w.shape[0]).astype(float))[:, None]
+    for _ in range(6):
+        w0 = w[:, 0]
+        nz = w0 != 0.0
+        e = np.zeros(w.shape[0], dtype=np.int64)
+        m, ex = np.frexp(np.abs(w0[nz]))
+        e[nz] = ex - (m == 0.5)  # ceil(log2 |w0|)
+        e += rng.integers(0, 4, w.shape[0])  # the row max may be larger
+        sigma = rng.choice([1, 2, 13, 19, 24, 31, 33, 34, 40], w.shape[0])
+        tau = np.ldexp(1.0, (e + sigma).astype(np.int64))
+        x = (w0 + tau) - tau
+        use = nz & (x != 0.0)
+        ws.append(w[use].copy())
+        ys.append(-x[use])
+        w = cpu.mf_add_double(K, w, np.where(use, -x, 0.0))
+    return np.concatenate(ws), np.concatenate(ys)
+
+
+@pytest.mark.parametrize("K", [3, 4])
+def test_split_residual_update_matches_reference(ref, port, K):
+    """The split's w -= x (kw_add<K, double, false, kLead = true>: one merge
+    comparison, see kword.cuh) equals the reference's MultiFloat -= double on
+    every (w, x) pair the split can produce."""
+    import __graft_entry__
+    if not os.path.exists(SO):
+        __graft_entry__._build_test_helpers()
+    lib = ctypes.CDLL(SO)
+    lib.kw_host_split_sub.argtypes = [ctypes.c_int, ctypes.c_size_t, ctypes.c_void_p,
+                                      ctypes.c_void_p, ctypes.c_void_p]
+    cpu = _checker(ref, port)
+    rng = np.random.default_rng(2468 + K)
+    x, y = _split_chain_cases(K, cpu, rng, 12_000)
+    assert x.shape[0] > 200_000
+    got = np.empty_like(x)
+    assert lib.kw_host_split_sub(K, x.shape[0], x.ctypes.data, y.ctypes.data,
+                                 got.ctypes.data) == 0
+    want = cpu.mf_add_double(K, x, y)
+    bad = np.flatnonzero((got.view(np.uint64) != want.view(np.uint64)).any(axis=1))
+    assert bad.size == 0, (bad.size, x[bad[0]], y[bad[0]], got[bad[0]], want[bad[0]])
+
+
+def test_split_residual_update_ts(port):
+    """The same for TS (binary32 words, S = 24) against the C restatement."""
+    import __graft_entry__
+    if not os.path.exists(SO):
+        __graft_entry__._build_test_helpers()
+    lib = ctypes.CDLL(SO)
+    lib.kw_host_split_sub_ts.argtypes = [ctypes.c_size_t, ctypes.c_void_p, ctypes.c_void_p,
+                                         ctypes.c_void_p]
+    rng = np.random.default_rng(1357)
+    w = port.gen_eq1_ts(4000, 8, 3).reshape(-1, 3).copy()
+    w *= np.exp2(rng.integers(-30, 30, w.shape[0]).astype(np.float32))[:, None]
+    xs, ys = [], []
+    for _ in range(5):
+        w0 = w[:, 0].astype(np.float32)
+        nz = w0 != 0
+        e = np.zeros(w.shape[0], dtype=np.int64)
+        m, ex = np.frexp(np.abs(w0[nz]))
+        e[nz] = ex - (m == 0.5)
+        e += rng.integers(0, 3, w.shape[0])
+        sigma = rng.choice([1, 5, 13, 19], w.shape[0])
+        tau = np.ldexp(np.float32(1.0), (e + sigma).astype(np.int64)).astype(np.float32)
+        x = ((w0 + tau).astype(np.float32) - tau).astype(np.float32)
+        use = nz & (x != 0)
+        xs.append(w[use].copy())
+        ys.append(-x[use])
+        w = port.ts_add_float(w, np.where(use, -x, np.float32(0)).astype(np.float32))
+    x = np.ascontiguousarray(np.concatenate(xs), dtype=np.float32)
+    y = np.ascontiguousarray(np.concatenate(ys), dtype=np.float32)
+    got = np.empty_like(x)
+    lib.kw_host_split_sub_ts(x.shape[0], x.ctypes.data, y.ctypes.data, got.ctypes.data)
+    want = port.ts_add_float(x, y)
+    bad = np.flatnonzero((got.view(np.uint32) != want.view(np.uint32)).any(axis=1))
+    assert bad.size == 0, (bad.size, x[bad[0]], y[bad[0]], got[bad[0]], want[bad[0]])
