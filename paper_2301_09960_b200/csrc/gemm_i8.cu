@@ -246,6 +246,16 @@ __device__ __forceinline__ uint64_t sw_desc(uint32_t saddr) {
     return (uint64_t)((saddr >> 4) & 0x3fff) | ((uint64_t)1 << 16) |
            ((uint64_t)((8 * BKB) >> 4) << 32) | ((uint64_t)1 << 46) | (kLayout << 61);
 }
+// L2 sector promotion of the operand TMA loads (OZK_I8_L2PROMO: 0 none, 1 64B,
+// 2 128B, 3 256B)
+#ifndef OZK_I8_L2PROMO
+#define OZK_I8_L2PROMO 3
+#endif
+constexpr CUtensorMapL2promotion kL2Promo =
+    OZK_I8_L2PROMO == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE
+    : OZK_I8_L2PROMO == 1 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+    : OZK_I8_L2PROMO == 2 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
+                          : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
 constexpr CUtensorMapSwizzle kTmaSwizzle =
     BKB == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
 __device__ __forceinline__ void umma_i8(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc,
@@ -999,7 +1009,7 @@ cudaError_t launch_i8_chunk(const I8Operands& op, const PairChunk& pairs, cudaSt
         cuuint32_t es[4] = {1, 1, 1, 1};
         if (encode(&maps.a, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<int8_t*>(op.a), dims,
                    strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, kTmaSwizzle,
-                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) !=
+                   kL2Promo, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) !=
             CUDA_SUCCESS)
             return cudaErrorInvalidValue;
     }
@@ -1010,7 +1020,7 @@ cudaError_t launch_i8_chunk(const I8Operands& op, const PairChunk& pairs, cudaSt
         cuuint32_t es[4] = {1, 1, 1, 1};
         if (encode(&maps.b, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<int8_t*>(op.b), dims,
                    strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, kTmaSwizzle,
-                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) !=
+                   kL2Promo, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) !=
             CUDA_SUCCESS)
             return cudaErrorInvalidValue;
     }
