@@ -98,13 +98,26 @@ def test_argument_errors_without_gpu():
     assert b"devices" in lib.ozk_last_error()
     with pytest.raises(ozk.shape_error):
         ozk.ozaki_gemm_multi(a, np.zeros((3, 2, 2)), 2, devices=[0])
+    # round-2 entry points: argument errors before any device work
+    assert lib.ozk_accumulate_products(7, 2, 2, None, 0, None) == 2
+    assert lib.ozk_accumulate_products(2, 0, 2, None, 0, None) == 1
+    assert lib.ozk_accumulate_products(2, 2, 2, None, -1, None) == 2
+    assert lib.ozk_split_digits_device_async(2, 2, 2, 2, None, 0, 0, None, 16, 2, None, None,
+                                             None, None) == 2
+    assert lib.ozk_split_digits_device_async(2, 300, 300, 300, None, 3, 0, None, 304, 300,
+                                             None, None, None, None) == 2  # null outputs
+    # a caller's backend is honoured, with the reference's argument checks first
+    with pytest.raises(ozk.param_error):
+        ozk.ozaki_gemm(a, a, 0, backend=lambda x, y: x @ y)
+    with pytest.raises(ozk.shape_error):
+        ozk.ozaki_gemm(a, np.zeros((3, 2, 2)), 2, backend=lambda x, y: x @ y)
 
 
 def test_pair_list_matches_reference_order(port):
     """ozaki.hpp:198-221: alpha-major triangular list with drop pruning."""
     import paper_2301_09960_b200 as ozk
     rng = np.random.default_rng(3)
-    for d in (1, 2, 3, 6, 12, 32):
+    for d in (1, 2, 3, 6, 12, 32, 40, 70):  # D > 32: pair lists run as several launches
         amax = np.sort(rng.random(d))[::-1] * np.exp2(-20.0 * np.arange(d))
         bmax = np.sort(rng.random(d))[::-1] * np.exp2(-20.0 * np.arange(d))
         for drop in (0.0, 2.0 ** -60, 2.0 ** -30, 0.5):
