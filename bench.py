@@ -535,7 +535,7 @@ def run_ours(args):
 
     e2e = None
     if not args.no_e2e and world == 1:
-        e2e = run_e2e(args, lib, OzkProfile, ha, hb, code, K, wb, d, n)
+        e2e = run_e2e(args, lib, OzkProfile, ha, hb, code, K, wb, d, n, C)
     elif not args.no_e2e:
         e2e = run_e2e_sharded(args, eng, A, B, K, wb, n)
 
@@ -619,7 +619,7 @@ def run_ours(args):
     return 0
 
 
-def run_e2e(args, lib, OzkProfile, ha, hb, code, K, wb, d, n):
+def run_e2e(args, lib, OzkProfile, ha, hb, code, K, wb, d, n, C_dev=None):
     """Same metric through the host-buffer C-ABI entry point (ozk_ozaki_gemm):
     H2D of A and B, the GEMM, D2H of C, every step.  From pinned memory (the
     contract's e2e) and, as `pageable`, from ordinary pageable numpy buffers --
@@ -644,7 +644,14 @@ def run_e2e(args, lib, OzkProfile, ha, hb, code, K, wb, d, n):
         return statistics.mean(times)
 
     t = timed(ha.data_ptr(), hb.data_ptr(), hc.data_ptr())
+    same_dev = None
+    if C_dev is not None:  # the host path's C must equal the timed device-resident C
+        same_dev = bool(torch.equal(hc.to(C_dev.device).view(torch.int32),
+                                    C_dev.view(torch.int32)))
+        if not same_dev:
+            raise AssertionError("ozk_ozaki_gemm (host buffers) differs from the device path")
     out = {"value": round(2.0 * n ** 3 / t / 1e9, 3), "unit": "GFLOP/s",
+           "c_identical_to_device_run": same_dev,
            "h2d_bytes_per_step": 2 * n * n * K * wb, "d2h_bytes_per_step": n * n * K * wb,
            "ms_per_step": round(1e3 * t, 3), "api": "ozk_ozaki_gemm (host buffers, pinned)",
            "engine": ENGINE_NAMES.get(prof.engine, "?")}

@@ -242,16 +242,19 @@ struct Timer {
 // t_wave: one cluster tile's work at the measured per-SM INT8 rate of the
 // format (bench_r01_f2: DD 19, TD 16.5, QD 15, TS 9.5 Tops/s per SM).
 struct BandKey {
-    size_t m, n, l, block_cols;
+    size_t m, n, l, block_cols, band0;
     int fmt, d, rows, cols, clusters;
     bool operator<(const BandKey& o) const {
-        return std::tie(m, n, l, block_cols, fmt, d, rows, cols, clusters) <
-               std::tie(o.m, o.n, o.l, o.block_cols, o.fmt, o.d, o.rows, o.cols, o.clusters);
+        return std::tie(m, n, l, block_cols, band0, fmt, d, rows, cols, clusters) <
+               std::tie(o.m, o.n, o.l, o.block_cols, o.band0, o.fmt, o.d, o.rows, o.cols,
+                        o.clusters);
     }
 };
 
+// band0_rows > 0 forces band 0's size (in rows, rounded to cluster rows)
 std::vector<size_t> plan_bands_uncached(int fmt, size_t m, size_t n, size_t l, int d,
-                                        size_t block_cols, const I8Geometry& g) {
+                                        size_t block_cols, const I8Geometry& g,
+                                        size_t band0_rows = 0) {
     std::vector<size_t> starts{0};
     const size_t rtot = g.group_rows > 0 ? (m + g.group_rows - 1) / g.group_rows : 0;
     if (m < 2048 || g.clusters <= 0 || rtot < 8) {
@@ -277,6 +280,8 @@ std::vector<size_t> plan_bands_uncached(int fmt, size_t m, size_t n, size_t l, i
                 best = fill(r, Tb) > best ? fill(r, Tb) : best;
                 r0 = r;
             }
+        if (band0_rows > 0)
+            r0 = std::max<size_t>(1, std::min(rtot - 1, band0_rows / g.group_rows));
     }
     const size_t rest = rtot - r0;
     const int K = words_of(fmt), wb = word_bytes_of(fmt);
@@ -359,16 +364,17 @@ std::vector<size_t> plan_bands_uncached(int fmt, size_t m, size_t n, size_t l, i
 }
 
 std::vector<size_t> plan_bands(int fmt, size_t m, size_t n, size_t l, int d, size_t block_cols,
-                               const I8Geometry& g) {
+                               const I8Geometry& g, size_t band0_rows = 0) {
     static std::mutex mu;
     static std::map<BandKey, std::vector<size_t>> cache;
-    const BandKey key{m, n, l, block_cols, fmt, d, g.group_rows, g.group_cols, g.clusters};
+    const BandKey key{m, n, l, block_cols, band0_rows, fmt, d, g.group_rows, g.group_cols,
+                      g.clusters};
     {
         std::lock_guard<std::mutex> lock(mu);
         auto it = cache.find(key);
         if (it != cache.end()) return it->second;
     }
-    std::vector<size_t> plan = plan_bands_uncached(fmt, m, n, l, d, block_cols, g);
+    std::vector<size_t> plan = plan_bands_uncached(fmt, m, n, l, d, block_cols, g, band0_rows);
     std::lock_guard<std::mutex> lock(mu);
     if (cache.size() > 256) cache.clear();
     cache[key] = plan;
@@ -769,7 +775,14 @@ ozk_status ozk_ozaki_gemm(ozk_format fmt, size_t m, size_t l, size_t n, const vo
     // n = 8192 a block's H2D time matches its GEMM block
     const bool i8 = engine_setting() != OZK_ENGINE_DMMA && int8_applicable((int)fmt, l, d);
     const bool blockable = m >= 2048 && drop == 0.0 && i8 && n >= 4096;
-    const size_t b_block_cols = blockable ? (((n + 3) / 4 + 127) / 128) * 128 : n;
+    // schedule knobs for A/B sweeps (tools/host_schedule_sweep.py):
+    // $OZK_HOST_BBLOCKS (B column blocks, default 4), $OZK_HOST_BAND0 (rows)
+    int nblk = 4;
+    size_t band0_rows = 0;
+    if (const char* v = std::getenv("OZK_HOST_BBLOCKS")) nblk = std::max(1, std::atoi(v));
+    if (const char* v = std::getenv("OZK_HOST_BAND0")) band0_rows = (size_t)std::max(0, std::atoi(v));
+    const size_t b_block_cols =
+        blockable ? (((n + nblk - 1) / nblk + 127) / 128) * 128 : n;
     // row bands from the slice GEMM's tile geometry (DMMA engine: 8 equal bands)
     const I8Geometry geo =
         i8 ? pair_gemm_i8_geometry(words_of((int)fmt), word_bytes_of((int)fmt),
@@ -777,7 +790,7 @@ ozk_status ozk_ozaki_gemm(ozk_format fmt, size_t m, size_t l, size_t n, const vo
            : I8Geometry{};
     std::vector<size_t> band_start;
     if (i8) {
-        band_start = plan_bands((int)fmt, m, n, l, d, b_block_cols, geo);
+        band_start = plan_bands((int)fmt, m, n, l, d, b_block_cols, geo, band0_rows);
     } else {
         const size_t nb = m >= 2048 ? 8 : 1;
         for (size_t q = 0; q <= nb; ++q) band_start.push_back(m * q / nb);
