@@ -770,14 +770,16 @@ ozk_status ozk_ozaki_gemm(ozk_format fmt, size_t m, size_t l, size_t n, const vo
     guard.evs.push_back(allocated);
     OZK_CUDA(cudaEventCreateWithFlags(&b_ready, cudaEventDisableTiming), "ozaki_gemm: event");
     guard.evs.push_back(b_ready);
-    // B in 4 column blocks (whole 128-column tiles) when the first band can be
-    // multiplied block by block (INT8 engine, no pruning, n >= 4096): at
-    // n = 8192 a block's H2D time matches its GEMM block
+    // B in column blocks (whole 128-column tiles) when the first band can be
+    // multiplied block by block (INT8 engine, no pruning, n >= 4096)
     const bool i8 = engine_setting() != OZK_ENGINE_DMMA && int8_applicable((int)fmt, l, d);
     const bool blockable = m >= 2048 && drop == 0.0 && i8 && n >= 4096;
-    // schedule knobs for A/B sweeps (tools/host_schedule_sweep.py):
-    // $OZK_HOST_BBLOCKS (B column blocks, default 4), $OZK_HOST_BAND0 (rows)
-    int nblk = 4;
+    // B column blocks: 8 at n >= 8192 (1024-column blocks: the first GEMM
+    // starts after 1/8 of B; TD n=8192 203 ms vs 208 with 4 blocks, DD within
+    // noise, profiles/r02_host_schedule_sweep_*.log), else 4.  Knobs for A/B
+    // sweeps (tools/host_schedule_sweep.py): $OZK_HOST_BBLOCKS, $OZK_HOST_BAND0
+    // (band-0 rows)
+    int nblk = n >= 8192 ? 8 : 4;
     size_t band0_rows = 0;
     if (const char* v = std::getenv("OZK_HOST_BBLOCKS")) nblk = std::max(1, std::atoi(v));
     if (const char* v = std::getenv("OZK_HOST_BAND0")) band0_rows = (size_t)std::max(0, std::atoi(v));

@@ -785,7 +785,8 @@ def test_accumulate_products_matches_reference(ozk, cpu, port):
     assert (zero == 0).all()
 
 
-def test_host_api_pinned_and_pageable_agree(ozk, cpu, monkeypatch):
+@pytest.mark.parametrize("n", [4200, 8320])
+def test_host_api_pinned_and_pageable_agree(ozk, cpu, monkeypatch, n):
     """ozk_ozaki_gemm's host path with every mix of pinned (page-locked) and
     pageable caller buffers -- pageable ones are staged through pinned slots on
     worker threads (csrc/staging.cu), strided B column blocks included -- and
@@ -794,7 +795,7 @@ def test_host_api_pinned_and_pageable_agree(ozk, cpu, monkeypatch):
     import ctypes
 
     import torch
-    K, m, l, n, d = 3, 2304, 300, 4200, 4
+    K, m, l, d = 3, 2304, 300, 4   # n = 8320: 8 ragged B column blocks
     a = cpu.gen_eq1(K, m, l, 31)
     b = cpu.gen_eq1(K, l, n, 32)
     pa, pb = torch.from_numpy(a).pin_memory(), torch.from_numpy(b).pin_memory()
