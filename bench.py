@@ -488,7 +488,7 @@ def run_ours(args):
     traffic = None
     traffic_src = None
     tfile = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles",
-                         "r01_i8_td8192_traffic.json")
+                         "r02_i8_td8192_traffic.json")
     if (engine_used == "int8" and world == 1 and args.format == "td" and n == 8192 and d == 9
             and args.spread == 0 and os.path.exists(tfile)):
         # dram__bytes_read.sum + dram__bytes_write.sum of this kernel on this
