@@ -51,6 +51,31 @@ extern "C" void kw_host_split_sub_ts(std::size_t n, const float* x, const float*
     run_split<3, float>(n, x, y, out);
 }
 
+template <int K, typename T>
+static void run_accum(std::size_t n, const T* x, const T* y, T* out) {
+    for (std::size_t i = 0; i < n; ++i) {
+        T w[K];
+        for (int k = 0; k < K; ++k) w[k] = x[i * K + k];
+        ozk::kw_add<K, T, true, false, true>(w, y[i]);  // the accumulation's flavour
+        for (int k = 0; k < K; ++k) out[i * K + k] = w[k];
+    }
+}
+
+// acc += y as the slice-GEMM epilogues run it (kAccum: negligible-addend exit)
+extern "C" int kw_host_add_accum(int K, std::size_t n, const double* x, const double* y,
+                                 double* out) {
+    switch (K) {
+    case 2: run_accum<2>(n, x, y, out); return 0;
+    case 3: run_accum<3>(n, x, y, out); return 0;
+    case 4: run_accum<4>(n, x, y, out); return 0;
+    default: return 2;
+    }
+}
+
+extern "C" void kw_host_add_accum_ts(std::size_t n, const float* x, const float* y, float* out) {
+    run_accum<3, float>(n, x, y, out);
+}
+
 extern "C" int kw_host_add_fpcmp(int K, std::size_t n, const double* x, const double* y,
                                  double* out) {
     switch (K) {

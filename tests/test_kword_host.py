@@ -325,3 +325,91 @@ def test_split_residual_update_ts(port):
     want = port.ts_add_float(x, y)
     bad = np.flatnonzero((got.view(np.uint32) != want.view(np.uint32)).any(axis=1))
     assert bad.size == 0, (bad.size, x[bad[0]], y[bad[0]], got[bad[0]], want[bad[0]])
+
+
+def _accum_lib():
+    import __graft_entry__
+    if not os.path.exists(SO):
+        __graft_entry__._build_test_helpers()
+    lib = ctypes.CDLL(SO)
+    lib.kw_host_add_accum.argtypes = [ctypes.c_int, ctypes.c_size_t, ctypes.c_void_p,
+                                      ctypes.c_void_p, ctypes.c_void_p]
+    lib.kw_host_add_accum_ts.argtypes = [ctypes.c_size_t, ctypes.c_void_p, ctypes.c_void_p,
+                                         ctypes.c_void_p]
+    return lib
+
+
+def _near_threshold(rng, x, K):
+    """Addends around ulp(x[K-1]) / 4 -- the negligible-addend exit's bound --
+    with both signs, exact powers of two, and x[K-1] itself a power of two."""
+    n = x.shape[0]
+    e = np.frexp(np.abs(x[:, K - 1]))[1] - 1          # floor(log2 |x[K-1]|)
+    base = np.ldexp(1.0, e - 54)                     # ulp / 4 (binary64)
+    f = rng.choice([0.5, 0.999, 1.0, 1.0000001, 1.5, 2.0, 4.0, 2.0 ** -30, 3.0], n)
+    y = base * f * np.where(rng.random(n) < 0.5, -1.0, 1.0)
+    pw = rng.random(n) < 0.2                          # x[K-1] an exact power of two
+    x[pw, K - 1] = np.copysign(np.ldexp(1.0, e[pw]), x[pw, K - 1])
+    return y
+
+
+@pytest.mark.parametrize("K", [2, 3, 4])
+def test_accumulation_negligible_exit_matches_reference(ref, port, K):
+    """kw_add's accumulation flavour (kAccum: x + y == x taken without the
+    sequence when y is below a quarter ulp of x's last word and x is a strict
+    fixpoint, kword.cuh kw_negligible) equals the reference on fixpoints from
+    the reference itself, on addends straddling the bound, on power-of-two last
+    words, on non-fixpoint x (the check must refuse), and along long chains."""
+    cpu = _checker(ref, port)
+    lib = _accum_lib()
+    rng = np.random.default_rng(97531 + K)
+
+    def run(x, y):
+        x = np.ascontiguousarray(x)
+        y = np.ascontiguousarray(y)
+        got = np.empty_like(x)
+        assert lib.kw_host_add_accum(K, x.shape[0], x.ctypes.data, y.ctypes.data,
+                                     got.ctypes.data) == 0
+        want = cpu.mf_add_double(K, x, y)
+        bad = np.flatnonzero((got.view(np.uint64) != want.view(np.uint64)).any(axis=1))
+        assert bad.size == 0, (bad.size, x[bad[0]], y[bad[0]], got[bad[0]], want[bad[0]])
+
+    # reference outputs (fixpoints) with addends around the bound
+    x = cpu.gen_eq1(K, 400, 100, 77).reshape(-1, K).copy()
+    x = cpu.mf_add_double(K, x, rng.standard_normal(x.shape[0]) * 2.0 ** -70)
+    run(x, _near_threshold(rng, x.copy(), K))
+    xp = x.copy()
+    y = _near_threshold(rng, xp, K)                   # power-of-two last words
+    run(xp, y)
+    # non-fixpoint x: adjacent words overlapping, sign patterns, zeros
+    xn = x.copy()
+    sel = rng.integers(0, 4, xn.shape[0])
+    xn[sel == 0, K - 1] = xn[sel == 0, K - 2] * 0.75
+    xn[sel == 1, 1] = -xn[sel == 1, 1] * 2.0 ** 60
+    xn[sel == 2, K - 2] = 0.0
+    run(xn, _near_threshold(rng, xn.copy(), K))
+    # chains: acc += C_p with the Ozaki magnitudes 2^-20 per level
+    acc_a = np.zeros((20000, K))
+    acc_b = np.zeros((20000, K))
+    for p in range(6 * (4 + 3 * K)):  # levels 0 .. 3K+3: past the last word's quarter ulp
+        y = rng.standard_normal(20000) * 2.0 ** (-20 * (p // 6))
+        got = np.empty_like(acc_a)
+        assert lib.kw_host_add_accum(K, acc_a.shape[0], acc_a.ctypes.data, y.ctypes.data,
+                                     got.ctypes.data) == 0
+        acc_a = got
+        acc_b = cpu.mf_add_double(K, acc_b, y)
+        assert np.array_equal(acc_a.view(np.uint64), acc_b.view(np.uint64)), p
+
+
+def test_accumulation_negligible_exit_ts(port):
+    lib = _accum_lib()
+    rng = np.random.default_rng(8642)
+    acc_a = np.zeros((8000, 3), dtype=np.float32)
+    acc_b = np.zeros((8000, 3), dtype=np.float32)
+    for p in range(60):
+        y = (rng.standard_normal(8000) * 2.0 ** (-5 * (p // 3))).astype(np.float32)
+        got = np.empty_like(acc_a)
+        lib.kw_host_add_accum_ts(acc_a.shape[0], acc_a.ctypes.data, y.ctypes.data,
+                                 got.ctypes.data)
+        acc_a = got
+        acc_b = port.ts_add_float(acc_b, y)
+        assert np.array_equal(acc_a.view(np.uint32), acc_b.view(np.uint32)), p
