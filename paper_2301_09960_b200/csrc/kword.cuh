@@ -457,51 +457,61 @@ inline void kw_add_full(T* x, T y) {
 // integer ALU ops where the FP64 pipe is the contended one (the slice-GEMM
 // epilogue, which shares it with the tensor cores), FP64 compares where the
 // ALU pipe is (the split).
-// x + y == x exactly for the reference's operator+(MultiFloat<K>, double),
-// K >= 3, when (i) every word of x is nonzero and x[K-1] is normal, (ii) x is
-// a strict_normalize fixpoint (fast_two_sum(x[i], x[i+1]) == (x[i], x[i+1])
-// for every i -- checked here, not assumed), and (iii) y != 0 with
-// |y| < 2^(E(x[K-1]) - M - 2) = ulp(x[K-1]) / 4 (M = 52, or 23 for binary32).
-// Proof, following multifloat.hpp:203-213 -> :420-430 -> :405-416: |y| is
-// below every |x[i]|, so merge_components appends y last; the finiteness
-// probe passes (kw_fast_ok); vec_sum's first two_sum(x[K-1], y) returns
-// (x[K-1], y) because |y| is below half the spacing on either side of
-// x[K-1] (the spacing below a power of two is half an ulp: hence the quarter),
-// and each further two_sum(x[i], x[i+1]) returns (x[i], x[i+1]) by (ii); so
-// vec_sum yields x[0..K-1], y unchanged, extract_components emits x[0..K-1]
-// (every lo is a nonzero x[i+1] or y) and stops at K, and strict_normalize
-// finds the fixpoint (ii): the result is x.  In the accumulation
-// acc += C_ab this is the typical last-diagonal pair at the saturating split
-// count (|C_ab| ~ 2^(-20 (alpha+beta)) |acc|), so those adds cost one
-// fixpoint check instead of the full sequence.
+// When y only reaches the last word.  For the reference's
+// operator+(MultiFloat<K>, double), K >= 3 (multifloat.hpp:203-213 ->
+// :420-430 -> :405-416 -> :394-401), with
+//   (i)   y != 0 and x[0..K-2] nonzero,
+//   (ii)  |y| < |x[K-2]|,
+//   (iii) fl(x[i] + x[i+1]) == x[i] for i < K-2 (x[0..K-2] is a strict
+//         fixpoint chain),
+//   (iv)  h = fl(x[K-1] + y) != 0 and fl(x[K-2] + h) == x[K-2],
+// the result is x[0..K-2], h.  Proof: by (ii) merge_components places y after
+// x[0..K-2] (before or after x[K-1]; both give the same below); the probe
+// passes (kw_fast_ok).  If x[K-1] == 0 sum_ordered drops it and vec_sum starts
+// at two_sum(x[K-2], y) = (x[K-2], y) by (iv) with h = y; otherwise vec_sum
+// starts with two_sum(x[K-1], y) (either order) = (h, l), l the exact error,
+// then two_sum(x[K-2], h) = (x[K-2], h) by (iv) (fl(a+b) == a makes both
+// two_sum and fast_two_sum return (a, b)), and (x[i], x[i+1]) for i < K-2 by
+// (iii): the terms stay x[0..K-2], h, l.  extract_components then emits x[0]
+// .. x[K-2] (each following term is a nonzero exact error), and h: two_sum(h,
+// l) = (h, l) as l is h's rounding error, so h is emitted with l != 0 or kept
+// as the final accumulator with l == 0.  strict_normalize finds every
+// adjacent pair a fixpoint by (iii)/(iv) and changes nothing.  The
+// negligible case h == x[K-1] (|y| < ulp(x[K-1]) / 4) is included.  In the
+// accumulation acc += C_ab at the saturating split count about half of the
+// pairs (the last ~3 levels alpha+beta, |C_ab| ~ 2^(-20 (alpha+beta)) |acc|)
+// fall here and cost K DADDs instead of the whole sequence.
+template <bool kInt, typename T>
+OZK_HD bool mag_less(T a, T b) {
+    if constexpr (kInt) {
+        const uint32_t ha = hi_word(a) & 0x7fffffffu, hb = hi_word(b) & 0x7fffffffu;
+        return ha < hb || (ha == hb && lo_word(a) < lo_word(b));
+    } else {
+        return fabs_(a) < fabs_(b);
+    }
+}
+
 template <int K, bool kInt, typename T>
-OZK_HD bool kw_negligible(const T* x, T y) {
-    constexpr int kMant = sizeof(T) == 8 ? 52 : 23;
-    constexpr int kExpShift = sizeof(T) == 8 ? 20 : 23;  // within the high 32-bit word
-    constexpr uint32_t kExpMask = sizeof(T) == 8 ? 0x7ffu : 0xffu;
-    const int eb = (int)((hi_word(x[K - 1]) >> kExpShift) & kExpMask);  // biased exponent
-    const int tb = eb - kMant - 2;  // biased exponent of ulp(x[K-1]) / 4
-    bool ok = tb > 0 && !is_zero<kInt>(y) &&
-              (hi_word(y) & 0x7fffffffu) < ((uint32_t)(tb > 0 ? tb : 0) << kExpShift);
+OZK_HD bool kw_add_tail(T* x, T y) {
+    bool ok = !is_zero<kInt>(y) && mag_less<kInt>(y, x[K - 2]);
 #pragma unroll
     for (int i = 0; i < K - 1; ++i) ok = ok && !is_zero<kInt>(x[i]);
     if (!ok) return false;
+    const T h = rn_add(x[K - 1], y);
+    ok = !is_zero<kInt>(h) && same<kInt>(rn_add(x[K - 2], h), x[K - 2]);
 #pragma unroll
-    for (int i = 0; i + 1 < K; ++i) {
-        T s, e;
-        fast_two_sum(x[i], x[i + 1], s, e);
-        ok = ok && same<kInt>(s, x[i]) && same<kInt>(e, x[i + 1]);
-    }
+    for (int i = 0; i + 2 < K; ++i) ok = ok && same<kInt>(rn_add(x[i], x[i + 1]), x[i]);
+    if (ok) x[K - 1] = h;
     return ok;
 }
 
-// OZK_KW_NEGLIGIBLE=0 disables the negligible-addend exit (A/B builds).
-#ifndef OZK_KW_NEGLIGIBLE
-#define OZK_KW_NEGLIGIBLE 1
+// OZK_KW_TAIL=0 disables the last-word shortcut (A/B builds).
+#ifndef OZK_KW_TAIL
+#define OZK_KW_TAIL 1
 #endif
 
 // kAccum: the accumulation acc += C_ab (slice-GEMM epilogues, accumulate.cu):
-// takes the kw_negligible exit first.
+// tries the last-word shortcut (kw_add_tail) first.
 template <int K, typename T = double, bool kIntCmp = true, bool kLead = false,
           bool kAccum = false>
 OZK_HD void kw_add(T* x, T y) {
@@ -510,8 +520,8 @@ OZK_HD void kw_add(T* x, T y) {
         // the reference sequence minus steps that are provably no-ops on
         // guarded inputs (kw_fast_ok); anything else takes the full sequence
         if (kw_fast_ok<K>(x, y)) {
-            if constexpr (kAccum && OZK_KW_NEGLIGIBLE)
-                if (kw_negligible<K, kIntCmp>(x, y)) return;
+            if constexpr (kAccum && OZK_KW_TAIL)
+                if (kw_add_tail<K, kIntCmp>(x, y)) return;
             kw_add_impl<K, kIntCmp, T, true, kLead>(x, y);
         } else {
             kw_add_full<K>(x, y);

@@ -339,26 +339,38 @@ def _accum_lib():
     return lib
 
 
-def _near_threshold(rng, x, K):
-    """Addends around ulp(x[K-1]) / 4 -- the negligible-addend exit's bound --
-    with both signs, exact powers of two, and x[K-1] itself a power of two."""
+def _tail_addends(rng, x, K):
+    """Addends for the last-word shortcut's bounds (kword.cuh kw_add_tail):
+    around ulp(x[K-1]) / 4 (h == x[K-1]), around ulp(x[K-2]) / 2 and |x[K-2]|
+    (where fl(x[K-2] + h) == x[K-2] stops holding and the merge order flips),
+    -x[K-1] (h == 0) and -x[K-1] plus a little, with both signs; some x[K-1]
+    become exact powers of two or zero."""
     n = x.shape[0]
-    e = np.frexp(np.abs(x[:, K - 1]))[1] - 1          # floor(log2 |x[K-1]|)
-    base = np.ldexp(1.0, e - 54)                     # ulp / 4 (binary64)
-    f = rng.choice([0.5, 0.999, 1.0, 1.0000001, 1.5, 2.0, 4.0, 2.0 ** -30, 3.0], n)
-    y = base * f * np.where(rng.random(n) < 0.5, -1.0, 1.0)
-    pw = rng.random(n) < 0.2                          # x[K-1] an exact power of two
-    x[pw, K - 1] = np.copysign(np.ldexp(1.0, e[pw]), x[pw, K - 1])
+    e1 = np.frexp(np.abs(x[:, K - 1]))[1] - 1
+    e2 = np.frexp(np.abs(x[:, K - 2]))[1] - 1
+    kind = rng.integers(0, 6, n)
+    f = rng.choice([0.5, 0.999, 1.0, 1.0000001, 1.5, 2.0, 2.0 ** -30, 3.0], n)
+    sgn = np.where(rng.random(n) < 0.5, -1.0, 1.0)
+    y = np.ldexp(1.0, e1 - 54) * f * sgn                       # ~ ulp(x[K-1]) / 4
+    y = np.where(kind == 1, np.ldexp(1.0, e2 - 53) * f * sgn, y)  # ~ ulp(x[K-2]) / 2
+    y = np.where(kind == 2, x[:, K - 2] * f * -sgn, y)           # ~ |x[K-2]|
+    y = np.where(kind == 3, -x[:, K - 1], y)                    # h == 0
+    y = np.where(kind == 4, -x[:, K - 1] * (1 + 2.0 ** -40) + np.ldexp(1.0, e1 - 80), y)
+    y = np.where(kind == 5, np.ldexp(1.0, (e1 + e2) // 2 - 53) * f * sgn, y)  # in between
+    pw = rng.random(n) < 0.15
+    x[pw, K - 1] = np.copysign(np.ldexp(1.0, e1[pw]), x[pw, K - 1])
+    z = rng.random(n) < 0.05
+    x[z, K - 1] = 0.0
     return y
 
 
 @pytest.mark.parametrize("K", [2, 3, 4])
-def test_accumulation_negligible_exit_matches_reference(ref, port, K):
-    """kw_add's accumulation flavour (kAccum: x + y == x taken without the
-    sequence when y is below a quarter ulp of x's last word and x is a strict
-    fixpoint, kword.cuh kw_negligible) equals the reference on fixpoints from
-    the reference itself, on addends straddling the bound, on power-of-two last
-    words, on non-fixpoint x (the check must refuse), and along long chains."""
+def test_accumulation_tail_shortcut_matches_reference(ref, port, K):
+    """kw_add's accumulation flavour (kAccum: the last-word shortcut of
+    kword.cuh kw_add_tail, taken when its conditions are checked true) equals
+    the reference on reference-produced fixpoints with addends straddling every
+    bound of the shortcut, on power-of-two and zero last words, on non-fixpoint
+    x (the checks must refuse), and along long Ozaki-shaped chains."""
     cpu = _checker(ref, port)
     lib = _accum_lib()
     rng = np.random.default_rng(97531 + K)
@@ -373,24 +385,24 @@ def test_accumulation_negligible_exit_matches_reference(ref, port, K):
         bad = np.flatnonzero((got.view(np.uint64) != want.view(np.uint64)).any(axis=1))
         assert bad.size == 0, (bad.size, x[bad[0]], y[bad[0]], got[bad[0]], want[bad[0]])
 
-    # reference outputs (fixpoints) with addends around the bound
-    x = cpu.gen_eq1(K, 400, 100, 77).reshape(-1, K).copy()
+    # reference outputs (fixpoints) with addends around every bound
+    x = cpu.gen_eq1(K, 500, 100, 77).reshape(-1, K).copy()
     x = cpu.mf_add_double(K, x, rng.standard_normal(x.shape[0]) * 2.0 ** -70)
-    run(x, _near_threshold(rng, x.copy(), K))
-    xp = x.copy()
-    y = _near_threshold(rng, xp, K)                   # power-of-two last words
-    run(xp, y)
+    for _ in range(4):
+        xx = x.copy()
+        run(xx, _tail_addends(rng, xx, K))
     # non-fixpoint x: adjacent words overlapping, sign patterns, zeros
     xn = x.copy()
-    sel = rng.integers(0, 4, xn.shape[0])
+    sel = rng.integers(0, 5, xn.shape[0])
     xn[sel == 0, K - 1] = xn[sel == 0, K - 2] * 0.75
     xn[sel == 1, 1] = -xn[sel == 1, 1] * 2.0 ** 60
     xn[sel == 2, K - 2] = 0.0
-    run(xn, _near_threshold(rng, xn.copy(), K))
+    xn[sel == 3, 0] = xn[sel == 3, 1] * 0.5
+    run(xn, _tail_addends(rng, xn.copy(), K))
     # chains: acc += C_p with the Ozaki magnitudes 2^-20 per level
     acc_a = np.zeros((20000, K))
     acc_b = np.zeros((20000, K))
-    for p in range(6 * (4 + 3 * K)):  # levels 0 .. 3K+3: past the last word's quarter ulp
+    for p in range(6 * (4 + 3 * K)):  # levels 0 .. 3K+3: past the last word
         y = rng.standard_normal(20000) * 2.0 ** (-20 * (p // 6))
         got = np.empty_like(acc_a)
         assert lib.kw_host_add_accum(K, acc_a.shape[0], acc_a.ctypes.data, y.ctypes.data,
@@ -400,7 +412,7 @@ def test_accumulation_negligible_exit_matches_reference(ref, port, K):
         assert np.array_equal(acc_a.view(np.uint64), acc_b.view(np.uint64)), p
 
 
-def test_accumulation_negligible_exit_ts(port):
+def test_accumulation_tail_shortcut_ts(port):
     lib = _accum_lib()
     rng = np.random.default_rng(8642)
     acc_a = np.zeros((8000, 3), dtype=np.float32)
