@@ -370,6 +370,42 @@ __device__ __forceinline__ double ldexp_fast(double y, int e) {
     return scalbn(y, e);
 }
 
+// The exact slice product s * 2^e (s: the recombined int64 level sum, exact in
+// W: |s| < 2^53 for binary64, < 2^24 for the TS products) built with integer
+// operations only: leading-one position, mantissa shift, exponent field.  The
+// FP64 pipe is the one the epilogue contends on with the tensor cores, and this
+// replaces the two-DADD + FMA conversion and the scaling multiply.  Results
+// that would be subnormal or overflow (and any |s| too wide) take the
+// floating-point path, so the value is identical either way.
+#ifndef OZK_I8_INTCONV
+#define OZK_I8_INTCONV 1
+#endif
+template <typename W>
+__device__ __forceinline__ W scaled_int_to(long long s, int e) {
+    constexpr int M = sizeof(W) == 8 ? 52 : 23;
+    constexpr int B = sizeof(W) == 8 ? 1023 : 127;
+    if (s == 0) return W(0);
+    const unsigned long long a = s < 0 ? 0ull - (unsigned long long)s : (unsigned long long)s;
+    const int msb = 63 - __clzll((long long)a);
+    const int be = msb + e + B;
+    if (msb > M || be <= 0 || be >= 2 * B + 1) return (W)ldexp_fast(i64_to_f64_exact(s), e);
+    const unsigned long long m = (a << (M - msb)) & ((1ull << M) - 1);
+    if constexpr (sizeof(W) == 8) {
+        const unsigned long long bits =
+            (s < 0 ? (1ull << 63) : 0ull) | ((unsigned long long)be << 52) | m;
+        return __longlong_as_double((long long)bits);
+    } else {
+        const unsigned bits = (s < 0 ? 0x80000000u : 0u) | ((unsigned)be << 23) | (unsigned)m;
+        return __uint_as_float(bits);
+    }
+}
+using ProdT = long long;  // the exact integer slice product as read from TMEM
+template <typename W>
+__device__ __forceinline__ W scale_prod(ProdT s, int e) {
+    if constexpr (OZK_I8_INTCONV) return scaled_int_to<W>(s, e);
+    else return (W)ldexp_fast(i64_to_f64_exact(s), e);
+}
+
 // C accesses with an L2 eviction-priority hint (OZK_I8_CHINT >= 1: C loads and
 // stores evict_last; 2: also the operand TMA loads evict_first).  Off: with
 // wave pacing both measured within noise / worse (n=8192 DD/TD/QD: evict_last
@@ -823,7 +859,7 @@ pair_gemm_i8_kernel(const __grid_constant__ MapsI8 maps, const __grid_constant__
                 };
                 // levels of rows [r, r + N) recombined to the exact binary64 products
                 auto read_levels = [&](int r, auto& y, uint32_t tbuf) {
-                    constexpr int N = sizeof(y) / sizeof(double);
+                    constexpr int N = sizeof(y) / sizeof(ProdT);
                     int32_t lv[kLevels][N];
 #pragma unroll
                     for (int u = 0; u < kLevels; ++u) tmem_ld<N>(tbuf + u * TR + r, lv[u]);
@@ -833,17 +869,17 @@ pair_gemm_i8_kernel(const __grid_constant__ MapsI8 maps, const __grid_constant__
                         long long sum = lv[0][j];
 #pragma unroll
                         for (int u = 1; u < kLevels; ++u) sum += (long long)lv[u][j] << (8 * u);
-                        y[j] = i64_to_f64_exact(sum);  // exact: |sum| < 2^53
+                        y[j] = sum;  // the exact integer slice product (|sum| < 2^53)
                     }
                 };
                 // NB == 1: drain every level of this thread's rows, then release TMEM
                 // so the next pair's MMAs start while the K-word updates run
-                double yall[NB == 1 ? kEpiRows : 1];
+                ProdT yall[NB == 1 ? kEpiRows : 1];
                 if constexpr (NB == 1) {
 #pragma unroll
                     for (int r = 0; r < kEpiRows; r += (kEpiRows % 16 == 0 ? 16 : 4)) {
-                        double (&ys)[kEpiRows % 16 == 0 ? 16 : 4] =
-                            *reinterpret_cast<double (*)[kEpiRows % 16 == 0 ? 16 : 4]>(yall + r);
+                        ProdT (&ys)[kEpiRows % 16 == 0 ? 16 : 4] =
+                            *reinterpret_cast<ProdT (*)[kEpiRows % 16 == 0 ? 16 : 4]>(yall + r);
                         read_levels(r, ys, tbufq[0]);
                     }
 #if !(defined(OZK_I8_EPI_MODE) && OZK_I8_EPI_MODE == 3)
@@ -853,7 +889,7 @@ pair_gemm_i8_kernel(const __grid_constant__ MapsI8 maps, const __grid_constant__
 #endif
                 }
                 auto update_chunk = [&](int r, W (&w)[kChunk][K]) {
-                    double yc[PG][kChunk];
+                    ProdT yc[PG][kChunk];
                     if constexpr (NB == 1) {
                         // this chunk's products are yall[0..kChunk); shift the rest
                         // down so every register index stays static
@@ -871,21 +907,21 @@ pair_gemm_i8_kernel(const __grid_constant__ MapsI8 maps, const __grid_constant__
 #pragma unroll
                         for (int q = 0; q < PG; ++q) {
                             if (q >= np) break;
-                            const double y = yc[q][j];
+                            const ProdT y = yc[q][j];
                             const int ga = __ldg(gapq[q] + row_of(r + j));
                             if constexpr (PR) {
                                 const size_t rr = row0 + r + j;
                                 if (col_ok && rr < prob.m)
                                     static_cast<double*>(prob.c)[(size_t)(p + q) * prob.pair_stride +
                                                                  rr * prob.ldc + col] =
-                                        ldexp_fast(y, ga + gbq[q]);
+                                        scale_prod<double>(y, ga + gbq[q]);
                                 continue;
                             }
                             // exact scaled slice product (a TS product is exact in binary32)
 #if defined(OZK_I8_EPI_MODE) && OZK_I8_EPI_MODE == 2
-                            w[j][0] += (W)ldexp_fast(y, ga + gbq[q]);  // diagnostic: no K-word add
+                            w[j][0] += scale_prod<W>(y, ga + gbq[q]);  // diagnostic: no K-word add
 #else
-                            kw_add<K, W, kEpiIntCmp, false, true>(w[j], (W)ldexp_fast(y, ga + gbq[q]));
+                            kw_add<K, W, kEpiIntCmp, false, true>(w[j], scale_prod<W>(y, ga + gbq[q]));
 #endif
                         }
                     }
