@@ -377,8 +377,11 @@ __device__ __forceinline__ double ldexp_fast(double y, int e) {
 // replaces the two-DADD + FMA conversion and the scaling multiply.  Results
 // that would be subnormal or overflow (and any |s| too wide) take the
 // floating-point path, so the value is identical either way.
+// Off: same-box A/B (profiles/r02_variants_intconv.log) measured it no faster
+// for TD/QD/DD and 3 % slower for TS -- the extra integer instructions cost more
+// issue slots than the four FP64 operations they replace save.
 #ifndef OZK_I8_INTCONV
-#define OZK_I8_INTCONV 1
+#define OZK_I8_INTCONV 0
 #endif
 template <typename W>
 __device__ __forceinline__ W scaled_int_to(long long s, int e) {

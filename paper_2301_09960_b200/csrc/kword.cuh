@@ -505,7 +505,29 @@ OZK_HD bool kw_add_tail(T* x, T y) {
     return ok;
 }
 
-// OZK_KW_TAIL=0 disables the last-word shortcut (A/B builds).
+// The K = 2 form (multifloat.hpp:203-207 + from_pair :384-392): with x[0], y
+// nonzero, all words finite below the guard, fl(x[0] + y) == x[0] and, for
+// v = fl(x[1] + y), fl(x[0] + v) == x[0], the reference returns (x[0], v):
+// two_sum(x[0], y) = (x[0], y) (fl(a+b) == a gives the exact error b for
+// b != 0), so its v = x[1] + e is this v; fast_two_sum(x[0], v) = (x[0], v),
+// and from_pair's second fast_two_sum and zero rules leave (x[0], v) (a zero v
+// is +0: x[1] + y == 0 rounds to +0).
+template <bool kInt, typename T>
+OZK_HD bool kw_add_tail2(T* x, T y) {
+    constexpr uint32_t kSafeHi = (uint32_t)(Bits<T>::kSafe >> (sizeof(T) == 8 ? 32 : 0));
+    const bool guard = (hi_word(x[0]) & 0x7fffffffu) < kSafeHi &&
+                       (hi_word(x[1]) & 0x7fffffffu) < kSafeHi &&
+                       (hi_word(y) & 0x7fffffffu) < kSafeHi;
+    if (!guard || is_zero<kInt>(x[0]) || is_zero<kInt>(y) ||
+        !same<kInt>(rn_add(x[0], y), x[0]))
+        return false;
+    const T v = rn_add(x[1], y);
+    if (!same<kInt>(rn_add(x[0], v), x[0])) return false;
+    x[1] = v;
+    return true;
+}
+
+// OZK_KW_TAIL=0 disables the last-word shortcuts (A/B builds).
 #ifndef OZK_KW_TAIL
 #define OZK_KW_TAIL 1
 #endif
@@ -529,6 +551,8 @@ OZK_HD void kw_add(T* x, T y) {
         return;
     }
 #endif
+    if constexpr (K == 2 && kAccum && OZK_KW_TAIL)
+        if (kw_add_tail2<kIntCmp>(x, y)) return;
     kw_add_impl<K, false>(x, y);
 }
 
