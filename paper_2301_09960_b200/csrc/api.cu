@@ -363,6 +363,34 @@ std::vector<size_t> plan_bands_uncached(int fmt, size_t m, size_t n, size_t l, i
     return starts;
 }
 
+// 2-D head schedule (HostOverlap::head_bands): h head bands of one wave per B
+// block each (rows = cluster rows x floor(clusters / tiles per block)), then
+// the remaining rows planned as above for full-width bands.  Returns the band
+// starts; the number of head bands actually used is written to *heads.
+std::vector<size_t> plan_head_bands(int fmt, size_t m, size_t n, size_t l, int d,
+                                    size_t block_cols, const I8Geometry& g, int h, int* heads) {
+    *heads = 0;
+    std::vector<size_t> starts{0};
+    const size_t tb = (block_cols + g.group_cols - 1) / g.group_cols;
+    if (h < 2 || g.clusters <= 0 || tb == 0) return starts;
+    const size_t rb = (size_t)g.group_rows * std::max<size_t>(1, (size_t)g.clusters / tb);
+    size_t acc = 0;
+    for (int q = 0; q < h && acc + rb < m; ++q) {
+        acc += rb;
+        starts.push_back(acc);
+        ++*heads;
+    }
+    if (*heads < 2) {
+        *heads = 0;
+        return {0};
+    }
+    const size_t m_tail = m - acc;
+    const std::vector<size_t> tail = plan_bands_uncached(fmt, m_tail, n, l, d, n, g);
+    for (size_t q = 1; q < tail.size(); ++q) starts.push_back(acc + tail[q]);
+    if (starts.back() != m) starts.push_back(m);
+    return starts;
+}
+
 std::vector<size_t> plan_bands(int fmt, size_t m, size_t n, size_t l, int d, size_t block_cols,
                                const I8Geometry& g, size_t band0_rows = 0) {
     static std::mutex mu;
@@ -405,6 +433,12 @@ struct HostOverlap {
     int b_blocks = 1;
     size_t b_block_cols = 0;
     const cudaEvent_t* b_block_ready = nullptr;
+    // optional (with B blocks): bands [0, head_bands) are "head" bands whose A
+    // rows arrive interleaved with the B blocks -- A0, B0, B1, A1, B2, A2, ...
+    // -- and every (head band, B block) product is multiplied as soon as both
+    // are in; the remaining bands follow full width.  0: only band 0 is
+    // multiplied block by block.
+    int head_bands = 0;
     // optional: called before every wait on one of the events above (pageable
     // buffers: blocks until the staging worker has recorded it)
     std::function<cudaError_t(cudaEvent_t)> before_wait;
@@ -534,6 +568,108 @@ ozk_status ozaki_device_impl(int fmt, size_t m, size_t l, size_t n, const void* 
     const size_t eb = elem_bytes(fmt);
     std::vector<std::unique_ptr<Timer>> split_timers;  // per-band A / per-block B splits (profile)
     int band = 0;
+    // C rows [r0, r0 + rows) x columns [c0, c0 + w) on the INT8 engine
+    auto gemm_block = [&](size_t r0, size_t rows, size_t c0, size_t w) -> cudaError_t {
+        I8Operands op{};
+        op.nd = nd;
+        op.a = da8.as<int8_t>() + r0 * ld8;
+        op.a_ld = ld8;
+        op.a_digit_stride = m * ld8;
+        op.a_slice_stride = (size_t)nd * m * ld8;
+        op.b = db8.as<int8_t>() + c0 * ld8;
+        op.b_ld = ld8;
+        op.b_digit_stride = n * ld8;
+        op.b_slice_stride = (size_t)nd * n * ld8;
+        op.gA = ga.as<int>() + r0;
+        op.gB = gb.as<int>() + c0;
+        op.gA_stride = m;
+        op.gB_stride = n;
+        op.m = rows;
+        op.n = w;
+        op.l = l;
+        op.d = d;
+        op.c = static_cast<char*>(c) + (r0 * n + c0) * eb;
+        op.ldc = n;
+        return launch_pair_gemm_i8(K, wb, op, pl, st, sms);
+    };
+    auto split_a_band = [&](size_t r0, size_t rows) -> cudaError_t {
+        // per-row split, identical to the rows of the whole-matrix split
+        // (ozaki.hpp:102-103)
+        DigitOut dband = digA;
+        if (use_i8) {
+            dband.digits += r0 * ld8;
+            dband.exps += r0;
+        }
+        split_timers.push_back(std::make_unique<Timer>(prof != nullptr));
+        split_timers.back()->mark(0, st);
+        const cudaError_t e =
+            split_to_slices(fmt, rows, l, lda, static_cast<const char*>(a) + r0 * lda * eb, d,
+                            OZK_SIDE_ROWS, use_i8 ? nullptr : sa.as<double>() + r0 * ldk, m,
+                            work.p, nullptr, err, st, dband);
+        split_timers.back()->mark(1, st);
+        return e;
+    };
+    auto split_b_block = [&](size_t c0, size_t w) -> cudaError_t {
+        // per-column split of B's columns [c0, c0 + w) (ozaki.hpp:102-103)
+        DigitOut dblk = digB;
+        dblk.digits += c0 * ld8;
+        dblk.exps += c0;
+        split_timers.push_back(std::make_unique<Timer>(prof != nullptr));
+        split_timers.back()->mark(0, st);
+        const cudaError_t e =
+            split_to_slices(fmt, l, w, ldb, static_cast<const char*>(b) + c0 * eb, d,
+                            OZK_SIDE_COLS, nullptr, n, work.p, nullptr, errB, st, dblk);
+        split_timers.back()->mark(1, st);
+        return e;
+    };
+    if (blocked_b && pl.count > 0 && ov->head_bands > 1) {
+        // 2-D head: A bands and B blocks arrive interleaved (A0, B0, B1, A1,
+        // B2, A2, ...); each arrival is split and multiplied against every
+        // block / band already in, so the GEMM work available grows with the
+        // product of what has crossed PCIe.  C elements are independent:
+        // bit-identical to one GEMM.
+        const int nb = ov->b_blocks, nh = std::min(ov->head_bands, bands);
+        auto blk = [&](int j, size_t& c0, size_t& w) {
+            c0 = std::min(n, (size_t)j * ov->b_block_cols);
+            w = std::min(ov->b_block_cols, n - c0);
+        };
+        int a_in = 0, b_in = 0;  // arrived head bands / B blocks
+        auto arrive_a = [&](int q) -> cudaError_t {
+            const size_t r0 = ov->band_start[q], rows = ov->band_start[q + 1] - r0;
+            cudaError_t e = ov->wait(st, ov->a_ready[q]);
+            if (e == cudaSuccess && rows) e = split_a_band(r0, rows);
+            for (int j = 0; j < b_in && e == cudaSuccess; ++j) {
+                size_t c0, w;
+                blk(j, c0, w);
+                if (rows && w) e = gemm_block(r0, rows, c0, w);
+            }
+            a_in = q + 1;
+            return e;
+        };
+        auto arrive_b = [&](int j) -> cudaError_t {
+            size_t c0, w;
+            blk(j, c0, w);
+            cudaError_t e = ov->wait(st, ov->b_block_ready[j]);
+            if (e == cudaSuccess && w) e = split_b_block(c0, w);
+            for (int q = 0; q < a_in && e == cudaSuccess; ++q) {
+                const size_t r0 = ov->band_start[q], rows = ov->band_start[q + 1] - r0;
+                if (rows && w) e = gemm_block(r0, rows, c0, w);
+            }
+            b_in = j + 1;
+            return e;
+        };
+        OZK_CUDA(arrive_a(0), "ozaki_gemm: head band");
+        OZK_CUDA(arrive_b(0), "ozaki_gemm: head block");
+        for (int k = 1; k < std::max(nb, nh); ++k) {
+            if (k < nb) OZK_CUDA(arrive_b(k), "ozaki_gemm: head block");
+            if (k < nh) OZK_CUDA(arrive_a(k), "ozaki_gemm: head band");
+        }
+        for (int q = 0; q < nh; ++q)  // head bands complete: their C rows go back
+            if (ov->on_band)
+                OZK_CUDA(ov->on_band(ov->band_start[q], ov->band_start[q + 1]),
+                         "ozaki_gemm: band copy");
+        band = nh;
+    }
     for (; band < bands; ++band) {
         size_t r0 = 0, r1 = m;
         if (bands > 1) {
@@ -544,50 +680,15 @@ ozk_status ozaki_device_impl(int fmt, size_t m, size_t l, size_t n, const void* 
         if (rows == 0) continue;
         char* cb = static_cast<char*>(c) + r0 * n * eb;
         if (banded_a) {
-            // this band's A rows: per-row split, identical to the rows of the
-            // whole-matrix split (ozaki.hpp:102-103)
             OZK_CUDA(ov->wait(st, ov->a_ready[band]), "ozaki_gemm: wait A");
-            DigitOut dband = digA;
-            if (use_i8) {
-                dband.digits += r0 * ld8;
-                dband.exps += r0;
-            }
-            split_timers.push_back(std::make_unique<Timer>(prof != nullptr));
-            split_timers.back()->mark(0, st);
-            OZK_CUDA(split_to_slices(fmt, rows, l, lda,
-                                     static_cast<const char*>(a) + r0 * lda * eb, d,
-                                     OZK_SIDE_ROWS, use_i8 ? nullptr : sa.as<double>() + r0 * ldk,
-                                     m, work.p, nullptr, err, st, dband),
-                     "ozaki_gemm: split A band");
-            split_timers.back()->mark(1, st);
+            OZK_CUDA(split_a_band(r0, rows), "ozaki_gemm: split A band");
         }
         if (pl.count == 0) {  // every pair pruned (drop_threshold > 1): C = 0
             OZK_CUDA(cudaMemsetAsync(cb, 0, eb * rows * n, st), "ozaki_gemm: zero C");
+            if (blocked_b && band == 0)  // the B blocks still arrive in order (nothing to split)
+                for (int j = 0; j < ov->b_blocks; ++j)
+                    OZK_CUDA(ov->wait(st, ov->b_block_ready[j]), "ozaki_gemm: wait B");
         } else if (use_i8) {
-            // C rows [r0, r0+rows) x columns [c0, c0+w)
-            auto gemm_cols = [&](size_t c0, size_t w) -> cudaError_t {
-                I8Operands op{};
-                op.nd = nd;
-                op.a = da8.as<int8_t>() + r0 * ld8;
-                op.a_ld = ld8;
-                op.a_digit_stride = m * ld8;
-                op.a_slice_stride = (size_t)nd * m * ld8;
-                op.b = db8.as<int8_t>() + c0 * ld8;
-                op.b_ld = ld8;
-                op.b_digit_stride = n * ld8;
-                op.b_slice_stride = (size_t)nd * n * ld8;
-                op.gA = ga.as<int>() + r0;
-                op.gB = gb.as<int>() + c0;
-                op.gA_stride = m;
-                op.gB_stride = n;
-                op.m = rows;
-                op.n = w;
-                op.l = l;
-                op.d = d;
-                op.c = cb + c0 * eb;
-                op.ldc = n;
-                return launch_pair_gemm_i8(K, wb, op, pl, st, sms);
-            };
             if (blocked_b && band == 0) {
                 // B column blocks: split each as it lands, then its GEMM block
                 for (int j = 0; j < ov->b_blocks; ++j) {
@@ -595,20 +696,11 @@ ozk_status ozaki_device_impl(int fmt, size_t m, size_t l, size_t n, const void* 
                     if (c0 >= n) break;
                     const size_t w = n - c0 < ov->b_block_cols ? n - c0 : ov->b_block_cols;
                     OZK_CUDA(ov->wait(st, ov->b_block_ready[j]), "ozaki_gemm: wait B");
-                    DigitOut dblk = digB;
-                    dblk.digits += c0 * ld8;
-                    dblk.exps += c0;
-                    split_timers.push_back(std::make_unique<Timer>(prof != nullptr));
-                    split_timers.back()->mark(0, st);
-                    OZK_CUDA(split_to_slices(fmt, l, w, ldb, static_cast<const char*>(b) + c0 * eb,
-                                             d, OZK_SIDE_COLS, nullptr, n, work.p, nullptr, errB,
-                                             st, dblk),
-                             "ozaki_gemm: split B block");
-                    split_timers.back()->mark(1, st);
-                    OZK_CUDA(gemm_cols(c0, w), "ozaki_gemm: INT8 slice GEMM");
+                    OZK_CUDA(split_b_block(c0, w), "ozaki_gemm: split B block");
+                    OZK_CUDA(gemm_block(r0, rows, c0, w), "ozaki_gemm: INT8 slice GEMM");
                 }
             } else {
-                OZK_CUDA(gemm_cols(0, n), "ozaki_gemm: INT8 slice GEMM");
+                OZK_CUDA(gemm_block(r0, rows, 0, n), "ozaki_gemm: INT8 slice GEMM");
             }
         } else {
             GemmProblem pb = prob;
@@ -791,7 +883,15 @@ ozk_status ozk_ozaki_gemm(ozk_format fmt, size_t m, size_t l, size_t n, const vo
                                    int8_digits((int)fmt, l, d), num_sms_cached())
            : I8Geometry{};
     std::vector<size_t> band_start;
-    if (i8) {
+    // $OZK_HOST_HEAD = h >= 2: the 2-D head schedule with h head bands
+    int head = 0;
+    if (const char* v = std::getenv("OZK_HOST_HEAD")) head = std::max(0, std::atoi(v));
+    int heads = 0;
+    if (i8 && blockable && head >= 2)
+        band_start = plan_head_bands((int)fmt, m, n, l, d, b_block_cols, geo, head, &heads);
+    if (heads >= 2) {
+        // planned above
+    } else if (i8) {
         band_start = plan_bands((int)fmt, m, n, l, d, b_block_cols, geo, band0_rows);
     } else {
         const size_t nb = m >= 2048 ? 8 : 1;
@@ -842,21 +942,33 @@ ozk_status ozk_ozaki_gemm(ozk_format fmt, size_t m, size_t l, size_t n, const vo
         return h2d(a_pg, static_cast<char*>(da.p) + r0 * l * eb, 0,
                    static_cast<const char*>(a) + r0 * l * eb, 0, rows * l * eb, 1, a_ready[q]);
     };
-    if (b_blocks > 1) {
+    auto copy_b_block = [&](int j) -> cudaError_t {
+        const size_t c0 = std::min(n, (size_t)j * b_block_cols);
+        const size_t w = std::min(b_block_cols, n - c0);
+        return h2d(b_pg, static_cast<char*>(db.p) + c0 * eb, n * eb,
+                   static_cast<const char*>(b) + c0 * eb, n * eb, w * eb, l, b_block_ready[j]);
+    };
+    int next_a = 0;  // first A band not yet queued
+    if (b_blocks > 1 && heads >= 2) {
+        // 2-D head: A0, B0, B1, A1, B2, A2, ... (ozaki_device_impl multiplies
+        // each arrival against everything already in, in this order)
         OZK_CUDA(copy_a_band(0), "ozaki_gemm: H2D A");
-        for (int j = 0; j < b_blocks; ++j) {
-            const size_t c0 = (size_t)j * b_block_cols;
-            const size_t w = n - c0 < b_block_cols ? n - c0 : b_block_cols;
-            OZK_CUDA(h2d(b_pg, static_cast<char*>(db.p) + c0 * eb, n * eb,
-                         static_cast<const char*>(b) + c0 * eb, n * eb, w * eb, l,
-                         b_block_ready[j]),
-                     "ozaki_gemm: H2D B block");
+        OZK_CUDA(copy_b_block(0), "ozaki_gemm: H2D B block");
+        for (int k = 1; k < std::max(b_blocks, heads); ++k) {
+            if (k < b_blocks) OZK_CUDA(copy_b_block(k), "ozaki_gemm: H2D B block");
+            if (k < heads) OZK_CUDA(copy_a_band(k), "ozaki_gemm: H2D A");
         }
         OZK_CUDA(h2d(b_pg, nullptr, 0, nullptr, 0, 0, 0, b_ready), "ozaki_gemm: event");
+        next_a = heads;
+    } else if (b_blocks > 1) {
+        OZK_CUDA(copy_a_band(0), "ozaki_gemm: H2D A");
+        for (int j = 0; j < b_blocks; ++j) OZK_CUDA(copy_b_block(j), "ozaki_gemm: H2D B block");
+        OZK_CUDA(h2d(b_pg, nullptr, 0, nullptr, 0, 0, 0, b_ready), "ozaki_gemm: event");
+        next_a = 1;
     } else {
         OZK_CUDA(h2d(b_pg, db.p, 0, b, 0, eb * l * n, 1, b_ready), "ozaki_gemm: H2D B");
     }
-    for (int q = b_blocks > 1 ? 1 : 0; q < bands; ++q) OZK_CUDA(copy_a_band(q), "ozaki_gemm: H2D A");
+    for (int q = next_a; q < bands; ++q) OZK_CUDA(copy_a_band(q), "ozaki_gemm: H2D A");
     HostOverlap ov;
     ov.b_ready = b_ready;
     ov.bands = bands;
@@ -866,6 +978,7 @@ ozk_status ozk_ozaki_gemm(ozk_format fmt, size_t m, size_t l, size_t n, const vo
         ov.b_blocks = b_blocks;
         ov.b_block_cols = b_block_cols;
         ov.b_block_ready = b_block_ready.data();
+        ov.head_bands = heads;
     }
     if (hs)
         ov.before_wait = [&](cudaEvent_t ev) -> cudaError_t {

@@ -525,13 +525,16 @@ def test_direct_gemm_spread_inputs(ozk, ref, port):
                                             (4, 2100, 130, 40, 12, 0.0), (2, 4097, 100, 33, 6, 0.0),
                                             (3, 2048, 140, 4101, 3, 0.0), (2, 2050, 300, 4352, 4, 0.0),
                                             (4, 2048, 129, 4096, 2, 0.0), (2, 2048, 200, 4100, 3, 2.0 ** -60)])
-def test_host_api_banded_overlap(ozk, cpu, K, m, l, n, d, drop):
+@pytest.mark.parametrize("head", [0, 4])
+def test_host_api_banded_overlap(ozk, cpu, monkeypatch, head, K, m, l, n, d, drop):
     """ozk_ozaki_gemm with host buffers at m >= 2048 runs the banded, transfer-
     overlapped schedule (B first, A + slice GEMM in 8 row bands, C copied back
     per band; drop > 0 keeps the whole-matrix A split); at n >= 4096 on the INT8
     engine B also arrives in 4 column blocks, each split as it lands, and the
     first band is multiplied block by block (ragged last block included):
     bit-identical."""
+    if head:
+        monkeypatch.setenv("OZK_HOST_HEAD", str(head))
     a = cpu.gen_eq1(K, m, l, 90 + K)
     b = cpu.gen_eq1(K, l, n, 91 + K)
     want = cpu.ozaki_gemm(K, a, b, d, drop)
@@ -785,8 +788,8 @@ def test_accumulate_products_matches_reference(ozk, cpu, port):
     assert (zero == 0).all()
 
 
-@pytest.mark.parametrize("n", [4200, 8320])
-def test_host_api_pinned_and_pageable_agree(ozk, cpu, monkeypatch, n):
+@pytest.mark.parametrize("n,head", [(4200, 0), (8320, 0), (8320, 4), (4200, 3)])
+def test_host_api_pinned_and_pageable_agree(ozk, cpu, monkeypatch, n, head):
     """ozk_ozaki_gemm's host path with every mix of pinned (page-locked) and
     pageable caller buffers -- pageable ones are staged through pinned slots on
     worker threads (csrc/staging.cu), strided B column blocks included -- and
@@ -796,6 +799,8 @@ def test_host_api_pinned_and_pageable_agree(ozk, cpu, monkeypatch, n):
 
     import torch
     K, m, l, d = 3, 2304, 300, 4   # n = 8320: 8 ragged B column blocks
+    if head:  # the 2-D head schedule: A bands interleaved with the B blocks
+        monkeypatch.setenv("OZK_HOST_HEAD", str(head))
     a = cpu.gen_eq1(K, m, l, 31)
     b = cpu.gen_eq1(K, l, n, 32)
     pa, pb = torch.from_numpy(a).pin_memory(), torch.from_numpy(b).pin_memory()

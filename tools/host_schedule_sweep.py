@@ -23,10 +23,11 @@ hc = torch.empty_like(ha).pin_memory()
 assert lib.ozk_gen_eq1(fmt, n, n, 1, ha.data_ptr(), 0) == 0
 assert lib.ozk_gen_eq1(fmt, n, n, 2, hb.data_ptr(), 0) == 0
 ref = None
-settings = [("4", ""), ("8", ""), ("8", "1728"), ("8", "1152"), ("8", "2304"), ("4", "1728"),
-            ("16", "1728"), ("4", "")]
-for bb, b0 in settings:
+settings = [("8", "", "0"), ("8", "", "2"), ("8", "", "4"), ("8", "", "6"), ("8", "", "8"),
+            ("4", "", "4"), ("16", "", "8"), ("8", "", "0")]
+for bb, b0, head in settings:
     os.environ["OZK_HOST_BBLOCKS"] = bb
+    os.environ["OZK_HOST_HEAD"] = head
     if b0:
         os.environ["OZK_HOST_BAND0"] = b0
     else:
@@ -43,5 +44,5 @@ for bb, b0 in settings:
     if ref is None:
         ref = iv.clone()
     ms = 1e3 * statistics.median(ts)
-    print(f"bblocks={bb} band0={b0 or 'planner'}: {ms:.1f} ms {2 * n ** 3 / ms / 1e6:.0f} "
+    print(f"bblocks={bb} band0={b0 or 'planner'} head={head}: {ms:.1f} ms {2 * n ** 3 / ms / 1e6:.0f} "
           f"GFLOP/s{same}", flush=True)
