@@ -242,9 +242,11 @@ class ShardedOzaki:
                         self._gather(self.b8_cat[s, t], self.b8[s, t])
                     self._gather(self.gb_cat[s], self.gb[s])
 
+            # (torch's fast path: a block of only all_gather_into_tensor calls
+            # becomes one allgather_into_tensor_coalesced = one NCCL group)
             cm = getattr(dist, "_coalescing_manager", None)
             if cm is not None and dist.get_backend(self.group) == "nccl":
-                with cm(group=self.group, device=self.b8.device):
+                with cm(group=self.group):
                     planes()
             else:
                 planes()
