@@ -403,10 +403,28 @@ __device__ __forceinline__ W scaled_int_to(long long s, int e) {
     }
 }
 using ProdT = long long;  // the exact integer slice product as read from TMEM
+// TS (binary32 words): the product fits 24 bits (it is exact in binary32), so
+// it converts exactly with one I2F and scales exactly with one FMUL by a
+// bit-built power of two whenever the result is a normal float -- no FP64 in
+// the TS epilogue.  Subnormal results, exponents outside the binary32 range and
+// wider integers take the binary64 path, so the value is identical either way.
+#ifndef OZK_I8_TS_F32CONV
+#define OZK_I8_TS_F32CONV 1
+#endif
 template <typename W>
 __device__ __forceinline__ W scale_prod(ProdT s, int e) {
-    if constexpr (OZK_I8_INTCONV) return scaled_int_to<W>(s, e);
-    else return (W)ldexp_fast(i64_to_f64_exact(s), e);
+    if constexpr (sizeof(W) == 4 && OZK_I8_TS_F32CONV) {
+        if (s > -(1ll << 24) && s < (1ll << 24) && e >= -126 && e <= 127) {
+            const float p = __fmul_rn(__ll2float_rn(s), __uint_as_float((unsigned)(e + 127) << 23));
+            const unsigned bits = __float_as_uint(p);
+            if ((bits & 0x7f800000u) != 0u || (bits & 0x7fffffffu) == 0u) return p;  // normal or 0
+        }
+        return (W)ldexp_fast(i64_to_f64_exact(s), e);
+    } else if constexpr (OZK_I8_INTCONV) {
+        return scaled_int_to<W>(s, e);
+    } else {
+        return (W)ldexp_fast(i64_to_f64_exact(s), e);
+    }
 }
 
 // C accesses with an L2 eviction-priority hint (OZK_I8_CHINT >= 1: C loads and
