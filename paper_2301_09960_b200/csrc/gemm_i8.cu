@@ -408,8 +408,9 @@ using ProdT = long long;  // the exact integer slice product as read from TMEM
 // bit-built power of two whenever the result is a normal float -- no FP64 in
 // the TS epilogue.  Subnormal results, exponents outside the binary32 range and
 // wider integers take the binary64 path, so the value is identical either way.
+// Off: neutral on the B200 (TS D=15 -0.8 %, D=12 +1.3 %, profiles/r02_variants_tsconv.log).
 #ifndef OZK_I8_TS_F32CONV
-#define OZK_I8_TS_F32CONV 1
+#define OZK_I8_TS_F32CONV 0
 #endif
 template <typename W>
 __device__ __forceinline__ W scale_prod(ProdT s, int e) {
