@@ -1,7 +1,7 @@
 """Split-count sweep at n = 8192: effective GFLOP/s of
 the INT8 engine for DD D=4..8, TD D=7..11, QD D=9..14 (median of 2 after a
 warm-up), one JSON object per line.  python tools/d_sweep.py [n] [K:lo-hi,...]
-(e.g. `4096 2:2-10` = BASELINE config 1, DD n=4096 with the split count swept)."""
+(e.g. `4096 2:2-10` = BASELINE config 2, DD n=4096 with the split count swept)."""
 import ctypes
 import json
 import statistics
@@ -21,11 +21,12 @@ if len(sys.argv) > 2:
                                                int(f.split(":")[1].split("-")[1]) + 1))
                  for f in sys.argv[2].split(","))
 for K, ds in plan:
-    A = torch.empty((n, n, K), dtype=torch.float64, device="cuda")
+    A = torch.empty((n, n, K), dtype=torch.float64)
     B = torch.empty_like(A)
+    lib.ozk_gen_eq1(K, n, n, 1, A.data_ptr(), 0)  # the reference's inputs (bench.cpp:111-112)
+    lib.ozk_gen_eq1(K, n, n, 2, B.data_ptr(), 0)
+    A, B = A.cuda(), B.cuda()
     C = torch.empty_like(A)
-    lib.ozk_gen_eq1_device(K, n, n, 1, A.data_ptr(), sh)
-    lib.ozk_gen_eq1_device(K, n, n, 2, B.data_ptr(), sh)
     for d in ds:
         ts, tk = [], []
         prof = OzkProfile()
