@@ -353,7 +353,7 @@ def unpin():
     return len(HOST_CPUS) if HOST_CPUS else (os.cpu_count() or 1)
 
 
-def host_inputs(lib, code, K, wdt, n, spread, rows=None, pin=True):
+def host_inputs(lib, code, K, wdt, n, spread, pin=True):
     """gen_matrix_eq1<K>(n, n, 1) and (n, n, 2) (or the config-5 spread variant)
     from the library's host generator, into (pinned) CPU tensors."""
     import torch

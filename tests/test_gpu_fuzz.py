@@ -84,3 +84,26 @@ def test_random_gemm_bitexact_multi_tile(ozk, cpu, port, seed):
     u = np.uint32 if fmt == TS else np.uint64
     bad = np.flatnonzero((got.view(u) != want.view(u)).reshape(m * n, -1).any(axis=1))
     assert bad.size == 0, (fmt, m, l, n, d, drop, bad.size)
+
+
+@pytest.mark.parametrize("seed", list(range(8)))
+def test_random_gemm_bitexact_large_d(ozk, cpu, port, seed):
+    """Split counts 33-48 (pair lists of 561-1176 pairs: two or three kernel
+    launches that continue the K-word sum) on small random shapes, both engines,
+    host and device API."""
+    import torch
+    rng = np.random.default_rng(9000 + seed)
+    fmt = [2, 3, 4, TS][seed % 4]
+    m, n = (int(x) for x in rng.integers(1, 41, 2))
+    l = int(rng.integers(1, 129)) if seed % 2 else int(rng.integers(129, 260))
+    d = int(rng.integers(33, 49))
+    a, b = _inputs(cpu, port, fmt, m, l, n, 0, seed + 4242)
+    want = port.ozaki_gemm_ts(a, b, d) if fmt == TS else cpu.ozaki_gemm(fmt, a, b, d)
+    if seed % 3 == 0:
+        got, prof = ozk.ozaki_gemm(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda(), d)
+        got = got.cpu().numpy()
+    else:
+        got, prof = ozk.ozaki_gemm(a, b, d)
+    assert prof.pairs == d * (d + 1) // 2
+    u = np.uint32 if fmt == TS else np.uint64
+    assert np.array_equal(got.view(u), want.view(u)), (fmt, m, l, n, d)
