@@ -43,12 +43,15 @@ namespace {
 constexpr int kSlots = 6;                    // per direction
 constexpr size_t kSlotBytes = size_t(32) << 20;
 
-// A set of pinned slots for both directions, reused across calls.
+// A set of pinned slots for both directions, reused across calls on the same
+// device (the slot events belong to the device current at creation; the
+// portable pinned memory itself would serve any device).
 struct SlotSet {
     char* mem[2][kSlots] = {};
     cudaEvent_t ev[2][kSlots] = {};
+    int device = -1;
     bool ok = false;
-    SlotSet() {
+    explicit SlotSet(int dev) : device(dev) {
         ok = true;
         for (int d = 0; d < 2 && ok; ++d)
             for (int s = 0; s < kSlots && ok; ++s)
@@ -61,16 +64,18 @@ struct SlotSet {
 std::mutex g_slot_mu;
 std::vector<std::unique_ptr<SlotSet>> g_free_slots;
 
-std::unique_ptr<SlotSet> acquire_slots() {
+// a cached set of device `dev` (the current device of the calling thread)
+std::unique_ptr<SlotSet> acquire_slots(int dev) {
     {
         std::lock_guard<std::mutex> lk(g_slot_mu);
-        if (!g_free_slots.empty()) {
-            auto s = std::move(g_free_slots.back());
-            g_free_slots.pop_back();
-            return s;
-        }
+        for (size_t i = g_free_slots.size(); i-- > 0;)
+            if (g_free_slots[i]->device == dev) {
+                auto s = std::move(g_free_slots[i]);
+                g_free_slots.erase(g_free_slots.begin() + (std::ptrdiff_t)i);
+                return s;
+            }
     }
-    auto s = std::make_unique<SlotSet>();
+    auto s = std::make_unique<SlotSet>(dev);
     return s->ok ? std::move(s) : nullptr;
 }
 
@@ -155,6 +160,7 @@ private:
 }  // namespace
 
 struct HostStaging::Impl {
+    int device;  // the caller's current device: the copy streams' device
     cudaStream_t h2d_stream, d2h_stream;
     std::unique_ptr<SlotSet> slots;
     Team h2d_team, d2h_team;
@@ -163,21 +169,31 @@ struct HostStaging::Impl {
     std::deque<StagedCopy> queue[2];
     int recorded = 0;  // H2D jobs whose ready event has been recorded
     bool closing = false;
-    cudaError_t err = cudaSuccess;
+    std::atomic<cudaError_t> err{cudaSuccess};  // first error; read by the workers' loops
     std::thread worker[2];
     int slot_next[2] = {0, 0};
     bool slot_used[2][kSlots] = {};
 
+    static int current_device() {
+        int d = 0;
+        if (cudaGetDevice(&d) != cudaSuccess) {
+            (void)cudaGetLastError();
+            d = 0;
+        }
+        return d;
+    }
+
     Impl(cudaStream_t h2d, cudaStream_t d2h, int h2d_threads, int d2h_threads)
-        : h2d_stream(h2d), d2h_stream(d2h), slots(acquire_slots()), h2d_team(h2d_threads),
-          d2h_team(d2h_threads) {
+        : device(current_device()), h2d_stream(h2d), d2h_stream(d2h),
+          slots(acquire_slots(device)), h2d_team(h2d_threads), d2h_team(d2h_threads) {
         if (!slots) err = cudaErrorMemoryAllocation;
         for (int d = 0; d < 2; ++d) worker[d] = std::thread([this, d] { run(d); });
     }
 
     void fail(cudaError_t e) {
         std::lock_guard<std::mutex> lk(mu);
-        if (err == cudaSuccess) err = e;
+        cudaError_t ok = cudaSuccess;
+        err.compare_exchange_strong(ok, e);
         cv.notify_all();
     }
 
@@ -257,6 +273,9 @@ struct HostStaging::Impl {
     }
 
     void run(int d) {
+        // a new thread starts on device 0: make the slot events' and copy
+        // streams' device current (ozk_ozaki_gemm called on another device)
+        if (const cudaError_t e = cudaSetDevice(device); e != cudaSuccess) fail(e);
         for (;;) {
             StagedCopy j;
             {
@@ -307,7 +326,7 @@ void HostStaging::push_d2h(const StagedCopy& c) {
 cudaError_t HostStaging::wait_recorded(int job) {
     std::unique_lock<std::mutex> lk(impl_->mu);
     impl_->cv.wait(lk, [&] { return impl_->recorded >= job || impl_->err != cudaSuccess; });
-    return impl_->err;
+    return impl_->err.load();
 }
 
 cudaError_t HostStaging::finish() {
@@ -319,7 +338,7 @@ cudaError_t HostStaging::finish() {
         impl_->cv.notify_all();
         for (auto& w : impl_->worker) w.join();
     }
-    return impl_->err;
+    return impl_->err.load();
 }
 
 }  // namespace ozk

@@ -828,6 +828,52 @@ def test_host_api_pinned_and_pageable_agree(ozk, cpu, monkeypatch, n, head):
     assert_bitwise(ref_c[rows], want, "sampled rows vs the reference")
 
 
+def test_host_api_pageable_concurrent_and_per_device(ozk, cpu):
+    """Concurrent ozk_ozaki_gemm calls from pageable buffers each take their
+    own pinned slot set (the cache hands one set per call) and give the
+    single-call bits; with a second GPU, a call made while device 1 is current
+    stages through a slot set of device 1 (the slot events belong to one
+    device) -- skipped on one GPU."""
+    import ctypes
+    import threading
+
+    import torch
+    K, m, l, n, d = 2, 2048, 200, 4096, 5
+    a = cpu.gen_eq1(K, m, l, 51)
+    b = cpu.gen_eq1(K, l, n, 52)
+    ref = np.empty((m, n, K))
+    assert ozk.lib.ozk_ozaki_gemm(K, m, l, n, a.ctypes.data, b.ctypes.data, d, 0.0,
+                                  ref.ctypes.data, None) == 0, ozk.lib.ozk_last_error()
+    outs = [np.empty((m, n, K)) for _ in range(3)]
+    status = [None] * 3
+
+    def call(i):
+        status[i] = ozk.lib.ozk_ozaki_gemm(K, m, l, n, a.ctypes.data, b.ctypes.data, d, 0.0,
+                                           outs[i].ctypes.data, None)
+
+    ths = [threading.Thread(target=call, args=(i,)) for i in range(3)]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    for i in range(3):
+        assert status[i] == 0
+        assert_bitwise(outs[i], ref, f"concurrent pageable call {i}")
+    rows = np.arange(0, m, 131)
+    assert_bitwise(ref[rows], cpu.ozaki_gemm(K, np.ascontiguousarray(a[rows]), b, d),
+                   "sampled rows vs the reference")
+    if torch.cuda.device_count() < 2:
+        return
+    for dev in (1, 0, 1):  # alternate devices: a cached set must not cross devices
+        c = np.empty((m, n, K))
+        with torch.cuda.device(dev):
+            torch.cuda.synchronize()
+            st = ozk.lib.ozk_ozaki_gemm(K, m, l, n, a.ctypes.data, b.ctypes.data, d, 0.0,
+                                        c.ctypes.data, None)
+        assert st == 0, ozk.lib.ozk_last_error()
+        assert_bitwise(c, ref, f"pageable call on device {dev}")
+
+
 @pytest.mark.parametrize("K,l,devs", [(2, 100, [0, 0]), (3, 64, [0, 0, 0]), (2, 300, [0, 0])])
 def test_ozaki_gemm_multi_pruning_uses_global_maxima(ozk, cpu, K, l, devs):
     """With drop_threshold > 0 every device prunes with the maxima of ALL rows
