@@ -22,7 +22,7 @@ __global__ void accumulate_kernel(const double* __restrict__ prods, int np, size
 #pragma unroll
         for (int k = 0; k < K; ++k) acc[k] = W(0);
         for (int p = 0; p < np; ++p)
-            kw_add<K, W, true, false, true>(acc, (W)prods[(size_t)p * count + e]);
+            kw_add<K, W, true, true>(acc, (W)prods[(size_t)p * count + e]);
 #pragma unroll
         for (int k = 0; k < K; ++k) c[e * K + k] = acc[k];
     }

@@ -356,7 +356,7 @@ pair_gemm_kernel(const __grid_constant__ TmaMaps maps, const __grid_constant__ P
                     for (int q = 0; q < 8; ++q) w[q][0] = w[q][0] + (W)y[q];
 #else
 #pragma unroll
-                    for (int q = 0; q < 8; ++q) kw_add<K, W, true, false, true>(w[q], (W)y[q]);
+                    for (int q = 0; q < 8; ++q) kw_add<K, W, true, true>(w[q], (W)y[q]);
 #endif
 #pragma unroll
                     for (int q = 0; q < 8; ++q) {

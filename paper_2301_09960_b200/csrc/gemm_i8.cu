@@ -943,7 +943,7 @@ pair_gemm_i8_kernel(const __grid_constant__ MapsI8 maps, const __grid_constant__
 #if defined(OZK_I8_EPI_MODE) && OZK_I8_EPI_MODE == 2
                             w[j][0] += scale_prod<W>(y, ga + gbq[q]);  // diagnostic: no K-word add
 #else
-                            kw_add<K, W, kEpiIntCmp, false, true>(w[j], scale_prod<W>(y, ga + gbq[q]));
+                            kw_add<K, W, kEpiIntCmp, true>(w[j], scale_prod<W>(y, ga + gbq[q]));
 #endif
                         }
                     }

@@ -339,11 +339,9 @@ OZK_HD bool kw_fast_ok(const T* x, T y) {
 // MultiFloat<K> + word (multifloat.hpp:203-213); x is updated in place.  T is
 // the word type: double for DD/TD/QD, float for TS (which uses the generic
 // K >= 3 branch with binary32 words, see oracle/ozk_oracle.c).
-// kLead (K >= 3): the caller guarantees |y| > |x[1]| (or x[1] == 0, y != 0),
-// so merge_components places y right before or right after x[0] and only that
-// one comparison is made.  The split's w -= x satisfies it: x != 0 is w0
-// rounded to a grid of at least 2^(e+sigma-S) (e >= the binade of w0), while
-// |w1| <= 1/2 ulp(w0) <= 2^(e-S) (renormalised residual), sigma >= 1.
+// kLead (K >= 3): the caller guarantees that y precedes x[1] in merge order
+// whenever x[0] precedes y, so merge_components places y right before or
+// right after x[0] and only that one comparison is made (kw_sub_piece).
 template <int K, bool kInt, typename T, bool kFast = false, bool kLead = false>
 OZK_HD void kw_add_impl(T* x, T y) {
     if constexpr (K == 2) {
@@ -534,8 +532,7 @@ OZK_HD bool kw_add_tail2(T* x, T y) {
 
 // kAccum: the accumulation acc += C_ab (slice-GEMM epilogues, accumulate.cu):
 // tries the last-word shortcut (kw_add_tail) first.
-template <int K, typename T = double, bool kIntCmp = true, bool kLead = false,
-          bool kAccum = false>
+template <int K, typename T = double, bool kIntCmp = true, bool kAccum = false>
 OZK_HD void kw_add(T* x, T y) {
 #if OZK_KW_FAST
     if constexpr (K >= 3) {
@@ -544,7 +541,7 @@ OZK_HD void kw_add(T* x, T y) {
         if (kw_fast_ok<K>(x, y)) {
             if constexpr (kAccum && OZK_KW_TAIL)
                 if (kw_add_tail<K, kIntCmp>(x, y)) return;
-            kw_add_impl<K, kIntCmp, T, true, kLead>(x, y);
+            kw_add_impl<K, kIntCmp, T, true>(x, y);
         } else {
             kw_add_full<K>(x, y);
         }
@@ -554,6 +551,80 @@ OZK_HD void kw_add(T* x, T y) {
     if constexpr (K == 2 && kAccum && OZK_KW_TAIL)
         if (kw_add_tail2<kIntCmp>(x, y)) return;
     kw_add_impl<K, false>(x, y);
+}
+
+// ---- the split's residual update ---------------------------------------------
+//
+// w -= x  ==  w + (-x)  (multifloat.hpp:304 -> :203-213) where x is the piece
+// shift_extract(w[0], tau) = fl(fl(w[0] + tau) - tau) (ozaki.hpp:53-56), tau =
+// 2^(e + sigma) with |w[0]| <= 2^e < tau, e + sigma below the shift guard.
+//
+// K = 2.  r0 = w[0] - x is exact and two_sum(w[0], -x) = (r0, +0): t =
+// fl(w[0] + tau) lies in [tau/2, 3tau/2], so x = fl(t - tau) = t - tau
+// (Sterbenz) and r0 = (w[0] + tau) - t is the rounding error of an addition,
+// which is representable; two_sum then computes bb = fl(r0 - w[0]) = -x
+// exactly and e = fl((w[0] - fl(r0 + x)) + (-x + x)) = +0.  So the reference's
+// first two_sum is one subtraction; the rest is its sequence.
+//
+// K >= 3.  The merge (merge_components, :420-430) puts -x right before or right
+// after w[0] whenever |w[1]| < |x| or w[0] does not precede -x: for a
+// canonical residual always (x != 0 is w[0] rounded to a grid G >= ulp(w[0]),
+// and |w[1]| <= ulp(w[0]) / 2 < G <= |x| when w[0] comes first), so one
+// comparison places it (kw_add_impl kLead).  A non-canonical first-pass input
+// (MultiFloat::from_components_unchecked, :147-151) can break that; it takes
+// the generic merge, out of line so the common path stays compact.
+// tests/test_kword_host.py checks both against the compiled reference.
+template <int K, bool kInt, typename T>
+OZK_HD void kw_add_general(T* x, T y);
+
+template <int K, bool kInt, typename T>
+OZK_HD void kw_sub_piece(T* w, T x) {
+    const T y = -x;
+    if constexpr (K == 2) {
+        const T s = rn_sub(w[0], x);        // two_sum(w[0], y) = (s, +0)
+        const T v = rn_add(w[1], T(0));
+        T fs, fe;
+        fast_two_sum(s, v, fs, fe);
+        if (!is_finite(fs)) {               // from_pair (:384-392)
+            w[0] = fs;
+            w[1] = T(0);
+            return;
+        }
+        T ps, pe;
+        fast_two_sum(fs, fe, ps, pe);
+        w[0] = is_zero<false>(ps) ? T(0) : ps;
+        w[1] = (is_zero<false>(pe) || is_zero<false>(ps)) ? T(0) : pe;
+    } else {
+        if (!kw_fast_ok<K>(w, y)) {
+            kw_add_full<K>(w, y);
+        } else if (fabs_(w[1]) < fabs_(y) || !merge_before<kInt>(w[0], y)) {
+            kw_add_impl<K, kInt, T, true, true>(w, y);
+        } else {
+            kw_add_general<K, kInt>(w, y);
+        }
+    }
+}
+
+// the generic-merge update, out of line on the device (rarely taken)
+#if defined(__CUDA_ARCH__)
+template <int K, bool kInt, typename T>
+__device__ __noinline__ KWords<K, T> kw_add_general_v(KWords<K, T> v, T y) {
+    kw_add_impl<K, kInt, T, true>(v.w, y);
+    return v;
+}
+#endif
+template <int K, bool kInt, typename T>
+OZK_HD void kw_add_general(T* x, T y) {
+#if defined(__CUDA_ARCH__)
+    KWords<K, T> v;
+#pragma unroll
+    for (int i = 0; i < K; ++i) v.w[i] = x[i];
+    v = kw_add_general_v<K, kInt, T>(v, y);
+#pragma unroll
+    for (int i = 0; i < K; ++i) x[i] = v.w[i];
+#else
+    kw_add_impl<K, kInt, T, true>(x, y);
+#endif
 }
 
 // -MultiFloat<K> (multifloat.hpp:178-182): zero words stay +0.

@@ -28,10 +28,6 @@ namespace {
 #define OZK_SPLIT_THREADS 512
 #endif
 constexpr int kSplitThreads = OZK_SPLIT_THREADS;
-// the residual update's one-comparison merge (kword.cuh kLead); 0 = generic
-#ifndef OZK_SPLIT_LEAD
-#define OZK_SPLIT_LEAD 1
-#endif
 
 __device__ __forceinline__ int ceil_log2(double x) {
     int e = ilogb(x);
@@ -243,9 +239,11 @@ split_rows_kernel(const T* __restrict__ in, size_t in_ld, T* __restrict__ work, 
                     drow[j + (dig.nd - 1) * dig.digit_stride] = (int8_t)mi;
                 }
                 if (update && x != T(0)) {
-                    // w -= x  ==  w + (-x)  (multifloat.hpp:304,215); FP64 compares:
-                    // this kernel is ALU-bound, its FP64 pipe mostly idle
-                    kw_add<K, T, false, OZK_SPLIT_LEAD != 0>(c, -x);  // kLead: see kword.cuh
+                    // w -= x  ==  w + (-x)  (multifloat.hpp:304,215), with x the
+                    // piece just extracted from w[0] (kword.cuh kw_sub_piece);
+                    // FP64 compares: this kernel is ALU-bound, its FP64 pipe
+                    // mostly idle
+                    kw_sub_piece<K, false>(c, x);
                     store_kw<K>(w + j * K, c);
                 } else if (store_all) {
                     store_kw<K>(w + j * K, c);

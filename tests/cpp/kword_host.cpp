@@ -31,7 +31,7 @@ static void run_split(std::size_t n, const T* x, const T* y, T* out) {
     for (std::size_t i = 0; i < n; ++i) {
         T w[K];
         for (int k = 0; k < K; ++k) w[k] = x[i * K + k];
-        ozk::kw_add<K, T, false, true>(w, y[i]);  // the split's w -= x (kLead merge)
+        ozk::kw_sub_piece<K, false>(w, -y[i]);  // the split's w -= x, x = -y[i]
         for (int k = 0; k < K; ++k) out[i * K + k] = w[k];
     }
 }
@@ -56,7 +56,7 @@ static void run_accum(std::size_t n, const T* x, const T* y, T* out) {
     for (std::size_t i = 0; i < n; ++i) {
         T w[K];
         for (int k = 0; k < K; ++k) w[k] = x[i * K + k];
-        ozk::kw_add<K, T, true, false, true>(w, y[i]);  // the accumulation's flavour
+        ozk::kw_add<K, T, true, true>(w, y[i]);  // the accumulation's flavour
         for (int k = 0; k < K; ++k) out[i * K + k] = w[k];
     }
 }

@@ -79,6 +79,29 @@ def test_split_skipped_rows_keep_their_residual(ozk, cpu):
             assert_bitwise(s.residual, want_r, f"residual d={d} side={side}")
 
 
+@pytest.mark.parametrize("K", [2, 3, 4])
+def test_split_and_gemm_noncanonical_input(ozk, cpu, K):
+    """Inputs that are not canonical K-word values (overlapping, unordered,
+    signed-zero words: MultiFloat::from_components_unchecked, multifloat.hpp:
+    147-151) go through the split's first pass as they are; slices, residual and
+    C still match the reference bit for bit (kword.cuh kw_sub_piece's generic
+    fallback)."""
+    rng = np.random.default_rng(900 + K)
+    m = rng.standard_normal((40, 300, K)) * np.exp2(rng.integers(-6, 6, (40, 300, K)))
+    m[::7, :, 1] = -0.0
+    m[1::5, :, K - 1] = 0.0
+    for d in (1, 3, 7):
+        for side in (0, 1):
+            want_p, want_r = cpu.split(K, m, d, side)
+            s = ozk.split_matrix(m, d, ozk.SplitSide(side))
+            assert_bitwise(np.stack(s.pieces), want_p, f"pieces K={K} d={d} side={side}")
+            assert_bitwise(s.residual, want_r, f"residual K={K} d={d} side={side}")
+    b = rng.standard_normal((300, 24, K)) * np.exp2(rng.integers(-6, 6, (300, 24, K)))
+    for d in (4, 8):
+        got, _ = ozk.ozaki_gemm(m, b, d)
+        assert_bitwise(got, cpu.ozaki_gemm(K, m, b, d), f"C K={K} d={d}")
+
+
 def test_split_errors(ozk, cpu):
     m = cpu.gen_eq1(2, 2, 2, 72)
     with pytest.raises(ozk.param_error):

@@ -252,6 +252,17 @@ def _split_chain_cases(K, cpu, rng, rows):
     w = cpu.gen_eq1(K, rows, 8, int(rng.integers(1, 1 << 30))).reshape(-1, K).copy()
     w[rng.random(w.shape[0]) < 0.05, 1:] = 0.0
     w *= np.exp2(rng.integers(-40, 40, w.shape[0]).astype(float))[:, None]
+    # non-canonical inputs (MultiFloat::from_components_unchecked, multifloat.hpp:
+    # 147-151), which the split reads in its first pass: overlapping, unordered
+    # and signed-zero words
+    q = w.shape[0] // 8
+    w[:q, 1:] = rng.standard_normal((q, K - 1)) * np.exp2(rng.integers(-60, 4, (q, K - 1)))
+    w[q:2 * q:3, 1] = -0.0
+    w[q + 1:2 * q:5, K - 1] = -0.0
+    w[q + 2:2 * q:7, 1:] = 0.0
+    # ties: w[1] exactly half an ulp of w[0]
+    t = slice(2 * q, 2 * q + q // 4)
+    w[t, 1] = np.spacing(np.abs(w[t, 0])) * 0.5 * rng.choice([-1.0, 1.0], w[t, 0].shape)
     for _ in range(6):
         w0 = w[:, 0]
         nz = w0 != 0.0
@@ -269,11 +280,12 @@ def _split_chain_cases(K, cpu, rng, rows):
     return np.concatenate(ws), np.concatenate(ys)
 
 
-@pytest.mark.parametrize("K", [3, 4])
+@pytest.mark.parametrize("K", [2, 3, 4])
 def test_split_residual_update_matches_reference(ref, port, K):
-    """The split's w -= x (kw_add<K, double, false, kLead = true>: one merge
-    comparison, see kword.cuh) equals the reference's MultiFloat -= double on
-    every (w, x) pair the split can produce."""
+    """The split's w -= x (kw_sub_piece<K, false>: K = 2 with the exact first
+    two_sum, K >= 3 with the one-comparison merge and its generic fallback, see
+    kword.cuh) equals the reference's MultiFloat -= double on every (w, x) pair
+    the split can produce, non-canonical first-pass inputs included."""
     import __graft_entry__
     if not os.path.exists(SO):
         __graft_entry__._build_test_helpers()
