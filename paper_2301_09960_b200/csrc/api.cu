@@ -22,6 +22,7 @@
 #include <thread>
 #include <cstdint>
 #include <tuple>
+#include <initializer_list>
 #include <map>
 
 #include <sched.h>
@@ -752,6 +753,14 @@ namespace ozk {
 void set_last_error(const std::string& msg) { g_last_error = msg; }
 }  // namespace ozk
 
+// Null operands are rejected at the boundary: a null device pointer would
+// fault the kernel and leave the CUDA context unusable for the process.
+static ozk_status need(std::initializer_list<const void*> ptrs, const char* what) {
+    for (const void* p : ptrs)
+        if (!p) return fail(OZK_EPARAM, std::string(what) + ": null pointer");
+    return OZK_OK;
+}
+
 extern "C" {
 
 const char* ozk_last_error(void) { return g_last_error.c_str(); }
@@ -789,6 +798,7 @@ ozk_status ozk_ozaki_gemm_device(ozk_format fmt, size_t m, size_t l, size_t n, c
                                  const void* b, int d, double drop, void* c, void* stream,
                                  ozk_profile* prof) {
     if (ozk_status s = check_gemm_args(fmt, m, l, n, d, drop)) return s;
+    if (ozk_status s = need({a, b, c}, "ozaki_gemm")) return s;
     return ozaki_device_impl((int)fmt, m, l, n, a, l, b, n, d, drop, c, (cudaStream_t)stream,
                              prof);
 }
@@ -796,6 +806,7 @@ ozk_status ozk_ozaki_gemm_device(ozk_format fmt, size_t m, size_t l, size_t n, c
 ozk_status ozk_ozaki_gemm(ozk_format fmt, size_t m, size_t l, size_t n, const void* a,
                           const void* b, int d, double drop, void* c, ozk_profile* prof) {
     if (ozk_status s = check_gemm_args(fmt, m, l, n, d, drop)) return s;
+    if (ozk_status s = need({a, b, c}, "ozaki_gemm")) return s;
     const size_t eb = elem_bytes(fmt);
     auto t0 = std::chrono::steady_clock::now();
     OwnStream os;
@@ -1032,6 +1043,7 @@ ozk_status ozk_split(ozk_format fmt, size_t rows, size_t cols, const void* mat, 
     if (d > kMaxSplits) return fail(OZK_EPARAM, "split_matrix: split count above 65535 is not supported");
     if (side != OZK_SIDE_ROWS && side != OZK_SIDE_COLS)
         return fail(OZK_EPARAM, "split_matrix: bad side");
+    if (ozk_status s = need({mat}, "split_matrix")) return s;
     const int K = words_of(fmt), wb = word_bytes_of(fmt);
     const size_t eb = elem_bytes(fmt);
     const size_t N = rows * cols;
@@ -1105,6 +1117,7 @@ ozk_status ozk_split_slices_device(ozk_format fmt, size_t rows, size_t cols, siz
     if (ld < cols) return fail(OZK_ESHAPE, "split_matrix: ld < cols");
     if (plane_rows < (side == OZK_SIDE_ROWS ? rows : cols))
         return fail(OZK_ESHAPE, "split_matrix: plane_rows < outer dimension");
+    if (ozk_status s = need({mat, slices}, "split_matrix")) return s;
     cudaStream_t st = (cudaStream_t)stream;
     num_sms_cached();
     DevBuf work, flags;
@@ -1162,6 +1175,7 @@ ozk_status ozk_slices_gemm_device(ozk_format fmt, size_t m, size_t l, size_t n,
     if (ldc < n) return fail(OZK_ESHAPE, "slices_gemm: ldc < n");
     PairList pl;
     if (ozk_status s = fill_pairs(d, pairs, npairs, pl)) return s;
+    if (ozk_status s = need({a_slices, b_slices, c}, "slices_gemm")) return s;
     cudaStream_t st = (cudaStream_t)stream;
     const size_t ldk = slice_ld(l);
     GemmProblem prob{};
@@ -1232,6 +1246,7 @@ ozk_status ozk_ozaki_gemm_multi(ozk_format fmt, int ngpus, const int* devices, s
                                 double drop, void* c, ozk_profile* prof) {
     if (ozk_status s = check_gemm_args(fmt, m, l, n, split_count, drop)) return s;
     if (ngpus < 1 || ngpus > 64) return fail(OZK_EPARAM, "ozaki_gemm_multi: 1..64 devices");
+    if (ozk_status s = need({a, b, c}, "ozaki_gemm_multi")) return s;
     const int d = split_count;
     const size_t eb = elem_bytes(fmt);
     const int nd = engine_setting() != OZK_ENGINE_DMMA ? int8_digits(fmt, l, d) : 0;
@@ -1555,6 +1570,7 @@ ozk_status ozk_split_digits_device_async(ozk_format fmt, size_t rows, size_t col
     if (ld8 < inner || ld8 % 16) return fail(OZK_ESHAPE, "split_digits: ld8 must be >= inner and a multiple of 16");
     if (plane_rows < outer) return fail(OZK_ESHAPE, "split_digits: plane_rows < outer dimension");
     if (!digits || !exps || !dev_flag) return fail(OZK_EPARAM, "split_digits: null output");
+    if (ozk_status s = need({mat}, "split_digits")) return s;
     cudaStream_t st = (cudaStream_t)stream;
     num_sms_cached();
     DigitOut dig;
@@ -1613,6 +1629,7 @@ ozk_status ozk_digits_gemm_device_async(ozk_format fmt, size_t m, size_t l, size
     if (ldc < n) return fail(OZK_ESHAPE, "digits_gemm: ldc < n");
     PairList pl;
     if (ozk_status s = fill_pairs(d, pairs, npairs, pl)) return s;
+    if (ozk_status s = need({a_digits, a_exps, b_digits, b_exps, c}, "digits_gemm")) return s;
     cudaStream_t st = (cudaStream_t)stream;
     if (pl.count == 0) {
         OZK_CUDA(cudaMemset2DAsync(c, ldc * elem_bytes(fmt), 0, n * elem_bytes(fmt), m, st),
@@ -1673,6 +1690,8 @@ ozk_status ozk_pair_products_digits_device(ozk_format fmt, size_t m, size_t l, s
     if (a_plane_rows < m || b_plane_rows < n) return fail(OZK_ESHAPE, "pair_products: plane_rows too small");
     PairList pl;
     if (ozk_status s = fill_pairs(d, pairs, npairs, pl)) return s;
+    if (ozk_status s = need({a_digits, a_exps, b_digits, b_exps, products}, "pair_products"))
+        return s;
     cudaStream_t st = (cudaStream_t)stream;
     if (pl.count > 0) {
         I8Operands op{};
@@ -1710,6 +1729,7 @@ ozk_status ozk_pair_products_device(size_t m, size_t l, size_t n, const double* 
     if (d < 1 || d > kMaxSplits) return fail(OZK_EPARAM, "pair_products: bad split count");
     PairList pl;
     if (ozk_status s = fill_pairs(d, pairs, npairs, pl)) return s;
+    if (ozk_status s = need({a_slices, b_slices, products}, "pair_products")) return s;
     cudaStream_t st = (cudaStream_t)stream;
     const size_t ldk = slice_ld(l);
     GemmProblem prob{};
@@ -1740,6 +1760,7 @@ ozk_status ozk_backend_gemm_device(size_t m, size_t l, size_t n, const double* a
     if (m == 0 || l == 0 || n == 0) return fail(OZK_ESHAPE, "matrix dimensions must be positive");
     if (m > 0x7fffffffull || n > 0x7fffffffull || l > 0x7fffffffull)
         return fail(OZK_ESHAPE, "backend_gemm: dimension too large");
+    if (ozk_status s = need({a, b, c}, "backend_gemm")) return s;
     cudaStream_t st = (cudaStream_t)stream;
     const size_t ldk = slice_ld(l);
     DevBuf ap, bt;
@@ -1777,6 +1798,7 @@ ozk_status ozk_backend_gemm_device(size_t m, size_t l, size_t n, const double* a
 ozk_status ozk_backend_gemm(size_t m, size_t l, size_t n, const double* a, const double* b,
                             double* c) {
     if (m == 0 || l == 0 || n == 0) return fail(OZK_ESHAPE, "matrix dimensions must be positive");
+    if (ozk_status s = need({a, b, c}, "backend_gemm")) return s;
     OwnStream os;
     OZK_CUDA(os.create(), "backend_gemm: stream");
     num_sms_cached();
@@ -1803,6 +1825,8 @@ ozk_status ozk_accumulate_products_device(ozk_format fmt, size_t m, size_t n,
     if (!valid_fmt(fmt)) return fail(OZK_EPARAM, "accumulate: format must be DD, TD, QD or TS");
     if (m == 0 || n == 0) return fail(OZK_ESHAPE, "matrix dimensions must be positive");
     if (nproducts < 0) return fail(OZK_EPARAM, "accumulate: negative product count");
+    if (nproducts > 0 && !products) return fail(OZK_EPARAM, "accumulate: null pointer");
+    if (ozk_status s = need({c}, "accumulate")) return s;
     cudaStream_t st = (cudaStream_t)stream;
     if (nproducts == 0) {
         OZK_CUDA(cudaMemsetAsync(c, 0, elem_bytes(fmt) * m * n, st), "accumulate: zero");
@@ -1821,6 +1845,9 @@ ozk_status ozk_accumulate_products(ozk_format fmt, size_t m, size_t n,
     if (m == 0 || n == 0) return fail(OZK_ESHAPE, "matrix dimensions must be positive");
     if (nproducts < 0 || (nproducts > 0 && !products))
         return fail(OZK_EPARAM, "accumulate: bad product list");
+    if (ozk_status s = need({c}, "accumulate")) return s;
+    for (int p = 0; p < nproducts; ++p)
+        if (!products[p]) return fail(OZK_EPARAM, "accumulate: null pointer");
     const size_t eb = elem_bytes(fmt);
     OwnStream os;
     OZK_CUDA(os.create(), "accumulate: stream");
@@ -1858,6 +1885,7 @@ ozk_status ozk_lu_trailing_update_device(ozk_format fmt, size_t tm, size_t pw, s
     if (ozk_status s = check_gemm_args(fmt, tm, pw, tn, d, 0.0)) return s;
     if (ldl < pw || ldu < tn || lda < tn)
         return fail(OZK_ESHAPE, "lu_trailing_update: leading dimension too small");
+    if (ozk_status s = need({l21, u12, a22}, "lu_trailing_update")) return s;
     cudaStream_t st = (cudaStream_t)stream;
     const int K = (int)fmt;
     DevBuf upd;
@@ -1880,6 +1908,7 @@ ozk_status ozk_lu_trailing_update(ozk_format fmt, size_t tm, size_t pw, size_t t
     if (ozk_status s = check_gemm_args(fmt, tm, pw, tn, d, 0.0)) return s;
     if (ldl < pw || ldu < tn || lda < tn)
         return fail(OZK_ESHAPE, "lu_trailing_update: leading dimension too small");
+    if (ozk_status s = need({l21, u12, a22}, "lu_trailing_update")) return s;
     const size_t eb = elem_bytes(fmt);
     OwnStream os;
     OZK_CUDA(os.create(), "lu_trailing_update: stream");
@@ -1912,6 +1941,7 @@ ozk_status ozk_ts_direct_gemm_device(size_t m, size_t l, size_t n, const float* 
     if (m == 0 || l == 0 || n == 0) return fail(OZK_ESHAPE, "matrix dimensions must be positive");
     if (m > 0x7fffffffull || n > 0x7fffffffull || l > 0x7fffffffull)
         return fail(OZK_ESHAPE, "ts_direct_gemm: dimension too large");
+    if (ozk_status s = need({a, b, c}, "ts_direct_gemm")) return s;
     cudaStream_t st = (cudaStream_t)stream;
     OZK_CUDA(launch_ts_direct(a, b, c, m, l, n, st), "ts_direct_gemm");
     OZK_CUDA(cudaStreamSynchronize(st), "ts_direct_gemm");
@@ -1921,6 +1951,7 @@ ozk_status ozk_ts_direct_gemm_device(size_t m, size_t l, size_t n, const float* 
 ozk_status ozk_ts_direct_gemm(size_t m, size_t l, size_t n, const float* a, const float* b,
                               float* c) {
     if (m == 0 || l == 0 || n == 0) return fail(OZK_ESHAPE, "matrix dimensions must be positive");
+    if (ozk_status s = need({a, b, c}, "ts_direct_gemm")) return s;
     OwnStream os;
     OZK_CUDA(os.create(), "ts_direct_gemm: stream");
     DevBuf da, db, dc;
@@ -1943,6 +1974,7 @@ ozk_status ozk_direct_gemm_device(ozk_format fmt, size_t m, size_t l, size_t n, 
         return fail(OZK_EPARAM, "direct_gemm: format must be DD, TD or QD (TS: ozk_ts_direct_gemm)");
     if (m == 0 || l == 0 || n == 0) return fail(OZK_ESHAPE, "matrix dimensions must be positive");
     if (m > 0xffff0ull * 16 || n > 0xffff0ull * 16) return fail(OZK_ESHAPE, "direct_gemm: dimension too large");
+    if (ozk_status s = need({a, b, c}, "direct_gemm")) return s;
     cudaStream_t st = (cudaStream_t)stream;
     OZK_CUDA(launch_direct_gemm(words_of(fmt), static_cast<const double*>(a),
                                 static_cast<const double*>(b), static_cast<double*>(c), m, l, n, st),
@@ -1956,6 +1988,7 @@ ozk_status ozk_direct_gemm(ozk_format fmt, size_t m, size_t l, size_t n, const v
     if (fmt != OZK_DD && fmt != OZK_TD && fmt != OZK_QD)
         return fail(OZK_EPARAM, "direct_gemm: format must be DD, TD or QD (TS: ozk_ts_direct_gemm)");
     if (m == 0 || l == 0 || n == 0) return fail(OZK_ESHAPE, "matrix dimensions must be positive");
+    if (ozk_status s = need({a, b, c}, "direct_gemm")) return s;
     const size_t eb = elem_bytes(fmt);
     OwnStream os;
     OZK_CUDA(os.create(), "direct_gemm: stream");
@@ -1976,6 +2009,7 @@ ozk_status ozk_gen_spread_device(ozk_format fmt, size_t rows, size_t cols, uint6
     if (!valid_fmt(fmt)) return fail(OZK_EPARAM, "gen: format must be DD, TD, QD or TS");
     if (rows == 0 || cols == 0) return fail(OZK_ESHAPE, "matrix dimensions must be positive");
     if (spread < 0 || spread > 400) return fail(OZK_EPARAM, "gen: spread must be in [0, 400]");
+    if (ozk_status s = need({out}, "gen")) return s;
     cudaStream_t st = (cudaStream_t)stream;
     OZK_CUDA(launch_gen_eq1(words_of(fmt), word_bytes_of(fmt), out, rows * cols, seed, spread, st),
              "gen");

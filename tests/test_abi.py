@@ -106,6 +106,18 @@ def test_argument_errors_without_gpu():
                                              None, None) == 2
     assert lib.ozk_split_digits_device_async(2, 300, 300, 300, None, 3, 0, None, 304, 300,
                                              None, None, None, None) == 2  # null outputs
+    # null operands are refused before any device work (after the shape and
+    # parameter checks, which keep the reference's order)
+    assert lib.ozk_ozaki_gemm(2, 2, 2, 2, None, None, 2, 0.0, None, None) == 2
+    assert b"null pointer" in lib.ozk_last_error()
+    assert lib.ozk_ozaki_gemm_device(2, 2, 2, 2, None, None, 2, 0.0, None, None, None) == 2
+    assert lib.ozk_split(2, 2, 2, None, 2, 0, None, None) == 2
+    assert b"null pointer" in lib.ozk_last_error()
+    assert lib.ozk_direct_gemm(2, 2, 2, 2, None, None, None) == 2
+    assert lib.ozk_backend_gemm(2, 2, 2, None, None, None) == 2
+    assert lib.ozk_lu_trailing_update(2, 2, 2, 2, None, 2, None, 2, None, 2, 2) == 2
+    assert lib.ozk_ozaki_gemm_multi(2, 1, None, 2, 2, 2, None, None, 2, 0.0, None, None) == 2
+    assert b"null pointer" in lib.ozk_last_error()
     # a caller's backend is honoured, with the reference's argument checks first
     with pytest.raises(ozk.param_error):
         ozk.ozaki_gemm(a, a, 0, backend=lambda x, y: x @ y)
