@@ -245,15 +245,19 @@ OZK_HD void strict_normalize(T* c) {
         // trailing zeros written by the reference's compaction are +0
 #pragma unroll
         for (int i = 0; i < K; ++i) c[i] = is_zero<kInt>(c[i]) ? T(0) : c[i];
+        // The reference assigns (s, e) only when they differ from (c[i], c[i+1]);
+        // assigning always is the same: with no difference they are equal
+        // numerically and not NaN, and no -0 is present on either side (the
+        // compaction above leaves nonzeros and +0; fl(a + b) is -0 only for a =
+        // b = -0, and fl(b - t) only for b = -0), so they are equal bitwise.
         bool changed = false;
 #pragma unroll
         for (int i = K - 2; i >= 0; --i) {
             T s, e;
             fast_two_sum(c[i], c[i + 1], s, e);
-            bool ch = !same<kInt>(s, c[i]) || !same<kInt>(e, c[i + 1]);
-            c[i] = ch ? s : c[i];
-            c[i + 1] = ch ? e : c[i + 1];
-            changed = changed || ch;
+            changed = changed || !same<kInt>(s, c[i]) || !same<kInt>(e, c[i + 1]);
+            c[i] = s;
+            c[i + 1] = e;
         }
         if (!changed) break;
     }
