@@ -12,9 +12,10 @@ Rank r of W owns C rows [r0, r1) and B columns [c0, c1):
    the A rows are split;
 4. with drop_threshold > 0, all-reduce(max) the per-slice maxima so every rank
    prunes the same pairs (ozaki.hpp:198-221);
-5. run every slice pair for its rows with the fused accumulation.  The
-   per-element accumulation order is unchanged, so C is bit-identical for any
-   number of GPUs.
+5. run every slice pair for its rows with the fused accumulation -- with the
+   INT8 engine first for its own B column block while the all-gather is still
+   in flight, then for the gathered columns.  The per-element accumulation
+   order is unchanged, so C is bit-identical for any number of GPUs.
 
 Two slice representations, bit-identical results:
 * INT8 engine (default where it applies, ozk_int8_digits > 0): the splits write
@@ -169,6 +170,18 @@ class GpuOps:
             plane_rows, exps.data_ptr() + 4 * r0, None, self.flags.data_ptr() + 4 * side,
             self._stream()))
 
+    def gemm_digit_block(self, plan: ShardPlan, r0, rows, a8, ga, b8, gb, b_row0, col0, col1,
+                         pairs, c):
+        """C rows [r0, r0 + rows) x columns [col0, col1), B digits from plane rows
+        [b_row0, ...) of b8."""
+        flat = (ctypes.c_int * (2 * len(pairs)))(*[v for p in pairs for v in p])
+        ld8, esz = a8.shape[3], c.element_size() * c.shape[2]
+        self._check(self.lib.ozk_digits_gemm_device_async(
+            plan.K, rows, plan.l, col1 - col0, a8.data_ptr() + r0 * ld8, ga.data_ptr() + 4 * r0,
+            a8.shape[2], b8.data_ptr() + b_row0 * ld8, gb.data_ptr() + 4 * b_row0, b8.shape[2],
+            ld8, plan.d, flat, len(pairs), c.data_ptr() + (r0 * plan.n + col0) * esz, plan.n,
+            self._stream()))
+
     def gemm_digit_rows(self, plan: ShardPlan, r0, rows, a8, ga, b8, gb, pairs, c):
         """gemm_digits for C rows [r0, r0 + rows) of this rank (c: all its rows)."""
         flat = (ctypes.c_int * (2 * len(pairs)))(*[v for p in pairs for v in p])
@@ -177,6 +190,12 @@ class GpuOps:
             plan.K, rows, plan.l, plan.n, a8.data_ptr() + r0 * ld8, ga.data_ptr() + 4 * r0,
             a8.shape[2], b8.data_ptr(), gb.data_ptr(), b8.shape[2], ld8, plan.d, flat, len(pairs),
             c.data_ptr() + r0 * plan.n * esz, plan.n, self._stream()))
+
+    def gemm_digit_cols(self, plan: ShardPlan, a8, ga, b8, gb, b_row0, col0, col1, pairs, c):
+        """gemm_digits for C columns [col0, col1) of this rank's rows, B digits from
+        plane rows [b_row0, b_row0 + col1 - col0) of b8 (its own plane height)."""
+        self.gemm_digit_block(plan, 0, plan.rows_local, a8, ga, b8, gb, b_row0, col0, col1,
+                              pairs, c)
 
     def gemm_digits(self, plan: ShardPlan, a8, ga, b8, gb, pairs, c):
         flat = (ctypes.c_int * (2 * len(pairs)))(*[v for p in pairs for v in p])
@@ -314,10 +333,22 @@ class ShardedOzaki:
             r0, r1 = bounds[q], bounds[q + 1]
             cur.wait_event(ev_a[q])
             ops.split_digit_rows(p.K, da[r0:r1], r1 - r0, p.l, p.l, p.d, 0, self.a8, r0, self.ga)
-            if q == 0 and comm is not None:
-                cur.wait_stream(comm)
-            ops.gemm_digit_rows(p, r0, r1 - r0, self.a8, self.ga, self.b8_cat, self.gb_cat,
-                                pairs, self.c)
+            if q == 0 and p.world > 1:
+                # band 0: the local B block while the gather is in flight
+                if p.c1 > p.c0:
+                    ops.gemm_digit_block(p, r0, r1 - r0, self.a8, self.ga, self.b8, self.gb, 0,
+                                         p.c0, p.c1, pairs, self.c)
+                if comm is not None:
+                    cur.wait_stream(comm)
+                for lo, hi in ((0, p.c0), (p.c1, p.n)):
+                    if hi > lo:
+                        ops.gemm_digit_block(p, r0, r1 - r0, self.a8, self.ga, self.b8_cat,
+                                             self.gb_cat, lo, lo, hi, pairs, self.c)
+            else:
+                if q == 0 and comm is not None:
+                    cur.wait_stream(comm)
+                ops.gemm_digit_rows(p, r0, r1 - r0, self.a8, self.ga, self.b8_cat, self.gb_cat,
+                                    pairs, self.c)
             done = torch.cuda.Event()
             done.record(cur)
             ys.wait_event(done)
@@ -332,7 +363,7 @@ class ShardedOzaki:
         Returns this rank's C rows (rows_local, n, K)."""
         p, ops = self.plan, self.ops
         if self.timing:
-            ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
             ev[0].record()
         a_rows = A[p.r0:p.r1] if A.shape[0] == p.m else A
         if hasattr(ops, "reset_flags"):
@@ -377,6 +408,16 @@ class ShardedOzaki:
             pairs = pruned_pairs(p.d, mx[0], mx[1], self.drop)
         else:
             pairs = triangular_pairs(p.d)
+        # INT8 engine, W > 1: this rank's own B column block is multiplied
+        # while the all-gather is still in flight, the other columns after it
+        # (C elements are independent: the same bits as one GEMM)
+        local_first = (self.engine == "int8" and p.world > 1 and p.rows_local and pairs
+                       and p.c1 > p.c0 and hasattr(ops, "gemm_digit_cols"))
+        if local_first:
+            ops.gemm_digit_cols(p, self.a8, self.ga, self.b8, self.gb, 0, p.c0, p.c1, pairs,
+                                self.c)
+        if self.timing:
+            ev[4].record()
         if comm is not None:
             torch.cuda.current_stream().wait_stream(comm)
         if self.timing:
@@ -384,6 +425,11 @@ class ShardedOzaki:
         if p.rows_local:
             if not pairs:
                 self.c.zero_()
+            elif local_first:
+                for lo, hi in ((0, p.c0), (p.c1, p.n)):
+                    if hi > lo:
+                        ops.gemm_digit_cols(p, self.a8, self.ga, self.b8_cat, self.gb_cat, lo,
+                                            lo, hi, pairs, self.c)
             elif self.engine == "int8":
                 ops.gemm_digits(p, self.a8, self.ga, self.b8_cat, self.gb_cat, pairs, self.c)
             else:
@@ -395,10 +441,12 @@ class ShardedOzaki:
             torch.cuda.current_stream().synchronize()
             if prof is not None:
                 # split = both splits; transfer = the part of the all-gather
-                # (+ maxima all-reduce) not hidden behind the A split
+                # (+ maxima all-reduce) not hidden behind the A split and the
+                # local-block GEMM; product = the GEMM work on either side
                 prof.split_seconds = ev[0].elapsed_time(ev[1]) * 1e-3
-                prof.transfer_seconds = ev[1].elapsed_time(ev[2]) * 1e-3
-                prof.product_seconds = ev[2].elapsed_time(ev[3]) * 1e-3
+                prof.transfer_seconds = ev[4].elapsed_time(ev[2]) * 1e-3
+                prof.product_seconds = (ev[1].elapsed_time(ev[4]) +
+                                        ev[2].elapsed_time(ev[3])) * 1e-3
                 prof.accumulate_seconds = 0.0
                 prof.total_seconds = ev[0].elapsed_time(ev[3]) * 1e-3
                 prof.split_count = p.d

@@ -78,6 +78,21 @@ class OracleDigitOps(OracleOps):
         c[:mr] = torch.from_numpy(acc.reshape(mr, n, K))
 
 
+    def gemm_digit_cols(self, plan, a8, ga, b8, gb, b_row0, col0, col1, pairs, c):
+        """C columns [col0, col1): the local B block (b8 = this rank's planes,
+        while the gather is in flight) or gathered rows [b_row0, ...)."""
+        assert b8.shape[2] in (plan.ncb, plan.world * plan.ncb)
+        assert b8.shape[2] == plan.world * plan.ncb or (b_row0, col0, col1) == (0, plan.c0, plan.c1)
+        self.cols_done = getattr(self, "cols_done", []) + [(col0, col1)]
+        K, l, w = plan.K, plan.l, col1 - col0
+        mr = plan.rows_local
+        acc = np.zeros((mr * w, K))
+        for (a, b) in pairs:
+            prod = a8[a, 0, :mr, :l].numpy() @ b8[b, 0, b_row0:b_row0 + w, :l].numpy().T
+            acc = self.port.mf_add_double(K, acc, prod.reshape(-1))
+        c[:mr, col0:col1] = torch.from_numpy(acc.reshape(mr, w, K))
+
+
 def _worker(rank, world, port_num, cases, q, digits=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port_num)
@@ -96,6 +111,11 @@ def _worker(rank, world, port_num, cases, q, digits=False):
             got = eng.run(torch.from_numpy(a), torch.from_numpy(b)).numpy()
             r0, r1 = eng.plan.r0, eng.plan.r1
             ok = np.array_equal(got.view(np.uint64), want[r0:r1].view(np.uint64))
+            if digits and r1 > r0 and eng.plan.c1 > eng.plan.c0:
+                # the local block went first, then the rest: every column once
+                cols = sorted(ops.cols_done)
+                ok = ok and cols[0][0] == 0 and cols[-1][1] == n and all(
+                    x[1] == y[0] for x, y in zip(cols, cols[1:]))
             q.put((rank, (K, m, l, n, d, drop), bool(ok)))
     finally:
         dist.destroy_process_group()
