@@ -1412,31 +1412,11 @@ ozk_status ozk_ozaki_gemm_multi(ozk_format fmt, int ngpus, const int* devices, s
         b8_of[r] = b8.as<int8_t>();
         gb_of[r] = gb.as<int>();
         bar.arrive_and_wait();  // every device has split its block
-        // 2. all-gather of the B digit planes and exponents by peer copies
+        // 2. pair list (global slice maxima with pruning: every device's
+        // maxima are in after the barrier)
+        PairList pl;
+        std::vector<int> flat;
         if (ok && !failed) {
-            for (int q = 0; q < ngpus && ok; ++q) {
-                if (q == r) continue;
-                const size_t q0 = std::min(n, (size_t)q * ncb), q1 = std::min(n, q0 + ncb);
-                if (q1 <= q0) continue;
-                for (int s2 = 0; s2 < d * nd && ok; ++s2) {
-                    const size_t off = ((size_t)s2 * n_pad + q0) * ld8;
-                    ok = cuda_ok(cudaMemcpyPeerAsync(b8_of[r] + off, dev_of(r), b8_of[q] + off,
-                                                     dev_of(q), (q1 - q0) * ld8, os.s),
-                                 "ozaki_gemm_multi: peer copy");
-                }
-                for (int s2 = 0; s2 < d && ok; ++s2) {
-                    const size_t off = (size_t)s2 * n_pad + q0;
-                    ok = cuda_ok(cudaMemcpyPeerAsync(gb_of[r] + off, dev_of(r), gb_of[q] + off,
-                                                     dev_of(q), (q1 - q0) * sizeof(int), os.s),
-                                 "ozaki_gemm_multi: peer copy");
-                }
-            }
-            if (ok) ok = cuda_ok(cudaStreamSynchronize(os.s), "ozaki_gemm_multi: gather");
-        }
-        bar.arrive_and_wait();  // no device frees what a peer still reads
-        // 3. pair list (global slice maxima with pruning), GEMM, C rows back
-        if (ok && !failed && rows) {
-            PairList pl;
             if (drop > 0.0) {
                 std::vector<double> am(d, 0.0), bm(d, 0.0);
                 for (int q = 0; q < ngpus; ++q)
@@ -1449,19 +1429,60 @@ ozk_status ozk_ozaki_gemm_multi(ozk_format fmt, int ngpus, const int* devices, s
                 triangular_pairs(d, pl);
             }
             pairs_used = pl.count;
-            if (pl.count == 0) {
-                ok = cuda_ok(cudaMemsetAsync(dc.p, 0, eb * rows * n, os.s), "memset C");
-            } else {
-                std::vector<int> flat(2 * (size_t)pl.count);
-                for (int p = 0; p < pl.count; ++p) {
-                    flat[2 * p] = pl.alpha[p];
-                    flat[2 * p + 1] = pl.beta[p];
-                }
-                const ozk_status s2 = ozk_digits_gemm_device(
-                    fmt, rows, l, n, a8.as<int8_t>(), ga.as<int>(), rows, b8.as<int8_t>(),
-                    gb.as<int>(), n_pad, ld8, d, flat.data(), pl.count, dc.p, n, os.s);
-                if (s2 != OZK_OK) fail_here(s2), ok = false;
+            flat.resize(2 * (size_t)pl.count);
+            for (int p = 0; p < pl.count; ++p) {
+                flat[2 * p] = pl.alpha[p];
+                flat[2 * p + 1] = pl.beta[p];
             }
+        }
+        // C columns [q0, q1) of this device's rows from the digit planes at
+        // plane rows [q0, q1) (the n_pad layout: column j is plane row j)
+        auto gemm_cols = [&](size_t q0, size_t q1) -> bool {
+            if (!rows || q1 <= q0 || pl.count == 0) return true;
+            const ozk_status s2 = ozk_digits_gemm_device_async(
+                fmt, rows, l, q1 - q0, a8.as<int8_t>(), ga.as<int>(), rows,
+                b8.as<int8_t>() + q0 * ld8, gb.as<int>() + q0, n_pad, ld8, d, flat.data(),
+                pl.count, static_cast<char*>(dc.p) + q0 * eb, n, os.s);
+            if (s2 != OZK_OK) fail_here(s2);
+            return s2 == OZK_OK;
+        };
+        // 3. the device's own B column block is multiplied while the other
+        // blocks arrive: all-gather of the B digit planes and exponents by peer
+        // copies on a second stream (C elements are independent: the same bits
+        // as one GEMM over all columns)
+        OwnStream cs;
+        if (ok && !failed) ok = cuda_ok(cs.create(), "ozaki_gemm_multi: stream");
+        if (ok && !failed) ok = gemm_cols(c0, c1);
+        if (ok && !failed) {
+            for (int q = 0; q < ngpus && ok; ++q) {
+                if (q == r) continue;
+                const size_t q0 = std::min(n, (size_t)q * ncb), q1 = std::min(n, q0 + ncb);
+                if (q1 <= q0) continue;
+                for (int s2 = 0; s2 < d * nd && ok; ++s2) {
+                    const size_t off = ((size_t)s2 * n_pad + q0) * ld8;
+                    ok = cuda_ok(cudaMemcpyPeerAsync(b8_of[r] + off, dev_of(r), b8_of[q] + off,
+                                                     dev_of(q), (q1 - q0) * ld8, cs.s),
+                                 "ozaki_gemm_multi: peer copy");
+                }
+                for (int s2 = 0; s2 < d && ok; ++s2) {
+                    const size_t off = (size_t)s2 * n_pad + q0;
+                    ok = cuda_ok(cudaMemcpyPeerAsync(gb_of[r] + off, dev_of(r), gb_of[q] + off,
+                                                     dev_of(q), (q1 - q0) * sizeof(int), cs.s),
+                                 "ozaki_gemm_multi: peer copy");
+                }
+            }
+        }
+        if (cs.s) {
+            const bool synced = cuda_ok(cudaStreamSynchronize(cs.s), "ozaki_gemm_multi: gather");
+            ok = ok && synced;
+        }
+        bar.arrive_and_wait();  // no device frees what a peer still reads
+        // 4. the gathered columns on either side, C rows back
+        if (ok && !failed && rows) {
+            if (pl.count == 0)
+                ok = cuda_ok(cudaMemsetAsync(dc.p, 0, eb * rows * n, os.s), "memset C");
+            else
+                ok = gemm_cols(0, c0) && gemm_cols(c1, n);
             if (ok)
                 ok = cuda_ok(cudaMemcpyAsync(static_cast<char*>(c) + r0 * n * eb, dc.p,
                                              rows * n * eb, cudaMemcpyDeviceToHost, os.s),
