@@ -14,8 +14,11 @@
 // cached process-wide and handed out one per concurrent call (the entry points
 // are reentrant).
 #include <cuda_runtime.h>
+#include <emmintrin.h>
 
 #include <atomic>
+#include <cstdint>
+#include <cstdlib>
 #include <condition_variable>
 #include <cstring>
 #include <deque>
@@ -85,6 +88,41 @@ void release_slots(std::unique_ptr<SlotSet> s) {
     g_free_slots.push_back(std::move(s));
 }
 
+// Copies of staged chunks use non-temporal (streaming) 16-byte stores: the
+// destination (a pinned slot, or the caller's C buffer) is not read again by
+// this thread, and plain stores would first read every destination line
+// (read-for-ownership) -- a third more host-memory traffic on a path that is
+// bound by it ($OZK_STAGING_NT=0: plain memcpy, for A/B runs).
+bool staging_nt() {  // read per chunk (cheap next to a 2 MB copy): A/B in one process
+    const char* v = std::getenv("OZK_STAGING_NT");
+    return !(v && !std::strcmp(v, "0"));
+}
+
+void stream_copy(char* dst, const char* src, size_t n) {
+    if (n < 4096 || !staging_nt()) {
+        std::memcpy(dst, src, n);
+        return;
+    }
+    const size_t head = (16 - (reinterpret_cast<uintptr_t>(dst) & 15)) & 15;
+    std::memcpy(dst, src, head);
+    dst += head;
+    src += head;
+    n -= head;
+    const size_t body = n & ~size_t(63);
+    for (size_t i = 0; i < body; i += 64) {
+        const __m128i a = _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + i));
+        const __m128i b = _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + i + 16));
+        const __m128i c = _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + i + 32));
+        const __m128i d = _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + i + 48));
+        _mm_stream_si128(reinterpret_cast<__m128i*>(dst + i), a);
+        _mm_stream_si128(reinterpret_cast<__m128i*>(dst + i + 16), b);
+        _mm_stream_si128(reinterpret_cast<__m128i*>(dst + i + 32), c);
+        _mm_stream_si128(reinterpret_cast<__m128i*>(dst + i + 48), d);
+    }
+    std::memcpy(dst + body, src + body, n - body);
+    _mm_sfence();  // the streamed lines are globally visible before the DMA / the caller
+}
+
 // A team of host threads for one parallel memcpy at a time (the caller is
 // member 0).
 class Team {
@@ -106,11 +144,11 @@ public:
         auto part = [=](int i) {
             if (rows == 1) {  // one long row: split the bytes
                 const size_t b0 = width * i / n_, b1 = width * (i + 1) / n_;
-                std::memcpy(dst + b0, src + b0, b1 - b0);
+                stream_copy(dst + b0, src + b0, b1 - b0);
                 return;
             }
             const size_t r0 = rows * i / n_, r1 = rows * (i + 1) / n_;
-            for (size_t r = r0; r < r1; ++r) std::memcpy(dst + r * dpitch, src + r * spitch, width);
+            for (size_t r = r0; r < r1; ++r) stream_copy(dst + r * dpitch, src + r * spitch, width);
         };
         if (n_ == 1) {
             part(0);

@@ -37,6 +37,13 @@ def run(a, b, c):
 
 
 print(f"pinned: {run(ha.data_ptr(), hb.data_ptr(), hc.data_ptr()):.1f} ms", flush=True)
+if "--nt" in sys.argv:  # streaming-store copies on / off, default thread counts
+    for nt in ["1", "0", "1", "0"]:
+        os.environ["OZK_STAGING_NT"] = nt
+        r = run(pa.ctypes.data, pb.ctypes.data, pc.ctypes.data)
+        print(f"pageable staged, OZK_STAGING_NT={nt}: {r:.1f} ms", flush=True)
+    assert np.array_equal(pc.view(np.uint64), hc.numpy().view(np.uint64))
+    sys.exit(0)
 for th in ["4,2", "4,4", "8,4", "8,8", "12,4", "16,8", "6,6"]:
     os.environ["OZK_STAGING_THREADS"] = th
     print(f"pageable staged threads {th}: {run(pa.ctypes.data, pb.ctypes.data, pc.ctypes.data):.1f} ms",
