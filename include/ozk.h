@@ -22,7 +22,9 @@
  *  - no exception crosses the ABI: every call returns an ozk_status and
  *    ozk_last_error() (thread-local) describes the last failure.  The status
  *    codes map 1:1 onto the reference's exception types (errors.hpp:7-25) and
- *    are raised for the same conditions in the same order.
+ *    are raised for the same conditions in the same order.  A null matrix
+ *    pointer (which the reference's references cannot express) is refused
+ *    with OZK_EPARAM after those checks, before any device work.
  *
  * All functions are reentrant (the reference calls its backend from an
  * OpenMP parallel loop, ozaki.hpp:224-231); host-buffer entry points use a
