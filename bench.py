@@ -98,6 +98,14 @@ class ClockSampler:
         self.index = index
         self.proc = None
         self.path = None
+        self.skip = 0
+
+    def _lines(self):
+        try:
+            with open(self.path) as f:
+                return sum(1 for _ in f)
+        except OSError:
+            return 0
 
     def start(self):
         try:
@@ -109,6 +117,14 @@ class ClockSampler:
                 stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
         except (OSError, FileNotFoundError):
             self.proc = None
+            return
+        # nvidia-smi takes a while to start: wait (outside the timed region)
+        # for its first line so short timed regions are sampled too, and
+        # drop the lines written before the region starts
+        t0 = time.monotonic()
+        while self._lines() == 0 and time.monotonic() - t0 < 5.0 and self.proc.poll() is None:
+            time.sleep(0.02)
+        self.skip = self._lines()
 
     def stop(self):
         if self.proc is None:
@@ -118,8 +134,13 @@ class ClockSampler:
             self.proc.wait(timeout=5)
         except subprocess.TimeoutExpired:
             self.proc.kill()
+        lines = open(self.path).read().splitlines()
+        if len(lines) > self.skip:
+            lines = lines[self.skip:]
+        else:  # the region was shorter than one sampling period: the last sample
+            lines = lines[-1:]
         rows = []
-        for line in open(self.path):
+        for line in lines:
             parts = [x.strip() for x in line.split(",")]
             if len(parts) < 9:
                 continue
