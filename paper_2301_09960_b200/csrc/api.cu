@@ -457,10 +457,19 @@ struct HostOverlap {
 // forced (optional): the pair list to use instead of the one from this call's
 // own slice maxima (ozk_ozaki_gemm_multi: one list from the global maxima of
 // every device's rows).
+// lu (optional, binary64 formats): the blocked-LU trailing update -- the
+// finished sum is subtracted from the m x n block lu->a22 (row stride lu->lda
+// elements) by the slice-GEMM epilogue of the last pair, and c is only the
+// running-sum scratch.
+struct LuTarget {
+    double* a22;
+    size_t lda;
+};
 ozk_status ozaki_device_impl(int fmt, size_t m, size_t l, size_t n, const void* a, size_t lda,
                              const void* b, size_t ldb, int d, double drop, void* c,
                              cudaStream_t st, ozk_profile* prof,
-                             const HostOverlap* ov = nullptr, const PairList* forced = nullptr) {
+                             const HostOverlap* ov = nullptr, const PairList* forced = nullptr,
+                             const LuTarget* lu = nullptr) {
     const int K = words_of(fmt), wb = word_bytes_of(fmt);
     const int sms = num_sms_cached();
     const size_t ldk = slice_ld(l);
@@ -591,6 +600,10 @@ ozk_status ozaki_device_impl(int fmt, size_t m, size_t l, size_t n, const void* 
         op.d = d;
         op.c = static_cast<char*>(c) + (r0 * n + c0) * eb;
         op.ldc = n;
+        if (lu) {
+            op.lu_a22 = lu->a22 + (r0 * lu->lda + c0) * K;
+            op.lu_lda = lu->lda;
+        }
         return launch_pair_gemm_i8(K, wb, op, pl, st, sms);
     };
     auto split_a_band = [&](size_t r0, size_t rows) -> cudaError_t {
@@ -686,6 +699,10 @@ ozk_status ozaki_device_impl(int fmt, size_t m, size_t l, size_t n, const void* 
         }
         if (pl.count == 0) {  // every pair pruned (drop_threshold > 1): C = 0
             OZK_CUDA(cudaMemsetAsync(cb, 0, eb * rows * n, st), "ozaki_gemm: zero C");
+            if (lu)  // A22 -= 0, through the reference's subtraction
+                OZK_CUDA(launch_kw_sub_inplace(K, lu->a22 + r0 * lu->lda * K, lu->lda,
+                                               reinterpret_cast<const double*>(cb), rows, n, st),
+                         "ozaki_gemm: LU subtract");
             if (blocked_b && band == 0)  // the B blocks still arrive in order (nothing to split)
                 for (int j = 0; j < ov->b_blocks; ++j)
                     OZK_CUDA(ov->wait(st, ov->b_block_ready[j]), "ozaki_gemm: wait B");
@@ -708,7 +725,12 @@ ozk_status ozaki_device_impl(int fmt, size_t m, size_t l, size_t n, const void* 
             pb.a = prob.a + r0 * ldk;
             pb.m = rows;
             pb.c = cb;
-            OZK_CUDA(launch_pair_gemm(K, kAccumulate, pb, pl, st, sms, wb), "ozaki_gemm: slice GEMM");
+            if (lu) {
+                pb.lu_a22 = lu->a22 + r0 * lu->lda * K;
+                pb.lu_lda = lu->lda;
+            }
+            OZK_CUDA(launch_pair_gemm(K, lu ? kAccumulateLU : kAccumulate, pb, pl, st, sms, wb),
+                     "ozaki_gemm: slice GEMM");
         }
         if (ov && ov->on_band) OZK_CUDA(ov->on_band(r0, r0 + rows), "ozaki_gemm: band copy");
     }
@@ -1909,14 +1931,14 @@ ozk_status ozk_lu_trailing_update_device(ozk_format fmt, size_t tm, size_t pw, s
     if (ozk_status s = need({l21, u12, a22}, "lu_trailing_update")) return s;
     cudaStream_t st = (cudaStream_t)stream;
     const int K = (int)fmt;
-    DevBuf upd;
-    OZK_CUDA(upd.alloc(sizeof(double) * K * tm * tn, st), "lu_trailing_update: update");
-    if (ozk_status s = ozaki_device_impl(K, tm, pw, tn, l21, ldl, u12, ldu, d, 0.0, upd.p, st,
-                                         nullptr))
+    // the running sum lives in `sum`; the last pair's epilogue subtracts it
+    // from A22 in place (no separate update matrix pass)
+    DevBuf sum;
+    OZK_CUDA(sum.alloc(sizeof(double) * K * tm * tn, st), "lu_trailing_update: sum");
+    const LuTarget lt{static_cast<double*>(a22), lda};
+    if (ozk_status s = ozaki_device_impl(K, tm, pw, tn, l21, ldl, u12, ldu, d, 0.0, sum.p, st,
+                                         nullptr, nullptr, nullptr, &lt))
         return s;
-    OZK_CUDA(launch_kw_sub_inplace(K, static_cast<double*>(a22), lda, upd.as<double>(), tm, tn,
-                                   st),
-             "lu_trailing_update: subtract");
     OZK_CUDA(cudaStreamSynchronize(st), "lu_trailing_update");
     return OZK_OK;
 }

@@ -164,6 +164,7 @@ pair_gemm_kernel(const __grid_constant__ TmaMaps maps, const __grid_constant__ P
     const int num_tiles = tiles_m * tiles_n_blk * prob.nblk;
     const int num_kb = (int)((prob.l + BK - 1) / BK);
     const int npairs = pairs.count;
+    constexpr bool kAcc = MODE == kAccumulate || MODE == kAccumulateLU;
     const int nworkers = gridDim.x * kGroups;
 
     if (threadIdx.x == 0) {
@@ -299,7 +300,7 @@ pair_gemm_kernel(const __grid_constant__ TmaMaps maps, const __grid_constant__ P
                     stage = 0;
                     phase ^= 1;
                 }
-                if constexpr (MODE == kAccumulate) {
+                if constexpr (kAcc) {
                     if (kb == num_kb - kPrefetchKb && (p > 0 || prob.c_continue)) {
                         // pull this pair's C rows into L2 ahead of the read-modify-write
 #pragma unroll
@@ -339,7 +340,7 @@ pair_gemm_kernel(const __grid_constant__ TmaMaps maps, const __grid_constant__ P
                     y[q] = v;
                 }
                 const size_t row = row0 + mf * 8;
-                if constexpr (MODE == kAccumulate) {
+                if constexpr (kAcc) {
                     // batch: load the 8 K-word elements of this row first
                     W w[8][K];
                     W* cp = static_cast<W*>(prob.c) + (row * prob.ldc + col0) * K;
@@ -358,6 +359,27 @@ pair_gemm_kernel(const __grid_constant__ TmaMaps maps, const __grid_constant__ P
 #pragma unroll
                     for (int q = 0; q < 8; ++q) kw_add<K, W, true, true>(w[q], (W)y[q]);
 #endif
+                    if constexpr (MODE == kAccumulateLU) {
+                        if (prob.lu_final && p == npairs - 1) {
+                            // the list's last pair: A22 -= sum (lu.hpp:121-124,
+                            // MultiFloat -= MultiFloat = x + (-y), multifloat.hpp:
+                            // 300,178-199) in place of the C store
+                            double* ap = prob.lu_a22 + (row * prob.lu_lda + col0) * K;
+#pragma unroll
+                            for (int q = 0; q < 8; ++q) {
+                                if (!((cmask >> q) & 1u)) continue;
+                                const int off = ((q >> 1) * 8 + (q & 1)) * K;
+                                double x[K], ny[K];
+#pragma unroll
+                                for (int k = 0; k < K; ++k) x[k] = ap[off + k];
+                                kw_neg<K>(w[q], ny);
+                                kw_add_kw<K>(x, ny);
+#pragma unroll
+                                for (int k = 0; k < K; ++k) ap[off + k] = x[k];
+                            }
+                            continue;
+                        }
+                    }
 #pragma unroll
                     for (int q = 0; q < 8; ++q) {
                         const int off = ((q >> 1) * 8 + (q & 1)) * K;
@@ -458,6 +480,15 @@ cudaError_t launch_chunk(int K, GemmMode mode, const GemmProblem& prob, const Pa
         return launch_typed<3, kAccumulate, float>(prob, pairs, st, num_sms);
     }
     if (mode == kStoreProducts) return launch_typed<1, kStoreProducts>(prob, pairs, st, num_sms);
+    if (mode == kAccumulateLU) {
+        if (word_bytes != 8) return cudaErrorInvalidValue;
+        switch (K) {
+        case 2: return launch_typed<2, kAccumulateLU>(prob, pairs, st, num_sms);
+        case 3: return launch_typed<3, kAccumulateLU>(prob, pairs, st, num_sms);
+        case 4: return launch_typed<4, kAccumulateLU>(prob, pairs, st, num_sms);
+        default: return cudaErrorInvalidValue;
+        }
+    }
     switch (K) {
     case 2: return launch_typed<2, kAccumulate>(prob, pairs, st, num_sms);
     case 3: return launch_typed<3, kAccumulate>(prob, pairs, st, num_sms);
@@ -474,7 +505,9 @@ cudaError_t launch_pair_gemm(int K, GemmMode mode, const GemmProblem& prob, cons
                              cudaStream_t st, int num_sms, int word_bytes) {
     for (int q0 = 0; q0 < pairs.count; q0 += kPairsPerLaunch) {
         GemmProblem pb = prob;
-        if (mode == kAccumulate) pb.c_continue = prob.c_continue || q0 > 0;
+        if (mode == kAccumulate || mode == kAccumulateLU)
+            pb.c_continue = prob.c_continue || q0 > 0;
+        pb.lu_final = q0 + kPairsPerLaunch >= pairs.count;
         if (mode == kStoreProducts) pb.c = static_cast<double*>(prob.c) + q0 * prob.c_pair_stride;
         const cudaError_t e = launch_chunk(K, mode, pb, pair_chunk(pairs, q0), st, num_sms,
                                            word_bytes);

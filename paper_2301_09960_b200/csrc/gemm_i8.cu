@@ -204,6 +204,11 @@ struct I8Problem {
     // started global step s = wave * npairs + pair; null disables pacing
     unsigned int* pace;
     int pace_slack;
+    // LU: after the list's last pair, A22 -= sum (row stride lu_lda) instead of
+    // the C store (lu_final: this launch holds the last pair)
+    double* lu_a22;
+    size_t lu_lda;
+    int lu_final;
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -564,8 +569,10 @@ __device__ __forceinline__ void trace_stamp(int, int, bool) {}
 // PR (parity hook, ozk_pair_products_digits_device): instead of the K-word
 // accumulation, every exact slice product C_ab is stored as binary64 into its
 // own plane (products[p][row][col]).
+// LU (blocked-LU trailing update, ozk_lu_trailing_update): the list's last
+// pair subtracts the finished K-word sum from A22 in place of the C store.
 template <int K, typename W, int ND, int TR, int EG, bool kVec, int CM, int CN, int NB,
-          bool PR = false>
+          bool PR = false, bool LU = false>
 __global__ void __launch_bounds__(I8Cfg<K, W, ND, TR, EG, NB>::kThreads, 1)
 pair_gemm_i8_kernel(const __grid_constant__ MapsI8 maps, const __grid_constant__ PairChunk pairs,
                     I8Problem prob, int tiles_m, int tiles_n) {
@@ -853,6 +860,7 @@ pair_gemm_i8_kernel(const __grid_constant__ MapsI8 maps, const __grid_constant__
                     tbufq[q] = tlane + ((step + q) % NB) * kBufCols;
                 }
                 const bool first = p == 0 && prob.c_init;  // C starts from zero
+                const bool lu_last = LU && prob.lu_final && p + np == npairs;
                 trace_stamp(step, 3, tracer);
                 for (int q = 0; q < np; ++q)
                     mbar_wait(tfull0 + 8 * ((step + q) % NB), ((step + q) / NB) & 1);
@@ -951,6 +959,21 @@ pair_gemm_i8_kernel(const __grid_constant__ MapsI8 maps, const __grid_constant__
                     for (int j = 0; j < (PR ? 0 : kChunk); ++j) {
                         const size_t rr = row0 + r + j;
                         if (col_ok && rr < prob.m) {
+                            if constexpr (LU) {
+                                if (lu_last) {
+                                    // A22 -= sum (lu.hpp:121-124; MultiFloat -=
+                                    // MultiFloat = x + (-y), multifloat.hpp:300,178-199)
+                                    double* ap = prob.lu_a22 + (rr * prob.lu_lda + col) * K;
+                                    double x[K], ny[K];
+#pragma unroll
+                                    for (int k = 0; k < K; ++k) x[k] = ap[k];
+                                    kw_neg<K>(w[j], ny);
+                                    kw_add_kw<K>(x, ny);
+#pragma unroll
+                                    for (int k = 0; k < K; ++k) ap[k] = x[k];
+                                    continue;
+                                }
+                            }
                             const size_t e = rr * prob.ldc + col;
                             st_kword<K>(cbase + e * K, (int)(e & 1), kVec, w[j], cpol);
                         }
@@ -1055,7 +1078,7 @@ I8Geometry geometry_typed(int num_sms) {
 template <int K, typename W, int ND, int TR, int EG = 2, int CM = 1, int CN = 1, int NB = 2,
           bool PR = false>
 cudaError_t launch_i8_chunk(const I8Operands& op, const PairChunk& pairs, cudaStream_t st,
-                            int num_sms) {
+                            int num_sms, bool lu_final) {
     using Cfg = I8Cfg<K, W, ND, TR, EG, NB>;
     auto encode = get_encode_i8();
     if (!encode) return cudaErrorNotSupported;
@@ -1096,13 +1119,23 @@ cudaError_t launch_i8_chunk(const I8Operands& op, const PairChunk& pairs, cudaSt
     prob.c_init = op.c_init ? 1 : 0;
     prob.pace = nullptr;
     prob.pace_slack = OZK_I8_PACE;
+    prob.lu_a22 = op.lu_a22;
+    prob.lu_lda = op.lu_lda;
+    prob.lu_final = lu_final ? 1 : 0;
     const bool vec = !PR && sizeof(W) == 8 && (reinterpret_cast<uintptr_t>(op.c) & 15) == 0;
     const int tiles_m = (int)((op.m + TR - 1) / TR), tiles_n = (int)((op.n + TC - 1) / TC);
     const int num_tiles = tiles_m * tiles_n;
     if (num_tiles == 0 || pairs.count == 0) return cudaSuccess;
     auto kern = pair_gemm_i8_kernel<K, W, ND, TR, EG, false, CM, CN, NB, PR>;
-    if constexpr (sizeof(W) == 8 && !PR)
-        if (vec) kern = pair_gemm_i8_kernel<K, W, ND, TR, EG, true, CM, CN, NB>;
+    if constexpr (sizeof(W) == 8 && !PR) {
+        if (op.lu_a22)
+            kern = vec ? pair_gemm_i8_kernel<K, W, ND, TR, EG, true, CM, CN, NB, false, true>
+                       : pair_gemm_i8_kernel<K, W, ND, TR, EG, false, CM, CN, NB, false, true>;
+        else if (vec)
+            kern = pair_gemm_i8_kernel<K, W, ND, TR, EG, true, CM, CN, NB>;
+    } else if (op.lu_a22) {
+        return cudaErrorInvalidValue;  // binary64 formats only
+    }
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          Cfg::kSmemBytes);
     if (e != cudaSuccess) return e;
@@ -1150,7 +1183,7 @@ cudaError_t launch_i8_typed(const I8Operands& op, const PairList& pairs, cudaStr
         o.c_init = op.c_init && q0 == 0;
         if (PR) o.c = static_cast<double*>(op.c) + q0 * op.pair_stride;
         const cudaError_t e = launch_i8_chunk<K, W, ND, TR, EG, CM, CN, NB, PR>(
-            o, pair_chunk(pairs, q0), st, num_sms);
+            o, pair_chunk(pairs, q0), st, num_sms, q0 + kPairsPerLaunch >= pairs.count);
         if (e != cudaSuccess) return e;
     }
     return cudaSuccess;

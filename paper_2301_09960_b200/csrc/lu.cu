@@ -1,6 +1,8 @@
-// lu.cu -- the blocked-LU trailing update's K-word subtraction,
-// A22(i, j) -= update(i, j) (proj/include/mpmat/lu.hpp:121-124), where
-// `update` is the Ozaki product L21 * U12 computed by the slice GEMM.
+// lu.cu -- the blocked-LU trailing update's K-word subtraction as a separate
+// pass, A22(i, j) -= update(i, j) (proj/include/mpmat/lu.hpp:121-124).  The
+// slice GEMMs fuse it into their last pair's epilogue (LuTarget in api.cu);
+// this pass serves the one case without a last pair (every pair pruned:
+// A22 -= 0 still goes through the reference's subtraction).
 // The subtraction is MultiFloat<K>::operator-=(MultiFloat<K>)
 // (multifloat.hpp:300,201: x + (-y)), replayed by kw_add_kw (kword.cuh).
 // Memory-bound elementwise pass: 3*K*8 bytes per element.

@@ -63,7 +63,10 @@ cudaError_t launch_transpose(int K, int word_bytes, const void* in, size_t in_ld
                              size_t out_ld, size_t rows, size_t cols, cudaStream_t st);
 
 // Slice-pair GEMM with fused epilogue (K2 + K3).
-enum GemmMode : int { kStorePlain = 0, kAccumulate = 1, kStoreProducts = 2 };
+// kAccumulateLU: kAccumulate whose final pair subtracts the finished sum from
+// an A22 block instead of storing it (the blocked-LU trailing update,
+// lu.hpp:121-124, fused into the slice-GEMM epilogue)
+enum GemmMode : int { kStorePlain = 0, kAccumulate = 1, kStoreProducts = 2, kAccumulateLU = 3 };
 
 // Host-side pair list (alpha-major, ozaki.hpp:210-221), any length.
 struct PairList {
@@ -114,6 +117,9 @@ struct GemmProblem {
     size_t c_pair_stride;  // kStoreProducts: doubles between consecutive pair products
     uint32_t zero;         // always 0 (runtime value: carries a register dependency)
     uint32_t c_continue;   // kAccumulate: 1 = C already holds a running sum (later pair chunk)
+    double* lu_a22;        // kAccumulateLU: A22 block (K-word, row stride lu_lda elements)
+    size_t lu_lda;
+    uint32_t lu_final;     // kAccumulateLU: this launch holds the list's last pair
 };
 
 cudaError_t launch_pair_gemm(int K, GemmMode mode, const GemmProblem& prob, const PairList& pairs,
@@ -136,6 +142,11 @@ struct I8Operands {
     size_t ldc;
     bool c_init = true;      // the first pair starts C from zero (false: accumulate onto C)
     size_t pair_stride = 0;  // launch_pair_products_i8: doubles between pair planes
+    // blocked-LU trailing update (binary64 formats): after the list's last pair
+    // the sum is subtracted from A22 (row stride lu_lda elements) instead of
+    // being stored to C, which then only carries the running sum
+    double* lu_a22 = nullptr;
+    size_t lu_lda = 0;
 };
 // Tile geometry of the INT8 slice GEMM for a format: C rows and columns per
 // cluster tile and the number of co-resident persistent clusters (one wave =

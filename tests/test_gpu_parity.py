@@ -435,14 +435,22 @@ def test_accuracy_t2_bound(ozk, port, K, dmax, ulp):
         assert ex.componentwise_ulp_error(got, a, b, ref, ulp) <= 4.0
 
 
-@pytest.mark.parametrize("K,n,j0,pw,d", [(2, 40, 8, 8, 6), (3, 64, 16, 16, 9), (4, 50, 10, 7, 12),
-                                         (2, 300, 32, 32, 6), (2, 129, 0, 1, 4)])
-def test_lu_trailing_update_bitexact(ozk, ref, K, n, j0, pw, d):
+@pytest.mark.parametrize("K,n,j0,pw,d,eng", [
+    (2, 40, 8, 8, 6, "auto"), (3, 64, 16, 16, 9, "auto"), (4, 50, 10, 7, 12, "auto"),
+    (2, 300, 32, 32, 6, "auto"), (2, 129, 0, 1, 4, "auto"),
+    # panels wider than 128: the INT8 engine's fused subtraction (and DMMA's)
+    (2, 420, 30, 160, 6, "auto"), (3, 430, 20, 200, 9, "auto"), (4, 390, 10, 150, 12, "auto"),
+    (3, 430, 20, 200, 9, "dmma"),
+    # 820 pairs = two launches: only the last one subtracts
+    (2, 330, 0, 140, 40, "auto"), (2, 200, 0, 64, 40, "auto")])
+def test_lu_trailing_update_bitexact(ozk, ref, engine, K, n, j0, pw, d, eng):
     """the blocked-LU trailing update A22 -= L21*U12
     (lu.hpp:104-124) on strided blocks of the full matrix, bit-identical to the
-    reference's own ozaki_gemm + MultiFloat operator-=."""
+    reference's own ozaki_gemm + MultiFloat operator-= -- with the subtraction
+    fused into the last pair's epilogue of either engine."""
     if ref is None:
         pytest.skip("oracle/_ref not built")
+    engine(eng)
     w = ref.gen_eq1(K, n, n, 90 + n)
     tm = n - j0 - pw
     l21 = w[j0 + pw:, j0:j0 + pw]
