@@ -5,13 +5,18 @@ pruning threshold, Eq. (1) or exponent-spread inputs, zero rows/columns, host
 or device API, auto or forced-DMMA engine.  Every C must be bit-identical to
 the reference's (D >= 2; D = 1 products round, as in the reference).
 """
+import os
+
 import numpy as np
 import pytest
 
 pytestmark = pytest.mark.gpu
 
 TS = 0x103
-SEEDS = list(range(160))
+# $OZK_FUZZ_SEEDS=a:b runs seeds [a, b) instead (extended sweeps,
+# profiles/r02_fuzz_extended.log)
+_span = os.environ.get("OZK_FUZZ_SEEDS")
+SEEDS = list(range(*map(int, _span.split(":")))) if _span else list(range(160))
 
 
 def _case(seed):
