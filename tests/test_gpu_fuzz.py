@@ -73,7 +73,11 @@ def test_random_gemm_bitexact(ozk, cpu, port, seed):
                            f"first {divmod(int(bad[0]), n)}")
 
 
-@pytest.mark.parametrize("seed", list(range(16)))
+_span_mt = os.environ.get("OZK_FUZZ_MT_SEEDS")
+MT_SEEDS = list(range(*map(int, _span_mt.split(":")))) if _span_mt else list(range(16))
+
+
+@pytest.mark.parametrize("seed", MT_SEEDS)
 def test_random_gemm_bitexact_multi_tile(ozk, cpu, port, seed):
     """Larger seeded cases (300-700 rows/columns: several tiles, waves and
     paced clusters of the INT8 engine; D <= 6 keeps the CPU oracle fast)."""
