@@ -116,3 +116,43 @@ def test_random_gemm_bitexact_large_d(ozk, cpu, port, seed):
     assert prof.pairs == d * (d + 1) // 2
     u = np.uint32 if fmt == TS else np.uint64
     assert np.array_equal(got.view(u), want.view(u)), (fmt, m, l, n, d)
+
+
+_span_lu = os.environ.get("OZK_FUZZ_LU_SEEDS")
+LU_SEEDS = list(range(*map(int, _span_lu.split(":")))) if _span_lu else list(range(12))
+
+
+@pytest.mark.parametrize("seed", LU_SEEDS)
+def test_random_lu_update_bitexact(ozk, ref, seed):
+    """Seeded blocked-LU trailing updates A22 -= L21*U12 (lu.hpp:104-124) with the
+    subtraction fused into the last pair's epilogue: random format, trailing
+    shape, panel width on both sides of 128 (DMMA / INT8 engine), split count,
+    forced-DMMA engine, on strided blocks of the full matrix -- bit-identical
+    to the reference's ozaki_gemm + MultiFloat operator-=."""
+    if ref is None:
+        pytest.skip("oracle/_ref not built")
+    rng = np.random.default_rng(9000 + seed)
+    K = [2, 3, 4][seed % 3]
+    pw = int(rng.integers(1, 97)) if rng.random() < 0.4 else int(rng.integers(129, 260))
+    j0 = int(rng.integers(0, 40))
+    tm, tn = (int(x) for x in rng.integers(1, 300, 2))
+    n = j0 + pw + max(tm, tn)
+    d = int(rng.integers(2, {2: 8, 3: 11, 4: 14}[K] + 1))
+    dmma = bool(rng.random() < 0.25)
+    w = ref.gen_eq1(K, n, n, 70 + seed)
+    r0, c0 = j0 + pw, j0 + pw
+    l21 = w[r0:r0 + tm, j0:j0 + pw]
+    u12 = w[j0:j0 + pw, c0:c0 + tn]
+    want = ref.lu_update(K, l21, u12, w[r0:r0 + tm, c0:c0 + tn], d)
+    got = w.copy()
+    ozk.set_engine("dmma" if dmma else "auto")
+    try:
+        ozk.lu_trailing_update(got[r0:r0 + tm, c0:c0 + tn], got[r0:r0 + tm, j0:j0 + pw],
+                               got[j0:j0 + pw, c0:c0 + tn], d)
+    finally:
+        ozk.set_engine("auto")
+    assert np.array_equal(got[r0:r0 + tm, c0:c0 + tn].view(np.uint64), want.view(np.uint64)), \
+        (K, tm, pw, tn, d, dmma)
+    mask = np.ones(got.shape[:2], dtype=bool)
+    mask[r0:r0 + tm, c0:c0 + tn] = False
+    assert np.array_equal(got[mask].view(np.uint64), w[mask].view(np.uint64)), "outside A22"
