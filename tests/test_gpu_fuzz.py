@@ -156,3 +156,34 @@ def test_random_lu_update_bitexact(ozk, ref, seed):
     mask = np.ones(got.shape[:2], dtype=bool)
     mask[r0:r0 + tm, c0:c0 + tn] = False
     assert np.array_equal(got[mask].view(np.uint64), w[mask].view(np.uint64)), "outside A22"
+
+
+_span_sp = os.environ.get("OZK_FUZZ_SPLIT_SEEDS")
+SPLIT_SEEDS = list(range(*map(int, _span_sp.split(":")))) if _span_sp else list(range(12))
+
+
+@pytest.mark.parametrize("seed", SPLIT_SEEDS)
+def test_random_split_bitexact(ozk, cpu, seed):
+    """Seeded split_matrix<K> (ozaki.hpp:74-147): random format, shape, side,
+    split count up to 40, zero rows/columns, exponent spread and non-canonical
+    K-word inputs; pieces AND residual bit-identical to the reference."""
+    rng = np.random.default_rng(12000 + seed)
+    K = [2, 3, 4][seed % 3]
+    rows, cols = (int(x) for x in rng.integers(1, 400, 2))
+    d = int(rng.integers(1, 41))
+    side = int(rng.integers(0, 2))
+    kind = rng.random()
+    if kind < 0.5:
+        m = cpu.gen_eq1(K, rows, cols, 300 + seed)
+    else:  # raw words: non-canonical expansions, wide exponent range
+        m = rng.standard_normal((rows, cols, K)) * np.exp2(rng.integers(-40, 40, (rows, cols, K)))
+    if rng.random() < 0.3:
+        m[int(rng.integers(0, rows))] = 0.0
+    if rng.random() < 0.3:
+        m[:, int(rng.integers(0, cols))] = 0.0
+    want_p, want_r = cpu.split(K, m, d, side)
+    s = ozk.split_matrix(m, d, ozk.SplitSide(side))
+    got_p = np.stack(s.pieces)
+    assert np.array_equal(got_p.view(np.uint64), want_p.view(np.uint64)), (K, rows, cols, d, side)
+    assert np.array_equal(np.ascontiguousarray(s.residual).view(np.uint64),
+                          want_r.view(np.uint64)), ("residual", K, rows, cols, d, side)
