@@ -187,3 +187,53 @@ def test_random_split_bitexact(ozk, cpu, seed):
     assert np.array_equal(got_p.view(np.uint64), want_p.view(np.uint64)), (K, rows, cols, d, side)
     assert np.array_equal(np.ascontiguousarray(s.residual).view(np.uint64),
                           want_r.view(np.uint64)), ("residual", K, rows, cols, d, side)
+
+
+_span_hp = os.environ.get("OZK_FUZZ_HOST_SEEDS")
+HOST_SEEDS = list(range(*map(int, _span_hp.split(":")))) if _span_hp else list(range(4))
+
+
+@pytest.mark.parametrize("seed", HOST_SEEDS)
+def test_random_host_path_bitexact(ozk, cpu, monkeypatch, seed):
+    """Seeded ozk_ozaki_gemm host path at the sizes where it bands A, blocks B
+    and stages pageable buffers (m >= 2048, n >= 4096): random format, shape,
+    pinned / pageable / 8-byte-misaligned buffers, B block count and 2-D head
+    schedule; C equals the device path's C, and sampled rows equal the
+    reference's."""
+    import torch
+    rng = np.random.default_rng(15000 + seed)
+    K = [2, 3, 4][seed % 3]
+    m = int(rng.integers(2048, 4600))
+    n = int(rng.integers(4096, 8800))
+    l = int(rng.integers(129, 420))
+    d = int(rng.integers(2, {2: 7, 3: 10, 4: 13}[K] + 1))
+    monkeypatch.setenv("OZK_HOST_BBLOCKS", str(int(rng.choice([1, 3, 4, 8]))))
+    monkeypatch.setenv("OZK_HOST_HEAD", str(int(rng.choice([0, 0, 2, 4]))))
+    a = cpu.gen_eq1(K, m, l, 400 + seed)
+    b = cpu.gen_eq1(K, l, n, 401 + seed)
+
+    def host(x, how):
+        if how == "pinned":
+            return torch.from_numpy(x).pin_memory()
+        if how == "misaligned":
+            buf = np.empty(x.size + 1)
+            v = buf[1:].reshape(x.shape)
+            v[...] = x
+            return v
+        return x
+
+    def ptr(x):
+        return x.data_ptr() if isinstance(x, torch.Tensor) else x.ctypes.data
+
+    kinds = ["pageable", "pinned", "misaligned"]
+    ha, hb = host(a, kinds[int(rng.integers(0, 3))]), host(b, kinds[int(rng.integers(0, 3))])
+    hc = host(np.zeros((m, n, K)), kinds[int(rng.integers(0, 3))])
+    assert ozk.lib.ozk_ozaki_gemm(K, m, l, n, ptr(ha), ptr(hb), d, 0.0, ptr(hc), None) == 0, \
+        ozk.lib.ozk_last_error()
+    got = hc.numpy() if isinstance(hc, torch.Tensor) else hc
+    dev, _ = ozk.ozaki_gemm(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda(), d)
+    assert np.array_equal(got.view(np.uint64), dev.cpu().numpy().view(np.uint64)), \
+        (K, m, l, n, d)
+    rows = np.sort(rng.choice(m, 24, replace=False))
+    want = cpu.ozaki_gemm(K, np.ascontiguousarray(a[rows]), b, d)
+    assert np.array_equal(got[rows].view(np.uint64), want.view(np.uint64)), (K, m, l, n, d)
