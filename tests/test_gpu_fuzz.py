@@ -194,7 +194,7 @@ HOST_SEEDS = list(range(*map(int, _span_hp.split(":")))) if _span_hp else list(r
 
 
 @pytest.mark.parametrize("seed", HOST_SEEDS)
-def test_random_host_path_bitexact(ozk, cpu, monkeypatch, seed):
+def test_random_host_path_bitexact(ozk, cpu, port, monkeypatch, seed):
     """Seeded ozk_ozaki_gemm host path at the sizes where it bands A, blocks B
     and stages pageable buffers (m >= 2048, n >= 4096): random format, shape,
     pinned / pageable / 8-byte-misaligned buffers, B block count and 2-D head
@@ -202,21 +202,25 @@ def test_random_host_path_bitexact(ozk, cpu, monkeypatch, seed):
     reference's."""
     import torch
     rng = np.random.default_rng(15000 + seed)
-    K = [2, 3, 4][seed % 3]
+    fmt = [2, 3, 4, TS][seed % 4]
+    K = 3 if fmt == TS else fmt
     m = int(rng.integers(2048, 4600))
     n = int(rng.integers(4096, 8800))
     l = int(rng.integers(129, 420))
-    d = int(rng.integers(2, {2: 7, 3: 10, 4: 13}[K] + 1))
+    d = int(rng.integers(2, {2: 7, 3: 10, 4: 13, TS: 14}[fmt] + 1))
     monkeypatch.setenv("OZK_HOST_BBLOCKS", str(int(rng.choice([1, 3, 4, 8]))))
     monkeypatch.setenv("OZK_HOST_HEAD", str(int(rng.choice([0, 0, 2, 4]))))
-    a = cpu.gen_eq1(K, m, l, 400 + seed)
-    b = cpu.gen_eq1(K, l, n, 401 + seed)
+    if fmt == TS:
+        a, b = port.gen_eq1_ts(m, l, 400 + seed), port.gen_eq1_ts(l, n, 401 + seed)
+    else:
+        a, b = cpu.gen_eq1(K, m, l, 400 + seed), cpu.gen_eq1(K, l, n, 401 + seed)
+    u = np.uint32 if fmt == TS else np.uint64
 
     def host(x, how):
         if how == "pinned":
             return torch.from_numpy(x).pin_memory()
-        if how == "misaligned":
-            buf = np.empty(x.size + 1)
+        if how == "misaligned":  # one word past a 16-byte boundary
+            buf = np.empty(x.size + 1, dtype=x.dtype)
             v = buf[1:].reshape(x.shape)
             v[...] = x
             return v
@@ -227,13 +231,13 @@ def test_random_host_path_bitexact(ozk, cpu, monkeypatch, seed):
 
     kinds = ["pageable", "pinned", "misaligned"]
     ha, hb = host(a, kinds[int(rng.integers(0, 3))]), host(b, kinds[int(rng.integers(0, 3))])
-    hc = host(np.zeros((m, n, K)), kinds[int(rng.integers(0, 3))])
-    assert ozk.lib.ozk_ozaki_gemm(K, m, l, n, ptr(ha), ptr(hb), d, 0.0, ptr(hc), None) == 0, \
+    hc = host(np.zeros((m, n, K), dtype=a.dtype), kinds[int(rng.integers(0, 3))])
+    assert ozk.lib.ozk_ozaki_gemm(fmt, m, l, n, ptr(ha), ptr(hb), d, 0.0, ptr(hc), None) == 0, \
         ozk.lib.ozk_last_error()
     got = hc.numpy() if isinstance(hc, torch.Tensor) else hc
     dev, _ = ozk.ozaki_gemm(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda(), d)
-    assert np.array_equal(got.view(np.uint64), dev.cpu().numpy().view(np.uint64)), \
-        (K, m, l, n, d)
-    rows = np.sort(rng.choice(m, 24, replace=False))
-    want = cpu.ozaki_gemm(K, np.ascontiguousarray(a[rows]), b, d)
-    assert np.array_equal(got[rows].view(np.uint64), want.view(np.uint64)), (K, m, l, n, d)
+    assert np.array_equal(got.view(u), dev.cpu().numpy().view(u)), (fmt, m, l, n, d)
+    rows = np.sort(rng.choice(m, 8 if fmt == TS else 24, replace=False))
+    ar = np.ascontiguousarray(a[rows])
+    want = port.ozaki_gemm_ts(ar, b, d) if fmt == TS else cpu.ozaki_gemm(K, ar, b, d)
+    assert np.array_equal(got[rows].view(u), want.view(u)), (fmt, m, l, n, d)
