@@ -241,3 +241,33 @@ def test_random_host_path_bitexact(ozk, cpu, port, monkeypatch, seed):
     ar = np.ascontiguousarray(a[rows])
     want = port.ozaki_gemm_ts(ar, b, d) if fmt == TS else cpu.ozaki_gemm(K, ar, b, d)
     assert np.array_equal(got[rows].view(u), want.view(u)), (fmt, m, l, n, d)
+
+
+_span_mg = os.environ.get("OZK_FUZZ_MULTI_SEEDS")
+MULTI_SEEDS = list(range(*map(int, _span_mg.split(":")))) if _span_mg else list(range(6))
+
+
+@pytest.mark.parametrize("seed", MULTI_SEEDS)
+def test_random_multi_device_bitexact(ozk, cpu, port, seed):
+    """Seeded ozk_ozaki_gemm_multi (C block rows per device, B digit planes
+    gathered by peer copies while each device multiplies its own block; the
+    devices repeat on one GPU): random format, 1-6 device entries, ragged and
+    empty column blocks, both engines' sides of l = 128, pruning -- C
+    bit-identical to the reference."""
+    rng = np.random.default_rng(17000 + seed)
+    fmt = [2, 3, 4, TS][seed % 4]
+    K = 3 if fmt == TS else fmt
+    m, n = (int(x) for x in rng.integers(1, 300, 2))
+    l = int(rng.integers(1, 129)) if rng.random() < 0.3 else int(rng.integers(129, 600))
+    d = int(rng.integers(2, {2: 8, 3: 11, 4: 14, TS: 16}[fmt] + 1))
+    drop = 0.0 if rng.random() < 0.6 else float(2.0 ** -int(rng.integers(10, 150)))
+    devs = [0] * int(rng.integers(1, 7))
+    if fmt == TS:
+        a, b = port.gen_eq1_ts(m, l, 500 + seed), port.gen_eq1_ts(l, n, 501 + seed)
+        want = port.ozaki_gemm_ts(a, b, d, drop)
+    else:
+        a, b = cpu.gen_eq1(K, m, l, 500 + seed), cpu.gen_eq1(K, l, n, 501 + seed)
+        want = cpu.ozaki_gemm(K, a, b, d, drop)
+    got, _ = ozk.ozaki_gemm_multi(a, b, d, devices=devs, drop_threshold=drop)
+    u = np.uint32 if fmt == TS else np.uint64
+    assert np.array_equal(got.view(u), want.view(u)), (fmt, m, l, n, d, drop, len(devs))
