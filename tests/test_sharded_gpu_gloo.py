@@ -117,3 +117,37 @@ def test_sharded_nccl_side_stream_gather(ozk):
     assert all(r[3] for r in res), res
     assert all(r[2] for r in res), res  # the side stream was used
     assert all(r[1] == "int8" and r[4] == 2 for r in res), res
+
+
+def _random_cases(seed, count):
+    rng = np.random.default_rng(21000 + seed)
+    cases = []
+    for _ in range(count):
+        K = int(rng.integers(2, 5))
+        m = int(rng.integers(1, 900))
+        n = int(rng.integers(1, 300))
+        l = int(rng.integers(1, 129)) if rng.random() < 0.3 else int(rng.integers(129, 900))
+        d = int(rng.integers(2, {2: 8, 3: 11, 4: 14}[K] + 1))
+        drop = 0.0 if rng.random() < 0.7 else float(2.0 ** -int(rng.integers(20, 140)))
+        cases.append((K, m, l, n, d, drop))
+    return cases
+
+
+_span_sh = os.environ.get("OZK_FUZZ_SHARD_SEEDS")
+SHARD_SEEDS = list(range(*map(int, _span_sh.split(":")))) if _span_sh else [0]
+
+
+@pytest.mark.parametrize("seed", SHARD_SEEDS)
+@pytest.mark.parametrize("world", [2, 4])
+def test_sharded_random_on_device(ozk, world, seed):
+    """Seeded shapes through the sharded path on one device (gloo): ragged and
+    empty row / column blocks, both engines, pruning, the local-block-first
+    GEMM order, device and banded host paths -- every rank's C rows
+    bit-identical to the reference."""
+    cases = _random_cases(seed * 10 + world, 6)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    mp.spawn(_worker, args=(world, _free_port(), cases, q), nprocs=world, join=True)
+    results = [q.get() for _ in range(world * len(cases))]
+    bad = [r for r in results if not r[3]]
+    assert not bad, bad
