@@ -854,8 +854,18 @@ ozk_status ozk_ozaki_gemm(ozk_format fmt, size_t m, size_t l, size_t n, const vo
         const char* v = std::getenv("OZK_PAGEABLE_STAGING");
         return !(v && !std::strcmp(v, "0"));
     }();
-    const bool a_pg = staging_on && !host_is_pinned(a), b_pg = staging_on && !host_is_pinned(b),
-               c_pg = staging_on && !host_is_pinned(c);
+    // Buffers below 2 MiB are left to the driver's own pageable copies, which
+    // are as fast at that size as starting the two staging workers
+    // ($OZK_STAGING_MIN_MB; the copy teams and slots are cached per process).
+    const size_t stage_min = [] {
+        const char* v = std::getenv("OZK_STAGING_MIN_MB");
+        return (size_t)(v ? std::max(0, std::atoi(v)) : 2) << 20;
+    }();
+    auto staged = [&](const void* p, size_t bytes) {
+        return staging_on && bytes >= stage_min && !host_is_pinned(p);
+    };
+    const bool a_pg = staged(a, eb * m * l), b_pg = staged(b, eb * l * n),
+               c_pg = staged(c, eb * m * n);
     std::unique_ptr<HostStaging> hs;
     // on every exit: the staging workers drained and the copy streams idle
     // before the device buffers go back to the pool

@@ -193,7 +193,34 @@ private:
     uint64_t gen_ = 0;
     int pending_ = 0;
     bool quit_ = false;
+
+public:
+    int size() const { return n_; }
 };
+
+// Copy teams are cached process-wide like the slot sets: starting ~24 host
+// threads per call cost ~1 ms, which small and mid-size calls felt.
+std::mutex g_team_mu;
+std::vector<std::unique_ptr<Team>> g_free_teams;
+
+std::unique_ptr<Team> acquire_team(int n) {
+    {
+        std::lock_guard<std::mutex> lk(g_team_mu);
+        for (size_t i = g_free_teams.size(); i-- > 0;)
+            if (g_free_teams[i]->size() == (n < 1 ? 1 : n)) {
+                auto t = std::move(g_free_teams[i]);
+                g_free_teams.erase(g_free_teams.begin() + (std::ptrdiff_t)i);
+                return t;
+            }
+    }
+    return std::make_unique<Team>(n);
+}
+
+void release_team(std::unique_ptr<Team> t) {
+    if (!t) return;
+    std::lock_guard<std::mutex> lk(g_team_mu);
+    g_free_teams.push_back(std::move(t));
+}
 
 }  // namespace
 
@@ -201,7 +228,7 @@ struct HostStaging::Impl {
     int device;  // the caller's current device: the copy streams' device
     cudaStream_t h2d_stream, d2h_stream;
     std::unique_ptr<SlotSet> slots;
-    Team h2d_team, d2h_team;
+    std::unique_ptr<Team> h2d_team, d2h_team;
     std::mutex mu;
     std::condition_variable cv;
     std::deque<StagedCopy> queue[2];
@@ -223,7 +250,8 @@ struct HostStaging::Impl {
 
     Impl(cudaStream_t h2d, cudaStream_t d2h, int h2d_threads, int d2h_threads)
         : device(current_device()), h2d_stream(h2d), d2h_stream(d2h),
-          slots(acquire_slots(device)), h2d_team(h2d_threads), d2h_team(d2h_threads) {
+          slots(acquire_slots(device)), h2d_team(acquire_team(h2d_threads)),
+          d2h_team(acquire_team(d2h_threads)) {
         if (!slots) err = cudaErrorMemoryAllocation;
         for (int d = 0; d < 2; ++d) worker[d] = std::thread([this, d] { run(d); });
     }
@@ -257,7 +285,7 @@ struct HostStaging::Impl {
                 const int s = take_slot(0);
                 char* slot = slots->mem[0][s];
                 const char* src = static_cast<const char*>(j.host) + r0 * j.host_pitch + b0;
-                h2d_team.copy2d(slot, w, src, j.host_pitch, w, rows);
+                h2d_team->copy2d(slot, w, src, j.host_pitch, w, rows);
                 char* dst = static_cast<char*>(j.dev) + r0 * j.dev_pitch + b0;
                 cudaError_t e = rows == 1
                     ? cudaMemcpyAsync(dst, slot, w, cudaMemcpyHostToDevice, h2d_stream)
@@ -293,7 +321,7 @@ struct HostStaging::Impl {
             inflight.pop_front();
             const cudaError_t e = cudaEventSynchronize(slots->ev[1][p.slot]);
             if (e != cudaSuccess) return fail(e);
-            d2h_team.copy2d(static_cast<char*>(j.host) + p.off, p.bytes, slots->mem[1][p.slot],
+            d2h_team->copy2d(static_cast<char*>(j.host) + p.off, p.bytes, slots->mem[1][p.slot],
                             p.bytes, p.bytes, 1);
             slot_used[1][p.slot] = false;
         };
@@ -345,6 +373,8 @@ HostStaging::HostStaging(cudaStream_t h2d, cudaStream_t d2h, int h2d_threads, in
 HostStaging::~HostStaging() {
     finish();
     release_slots(std::move(impl_->slots));
+    release_team(std::move(impl_->h2d_team));
+    release_team(std::move(impl_->d2h_team));
     delete impl_;
 }
 
