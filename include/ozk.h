@@ -111,6 +111,19 @@ ozk_status ozk_ozaki_gemm_device(ozk_format fmt, size_t m, size_t l, size_t n, c
                                  const void* b, int split_count, double drop_threshold, void* c,
                                  void* stream, ozk_profile* prof);
 
+/* Asynchronous ozk_ozaki_gemm_device for pipelined callers: returns once the
+ * work is queued on `stream` (scratch is stream-ordered).  The split's data
+ * errors (non-finite entry, entry too large to shift; A's, then B's) land in
+ * dev_flags[0..1], two device ints read with ozk_check_split_flag (A's flag
+ * first, as the reference splits A first); the return value covers argument
+ * and launch errors.  With drop_threshold > 0 the pair list needs the slice
+ * maxima on the host, so that case synchronises once mid-call and returns a
+ * data error directly, as ozk_ozaki_gemm_device does. */
+ozk_status ozk_ozaki_gemm_device_async(ozk_format fmt, size_t m, size_t l, size_t n,
+                                       const void* a, const void* b, int split_count,
+                                       double drop_threshold, void* c, int* dev_flags,
+                                       void* stream);
+
 /* split_matrix<K> (ozaki.hpp:74-147): host buffers.  pieces receives
  * split_count row-major (rows x cols) slices (binary64; binary32 for TS),
  * residual the K-word working matrix after the last extraction (SplitSet<K>,

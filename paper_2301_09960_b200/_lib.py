@@ -40,6 +40,9 @@ SIGNATURES = {
     "ozk_ozaki_gemm_device": (ctypes.c_int, [ctypes.c_int, _sz, _sz, _sz, _dp, _dp, ctypes.c_int,
                                              ctypes.c_double, _dp, ctypes.c_void_p,
                                              ctypes.POINTER(OzkProfile)]),
+    "ozk_ozaki_gemm_device_async": (ctypes.c_int, [ctypes.c_int, _sz, _sz, _sz, _dp, _dp,
+                                                   ctypes.c_int, ctypes.c_double, _dp, _dp,
+                                                   ctypes.c_void_p]),
     "ozk_split": (ctypes.c_int, [ctypes.c_int, _sz, _sz, _dp, ctypes.c_int, ctypes.c_int, _dp,
                                  _dp]),
     "ozk_backend_gemm": (ctypes.c_int, [_sz, _sz, _sz, _dp, _dp, _dp]),

@@ -469,7 +469,7 @@ ozk_status ozaki_device_impl(int fmt, size_t m, size_t l, size_t n, const void* 
                              const void* b, size_t ldb, int d, double drop, void* c,
                              cudaStream_t st, ozk_profile* prof,
                              const HostOverlap* ov = nullptr, const PairList* forced = nullptr,
-                             const LuTarget* lu = nullptr) {
+                             const LuTarget* lu = nullptr, int* async_flags = nullptr) {
     const int K = words_of(fmt), wb = word_bytes_of(fmt);
     const int sms = num_sms_cached();
     const size_t ldk = slice_ld(l);
@@ -736,6 +736,13 @@ ozk_status ozaki_device_impl(int fmt, size_t m, size_t l, size_t n, const void* 
     }
     tm.mark(2, st);
 
+    if (async_flags) {
+        // asynchronous form: the split's data-error flags (A, then B) go to the
+        // caller's device ints, read later with ozk_check_split_flag
+        OZK_CUDA(cudaMemcpyAsync(async_flags, err, 2 * sizeof(int), cudaMemcpyDeviceToDevice, st),
+                 "ozaki_gemm: flag");
+        return OZK_OK;
+    }
     int flag[2] = {0, 0};
     OZK_CUDA(cudaMemcpyAsync(flag, err, sizeof(flag), cudaMemcpyDeviceToHost, st),
              "ozaki_gemm: flag");
@@ -823,6 +830,15 @@ ozk_status ozk_ozaki_gemm_device(ozk_format fmt, size_t m, size_t l, size_t n, c
     if (ozk_status s = need({a, b, c}, "ozaki_gemm")) return s;
     return ozaki_device_impl((int)fmt, m, l, n, a, l, b, n, d, drop, c, (cudaStream_t)stream,
                              prof);
+}
+
+ozk_status ozk_ozaki_gemm_device_async(ozk_format fmt, size_t m, size_t l, size_t n,
+                                       const void* a, const void* b, int d, double drop, void* c,
+                                       int* dev_flags, void* stream) {
+    if (ozk_status s = check_gemm_args(fmt, m, l, n, d, drop)) return s;
+    if (ozk_status s = need({a, b, c, dev_flags}, "ozaki_gemm")) return s;
+    return ozaki_device_impl((int)fmt, m, l, n, a, l, b, n, d, drop, c, (cudaStream_t)stream,
+                             nullptr, nullptr, nullptr, nullptr, dev_flags);
 }
 
 ozk_status ozk_ozaki_gemm(ozk_format fmt, size_t m, size_t l, size_t n, const void* a,

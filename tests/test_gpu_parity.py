@@ -859,6 +859,53 @@ def test_host_api_pinned_and_pageable_agree(ozk, cpu, monkeypatch, n, head):
     assert_bitwise(ref_c[rows], want, "sampled rows vs the reference")
 
 
+def test_device_async_entry(ozk, cpu):
+    """ozk_ozaki_gemm_device_async: several GEMMs queued back to back on one
+    stream with no synchronisation in between give the synchronous entry's
+    bits; data errors arrive in the device flags (A's before B's), argument
+    errors in the return value."""
+    import torch
+    lib = ozk.lib
+    st = torch.cuda.current_stream().cuda_stream
+    flags = torch.full((2,), -1, dtype=torch.int32, device="cuda")
+    outs, wants = [], []
+    for K, m, l, n, d in ((2, 300, 257, 190, 6), (3, 64, 100, 80, 9), (4, 130, 300, 140, 11)):
+        a = cpu.gen_eq1(K, m, l, 30 + K)
+        b = cpu.gen_eq1(K, l, n, 31 + K)
+        wants.append(cpu.ozaki_gemm(K, a, b, d))
+        A, B = torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()
+        C = torch.empty((m, n, K), dtype=torch.float64, device="cuda")
+        assert lib.ozk_ozaki_gemm_device_async(K, m, l, n, A.data_ptr(), B.data_ptr(), d, 0.0,
+                                               C.data_ptr(), flags.data_ptr(), st) == 0
+        outs.append((A, B, C))
+    assert lib.ozk_check_split_flag(flags.data_ptr(), st) == 0
+    assert lib.ozk_check_split_flag(flags.data_ptr() + 4, st) == 0
+    for (_, _, C), want in zip(outs, wants):
+        assert_bitwise(C.cpu().numpy(), want, "async entry")
+    # data errors: NaN in B only -> flag 1; too large in A and NaN in B -> A's flag
+    a = cpu.gen_eq1(2, 40, 200, 5)
+    b = cpu.gen_eq1(2, 200, 30, 6)
+    b[3, 4, 0] = np.nan
+    A, B = torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()
+    C = torch.empty((40, 30, 2), dtype=torch.float64, device="cuda")
+    assert lib.ozk_ozaki_gemm_device_async(2, 40, 200, 30, A.data_ptr(), B.data_ptr(), 4, 0.0,
+                                           C.data_ptr(), flags.data_ptr(), st) == 0
+    assert lib.ozk_check_split_flag(flags.data_ptr(), st) == 0
+    assert lib.ozk_check_split_flag(flags.data_ptr() + 4, st) == 2  # OZK_EPARAM
+    assert b"non-finite" in lib.ozk_last_error()
+    a[0, 0, :] = [2.0 ** 1000, 0.0]
+    A = torch.from_numpy(a).cuda()
+    assert lib.ozk_ozaki_gemm_device_async(2, 40, 200, 30, A.data_ptr(), B.data_ptr(), 4, 0.0,
+                                           C.data_ptr(), flags.data_ptr(), st) == 0
+    assert lib.ozk_check_split_flag(flags.data_ptr(), st) == 2
+    assert b"too large" in lib.ozk_last_error()
+    # argument errors come back at once
+    assert lib.ozk_ozaki_gemm_device_async(2, 0, 200, 30, A.data_ptr(), B.data_ptr(), 4, 0.0,
+                                           C.data_ptr(), flags.data_ptr(), st) == 1
+    assert lib.ozk_ozaki_gemm_device_async(2, 40, 200, 30, A.data_ptr(), B.data_ptr(), 4, 0.0,
+                                           C.data_ptr(), None, st) == 2
+
+
 def test_host_api_pageable_misaligned(ozk, cpu):
     """Pageable caller buffers that are only 8-byte aligned (a DenseMatrix
     inside a larger allocation): the staging copies' streaming 16-byte stores
