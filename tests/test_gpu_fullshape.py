@@ -44,6 +44,12 @@ CONFIGS = [
     ("dd", 16384, 10, 8, 6),       # config 5, ill-conditioned
     ("qd", 16384, 16, 8, 4),       # config 5
 ]
+# $OZK_FULLSHAPE_EXTRA="fmt:n:D:spread:pairs,..." adds one-off sizes (ragged
+# tile counts, profiles/r02_fullshape_extra.log); pairs "all" or a count
+import os  # noqa: E402
+for _c in filter(None, os.environ.get("OZK_FULLSHAPE_EXTRA", "").split(",")):
+    _f, _n, _d, _s, _p = _c.split(":")
+    CONFIGS.append((_f, int(_n), int(_d), int(_s), _p if _p == "all" else int(_p)))
 
 
 def bits(x):
